@@ -1,0 +1,265 @@
+"""ctypes bindings for the CPU oracle libraries.
+
+TEST INFRASTRUCTURE ONLY.  Importable from tests/, __graft_entry__.smoke() and
+bench.py's CPU-baseline legs; the product (paper_2402_03307_b200) never imports it.
+
+Two libraries share one C signature set:
+  * ``liboracle.so``        — oracle/rgs_oracle.c, the plain-C restatement (prefix ``orc_``)
+  * ``_ref/librgs_ref.so``  — the reference's own render sources compiled in place
+                              (prefix ``ref_``); only present where it was built.
+
+Scene arrays follow the "host scene" layout of include/rgs_cuda.h:
+mean (N,4), log_scales (N,4), rotor (N,8), opacity_logit (N,), sh (N,3,16)
+channel-major, all float64.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "librgs_ref.so")
+
+_dp = ctypes.POINTER(ctypes.c_double)
+_vp = ctypes.c_void_p
+
+
+class CCamera(ctypes.Structure):
+    _fields_ = [
+        ("width", ctypes.c_int),
+        ("height", ctypes.c_int),
+        ("fx", ctypes.c_double),
+        ("fy", ctypes.c_double),
+        ("cx", ctypes.c_double),
+        ("cy", ctypes.c_double),
+        ("world_to_camera", ctypes.c_double * 16),
+        ("time", ctypes.c_double),
+    ]
+
+
+SPLAT_DTYPE = np.dtype(
+    [
+        ("mean2", "<f8", (2,)),
+        ("conic", "<f8", (3,)),
+        ("depth", "<f8"),
+        ("color", "<f8", (3,)),
+        ("alpha_base", "<f8"),
+        ("flow2", "<f8", (2,)),
+        ("radius", "<f8"),
+        ("source_index", "<i4"),
+        ("pad", "<i4"),
+    ]
+)
+assert SPLAT_DTYPE.itemsize == 112
+
+
+def make_ccamera(cam) -> CCamera:
+    c = CCamera()
+    c.width, c.height = int(cam.width), int(cam.height)
+    c.fx, c.fy, c.cx, c.cy = float(cam.fx), float(cam.fy), float(cam.cx), float(cam.cy)
+    w2c = np.asarray(cam.world_to_camera, dtype=np.float64).reshape(16)
+    for i in range(16):
+        c.world_to_camera[i] = float(w2c[i])
+    c.time = float(cam.time)
+    return c
+
+
+def _p(a):
+    return a.ctypes.data_as(_vp) if a is not None else None
+
+
+@dataclass
+class Records:
+    splats: np.ndarray  # SPLAT_DTYPE
+    tile_offsets: np.ndarray  # int64 (tiles+1)
+    tile_ids: np.ndarray  # int32
+    final_T: np.ndarray  # float64 (H,W)
+    n_contrib: np.ndarray  # int32 (H,W)
+    retained: bool
+    handle: object = None  # live C handle for backward
+
+    def tile_list(self, t):
+        return self.tile_ids[self.tile_offsets[t] : self.tile_offsets[t + 1]]
+
+
+class OracleLib:
+    """One of the two CPU libraries (restatement or reference build)."""
+
+    def __init__(self, path: str, prefix: str):
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} not built (run `make -C oracle`)")
+        self.path, self.prefix = path, prefix
+        self.lib = ctypes.CDLL(path)
+        f = self._f
+        f("last_error").restype = ctypes.c_char_p
+        for name in ("records_num_splats", "records_num_tiles", "records_retained"):
+            f(name).restype = ctypes.c_int
+            f(name).argtypes = [_vp]
+        f("records_num_pairs").restype = ctypes.c_longlong
+        f("records_num_pairs").argtypes = [_vp]
+        f("records_free").argtypes = [_vp]
+        for name in ("records_splats", "records_tiles", "records_pixels"):
+            f(name).restype = None
+        self._free = f("records_free")
+
+    def _f(self, name):
+        return getattr(self.lib, f"{self.prefix}_{name}")
+
+    def _check(self, rc):
+        if rc != 0:
+            msg = self._f("last_error")().decode()
+            raise OracleError(rc, msg)
+
+    @staticmethod
+    def _scene(store):
+        mean = np.ascontiguousarray(store.mean, dtype=np.float64)
+        ls = np.ascontiguousarray(store.log_scales, dtype=np.float64)
+        rot = np.ascontiguousarray(store.rotor, dtype=np.float64)
+        op = np.ascontiguousarray(store.opacity_logit, dtype=np.float64)
+        sh = np.ascontiguousarray(store.sh, dtype=np.float64)
+        return mean, ls, rot, op, sh
+
+    def _records(self, h, cam, retained_default=None):
+        ns = self._f("records_num_splats")(h)
+        nt = self._f("records_num_tiles")(h)
+        npairs = self._f("records_num_pairs")(h)
+        splats = np.zeros(ns, dtype=SPLAT_DTYPE)
+        self._f("records_splats")(_vp(h), _p(splats))
+        off = np.zeros(nt + 1, dtype=np.int64)
+        ids = np.zeros(max(npairs, 1), dtype=np.int32)
+        self._f("records_tiles")(_vp(h), _p(off), _p(ids))
+        fT = np.zeros((cam.height, cam.width), dtype=np.float64)
+        nc = np.zeros((cam.height, cam.width), dtype=np.int32)
+        self._f("records_pixels")(_vp(h), _p(fT), _p(nc))
+        ret = bool(self._f("records_retained")(h))
+        return Records(splats, off, ids[:npairs], fT, nc, ret, _Handle(self, h))
+
+    def render_forward(self, store, cam, background=(0.0, 0.0, 0.0), threads=1, retain=False):
+        mean, ls, rot, op, sh = self._scene(store)
+        c = make_ccamera(cam)
+        bg = np.asarray(background, dtype=np.float64)
+        img = np.zeros((cam.height, cam.width, 3), dtype=np.float64)
+        h = _vp()
+        rc = self._f("render_forward")(
+            ctypes.c_int(len(op)), _p(mean), _p(ls), _p(rot), _p(op), _p(sh),
+            ctypes.c_int(store.active_sh_degree), ctypes.byref(c), _p(bg), ctypes.c_int(threads),
+            ctypes.c_int(1 if retain else 0), _p(img), ctypes.byref(h))
+        self._check(rc)
+        return img, self._records(h.value, cam)
+
+    def rasterize_forward(self, splats, cam, background=(0.0, 0.0, 0.0), threads=1):
+        sp = np.ascontiguousarray(splats, dtype=SPLAT_DTYPE)
+        c = make_ccamera(cam)
+        bg = np.asarray(background, dtype=np.float64)
+        img = np.zeros((cam.height, cam.width, 3), dtype=np.float64)
+        h = _vp()
+        rc = self._f("rasterize_forward")(ctypes.c_int(len(sp)), _p(sp), ctypes.byref(c), _p(bg),
+                                         ctypes.c_int(threads), _p(img), ctypes.byref(h))
+        self._check(rc)
+        return img, self._records(h.value, cam)
+
+    def render_backward(self, store, cam, records, dL_dimage, threads=1):
+        mean, ls, rot, op, sh = self._scene(store)
+        c = make_ccamera(cam)
+        n = len(op)
+        dl = np.ascontiguousarray(dL_dimage, dtype=np.float64)
+        grads = np.zeros((n, 65), dtype=np.float64)
+        vnorm = np.zeros(n, dtype=np.float64)
+        vis = np.zeros(n, dtype=np.uint8)
+        rc = self._f("render_backward")(
+            ctypes.c_int(n), _p(mean), _p(ls), _p(rot), _p(op), _p(sh),
+            ctypes.c_int(store.active_sh_degree), ctypes.byref(c), _vp(records.handle.h), _p(dl),
+            ctypes.c_int(threads), _p(grads), _p(vnorm), _p(vis))
+        self._check(rc)
+        return grads, vnorm, vis
+
+    def render_flow(self, store, cam, threads=1):
+        mean, ls, rot, op, sh = self._scene(store)
+        c = make_ccamera(cam)
+        flow = np.zeros((cam.height, cam.width, 2), dtype=np.float64)
+        rc = self._f("render_flow")(ctypes.c_int(len(op)), _p(mean), _p(ls), _p(rot), _p(op), _p(sh),
+                                   ctypes.c_int(store.active_sh_degree), ctypes.byref(c),
+                                   ctypes.c_int(threads), _p(flow))
+        self._check(rc)
+        return flow
+
+    def naive_render(self, store, cam, background=(0.0, 0.0, 0.0)):
+        mean, ls, rot, op, sh = self._scene(store)
+        c = make_ccamera(cam)
+        bg = np.asarray(background, dtype=np.float64)
+        img = np.zeros((cam.height, cam.width, 3), dtype=np.float64)
+        ws = np.zeros((cam.height, cam.width), dtype=np.float64)
+        ft = np.zeros((cam.height, cam.width), dtype=np.float64)
+        rc = self._f("naive_render")(ctypes.c_int(len(op)), _p(mean), _p(ls), _p(rot), _p(op), _p(sh),
+                                    ctypes.c_int(store.active_sh_degree), ctypes.byref(c), _p(bg),
+                                    _p(img), _p(ws), _p(ft))
+        self._check(rc)
+        return img, ws, ft
+
+    def slice_at(self, mean, ls, rot, t):
+        out = np.zeros(17, dtype=np.float64)
+        rc = self._f("slice_at")(_p(np.ascontiguousarray(mean, np.float64)),
+                                 _p(np.ascontiguousarray(ls, np.float64)),
+                                 _p(np.ascontiguousarray(rot, np.float64)), ctypes.c_double(t), _p(out))
+        self._check(rc)
+        return out
+
+    def normalize(self, rot):
+        out = np.zeros(8, dtype=np.float64)
+        self._check(self._f("normalize")(_p(np.ascontiguousarray(rot, np.float64)), _p(out)))
+        return out
+
+    def to_matrix(self, rot):
+        out = np.zeros(16, dtype=np.float64)
+        self._check(self._f("to_matrix")(_p(np.ascontiguousarray(rot, np.float64)), _p(out)))
+        return out.reshape(4, 4)
+
+    def project(self, sliced16, cam, sh48, sh_degree, opacity_logit):
+        c = make_ccamera(cam)
+        out = np.zeros(1, dtype=SPLAT_DTYPE)
+        r = self._f("project")(_p(np.ascontiguousarray(sliced16, np.float64)), ctypes.byref(c),
+                               _p(np.ascontiguousarray(sh48, np.float64)), ctypes.c_int(sh_degree),
+                               ctypes.c_double(opacity_logit), _p(out))
+        if r < 0:
+            self._check(-r)
+        return out[0] if r == 1 else None
+
+
+class _Handle:
+    def __init__(self, lib, h):
+        self.lib, self.h = lib, h
+
+    def __del__(self):
+        try:
+            self.lib._free(_vp(self.h))
+        except Exception:
+            pass
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+_cache = {}
+
+
+def restatement() -> OracleLib:
+    if "orc" not in _cache:
+        _cache["orc"] = OracleLib(ORACLE_SO, "orc")
+    return _cache["orc"]
+
+
+def reference_build() -> OracleLib:
+    if "ref" not in _cache:
+        _cache["ref"] = OracleLib(REF_SO, "ref")
+    return _cache["ref"]
+
+
+def reference_available() -> bool:
+    return os.path.exists(REF_SO)
