@@ -1,0 +1,191 @@
+/* rgs_cuda.h — C ABI of the B200-native 4D-rotor Gaussian slicing + splatting path.
+ *
+ * Drop-in boundary for the reference renderer API in /root/reference/proj/include/rgs:
+ *   render_forward     rasterizer.hpp:82-83   -> rgs_render_forward / rgs_render_views
+ *   rasterize_forward  rasterizer.hpp:87-89   -> rgs_rasterize_forward
+ *   render_backward    rasterizer.hpp:93-95   -> rgs_render_backward
+ *   render_flow        rasterizer.hpp:99      -> rgs_render_flow
+ *   RenderRecords      rasterizer.hpp:61-70   -> rgs_records (opaque; rgs_records_export)
+ *   GaussianStore      gaussian.hpp:79-103    -> rgs_scene   (device-resident FP32 SoA)
+ *   StoreGrads         gaussian.hpp:106-119   -> grads / viewspace_norm / visible buffers
+ *   Camera             camera.hpp:11-27       -> rgs_camera
+ * The C++ drop-in (paper_2402_03307_b200/host/rgs_b200.hpp) and the Python
+ * mirror (paper_2402_03307_b200/rgs.py) sit on top of exactly these symbols.
+ *
+ * Plain C: pointers and sizes only, no CUDA or torch types in signatures (streams
+ * are passed as void*).  Every entry point returns an rgs_status; on failure
+ * rgs_ctx_last_error() gives the reference's exception message.
+ *
+ * Precision contract:
+ *   * slicing / projection / SH / culls / tile rectangles / depth keys: FP64 with
+ *     the reference's expression order and no FMA contraction -> tile lists and
+ *     per-tile order match the CPU reference bit for bit;
+ *   * blending: FP32 with a per-evaluation error bound; any pixel whose gate
+ *     decision falls inside the bound is recomputed in FP64 ("slow pixel"),
+ *     so gate decisions match FP64 and the image is within 1e-4;
+ *     RGS_FLAG_BLEND_FP64 forces the FP64 path for every pixel.
+ */
+#ifndef RGS_CUDA_H
+#define RGS_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RGS_ABI_VERSION 1
+
+typedef enum {
+    RGS_OK = 0,
+    RGS_E_CAMERA = 1,          /* std::runtime_error from Camera::validate (camera.hpp:21-26) */
+    RGS_E_MISSING_RECORDS = 2, /* MissingRecordsError (rasterizer.hpp:78-80) */
+    RGS_E_ZERO_ROTOR = 3,      /* ZeroRotorError (rotor.hpp:56-58, rotor.cpp:121) */
+    RGS_E_NONFINITE_ROTOR = 4, /* NonFiniteRotorError (rotor.hpp:59-61, rotor.cpp:119,132-134) */
+    RGS_E_CUDA = 5,            /* CUDA runtime failure */
+    RGS_E_INVALID = 6,         /* bad argument (null pointer, size mismatch, ...) */
+    RGS_E_NO_DEVICE = 8        /* no CUDA device: the product has no CPU fallback */
+} rgs_status;
+
+/* Render flags. */
+#define RGS_FLAG_RETAIN_RECORDS 1u /* RenderOptions::retain_records (rasterizer.hpp:56-60) */
+#define RGS_FLAG_BLEND_FP64 2u     /* blend every pixel in FP64 (reference-KAT mode) */
+#define RGS_FLAG_ACCUMULATE 4u     /* backward: add into grads (StoreGrads::add, gaussian.cpp:199) */
+#define RGS_FLAG_HOST_BUFFERS 8u   /* image / splat pointers are host memory */
+
+typedef struct rgs_ctx rgs_ctx;
+typedef struct rgs_scene rgs_scene;
+typedef struct rgs_records rgs_records;
+
+/* camera.hpp:11-27.  world_to_camera is row-major 4x4, +z forward. */
+typedef struct {
+    int width, height;
+    double fx, fy, cx, cy;
+    double world_to_camera[16];
+    double time;
+} rgs_camera;
+
+/* Splat2D (rasterizer.hpp:21-30), 112 bytes. */
+typedef struct {
+    double mean2[2];
+    double conic[3];
+    double depth;
+    double color[3];
+    double alpha_base;
+    double flow2[2];
+    double radius;
+    int32_t source_index;
+    int32_t pad;
+} rgs_splat;
+
+typedef struct {
+    int n_splats;      /* RenderRecords::splats.size() */
+    int tiles_x, tiles_y;
+    int retained;      /* RenderRecords::retained */
+    long long n_pairs; /* sum over tiles of tile_splats[t].size() */
+    int n_slow_pixels; /* pixels recomputed in FP64 by the guard band */
+    int width, height;
+} rgs_records_info;
+
+/* ---------------------------------------------------------------- context */
+int rgs_abi_version(void);
+int rgs_device_count(void);
+int rgs_ctx_create(int device, rgs_ctx** out);
+void rgs_ctx_destroy(rgs_ctx* ctx);
+/* Use `stream` (a cudaStream_t) for all subsequent work; NULL = the context's own stream. */
+int rgs_ctx_set_stream(rgs_ctx* ctx, void* stream);
+void* rgs_ctx_stream(rgs_ctx* ctx);
+const char* rgs_ctx_last_error(const rgs_ctx* ctx);
+/* Gaussian index of the last rotor error (ZeroRotor / NonFiniteRotor), -1 if none. */
+int rgs_ctx_error_index(const rgs_ctx* ctx);
+/* Block until the context's stream is idle. */
+int rgs_ctx_synchronize(rgs_ctx* ctx);
+/* Count of kernels this context launched since creation (bench evidence). */
+long long rgs_ctx_kernel_launches(const rgs_ctx* ctx);
+
+/* ---------------------------------------------------------------- scene */
+/* Device scene (GaussianStore replacement).  Host layout of the upload arrays
+ * (the reference's Eigen memory order, gaussian.hpp:79-85):
+ *   mean[N*4] (x,y,z,t), log_scales[N*4], rotor[N*8] (s,b01,b02,b03,b12,b13,b23,p),
+ *   opacity_logit[N], sh[N*48] channel-major (sh[i*48 + ch*16 + k] = ShCoeffs(ch,k)).
+ * Device storage is FP32 SoA (65 floats per Gaussian, see rgs_scene_params). */
+int rgs_scene_create(rgs_ctx* ctx, int n, int sh_degree, rgs_scene** out);
+void rgs_scene_destroy(rgs_scene* scene);
+int rgs_scene_size(const rgs_scene* scene);
+int rgs_scene_set_sh_degree(rgs_scene* scene, int sh_degree);
+/* Host float64 arrays; values are rounded to float32 (exact for checkpoint-loaded
+ * stores, checkpoint.cpp:75-82).  *n_inexact (may be NULL) receives the number of
+ * coefficients that were not float32-representable. */
+int rgs_scene_upload_f64(rgs_ctx* ctx, rgs_scene* scene, const double* mean, const double* log_scales,
+                         const double* rotor, const double* opacity_logit, const double* sh,
+                         long long* n_inexact);
+/* float32 arrays in the same layout; host or device pointers (cudaMemcpyDefault). */
+int rgs_scene_upload_f32(rgs_ctx* ctx, rgs_scene* scene, const float* mean, const float* log_scales,
+                         const float* rotor, const float* opacity_logit, const float* sh);
+/* Device pointer of the SoA parameter block (65*N floats):
+ *   [0,4N) mean float4, [4N,8N) log_scales float4, [8N,12N) rotor(s,b01,b02,b03) float4,
+ *   [12N,16N) rotor(b12,b13,b23,p) float4, [16N,64N) sh: 12 float4 blocks, block m
+ *   holding coefficients j=4m..4m+3 with j = k*3+ch, [64N,65N) opacity_logit. */
+float* rgs_scene_params(rgs_scene* scene);
+/* Copy the device scene back to host arrays in the upload layout (float64). */
+int rgs_scene_download_f64(rgs_ctx* ctx, const rgs_scene* scene, double* mean, double* log_scales,
+                           double* rotor, double* opacity_logit, double* sh);
+
+/* ---------------------------------------------------------------- forward */
+/* render_forward (rasterizer.cpp:308-318).  image: H*W*3 floats, row-major,
+ * channel-interleaved (device memory unless RGS_FLAG_HOST_BUFFERS).
+ * records may be NULL; otherwise *records receives a new handle. */
+int rgs_render_forward(rgs_ctx* ctx, const rgs_scene* scene, const rgs_camera* cam,
+                       const double background[3], unsigned flags, float* image,
+                       rgs_records** records);
+/* A batch of views (camera x timestamp sweep): images[v] = render_forward(cams[v]).
+ * images: n_views*H*W*3 floats; all cameras must share width/height. */
+int rgs_render_views(rgs_ctx* ctx, const rgs_scene* scene, const rgs_camera* cams, int n_views,
+                     const double background[3], unsigned flags, float* images);
+/* End-to-end host path: uploads the host scene (upload layout, float32), renders
+ * every view, copies the images back into host memory (pinned for best speed).
+ * Timed region of bench.py's "e2e" figure. */
+int rgs_render_views_host(rgs_ctx* ctx, int n, int sh_degree, const float* mean,
+                          const float* log_scales, const float* rotor, const float* opacity_logit,
+                          const float* sh, const rgs_camera* cams, int n_views,
+                          const double background[3], float* images_host);
+/* rasterize_forward (rasterizer.cpp:278-306) on already-projected splats. */
+int rgs_rasterize_forward(rgs_ctx* ctx, const rgs_splat* splats, int n_splats, const rgs_camera* cam,
+                          const double background[3], unsigned flags, float* image,
+                          rgs_records** records);
+/* render_flow (rasterizer.cpp:399-425).  flow: H*W*2 floats. */
+int rgs_render_flow(rgs_ctx* ctx, const rgs_scene* scene, const rgs_camera* cam, unsigned flags,
+                    float* flow);
+
+/* ---------------------------------------------------------------- records */
+void rgs_records_destroy(rgs_records* rec);
+int rgs_records_info_get(const rgs_records* rec, rgs_records_info* info);
+/* Materialise the reference's RenderRecords on the host.  Any pointer may be NULL.
+ *   splats[n_splats]          compacted splats in Gaussian-index order (rasterizer.cpp:206-210)
+ *   tile_offsets[tiles+1]     CSR offsets into tile_ids
+ *   tile_ids[n_pairs]         per-tile depth-sorted indices into splats (rasterizer.cpp:57-74)
+ *   final_T[H*W], n_contrib[H*W]. */
+int rgs_records_export(rgs_ctx* ctx, const rgs_records* rec, rgs_splat* splats,
+                       long long* tile_offsets, int32_t* tile_ids, double* final_T,
+                       int32_t* n_contrib);
+
+/* ---------------------------------------------------------------- backward */
+/* render_backward (rasterizer.cpp:320-397).  dL_dimage: H*W*3 floats (device).
+ * grads: 65*N floats in the rgs_scene_params layout; viewspace_norm: N floats;
+ * visible: N int32 (0/1, or a count with RGS_FLAG_ACCUMULATE, so visible>0
+ * reproduces StoreGrads::add's OR).  Without RGS_FLAG_ACCUMULATE the outputs are
+ * overwritten; with it they are added to. */
+int rgs_render_backward(rgs_ctx* ctx, const rgs_scene* scene, const rgs_camera* cam,
+                        const rgs_records* records, const float* dL_dimage, unsigned flags,
+                        float* grads, float* viewspace_norm, int32_t* visible);
+
+/* ---------------------------------------------------------------- utilities */
+/* Camera::validate (camera.hpp:21-26) on the host; RGS_E_CAMERA with the
+ * reference's message on failure. */
+int rgs_camera_validate(rgs_ctx* ctx, const rgs_camera* cam);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RGS_CUDA_H */

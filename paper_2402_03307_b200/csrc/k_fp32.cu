@@ -1,0 +1,511 @@
+// FP32 tile kernels (K5 forward blend, K6 backward replay) and the binning /
+// bookkeeping kernels between preprocess and blend.
+//
+// K5/K6 evaluate every (pixel, splat) pair in FP32 together with a bound on the
+// error of that evaluation against the FP64 reference (rasterizer.cpp:97-122,
+// 437-468).  A gate decision (power > 0, alpha < 1/255, T(1-alpha) < 1e-4, and the
+// backward's unclamped alpha <= 0.99) whose FP32 value lies inside its bound marks
+// the pixel "slow": the thread stops, and k_blend_fp64 (k_fp64.cu) recomputes the
+// whole pixel in FP64.  Every decision the FP32 path keeps is therefore the FP64
+// decision, and the backward (K6) replays exactly those.
+#include "rgs_internal.cuh"
+
+namespace rgs_dev {
+
+// One staged splat of a tile batch.
+struct StagedSplat {
+    float4 mean;   // (mx_hi, my_hi, mx_lo, my_lo) relative to the tile origin
+    float4 conic;  // (ca, cb, cc, alpha_base)
+    float4 color;  // (r, g, b, p_alpha)   (flow: (fx, fy, 0, p_alpha))
+    float2 guard;  // (c_s, p_clamp)
+};
+
+template <bool FLOW>
+__device__ __forceinline__ void stage(const SplatArrays& sp, uint32_t id, double px0, double py0, StagedSplat* dst) {
+    const double2 m = sp.mean2[id];
+    const double lx = m.x - px0, ly = m.y - py0;
+    const float hx = (float)lx, hy = (float)ly;
+    dst->mean = make_float4(hx, hy, (float)(lx - (double)hx), (float)(ly - (double)hy));
+    dst->conic = sp.conic_f[id];
+    float4 c = sp.color_f[id];
+    if (FLOW) {
+        const double4 f = sp.flow_radius[id];
+        c = make_float4((float)f.x, (float)f.y, 0.f, c.w);
+    }
+    dst->color = c;
+    dst->guard = sp.guard_f[id];
+}
+
+// Outcome of one FP32 evaluation.
+enum { kSkip = 0, kAccept = 1, kAmbiguous = 2 };
+
+// Gate evaluation shared by K5 and K6 (same instruction sequence -> same decisions).
+__device__ __forceinline__ int eval_gates(const StagedSplat& s, float fpx, float fpy, float* power, float* dx,
+                                          float* dy, float* margin) {
+    const float ddx = __fsub_rn(__fsub_rn(fpx, s.mean.x), s.mean.z);
+    const float ddy = __fsub_rn(__fsub_rn(fpy, s.mean.y), s.mean.w);
+    const float t1 = __fmul_rn(__fmul_rn(s.conic.x, ddx), ddx);
+    const float t2 = __fmul_rn(__fmul_rn(s.conic.z, ddy), ddy);
+    const float t3 = __fmul_rn(__fmul_rn(s.conic.y, ddx), ddy);
+    const float Q = __fadd_rn(t1, t2);
+    const float p = __fsub_rn(__fmul_rn(-0.5f, Q), t3);
+    const float E = __fmul_rn(s.guard.x, Q);
+    *power = p;
+    *dx = ddx;
+    *dy = ddy;
+    // power > 0 gate (rasterizer.cpp:107)
+    if (p > -E - 1e-30f) {
+        if (p > E + 1e-30f) return kSkip;
+        return kAmbiguous;
+    }
+    // alpha < 1/255 gate (rasterizer.cpp:109), decided in power space
+    const float M = __fadd_rn(E, kGuardFloor);
+    *margin = M;
+    if (p < __fsub_rn(s.color.w, M)) return kSkip;
+    if (p <= __fadd_rn(s.color.w, M)) return kAmbiguous;
+    return kAccept;
+}
+
+// K5: one CTA per 16x16 tile, one thread per pixel, splats staged 256 at a time.
+template <bool FLOW>
+__global__ void __launch_bounds__(256) k_blend_fp32(SplatArrays sp, const uint32_t* __restrict__ vals,
+                                                    const uint2* __restrict__ ranges, DevCamera cam, float3 bg,
+                                                    float* __restrict__ image, double* __restrict__ final_T,
+                                                    uint32_t* __restrict__ n_contrib, uint32_t* slow_list,
+                                                    int* slow_count) {
+    __shared__ StagedSplat sm[kTilePixels];
+    const int tile = blockIdx.x;
+    const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
+    const int lx = threadIdx.x & (kTile - 1), ly = threadIdx.x / kTile;
+    const int px = tx * kTile + lx, py = ty * kTile + ly;
+    const bool inside = px < cam.width && py < cam.height;
+    const uint2 rg = ranges[tile];
+    const double px0 = tx * kTile, py0 = ty * kTile;
+    const float fpx = (float)lx, fpy = (float)ly;
+
+    float T = 1.f, errT = 0.f, acc0 = 0.f, acc1 = 0.f, acc2 = 0.f;
+    int contrib = 0;
+    bool done = !inside, slow = false;
+
+    for (uint32_t start = rg.x; start < rg.y; start += kTilePixels) {
+        if (__syncthreads_count(done) == kTilePixels) break;
+        const uint32_t j = start + threadIdx.x;
+        if (j < rg.y) stage<FLOW>(sp, vals[j], px0, py0, &sm[threadIdx.x]);
+        __syncthreads();
+        const int n = min((uint32_t)kTilePixels, rg.y - start);
+        for (int k = 0; k < n && !done; ++k) {
+            const StagedSplat s = sm[k];
+            float p, dx, dy, M;
+            const int g = eval_gates(s, fpx, fpy, &p, &dx, &dy, &M);
+            if (g == kSkip) continue;
+            if (g == kAmbiguous) {
+                slow = true;
+                done = true;
+                break;
+            }
+            const float raw = __fmul_rn(s.conic.w, __expf(p));
+            const float a = fminf(0.99f, raw);
+            // backward's clamp gate raw <= 0.99 (rasterizer.cpp:356)
+            if (fabsf(__fsub_rn(p, s.guard.y)) <= M) {
+                slow = true;
+                done = true;
+                break;
+            }
+            const float om = __fsub_rn(1.f, a);
+            const float test_T = __fmul_rn(T, om);
+            const float errN = errT + __fdividef(a * M, om) + 2.5e-7f;
+            if (fabsf(test_T - 1e-4f) <= test_T * errN + 1e-12f) {
+                slow = true;
+                done = true;
+                break;
+            }
+            if (test_T < 1e-4f) {  // rasterizer.cpp:111
+                done = true;
+                break;
+            }
+            const float w = a * T;
+            acc0 = fmaf(s.color.x, w, acc0);
+            acc1 = fmaf(s.color.y, w, acc1);
+            acc2 = fmaf(s.color.z, w, acc2);
+            T = test_T;
+            errT = errN;
+            contrib = (int)(start - rg.x) + k + 1;
+        }
+    }
+    if (!inside) return;
+    const uint32_t pix = (uint32_t)py * cam.width + px;
+    if (slow) {
+        slow_list[atomicAdd(slow_count, 1)] = pix;
+        return;
+    }
+    if (FLOW) {
+        image[(size_t)pix * 2 + 0] = acc0;
+        image[(size_t)pix * 2 + 1] = acc1;
+    } else {
+        image[(size_t)pix * 3 + 0] = fmaf(T, bg.x, acc0);
+        image[(size_t)pix * 3 + 1] = fmaf(T, bg.y, acc1);
+        image[(size_t)pix * 3 + 2] = fmaf(T, bg.z, acc2);
+        final_T[pix] = (double)T;
+        n_contrib[pix] = (uint32_t)contrib;
+    }
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// K6: back-to-front replay per tile (rasterizer.cpp:437-468) for the FP32
+// pixels; per-splat partial sums are warp-reduced, combined in shared memory
+// and scattered with one FP64 atomic per (tile, splat, component).
+__global__ void __launch_bounds__(256) k_backward_fp32(SplatArrays sp, const uint32_t* __restrict__ vals,
+                                                       const uint2* __restrict__ ranges, DevCamera cam, float3 bg,
+                                                       const double* __restrict__ final_T,
+                                                       const uint32_t* __restrict__ n_contrib,
+                                                       const float* __restrict__ dL, double* sg) {
+    __shared__ StagedSplat sm[kTilePixels];
+    __shared__ uint32_t sid[kTilePixels];
+    __shared__ float acc[9][kTilePixels];
+    __shared__ int s_max;
+    const int tile = blockIdx.x;
+    const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
+    const int lx = threadIdx.x & (kTile - 1), ly = threadIdx.x / kTile;
+    const int px = tx * kTile + lx, py = ty * kTile + ly;
+    const bool inside = px < cam.width && py < cam.height;
+    const uint2 rg = ranges[tile];
+    const double px0 = tx * kTile, py0 = ty * kTile;
+    const float fpx = (float)lx, fpy = (float)ly;
+    const int lane = threadIdx.x & 31;
+
+    int contrib = 0;
+    float T_run = 1.f, g0 = 0.f, g1 = 0.f, g2 = 0.f, s0 = 0.f, s1 = 0.f, s2 = 0.f;
+    if (threadIdx.x == 0) s_max = 0;
+    if (inside) {
+        const uint32_t pix = (uint32_t)py * cam.width + px;
+        const uint32_t c = n_contrib[pix];
+        if (!(c & kSlowBit)) {
+            contrib = (int)c;
+            const float fT = (float)final_T[pix];
+            T_run = fT;
+            g0 = dL[(size_t)pix * 3 + 0];
+            g1 = dL[(size_t)pix * 3 + 1];
+            g2 = dL[(size_t)pix * 3 + 2];
+            s0 = bg.x * fT;
+            s1 = bg.y * fT;
+            s2 = bg.z * fT;
+        }
+    }
+    __syncthreads();
+    if (contrib > 0) atomicMax(&s_max, contrib);
+    __syncthreads();
+    const int max_contrib = s_max;
+
+    for (int end = max_contrib; end > 0; end -= kTilePixels) {
+        const int beg = end > kTilePixels ? end - kTilePixels : 0;
+        const int cnt = end - beg;
+        if ((int)threadIdx.x < cnt) {
+            const uint32_t id = vals[rg.x + beg + threadIdx.x];
+            sid[threadIdx.x] = id;
+            stage<false>(sp, id, px0, py0, &sm[threadIdx.x]);
+        }
+#pragma unroll
+        for (int q = 0; q < 9; ++q) acc[q][threadIdx.x] = 0.f;
+        __syncthreads();
+        for (int k = cnt - 1; k >= 0; --k) {
+            const int pos = beg + k;
+            float v[9];
+#pragma unroll
+            for (int q = 0; q < 9; ++q) v[q] = 0.f;
+            bool act = false;
+            if (pos < contrib) {
+                const StagedSplat s = sm[k];
+                float p, dx, dy, M;
+                const int g = eval_gates(s, fpx, fpy, &p, &dx, &dy, &M);
+                if (g == kAccept) {
+                    const float a = fminf(0.99f, __fmul_rn(s.conic.w, __expf(p)));
+                    const float om = 1.f - a;
+                    const float T_before = T_run / om;
+                    const float w = a * T_before;
+                    v[0] = w * g0;
+                    v[1] = w * g1;
+                    v[2] = w * g2;
+                    const float dL_da = g0 * (s.color.x * T_before - s0 / om) +
+                                        g1 * (s.color.y * T_before - s1 / om) +
+                                        g2 * (s.color.z * T_before - s2 / om);
+                    if (p <= s.guard.y) {  // unclamped alpha <= 0.99
+                        v[8] = dL_da * (a / s.conic.w);
+                        const float dp = dL_da * a;
+                        v[3] = dp * (-0.5f * dx * dx);
+                        v[4] = dp * (-dx * dy);
+                        v[5] = dp * (-0.5f * dy * dy);
+                        v[6] = dp * (s.conic.x * dx + s.conic.y * dy);
+                        v[7] = dp * (s.conic.y * dx + s.conic.z * dy);
+                    }
+                    s0 = fmaf(s.color.x, w, s0);
+                    s1 = fmaf(s.color.y, w, s1);
+                    s2 = fmaf(s.color.z, w, s2);
+                    T_run = T_before;
+                    act = true;
+                }
+            }
+            const unsigned am = __ballot_sync(0xffffffffu, act);
+            if (am) {
+                if (__popc(am) == 1) {
+                    if (act) {
+#pragma unroll
+                        for (int q = 0; q < 9; ++q)
+                            if (v[q] != 0.f) atomicAdd(&acc[q][k], v[q]);
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 9; ++q) v[q] = warp_sum(v[q]);
+                    if (lane == 0) {
+#pragma unroll
+                        for (int q = 0; q < 9; ++q)
+                            if (v[q] != 0.f) atomicAdd(&acc[q][k], v[q]);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        if ((int)threadIdx.x < cnt) {
+            double* o = sg + (size_t)sid[threadIdx.x] * 9;
+#pragma unroll
+            for (int q = 0; q < 9; ++q) {
+                const float val = acc[q][threadIdx.x];
+                if (val != 0.f) atomicAdd(o + q, (double)val);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Binning.
+
+__global__ void k_gather_counts(const uint32_t* __restrict__ ids, const uint32_t* __restrict__ tiles, int n,
+                                uint32_t* counts) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) counts[k] = tiles[ids[k]];
+}
+
+// Duplicate-with-key: splats in depth order emit (tile, splat) pairs; a stable
+// sort on the tile id then yields per-tile lists in (depth, index) order.
+__global__ void k_duplicate(const uint32_t* __restrict__ ids, const uint32_t* __restrict__ offsets,
+                            const uint32_t* __restrict__ counts, int n, const ushort4* __restrict__ rect,
+                            int tiles_x, uint32_t* tile_keys, uint32_t* pair_vals) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const uint32_t c = counts[k];
+    if (c == 0) return;
+    const uint32_t id = ids[k];
+    uint32_t o = offsets[k];
+    const ushort4 r = rect[id];
+    for (int y = r.z; y <= r.w; ++y)
+        for (int x = r.x; x <= r.y; ++x) {
+            tile_keys[o] = (uint32_t)y * tiles_x + x;
+            pair_vals[o] = id;
+            ++o;
+        }
+}
+
+__global__ void k_tile_ranges(const uint32_t* __restrict__ keys, long long n, uint2* ranges) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t k = keys[i];
+    if (i == 0 || keys[i - 1] != k) ranges[k].x = (uint32_t)i;
+    if (i == n - 1 || keys[i + 1] != k) ranges[k].y = (uint32_t)(i + 1);
+}
+
+// ---------------------------------------------------------------------------
+// Records export / scene layout.
+
+struct OutSplat {
+    double mean2[2];
+    double conic[3];
+    double depth;
+    double color[3];
+    double alpha_base;
+    double flow2[2];
+    double radius;
+    int32_t source_index;
+    int32_t pad;
+};
+
+__global__ void k_compact_index(const uint8_t* __restrict__ valid, const uint32_t* __restrict__ scan, int n,
+                                uint32_t* compact_ids) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && valid[i]) compact_ids[scan[i]] = (uint32_t)i;
+}
+
+__global__ void k_export_splats(SplatArrays sp, const uint32_t* __restrict__ ids, int n, OutSplat* out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const uint32_t i = ids[k];
+    OutSplat o;
+    const double2 m = sp.mean2[i];
+    const double4 c = sp.conic_ab[i];
+    const double4 cd = sp.color_depth[i];
+    const double4 fr = sp.flow_radius[i];
+    o.mean2[0] = m.x;
+    o.mean2[1] = m.y;
+    o.conic[0] = c.x;
+    o.conic[1] = c.y;
+    o.conic[2] = c.z;
+    o.alpha_base = c.w;
+    o.color[0] = cd.x;
+    o.color[1] = cd.y;
+    o.color[2] = cd.z;
+    o.depth = cd.w;
+    o.flow2[0] = fr.x;
+    o.flow2[1] = fr.y;
+    o.radius = fr.z;
+    o.source_index = sp.source_index ? sp.source_index[i] : (int32_t)i;
+    o.pad = 0;
+    out[k] = o;
+}
+
+__global__ void k_map_ids(const uint32_t* __restrict__ vals, long long n, const uint32_t* __restrict__ scan,
+                          int32_t* out) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = (int32_t)scan[vals[i]];
+}
+
+__global__ void k_valid_u32(const uint8_t* __restrict__ v, int n, uint32_t* out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = v[i];
+}
+
+__global__ void k_source_keys(const int32_t* __restrict__ src, int n, uint32_t* keys, uint32_t* vals) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        keys[i] = (uint32_t)src[i] ^ 0x80000000u;  // signed -> order-preserving unsigned
+        vals[i] = (uint32_t)i;
+    }
+}
+
+// Host upload layout -> device SoA blocks (see rgs_scene_params).
+__global__ void k_scene_pack(const float* __restrict__ mean, const float* __restrict__ ls,
+                             const float* __restrict__ rot, const float* __restrict__ op,
+                             const float* __restrict__ sh, int n, float* P) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float4* pm = reinterpret_cast<float4*>(P);
+    float4* pl = reinterpret_cast<float4*>(P + 4 * (size_t)n);
+    float4* r0 = reinterpret_cast<float4*>(P + 8 * (size_t)n);
+    float4* r1 = reinterpret_cast<float4*>(P + 12 * (size_t)n);
+    pm[i] = make_float4(mean[4 * (size_t)i], mean[4 * (size_t)i + 1], mean[4 * (size_t)i + 2], mean[4 * (size_t)i + 3]);
+    pl[i] = make_float4(ls[4 * (size_t)i], ls[4 * (size_t)i + 1], ls[4 * (size_t)i + 2], ls[4 * (size_t)i + 3]);
+    const float* r = rot + 8 * (size_t)i;
+    r0[i] = make_float4(r[0], r[1], r[2], r[3]);
+    r1[i] = make_float4(r[4], r[5], r[6], r[7]);
+    const float* s = sh + 48 * (size_t)i;
+    float v[48];
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch)
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k * 3 + ch] = s[ch * 16 + k];
+#pragma unroll
+    for (int b = 0; b < 12; ++b)
+        reinterpret_cast<float4*>(P + (16 + 4 * (size_t)b) * n)[i] =
+            make_float4(v[4 * b], v[4 * b + 1], v[4 * b + 2], v[4 * b + 3]);
+    P[64 * (size_t)n + i] = op[i];
+}
+
+__global__ void k_scene_unpack(const float* __restrict__ P, int n, double* mean, double* ls, double* rot,
+                               double* op, double* sh) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float4 m = reinterpret_cast<const float4*>(P)[i];
+    const float4 l = reinterpret_cast<const float4*>(P + 4 * (size_t)n)[i];
+    const float4 a = reinterpret_cast<const float4*>(P + 8 * (size_t)n)[i];
+    const float4 b = reinterpret_cast<const float4*>(P + 12 * (size_t)n)[i];
+    double* pm = mean + 4 * (size_t)i;
+    pm[0] = m.x; pm[1] = m.y; pm[2] = m.z; pm[3] = m.w;
+    double* pl = ls + 4 * (size_t)i;
+    pl[0] = l.x; pl[1] = l.y; pl[2] = l.z; pl[3] = l.w;
+    double* pr = rot + 8 * (size_t)i;
+    pr[0] = a.x; pr[1] = a.y; pr[2] = a.z; pr[3] = a.w;
+    pr[4] = b.x; pr[5] = b.y; pr[6] = b.z; pr[7] = b.w;
+    op[i] = P[64 * (size_t)n + i];
+    for (int j = 0; j < 48; ++j) {
+        const int k = j / 3, ch = j % 3;
+        sh[48 * (size_t)i + ch * 16 + k] = P[(16 + 4 * (size_t)(j / 4)) * n + 4 * (size_t)i + (j % 4)];
+    }
+}
+
+}  // namespace rgs_dev
+
+namespace rgs_launch {
+using namespace rgs_dev;
+
+static inline int blocks(long long n, int t) { return (int)((n + t - 1) / t); }
+
+void blend_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges, const DevCamera& cam,
+                float3 bg, int flow_mode, float* image, double* final_T, uint32_t* n_contrib, uint32_t* slow_list,
+                int* slow_count, cudaStream_t s) {
+    const int tiles = cam.tiles_x * cam.tiles_y;
+    if (flow_mode)
+        k_blend_fp32<true><<<tiles, kTilePixels, 0, s>>>(sp, pair_vals, ranges, cam, bg, image, final_T, n_contrib,
+                                                          slow_list, slow_count);
+    else
+        k_blend_fp32<false><<<tiles, kTilePixels, 0, s>>>(sp, pair_vals, ranges, cam, bg, image, final_T, n_contrib,
+                                                           slow_list, slow_count);
+}
+
+void backward_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges, const DevCamera& cam,
+                   float3 bg, const double* final_T, const uint32_t* n_contrib, const float* dL_dimage,
+                   double* screen_grads, cudaStream_t s) {
+    const int tiles = cam.tiles_x * cam.tiles_y;
+    k_backward_fp32<<<tiles, kTilePixels, 0, s>>>(sp, pair_vals, ranges, cam, bg, final_T, n_contrib, dL_dimage,
+                                                  screen_grads);
+}
+
+void gather_counts(const uint32_t* sorted_ids, const uint32_t* tiles, int n, uint32_t* counts, cudaStream_t s) {
+    if (n > 0) k_gather_counts<<<blocks(n, 256), 256, 0, s>>>(sorted_ids, tiles, n, counts);
+}
+
+void duplicate(const uint32_t* sorted_ids, const uint32_t* offsets, const uint32_t* counts, int n, const ushort4* rect,
+               int tiles_x, uint32_t* tile_keys, uint32_t* pair_vals, cudaStream_t s) {
+    if (n > 0)
+        k_duplicate<<<blocks(n, 256), 256, 0, s>>>(sorted_ids, offsets, counts, n, rect, tiles_x, tile_keys, pair_vals);
+}
+
+void tile_ranges(const uint32_t* keys, long long n_pairs, int n_tiles, uint2* ranges, cudaStream_t s) {
+    cudaMemsetAsync(ranges, 0, sizeof(uint2) * (size_t)n_tiles, s);
+    if (n_pairs > 0) k_tile_ranges<<<blocks(n_pairs, 256), 256, 0, s>>>(keys, n_pairs, ranges);
+}
+
+void compact_index(const uint8_t* valid, const uint32_t* scan, int n, uint32_t* compact_ids, cudaStream_t s) {
+    if (n > 0) k_compact_index<<<blocks(n, 256), 256, 0, s>>>(valid, scan, n, compact_ids);
+}
+
+void export_splats(const SplatArrays& sp, const uint32_t* compact_ids, int n_valid, void* out, cudaStream_t s) {
+    if (n_valid > 0)
+        k_export_splats<<<blocks(n_valid, 128), 128, 0, s>>>(sp, compact_ids, n_valid, reinterpret_cast<OutSplat*>(out));
+}
+
+void map_ids(const uint32_t* pair_vals, long long n_pairs, const uint32_t* scan, int32_t* out, cudaStream_t s) {
+    if (n_pairs > 0) k_map_ids<<<blocks(n_pairs, 256), 256, 0, s>>>(pair_vals, n_pairs, scan, out);
+}
+
+void valid_to_u32(const uint8_t* valid, int n, uint32_t* out, cudaStream_t s) {
+    if (n > 0) k_valid_u32<<<blocks(n, 256), 256, 0, s>>>(valid, n, out);
+}
+
+void source_keys(const int32_t* src, int n, uint32_t* keys, uint32_t* vals, cudaStream_t s) {
+    if (n > 0) k_source_keys<<<blocks(n, 256), 256, 0, s>>>(src, n, keys, vals);
+}
+
+void scene_pack(const float* mean, const float* ls, const float* rot, const float* op, const float* sh, int n,
+                float* params, cudaStream_t s) {
+    if (n > 0) k_scene_pack<<<blocks(n, 128), 128, 0, s>>>(mean, ls, rot, op, sh, n, params);
+}
+
+void scene_unpack(const float* params, int n, double* mean, double* ls, double* rot, double* op, double* sh,
+                  cudaStream_t s) {
+    if (n > 0) k_scene_unpack<<<blocks(n, 128), 128, 0, s>>>(params, n, mean, ls, rot, op, sh);
+}
+
+}  // namespace rgs_launch

@@ -1,0 +1,760 @@
+// FP64 kernels: per-Gaussian slice+project+SH (K1), FP64 pixel blend (guard-band
+// fix-up / reference mode), FP64 backward replay of those pixels, and the
+// per-Gaussian backward chain (K7).
+//
+// Compiled with -fmad=false: the FP64 expression order is the reference's
+// (see fp64_math.cuh), which is what makes tile rectangles, depths and culls
+// bit-identical to the CPU oracle.
+#include "fp64_math.cuh"
+#include "rgs_internal.cuh"
+
+namespace rgs_dev {
+
+__device__ __forceinline__ unsigned long long order_key(double d) {
+    unsigned long long b = (unsigned long long)__double_as_longlong(d);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// rasterizer.cpp:26-38
+__device__ __forceinline__ uint32_t d_tile_rect(double mx, double my, double r, int tiles_x, int tiles_y,
+                                                ushort4* rect) {
+    int a;
+    a = x86_double_to_int(floor((mx - r) / kTile));
+    int x0 = a > 0 ? a : 0;
+    a = x86_double_to_int(floor((mx + r) / kTile));
+    int x1 = a < tiles_x - 1 ? a : tiles_x - 1;
+    a = x86_double_to_int(floor((my - r) / kTile));
+    int y0 = a > 0 ? a : 0;
+    a = x86_double_to_int(floor((my + r) / kTile));
+    int y1 = a < tiles_y - 1 ? a : tiles_y - 1;
+    if (!(x0 <= x1 && y0 <= y1)) {
+        *rect = make_ushort4(0, 0, 0, 0);
+        return 0;
+    }
+    *rect = make_ushort4((unsigned short)x0, (unsigned short)x1, (unsigned short)y0, (unsigned short)y1);
+    return (uint32_t)(x1 - x0 + 1) * (uint32_t)(y1 - y0 + 1);
+}
+
+// FP32 guard-band constants of one splat.
+__device__ __forceinline__ void d_guard(double ca, double cb, double cc, double ab, float* p_alpha, float* c_s,
+                                        float* p_clamp) {
+    *p_alpha = (float)log(kMinAlpha / ab);
+    *p_clamp = (float)log(kAlphaClamp / ab);
+    double kappa = fabs(cb) / sqrt(ca * cc);
+    double cs = (kappa < 0.999) ? 1.5e-6 * (1 + kappa) / (1 - kappa) : 1e30;
+    if (!(ca > 0) || !(cc > 0)) cs = 1e30;
+    *c_s = (float)cs;
+}
+
+__device__ __forceinline__ void store_splat(const SplatArrays& out, int i, double mx, double my, double ca,
+                                            double cb, double cc, double ab, double r, double g, double b,
+                                            double depth, double fx, double fy, double radius, int tiles_x,
+                                            int tiles_y, uint32_t* ntiles) {
+    out.mean2[i] = make_double2(mx, my);
+    out.conic_ab[i] = make_double4(ca, cb, cc, ab);
+    out.color_depth[i] = make_double4(r, g, b, depth);
+    out.flow_radius[i] = make_double4(fx, fy, radius, 0.0);
+    ushort4 rect;
+    *ntiles = d_tile_rect(mx, my, radius, tiles_x, tiles_y, &rect);
+    out.rect[i] = rect;
+    float pa, cs, pc;
+    d_guard(ca, cb, cc, ab, &pa, &cs, &pc);
+    out.conic_f[i] = make_float4((float)ca, (float)cb, (float)cc, (float)ab);
+    out.color_f[i] = make_float4((float)r, (float)g, (float)b, pa);
+    out.guard_f[i] = make_float2(cs, pc);
+}
+
+__device__ __forceinline__ void count_valid(bool ok, int* n_valid) {
+    unsigned m = __ballot_sync(0xffffffffu, ok);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(n_valid, __popc(m));
+}
+
+// K1: slice + visibility gate + project + SH colour, one thread per Gaussian
+// (rasterizer.cpp:189-204, gaussian.cpp:32-47, rasterizer.cpp:215-276, sh.cpp:16-97).
+__global__ void __launch_bounds__(128) k_preprocess(ParamView P, int sh_degree, DevCamera cam, SplatArrays out,
+                                                    unsigned long long* err, int* n_valid) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    bool ok = false;
+    uint32_t ntiles = 0;
+    unsigned long long key = ~0ull;
+    if (i < P.n) {
+        const float4 m = P.mean()[i], l = P.ls()[i], r0 = P.rot0()[i], r1 = P.rot1()[i];
+        const double mean4[4] = {m.x, m.y, m.z, m.w};
+        const double ls[4] = {l.x, l.y, l.z, l.w};
+        const double rot[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+        const double op = P.opacity()[i];
+        SliceState s;
+        const int rc = d_slice(mean4, ls, rot, cam.time, s);
+        if (rc > 0) {
+            atomicMin(err, ((unsigned long long)i << 8) | (unsigned long long)rc);
+        } else if (rc == 0) {
+            const double dt = cam.time - mean4[3];
+            ProjState o;
+            if (!(s.lambda * dt * dt > kVisibility) && d_project_geom(s, cam, op, o)) {
+                ok = true;
+                double basis[16];
+                d_sh_basis(o.dir, sh_degree, basis);
+                const int deg = sh_degree < 0 ? 0 : (sh_degree > 3 ? 3 : sh_degree);
+                const int K = (deg + 1) * (deg + 1);
+                const int nblk = (3 * K + 3) / 4;
+                float shv[48];
+#pragma unroll
+                for (int b = 0; b < 12; ++b) {
+                    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (b < nblk) v = P.sh(b)[i];
+                    shv[4 * b + 0] = v.x;
+                    shv[4 * b + 1] = v.y;
+                    shv[4 * b + 2] = v.z;
+                    shv[4 * b + 3] = v.w;
+                }
+                double col[3];
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch) {
+                    double a = (double)shv[ch] * basis[0];
+#pragma unroll
+                    for (int k = 1; k < 16; ++k)
+                        if (k < K) a += (double)shv[k * 3 + ch] * basis[k];
+                    double c = a + 0.5;
+                    col[ch] = c < 0 ? 0.0 : c;
+                }
+                double flow[2];
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    double a = o.T[r * 3 + 0] * s.speed[0];
+                    a += o.T[r * 3 + 1] * s.speed[1];
+                    a += o.T[r * 3 + 2] * s.speed[2];
+                    flow[r] = a;
+                }
+                store_splat(out, i, o.mean2[0], o.mean2[1], o.conic[0], o.conic[1], o.conic[2], o.alpha_base,
+                            col[0], col[1], col[2], o.p[2], flow[0], flow[1], o.radius, cam.tiles_x, cam.tiles_y,
+                            &ntiles);
+                key = order_key(o.p[2]);
+            }
+        }
+        out.valid[i] = ok ? 1 : 0;
+        out.tiles[i] = ntiles;
+        out.depth_key[i] = key;
+        out.depth_val[i] = (uint32_t)i;
+    }
+    count_valid(ok, n_valid);
+}
+
+// Host-provided splats (rasterize_forward, rasterizer.cpp:278-306).
+struct HostSplat {
+    double mean2[2];
+    double conic[3];
+    double depth;
+    double color[3];
+    double alpha_base;
+    double flow2[2];
+    double radius;
+    int32_t source_index;
+    int32_t pad;
+};
+
+__global__ void k_splats_from_host(const HostSplat* sp, int n, DevCamera cam, SplatArrays out, int* n_valid) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        const HostSplat s = sp[i];
+        uint32_t ntiles = 0;
+        store_splat(out, i, s.mean2[0], s.mean2[1], s.conic[0], s.conic[1], s.conic[2], s.alpha_base, s.color[0],
+                    s.color[1], s.color[2], s.depth, s.flow2[0], s.flow2[1], s.radius, cam.tiles_x, cam.tiles_y,
+                    &ntiles);
+        out.valid[i] = 1;
+        out.tiles[i] = ntiles;
+        out.depth_key[i] = order_key(s.depth);
+        out.depth_val[i] = (uint32_t)i;
+        out.source_index[i] = s.source_index;
+    }
+    count_valid(i < n, n_valid);
+}
+
+// ---------------------------------------------------------------------------
+// FP64 pixel blend, one warp per listed pixel (rasterizer.cpp:97-122 exactly).
+// Lanes evaluate 32 consecutive splats of the tile list in parallel; the
+// sequential transmittance walk is then replayed identically by every lane.
+__global__ void __launch_bounds__(256) k_blend_fp64(SplatArrays sp, const uint32_t* __restrict__ vals,
+                                                    const uint2* __restrict__ ranges, DevCamera cam, double3 bg,
+                                                    int flow_mode, float* image, double* final_T,
+                                                    uint32_t* n_contrib, const uint32_t* __restrict__ list,
+                                                    const int* __restrict__ count) {
+    const int lane = threadIdx.x & 31;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int total = *count;
+    for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < total; w += nwarps) {
+        const uint32_t pix = list[w];
+        const int x = pix % cam.width, y = pix / cam.width;
+        const int tile = (y / kTile) * cam.tiles_x + (x / kTile);
+        const uint2 rg = ranges[tile];
+        double T = 1, acc0 = 0, acc1 = 0, acc2 = 0;
+        int contrib = 0;
+        bool done = false;
+        for (uint32_t base = rg.x; base < rg.y && !done; base += 32) {
+            const uint32_t j = base + lane;
+            bool accept = false;
+            double a = 0, c0 = 0, c1 = 0, c2 = 0;
+            if (j < rg.y) {
+                const uint32_t id = vals[j];
+                const double2 m = sp.mean2[id];
+                const double4 cab = sp.conic_ab[id];
+                const double dx = x - m.x, dy = y - m.y;
+                const double power = -0.5 * (cab.x * dx * dx + cab.z * dy * dy) - cab.y * dx * dy;
+                if (!(power > 0)) {
+                    a = smin(kAlphaClamp, cab.w * rgs_exp::glibc_exp(power));
+                    accept = !(a < kMinAlpha);
+                }
+                if (accept) {
+                    if (flow_mode) {
+                        const double4 f = sp.flow_radius[id];
+                        c0 = f.x;
+                        c1 = f.y;
+                        c2 = 0;
+                    } else {
+                        const double4 c = sp.color_depth[id];
+                        c0 = c.x;
+                        c1 = c.y;
+                        c2 = c.z;
+                    }
+                }
+            }
+            unsigned mask = __ballot_sync(0xffffffffu, accept);
+            while (mask) {
+                const int l = __ffs(mask) - 1;
+                mask &= mask - 1;
+                const double al = __shfl_sync(0xffffffffu, a, l);
+                const double test_T = T * (1 - al);
+                if (test_T < kStopT) {
+                    done = true;
+                    break;
+                }
+                const double wgt = al * T;
+                acc0 = acc0 + __shfl_sync(0xffffffffu, c0, l) * wgt;
+                acc1 = acc1 + __shfl_sync(0xffffffffu, c1, l) * wgt;
+                acc2 = acc2 + __shfl_sync(0xffffffffu, c2, l) * wgt;
+                T = test_T;
+                contrib = (int)(base + l - rg.x) + 1;
+            }
+        }
+        if (lane == 0) {
+            acc0 = acc0 + T * bg.x;
+            acc1 = acc1 + T * bg.y;
+            acc2 = acc2 + T * bg.z;
+            if (flow_mode) {
+                image[(size_t)pix * 2 + 0] = (float)acc0;
+                image[(size_t)pix * 2 + 1] = (float)acc1;
+            } else {
+                image[(size_t)pix * 3 + 0] = (float)acc0;
+                image[(size_t)pix * 3 + 1] = (float)acc1;
+                image[(size_t)pix * 3 + 2] = (float)acc2;
+                if (final_T) final_T[pix] = T;
+                if (n_contrib) n_contrib[pix] = (uint32_t)contrib | kSlowBit;
+            }
+        }
+    }
+}
+
+__global__ void k_mark_all_slow(int n, uint32_t* list, int* count) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) list[i] = (uint32_t)i;
+    if (i == 0) *count = n;
+}
+
+// ---------------------------------------------------------------------------
+// FP64 backward replay of the listed (slow) pixels, one warp per pixel
+// (rasterizer.cpp:437-468).  Lanes evaluate 32 positions (descending) in parallel,
+// the T/suffix recursion is replayed by every lane, then each lane scatters its
+// splat's nine screen-space gradients with FP64 atomics.
+__global__ void __launch_bounds__(256) k_backward_fp64(SplatArrays sp, const uint32_t* __restrict__ vals,
+                                                       const uint2* __restrict__ ranges, DevCamera cam,
+                                                       double3 bg, const double* __restrict__ final_T,
+                                                       const uint32_t* __restrict__ n_contrib,
+                                                       const float* __restrict__ dL, const uint32_t* list,
+                                                       const int* count, double* sg) {
+    const int lane = threadIdx.x & 31;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int total = *count;
+    for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < total; w += nwarps) {
+        const uint32_t pix = list[w];
+        const int contrib = (int)(n_contrib[pix] & ~kSlowBit);
+        if (contrib == 0) continue;
+        const int x = pix % cam.width, y = pix / cam.width;
+        const int tile = (y / kTile) * cam.tiles_x + (x / kTile);
+        const uint2 rg = ranges[tile];
+        const double g0 = dL[(size_t)pix * 3 + 0], g1 = dL[(size_t)pix * 3 + 1], g2 = dL[(size_t)pix * 3 + 2];
+        const double fT = final_T[pix];
+        double T_run = fT;
+        double s0 = bg.x * fT, s1 = bg.y * fT, s2 = bg.z * fT;
+        for (int hi = contrib; hi > 0; hi -= 32) {
+            const int pos = hi - 1 - lane;
+            bool pass = false;
+            double a = 0, raw = 0, dx = 0, dy = 0, c0 = 0, c1 = 0, c2 = 0;
+            double4 cab = make_double4(0, 0, 0, 0);
+            uint32_t id = 0;
+            if (pos >= 0) {
+                id = vals[rg.x + pos];
+                const double2 m = sp.mean2[id];
+                cab = sp.conic_ab[id];
+                dx = (double)x - m.x;
+                dy = (double)y - m.y;
+                const double power = -0.5 * (cab.x * dx * dx + cab.z * dy * dy) - cab.y * dx * dy;
+                if (!(power > 0)) {
+                    raw = cab.w * rgs_exp::glibc_exp(power);
+                    a = smin(kAlphaClamp, raw);
+                    pass = !(a < kMinAlpha);
+                }
+                if (pass) {
+                    const double4 c = sp.color_depth[id];
+                    c0 = c.x;
+                    c1 = c.y;
+                    c2 = c.z;
+                }
+            }
+            // Sequential recursion over lanes 0..31 (= descending positions).
+            double my_Tb = 0, my_s0 = 0, my_s1 = 0, my_s2 = 0;
+            unsigned mask = __ballot_sync(0xffffffffu, pass);
+            while (mask) {
+                const int l = __ffs(mask) - 1;
+                mask &= mask - 1;
+                const double al = __shfl_sync(0xffffffffu, a, l);
+                const double T_before = T_run / (1 - al);
+                const double wgt = al * T_before;
+                if (lane == l) {
+                    my_Tb = T_before;
+                    my_s0 = s0;
+                    my_s1 = s1;
+                    my_s2 = s2;
+                }
+                s0 = s0 + __shfl_sync(0xffffffffu, c0, l) * wgt;
+                s1 = s1 + __shfl_sync(0xffffffffu, c1, l) * wgt;
+                s2 = s2 + __shfl_sync(0xffffffffu, c2, l) * wgt;
+                T_run = T_before;
+            }
+            if (pass) {
+                const double T_before = my_Tb;
+                const double wgt = a * T_before;
+                double* o = sg + (size_t)id * 9;
+                atomicAdd(o + 0, wgt * g0);
+                atomicAdd(o + 1, wgt * g1);
+                atomicAdd(o + 2, wgt * g2);
+                const double v0 = c0 * T_before - my_s0 / (1 - a);
+                const double v1 = c1 * T_before - my_s1 / (1 - a);
+                const double v2 = c2 * T_before - my_s2 / (1 - a);
+                double dL_da = g0 * v0;
+                dL_da += g1 * v1;
+                dL_da += g2 * v2;
+                if (raw <= kAlphaClamp) {
+                    atomicAdd(o + 8, dL_da * (a / cab.w));
+                    const double dpow = dL_da * a;
+                    atomicAdd(o + 3, dpow * (-0.5 * dx * dx));
+                    atomicAdd(o + 4, dpow * (-dx * dy));
+                    atomicAdd(o + 5, dpow * (-0.5 * dy * dy));
+                    atomicAdd(o + 6, dpow * (cab.x * dx + cab.y * dy));
+                    atomicAdd(o + 7, dpow * (cab.y * dx + cab.z * dy));
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K7: per-Gaussian backward (rasterizer.cpp:134-181, gaussian.cpp:57-101,
+// rotor.cpp:138-194).  Recomputes the forward chain from the parameters.
+__global__ void __launch_bounds__(128) k_gaussian_backward(ParamView P, int sh_degree, DevCamera cam,
+                                                           const uint8_t* __restrict__ valid,
+                                                           const double* __restrict__ sgrad, int accumulate,
+                                                           float* grads, float* vnorm, int32_t* visible) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.n) return;
+    const int n = P.n;
+    float4* gm = reinterpret_cast<float4*>(grads);
+    float4* gl = reinterpret_cast<float4*>(grads + 4 * (size_t)n);
+    float4* gr0 = reinterpret_cast<float4*>(grads + 8 * (size_t)n);
+    float4* gr1 = reinterpret_cast<float4*>(grads + 12 * (size_t)n);
+    float* gop = grads + 64 * (size_t)n;
+    if (!valid[i]) {
+        if (!accumulate) {
+            const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+            gm[i] = z;
+            gl[i] = z;
+            gr0[i] = z;
+            gr1[i] = z;
+#pragma unroll
+            for (int b = 0; b < 12; ++b) reinterpret_cast<float4*>(grads + (16 + 4 * (size_t)b) * n)[i] = z;
+            gop[i] = 0.f;
+            vnorm[i] = 0.f;
+            visible[i] = 0;
+        }
+        return;
+    }
+    const float4 m = P.mean()[i], l = P.ls()[i], r0 = P.rot0()[i], r1 = P.rot1()[i];
+    const double mean4[4] = {m.x, m.y, m.z, m.w};
+    const double ls[4] = {l.x, l.y, l.z, l.w};
+    const double rot[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+    const double op = P.opacity()[i];
+    SliceState s;
+    d_slice(mean4, ls, rot, cam.time, s);
+    ProjState o;
+    d_project_geom(s, cam, op, o);
+
+    const double* g9 = sgrad + (size_t)i * 9;
+    const double dcol[3] = {g9[0], g9[1], g9[2]};
+    const double dcon[3] = {g9[3], g9[4], g9[5]};
+    const double dm2[2] = {g9[6], g9[7]};
+    const double dab = g9[8];
+
+    double out[65];
+#pragma unroll
+    for (int k = 0; k < 65; ++k) out[k] = 0;
+
+    // ---- colour path: SH coefficients and view direction (rasterizer.cpp:137-147)
+    const int deg = sh_degree < 0 ? 0 : (sh_degree > 3 ? 3 : sh_degree);
+    const int K = (deg + 1) * (deg + 1);
+    double basis[16];
+    d_sh_basis(o.dir, sh_degree, basis);
+    float shv[48];
+#pragma unroll
+    for (int b = 0; b < 12; ++b) {
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (b < (3 * K + 3) / 4) v = P.sh(b)[i];
+        shv[4 * b + 0] = v.x;
+        shv[4 * b + 1] = v.y;
+        shv[4 * b + 2] = v.z;
+        shv[4 * b + 3] = v.w;
+    }
+    double dL_ddir[3] = {0, 0, 0};
+    {
+        double bgrad[48];
+        d_sh_basis_grad(o.dir, sh_degree, bgrad);
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+            double a = (double)shv[ch] * basis[0];
+#pragma unroll
+            for (int k = 1; k < 16; ++k)
+                if (k < K) a += (double)shv[k * 3 + ch] * basis[k];
+            const bool clamped = (a + 0.5) < 0;
+            if (clamped || dcol[ch] == 0) continue;
+#pragma unroll
+            for (int k = 0; k < 16; ++k) out[17 + ch * 16 + k] += dcol[ch] * basis[k];
+#pragma unroll
+            for (int ax = 0; ax < 3; ++ax) {
+                double t = bgrad[ax] * (double)shv[ch];
+#pragma unroll
+                for (int k = 1; k < 16; ++k)
+                    if (k < K) t += bgrad[k * 3 + ax] * (double)shv[k * 3 + ch];
+                dL_ddir[ax] += dcol[ch] * t;
+            }
+        }
+    }
+    double dmean3[3] = {0, 0, 0};
+    if (dL_ddir[0] != 0 || dL_ddir[1] != 0 || dL_ddir[2] != 0) {
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+            double a = 0;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) a += ((r == c ? 1.0 : 0.0) - o.dir[r] * o.dir[c]) / o.dist * dL_ddir[c];
+            dmean3[r] += a;
+        }
+    }
+    // ---- alpha_base = opacity * decay
+    const double dL_ddecay = dab * o.opacity;
+    out[16] += dab * s.decay * o.opacity * (1 - o.opacity);
+
+    // ---- conic = cov2^-1 -> cov2 -> cov3, T
+    const double invdet = 1.0 / o.det;
+    const double con[4] = {o.cov2[3] * invdet, -o.cov2[1] * invdet, -o.cov2[2] * invdet, o.cov2[0] * invdet};
+    const double gh[4] = {dcon[0], dcon[1] / 2, dcon[1] / 2, dcon[2]};
+    double P1[4], H[4];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) P1[r * 2 + c] = (-con[r * 2]) * gh[c] + (-con[r * 2 + 1]) * gh[2 + c];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) H[r * 2 + c] = P1[r * 2] * con[c] + P1[r * 2 + 1] * con[2 + c];
+    double dcov3[9];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        const double q0 = o.T[r] * H[0] + o.T[3 + r] * H[2];
+        const double q1 = o.T[r] * H[1] + o.T[3 + r] * H[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) dcov3[r * 3 + c] = q0 * o.T[c] + q1 * o.T[3 + c];
+    }
+    double dT[6];
+    {
+        const double HH[4] = {H[0] + H[0], H[1] + H[2], H[2] + H[1], H[3] + H[3]};
+        double HT[6];
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) HT[r * 3 + c] = HH[r * 2] * o.T[c] + HH[r * 2 + 1] * o.T[3 + c];
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                double a = HT[r * 3 + 0] * s.cov[0 * 3 + c];
+                a += HT[r * 3 + 1] * s.cov[1 * 3 + c];
+                a += HT[r * 3 + 2] * s.cov[2 * 3 + c];
+                dT[r * 3 + c] = a;
+            }
+    }
+    // ---- mean2 = pinhole(p_cam); T = J R (J depends on p_cam)
+    const double z = o.p[2], z2 = z * z, z3 = z2 * z;
+    const double J[6] = {cam.fx / z, 0, -cam.fx * o.p[0] / z2, 0, cam.fy / z, -cam.fy * o.p[1] / z2};
+    double dpc[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) dpc[r] = J[r] * dm2[0] + J[3 + r] * dm2[1];
+    double dJ[6];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            double a = dT[r * 3 + 0] * cam.R[c * 3 + 0];
+            a += dT[r * 3 + 1] * cam.R[c * 3 + 1];
+            a += dT[r * 3 + 2] * cam.R[c * 3 + 2];
+            dJ[r * 3 + c] = a;
+        }
+    dpc[0] += dJ[2] * (-cam.fx / z2);
+    dpc[1] += dJ[5] * (-cam.fy / z2);
+    dpc[2] += dJ[0] * (-cam.fx / z2) + dJ[2] * (2 * cam.fx * o.p[0] / z3) + dJ[4] * (-cam.fy / z2) +
+              dJ[5] * (2 * cam.fy * o.p[1] / z3);
+#pragma unroll
+    for (int r = 0; r < 3; ++r) dmean3[r] += cam.R[r] * dpc[0] + cam.R[3 + r] * dpc[1] + cam.R[6 + r] * dpc[2];
+
+    // ---- slice_backward (gaussian.cpp:57-101), dL_dspeed = 0
+    {
+        const double W = s.W, lambda = 1 / W, dt = s.dt;
+        const double dL_dlambda = dL_ddecay * (-0.5 * dt * dt) * s.decay;
+        out[3] += dL_ddecay * lambda * dt * s.decay;
+        out[0] += dmean3[0];
+        out[1] += dmean3[1];
+        out[2] += dmean3[2];
+        out[3] += -(s.speed[0] * dmean3[0] + s.speed[1] * dmean3[1] + s.speed[2] * dmean3[2]);
+        double dV[3];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) dV[r] = (dt / W) * dmean3[r];
+        const double vdm = s.V[0] * dmean3[0] + s.V[1] * dmean3[1] + s.V[2] * dmean3[2];
+        double dW = -(dt * vdm) / (W * W);
+        double GV[3], SV[3];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+            GV[r] = dcov3[r * 3] * s.V[0] + dcov3[r * 3 + 1] * s.V[1] + dcov3[r * 3 + 2] * s.V[2];
+            SV[r] = (dcov3[r * 3] + dcov3[r]) * s.V[0] + (dcov3[r * 3 + 1] + dcov3[3 + r]) * s.V[1] +
+                    (dcov3[r * 3 + 2] + dcov3[6 + r]) * s.V[2];
+        }
+#pragma unroll
+        for (int r = 0; r < 3; ++r) dV[r] += (-SV[r]) / W;
+        dW += (s.V[0] * GV[0] + s.V[1] * GV[1] + s.V[2] * GV[2]) / (W * W);
+        dW += -dL_dlambda / (W * W);
+        double G4[16];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) G4[r * 4 + c] = 0;
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) G4[r * 4 + c] = dcov3[r * 3 + c];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) G4[r * 4 + 3] = dV[r];
+        G4[15] = dW;
+        // d log_scales: 2 q_k (R^T G4 R)_kk
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            double acc = 0;
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                double ga = 0;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) ga += G4[a * 4 + b] * s.R[b * 4 + k];
+                acc += s.R[a * 4 + k] * ga;
+            }
+            out[4 + k] += 2 * s.q[k] * acc;
+        }
+        // dL/dR = (G4 + G4^T) R diag(q)
+        double dR[16];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                double a = 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) a += (G4[r * 4 + k] + G4[k * 4 + r]) * s.R[k * 4 + c];
+                dR[r * 4 + c] = a * s.q[c];
+            }
+        // through the quadratic forms (to_matrix_jacobian, rotor.cpp:183-194)
+        const double* v = s.nrm;
+        double drn[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#define RGS_JT(e, a, b, c)               \
+    drn[a] += dR[e] * (c) * v[b];         \
+    drn[b] += dR[e] * (c) * v[a];
+        RGS_JT(0, 0, 0, 1.0) RGS_JT(0, 1, 1, -1.0) RGS_JT(0, 2, 2, -1.0) RGS_JT(0, 3, 3, -1.0)
+        RGS_JT(0, 4, 4, 1.0) RGS_JT(0, 5, 5, 1.0) RGS_JT(0, 6, 6, 1.0) RGS_JT(0, 7, 7, -1.0)
+        RGS_JT(1, 1, 0, 2.0) RGS_JT(1, 2, 4, -2.0) RGS_JT(1, 3, 5, -2.0) RGS_JT(1, 6, 7, 2.0)
+        RGS_JT(2, 1, 4, 2.0) RGS_JT(2, 2, 0, 2.0) RGS_JT(2, 3, 6, -2.0) RGS_JT(2, 5, 7, -2.0)
+        RGS_JT(3, 1, 5, 2.0) RGS_JT(3, 2, 6, 2.0) RGS_JT(3, 3, 0, 2.0) RGS_JT(3, 4, 7, 2.0)
+        RGS_JT(4, 1, 0, -2.0) RGS_JT(4, 2, 4, -2.0) RGS_JT(4, 3, 5, -2.0) RGS_JT(4, 6, 7, -2.0)
+        RGS_JT(5, 0, 0, 1.0) RGS_JT(5, 1, 1, -1.0) RGS_JT(5, 2, 2, 1.0) RGS_JT(5, 3, 3, 1.0)
+        RGS_JT(5, 4, 4, -1.0) RGS_JT(5, 5, 5, -1.0) RGS_JT(5, 6, 6, 1.0) RGS_JT(5, 7, 7, -1.0)
+        RGS_JT(6, 1, 2, -2.0) RGS_JT(6, 3, 7, 2.0) RGS_JT(6, 4, 0, 2.0) RGS_JT(6, 5, 6, -2.0)
+        RGS_JT(7, 1, 3, -2.0) RGS_JT(7, 2, 7, -2.0) RGS_JT(7, 4, 6, 2.0) RGS_JT(7, 5, 0, 2.0)
+        RGS_JT(8, 1, 4, 2.0) RGS_JT(8, 2, 0, -2.0) RGS_JT(8, 3, 6, -2.0) RGS_JT(8, 5, 7, 2.0)
+        RGS_JT(9, 1, 2, -2.0) RGS_JT(9, 3, 7, -2.0) RGS_JT(9, 4, 0, -2.0) RGS_JT(9, 5, 6, -2.0)
+        RGS_JT(10, 0, 0, 1.0) RGS_JT(10, 1, 1, 1.0) RGS_JT(10, 2, 2, -1.0) RGS_JT(10, 3, 3, 1.0)
+        RGS_JT(10, 4, 4, -1.0) RGS_JT(10, 5, 5, 1.0) RGS_JT(10, 6, 6, -1.0) RGS_JT(10, 7, 7, -1.0)
+        RGS_JT(11, 1, 7, 2.0) RGS_JT(11, 2, 3, -2.0) RGS_JT(11, 4, 5, -2.0) RGS_JT(11, 6, 0, 2.0)
+        RGS_JT(12, 1, 5, 2.0) RGS_JT(12, 2, 6, 2.0) RGS_JT(12, 3, 0, -2.0) RGS_JT(12, 4, 7, -2.0)
+        RGS_JT(13, 1, 3, -2.0) RGS_JT(13, 2, 7, 2.0) RGS_JT(13, 4, 6, 2.0) RGS_JT(13, 5, 0, -2.0)
+        RGS_JT(14, 1, 7, -2.0) RGS_JT(14, 2, 3, -2.0) RGS_JT(14, 4, 5, -2.0) RGS_JT(14, 6, 0, -2.0)
+        RGS_JT(15, 0, 0, 1.0) RGS_JT(15, 1, 1, 1.0) RGS_JT(15, 2, 2, 1.0) RGS_JT(15, 3, 3, -1.0)
+        RGS_JT(15, 4, 4, 1.0) RGS_JT(15, 5, 5, -1.0) RGS_JT(15, 6, 6, -1.0) RGS_JT(15, 7, 7, -1.0)
+#undef RGS_JT
+        // normalize_jacobian^T (rotor.cpp:138-168): Jn^T w = j1^T (j2^T w), j2 symmetric.
+        double l2 = sqnorm8(rot);
+        double eps = rotor_epsilon(rot);
+        double grad[8], upd[8];
+        epsilon_gradient(rot, grad);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) upd[k] = rot[k];
+        double delta = 0, ddr[8];
+        const bool branch = fabs(eps) >= kEpsBranch;
+        if (branch) {
+            const double rad = smax(l2 * l2 - 4 * eps * eps, 0.0);
+            const double sq = smax(sqrt(rad), 1e-30);
+            const double den = l2 + sq;
+            delta = -2 * eps / den;
+            const double dde = -2 / den - 8 * eps * eps / (sq * den * den);
+            const double ddl = 2 * eps * (1 + l2 / sq) / (den * den);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                ddr[k] = dde * grad[k] + ddl * 2 * rot[k];
+                upd[k] = rot[k] + delta * grad[k];
+            }
+        }
+        const double len = sqrt(sqnorm8(upd));
+        double u[8], w2[8];
+        double udot = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            u[k] = upd[k] / len;
+            udot += u[k] * drn[k];
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) w2[k] = (drn[k] - u[k] * udot) / len;
+        double gdot = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) gdot += grad[k] * w2[k];
+        // epsilon Hessian pairs: (0,7)=+1, (1,6)=-1, (2,5)=+1, (3,4)=-1
+        const double Hw[8] = {w2[7], -w2[6], w2[5], -w2[4], -w2[3], w2[2], -w2[1], w2[0]};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            double r;
+            if (branch) r = w2[k] + ddr[k] * gdot + delta * Hw[k];
+            else r = w2[k] - grad[k] * gdot / l2;
+            out[8 + k] += r;
+        }
+    }
+    // ---- write (scene SoA layout)
+    float f[65];
+#pragma unroll
+    for (int k = 0; k < 65; ++k) f[k] = (float)out[k];
+    float4 om = make_float4(f[0], f[1], f[2], f[3]);
+    float4 ol = make_float4(f[4], f[5], f[6], f[7]);
+    float4 o0 = make_float4(f[8], f[9], f[10], f[11]);
+    float4 o1 = make_float4(f[12], f[13], f[14], f[15]);
+    float shg[48];
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch)
+#pragma unroll
+        for (int k = 0; k < 16; ++k) shg[k * 3 + ch] = f[17 + ch * 16 + k];
+    const float vn = (float)sqrt(dm2[0] * dm2[0] + dm2[1] * dm2[1]);
+    if (accumulate) {
+        float4 t;
+        t = gm[i]; gm[i] = make_float4(t.x + om.x, t.y + om.y, t.z + om.z, t.w + om.w);
+        t = gl[i]; gl[i] = make_float4(t.x + ol.x, t.y + ol.y, t.z + ol.z, t.w + ol.w);
+        t = gr0[i]; gr0[i] = make_float4(t.x + o0.x, t.y + o0.y, t.z + o0.z, t.w + o0.w);
+        t = gr1[i]; gr1[i] = make_float4(t.x + o1.x, t.y + o1.y, t.z + o1.z, t.w + o1.w);
+#pragma unroll
+        for (int b = 0; b < 12; ++b) {
+            float4* p = reinterpret_cast<float4*>(grads + (16 + 4 * (size_t)b) * n) + i;
+            t = *p;
+            *p = make_float4(t.x + shg[4 * b], t.y + shg[4 * b + 1], t.z + shg[4 * b + 2], t.w + shg[4 * b + 3]);
+        }
+        gop[i] += f[16];
+        vnorm[i] += vn;
+        visible[i] += 1;
+    } else {
+        gm[i] = om;
+        gl[i] = ol;
+        gr0[i] = o0;
+        gr1[i] = o1;
+#pragma unroll
+        for (int b = 0; b < 12; ++b)
+            reinterpret_cast<float4*>(grads + (16 + 4 * (size_t)b) * n)[i] =
+                make_float4(shg[4 * b], shg[4 * b + 1], shg[4 * b + 2], shg[4 * b + 3]);
+        gop[i] = f[16];
+        vnorm[i] = vn;
+        visible[i] = 1;
+    }
+}
+
+}  // namespace rgs_dev
+
+// ---------------------------------------------------------------------------
+namespace rgs_launch {
+using namespace rgs_dev;
+
+static inline int blocks(long long n, int t) { return (int)((n + t - 1) / t); }
+
+void preprocess(const float* params, int n, int sh_degree, const DevCamera& cam, const SplatArrays& out,
+                unsigned long long* err_word, int* n_valid, cudaStream_t s) {
+    if (n <= 0) return;
+    ParamView P{params, n};
+    k_preprocess<<<blocks(n, 128), 128, 0, s>>>(P, sh_degree, cam, out, err_word, n_valid);
+}
+
+void splats_from_host(const void* splats, int n, const DevCamera& cam, const SplatArrays& out, int* n_valid,
+                      cudaStream_t s) {
+    if (n <= 0) return;
+    k_splats_from_host<<<blocks(n, 128), 128, 0, s>>>(reinterpret_cast<const HostSplat*>(splats), n, cam, out,
+                                                       n_valid);
+}
+
+void mark_all_slow(int n_pixels, uint32_t* slow_list, int* slow_count, cudaStream_t s) {
+    k_mark_all_slow<<<blocks(n_pixels, 256), 256, 0, s>>>(n_pixels, slow_list, slow_count);
+}
+
+static int persistent_blocks(int max_items) {
+    // Persistent grid: 148 SMs x 8 CTAs x 8 warps, capped by the item count.
+    const int warps = 148 * 8 * 8;
+    const int need = max_items < warps ? max_items : warps;
+    return (need + 7) / 8 > 0 ? (need + 7) / 8 : 1;
+}
+
+void blend_fp64_pixels(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges, const DevCamera& cam,
+                       double3 bg, int flow_mode, float* image, double* final_T, uint32_t* n_contrib,
+                       const uint32_t* slow_list, const int* slow_count, int max_pixels, cudaStream_t s) {
+    if (max_pixels <= 0) return;
+    k_blend_fp64<<<persistent_blocks(max_pixels), 256, 0, s>>>(sp, pair_vals, ranges, cam, bg, flow_mode, image,
+                                                               final_T, n_contrib, slow_list, slow_count);
+}
+
+void backward_fp64_pixels(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges,
+                          const DevCamera& cam, double3 bg, const double* final_T, const uint32_t* n_contrib,
+                          const float* dL_dimage, const uint32_t* slow_list, const int* slow_count, int max_pixels,
+                          double* screen_grads, cudaStream_t s) {
+    if (max_pixels <= 0) return;
+    k_backward_fp64<<<persistent_blocks(max_pixels), 256, 0, s>>>(sp, pair_vals, ranges, cam, bg, final_T, n_contrib,
+                                                                  dL_dimage, slow_list, slow_count, screen_grads);
+}
+
+void gaussian_backward(const float* params, int n, int sh_degree, const DevCamera& cam, const uint8_t* valid,
+                       const double* screen_grads, int accumulate, float* grads, float* vnorm, int32_t* visible,
+                       cudaStream_t s) {
+    if (n <= 0) return;
+    ParamView P{params, n};
+    k_gaussian_backward<<<blocks(n, 128), 128, 0, s>>>(P, sh_degree, cam, valid, screen_grads, accumulate, grads,
+                                                       vnorm, visible);
+}
+
+}  // namespace rgs_launch

@@ -1,0 +1,855 @@
+// C-ABI implementation (include/rgs_cuda.h): contexts, device scenes, the
+// forward / backward pipelines and records export.
+//
+// Forward pipeline per view (render_forward, rasterizer.cpp:308-318):
+//   K1 preprocess (FP64)  -> per-Gaussian splat records, tile rects, depth keys
+//   depth sort            -> splat order by (depth, index)       [stable radix sort]
+//   counts + scan         -> pair offsets in depth order
+//   duplicate-with-key    -> (tile, splat) pairs in depth order
+//   stable sort by tile   -> per-tile lists in (depth, index) order == bin_and_sort
+//   tile ranges           -> [begin, end) per tile
+//   K5 FP32 blend         -> image, final_T, n_contrib, slow-pixel list
+//   FP64 fix-up           -> slow pixels recomputed exactly
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <cub/cub.cuh>
+#include <string>
+#include <vector>
+
+#include "../../include/rgs_cuda.h"
+#include "rgs_internal.cuh"
+
+using namespace rgs_dev;
+
+namespace {
+
+struct CudaError {
+    cudaError_t e;
+    const char* what;
+};
+
+#define CK(x)                                                                   \
+    do {                                                                        \
+        cudaError_t _e = (x);                                                   \
+        if (_e != cudaSuccess) throw CudaError{_e, #x};                         \
+    } while (0)
+
+// Grow-only device buffer, stream-ordered allocation.
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void ensure(size_t need, cudaStream_t s) {
+        if (need <= bytes) return;
+        if (p) CK(cudaFreeAsync(p, s));
+        size_t b = std::max(need, bytes + bytes / 2);
+        b = (b + 255) & ~size_t(255);
+        CK(cudaMallocAsync(&p, b, s));
+        bytes = b;
+    }
+    void release(cudaStream_t s) {
+        if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <typename T>
+    T* as() const {
+        return reinterpret_cast<T*>(p);
+    }
+};
+
+struct DevStats {
+    unsigned long long err;
+    long long n_pairs;
+    int n_valid;
+    int slow_count;
+};
+
+__global__ void k_finish_counts(const uint32_t* offsets, const uint32_t* counts, int n, DevStats* st) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) st->n_pairs = n > 0 ? (long long)offsets[n - 1] + counts[n - 1] : 0;
+}
+
+int bits_for(long long v) {
+    int b = 1;
+    while ((1ll << b) < v) ++b;
+    return b;
+}
+
+// All per-view device state (one set per render in flight / per retained record).
+struct Frame {
+    // per Gaussian
+    DevBuf valid, tiles, mean2, conic_ab, color_depth, flow_radius, rect, conic_f, color_f, guard_f, src;
+    DevBuf dkey[2], dval[2], counts, offsets;
+    // pairs
+    DevBuf tkey[2], pval[2];
+    // tiles / pixels
+    DevBuf ranges, final_T, n_contrib, slow_list;
+    DevBuf stats;  // DevStats
+    DevBuf cub_tmp;
+    // results
+    int n = 0, n_valid = 0;
+    long long n_pairs = 0;
+    int width = 0, height = 0, tiles_x = 0, tiles_y = 0;
+    int pairs_sel = 0;  // which pval buffer holds the sorted values
+    bool have_src = false;
+    double bg[3] = {0, 0, 0};
+
+    SplatArrays arrays() const {
+        SplatArrays a;
+        a.valid = valid.as<uint8_t>();
+        a.tiles = tiles.as<uint32_t>();
+        a.mean2 = mean2.as<double2>();
+        a.conic_ab = conic_ab.as<double4>();
+        a.color_depth = color_depth.as<double4>();
+        a.flow_radius = flow_radius.as<double4>();
+        a.rect = rect.as<ushort4>();
+        a.conic_f = conic_f.as<float4>();
+        a.color_f = color_f.as<float4>();
+        a.guard_f = guard_f.as<float2>();
+        a.source_index = have_src ? src.as<int32_t>() : nullptr;
+        a.depth_key = dkey[0].as<unsigned long long>();
+        a.depth_val = dval[0].as<uint32_t>();
+        return a;
+    }
+    const uint32_t* pair_vals() const { return pval[pairs_sel].as<uint32_t>(); }
+    DevStats* dstats() const { return stats.as<DevStats>(); }
+
+    void ensure_gaussians(int cap, cudaStream_t s) {
+        size_t n1 = std::max(cap, 1);
+        valid.ensure(n1, s);
+        tiles.ensure(4 * n1, s);
+        mean2.ensure(16 * n1, s);
+        conic_ab.ensure(32 * n1, s);
+        color_depth.ensure(32 * n1, s);
+        flow_radius.ensure(32 * n1, s);
+        rect.ensure(8 * n1, s);
+        conic_f.ensure(16 * n1, s);
+        color_f.ensure(16 * n1, s);
+        guard_f.ensure(8 * n1, s);
+        for (int k = 0; k < 2; ++k) {
+            dkey[k].ensure(8 * n1, s);
+            dval[k].ensure(4 * n1, s);
+        }
+        counts.ensure(4 * n1, s);
+        offsets.ensure(4 * n1, s);
+        stats.ensure(sizeof(DevStats), s);
+    }
+    void ensure_pixels(size_t npix, int ntiles, cudaStream_t s) {
+        final_T.ensure(8 * std::max<size_t>(npix, 1), s);
+        n_contrib.ensure(4 * std::max<size_t>(npix, 1), s);
+        slow_list.ensure(4 * std::max<size_t>(npix, 1), s);
+        ranges.ensure(8 * (size_t)std::max(ntiles, 1), s);
+    }
+    void ensure_pairs(long long p, cudaStream_t s) {
+        size_t p1 = (size_t)std::max<long long>(p, 1);
+        for (int k = 0; k < 2; ++k) {
+            tkey[k].ensure(4 * p1, s);
+            pval[k].ensure(4 * p1, s);
+        }
+    }
+    void release(cudaStream_t s) {
+        DevBuf* all[] = {&valid, &tiles, &mean2, &conic_ab, &color_depth, &flow_radius, &rect, &conic_f,
+                         &color_f, &guard_f, &src, &dkey[0], &dkey[1], &dval[0], &dval[1], &counts,
+                         &offsets, &tkey[0], &tkey[1], &pval[0], &pval[1], &ranges, &final_T, &n_contrib,
+                         &slow_list, &stats, &cub_tmp};
+        for (DevBuf* b : all) b->release(s);
+    }
+};
+
+}  // namespace
+
+struct rgs_ctx {
+    int device = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;
+    std::string err;
+    int err_index = -1;
+    long long launches = 0;
+    Frame scratch;
+    DevBuf sgrad;     // N x 9 doubles (screen-space gradients)
+    DevBuf tmp_img;   // host-buffer staging
+    DevBuf tmp_splats, tmp_scan, tmp_ids;
+    DevStats* host_stats = nullptr;  // pinned
+};
+
+struct rgs_scene {
+    rgs_ctx* ctx = nullptr;
+    int n = 0;
+    int sh_degree = 0;
+    float* params = nullptr;
+};
+
+struct rgs_records {
+    rgs_ctx* ctx = nullptr;
+    Frame fb;
+    int retained = 0;
+    int n_slow = -1;
+};
+
+namespace {
+
+int set_err(rgs_ctx* ctx, int code, const std::string& msg) {
+    if (ctx) ctx->err = msg;
+    return code;
+}
+
+int cuda_fail(rgs_ctx* ctx, const CudaError& e) {
+    return set_err(ctx, RGS_E_CUDA, std::string("CUDA error: ") + cudaGetErrorString(e.e) + " at " + e.what);
+}
+
+// camera.hpp:19-24 with the reference's expression order.
+int validate_camera(rgs_ctx* ctx, const rgs_camera* c) {
+    if (!(c->fx > 0) || !(c->fy > 0)) return set_err(ctx, RGS_E_CAMERA, "camera: focal lengths must be positive");
+    const double* w = c->world_to_camera;
+    double mx = 0;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double s = w[i * 4 + 0] * w[j * 4 + 0];
+            s += w[i * 4 + 1] * w[j * 4 + 1];
+            s += w[i * 4 + 2] * w[j * 4 + 2];
+            double d = std::fabs(s - (i == j ? 1.0 : 0.0));
+            mx = (i == 0 && j == 0) ? d : ((mx < d) ? d : mx);
+        }
+    if (mx > 1e-6) return set_err(ctx, RGS_E_CAMERA, "camera: rotation block not orthogonal");
+    if (c->width <= 0 || c->height <= 0) return set_err(ctx, RGS_E_INVALID, "camera: empty image");
+    return RGS_OK;
+}
+
+DevCamera make_dev_camera(const rgs_camera* c) {
+    DevCamera d;
+    d.width = c->width;
+    d.height = c->height;
+    d.tiles_x = (c->width + kTile - 1) / kTile;
+    d.tiles_y = (c->height + kTile - 1) / kTile;
+    d.fx = c->fx;
+    d.fy = c->fy;
+    d.cx = c->cx;
+    d.cy = c->cy;
+    d.time = c->time;
+    const double* w = c->world_to_camera;
+    for (int i = 0; i < 3; ++i) {
+        for (int j = 0; j < 3; ++j) d.R[i * 3 + j] = w[i * 4 + j];
+        d.t[i] = w[i * 4 + 3];
+    }
+    // center = -R^T t, sequential sum (camera.hpp:17 under the Eigen subset).
+    for (int i = 0; i < 3; ++i) {
+        volatile double s = (-d.R[0 * 3 + i]) * d.t[0];
+        s = s + (-d.R[1 * 3 + i]) * d.t[1];
+        s = s + (-d.R[2 * 3 + i]) * d.t[2];
+        d.center[i] = s;
+    }
+    return d;
+}
+
+const char* rotor_msg(int code) {
+    return code == RGS_E_ZERO_ROTOR ? "normalize: zero rotor" : "normalize: result violates rotor invariants";
+}
+
+enum Source { kFromScene, kFromSplats };
+}  // namespace
+void rgs_gather_keys(const unsigned long long* keys, const uint32_t* ids, int n, unsigned long long* out,
+                     uint32_t* out_ids, cudaStream_t s);
+namespace {
+
+// Runs the forward pipeline into `f`.  image may be null (records only).
+int run_forward(rgs_ctx* ctx, Frame& f, Source src, const rgs_scene* scene, const void* dev_splats, int n_splats,
+                bool splats_monotone, const rgs_camera* cam, const double bg[3], unsigned flags, float* image,
+                bool flow_mode) {
+    cudaStream_t s = ctx->stream;
+    const DevCamera dc = make_dev_camera(cam);
+    const int n = src == kFromScene ? scene->n : n_splats;
+    const size_t npix = (size_t)cam->width * cam->height;
+    const int ntiles = dc.tiles_x * dc.tiles_y;
+    f.n = n;
+    f.width = cam->width;
+    f.height = cam->height;
+    f.tiles_x = dc.tiles_x;
+    f.tiles_y = dc.tiles_y;
+    for (int k = 0; k < 3; ++k) f.bg[k] = bg ? bg[k] : 0.0;
+    f.ensure_gaussians(n, s);
+    f.ensure_pixels(npix, ntiles, s);
+    if (src == kFromSplats) {
+        f.src.ensure(4 * (size_t)std::max(n, 1), s);
+        f.have_src = true;
+    }
+    DevStats init{kNoError, 0, 0, 0};
+    CK(cudaMemcpyAsync(f.dstats(), &init, sizeof init, cudaMemcpyHostToDevice, s));
+    SplatArrays sa = f.arrays();
+
+    // K1
+    if (src == kFromScene)
+        rgs_launch::preprocess(scene->params, n, scene->sh_degree, dc, sa, &f.dstats()->err, &f.dstats()->n_valid, s);
+    else
+        rgs_launch::splats_from_host(dev_splats, n, dc, sa, &f.dstats()->n_valid, s);
+    ctx->launches += 1;
+
+    // Depth order (stable; ties by index == source index for scenes).
+    cub::DoubleBuffer<unsigned long long> dk(f.dkey[0].as<unsigned long long>(), f.dkey[1].as<unsigned long long>());
+    cub::DoubleBuffer<uint32_t> dv(f.dval[0].as<uint32_t>(), f.dval[1].as<uint32_t>());
+    size_t need = 0;
+    if (src == kFromSplats && !splats_monotone) {
+        // Ties must break on source_index (rasterizer.cpp:70): stable pre-sort by it,
+        // then gather the depth keys in that order.
+        cub::DoubleBuffer<uint32_t> sk(f.counts.as<uint32_t>(), f.offsets.as<uint32_t>());
+        cub::DoubleBuffer<uint32_t> sv(f.dval[0].as<uint32_t>(), f.dval[1].as<uint32_t>());
+        rgs_launch::source_keys(f.src.as<int32_t>(), n, sk.Current(), sv.Current(), s);
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, need, sk, sv, n, 0, 32, s));
+        f.cub_tmp.ensure(need, s);
+        CK(cub::DeviceRadixSort::SortPairs(f.cub_tmp.p, need, sk, sv, n, 0, 32, s));
+        uint32_t* ids_in = sv.Current();
+        uint32_t* ids_out = sv.Alternate();
+        rgs_gather_keys(f.dkey[0].as<unsigned long long>(), ids_in, n, f.dkey[1].as<unsigned long long>(), ids_out,
+                        s);
+        ctx->launches += 2;
+        dk = cub::DoubleBuffer<unsigned long long>(f.dkey[1].as<unsigned long long>(),
+                                                   f.dkey[0].as<unsigned long long>());
+        dv = cub::DoubleBuffer<uint32_t>(ids_out, ids_in);
+    }
+    need = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, need, dk, dv, n, 0, 64, s));
+    size_t need_scan = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, need_scan, f.counts.as<uint32_t>(), f.offsets.as<uint32_t>(), n, s));
+    f.cub_tmp.ensure(std::max(need, need_scan), s);
+    if (n > 0) CK(cub::DeviceRadixSort::SortPairs(f.cub_tmp.p, need, dk, dv, n, 0, 64, s));
+    const uint32_t* sorted_ids = dv.Current();
+
+    rgs_launch::gather_counts(sorted_ids, f.tiles.as<uint32_t>(), n, f.counts.as<uint32_t>(), s);
+    if (n > 0)
+        CK(cub::DeviceScan::ExclusiveSum(f.cub_tmp.p, need_scan, f.counts.as<uint32_t>(), f.offsets.as<uint32_t>(), n,
+                                         s));
+    k_finish_counts<<<1, 32, 0, s>>>(f.offsets.as<uint32_t>(), f.counts.as<uint32_t>(), n, f.dstats());
+    ctx->launches += 2;
+    CK(cudaMemcpyAsync(ctx->host_stats, f.dstats(), sizeof(DevStats), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const DevStats st = *ctx->host_stats;
+    if (st.err != kNoError) {
+        const int code = (int)(st.err & 0xff);
+        ctx->err_index = (int)(st.err >> 8);
+        return set_err(ctx, code, rotor_msg(code));
+    }
+    f.n_valid = st.n_valid;
+    f.n_pairs = st.n_pairs;
+
+    // Duplicate-with-key + stable sort by tile id.
+    f.ensure_pairs(f.n_pairs, s);
+    rgs_launch::duplicate(sorted_ids, f.offsets.as<uint32_t>(), f.counts.as<uint32_t>(), n, f.rect.as<ushort4>(),
+                          dc.tiles_x, f.tkey[0].as<uint32_t>(), f.pval[0].as<uint32_t>(), s);
+    ctx->launches += 1;
+    cub::DoubleBuffer<uint32_t> tk(f.tkey[0].as<uint32_t>(), f.tkey[1].as<uint32_t>());
+    cub::DoubleBuffer<uint32_t> tv(f.pval[0].as<uint32_t>(), f.pval[1].as<uint32_t>());
+    const int tbits = bits_for(ntiles);
+    if (f.n_pairs > 0) {
+        need = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, need, tk, tv, (int)f.n_pairs, 0, tbits, s));
+        f.cub_tmp.ensure(need, s);
+        CK(cub::DeviceRadixSort::SortPairs(f.cub_tmp.p, need, tk, tv, (int)f.n_pairs, 0, tbits, s));
+    }
+    f.pairs_sel = tv.Current() == f.pval[0].as<uint32_t>() ? 0 : 1;
+    rgs_launch::tile_ranges(tk.Current(), f.n_pairs, ntiles, f.ranges.as<uint2>(), s);
+    ctx->launches += 1;
+
+    // Blend.
+    uint32_t* nc = flow_mode ? nullptr : f.n_contrib.as<uint32_t>();
+    double* fT = flow_mode ? nullptr : f.final_T.as<double>();
+    int* slow_count = &f.dstats()->slow_count;
+    if (flags & RGS_FLAG_BLEND_FP64) {
+        rgs_launch::mark_all_slow((int)npix, f.slow_list.as<uint32_t>(), slow_count, s);
+        ctx->launches += 1;
+    } else if (image || !flow_mode) {
+        float* img = image;
+        if (!img) {
+            ctx->tmp_img.ensure(npix * 3 * sizeof(float), s);
+            img = ctx->tmp_img.as<float>();
+        }
+        image = img;
+        rgs_launch::blend_fp32(sa, f.pair_vals(), f.ranges.as<uint2>(), dc,
+                               make_float3((float)f.bg[0], (float)f.bg[1], (float)f.bg[2]), flow_mode ? 1 : 0, img,
+                               fT, nc, f.slow_list.as<uint32_t>(), slow_count, s);
+        ctx->launches += 1;
+    }
+    if (!image) {
+        ctx->tmp_img.ensure(npix * 3 * sizeof(float), s);
+        image = ctx->tmp_img.as<float>();
+    }
+    rgs_launch::blend_fp64_pixels(sa, f.pair_vals(), f.ranges.as<uint2>(), dc,
+                                  make_double3(f.bg[0], f.bg[1], f.bg[2]), flow_mode ? 1 : 0, image, fT, nc,
+                                  f.slow_list.as<uint32_t>(), slow_count, (int)npix, s);
+    ctx->launches += 1;
+    CK(cudaGetLastError());
+    return RGS_OK;
+}
+
+template <typename F>
+int guarded(rgs_ctx* ctx, F&& fn) {
+    if (!ctx) return RGS_E_INVALID;
+    try {
+        CK(cudaSetDevice(ctx->device));
+        ctx->err.clear();
+        return fn();
+    } catch (const CudaError& e) {
+        return cuda_fail(ctx, e);
+    } catch (const std::exception& e) {
+        return set_err(ctx, RGS_E_INVALID, e.what());
+    }
+}
+
+}  // namespace
+
+// Gather kernel used by the rasterize_forward source-index pre-sort.
+__global__ void k_gather_keys(const unsigned long long* keys, const uint32_t* ids, int n, unsigned long long* out,
+                              uint32_t* out_ids) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) {
+        out[k] = keys[ids[k]];
+        out_ids[k] = ids[k];
+    }
+}
+void rgs_gather_keys(const unsigned long long* keys, const uint32_t* ids, int n, unsigned long long* out,
+                     uint32_t* out_ids, cudaStream_t s) {
+    if (n > 0) k_gather_keys<<<(n + 255) / 256, 256, 0, s>>>(keys, ids, n, out, out_ids);
+}
+
+extern "C" {
+
+int rgs_abi_version(void) { return RGS_ABI_VERSION; }
+
+int rgs_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int rgs_ctx_create(int device, rgs_ctx** out) {
+    if (!out) return RGS_E_INVALID;
+    *out = nullptr;
+    int n = rgs_device_count();
+    if (n <= 0 || device < 0 || device >= n) return RGS_E_NO_DEVICE;
+    rgs_ctx* c = new rgs_ctx;
+    c->device = device;
+    try {
+        CK(cudaSetDevice(device));
+        CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+        CK(cudaMallocHost(&c->host_stats, sizeof(DevStats)));
+        // Keep freed blocks in the pool: frames re-grow without hitting the driver.
+        cudaMemPool_t pool;
+        CK(cudaDeviceGetDefaultMemPool(&pool, device));
+        unsigned long long thresh = ~0ull;
+        CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+    } catch (const CudaError& e) {
+        delete c;
+        return RGS_E_CUDA;
+    }
+    c->stream = c->own_stream;
+    *out = c;
+    return RGS_OK;
+}
+
+void rgs_ctx_destroy(rgs_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    c->scratch.release(c->stream);
+    c->sgrad.release(c->stream);
+    c->tmp_img.release(c->stream);
+    c->tmp_splats.release(c->stream);
+    c->tmp_scan.release(c->stream);
+    c->tmp_ids.release(c->stream);
+    cudaStreamSynchronize(c->stream);
+    if (c->host_stats) cudaFreeHost(c->host_stats);
+    if (c->own_stream) cudaStreamDestroy(c->own_stream);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    delete c;
+}
+
+int rgs_ctx_set_stream(rgs_ctx* c, void* stream) {
+    if (!c) return RGS_E_INVALID;
+    c->stream = stream ? reinterpret_cast<cudaStream_t>(stream) : c->own_stream;
+    return RGS_OK;
+}
+void* rgs_ctx_stream(rgs_ctx* c) { return c ? (void*)c->stream : nullptr; }
+const char* rgs_ctx_last_error(const rgs_ctx* c) { return c ? c->err.c_str() : "null context"; }
+int rgs_ctx_error_index(const rgs_ctx* c) { return c ? c->err_index : -1; }
+long long rgs_ctx_kernel_launches(const rgs_ctx* c) { return c ? c->launches : 0; }
+int rgs_ctx_synchronize(rgs_ctx* c) {
+    return guarded(c, [&] {
+        CK(cudaStreamSynchronize(c->stream));
+        return RGS_OK;
+    });
+}
+
+int rgs_camera_validate(rgs_ctx* c, const rgs_camera* cam) {
+    if (!cam) return RGS_E_INVALID;
+    return validate_camera(c, cam);
+}
+
+// ------------------------------------------------------------------ scene
+int rgs_scene_create(rgs_ctx* c, int n, int sh_degree, rgs_scene** out) {
+    if (!out || n < 0) return RGS_E_INVALID;
+    return guarded(c, [&] {
+        rgs_scene* s = new rgs_scene;
+        s->ctx = c;
+        s->n = n;
+        s->sh_degree = sh_degree;
+        CK(cudaMalloc(&s->params, sizeof(float) * 65 * (size_t)std::max(n, 1)));
+        CK(cudaMemsetAsync(s->params, 0, sizeof(float) * 65 * (size_t)std::max(n, 1), c->stream));
+        *out = s;
+        return RGS_OK;
+    });
+}
+
+void rgs_scene_destroy(rgs_scene* s) {
+    if (!s) return;
+    cudaSetDevice(s->ctx->device);
+    cudaFree(s->params);
+    delete s;
+}
+int rgs_scene_size(const rgs_scene* s) { return s ? s->n : 0; }
+int rgs_scene_set_sh_degree(rgs_scene* s, int d) {
+    if (!s) return RGS_E_INVALID;
+    s->sh_degree = d;
+    return RGS_OK;
+}
+float* rgs_scene_params(rgs_scene* s) { return s ? s->params : nullptr; }
+
+int rgs_scene_upload_f32(rgs_ctx* c, rgs_scene* s, const float* mean, const float* ls, const float* rot,
+                         const float* op, const float* sh) {
+    if (!s || !mean || !ls || !rot || !op || !sh) return RGS_E_INVALID;
+    return guarded(c, [&] {
+        const size_t n = (size_t)s->n;
+        if (n == 0) return RGS_OK;
+        DevBuf tmp;
+        tmp.ensure(sizeof(float) * 65 * n, c->stream);
+        float* t = tmp.as<float>();
+        CK(cudaMemcpyAsync(t, mean, 16 * n, cudaMemcpyDefault, c->stream));
+        CK(cudaMemcpyAsync(t + 4 * n, ls, 16 * n, cudaMemcpyDefault, c->stream));
+        CK(cudaMemcpyAsync(t + 8 * n, rot, 32 * n, cudaMemcpyDefault, c->stream));
+        CK(cudaMemcpyAsync(t + 16 * n, op, 4 * n, cudaMemcpyDefault, c->stream));
+        CK(cudaMemcpyAsync(t + 17 * n, sh, 192 * n, cudaMemcpyDefault, c->stream));
+        rgs_launch::scene_pack(t, t + 4 * n, t + 8 * n, t + 16 * n, t + 17 * n, (int)n, s->params, c->stream);
+        c->launches += 1;
+        tmp.release(c->stream);
+        CK(cudaStreamSynchronize(c->stream));
+        return RGS_OK;
+    });
+}
+
+int rgs_scene_upload_f64(rgs_ctx* c, rgs_scene* s, const double* mean, const double* ls, const double* rot,
+                         const double* op, const double* sh, long long* n_inexact) {
+    if (!s || !mean || !ls || !rot || !op || !sh) return RGS_E_INVALID;
+    const size_t n = (size_t)s->n;
+    std::vector<float> f(65 * std::max<size_t>(n, 1));
+    long long inexact = 0;
+    auto conv = [&](const double* src, size_t cnt, float* dst) {
+        for (size_t i = 0; i < cnt; ++i) {
+            dst[i] = (float)src[i];
+            if ((double)dst[i] != src[i] && !(std::isnan(src[i]))) ++inexact;
+        }
+    };
+    conv(mean, 4 * n, f.data());
+    conv(ls, 4 * n, f.data() + 4 * n);
+    conv(rot, 8 * n, f.data() + 8 * n);
+    conv(op, n, f.data() + 16 * n);
+    conv(sh, 48 * n, f.data() + 17 * n);
+    if (n_inexact) *n_inexact = inexact;
+    return rgs_scene_upload_f32(c, s, f.data(), f.data() + 4 * n, f.data() + 8 * n, f.data() + 16 * n,
+                                f.data() + 17 * n);
+}
+
+int rgs_scene_download_f64(rgs_ctx* c, const rgs_scene* s, double* mean, double* ls, double* rot, double* op,
+                           double* sh) {
+    if (!s) return RGS_E_INVALID;
+    return guarded(c, [&] {
+        const size_t n = (size_t)s->n;
+        if (n == 0) return RGS_OK;
+        DevBuf tmp;
+        tmp.ensure(sizeof(double) * 65 * n, c->stream);
+        double* t = tmp.as<double>();
+        rgs_launch::scene_unpack(s->params, (int)n, t, t + 4 * n, t + 8 * n, t + 16 * n, t + 17 * n, c->stream);
+        c->launches += 1;
+        if (mean) CK(cudaMemcpyAsync(mean, t, 32 * n, cudaMemcpyDeviceToHost, c->stream));
+        if (ls) CK(cudaMemcpyAsync(ls, t + 4 * n, 32 * n, cudaMemcpyDeviceToHost, c->stream));
+        if (rot) CK(cudaMemcpyAsync(rot, t + 8 * n, 64 * n, cudaMemcpyDeviceToHost, c->stream));
+        if (op) CK(cudaMemcpyAsync(op, t + 16 * n, 8 * n, cudaMemcpyDeviceToHost, c->stream));
+        if (sh) CK(cudaMemcpyAsync(sh, t + 17 * n, 384 * n, cudaMemcpyDeviceToHost, c->stream));
+        tmp.release(c->stream);
+        CK(cudaStreamSynchronize(c->stream));
+        return RGS_OK;
+    });
+}
+
+// ------------------------------------------------------------------ forward
+static int forward_common(rgs_ctx* c, Source src, const rgs_scene* scene, const rgs_splat* splats, int n_splats,
+                          const rgs_camera* cam, const double bg[3], unsigned flags, float* image,
+                          rgs_records** records, bool flow) {
+    if (!cam) return RGS_E_INVALID;
+    return guarded(c, [&]() -> int {
+        int rc = validate_camera(c, cam);
+        if (rc) return rc;
+        c->err_index = -1;
+        const size_t npix = (size_t)cam->width * cam->height;
+        const size_t chans = flow ? 2 : 3;
+        const bool host_io = (flags & RGS_FLAG_HOST_BUFFERS) != 0;
+        float* dimg = image;
+        if (host_io && image) {
+            c->tmp_img.ensure(npix * 3 * sizeof(float), c->stream);
+            dimg = c->tmp_img.as<float>();
+        }
+        const void* dsp = nullptr;
+        bool monotone = true;
+        if (src == kFromSplats) {
+            c->tmp_splats.ensure(sizeof(rgs_splat) * (size_t)std::max(n_splats, 1), c->stream);
+            if (n_splats > 0)
+                CK(cudaMemcpyAsync(c->tmp_splats.p, splats, sizeof(rgs_splat) * (size_t)n_splats,
+                                   host_io ? cudaMemcpyHostToDevice : cudaMemcpyDefault, c->stream));
+            dsp = c->tmp_splats.p;
+            if (host_io || true) {
+                // monotone source indices -> index order already is the tie-break order
+                std::vector<rgs_splat> h;
+                const rgs_splat* hp = splats;
+                cudaPointerAttributes attr;
+                if (cudaPointerGetAttributes(&attr, splats) == cudaSuccess && attr.type == cudaMemoryTypeDevice) {
+                    h.resize(n_splats);
+                    CK(cudaMemcpy(h.data(), splats, sizeof(rgs_splat) * n_splats, cudaMemcpyDeviceToHost));
+                    hp = h.data();
+                }
+                cudaGetLastError();
+                for (int i = 1; i < n_splats; ++i)
+                    if (hp[i].source_index <= hp[i - 1].source_index) monotone = false;
+            }
+        }
+        rgs_records* rec = nullptr;
+        Frame* f = &c->scratch;
+        if (records) {
+            rec = new rgs_records;
+            rec->ctx = c;
+            rec->retained = (flags & RGS_FLAG_RETAIN_RECORDS) ? 1 : 0;
+            f = &rec->fb;
+        }
+        rc = run_forward(c, *f, src, scene, dsp, n_splats, monotone, cam, bg, flags, dimg, flow);
+        if (rc) {
+            if (rec) {
+                rec->fb.release(c->stream);
+                delete rec;
+            }
+            return rc;
+        }
+        if (host_io && image) {
+            CK(cudaMemcpyAsync(image, dimg, npix * chans * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+        }
+        if (records) *records = rec;
+        return RGS_OK;
+    });
+}
+
+int rgs_render_forward(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* cam, const double bg[3], unsigned flags,
+                       float* image, rgs_records** records) {
+    if (!scene) return RGS_E_INVALID;
+    return forward_common(c, kFromScene, scene, nullptr, 0, cam, bg, flags, image, records, false);
+}
+
+int rgs_rasterize_forward(rgs_ctx* c, const rgs_splat* splats, int n_splats, const rgs_camera* cam,
+                          const double bg[3], unsigned flags, float* image, rgs_records** records) {
+    if (n_splats < 0 || (n_splats > 0 && !splats)) return RGS_E_INVALID;
+    return forward_common(c, kFromSplats, nullptr, splats, n_splats, cam, bg, flags, image, records, false);
+}
+
+int rgs_render_flow(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* cam, unsigned flags, float* flow) {
+    if (!scene || !flow) return RGS_E_INVALID;
+    const double zero[3] = {0, 0, 0};
+    return forward_common(c, kFromScene, scene, nullptr, 0, cam, zero, flags & ~RGS_FLAG_RETAIN_RECORDS, flow, nullptr,
+                          true);
+}
+
+int rgs_render_views(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* cams, int n_views, const double bg[3],
+                     unsigned flags, float* images) {
+    if (!scene || !cams || n_views < 0 || !images) return RGS_E_INVALID;
+    for (int v = 0; v < n_views; ++v)
+        if (cams[v].width != cams[0].width || cams[v].height != cams[0].height) return RGS_E_INVALID;
+    const size_t per = (size_t)cams[0].width * cams[0].height * 3;
+    for (int v = 0; v < n_views; ++v) {
+        int rc = forward_common(c, kFromScene, scene, nullptr, 0, &cams[v], bg, flags & ~RGS_FLAG_HOST_BUFFERS,
+                                images + per * v, nullptr, false);
+        if (rc) return rc;
+    }
+    return RGS_OK;
+}
+
+int rgs_render_views_host(rgs_ctx* c, int n, int sh_degree, const float* mean, const float* ls, const float* rot,
+                          const float* op, const float* sh, const rgs_camera* cams, int n_views, const double bg[3],
+                          float* images_host) {
+    if (!cams || n_views < 0 || !images_host) return RGS_E_INVALID;
+    rgs_scene* scene = nullptr;
+    int rc = rgs_scene_create(c, n, sh_degree, &scene);
+    if (rc) return rc;
+    rc = rgs_scene_upload_f32(c, scene, mean, ls, rot, op, sh);
+    if (rc) {
+        rgs_scene_destroy(scene);
+        return rc;
+    }
+    rc = guarded(c, [&]() -> int {
+        const size_t per = (size_t)cams[0].width * cams[0].height * 3;
+        DevBuf img[2];
+        cudaEvent_t rendered[2], copied[2];
+        for (int k = 0; k < 2; ++k) {
+            img[k].ensure(per * sizeof(float), c->stream);
+            CK(cudaEventCreateWithFlags(&rendered[k], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&copied[k], cudaEventDisableTiming));
+            CK(cudaEventRecord(copied[k], c->copy_stream));
+        }
+        int r = RGS_OK;
+        for (int v = 0; v < n_views && r == RGS_OK; ++v) {
+            const int k = v & 1;
+            CK(cudaStreamWaitEvent(c->stream, copied[k], 0));
+            r = forward_common(c, kFromScene, scene, nullptr, 0, &cams[v], bg, 0, img[k].as<float>(), nullptr,
+                               false);
+            if (r) break;
+            CK(cudaEventRecord(rendered[k], c->stream));
+            CK(cudaStreamWaitEvent(c->copy_stream, rendered[k], 0));
+            CK(cudaMemcpyAsync(images_host + per * v, img[k].p, per * sizeof(float), cudaMemcpyDeviceToHost,
+                               c->copy_stream));
+            CK(cudaEventRecord(copied[k], c->copy_stream));
+        }
+        CK(cudaStreamSynchronize(c->copy_stream));
+        CK(cudaStreamSynchronize(c->stream));
+        for (int k = 0; k < 2; ++k) {
+            img[k].release(c->stream);
+            cudaEventDestroy(rendered[k]);
+            cudaEventDestroy(copied[k]);
+        }
+        return r;
+    });
+    rgs_scene_destroy(scene);
+    return rc;
+}
+
+// ------------------------------------------------------------------ records
+void rgs_records_destroy(rgs_records* r) {
+    if (!r) return;
+    cudaSetDevice(r->ctx->device);
+    r->fb.release(r->ctx->stream);
+    delete r;
+}
+
+int rgs_records_info_get(const rgs_records* r, rgs_records_info* info) {
+    if (!r || !info) return RGS_E_INVALID;
+    rgs_ctx* c = r->ctx;
+    return guarded(c, [&] {
+        DevStats st;
+        CK(cudaMemcpyAsync(c->host_stats, r->fb.dstats(), sizeof st, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        st = *c->host_stats;
+        info->n_splats = r->fb.n_valid;
+        info->tiles_x = r->fb.tiles_x;
+        info->tiles_y = r->fb.tiles_y;
+        info->retained = r->retained;
+        info->n_pairs = r->fb.n_pairs;
+        info->n_slow_pixels = st.slow_count;
+        info->width = r->fb.width;
+        info->height = r->fb.height;
+        return RGS_OK;
+    });
+}
+
+int rgs_records_export(rgs_ctx* c, const rgs_records* r, rgs_splat* splats, long long* tile_offsets, int32_t* tile_ids,
+                       double* final_T, int32_t* n_contrib) {
+    if (!r) return RGS_E_INVALID;
+    return guarded(c, [&] {
+        const Frame& f = r->fb;
+        cudaStream_t s = c->stream;
+        const int n = f.n;
+        const size_t npix = (size_t)f.width * f.height;
+        const int ntiles = f.tiles_x * f.tiles_y;
+        // compacted index of each valid splat (rasterizer.cpp:206-210)
+        c->tmp_scan.ensure(4 * (size_t)std::max(n, 1) * 2, s);
+        uint32_t* v32 = c->tmp_scan.as<uint32_t>();
+        uint32_t* scan = v32 + std::max(n, 1);
+        rgs_launch::valid_to_u32(f.valid.as<uint8_t>(), n, v32, s);
+        size_t need = 0;
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, need, v32, scan, n, s));
+        DevBuf tmp;
+        tmp.ensure(std::max<size_t>(need, 16), s);
+        if (n > 0) CK(cub::DeviceScan::ExclusiveSum(tmp.p, need, v32, scan, n, s));
+        c->launches += 1;
+        if (splats && f.n_valid > 0) {
+            c->tmp_ids.ensure(4 * (size_t)f.n_valid, s);
+            rgs_launch::compact_index(f.valid.as<uint8_t>(), scan, n, c->tmp_ids.as<uint32_t>(), s);
+            DevBuf out;
+            out.ensure(sizeof(rgs_splat) * (size_t)f.n_valid, s);
+            rgs_launch::export_splats(f.arrays(), c->tmp_ids.as<uint32_t>(), f.n_valid, out.p, s);
+            c->launches += 2;
+            CK(cudaMemcpyAsync(splats, out.p, sizeof(rgs_splat) * (size_t)f.n_valid, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            out.release(s);
+        }
+        if (tile_offsets) {
+            std::vector<uint2> rg(ntiles);
+            CK(cudaMemcpyAsync(rg.data(), f.ranges.p, sizeof(uint2) * ntiles, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            long long acc = 0;
+            for (int t = 0; t < ntiles; ++t) {
+                tile_offsets[t] = acc;
+                acc += (long long)rg[t].y - (long long)rg[t].x;
+            }
+            tile_offsets[ntiles] = acc;
+        }
+        if (tile_ids && f.n_pairs > 0) {
+            DevBuf out;
+            out.ensure(4 * (size_t)f.n_pairs, s);
+            rgs_launch::map_ids(f.pair_vals(), f.n_pairs, scan, out.as<int32_t>(), s);
+            c->launches += 1;
+            CK(cudaMemcpyAsync(tile_ids, out.p, 4 * (size_t)f.n_pairs, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            out.release(s);
+        }
+        if (final_T) CK(cudaMemcpyAsync(final_T, f.final_T.p, 8 * npix, cudaMemcpyDeviceToHost, s));
+        if (n_contrib) CK(cudaMemcpyAsync(n_contrib, f.n_contrib.p, 4 * npix, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (n_contrib)
+            for (size_t i = 0; i < npix; ++i) n_contrib[i] &= 0x7fffffff;
+        tmp.release(s);
+        return RGS_OK;
+    });
+}
+
+// ------------------------------------------------------------------ backward
+int rgs_render_backward(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* cam, const rgs_records* r,
+                        const float* dL_dimage, unsigned flags, float* grads, float* vnorm, int32_t* visible) {
+    if (!scene || !cam || !r || !dL_dimage || !grads || !vnorm || !visible) return RGS_E_INVALID;
+    if (!r->retained)
+        return set_err(c, RGS_E_MISSING_RECORDS, "rasterize_backward: forward pass did not retain records");
+    return guarded(c, [&]() -> int {
+        const Frame& f = r->fb;
+        if (cam->width != f.width || cam->height != f.height || scene->n != f.n)
+            return set_err(c, RGS_E_INVALID, "render_backward: camera/scene does not match the records");
+        cudaStream_t s = c->stream;
+        const DevCamera dc = make_dev_camera(cam);
+        const int n = scene->n;
+        c->sgrad.ensure(sizeof(double) * 9 * (size_t)std::max(n, 1), s);
+        CK(cudaMemsetAsync(c->sgrad.p, 0, sizeof(double) * 9 * (size_t)std::max(n, 1), s));
+        SplatArrays sa = f.arrays();
+        const float3 bgf = make_float3((float)f.bg[0], (float)f.bg[1], (float)f.bg[2]);
+        rgs_launch::backward_fp32(sa, f.pair_vals(), f.ranges.as<uint2>(), dc, bgf, f.final_T.as<double>(),
+                                  f.n_contrib.as<uint32_t>(), dL_dimage, c->sgrad.as<double>(), s);
+        rgs_launch::backward_fp64_pixels(sa, f.pair_vals(), f.ranges.as<uint2>(), dc,
+                                         make_double3(f.bg[0], f.bg[1], f.bg[2]), f.final_T.as<double>(),
+                                         f.n_contrib.as<uint32_t>(), dL_dimage, f.slow_list.as<uint32_t>(),
+                                         &f.dstats()->slow_count, (int)((size_t)f.width * f.height),
+                                         c->sgrad.as<double>(), s);
+        rgs_launch::gaussian_backward(scene->params, n, scene->sh_degree, dc, f.valid.as<uint8_t>(),
+                                      c->sgrad.as<double>(), (flags & RGS_FLAG_ACCUMULATE) ? 1 : 0, grads, vnorm,
+                                      visible, s);
+        c->launches += 3;
+        CK(cudaGetLastError());
+        return RGS_OK;
+    });
+}
+
+}  // extern "C"

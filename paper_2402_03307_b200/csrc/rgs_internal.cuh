@@ -1,0 +1,117 @@
+// Internal declarations shared by the device translation units and the C-ABI host code.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rgs_dev {
+
+// rasterizer.hpp:13-18, gaussian.hpp:57-59
+constexpr int kTile = 16;
+constexpr int kTilePixels = kTile * kTile;
+constexpr double kNearPlane = 0.2;
+constexpr double kAlphaClamp = 0.99;
+constexpr double kMinAlpha = 1.0 / 255.0;
+constexpr double kStopT = 1e-4;
+constexpr double kCovDilation = 0.3;
+constexpr double kCov3Eps = 1e-9;
+constexpr double kTemporalFloor = 1e-12;
+constexpr double kVisibility = 16;
+constexpr double kEpsBranch = 1e-12;
+
+// Camera in the form the kernels use (camera.hpp:11-27); center = -R^T t is
+// computed on the host with the reference's expression order.
+struct DevCamera {
+    int width, height, tiles_x, tiles_y;
+    double fx, fy, cx, cy, time;
+    double R[9];  // row-major rotation block
+    double t[3];
+    double center[3];
+};
+
+// Offsets (in floats) of the SoA parameter blocks, see rgs_scene_params().
+struct ParamView {
+    const float* base;
+    int n;
+    __host__ __device__ const float4* mean() const { return reinterpret_cast<const float4*>(base); }
+    __host__ __device__ const float4* ls() const { return reinterpret_cast<const float4*>(base + 4 * (size_t)n); }
+    __host__ __device__ const float4* rot0() const { return reinterpret_cast<const float4*>(base + 8 * (size_t)n); }
+    __host__ __device__ const float4* rot1() const { return reinterpret_cast<const float4*>(base + 12 * (size_t)n); }
+    __host__ __device__ const float4* sh(int m) const {
+        return reinterpret_cast<const float4*>(base + (16 + 4 * (size_t)m) * (size_t)n);
+    }
+    __host__ __device__ const float* opacity() const { return base + 64 * (size_t)n; }
+};
+
+// Per-Gaussian splat records written by the preprocess kernel (dense, indexed by
+// Gaussian / input-splat index; `valid` marks the ones that produced a splat).
+struct SplatArrays {
+    uint8_t* valid;
+    uint32_t* tiles;         // number of tiles in the rectangle (0 if empty)
+    double2* mean2;          // FP64 screen mean
+    double4* conic_ab;       // (ca, cb, cc, alpha_base) FP64
+    double4* color_depth;    // (r, g, b, depth) FP64
+    double4* flow_radius;    // (flow_x, flow_y, radius, 0)
+    ushort4* rect;           // tile rectangle (x0, x1, y0, y1), inclusive
+    float4* conic_f;         // (ca, cb, cc, alpha_base) FP32
+    float4* color_f;         // (r, g, b, p_alpha) FP32; p_alpha = log(1/(255 ab))
+    float2* guard_f;         // (c_s, p_clamp): error-bound slope and clamp-gate power
+    int32_t* source_index;   // only for rasterize_forward (else NULL -> index)
+    unsigned long long* depth_key;  // sort key: depth bits, ~0 for invalid
+    uint32_t* depth_val;            // Gaussian index
+};
+
+// Error word: (index << 8) | code, minimum wins (lowest failing index).
+constexpr unsigned long long kNoError = ~0ull;
+
+// Guard-band constants for the FP32 blend (DESIGN.md §"FP32 blend with FP64 re-decision").
+constexpr float kGuardFloor = 1e-6f;
+
+// Packed per-pixel state written by the forward: bit 31 = slow (FP64) pixel.
+constexpr uint32_t kSlowBit = 0x80000000u;
+
+}  // namespace rgs_dev
+
+// ---------------------------------------------------------------------------
+// Kernel launchers (defined in k_fp64.cu / k_fp32.cu).
+namespace rgs_launch {
+using namespace rgs_dev;
+
+void preprocess(const float* params, int n, int sh_degree, const DevCamera& cam, const SplatArrays& out,
+                unsigned long long* err_word, int* n_valid, cudaStream_t s);
+void splats_from_host(const void* splats, int n, const DevCamera& cam, const SplatArrays& out,
+                      int* n_valid, cudaStream_t s);
+void gather_counts(const uint32_t* sorted_ids, const uint32_t* tiles, int n, uint32_t* counts,
+                   cudaStream_t s);
+void duplicate(const uint32_t* sorted_ids, const uint32_t* offsets, const uint32_t* counts, int n,
+               const ushort4* rect, int tiles_x, uint32_t* tile_keys, uint32_t* pair_vals, cudaStream_t s);
+void tile_ranges(const uint32_t* keys, long long n_pairs, int n_tiles, uint2* ranges, cudaStream_t s);
+void blend_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges, const DevCamera& cam,
+                float3 bg, int flow_mode, float* image, double* final_T, uint32_t* n_contrib,
+                uint32_t* slow_list, int* slow_count, cudaStream_t s);
+void mark_all_slow(int n_pixels, uint32_t* slow_list, int* slow_count, cudaStream_t s);
+void blend_fp64_pixels(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges,
+                       const DevCamera& cam, double3 bg, int flow_mode, float* image, double* final_T,
+                       uint32_t* n_contrib, const uint32_t* slow_list, const int* slow_count,
+                       int max_pixels, cudaStream_t s);
+void backward_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges,
+                   const DevCamera& cam, float3 bg, const double* final_T, const uint32_t* n_contrib,
+                   const float* dL_dimage, double* screen_grads, cudaStream_t s);
+void backward_fp64_pixels(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges,
+                          const DevCamera& cam, double3 bg, const double* final_T, const uint32_t* n_contrib,
+                          const float* dL_dimage, const uint32_t* slow_list, const int* slow_count,
+                          int max_pixels, double* screen_grads, cudaStream_t s);
+void gaussian_backward(const float* params, int n, int sh_degree, const DevCamera& cam, const uint8_t* valid,
+                       const double* screen_grads, int accumulate, float* grads, float* vnorm,
+                       int32_t* visible, cudaStream_t s);
+void export_splats(const SplatArrays& sp, const uint32_t* compact_ids, int n_valid, void* out,
+                   cudaStream_t s);
+void compact_index(const uint8_t* valid, const uint32_t* scan, int n, uint32_t* compact_ids, cudaStream_t s);
+void map_ids(const uint32_t* pair_vals, long long n_pairs, const uint32_t* scan, int32_t* out, cudaStream_t s);
+void scene_pack(const float* mean, const float* ls, const float* rot, const float* op, const float* sh,
+                int n, float* params, cudaStream_t s);
+void scene_unpack(const float* params, int n, double* mean, double* ls, double* rot, double* op, double* sh,
+                  cudaStream_t s);
+void source_keys(const int32_t* src, int n, uint32_t* keys, uint32_t* vals, cudaStream_t s);
+void valid_to_u32(const uint8_t* valid, int n, uint32_t* out, cudaStream_t s);
+}  // namespace rgs_launch

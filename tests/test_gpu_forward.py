@@ -1,0 +1,147 @@
+"""GPU forward parity against the CPU oracle (sm_100a kernels through the C-ABI).
+
+Bar (BASELINE.json north_star): splat records and per-tile lists / sort order
+bit-exact; image within 1e-4 max abs per channel; final_T / n_contrib consistent.
+"""
+import numpy as np
+import pytest
+
+from paper_2402_03307_b200 import rgs, scenes
+from parity import splat_mismatch
+
+pytestmark = pytest.mark.gpu
+
+
+def _compare_forward(ctx, orc, store, cam, bg=(0.0, 0.0, 0.0), threads=8, fp64=False):
+    ref_img, ref = orc.render_forward(store, cam, bg, threads=threads, retain=True)
+    out = rgs.render_forward(store, cam, rgs.RenderOptions(background=bg, retain_records=True, blend_fp64=fp64),
+                             ctx=ctx)
+    rec = out.records
+    mm = splat_mismatch(rec.splats, ref.splats)
+    assert mm == {}, f"splat records differ: {mm}"
+    assert np.array_equal(rec.tile_offsets, ref.tile_offsets), "tile list lengths differ"
+    assert np.array_equal(rec.tile_ids, ref.tile_ids), "tile lists / sort order differ"
+    err = np.abs(out.image.astype(np.float64) - ref_img).max() if ref_img.size else 0.0
+    nc_diff = int((rec.n_contrib != ref.n_contrib).sum())
+    return err, nc_diff, rec, ref, out
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_random_scenes_small(ctx, orc, seed):
+    store = scenes.random_scene(60, sh_degree=seed % 4, seed=seed)
+    cam = scenes.bench_camera(64 + 7 * seed, 64, time=0.3, pose=scenes.yaw_pose(3.0 * seed, (0.05, -0.02, 0.1)))
+    cam.fx = cam.fy = 64.0
+    err, ncd, rec, ref, out = _compare_forward(ctx, orc, store, cam, bg=(0.1, 0.2, 0.3))
+    assert err <= 1e-4
+    assert ncd == 0
+
+
+def test_c1_full_frame(ctx, orc):
+    """Config C1: 50K Gaussians, SH3, 800x800, t=0.5 (yawed pose exercises the FP64 path)."""
+    store = scenes.synthetic_scene(50_000, 800, 800, seed=1)
+    for pose in (None, scenes.yaw_pose(7.0, (0.05, -0.02, 0.1))):
+        cam = scenes.bench_camera(800, 800, 0.5, pose)
+        err, ncd, rec, ref, out = _compare_forward(ctx, orc, store, cam)
+        assert err <= 1e-4, err
+        assert ncd == 0
+        print(f"C1 pose={'yaw' if pose is not None else 'id'}: splats={len(ref.splats)} pairs={len(ref.tile_ids)}"
+              f" max_err={err:.3e} slow_pixels={rec.n_slow_pixels}")
+
+
+def test_c2_frame(ctx, orc):
+    """Config C2 shape: 300K Gaussians at 1352x1014, two timestamps of the sweep."""
+    store = scenes.synthetic_scene(300_000, 1352, 1014, seed=2)
+    for t in (0.0, 150 / 299):
+        cam = scenes.bench_camera(1352, 1014, t, scenes.yaw_pose(7.0, (0.05, -0.02, 0.1)))
+        err, ncd, rec, ref, out = _compare_forward(ctx, orc, store, cam, threads=16)
+        assert err <= 1e-4, err
+        assert ncd == 0
+        print(f"C2 t={t:.3f}: splats={len(ref.splats)} pairs={len(ref.tile_ids)} max_err={err:.3e}"
+              f" slow_pixels={rec.n_slow_pixels}")
+
+
+def test_fp64_mode_matches_oracle_tightly(ctx, orc):
+    store = scenes.random_scene(40, sh_degree=2, seed=11)
+    cam = scenes.bench_camera(64, 48, 0.4)
+    cam.fx = cam.fy = 64.0
+    err, ncd, rec, ref, out = _compare_forward(ctx, orc, store, cam, bg=(0.3, 0.1, 0.2), fp64=True)
+    assert err <= 1e-6  # float32 output rounding only
+    assert ncd == 0
+    assert np.abs(rec.final_T - ref.final_T).max() <= 1e-12
+
+
+def test_final_T_and_contrib(ctx, orc):
+    store = scenes.random_scene(80, sh_degree=1, seed=5)
+    cam = scenes.bench_camera(96, 80, 0.6)
+    cam.fx = cam.fy = 80.0
+    err, ncd, rec, ref, out = _compare_forward(ctx, orc, store, cam)
+    assert ncd == 0
+    assert np.abs(rec.final_T - ref.final_T).max() <= 1e-5
+
+
+def test_rasterize_forward_on_oracle_splats(ctx, orc):
+    """rasterize_forward on host splats, including a non-monotone source_index order."""
+    store = scenes.random_scene(50, sh_degree=1, seed=9)
+    cam = scenes.bench_camera(64, 64, 0.3)
+    cam.fx = cam.fy = 64.0
+    _, ref = orc.render_forward(store, cam, retain=True)
+    splats = ref.splats.copy()
+    rng = np.random.default_rng(0)
+    for perm in (np.arange(len(splats)), rng.permutation(len(splats))):
+        sp = splats[perm]
+        ref_img, r2 = orc.rasterize_forward(sp, cam, (0.2, 0.2, 0.2))
+        img, rec = rgs.rasterize_forward(sp, cam, (0.2, 0.2, 0.2), ctx=ctx)
+        assert np.array_equal(rec.tile_offsets, r2.tile_offsets)
+        assert np.array_equal(rec.tile_ids, r2.tile_ids)
+        assert np.abs(img - ref_img).max() <= 1e-4
+
+
+def test_flow(ctx, orc):
+    store = scenes.synthetic_scene(3000, 128, 96, seed=4)
+    cam = scenes.bench_camera(128, 96, 0.5, scenes.yaw_pose(5.0))
+    ref = orc.render_flow(store, cam, threads=4)
+    got = rgs.render_flow(store, cam, ctx=ctx)
+    scale = max(1.0, np.abs(ref).max())
+    assert np.abs(got - ref).max() <= 1e-4 * scale
+
+
+def test_empty_and_offscreen(ctx, orc):
+    empty = rgs.GaussianStore.empty(0, 0)
+    cam = scenes.bench_camera(40, 24, 0.5)
+    out = rgs.render_forward(empty, cam, rgs.RenderOptions(background=(0.25, 0.5, 0.75)), ctx=ctx)
+    assert np.allclose(out.image, np.array([0.25, 0.5, 0.75], np.float32))
+    # everything behind the camera
+    st = scenes.random_scene(20, seed=3)
+    st.mean[:, 2] = -5
+    out = rgs.render_forward(st, cam, rgs.RenderOptions(retain_records=True), ctx=ctx)
+    assert len(out.records.splats) == 0 and out.records.n_pairs == 0
+    assert np.all(out.image == 0)
+
+
+def test_camera_and_rotor_errors(ctx):
+    st = scenes.random_scene(10, seed=1)
+    cam = scenes.bench_camera(32, 32, 0.5)
+    bad = scenes.bench_camera(32, 32, 0.5)
+    bad.fx = 0
+    with pytest.raises(rgs.CameraError, match="focal lengths must be positive"):
+        rgs.render_forward(st, bad, ctx=ctx)
+    bad = scenes.bench_camera(32, 32, 0.5, pose=np.diag([2.0, 1, 1, 1]))
+    with pytest.raises(rgs.CameraError, match="not orthogonal"):
+        rgs.render_forward(st, bad, ctx=ctx)
+    z = st.copy()
+    z.rotor[4] = 0
+    with pytest.raises(rgs.ZeroRotorError) as e:
+        rgs.render_forward(z, cam, ctx=ctx)
+    assert e.value.index == 4
+    nf = st.copy()
+    nf.rotor[7, 2] = np.nan
+    with pytest.raises(rgs.NonFiniteRotorError):
+        rgs.render_forward(nf, cam, ctx=ctx)
+
+
+def test_missing_records(ctx):
+    st = scenes.random_scene(3, seed=2)
+    cam = scenes.bench_camera(32, 32, 0.3)
+    out = rgs.render_forward(st, cam, rgs.RenderOptions(), ctx=ctx)
+    with pytest.raises(rgs.MissingRecordsError):
+        rgs.render_backward(st, cam, out.records, np.zeros((32, 32, 3)), ctx=ctx)
