@@ -1,0 +1,357 @@
+#!/usr/bin/env python3
+"""Benchmark: render FPS of the 4D-rotor splatting hot path on B200 (BASELINE.json).
+
+Workload (N=1): config C2 — 300K synthetic 4D Gaussians (SH degree 3), a
+1352x1014 Plenoptic-shaped camera, a 300-timestamp forward-render sweep.
+One "step" = one full sweep (300 frames).  `value` = frames/s over the K timed
+sweeps with the scene already resident in HBM; `e2e` = the same sweep through
+the C-ABI host-buffer entry point (rgs_render_views_host): scene H2D from pinned
+memory, 300 renders, every image D2H into pinned memory, inside the timed region.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Multi-GPU (torchrun, one process per GPU): each rank renders its own 300-frame
+sweep (distinct camera x timestamp views) with no data-path collective ->
+"scaling": "weak"; the timed region is bracketed by a barrier and the time is
+the max over ranks.  --impl reference times the reference's CPU render path
+(oracle/_ref: the reference sources compiled in place; else the oracle port) on
+the host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+W, H, N_GAUSS, N_TIMES, SEED = 1352, 1014, 300_000, 300, 2
+METRIC = "render FPS at 1352×1014 (300K 4D Gaussians)"
+WORKLOAD = "C2: 300K 4D rotor Gaussians, SH deg 3, 1352x1014, 300-timestamp forward-render sweep"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile-only", action="store_true", help="one warm sweep, no JSON (for ncu)")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+def max_over_ranks(value: float, dist=None, device=None) -> float:
+    """Max of a per-rank time over all ranks (the multi-GPU timing rule)."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return float(value)
+    import torch
+
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sweep_for_rank(rank):
+    from paper_2402_03307_b200 import scenes
+
+    # rank 0: identity pose (criterion-10 camera); other ranks: distinct yaw -> distinct views
+    pose = scenes.yaw_pose(2.0 * rank, (0.0, 0.0, 0.0))
+    return scenes.sweep_cameras(W, H, N_TIMES, pose)
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[3 + k].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- CPU reference
+def cpu_reference_lib():
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+
+    if oracle.reference_available():
+        return oracle.reference_build(), "reference"
+    return oracle.restatement(), "port"
+
+
+def cpu_frames(store, cams, lib, threads):
+    t0 = time.perf_counter()
+    for c in cams:
+        lib.render_forward(store, c, (0.0, 0.0, 0.0), threads=threads, retain=False)
+    return time.perf_counter() - t0
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU render path on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    from paper_2402_03307_b200 import scenes
+
+    lib, kind = cpu_reference_lib()
+    threads = os.cpu_count() or 1
+    store = scenes.synthetic_scene(N_GAUSS, W, H, seed=SEED)
+    cams = sweep_for_rank(0)
+    picks = np.linspace(0, N_TIMES - 1, args.warmup + args.steps).astype(int)
+    for k in range(args.warmup):
+        cpu_frames(store, [cams[picks[k]]], lib, threads)
+    t = cpu_frames(store, [cams[i] for i in picks[args.warmup:]], lib, threads)
+    fps = args.steps / t
+    sample = (f"{args.steps} frames of the 300-timestamp sweep (t index {list(map(int, picks[args.warmup:]))}), "
+              f"one frame per step, full 1352x1014, {threads} threads ({cpu_model()})")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD + " (CPU: one frame per step)", "n_gaussians": N_GAUSS, "width": W,
+                   "height": H, "timestamps": N_TIMES, "sh_degree": 3},
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": threads, "kind": kind, "sample": sample},
+        "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- ours
+def run_ours(args, rank, local_rank, world):
+    import torch
+
+    from paper_2402_03307_b200 import rgs, scenes
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+
+    store = scenes.synthetic_scene(N_GAUSS, W, H, seed=SEED)
+    cams = sweep_for_rank(rank)
+    ctx = rgs.Context(local_rank)
+    scene = rgs.DeviceScene.from_store(ctx, store)
+    images = torch.empty((N_TIMES, H, W, 3), dtype=torch.float32, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def sweep():
+        ctx.render_views(scene, cams, (0.0, 0.0, 0.0), out=images)
+
+    for _ in range(max(args.warmup, 1)):
+        sweep()
+    torch.cuda.synchronize(dev)
+    if args.profile_only:
+        sweep()
+        torch.cuda.synchronize(dev)
+        return
+
+    # ---- timed region: K sweeps, L2 flushed between sweeps, per-stage events on
+    # the launching stream (the torch current stream, which the context uses).
+    ctx.set_profiling(timing=True, count_evals=False)
+    ctx.profile_reset()
+    launches0 = ctx.kernel_launches
+    sampler = ClockSampler(local_rank)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    sampler.start()
+    evs = []
+    t_wall = time.perf_counter()
+    for _ in range(args.steps):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        sweep()
+        b.record(stream)
+        evs.append((a, b))
+    torch.cuda.synchronize(dev)
+    t_wall = time.perf_counter() - t_wall
+    if dist:
+        dist.barrier()
+    clocks = sampler.stop()
+    launches = ctx.kernel_launches - launches0
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = sum(step_ms)
+    stages, _ = ctx.profile_read()
+    ctx.set_profiling(timing=False, count_evals=False)
+    total_ms = max_over_ranks(total_ms, dist, dev)
+    frames = N_TIMES * args.steps * world
+    fps = frames / (total_ms / 1e3)
+
+    # ---- workload counters (untimed extra sweep): E, B, splats, pairs
+    ctx.set_profiling(timing=False, count_evals=True)
+    ctx.profile_reset()
+    sweep()
+    _, (E, B) = ctx.profile_read()
+    ctx.set_profiling(False, False)
+    img0, rec0 = ctx.render_forward_device(scene, cams[N_TIMES // 2], retain=False)
+    n_vis, n_pairs, n_slow = rec0._n_splats, rec0.n_pairs, rec0.n_slow_pixels
+    rec0.close()
+
+    # ---- roofline of the dominant stage
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    hbm_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "B200_PROFILING.md fallback 6.65 TB/s"
+    fp32_peak = ctx.measure_fp32_tflops()
+    n_frames_rank = N_TIMES * args.steps
+    per_stage = {}
+    for name, (ms, cnt) in stages.items():
+        if cnt:
+            per_stage[name] = {"ms_per_frame": ms / n_frames_rank, "share": ms / max(sum(v[0] for v in stages.values()), 1e-9)}
+    # algorithmic work per frame: blend 16 E + 10 B FLOP; preprocess
+    # 260 N read + 48 N_vis written; tile sort 2 passes x 16 B per pair.
+    e_frame, b_frame = E / N_TIMES, B / N_TIMES
+    kernels = {
+        "blend_fp32_k5": ("fp32", (16 * e_frame + 10 * b_frame) / 1e12, "TFLOP/s", fp32_peak),
+        "preprocess_k1": ("hbm", (260 * N_GAUSS + 48 * n_vis) / 1e9, "GB/s", hbm_peak),
+        "tile_sort_k4": ("hbm", (2 * 16 * n_pairs) / 1e9, "GB/s", hbm_peak),
+        "depth_sort": ("hbm", (8 * 2 * 12 * N_GAUSS) / 1e9, "GB/s", hbm_peak),
+    }
+    roof_all = {}
+    for name, (bound, work, unit, peak) in kernels.items():
+        if name in per_stage and per_stage[name]["ms_per_frame"] > 0:
+            ach = work / (per_stage[name]["ms_per_frame"] / 1e3)
+            roof_all[name] = {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak}
+    dominant = max(per_stage, key=lambda k: per_stage[k]["share"]) if per_stage else None
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(dominant)
+    except Exception:
+        pass
+    roofline = dict(roof_all.get(dominant, {}), kernel=dominant, traffic=traffic,
+                    peak_source=("bench FFMA probe (rgs_measure_fp32_tflops)" if dominant == "blend_fp32_k5"
+                                 else hbm_src))
+
+    # ---- e2e through the host-buffer C-ABI entry point
+    e2e = None
+    if not args.no_e2e:
+        f32 = store.arrays_f32()
+        pinned = [torch.from_numpy(a).pin_memory() for a in f32]
+        host_imgs = torch.empty((N_TIMES, H, W, 3), dtype=torch.float32, pin_memory=True)
+        h2d = sum(int(a.numel() * 4) for a in pinned) + N_TIMES * 8 * 24
+        d2h = host_imgs.numel() * 4
+        ctx.render_views_host([p.numpy() for p in pinned], store.active_sh_degree, cams, (0, 0, 0), host_imgs.numpy())
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        reps = 2
+        for _ in range(reps):
+            ctx.render_views_host([p.numpy() for p in pinned], store.active_sh_degree, cams, (0, 0, 0),
+                                  host_imgs.numpy())
+        dt = max_over_ranks(time.perf_counter() - t0, dist, dev)
+        e2e = {"value": N_TIMES * reps * world / dt, "unit": "frames/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "steps": reps,
+               "note": "rgs_render_views_host: pinned host scene -> HBM, 300 renders, 300 images -> pinned host"}
+
+    # ---- CPU baseline (rank 0, N=1 only, bounded sample)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        lib, kind = cpu_reference_lib()
+        threads = os.cpu_count() or 1
+        picks = [0, 100, 200, 299]
+        cpu_frames(store, [cams[0]], lib, threads)  # warm
+        t = cpu_frames(store, [cams[i] for i in picks], lib, threads)
+        cpu = {"value": len(picks) / t, "unit": "frames/s", "cores": threads, "kind": kind,
+               "sample": f"{len(picks)} frames (t index {picks}) of the same sweep, full 1352x1014, "
+                         f"{threads} threads, {cpu_model()}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "n_gaussians": N_GAUSS, "width": W, "height": H,
+                       "timestamps": N_TIMES, "sh_degree": 3, "seed": SEED,
+                       "l2": "256 MiB buffer written between sweeps; frames inside a sweep share L2 as a real sweep does",
+                       "parallelism": f"view-batch x{world} (replicated scene, no collective)",
+                       "n_visible_mid": n_vis, "n_pairs_mid": n_pairs, "slow_pixels_mid": n_slow,
+                       "evals_per_frame": e_frame, "blends_per_frame": b_frame},
+            "ms_per_frame": total_ms / (N_TIMES * args.steps), "wall_s": t_wall,
+            "target_fps": 600, "roofline": roofline, "kernels": roof_all, "stages": per_stage,
+            "fp32_peak_tflops": fp32_peak, "clocks": clocks, "gpu_launches": launches,
+            "e2e": e2e, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    rank, local_rank, world = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_ours(args, rank, local_rank, world)
+
+
+if __name__ == "__main__":
+    main()

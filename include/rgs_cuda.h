@@ -104,6 +104,20 @@ int rgs_ctx_synchronize(rgs_ctx* ctx);
 /* Count of kernels this context launched since creation (bench evidence). */
 long long rgs_ctx_kernel_launches(const rgs_ctx* ctx);
 
+/* ---------------------------------------------------------------- profiling */
+/* Per-stage CUDA-event timing on the launching stream (timing != 0) and
+ * counting of evaluated / blended (pixel, splat) pairs in the FP32 blend
+ * (count_evals != 0; the E and B of the blend roofline). */
+int rgs_profile_num_stages(void);
+const char* rgs_profile_stage_name(int stage);
+int rgs_ctx_set_profiling(rgs_ctx* ctx, int timing, int count_evals);
+int rgs_ctx_profile_reset(rgs_ctx* ctx);
+/* stage_ms[rgs_profile_num_stages()], stage_launches[...], evals[2] = {E, B}; any may be NULL. */
+int rgs_ctx_profile_read(rgs_ctx* ctx, double* stage_ms, long long* stage_launches,
+                         unsigned long long* evals);
+/* FP32 FMA-pipe throughput of this device (FFMA probe, best of 5), TFLOP/s with FMA = 2. */
+int rgs_measure_fp32_tflops(rgs_ctx* ctx, double* tflops);
+
 /* ---------------------------------------------------------------- scene */
 /* Device scene (GaussianStore replacement).  Host layout of the upload arrays
  * (the reference's Eigen memory order, gaussian.hpp:79-85):

@@ -67,12 +67,12 @@ __device__ __forceinline__ int eval_gates(const StagedSplat& s, float fpx, float
 }
 
 // K5: one CTA per 16x16 tile, one thread per pixel, splats staged 256 at a time.
-template <bool FLOW>
+template <bool FLOW, bool COUNT>
 __global__ void __launch_bounds__(256) k_blend_fp32(SplatArrays sp, const uint32_t* __restrict__ vals,
                                                     const uint2* __restrict__ ranges, DevCamera cam, float3 bg,
                                                     float* __restrict__ image, double* __restrict__ final_T,
                                                     uint32_t* __restrict__ n_contrib, uint32_t* slow_list,
-                                                    int* slow_count) {
+                                                    int* slow_count, unsigned long long* counters) {
     __shared__ StagedSplat sm[kTilePixels];
     const int tile = blockIdx.x;
     const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(256) k_blend_fp32(SplatArrays sp, const uint32
     float T = 1.f, errT = 0.f, acc0 = 0.f, acc1 = 0.f, acc2 = 0.f;
     int contrib = 0;
     bool done = !inside, slow = false;
+    uint32_t n_eval = 0, n_blend = 0;  // COUNT only: E and B of the roofline
 
     for (uint32_t start = rg.x; start < rg.y; start += kTilePixels) {
         if (__syncthreads_count(done) == kTilePixels) break;
@@ -97,6 +98,7 @@ __global__ void __launch_bounds__(256) k_blend_fp32(SplatArrays sp, const uint32
             const StagedSplat s = sm[k];
             float p, dx, dy, M;
             const int g = eval_gates(s, fpx, fpy, &p, &dx, &dy, &M);
+            if (COUNT) ++n_eval;
             if (g == kSkip) continue;
             if (g == kAmbiguous) {
                 slow = true;
@@ -130,6 +132,19 @@ __global__ void __launch_bounds__(256) k_blend_fp32(SplatArrays sp, const uint32
             T = test_T;
             errT = errN;
             contrib = (int)(start - rg.x) + k + 1;
+            if (COUNT) ++n_blend;
+        }
+    }
+    if (COUNT) {
+        unsigned long long e = n_eval, b = n_blend;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            e += __shfl_xor_sync(0xffffffffu, e, o);
+            b += __shfl_xor_sync(0xffffffffu, b, o);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicAdd(counters + 0, e);
+            atomicAdd(counters + 1, b);
         }
     }
     if (!inside) return;
@@ -444,14 +459,17 @@ static inline int blocks(long long n, int t) { return (int)((n + t - 1) / t); }
 
 void blend_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges, const DevCamera& cam,
                 float3 bg, int flow_mode, float* image, double* final_T, uint32_t* n_contrib, uint32_t* slow_list,
-                int* slow_count, cudaStream_t s) {
+                int* slow_count, unsigned long long* counters, cudaStream_t s) {
     const int tiles = cam.tiles_x * cam.tiles_y;
     if (flow_mode)
-        k_blend_fp32<true><<<tiles, kTilePixels, 0, s>>>(sp, pair_vals, ranges, cam, bg, image, final_T, n_contrib,
-                                                          slow_list, slow_count);
+        k_blend_fp32<true, false><<<tiles, kTilePixels, 0, s>>>(sp, pair_vals, ranges, cam, bg, image, final_T,
+                                                                 n_contrib, slow_list, slow_count, counters);
+    else if (counters)
+        k_blend_fp32<false, true><<<tiles, kTilePixels, 0, s>>>(sp, pair_vals, ranges, cam, bg, image, final_T,
+                                                                 n_contrib, slow_list, slow_count, counters);
     else
-        k_blend_fp32<false><<<tiles, kTilePixels, 0, s>>>(sp, pair_vals, ranges, cam, bg, image, final_T, n_contrib,
-                                                           slow_list, slow_count);
+        k_blend_fp32<false, false><<<tiles, kTilePixels, 0, s>>>(sp, pair_vals, ranges, cam, bg, image, final_T,
+                                                                  n_contrib, slow_list, slow_count, counters);
 }
 
 void backward_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges, const DevCamera& cam,
@@ -508,4 +526,30 @@ void scene_unpack(const float* params, int n, double* mean, double* ls, double* 
     if (n > 0) k_scene_unpack<<<blocks(n, 128), 128, 0, s>>>(params, n, mean, ls, rot, op, sh);
 }
 
+}  // namespace rgs_launch
+
+// ---------------------------------------------------------------------------
+// FP32 FMA-pipe peak probe (roofline denominator for the blend kernels; the
+// driver's MEASURED_PEAKS.json has HBM and bf16 tensor peaks only).
+namespace rgs_dev {
+__global__ void __launch_bounds__(256) k_ffma_peak(float* out, int iters, float a, float b) {
+    float x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6,
+          x7 = x0 + 7;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            x0 = fmaf(x0, a, b); x1 = fmaf(x1, a, b); x2 = fmaf(x2, a, b); x3 = fmaf(x3, a, b);
+            x4 = fmaf(x4, a, b); x5 = fmaf(x5, a, b); x6 = fmaf(x6, a, b); x7 = fmaf(x7, a, b);
+        }
+    }
+    const float s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+    if (s == 1234.5f) out[0] = s;  // keep the chains live
+}
+}  // namespace rgs_dev
+namespace rgs_launch {
+// Returns the FMA count of the launch.
+double ffma_peak(float* out, int blocks, int iters, cudaStream_t s) {
+    rgs_dev::k_ffma_peak<<<blocks, 256, 0, s>>>(out, iters, 0.999999f, 1e-6f);
+    return (double)blocks * 256.0 * iters * 16.0 * 8.0;
+}
 }  // namespace rgs_launch

@@ -161,6 +161,15 @@ struct Frame {
 
 }  // namespace
 
+// Pipeline stages timed by the profiling mode (rgs_ctx_set_profiling).
+enum Stage {
+    kStPreprocess = 0, kStDepthSort, kStCounts, kStDuplicate, kStTileSort, kStRanges, kStBlend, kStFixup,
+    kStBwdTiles, kStBwdFixup, kStBwdGauss, kNumStages
+};
+static const char* kStageNames[kNumStages] = {
+    "preprocess_k1", "depth_sort", "pair_counts_scan", "duplicate_k3", "tile_sort_k4", "tile_ranges",
+    "blend_fp32_k5", "blend_fp64_fixup", "backward_tiles_k6", "backward_fp64_fixup", "backward_gauss_k7"};
+
 struct rgs_ctx {
     int device = 0;
     cudaStream_t own_stream = nullptr;
@@ -174,7 +183,62 @@ struct rgs_ctx {
     DevBuf tmp_img;   // host-buffer staging
     DevBuf tmp_splats, tmp_scan, tmp_ids;
     DevStats* host_stats = nullptr;  // pinned
+    // profiling: CUDA events around every stage, on the launching stream
+    bool timing = false;
+    bool count_evals = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    struct Pending {
+        int stage;
+        cudaEvent_t a, b;
+    };
+    std::vector<Pending> pending;
+    double stage_ms[kNumStages] = {0};
+    long long stage_n[kNumStages] = {0};
+    DevBuf counters;  // 2 x u64: evaluated / blended (pixel, splat) pairs
+    cudaEvent_t next_event() {
+        if (ev_used == ev_pool.size()) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            ev_pool.push_back(e);
+        }
+        return ev_pool[ev_used++];
+    }
+    void collect() {
+        if (pending.empty()) return;
+        CK(cudaStreamSynchronize(stream));
+        for (const Pending& p : pending) {
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, p.a, p.b));
+            stage_ms[p.stage] += ms;
+            stage_n[p.stage] += 1;
+        }
+        pending.clear();
+        ev_used = 0;
+    }
 };
+
+namespace {
+// RAII: brackets one pipeline stage with events when profiling is on.
+struct StageTimer {
+    rgs_ctx* c;
+    int stage;
+    cudaEvent_t a = nullptr;
+    StageTimer(rgs_ctx* ctx, int st) : c(ctx), stage(st) {
+        if (c->timing) {
+            a = c->next_event();
+            CK(cudaEventRecord(a, c->stream));
+        }
+    }
+    ~StageTimer() {
+        if (c->timing && a) {
+            cudaEvent_t b = c->next_event();
+            cudaEventRecord(b, c->stream);
+            c->pending.push_back({stage, a, b});
+        }
+    }
+};
+}  // namespace
 
 struct rgs_scene {
     rgs_ctx* ctx = nullptr;
@@ -281,48 +345,57 @@ int run_forward(rgs_ctx* ctx, Frame& f, Source src, const rgs_scene* scene, cons
     SplatArrays sa = f.arrays();
 
     // K1
-    if (src == kFromScene)
-        rgs_launch::preprocess(scene->params, n, scene->sh_degree, dc, sa, &f.dstats()->err, &f.dstats()->n_valid, s);
-    else
-        rgs_launch::splats_from_host(dev_splats, n, dc, sa, &f.dstats()->n_valid, s);
-    ctx->launches += 1;
+    {
+        StageTimer t(ctx, kStPreprocess);
+        if (src == kFromScene)
+            rgs_launch::preprocess(scene->params, n, scene->sh_degree, dc, sa, &f.dstats()->err,
+                                   &f.dstats()->n_valid, s);
+        else
+            rgs_launch::splats_from_host(dev_splats, n, dc, sa, &f.dstats()->n_valid, s);
+        ctx->launches += 1;
+    }
 
     // Depth order (stable; ties by index == source index for scenes).
     cub::DoubleBuffer<unsigned long long> dk(f.dkey[0].as<unsigned long long>(), f.dkey[1].as<unsigned long long>());
     cub::DoubleBuffer<uint32_t> dv(f.dval[0].as<uint32_t>(), f.dval[1].as<uint32_t>());
-    size_t need = 0;
-    if (src == kFromSplats && !splats_monotone) {
-        // Ties must break on source_index (rasterizer.cpp:70): stable pre-sort by it,
-        // then gather the depth keys in that order.
-        cub::DoubleBuffer<uint32_t> sk(f.counts.as<uint32_t>(), f.offsets.as<uint32_t>());
-        cub::DoubleBuffer<uint32_t> sv(f.dval[0].as<uint32_t>(), f.dval[1].as<uint32_t>());
-        rgs_launch::source_keys(f.src.as<int32_t>(), n, sk.Current(), sv.Current(), s);
-        CK(cub::DeviceRadixSort::SortPairs(nullptr, need, sk, sv, n, 0, 32, s));
-        f.cub_tmp.ensure(need, s);
-        CK(cub::DeviceRadixSort::SortPairs(f.cub_tmp.p, need, sk, sv, n, 0, 32, s));
-        uint32_t* ids_in = sv.Current();
-        uint32_t* ids_out = sv.Alternate();
-        rgs_gather_keys(f.dkey[0].as<unsigned long long>(), ids_in, n, f.dkey[1].as<unsigned long long>(), ids_out,
-                        s);
-        ctx->launches += 2;
-        dk = cub::DoubleBuffer<unsigned long long>(f.dkey[1].as<unsigned long long>(),
-                                                   f.dkey[0].as<unsigned long long>());
-        dv = cub::DoubleBuffer<uint32_t>(ids_out, ids_in);
-    }
-    need = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, need, dk, dv, n, 0, 64, s));
-    size_t need_scan = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, need_scan, f.counts.as<uint32_t>(), f.offsets.as<uint32_t>(), n, s));
-    f.cub_tmp.ensure(std::max(need, need_scan), s);
-    if (n > 0) CK(cub::DeviceRadixSort::SortPairs(f.cub_tmp.p, need, dk, dv, n, 0, 64, s));
-    const uint32_t* sorted_ids = dv.Current();
-
-    rgs_launch::gather_counts(sorted_ids, f.tiles.as<uint32_t>(), n, f.counts.as<uint32_t>(), s);
-    if (n > 0)
-        CK(cub::DeviceScan::ExclusiveSum(f.cub_tmp.p, need_scan, f.counts.as<uint32_t>(), f.offsets.as<uint32_t>(), n,
+    size_t need = 0, need_scan = 0;
+    {
+        StageTimer t(ctx, kStDepthSort);
+        if (src == kFromSplats && !splats_monotone) {
+            // Ties must break on source_index (rasterizer.cpp:70): stable pre-sort by it,
+            // then gather the depth keys in that order.
+            cub::DoubleBuffer<uint32_t> sk(f.counts.as<uint32_t>(), f.offsets.as<uint32_t>());
+            cub::DoubleBuffer<uint32_t> sv(f.dval[0].as<uint32_t>(), f.dval[1].as<uint32_t>());
+            rgs_launch::source_keys(f.src.as<int32_t>(), n, sk.Current(), sv.Current(), s);
+            CK(cub::DeviceRadixSort::SortPairs(nullptr, need, sk, sv, n, 0, 32, s));
+            f.cub_tmp.ensure(need, s);
+            CK(cub::DeviceRadixSort::SortPairs(f.cub_tmp.p, need, sk, sv, n, 0, 32, s));
+            uint32_t* ids_in = sv.Current();
+            uint32_t* ids_out = sv.Alternate();
+            rgs_gather_keys(f.dkey[0].as<unsigned long long>(), ids_in, n, f.dkey[1].as<unsigned long long>(),
+                            ids_out, s);
+            ctx->launches += 2;
+            dk = cub::DoubleBuffer<unsigned long long>(f.dkey[1].as<unsigned long long>(),
+                                                       f.dkey[0].as<unsigned long long>());
+            dv = cub::DoubleBuffer<uint32_t>(ids_out, ids_in);
+        }
+        need = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, need, dk, dv, n, 0, 64, s));
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, need_scan, f.counts.as<uint32_t>(), f.offsets.as<uint32_t>(), n,
                                          s));
-    k_finish_counts<<<1, 32, 0, s>>>(f.offsets.as<uint32_t>(), f.counts.as<uint32_t>(), n, f.dstats());
-    ctx->launches += 2;
+        f.cub_tmp.ensure(std::max(need, need_scan), s);
+        if (n > 0) CK(cub::DeviceRadixSort::SortPairs(f.cub_tmp.p, need, dk, dv, n, 0, 64, s));
+    }
+    const uint32_t* sorted_ids = dv.Current();
+    {
+        StageTimer t(ctx, kStCounts);
+        rgs_launch::gather_counts(sorted_ids, f.tiles.as<uint32_t>(), n, f.counts.as<uint32_t>(), s);
+        if (n > 0)
+            CK(cub::DeviceScan::ExclusiveSum(f.cub_tmp.p, need_scan, f.counts.as<uint32_t>(),
+                                             f.offsets.as<uint32_t>(), n, s));
+        k_finish_counts<<<1, 32, 0, s>>>(f.offsets.as<uint32_t>(), f.counts.as<uint32_t>(), n, f.dstats());
+        ctx->launches += 2;
+    }
     CK(cudaMemcpyAsync(ctx->host_stats, f.dstats(), sizeof(DevStats), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     const DevStats st = *ctx->host_stats;
@@ -336,9 +409,12 @@ int run_forward(rgs_ctx* ctx, Frame& f, Source src, const rgs_scene* scene, cons
 
     // Duplicate-with-key + stable sort by tile id.
     f.ensure_pairs(f.n_pairs, s);
-    rgs_launch::duplicate(sorted_ids, f.offsets.as<uint32_t>(), f.counts.as<uint32_t>(), n, f.rect.as<ushort4>(),
-                          dc.tiles_x, f.tkey[0].as<uint32_t>(), f.pval[0].as<uint32_t>(), s);
-    ctx->launches += 1;
+    {
+        StageTimer t(ctx, kStDuplicate);
+        rgs_launch::duplicate(sorted_ids, f.offsets.as<uint32_t>(), f.counts.as<uint32_t>(), n,
+                              f.rect.as<ushort4>(), dc.tiles_x, f.tkey[0].as<uint32_t>(), f.pval[0].as<uint32_t>(), s);
+        ctx->launches += 1;
+    }
     cub::DoubleBuffer<uint32_t> tk(f.tkey[0].as<uint32_t>(), f.tkey[1].as<uint32_t>());
     cub::DoubleBuffer<uint32_t> tv(f.pval[0].as<uint32_t>(), f.pval[1].as<uint32_t>());
     const int tbits = bits_for(ntiles);
@@ -346,11 +422,15 @@ int run_forward(rgs_ctx* ctx, Frame& f, Source src, const rgs_scene* scene, cons
         need = 0;
         CK(cub::DeviceRadixSort::SortPairs(nullptr, need, tk, tv, (int)f.n_pairs, 0, tbits, s));
         f.cub_tmp.ensure(need, s);
+        StageTimer t(ctx, kStTileSort);
         CK(cub::DeviceRadixSort::SortPairs(f.cub_tmp.p, need, tk, tv, (int)f.n_pairs, 0, tbits, s));
     }
     f.pairs_sel = tv.Current() == f.pval[0].as<uint32_t>() ? 0 : 1;
-    rgs_launch::tile_ranges(tk.Current(), f.n_pairs, ntiles, f.ranges.as<uint2>(), s);
-    ctx->launches += 1;
+    {
+        StageTimer t(ctx, kStRanges);
+        rgs_launch::tile_ranges(tk.Current(), f.n_pairs, ntiles, f.ranges.as<uint2>(), s);
+        ctx->launches += 1;
+    }
 
     // Blend.
     uint32_t* nc = flow_mode ? nullptr : f.n_contrib.as<uint32_t>();
@@ -366,19 +446,28 @@ int run_forward(rgs_ctx* ctx, Frame& f, Source src, const rgs_scene* scene, cons
             img = ctx->tmp_img.as<float>();
         }
         image = img;
+        unsigned long long* counters = nullptr;
+        if (ctx->count_evals && !flow_mode) {
+            ctx->counters.ensure(16, s);
+            counters = ctx->counters.as<unsigned long long>();
+        }
+        StageTimer t(ctx, kStBlend);
         rgs_launch::blend_fp32(sa, f.pair_vals(), f.ranges.as<uint2>(), dc,
                                make_float3((float)f.bg[0], (float)f.bg[1], (float)f.bg[2]), flow_mode ? 1 : 0, img,
-                               fT, nc, f.slow_list.as<uint32_t>(), slow_count, s);
+                               fT, nc, f.slow_list.as<uint32_t>(), slow_count, counters, s);
         ctx->launches += 1;
     }
     if (!image) {
         ctx->tmp_img.ensure(npix * 3 * sizeof(float), s);
         image = ctx->tmp_img.as<float>();
     }
-    rgs_launch::blend_fp64_pixels(sa, f.pair_vals(), f.ranges.as<uint2>(), dc,
-                                  make_double3(f.bg[0], f.bg[1], f.bg[2]), flow_mode ? 1 : 0, image, fT, nc,
-                                  f.slow_list.as<uint32_t>(), slow_count, (int)npix, s);
-    ctx->launches += 1;
+    {
+        StageTimer t(ctx, kStFixup);
+        rgs_launch::blend_fp64_pixels(sa, f.pair_vals(), f.ranges.as<uint2>(), dc,
+                                      make_double3(f.bg[0], f.bg[1], f.bg[2]), flow_mode ? 1 : 0, image, fT, nc,
+                                      f.slow_list.as<uint32_t>(), slow_count, (int)npix, s);
+        ctx->launches += 1;
+    }
     CK(cudaGetLastError());
     return RGS_OK;
 }
@@ -477,6 +566,81 @@ void* rgs_ctx_stream(rgs_ctx* c) { return c ? (void*)c->stream : nullptr; }
 const char* rgs_ctx_last_error(const rgs_ctx* c) { return c ? c->err.c_str() : "null context"; }
 int rgs_ctx_error_index(const rgs_ctx* c) { return c ? c->err_index : -1; }
 long long rgs_ctx_kernel_launches(const rgs_ctx* c) { return c ? c->launches : 0; }
+
+int rgs_profile_num_stages(void) { return kNumStages; }
+const char* rgs_profile_stage_name(int k) { return (k >= 0 && k < kNumStages) ? kStageNames[k] : ""; }
+
+int rgs_ctx_set_profiling(rgs_ctx* c, int timing, int count_evals) {
+    return guarded(c, [&] {
+        c->collect();
+        c->timing = timing != 0;
+        c->count_evals = count_evals != 0;
+        if (c->count_evals) {
+            c->counters.ensure(16, c->stream);
+            CK(cudaMemsetAsync(c->counters.p, 0, 16, c->stream));
+        }
+        return RGS_OK;
+    });
+}
+
+int rgs_measure_fp32_tflops(rgs_ctx* c, double* tflops) {
+    if (!tflops) return RGS_E_INVALID;
+    return guarded(c, [&] {
+        DevBuf out;
+        out.ensure(64, c->stream);
+        cudaEvent_t a, b;
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b));
+        const int blocks = 148 * 8;
+        rgs_launch::ffma_peak(out.as<float>(), blocks, 64, c->stream);  // warm-up
+        double best = 0;
+        for (int rep = 0; rep < 5; ++rep) {
+            CK(cudaEventRecord(a, c->stream));
+            const double fmas = rgs_launch::ffma_peak(out.as<float>(), blocks, 4096, c->stream);
+            CK(cudaEventRecord(b, c->stream));
+            CK(cudaEventSynchronize(b));
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, a, b));
+            best = std::max(best, 2.0 * fmas / (ms * 1e-3) / 1e12);
+        }
+        c->launches += 6;
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        out.release(c->stream);
+        *tflops = best;
+        return RGS_OK;
+    });
+}
+
+int rgs_ctx_profile_reset(rgs_ctx* c) {
+    return guarded(c, [&] {
+        c->collect();
+        for (int k = 0; k < kNumStages; ++k) {
+            c->stage_ms[k] = 0;
+            c->stage_n[k] = 0;
+        }
+        if (c->counters.p) CK(cudaMemsetAsync(c->counters.p, 0, 16, c->stream));
+        return RGS_OK;
+    });
+}
+
+int rgs_ctx_profile_read(rgs_ctx* c, double* stage_ms, long long* stage_launches, unsigned long long* evals) {
+    return guarded(c, [&] {
+        c->collect();
+        for (int k = 0; k < kNumStages; ++k) {
+            if (stage_ms) stage_ms[k] = c->stage_ms[k];
+            if (stage_launches) stage_launches[k] = c->stage_n[k];
+        }
+        if (evals) {
+            evals[0] = evals[1] = 0;
+            if (c->counters.p) {
+                CK(cudaMemcpyAsync(evals, c->counters.p, 16, cudaMemcpyDeviceToHost, c->stream));
+                CK(cudaStreamSynchronize(c->stream));
+            }
+        }
+        return RGS_OK;
+    });
+}
 int rgs_ctx_synchronize(rgs_ctx* c) {
     return guarded(c, [&] {
         CK(cudaStreamSynchronize(c->stream));
@@ -836,16 +1000,25 @@ int rgs_render_backward(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* ca
         CK(cudaMemsetAsync(c->sgrad.p, 0, sizeof(double) * 9 * (size_t)std::max(n, 1), s));
         SplatArrays sa = f.arrays();
         const float3 bgf = make_float3((float)f.bg[0], (float)f.bg[1], (float)f.bg[2]);
-        rgs_launch::backward_fp32(sa, f.pair_vals(), f.ranges.as<uint2>(), dc, bgf, f.final_T.as<double>(),
-                                  f.n_contrib.as<uint32_t>(), dL_dimage, c->sgrad.as<double>(), s);
-        rgs_launch::backward_fp64_pixels(sa, f.pair_vals(), f.ranges.as<uint2>(), dc,
-                                         make_double3(f.bg[0], f.bg[1], f.bg[2]), f.final_T.as<double>(),
-                                         f.n_contrib.as<uint32_t>(), dL_dimage, f.slow_list.as<uint32_t>(),
-                                         &f.dstats()->slow_count, (int)((size_t)f.width * f.height),
-                                         c->sgrad.as<double>(), s);
-        rgs_launch::gaussian_backward(scene->params, n, scene->sh_degree, dc, f.valid.as<uint8_t>(),
-                                      c->sgrad.as<double>(), (flags & RGS_FLAG_ACCUMULATE) ? 1 : 0, grads, vnorm,
-                                      visible, s);
+        {
+            StageTimer t(c, kStBwdTiles);
+            rgs_launch::backward_fp32(sa, f.pair_vals(), f.ranges.as<uint2>(), dc, bgf, f.final_T.as<double>(),
+                                      f.n_contrib.as<uint32_t>(), dL_dimage, c->sgrad.as<double>(), s);
+        }
+        {
+            StageTimer t(c, kStBwdFixup);
+            rgs_launch::backward_fp64_pixels(sa, f.pair_vals(), f.ranges.as<uint2>(), dc,
+                                             make_double3(f.bg[0], f.bg[1], f.bg[2]), f.final_T.as<double>(),
+                                             f.n_contrib.as<uint32_t>(), dL_dimage, f.slow_list.as<uint32_t>(),
+                                             &f.dstats()->slow_count, (int)((size_t)f.width * f.height),
+                                             c->sgrad.as<double>(), s);
+        }
+        {
+            StageTimer t(c, kStBwdGauss);
+            rgs_launch::gaussian_backward(scene->params, n, scene->sh_degree, dc, f.valid.as<uint8_t>(),
+                                          c->sgrad.as<double>(), (flags & RGS_FLAG_ACCUMULATE) ? 1 : 0, grads,
+                                          vnorm, visible, s);
+        }
         c->launches += 3;
         CK(cudaGetLastError());
         return RGS_OK;

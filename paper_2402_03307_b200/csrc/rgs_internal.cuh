@@ -88,7 +88,7 @@ void duplicate(const uint32_t* sorted_ids, const uint32_t* offsets, const uint32
 void tile_ranges(const uint32_t* keys, long long n_pairs, int n_tiles, uint2* ranges, cudaStream_t s);
 void blend_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges, const DevCamera& cam,
                 float3 bg, int flow_mode, float* image, double* final_T, uint32_t* n_contrib,
-                uint32_t* slow_list, int* slow_count, cudaStream_t s);
+                uint32_t* slow_list, int* slow_count, unsigned long long* counters, cudaStream_t s);
 void mark_all_slow(int n_pixels, uint32_t* slow_list, int* slow_count, cudaStream_t s);
 void blend_fp64_pixels(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges,
                        const DevCamera& cam, double3 bg, int flow_mode, float* image, double* final_T,
@@ -114,4 +114,5 @@ void scene_unpack(const float* params, int n, double* mean, double* ls, double* 
                   cudaStream_t s);
 void source_keys(const int32_t* src, int n, uint32_t* keys, uint32_t* vals, cudaStream_t s);
 void valid_to_u32(const uint8_t* valid, int n, uint32_t* out, cudaStream_t s);
+double ffma_peak(float* out, int blocks, int iters, cudaStream_t s);
 }  // namespace rgs_launch

@@ -128,7 +128,9 @@ EXPORTS = [
     "rgs_scene_set_sh_degree", "rgs_scene_upload_f64", "rgs_scene_upload_f32", "rgs_scene_params",
     "rgs_scene_download_f64", "rgs_render_forward", "rgs_render_views", "rgs_render_views_host",
     "rgs_rasterize_forward", "rgs_render_flow", "rgs_records_destroy", "rgs_records_info_get",
-    "rgs_records_export", "rgs_render_backward", "rgs_camera_validate",
+    "rgs_records_export", "rgs_render_backward", "rgs_camera_validate", "rgs_profile_num_stages",
+    "rgs_profile_stage_name", "rgs_ctx_set_profiling", "rgs_ctx_profile_reset", "rgs_ctx_profile_read",
+    "rgs_measure_fp32_tflops",
 ]
 
 
@@ -170,6 +172,12 @@ def load_library(path: str = LIB_PATH):
         "rgs_records_export": (i, [p, p, p, p, p, p, p]),
         "rgs_render_backward": (i, [p, p, p, p, p, ctypes.c_uint, p, p, p]),
         "rgs_camera_validate": (i, [p, p]),
+        "rgs_profile_num_stages": (i, []),
+        "rgs_profile_stage_name": (ctypes.c_char_p, [i]),
+        "rgs_ctx_set_profiling": (i, [p, i, i]),
+        "rgs_ctx_profile_reset": (i, [p]),
+        "rgs_ctx_profile_read": (i, [p, p, p, p]),
+        "rgs_measure_fp32_tflops": (i, [p, p]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -381,6 +389,28 @@ class Context:
 
     def synchronize(self):
         self.check(self.L.rgs_ctx_synchronize(self.h))
+
+    # --- profiling (CUDA events per pipeline stage, on the launching stream)
+    def set_profiling(self, timing: bool = True, count_evals: bool = False):
+        self.check(self.L.rgs_ctx_set_profiling(self.h, int(timing), int(count_evals)))
+
+    def measure_fp32_tflops(self) -> float:
+        v = ctypes.c_double(0)
+        self.check(self.L.rgs_measure_fp32_tflops(self.h, ctypes.byref(v)))
+        return v.value
+
+    def profile_reset(self):
+        self.check(self.L.rgs_ctx_profile_reset(self.h))
+
+    def profile_read(self):
+        """{stage: (total_ms, launches)}, (E, B)."""
+        k = self.L.rgs_profile_num_stages()
+        ms = (ctypes.c_double * k)()
+        cnt = (ctypes.c_longlong * k)()
+        ev = (ctypes.c_ulonglong * 2)()
+        self.check(self.L.rgs_ctx_profile_read(self.h, ms, cnt, ev))
+        names = [self.L.rgs_profile_stage_name(i).decode() for i in range(k)]
+        return {names[i]: (ms[i], cnt[i]) for i in range(k)}, (ev[0], ev[1])
 
     # --- scenes
     def scene(self, store: GaussianStore) -> "DeviceScene":

@@ -145,3 +145,29 @@ def test_missing_records(ctx):
     out = rgs.render_forward(st, cam, rgs.RenderOptions(), ctx=ctx)
     with pytest.raises(rgs.MissingRecordsError):
         rgs.render_backward(st, cam, out.records, np.zeros((32, 32, 3)), ctx=ctx)
+
+
+GOLDEN = sorted(__import__("glob").glob(__import__("os").path.join(__import__("os").path.dirname(__file__),
+                                                                   "golden", "*.npz")))
+
+
+@pytest.mark.parametrize("path", GOLDEN, ids=lambda p: p.split("/")[-1])
+def test_against_reference_golden(ctx, path):
+    """CUDA path vs outputs of the reference itself (tests/golden, made by oracle/_ref)."""
+    from test_oracle import load_case
+    from parity import floored_rel_err
+
+    z, store, cam, dl = load_case(path)
+    bg = tuple(z["background"])
+    out = rgs.render_forward(store, cam, rgs.RenderOptions(background=bg, retain_records=True), ctx=ctx)
+    rec = out.records
+    assert splat_mismatch(rec.splats, z["splats"]) == {}
+    assert np.array_equal(rec.tile_offsets, z["tile_offsets"])
+    assert np.array_equal(rec.tile_ids, z["tile_ids"])
+    assert np.array_equal(rec.n_contrib, z["n_contrib"])
+    assert np.abs(out.image - z["image"]).max() <= 1e-4
+    g = rgs.render_backward(store, cam, rec, dl, ctx=ctx)
+    assert np.array_equal(g.visible.astype(bool), z["visible"].astype(bool))
+    assert floored_rel_err(g.as_matrix(), z["grads"]).max() <= 1e-3
+    flow = rgs.render_flow(store, cam, ctx=ctx)
+    assert np.abs(flow - z["flow"]).max() <= 1e-4 * max(1.0, np.abs(z["flow"]).max())
