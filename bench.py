@@ -245,7 +245,7 @@ def run_ours(args, rank, local_rank, world):
     ctx.set_profiling(timing=False, count_evals=True)
     ctx.profile_reset()
     sweep()
-    _, (E, B) = ctx.profile_read()
+    _, (E, B, E_kernel) = ctx.profile_read()
     ctx.set_profiling(False, False)
     img0, rec0 = ctx.render_forward_device(scene, cams[N_TIMES // 2], retain=False)
     n_vis, n_pairs, n_slow = rec0._n_splats, rec0.n_pairs, rec0.n_slow_pixels
@@ -271,8 +271,9 @@ def run_ours(args, rank, local_rank, world):
     kernels = {
         "blend_fp32_k5": ("fp32", (16 * e_frame + 10 * b_frame) / 1e12, "TFLOP/s", fp32_peak),
         "preprocess_k1": ("hbm", (260 * N_GAUSS + 48 * n_vis) / 1e9, "GB/s", hbm_peak),
-        "tile_sort_k4": ("hbm", (2 * 16 * n_pairs) / 1e9, "GB/s", hbm_peak),
-        "depth_sort": ("hbm", (8 * 2 * 12 * N_GAUSS) / 1e9, "GB/s", hbm_peak),
+        "tile_fill_k3": ("hbm", (4 * n_pairs + 12 * n_vis) / 1e9, "GB/s", hbm_peak),
+        "tile_counts_scan": ("hbm", (12 * n_vis) / 1e9, "GB/s", hbm_peak),
+        "depth_rank": ("hbm", (32 * n_vis) / 1e9, "GB/s", hbm_peak),
     }
     roof_all = {}
     for name, (bound, work, unit, peak) in kernels.items():
@@ -332,7 +333,8 @@ def run_ours(args, rank, local_rank, world):
                        "l2": "256 MiB buffer written between sweeps; frames inside a sweep share L2 as a real sweep does",
                        "parallelism": f"view-batch x{world} (replicated scene, no collective)",
                        "n_visible_mid": n_vis, "n_pairs_mid": n_pairs, "slow_pixels_mid": n_slow,
-                       "evals_per_frame": e_frame, "blends_per_frame": b_frame},
+                       "evals_per_frame": e_frame, "blends_per_frame": b_frame,
+                       "kernel_evals_per_frame": E_kernel / N_TIMES},
             "ms_per_frame": total_ms / (N_TIMES * args.steps), "wall_s": t_wall,
             "target_fps": 600, "roofline": roofline, "kernels": roof_all, "stages": per_stage,
             "fp32_peak_tflops": fp32_peak, "clocks": clocks, "gpu_launches": launches,

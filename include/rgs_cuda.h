@@ -112,7 +112,10 @@ int rgs_profile_num_stages(void);
 const char* rgs_profile_stage_name(int stage);
 int rgs_ctx_set_profiling(rgs_ctx* ctx, int timing, int count_evals);
 int rgs_ctx_profile_reset(rgs_ctx* ctx);
-/* stage_ms[rgs_profile_num_stages()], stage_launches[...], evals[2] = {E, B}; any may be NULL. */
+/* stage_ms[rgs_profile_num_stages()], stage_launches[...], evals[3] = {E, B, E_kernel}; any may be
+ * NULL.  E: (pixel, splat) evaluations of the reference algorithm (every tile-list entry up
+ * to each pixel's termination), B: blended pairs, E_kernel: pairs the kernel evaluated
+ * after its per-warp culling. */
 int rgs_ctx_profile_read(rgs_ctx* ctx, double* stage_ms, long long* stage_launches,
                          unsigned long long* evals);
 /* FP32 FMA-pipe throughput of this device (FFMA probe, best of 5), TFLOP/s with FMA = 2. */

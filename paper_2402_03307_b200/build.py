@@ -32,7 +32,9 @@ COMMON = ARCH + [
 # FMA: its expression order is the parity contract with the CPU reference.
 SOURCES = [
     ("k_fp64.cu", ["-fmad=false"]),
-    ("k_fp32.cu", []),
+    ("k_raster.cu", []),
+    ("k_binning.cu", []),
+    ("k_misc.cu", []),
     ("rgs_capi.cu", []),
 ]
 

@@ -1,0 +1,524 @@
+// Tile binning (replaces bin_and_sort, rasterizer.cpp:57-74).
+//
+// The reference appends splat k to every tile of its rectangle in k order, then sorts
+// each tile's list by (depth, source_index).  Here:
+//
+//   1. Depth ranks: an MSD counting sort of the visible splats on a depth bucket (the
+//      top bits of key - min_key, 2^18 buckets); every bucket is then sorted by the
+//      exact (64-bit depth key, source index) -- insertion sort per bucket, shared-memory
+//      bitonic for rare large buckets.  sorted_ids[r] = splat of rank r.
+//   2. Duplicate-with-key in rank order: an exclusive scan of tiles-touched over the
+//      ranks gives each splat its pair offset; warps emit the (tile, splat) pairs of 32
+//      consecutive ranks cooperatively (coalesced stores).
+//   3. LSD radix sort of the pairs on the packed key (ty << 8 | tx), as two stable 8-bit
+//      digit passes (tx, then ty).  Each pass: per-block digit histogram, exclusive scan
+//      of the [digit][block] counts, and a scatter that ranks each block's elements with
+//      warp __match_any_sync peer groups, sorts them by digit in shared memory and writes
+//      contiguous per-digit runs.
+//
+// Stable passes over pairs emitted in rank order leave every tile's list in
+// (depth, index) order: the reference's std::sort order bit for bit.
+#include <algorithm>
+
+#include "rgs_internal.cuh"
+
+namespace rgs_dev {
+
+constexpr int kBucketBits = 18;
+constexpr int kNumBuckets = 1 << kBucketBits;
+constexpr int kSmallBucket = 32;
+constexpr unsigned kFullMask = 0xffffffffu;
+
+__device__ __forceinline__ bool key_less(unsigned long long ka, uint32_t ta, unsigned long long kb, uint32_t tb) {
+    return ka < kb || (ka == kb && ta < tb);
+}
+
+// Tie-break value of splat i: its source index (rasterize_forward) or i itself.
+__device__ __forceinline__ uint32_t tie_of(const int32_t* src, uint32_t i) {
+    return src ? ((uint32_t)src[i] ^ 0x80000000u) : i;
+}
+
+// --------------------------------------------------------------------------- scan
+// Exclusive scan of a u32 array in three phases (block sums, scan of sums, apply).
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 4;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* total) {
+    __shared__ uint32_t warp_sums[32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFullMask, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        const int nw = blockDim.x >> 5;
+        uint32_t s = lane < nw ? warp_sums[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFullMask, s, o);
+            if (lane >= o) s += y;
+        }
+        if (lane < nw) warp_sums[lane] = s;
+    }
+    __syncthreads();
+    const uint32_t before = (w > 0 ? warp_sums[w - 1] : 0) + x - v;
+    if (total) *total = warp_sums[(blockDim.x >> 5) - 1];
+    __syncthreads();
+    return before;
+}
+
+// `n_dev` (optional) overrides n with a device-side count.
+__global__ void __launch_bounds__(kScanThreads) k_scan_sums(const uint32_t* __restrict__ in, int n,
+                                                            const int* __restrict__ n_dev, uint32_t* sums) {
+    if (n_dev) n = min(n, *n_dev);
+    const int base = blockIdx.x * kScanTile + threadIdx.x * kScanItems;
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k)
+        if (base + k < n) s += in[base + k];
+    uint32_t total;
+    block_exclusive_scan(s, &total);
+    if (threadIdx.x == 0) sums[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_block_sums(uint32_t* sums, int nb, uint32_t* grand_total) {
+    uint32_t carry = 0;
+    for (int base = 0; base < nb; base += kScanThreads) {
+        const int i = base + threadIdx.x;
+        const uint32_t v = i < nb ? sums[i] : 0;
+        uint32_t total;
+        const uint32_t ex = block_exclusive_scan(v, &total);
+        if (i < nb) sums[i] = carry + ex;
+        carry += total;
+    }
+    if (threadIdx.x == 0 && grand_total) *grand_total = carry;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_apply(const uint32_t* __restrict__ in, int n,
+                                                             const int* __restrict__ n_dev,
+                                                             const uint32_t* __restrict__ sums, uint32_t* out) {
+    if (n_dev) n = min(n, *n_dev);
+    const int base = blockIdx.x * kScanTile + threadIdx.x * kScanItems;
+    uint32_t v[kScanItems];
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        v[k] = base + k < n ? in[base + k] : 0;
+        s += v[k];
+    }
+    uint32_t run = block_exclusive_scan(s, nullptr) + sums[blockIdx.x];
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        if (base + k < n) out[base + k] = run;
+        run += v[k];
+    }
+}
+
+// --------------------------------------------------------------------------- depth ranks
+__global__ void k_bucket_setup(BinState* st) {
+    const unsigned long long lo = st->key_min, hi = st->key_max;
+    int shift = 0;
+    if (hi > lo) {
+        const unsigned long long range = hi - lo;
+        const int bits = 64 - __clzll(range);
+        shift = bits > kBucketBits ? bits - kBucketBits : 0;
+    }
+    st->shift = shift;
+}
+
+__global__ void k_bucket_hist(const uint8_t* __restrict__ valid, const unsigned long long* __restrict__ key, int n,
+                              const BinState* __restrict__ st, uint32_t* bucket_count) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || !valid[i]) return;
+    atomicAdd(&bucket_count[(uint32_t)((key[i] - st->key_min) >> st->shift)], 1u);
+}
+
+__global__ void k_bucket_scatter(const uint8_t* __restrict__ valid, const unsigned long long* __restrict__ key,
+                                 int n, const BinState* __restrict__ st, const uint32_t* __restrict__ bucket_off,
+                                 uint32_t* bucket_cur, unsigned long long* ent_key, uint32_t* ent_id) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || !valid[i]) return;
+    const unsigned long long k = key[i];
+    const uint32_t b = (uint32_t)((k - st->key_min) >> st->shift);
+    const uint32_t pos = bucket_off[b] + atomicAdd(&bucket_cur[b], 1u);
+    ent_key[pos] = k;
+    ent_id[pos] = (uint32_t)i;
+}
+
+// One thread per bucket: insertion sort of small buckets in place, big ones deferred.
+__global__ void k_bucket_sort_small(const uint32_t* __restrict__ bucket_count, const uint32_t* __restrict__ bucket_off,
+                                    unsigned long long* ent_key, uint32_t* ent_id, const int32_t* __restrict__ src,
+                                    const uint32_t* __restrict__ tiles, uint32_t* sorted_ids,
+                                    uint32_t* sorted_tiles, BinState* st, uint32_t* big_list) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= kNumBuckets) return;
+    const uint32_t cnt = bucket_count[b];
+    if (cnt == 0) return;
+    const uint32_t off = bucket_off[b];
+    if (cnt > kSmallBucket) {
+        big_list[atomicAdd(&st->n_big, 1u)] = (uint32_t)b;
+        return;
+    }
+    unsigned long long* K = ent_key + off;
+    uint32_t* I = ent_id + off;
+    for (uint32_t a = 1; a < cnt; ++a) {
+        const unsigned long long kv = K[a];
+        const uint32_t iv = I[a];
+        const uint32_t tv = tie_of(src, iv);
+        int j = (int)a - 1;
+        while (j >= 0 && key_less(kv, tv, K[j], tie_of(src, I[j]))) {
+            K[j + 1] = K[j];
+            I[j + 1] = I[j];
+            --j;
+        }
+        K[j + 1] = kv;
+        I[j + 1] = iv;
+    }
+    for (uint32_t a = 0; a < cnt; ++a) {
+        sorted_ids[off + a] = I[a];
+        sorted_tiles[off + a] = tiles[I[a]];
+    }
+}
+
+struct SortRec {
+    unsigned long long key;
+    uint32_t tie;
+    uint32_t id;
+};
+
+__device__ __forceinline__ bool rec_greater(const SortRec& a, const SortRec& b) {
+    return key_less(b.key, b.tie, a.key, a.tie);
+}
+
+__device__ void block_bitonic(SortRec* s, int n_pow2) {
+    for (int k = 2; k <= n_pow2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < n_pow2; i += blockDim.x) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const bool up = (i & k) == 0;
+                    SortRec a = s[i], b = s[l];
+                    if (rec_greater(a, b) == up) {
+                        s[i] = b;
+                        s[l] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+constexpr int kBigSmem = 4096;  // records per block in shared memory (64 KB)
+
+// One block per big bucket: bitonic in shared memory, or in a disjoint window
+// [2 off, 2 off + np) of global scratch when the bucket exceeds kBigSmem records.
+__global__ void __launch_bounds__(512) k_bucket_sort_big(const uint32_t* __restrict__ bucket_count,
+                                                         const uint32_t* __restrict__ bucket_off,
+                                                         const unsigned long long* __restrict__ ent_key,
+                                                         const uint32_t* __restrict__ ent_id,
+                                                         const int32_t* __restrict__ src,
+                                                         const uint32_t* __restrict__ tiles, const BinState* st,
+                                                         const uint32_t* __restrict__ big_list, uint32_t* sorted_ids,
+                                                         uint32_t* sorted_tiles, SortRec* scratch) {
+    extern __shared__ SortRec smem_rec[];
+    for (uint32_t w = blockIdx.x; w < st->n_big; w += gridDim.x) {
+        const uint32_t b = big_list[w];
+        const uint32_t cnt = bucket_count[b], off = bucket_off[b];
+        int np = 1;
+        while (np < (int)cnt) np <<= 1;
+        SortRec* s = np <= kBigSmem ? smem_rec : scratch + (size_t)off * 2;
+        for (int i = threadIdx.x; i < np; i += blockDim.x) {
+            if (i < (int)cnt) {
+                const uint32_t id = ent_id[off + i];
+                s[i] = SortRec{ent_key[off + i], tie_of(src, id), id};
+            } else {
+                s[i] = SortRec{~0ull, 0xffffffffu, 0xffffffffu};
+            }
+        }
+        __syncthreads();
+        block_bitonic(s, np);
+        for (int i = threadIdx.x; i < (int)cnt; i += blockDim.x) {
+            sorted_ids[off + i] = s[i].id;
+            sorted_tiles[off + i] = tiles[s[i].id];
+        }
+        __syncthreads();
+    }
+}
+
+// --------------------------------------------------------------------------- duplicate
+// Warp-cooperative: the pairs of 32 consecutive ranks are written as one contiguous
+// run (lane l writes pair l, l+32, ...).  key = tile id, value = splat id.
+__global__ void __launch_bounds__(256) k_duplicate(const uint32_t* __restrict__ sorted_ids,
+                                                   const uint32_t* __restrict__ pair_off,
+                                                   const uint32_t* __restrict__ sorted_tiles,
+                                                   const ushort4* __restrict__ rect, const BinState* __restrict__ st,
+                                                   int tiles_x, uint32_t* keys, uint32_t* vals) {
+    const int lane = threadIdx.x & 31;
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nv = st->n_valid;
+    if (st->overflow || r - lane >= nv) return;  // buffers too small / whole warp past the end
+    uint32_t id = 0, cnt = 0, off = 0;
+    ushort4 q = make_ushort4(0, 0, 0, 0);
+    if (r < nv) {
+        id = sorted_ids[r];
+        cnt = sorted_tiles[r];
+        off = pair_off[r];
+        if (cnt) q = rect[id];
+    }
+    // inclusive prefix of counts within the warp
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFullMask, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const uint32_t total = __shfl_sync(kFullMask, incl, 31);
+    const uint32_t base = __shfl_sync(kFullMask, off, 0);
+    const int w = q.y - q.x + 1;
+    for (uint32_t k0 = 0; k0 < total; k0 += 32) {  // warp-uniform trip count (full-mask shuffles)
+        const uint32_t k = k0 + lane;
+        // owner: first lane whose inclusive prefix exceeds k (binary search over lanes)
+        int lo = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            const uint32_t v = __shfl_sync(kFullMask, incl, lo + step - 1);
+            if (v <= k) lo += step;
+        }
+        // lane `lo` owns pair k; fetch its rectangle and exclusive prefix
+        const uint32_t o_incl = __shfl_sync(kFullMask, incl, lo);
+        const uint32_t o_cnt = __shfl_sync(kFullMask, cnt, lo);
+        const int o_w = __shfl_sync(kFullMask, w, lo);
+        const int o_x0 = __shfl_sync(kFullMask, (int)q.x, lo);
+        const int o_y0 = __shfl_sync(kFullMask, (int)q.z, lo);
+        const uint32_t o_id = __shfl_sync(kFullMask, id, lo);
+        if (k < total) {
+            const int m = (int)(k - (o_incl - o_cnt));
+            const int dy = m / o_w, dx = m - dy * o_w;
+            keys[base + k] = ((uint32_t)(o_y0 + dy) << 8) | (uint32_t)(o_x0 + dx);  // packed (ty, tx)
+            vals[base + k] = o_id;
+        }
+    }
+}
+
+// --------------------------------------------------------------------------- LSD digit pass
+// Stable counting-sort pass on one byte of the packed key (ty << 8 | tx): tx for pass 0,
+// ty for pass 1.  A block sorts a tile of kBlockTile consecutive elements locally:
+// warp w ranks the tile's elements [256 w, 256 w + 256) in 8 rounds of 32 (lane order,
+// __match_any_sync peer groups, warp-private running counts per digit); a per-digit
+// prefix over the 8 warps gives each element its position in a digit-sorted copy of
+// the tile in shared memory, which is then written out as contiguous per-digit runs
+// at the global offsets of (digit, block).  Stability follows from (block, warp,
+// round, lane) order = element order.
+constexpr int kRadixThreads = 256;
+constexpr int kRadixWarps = kRadixThreads / 32;
+constexpr int kRadixRounds = 8;
+constexpr int kBlockTile = kRadixThreads * kRadixRounds;  // 2048
+constexpr int kRadixDigits = 256;
+
+// counts layout: [digit][block], so one exclusive scan yields every (digit, block) offset.
+__global__ void __launch_bounds__(kRadixThreads) k_radix_hist(const uint32_t* __restrict__ keys,
+                                                              const BinState* __restrict__ st, int shift, int n_blocks,
+                                                              uint32_t* counts) {
+    __shared__ uint32_t h[kRadixDigits];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const uint32_t n = st->n_pairs_eff;
+    const uint32_t base = (uint32_t)blockIdx.x * kBlockTile;
+    uint32_t d[kRadixRounds];
+#pragma unroll
+    for (int j = 0; j < kRadixRounds; ++j) {
+        const uint32_t e = base + j * kRadixThreads + threadIdx.x;
+        d[j] = e < n ? (keys[e] >> shift) & 0xffu : 0xffffffffu;
+    }
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int j = 0; j < kRadixRounds; ++j) {
+        const unsigned peers = __match_any_sync(0xffffffffu, d[j]);
+        if (d[j] != 0xffffffffu && (peers & ((1u << lane) - 1u)) == 0) atomicAdd(&h[d[j]], __popc(peers));
+    }
+    __syncthreads();
+    counts[(size_t)threadIdx.x * n_blocks + blockIdx.x] = h[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(const uint32_t* __restrict__ keys_in,
+                                                                 const uint32_t* __restrict__ vals_in,
+                                                                 const BinState* __restrict__ st, int shift,
+                                                                 int n_blocks, const uint32_t* __restrict__ offsets,
+                                                                 uint32_t* keys_out, uint32_t* vals_out) {
+    __shared__ uint32_t wcnt[kRadixWarps][kRadixDigits];  // per-warp counts -> per-warp starts
+    __shared__ uint32_t dstart[kRadixDigits];             // digit start inside the sorted tile
+    __shared__ uint32_t gbase[kRadixDigits];              // global offset of (digit, block)
+    __shared__ uint32_t skey[kBlockTile], sval[kBlockTile];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < kRadixWarps; ++k) wcnt[k][threadIdx.x] = 0;
+    gbase[threadIdx.x] = offsets[(size_t)threadIdx.x * n_blocks + blockIdx.x];
+    const uint32_t n = st->n_pairs_eff;
+    const uint32_t base = (uint32_t)blockIdx.x * kBlockTile + w * (kBlockTile / kRadixWarps);
+    uint32_t key[kRadixRounds], val[kRadixRounds], rk[kRadixRounds];
+#pragma unroll
+    for (int j = 0; j < kRadixRounds; ++j) {
+        const uint32_t e = base + j * 32 + lane;
+        key[j] = e < n ? keys_in[e] : 0xffffffffu;
+        val[j] = e < n ? vals_in[e] : 0u;
+    }
+    __syncthreads();
+    // warp-local ranks (element order within the warp's 256 elements)
+#pragma unroll
+    for (int j = 0; j < kRadixRounds; ++j) {
+        const uint32_t d = key[j] != 0xffffffffu ? (key[j] >> shift) & 0xffu : 0xffffffffu;
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t below = __popc(peers & ((1u << lane) - 1u));
+        uint32_t r = 0;
+        if (d != 0xffffffffu) r = wcnt[w][d] + below;
+        __syncwarp();
+        if (d != 0xffffffffu && below == 0) wcnt[w][d] += __popc(peers);
+        __syncwarp();
+        rk[j] = r;
+    }
+    __syncthreads();
+    // per digit: prefix over warps, and the digit's start in the sorted tile
+    {
+        const int dd = threadIdx.x;
+        uint32_t tot = 0;
+#pragma unroll
+        for (int k = 0; k < kRadixWarps; ++k) {
+            const uint32_t c = wcnt[k][dd];
+            wcnt[k][dd] = tot;
+            tot += c;
+        }
+        dstart[dd] = tot;  // digit total for now; scanned below
+    }
+    __syncthreads();
+    {
+        uint32_t total;
+        const uint32_t ex = block_exclusive_scan(dstart[threadIdx.x], &total);
+        __syncthreads();
+        dstart[threadIdx.x] = ex;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kRadixRounds; ++j) {
+        if (key[j] == 0xffffffffu) continue;
+        const uint32_t d = (key[j] >> shift) & 0xffu;
+        const uint32_t p = dstart[d] + wcnt[w][d] + rk[j];
+        skey[p] = key[j];
+        sval[p] = val[j];
+    }
+    __syncthreads();
+    const uint32_t valid_in_tile = n > (uint32_t)blockIdx.x * kBlockTile
+                                       ? min((uint32_t)kBlockTile, n - (uint32_t)blockIdx.x * kBlockTile)
+                                       : 0u;
+    for (uint32_t i = threadIdx.x; i < valid_in_tile; i += kRadixThreads) {
+        const uint32_t k = skey[i];
+        const uint32_t d = (k >> shift) & 0xffu;
+        const uint32_t g = gbase[d] + (i - dstart[d]);
+        keys_out[g] = k;
+        vals_out[g] = sval[i];
+    }
+}
+
+// Pair total vs buffer capacity: an overflowing view does no pair work and is re-rendered.
+__global__ void k_check_capacity(BinState* st) {
+    const bool over = st->n_pairs > st->pair_cap;
+    st->overflow = over ? 1u : 0u;
+    st->n_pairs_eff = over ? 0u : st->n_pairs;
+}
+
+__global__ void k_tile_ranges(const uint32_t* __restrict__ keys, const BinState* __restrict__ st, int tiles_x,
+                              uint2* ranges) {
+    const uint32_t n = st->n_pairs_eff;
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t k = keys[i];
+    const uint32_t t = (k >> 8) * (uint32_t)tiles_x + (k & 0xffu);
+    if (i == 0 || keys[i - 1] != k) ranges[t].x = i;
+    if (i == n - 1 || keys[i + 1] != k) ranges[t].y = i + 1;
+}
+
+}  // namespace rgs_dev
+
+// ---------------------------------------------------------------------------
+namespace rgs_launch {
+using namespace rgs_dev;
+
+static inline int blocks(long long n, int t) { return (int)((n + t - 1) / t); }
+
+int num_depth_buckets() { return kNumBuckets; }
+
+void exclusive_scan(const uint32_t* in, int n, uint32_t* out, uint32_t* scratch, uint32_t* total, cudaStream_t s,
+                    const int* n_dev) {
+    const int nb = blocks(n, kScanTile);
+    if (nb <= 0) return;
+    k_scan_sums<<<nb, kScanThreads, 0, s>>>(in, n, n_dev, scratch);
+    k_scan_block_sums<<<1, kScanThreads, 0, s>>>(scratch, nb, total);
+    k_scan_apply<<<nb, kScanThreads, 0, s>>>(in, n, n_dev, scratch, out);
+}
+
+void bucket_hist(const uint8_t* valid, const unsigned long long* key, int n, BinState* st, uint32_t* bucket_count,
+                 cudaStream_t s) {
+    k_bucket_setup<<<1, 1, 0, s>>>(st);
+    if (n > 0) k_bucket_hist<<<blocks(n, 256), 256, 0, s>>>(valid, key, n, st, bucket_count);
+}
+
+void depth_ranks(const uint8_t* valid, const unsigned long long* key, const uint32_t* tiles, int n,
+                 const int32_t* src, BinState* st, const uint32_t* bucket_count, const uint32_t* bucket_off,
+                 uint32_t* bucket_cur, unsigned long long* ent_key, uint32_t* ent_id, uint32_t* sorted_ids,
+                 uint32_t* sorted_tiles, uint32_t* big_list, void* big_scratch, cudaStream_t s) {
+    if (n <= 0) return;
+    k_bucket_scatter<<<blocks(n, 256), 256, 0, s>>>(valid, key, n, st, bucket_off, bucket_cur, ent_key, ent_id);
+    k_bucket_sort_small<<<blocks(kNumBuckets, 256), 256, 0, s>>>(bucket_count, bucket_off, ent_key, ent_id, src,
+                                                                 tiles, sorted_ids, sorted_tiles, st, big_list);
+    k_bucket_sort_big<<<148, 512, kBigSmem * sizeof(SortRec), s>>>(bucket_count, bucket_off, ent_key, ent_id, src,
+                                                                   tiles, st, big_list, sorted_ids, sorted_tiles,
+                                                                   reinterpret_cast<SortRec*>(big_scratch));
+}
+
+void duplicate(const uint32_t* sorted_ids, const uint32_t* pair_off, const uint32_t* sorted_tiles,
+               const ushort4* rect, const BinState* st, int n, int tiles_x, uint32_t* keys, uint32_t* vals,
+               cudaStream_t s) {
+    if (n > 0)
+        k_duplicate<<<blocks(n, 256), 256, 0, s>>>(sorted_ids, pair_off, sorted_tiles, rect, st, tiles_x, keys,
+                                                    vals);
+}
+
+int radix_blocks(long long n_pairs) { return std::max(blocks(n_pairs, kBlockTile), 1); }
+size_t radix_count_entries(long long n_pairs) { return (size_t)kRadixDigits * radix_blocks(n_pairs); }
+
+// Two stable byte passes (tx, then ty); the sorted pairs end back in (keys_a, vals_a).
+// counts/offsets: radix_count_entries() u32 each; scratch for the scan: entries/1024 + 1 u32.
+void tile_radix_sort(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32_t* vals_b, const BinState* st,
+                     long long n_pairs, int tiles_x, int n_tiles, uint32_t* counts, uint32_t* offsets,
+                     uint32_t* scratch, uint2* ranges, cudaStream_t s) {
+    const int nb = radix_blocks(n_pairs);
+    const int entries = kRadixDigits * nb;
+    uint32_t* kin = keys_a;
+    uint32_t* vin = vals_a;
+    uint32_t* kout = keys_b;
+    uint32_t* vout = vals_b;
+    for (int pass = 0; pass < 2; ++pass) {
+        const int shift = pass == 0 ? 0 : 8;
+        k_radix_hist<<<nb, kRadixThreads, 0, s>>>(kin, st, shift, nb, counts);
+        exclusive_scan(counts, entries, offsets, scratch, nullptr, s, nullptr);
+        k_radix_scatter<<<nb, kRadixThreads, 0, s>>>(kin, vin, st, shift, nb, offsets, kout, vout);
+        std::swap(kin, kout);
+        std::swap(vin, vout);
+    }
+    cudaMemsetAsync(ranges, 0, sizeof(uint2) * (size_t)n_tiles, s);
+    k_tile_ranges<<<std::max(blocks(n_pairs, 256), 1), 256, 0, s>>>(kin, st, tiles_x, ranges);
+}
+
+void check_capacity(BinState* st, cudaStream_t s) { k_check_capacity<<<1, 1, 0, s>>>(st); }
+
+bool binning_init() {
+    return cudaFuncSetAttribute(k_bucket_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kBigSmem * (int)sizeof(SortRec)) == cudaSuccess;
+}
+
+}  // namespace rgs_launch

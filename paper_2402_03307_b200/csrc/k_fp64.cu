@@ -35,21 +35,40 @@ __device__ __forceinline__ uint32_t d_tile_rect(double mx, double my, double r, 
     return (uint32_t)(x1 - x0 + 1) * (uint32_t)(y1 - y0 + 1);
 }
 
-// FP32 guard-band constants of one splat.
-__device__ __forceinline__ void d_guard(double ca, double cb, double cc, double ab, float* p_alpha, float* c_s,
-                                        float* p_clamp) {
-    *p_alpha = (float)log(kMinAlpha / ab);
-    *p_clamp = (float)log(kAlphaClamp / ab);
-    double kappa = fabs(cb) / sqrt(ca * cc);
+// FP32 blend record of one splat.
+// Everything is in log2 units so the blend evaluates p2 = log2(e) * power and
+// alpha = alpha_base * 2^p2 with one MUFU.EX2:
+//   conic_f = (ca2, cb2, cc2, ab),  p2 = ca2 dx^2 + cc2 dy^2 + cb2 dx dy
+//   color_f = (r, g, b, pa2),        pa2 = log2(1/(255 ab))   alpha gate: p2 < pa2
+//   guard_f = (cs2n, pc2),           pc2 = log2(0.99 / ab)    clamp gate: p2 <= pc2
+//   ext_f   = (ex, ey, gx2, gy2)     bbox half-extents of the alpha ellipse (per-warp
+//                                    culling) and max |dp2/dx|, |dp2/dy| inside it.
+// cs2n * q (q = ca2 dx^2 + cc2 dy^2 <= 0) bounds the FP32 rounding error of p2.
+constexpr double kLog2e = 1.4426950408889634;
+
+__device__ __forceinline__ void d_blend_record(const SplatArrays& out, int i, double ca, double cb, double cc,
+                                               double ab, double r, double g, double b, double s00, double s11) {
+    const double pa = log(kMinAlpha / ab);  // natural-log alpha threshold (<= 0)
+    const double kappa = fabs(cb) / sqrt(ca * cc);
     double cs = (kappa < 0.999) ? 1.5e-6 * (1 + kappa) / (1 - kappa) : 1e30;
     if (!(ca > 0) || !(cc > 0)) cs = 1e30;
-    *c_s = (float)cs;
+    const double L = fabs(pa) * 2;
+    const double ex = sqrt(L * fmax(s00, 0.0)) * (1 + 1e-3) + 1e-2;
+    const double ey = sqrt(L * fmax(s11, 0.0)) * (1 + 1e-3) + 1e-2;
+    const double gx = kLog2e * sqrt(L * fmax(ca, 0.0));
+    const double gy = kLog2e * sqrt(L * fmax(cc, 0.0));
+    out.conic_f[i] = make_float4((float)(-0.5 * kLog2e * ca), (float)(-kLog2e * cb), (float)(-0.5 * kLog2e * cc),
+                                 (float)ab);
+    out.color_f[i] = make_float4((float)r, (float)g, (float)b, (float)(kLog2e * pa));
+    out.guard_f[i] = make_float2((float)(-2.0 * cs), (float)log2(kAlphaClamp / ab));
+    out.ext_f[i] = make_float4(isfinite(ex) ? (float)ex : 3e38f, isfinite(ey) ? (float)ey : 3e38f, (float)gx,
+                               (float)gy);
 }
 
 __device__ __forceinline__ void store_splat(const SplatArrays& out, int i, double mx, double my, double ca,
                                             double cb, double cc, double ab, double r, double g, double b,
                                             double depth, double fx, double fy, double radius, int tiles_x,
-                                            int tiles_y, uint32_t* ntiles) {
+                                            int tiles_y, uint32_t* ntiles, double s00, double s11) {
     out.mean2[i] = make_double2(mx, my);
     out.conic_ab[i] = make_double4(ca, cb, cc, ab);
     out.color_depth[i] = make_double4(r, g, b, depth);
@@ -57,22 +76,31 @@ __device__ __forceinline__ void store_splat(const SplatArrays& out, int i, doubl
     ushort4 rect;
     *ntiles = d_tile_rect(mx, my, radius, tiles_x, tiles_y, &rect);
     out.rect[i] = rect;
-    float pa, cs, pc;
-    d_guard(ca, cb, cc, ab, &pa, &cs, &pc);
-    out.conic_f[i] = make_float4((float)ca, (float)cb, (float)cc, (float)ab);
-    out.color_f[i] = make_float4((float)r, (float)g, (float)b, pa);
-    out.guard_f[i] = make_float2(cs, pc);
+    d_blend_record(out, i, ca, cb, cc, ab, r, g, b, s00, s11);
 }
 
-__device__ __forceinline__ void count_valid(bool ok, int* n_valid) {
-    unsigned m = __ballot_sync(0xffffffffu, ok);
-    if ((threadIdx.x & 31) == 0 && m) atomicAdd(n_valid, __popc(m));
+// Warp-aggregated: count of valid splats and min / max depth key (bucket range).
+__device__ __forceinline__ void count_valid(bool ok, unsigned long long key, BinState* st) {
+    const unsigned m = __ballot_sync(0xffffffffu, ok);
+    if (!m) return;
+    unsigned long long lo = ok ? key : ~0ull, hi = ok ? key : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long a = __shfl_xor_sync(0xffffffffu, lo, o), b = __shfl_xor_sync(0xffffffffu, hi, o);
+        lo = a < lo ? a : lo;
+        hi = b > hi ? b : hi;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&st->n_valid, __popc(m));
+        atomicMin(&st->key_min, lo);
+        atomicMax(&st->key_max, hi);
+    }
 }
 
 // K1: slice + visibility gate + project + SH colour, one thread per Gaussian
 // (rasterizer.cpp:189-204, gaussian.cpp:32-47, rasterizer.cpp:215-276, sh.cpp:16-97).
 __global__ void __launch_bounds__(128) k_preprocess(ParamView P, int sh_degree, DevCamera cam, SplatArrays out,
-                                                    unsigned long long* err, int* n_valid) {
+                                                    BinState* st) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     bool ok = false;
     uint32_t ntiles = 0;
@@ -86,7 +114,7 @@ __global__ void __launch_bounds__(128) k_preprocess(ParamView P, int sh_degree, 
         SliceState s;
         const int rc = d_slice(mean4, ls, rot, cam.time, s);
         if (rc > 0) {
-            atomicMin(err, ((unsigned long long)i << 8) | (unsigned long long)rc);
+            atomicMin(&st->err, ((unsigned long long)i << 8) | (unsigned long long)rc);
         } else if (rc == 0) {
             const double dt = cam.time - mean4[3];
             ProjState o;
@@ -127,16 +155,15 @@ __global__ void __launch_bounds__(128) k_preprocess(ParamView P, int sh_degree, 
                 }
                 store_splat(out, i, o.mean2[0], o.mean2[1], o.conic[0], o.conic[1], o.conic[2], o.alpha_base,
                             col[0], col[1], col[2], o.p[2], flow[0], flow[1], o.radius, cam.tiles_x, cam.tiles_y,
-                            &ntiles);
+                            &ntiles, o.cov2[0], o.cov2[3]);
                 key = order_key(o.p[2]);
             }
         }
         out.valid[i] = ok ? 1 : 0;
         out.tiles[i] = ntiles;
         out.depth_key[i] = key;
-        out.depth_val[i] = (uint32_t)i;
     }
-    count_valid(ok, n_valid);
+    count_valid(ok, key, st);
 }
 
 // Host-provided splats (rasterize_forward, rasterizer.cpp:278-306).
@@ -152,21 +179,25 @@ struct HostSplat {
     int32_t pad;
 };
 
-__global__ void k_splats_from_host(const HostSplat* sp, int n, DevCamera cam, SplatArrays out, int* n_valid) {
+__global__ void k_splats_from_host(const HostSplat* sp, int n, DevCamera cam, SplatArrays out, BinState* st) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long key = 0;
     if (i < n) {
         const HostSplat s = sp[i];
         uint32_t ntiles = 0;
+        // screen covariance = conic^-1 (only its diagonal feeds the culling extents)
+        const double det = s.conic[0] * s.conic[2] - s.conic[1] * s.conic[1];
+        const double s00 = det > 0 ? s.conic[2] / det : 1e300, s11 = det > 0 ? s.conic[0] / det : 1e300;
         store_splat(out, i, s.mean2[0], s.mean2[1], s.conic[0], s.conic[1], s.conic[2], s.alpha_base, s.color[0],
                     s.color[1], s.color[2], s.depth, s.flow2[0], s.flow2[1], s.radius, cam.tiles_x, cam.tiles_y,
-                    &ntiles);
+                    &ntiles, s00, s11);
         out.valid[i] = 1;
         out.tiles[i] = ntiles;
-        out.depth_key[i] = order_key(s.depth);
-        out.depth_val[i] = (uint32_t)i;
+        key = order_key(s.depth);
+        out.depth_key[i] = key;
         out.source_index[i] = s.source_index;
     }
-    count_valid(i < n, n_valid);
+    count_valid(i < n, key, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -707,17 +738,16 @@ using namespace rgs_dev;
 static inline int blocks(long long n, int t) { return (int)((n + t - 1) / t); }
 
 void preprocess(const float* params, int n, int sh_degree, const DevCamera& cam, const SplatArrays& out,
-                unsigned long long* err_word, int* n_valid, cudaStream_t s) {
+                BinState* st, cudaStream_t s) {
     if (n <= 0) return;
     ParamView P{params, n};
-    k_preprocess<<<blocks(n, 128), 128, 0, s>>>(P, sh_degree, cam, out, err_word, n_valid);
+    k_preprocess<<<blocks(n, 128), 128, 0, s>>>(P, sh_degree, cam, out, st);
 }
 
-void splats_from_host(const void* splats, int n, const DevCamera& cam, const SplatArrays& out, int* n_valid,
+void splats_from_host(const void* splats, int n, const DevCamera& cam, const SplatArrays& out, BinState* st,
                       cudaStream_t s) {
     if (n <= 0) return;
-    k_splats_from_host<<<blocks(n, 128), 128, 0, s>>>(reinterpret_cast<const HostSplat*>(splats), n, cam, out,
-                                                       n_valid);
+    k_splats_from_host<<<blocks(n, 128), 128, 0, s>>>(reinterpret_cast<const HostSplat*>(splats), n, cam, out, st);
 }
 
 void mark_all_slow(int n_pixels, uint32_t* slow_list, int* slow_count, cudaStream_t s) {

@@ -1,0 +1,176 @@
+// Binning and bookkeeping kernels between preprocess and blend (duplicate-with-key,
+// tile ranges), records export, scene layout packing and the FP32 peak probe.
+#include "rgs_internal.cuh"
+
+namespace rgs_dev {
+
+// ---------------------------------------------------------------------------
+// Records export / scene layout.
+
+struct OutSplat {
+    double mean2[2];
+    double conic[3];
+    double depth;
+    double color[3];
+    double alpha_base;
+    double flow2[2];
+    double radius;
+    int32_t source_index;
+    int32_t pad;
+};
+
+__global__ void k_compact_index(const uint8_t* __restrict__ valid, const uint32_t* __restrict__ scan, int n,
+                                uint32_t* compact_ids) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && valid[i]) compact_ids[scan[i]] = (uint32_t)i;
+}
+
+__global__ void k_export_splats(SplatArrays sp, const uint32_t* __restrict__ ids, int n, OutSplat* out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const uint32_t i = ids[k];
+    OutSplat o;
+    const double2 m = sp.mean2[i];
+    const double4 c = sp.conic_ab[i];
+    const double4 cd = sp.color_depth[i];
+    const double4 fr = sp.flow_radius[i];
+    o.mean2[0] = m.x;
+    o.mean2[1] = m.y;
+    o.conic[0] = c.x;
+    o.conic[1] = c.y;
+    o.conic[2] = c.z;
+    o.alpha_base = c.w;
+    o.color[0] = cd.x;
+    o.color[1] = cd.y;
+    o.color[2] = cd.z;
+    o.depth = cd.w;
+    o.flow2[0] = fr.x;
+    o.flow2[1] = fr.y;
+    o.radius = fr.z;
+    o.source_index = sp.source_index ? sp.source_index[i] : (int32_t)i;
+    o.pad = 0;
+    out[k] = o;
+}
+
+__global__ void k_map_ids(const uint32_t* __restrict__ vals, long long n, const uint32_t* __restrict__ scan,
+                          int32_t* out) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = (int32_t)scan[vals[i]];
+}
+
+__global__ void k_valid_u32(const uint8_t* __restrict__ v, int n, uint32_t* out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = v[i];
+}
+
+// Host upload layout -> device SoA blocks (see rgs_scene_params).
+__global__ void k_scene_pack(const float* __restrict__ mean, const float* __restrict__ ls,
+                             const float* __restrict__ rot, const float* __restrict__ op,
+                             const float* __restrict__ sh, int n, float* P) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float4* pm = reinterpret_cast<float4*>(P);
+    float4* pl = reinterpret_cast<float4*>(P + 4 * (size_t)n);
+    float4* r0 = reinterpret_cast<float4*>(P + 8 * (size_t)n);
+    float4* r1 = reinterpret_cast<float4*>(P + 12 * (size_t)n);
+    pm[i] = make_float4(mean[4 * (size_t)i], mean[4 * (size_t)i + 1], mean[4 * (size_t)i + 2], mean[4 * (size_t)i + 3]);
+    pl[i] = make_float4(ls[4 * (size_t)i], ls[4 * (size_t)i + 1], ls[4 * (size_t)i + 2], ls[4 * (size_t)i + 3]);
+    const float* r = rot + 8 * (size_t)i;
+    r0[i] = make_float4(r[0], r[1], r[2], r[3]);
+    r1[i] = make_float4(r[4], r[5], r[6], r[7]);
+    const float* s = sh + 48 * (size_t)i;
+    float v[48];
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch)
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k * 3 + ch] = s[ch * 16 + k];
+#pragma unroll
+    for (int b = 0; b < 12; ++b)
+        reinterpret_cast<float4*>(P + (16 + 4 * (size_t)b) * n)[i] =
+            make_float4(v[4 * b], v[4 * b + 1], v[4 * b + 2], v[4 * b + 3]);
+    P[64 * (size_t)n + i] = op[i];
+}
+
+__global__ void k_scene_unpack(const float* __restrict__ P, int n, double* mean, double* ls, double* rot,
+                               double* op, double* sh) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float4 m = reinterpret_cast<const float4*>(P)[i];
+    const float4 l = reinterpret_cast<const float4*>(P + 4 * (size_t)n)[i];
+    const float4 a = reinterpret_cast<const float4*>(P + 8 * (size_t)n)[i];
+    const float4 b = reinterpret_cast<const float4*>(P + 12 * (size_t)n)[i];
+    double* pm = mean + 4 * (size_t)i;
+    pm[0] = m.x; pm[1] = m.y; pm[2] = m.z; pm[3] = m.w;
+    double* pl = ls + 4 * (size_t)i;
+    pl[0] = l.x; pl[1] = l.y; pl[2] = l.z; pl[3] = l.w;
+    double* pr = rot + 8 * (size_t)i;
+    pr[0] = a.x; pr[1] = a.y; pr[2] = a.z; pr[3] = a.w;
+    pr[4] = b.x; pr[5] = b.y; pr[6] = b.z; pr[7] = b.w;
+    op[i] = P[64 * (size_t)n + i];
+    for (int j = 0; j < 48; ++j) {
+        const int k = j / 3, ch = j % 3;
+        sh[48 * (size_t)i + ch * 16 + k] = P[(16 + 4 * (size_t)(j / 4)) * n + 4 * (size_t)i + (j % 4)];
+    }
+}
+
+}  // namespace rgs_dev
+
+namespace rgs_launch {
+using namespace rgs_dev;
+
+static inline int blocks(long long n, int t) { return (int)((n + t - 1) / t); }
+
+void compact_index(const uint8_t* valid, const uint32_t* scan, int n, uint32_t* compact_ids, cudaStream_t s) {
+    if (n > 0) k_compact_index<<<blocks(n, 256), 256, 0, s>>>(valid, scan, n, compact_ids);
+}
+
+void export_splats(const SplatArrays& sp, const uint32_t* compact_ids, int n_valid, void* out, cudaStream_t s) {
+    if (n_valid > 0)
+        k_export_splats<<<blocks(n_valid, 128), 128, 0, s>>>(sp, compact_ids, n_valid, reinterpret_cast<OutSplat*>(out));
+}
+
+void map_ids(const uint32_t* pair_vals, long long n_pairs, const uint32_t* scan, int32_t* out, cudaStream_t s) {
+    if (n_pairs > 0) k_map_ids<<<blocks(n_pairs, 256), 256, 0, s>>>(pair_vals, n_pairs, scan, out);
+}
+
+void valid_to_u32(const uint8_t* valid, int n, uint32_t* out, cudaStream_t s) {
+    if (n > 0) k_valid_u32<<<blocks(n, 256), 256, 0, s>>>(valid, n, out);
+}
+
+void scene_pack(const float* mean, const float* ls, const float* rot, const float* op, const float* sh, int n,
+                float* params, cudaStream_t s) {
+    if (n > 0) k_scene_pack<<<blocks(n, 128), 128, 0, s>>>(mean, ls, rot, op, sh, n, params);
+}
+
+void scene_unpack(const float* params, int n, double* mean, double* ls, double* rot, double* op, double* sh,
+                  cudaStream_t s) {
+    if (n > 0) k_scene_unpack<<<blocks(n, 128), 128, 0, s>>>(params, n, mean, ls, rot, op, sh);
+}
+
+}  // namespace rgs_launch
+
+// ---------------------------------------------------------------------------
+// FP32 FMA-pipe peak probe (roofline denominator for the blend kernels; the
+// driver's MEASURED_PEAKS.json has HBM and bf16 tensor peaks only).
+namespace rgs_dev {
+__global__ void __launch_bounds__(256) k_ffma_peak(float* out, int iters, float a, float b) {
+    float x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6,
+          x7 = x0 + 7;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            x0 = fmaf(x0, a, b); x1 = fmaf(x1, a, b); x2 = fmaf(x2, a, b); x3 = fmaf(x3, a, b);
+            x4 = fmaf(x4, a, b); x5 = fmaf(x5, a, b); x6 = fmaf(x6, a, b); x7 = fmaf(x7, a, b);
+        }
+    }
+    const float s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+    if (s == 1234.5f) out[0] = s;  // keep the chains live
+}
+}  // namespace rgs_dev
+namespace rgs_launch {
+// Returns the FMA count of the launch.
+double ffma_peak(float* out, int blocks, int iters, cudaStream_t s) {
+    rgs_dev::k_ffma_peak<<<blocks, 256, 0, s>>>(out, iters, 0.999999f, 1e-6f);
+    return (double)blocks * 256.0 * iters * 16.0 * 8.0;
+}
+}  // namespace rgs_launch

@@ -1,0 +1,375 @@
+// FP32 tile kernels: K5 forward blend and K6 backward replay
+// (rasterizer.cpp:97-122 and 437-468).
+//
+// Every (pixel, splat) evaluation is done in FP32 together with a bound on its error
+// against the FP64 reference.  A gate decision (power > 0, alpha < 1/255,
+// T(1-alpha) < 1e-4, and the backward's unclamped alpha <= 0.99) whose FP32 value
+// lies inside the bound marks the pixel "slow": the thread stops and k_blend_fp64
+// (k_fp64.cu) recomputes the whole pixel in FP64.  Every decision the FP32 path keeps
+// is therefore the FP64 decision, and K6 replays exactly those.
+//
+// Layout: one CTA per 16x16 tile, one thread per pixel, each warp owns an 8x4
+// sub-tile.  Splats are staged 256 at a time in shared memory; each warp first culls
+// the staged splats against its sub-tile with the bounding box of the alpha >= 1/255
+// ellipse (a ballot per 32 splats) and then walks only the surviving ones, in depth
+// order.  The exponent is kept in log2 units so alpha costs one MUFU.EX2.
+#include "rgs_internal.cuh"
+
+namespace rgs_dev {
+
+// One staged splat of a tile batch (64 B).
+struct StagedSplat {
+    float4 a;  // (mx, my, ca2, cb2)   mean relative to the tile origin
+    float4 b;  // (cc2, D, pa2, cs2n)  D: error floor incl. the mean's FP32 rounding
+    float4 c;  // (r, g, b, alpha_base)   flow: (fx, fy, 0, alpha_base)
+    float4 d;  // (ex, ey, pc2, 0)     culling extents, clamp-gate power
+};
+
+template <bool FLOW>
+__device__ __forceinline__ void stage(const SplatArrays& sp, uint32_t id, double px0, double py0, StagedSplat* dst) {
+    const double2 m = sp.mean2[id];
+    const float mx = (float)(m.x - px0), my = (float)(m.y - py0);
+    const float4 cf = sp.conic_f[id];
+    const float4 col = sp.color_f[id];
+    const float2 g = sp.guard_f[id];
+    const float4 e = sp.ext_f[id];
+    const float D = 1.5e-6f + 1.2e-7f * (fabsf(mx) * e.z + fabsf(my) * e.w);
+    dst->a = make_float4(mx, my, cf.x, cf.y);
+    dst->b = make_float4(cf.z, D, col.w, g.x);
+    if (FLOW) {
+        const double4 f = sp.flow_radius[id];
+        dst->c = make_float4((float)f.x, (float)f.y, 0.f, cf.w);
+    } else {
+        dst->c = make_float4(col.x, col.y, col.z, cf.w);
+    }
+    dst->d = make_float4(e.x, e.y, g.y, 0.f);
+}
+
+__device__ __forceinline__ bool overlaps(const StagedSplat& s, float sx0, float sy0) {
+    return (s.a.x + s.d.x >= sx0) && (s.a.x - s.d.x <= sx0 + 7.f) && (s.a.y + s.d.y >= sy0) &&
+           (s.a.y - s.d.y <= sy0 + 3.f);
+}
+
+enum { kSkip = 0, kAccept = 1, kAmbiguous = 2 };
+
+// Gate classification shared by K5 and K6: explicit-rounding intrinsics, so both
+// kernels compute bit-identical p2 / M and take identical decisions.
+__device__ __forceinline__ int classify(const float4& a, const float4& b, float fpx, float fpy, float& p, float& M,
+                                        float& dx, float& dy) {
+    dx = __fsub_rn(fpx, a.x);
+    dy = __fsub_rn(fpy, a.y);
+    const float t = __fmul_rn(a.z, dx), u = __fmul_rn(b.x, dy), v = __fmul_rn(a.w, dx);
+    const float q = __fmaf_rn(t, dx, __fmul_rn(u, dy));  // ca2 dx^2 + cc2 dy^2  (<= 0)
+    p = __fmaf_rn(v, dy, q);                             // log2(e) * power
+    M = __fmaf_rn(b.w, q, b.y);                          // error bound of p
+    if (__fadd_rn(p, M) < b.z) return kSkip;             // alpha < 1/255 for certain
+    if (p > -M) return (p > M) ? kSkip : kAmbiguous;     // power > 0 gate
+    if (__fsub_rn(p, M) <= b.z) return kAmbiguous;       // alpha gate within the bound
+    return kAccept;
+}
+
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// alpha = min(0.99, ab 2^p2), identical in K5 and K6.
+__device__ __forceinline__ float blend_alpha(float ab, float p) { return fminf(0.99f, __fmul_rn(ab, ex2_approx(p))); }
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// K5: forward blend.
+template <bool FLOW, bool COUNT>
+__global__ void __launch_bounds__(256) k_blend_fp32(SplatArrays sp, const uint32_t* __restrict__ vals,
+                                                    const uint2* __restrict__ ranges, DevCamera cam, float3 bg,
+                                                    float* __restrict__ image, double* __restrict__ final_T,
+                                                    uint32_t* __restrict__ n_contrib, uint32_t* slow_list,
+                                                    int* slow_count, unsigned long long* counters) {
+    __shared__ StagedSplat sm[kTilePixels];
+    const int tile = blockIdx.x;
+    const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sx0 = (warp & 1) * 8, sy0 = (warp >> 1) * 4;
+    const int lx = sx0 + (lane & 7), ly = sy0 + (lane >> 3);
+    const int px = tx * kTile + lx, py = ty * kTile + ly;
+    const bool inside = px < cam.width && py < cam.height;
+    const uint2 rg = ranges[tile];
+    const double px0 = tx * kTile, py0 = ty * kTile;
+    const float fpx = (float)lx, fpy = (float)ly, fsx0 = (float)sx0, fsy0 = (float)sy0;
+
+    float T = 1.f, errT = 0.f, acc0 = 0.f, acc1 = 0.f, acc2 = 0.f;
+    int contrib = 0;
+    bool done = !inside, slow = false, stopped = false;
+    uint32_t n_eval = 0, n_blend = 0, n_ref = 0;  // COUNT only
+    bool warp_done = __all_sync(kFull, done);
+
+    for (uint32_t start = rg.x; start < rg.y; start += kTilePixels) {
+        if (__syncthreads_count(done) == kTilePixels) break;
+        const uint32_t j = start + threadIdx.x;
+        if (j < rg.y) stage<FLOW>(sp, vals[j], px0, py0, &sm[threadIdx.x]);
+        __syncthreads();
+        const int n = (int)min((uint32_t)kTilePixels, rg.y - start);
+        if (warp_done) continue;
+        for (int c = 0; c < n; c += 32) {
+            const int k0 = c + lane;
+            unsigned mask = __ballot_sync(kFull, k0 < n && overlaps(sm[k0], fsx0, fsy0));
+            while (mask) {
+                const int k = c + __ffs(mask) - 1;
+                mask &= mask - 1;
+                if (done) continue;
+                const float4 a = sm[k].a, b = sm[k].b;
+                float p, M, dx, dy;
+                const int g = classify(a, b, fpx, fpy, p, M, dx, dy);
+                if (COUNT) ++n_eval;
+                if (g == kSkip) continue;
+                if (g == kAmbiguous) {
+                    slow = done = true;
+                    continue;
+                }
+                const float4 cc = sm[k].c;
+                const float pc = sm[k].d.z;
+                const float al = blend_alpha(cc.w, p);
+                // backward's clamp gate: unclamped alpha <= 0.99 (rasterizer.cpp:356)
+                if (__fadd_rn(p, M) >= pc && __fsub_rn(p, M) <= pc) {
+                    slow = done = true;
+                    continue;
+                }
+                const float om = __fsub_rn(1.f, al);
+                const float test_T = __fmul_rn(T, om);
+                const float errN = fmaf(al * M, rcp_approx(om), errT + 3e-7f);
+                if (fabsf(test_T - 1e-4f) <= test_T * errN) {
+                    slow = done = true;
+                    continue;
+                }
+                if (test_T < 1e-4f) {  // rasterizer.cpp:111: the splat is not blended
+                    done = stopped = true;
+                    if (COUNT) n_ref = start - rg.x + k + 1;
+                    continue;
+                }
+                const float w = al * T;
+                acc0 = fmaf(cc.x, w, acc0);
+                acc1 = fmaf(cc.y, w, acc1);
+                acc2 = fmaf(cc.z, w, acc2);
+                T = test_T;
+                errT = errN;
+                contrib = (int)(start - rg.x) + k + 1;
+                if (COUNT) ++n_blend;
+            }
+            if (__all_sync(kFull, done)) {
+                warp_done = true;
+                break;
+            }
+        }
+    }
+    if (COUNT) {
+        // E of the roofline = evaluations of the reference algorithm (every list entry up
+        // to the termination point); n_eval = the ones this kernel actually evaluated.
+        unsigned long long e = inside ? (stopped ? n_ref : rg.y - rg.x) : 0, b = n_blend, ke = n_eval;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            e += __shfl_xor_sync(kFull, e, o);
+            b += __shfl_xor_sync(kFull, b, o);
+            ke += __shfl_xor_sync(kFull, ke, o);
+        }
+        if (lane == 0) {
+            atomicAdd(counters + 0, e);
+            atomicAdd(counters + 1, b);
+            atomicAdd(counters + 2, ke);
+        }
+    }
+    if (!inside) return;
+    const uint32_t pix = (uint32_t)py * cam.width + px;
+    if (slow) {
+        slow_list[atomicAdd(slow_count, 1)] = pix;
+        return;
+    }
+    if (FLOW) {
+        image[(size_t)pix * 2 + 0] = acc0;
+        image[(size_t)pix * 2 + 1] = acc1;
+    } else {
+        image[(size_t)pix * 3 + 0] = fmaf(T, bg.x, acc0);
+        image[(size_t)pix * 3 + 1] = fmaf(T, bg.y, acc1);
+        image[(size_t)pix * 3 + 2] = fmaf(T, bg.z, acc2);
+        final_T[pix] = (double)T;
+        n_contrib[pix] = (uint32_t)contrib;
+    }
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    return v;
+}
+
+// K6: back-to-front replay of the FP32 pixels (rasterizer.cpp:437-468).  Per-splat
+// partial sums are warp-reduced, combined in shared memory and scattered with one
+// FP64 atomic per (tile, splat, component).  Slow pixels are replayed in FP64 by
+// k_backward_fp64.
+__global__ void __launch_bounds__(256) k_backward_fp32(SplatArrays sp, const uint32_t* __restrict__ vals,
+                                                       const uint2* __restrict__ ranges, DevCamera cam, float3 bg,
+                                                       const double* __restrict__ final_T,
+                                                       const uint32_t* __restrict__ n_contrib,
+                                                       const float* __restrict__ dL, double* sg) {
+    __shared__ StagedSplat sm[kTilePixels];
+    __shared__ uint32_t sid[kTilePixels];
+    __shared__ float acc[9][kTilePixels];
+    __shared__ int s_max;
+    const int tile = blockIdx.x;
+    const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sx0 = (warp & 1) * 8, sy0 = (warp >> 1) * 4;
+    const int lx = sx0 + (lane & 7), ly = sy0 + (lane >> 3);
+    const int px = tx * kTile + lx, py = ty * kTile + ly;
+    const bool inside = px < cam.width && py < cam.height;
+    const uint2 rg = ranges[tile];
+    const double px0 = tx * kTile, py0 = ty * kTile;
+    const float fpx = (float)lx, fpy = (float)ly, fsx0 = (float)sx0, fsy0 = (float)sy0;
+    constexpr float kLn2 = 0.69314718055994531f;
+
+    int contrib = 0;
+    float T_run = 1.f, g0 = 0.f, g1 = 0.f, g2 = 0.f, s0 = 0.f, s1 = 0.f, s2 = 0.f;
+    if (threadIdx.x == 0) s_max = 0;
+    if (inside) {
+        const uint32_t pix = (uint32_t)py * cam.width + px;
+        const uint32_t c = n_contrib[pix];
+        if (!(c & kSlowBit)) {
+            contrib = (int)c;
+            const float fT = (float)final_T[pix];
+            T_run = fT;
+            g0 = dL[(size_t)pix * 3 + 0];
+            g1 = dL[(size_t)pix * 3 + 1];
+            g2 = dL[(size_t)pix * 3 + 2];
+            s0 = bg.x * fT;
+            s1 = bg.y * fT;
+            s2 = bg.z * fT;
+        }
+    }
+    __syncthreads();
+    const int wmax = __reduce_max_sync(kFull, contrib);
+    if (lane == 0 && wmax > 0) atomicMax(&s_max, wmax);
+    __syncthreads();
+    const int max_contrib = s_max;
+
+    for (int end = max_contrib; end > 0; end -= kTilePixels) {
+        const int beg = end > kTilePixels ? end - kTilePixels : 0;
+        const int cnt = end - beg;
+        if ((int)threadIdx.x < cnt) {
+            const uint32_t id = vals[rg.x + beg + threadIdx.x];
+            sid[threadIdx.x] = id;
+            stage<false>(sp, id, px0, py0, &sm[threadIdx.x]);
+        }
+#pragma unroll
+        for (int q = 0; q < 9; ++q) acc[q][threadIdx.x] = 0.f;
+        __syncthreads();
+        for (int c = ((cnt - 1) >> 5) << 5; c >= 0; c -= 32) {
+            const int k0 = c + lane;
+            unsigned mask =
+                __ballot_sync(kFull, k0 < cnt && beg + k0 < wmax && overlaps(sm[k0], fsx0, fsy0));
+            while (mask) {
+                const int j = 31 - __clz(mask);
+                mask &= ~(1u << j);
+                const int k = c + j;
+                float v[9];
+#pragma unroll
+                for (int q = 0; q < 9; ++q) v[q] = 0.f;
+                bool act = false;
+                if (beg + k < contrib) {
+                    const float4 a = sm[k].a, b = sm[k].b;
+                    float p, M, dx, dy;
+                    // Non-slow pixels: every kept decision was certain in K5; an ambiguous
+                    // value here means K5 culled the pair, whose FP64 decision is "skip".
+                    if (classify(a, b, fpx, fpy, p, M, dx, dy) == kAccept) {
+                        const float4 cc = sm[k].c;
+                        const float al = blend_alpha(cc.w, p);
+                        const float om = 1.f - al;
+                        const float T_before = T_run / om;
+                        const float w = al * T_before;
+                        v[0] = w * g0;
+                        v[1] = w * g1;
+                        v[2] = w * g2;
+                        const float dL_da = g0 * (cc.x * T_before - s0 / om) + g1 * (cc.y * T_before - s1 / om) +
+                                            g2 * (cc.z * T_before - s2 / om);
+                        if (p <= sm[k].d.z) {  // unclamped alpha <= 0.99
+                            const float A = -2.f * kLn2 * a.z, B = -kLn2 * a.w, C = -2.f * kLn2 * b.x;
+                            v[8] = dL_da * (al / cc.w);
+                            const float dp = dL_da * al;
+                            v[3] = dp * (-0.5f * dx * dx);
+                            v[4] = dp * (-dx * dy);
+                            v[5] = dp * (-0.5f * dy * dy);
+                            v[6] = dp * (A * dx + B * dy);
+                            v[7] = dp * (B * dx + C * dy);
+                        }
+                        s0 = fmaf(cc.x, w, s0);
+                        s1 = fmaf(cc.y, w, s1);
+                        s2 = fmaf(cc.z, w, s2);
+                        T_run = T_before;
+                        act = true;
+                    }
+                }
+                const unsigned am = __ballot_sync(kFull, act);
+                if (am == 0) continue;
+                if (__popc(am) == 1) {
+                    if (act) {
+#pragma unroll
+                        for (int q = 0; q < 9; ++q)
+                            if (v[q] != 0.f) atomicAdd(&acc[q][k], v[q]);
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 9; ++q) v[q] = warp_sum(v[q]);
+                    if (lane == 0) {
+#pragma unroll
+                        for (int q = 0; q < 9; ++q)
+                            if (v[q] != 0.f) atomicAdd(&acc[q][k], v[q]);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        if ((int)threadIdx.x < cnt) {
+            double* o = sg + (size_t)sid[threadIdx.x] * 9;
+#pragma unroll
+            for (int q = 0; q < 9; ++q) {
+                const float val = acc[q][threadIdx.x];
+                if (val != 0.f) atomicAdd(o + q, (double)val);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace rgs_dev
+
+namespace rgs_launch {
+using namespace rgs_dev;
+
+void blend_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges, const DevCamera& cam,
+                float3 bg, int flow_mode, float* image, double* final_T, uint32_t* n_contrib, uint32_t* slow_list,
+                int* slow_count, unsigned long long* counters, cudaStream_t s) {
+    const int tiles = cam.tiles_x * cam.tiles_y;
+    if (flow_mode)
+        k_blend_fp32<true, false><<<tiles, kTilePixels, 0, s>>>(sp, pair_vals, ranges, cam, bg, image, final_T,
+                                                                 n_contrib, slow_list, slow_count, counters);
+    else if (counters)
+        k_blend_fp32<false, true><<<tiles, kTilePixels, 0, s>>>(sp, pair_vals, ranges, cam, bg, image, final_T,
+                                                                 n_contrib, slow_list, slow_count, counters);
+    else
+        k_blend_fp32<false, false><<<tiles, kTilePixels, 0, s>>>(sp, pair_vals, ranges, cam, bg, image, final_T,
+                                                                  n_contrib, slow_list, slow_count, counters);
+}
+
+void backward_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges, const DevCamera& cam,
+                   float3 bg, const double* final_T, const uint32_t* n_contrib, const float* dL_dimage,
+                   double* screen_grads, cudaStream_t s) {
+    const int tiles = cam.tiles_x * cam.tiles_y;
+    k_backward_fp32<<<tiles, kTilePixels, 0, s>>>(sp, pair_vals, ranges, cam, bg, final_T, n_contrib, dL_dimage,
+                                                  screen_grads);
+}
+
+}  // namespace rgs_launch

@@ -16,7 +16,6 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
-#include <cub/cub.cuh>
 #include <string>
 #include <vector>
 
@@ -61,39 +60,25 @@ struct DevBuf {
     }
 };
 
-struct DevStats {
-    unsigned long long err;
-    long long n_pairs;
-    int n_valid;
-    int slow_count;
-};
-
-__global__ void k_finish_counts(const uint32_t* offsets, const uint32_t* counts, int n, DevStats* st) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) st->n_pairs = n > 0 ? (long long)offsets[n - 1] + counts[n - 1] : 0;
-}
-
-int bits_for(long long v) {
-    int b = 1;
-    while ((1ll << b) < v) ++b;
-    return b;
-}
-
 // All per-view device state (one set per render in flight / per retained record).
 struct Frame {
-    // per Gaussian
-    DevBuf valid, tiles, mean2, conic_ab, color_depth, flow_radius, rect, conic_f, color_f, guard_f, src;
-    DevBuf dkey[2], dval[2], counts, offsets;
-    // pairs
-    DevBuf tkey[2], pval[2];
-    // tiles / pixels
-    DevBuf ranges, final_T, n_contrib, slow_list;
-    DevBuf stats;  // DevStats
-    DevBuf cub_tmp;
+    // per Gaussian / input splat
+    DevBuf valid, tiles, mean2, conic_ab, color_depth, flow_radius, rect, conic_f, color_f, guard_f, ext_f, src, key;
+    DevBuf ent_key, ent_id, sorted_ids, sorted_tiles, pair_off;
+    // depth buckets
+    DevBuf bucket_count, bucket_off, bucket_cur, big_list, big_scratch;
+    // tiles / pairs / pixels: pairs ping-pong between (keys_a, pair_vals_buf) and (keys_b, vals_b)
+    DevBuf ranges, keys_a, pair_vals_buf, keys_b, vals_b, radix_counts, radix_offsets;
+    DevBuf final_T, n_contrib, slow_list;
+    DevBuf stats;  // BinState
+    DevBuf scan_tmp;
+    DevBuf tmp_img;                    // image target when the caller passes none
+    BinState* host_stats = nullptr;    // pinned copy of `stats`
+    long long pair_cap = 0;            // capacity of the pair buffers (0: not learned yet)
     // results
     int n = 0, n_valid = 0;
     long long n_pairs = 0;
     int width = 0, height = 0, tiles_x = 0, tiles_y = 0;
-    int pairs_sel = 0;  // which pval buffer holds the sorted values
     bool have_src = false;
     double bg[3] = {0, 0, 0};
 
@@ -109,13 +94,13 @@ struct Frame {
         a.conic_f = conic_f.as<float4>();
         a.color_f = color_f.as<float4>();
         a.guard_f = guard_f.as<float2>();
+        a.ext_f = ext_f.as<float4>();
         a.source_index = have_src ? src.as<int32_t>() : nullptr;
-        a.depth_key = dkey[0].as<unsigned long long>();
-        a.depth_val = dval[0].as<uint32_t>();
+        a.depth_key = key.as<unsigned long long>();
         return a;
     }
-    const uint32_t* pair_vals() const { return pval[pairs_sel].as<uint32_t>(); }
-    DevStats* dstats() const { return stats.as<DevStats>(); }
+    const uint32_t* pair_vals() const { return pair_vals_buf.as<uint32_t>(); }
+    BinState* dstats() const { return stats.as<BinState>(); }
 
     void ensure_gaussians(int cap, cudaStream_t s) {
         size_t n1 = std::max(cap, 1);
@@ -129,33 +114,54 @@ struct Frame {
         conic_f.ensure(16 * n1, s);
         color_f.ensure(16 * n1, s);
         guard_f.ensure(8 * n1, s);
-        for (int k = 0; k < 2; ++k) {
-            dkey[k].ensure(8 * n1, s);
-            dval[k].ensure(4 * n1, s);
-        }
-        counts.ensure(4 * n1, s);
-        offsets.ensure(4 * n1, s);
-        stats.ensure(sizeof(DevStats), s);
+        ext_f.ensure(16 * n1, s);
+        key.ensure(8 * n1, s);
+        ent_key.ensure(8 * n1, s);
+        ent_id.ensure(4 * n1, s);
+        sorted_ids.ensure(4 * n1, s);
+        sorted_tiles.ensure(4 * n1, s);
+        pair_off.ensure(4 * n1, s);
+        big_scratch.ensure(16 * 2 * n1, s);
+        const size_t nb = (size_t)rgs_launch::num_depth_buckets();
+        bucket_count.ensure(4 * nb, s);
+        bucket_off.ensure(4 * nb, s);
+        bucket_cur.ensure(4 * nb, s);
+        big_list.ensure(4 * nb, s);
+        stats.ensure(sizeof(BinState), s);
+        scan_tmp.ensure(4 * 4096, s);
+        if (!host_stats) CK(cudaMallocHost(&host_stats, sizeof(BinState)));
     }
     void ensure_pixels(size_t npix, int ntiles, cudaStream_t s) {
         final_T.ensure(8 * std::max<size_t>(npix, 1), s);
         n_contrib.ensure(4 * std::max<size_t>(npix, 1), s);
         slow_list.ensure(4 * std::max<size_t>(npix, 1), s);
-        ranges.ensure(8 * (size_t)std::max(ntiles, 1), s);
+        const size_t nt = (size_t)std::max(ntiles, 1) + 1;
+        ranges.ensure(8 * nt, s);
     }
     void ensure_pairs(long long p, cudaStream_t s) {
         size_t p1 = (size_t)std::max<long long>(p, 1);
-        for (int k = 0; k < 2; ++k) {
-            tkey[k].ensure(4 * p1, s);
-            pval[k].ensure(4 * p1, s);
-        }
+        keys_a.ensure(4 * p1, s);
+        pair_vals_buf.ensure(4 * p1, s);
+        keys_b.ensure(4 * p1, s);
+        vals_b.ensure(4 * p1, s);
+        const size_t e = rgs_launch::radix_count_entries(p);
+        radix_counts.ensure(4 * e, s);
+        radix_offsets.ensure(4 * e, s);
+        scan_tmp.ensure(4 * (e / 1024 + 4096), s);
     }
     void release(cudaStream_t s) {
         DevBuf* all[] = {&valid, &tiles, &mean2, &conic_ab, &color_depth, &flow_radius, &rect, &conic_f,
-                         &color_f, &guard_f, &src, &dkey[0], &dkey[1], &dval[0], &dval[1], &counts,
-                         &offsets, &tkey[0], &tkey[1], &pval[0], &pval[1], &ranges, &final_T, &n_contrib,
-                         &slow_list, &stats, &cub_tmp};
+                         &color_f, &guard_f, &ext_f, &src, &key, &ent_key, &ent_id, &sorted_ids, &sorted_tiles,
+                         &pair_off, &bucket_count, &bucket_off, &bucket_cur, &big_list, &big_scratch, &ranges,
+                         &keys_a, &pair_vals_buf, &keys_b, &vals_b, &radix_counts, &radix_offsets, &final_T,
+                         &n_contrib, &slow_list, &stats, &scan_tmp, &tmp_img};
         for (DevBuf* b : all) b->release(s);
+        if (host_stats) {
+            cudaStreamSynchronize(s);
+            cudaFreeHost(host_stats);
+            host_stats = nullptr;
+        }
+        pair_cap = 0;
     }
 };
 
@@ -163,12 +169,12 @@ struct Frame {
 
 // Pipeline stages timed by the profiling mode (rgs_ctx_set_profiling).
 enum Stage {
-    kStPreprocess = 0, kStDepthSort, kStCounts, kStDuplicate, kStTileSort, kStRanges, kStBlend, kStFixup,
-    kStBwdTiles, kStBwdFixup, kStBwdGauss, kNumStages
+    kStPreprocess = 0, kStDepthRank, kStHist, kStTileFill, kStTileSort, kStBlend, kStFixup, kStBwdTiles,
+    kStBwdFixup, kStBwdGauss, kNumStages
 };
 static const char* kStageNames[kNumStages] = {
-    "preprocess_k1", "depth_sort", "pair_counts_scan", "duplicate_k3", "tile_sort_k4", "tile_ranges",
-    "blend_fp32_k5", "blend_fp64_fixup", "backward_tiles_k6", "backward_fp64_fixup", "backward_gauss_k7"};
+    "preprocess_k1", "depth_rank", "pair_offsets_scan", "duplicate_k3", "tile_radix_sort_k4", "blend_fp32_k5",
+    "blend_fp64_fixup", "backward_tiles_k6", "backward_fp64_fixup", "backward_gauss_k7"};
 
 struct rgs_ctx {
     int device = 0;
@@ -182,7 +188,7 @@ struct rgs_ctx {
     DevBuf sgrad;     // N x 9 doubles (screen-space gradients)
     DevBuf tmp_img;   // host-buffer staging
     DevBuf tmp_splats, tmp_scan, tmp_ids;
-    DevStats* host_stats = nullptr;  // pinned
+    BinState* host_stats = nullptr;  // pinned
     // profiling: CUDA events around every stage, on the launching stream
     bool timing = false;
     bool count_evals = false;
@@ -195,7 +201,21 @@ struct rgs_ctx {
     std::vector<Pending> pending;
     double stage_ms[kNumStages] = {0};
     long long stage_n[kNumStages] = {0};
-    DevBuf counters;  // 2 x u64: evaluated / blended (pixel, splat) pairs
+    DevBuf counters;  // 3 x u64: E, B, E_kernel of the FP32 blend
+    // multi-view batches (render_batch)
+    static constexpr int kSlots = 3;
+    Frame slot_frame[kSlots];
+    cudaStream_t slot_stream[kSlots] = {};
+    cudaEvent_t slot_done[kSlots] = {};
+    cudaEvent_t join_ev = nullptr;
+    BinState* view_stats = nullptr;  // pinned, one per view of the current batch
+    size_t view_stats_cap = 0;
+    void ensure_view_stats(size_t n) {
+        if (n <= view_stats_cap) return;
+        if (view_stats) cudaFreeHost(view_stats);
+        CK(cudaMallocHost(&view_stats, sizeof(BinState) * n));
+        view_stats_cap = n;
+    }
     cudaEvent_t next_event() {
         if (ev_used == ev_pool.size()) {
             cudaEvent_t e;
@@ -206,9 +226,9 @@ struct rgs_ctx {
     }
     void collect() {
         if (pending.empty()) return;
-        CK(cudaStreamSynchronize(stream));
         for (const Pending& p : pending) {
             float ms = 0;
+            CK(cudaEventSynchronize(p.b));
             CK(cudaEventElapsedTime(&ms, p.a, p.b));
             stage_ms[p.stage] += ms;
             stage_n[p.stage] += 1;
@@ -223,17 +243,18 @@ namespace {
 struct StageTimer {
     rgs_ctx* c;
     int stage;
+    cudaStream_t s;
     cudaEvent_t a = nullptr;
-    StageTimer(rgs_ctx* ctx, int st) : c(ctx), stage(st) {
+    StageTimer(rgs_ctx* ctx, int st, cudaStream_t stream) : c(ctx), stage(st), s(stream) {
         if (c->timing) {
             a = c->next_event();
-            CK(cudaEventRecord(a, c->stream));
+            CK(cudaEventRecord(a, s));
         }
     }
     ~StageTimer() {
         if (c->timing && a) {
             cudaEvent_t b = c->next_event();
-            cudaEventRecord(b, c->stream);
+            cudaEventRecord(b, s);
             c->pending.push_back({stage, a, b});
         }
     }
@@ -315,19 +336,24 @@ const char* rotor_msg(int code) {
 
 enum Source { kFromScene, kFromSplats };
 }  // namespace
-void rgs_gather_keys(const unsigned long long* keys, const uint32_t* ids, int n, unsigned long long* out,
-                     uint32_t* out_ids, cudaStream_t s);
 namespace {
 
-// Runs the forward pipeline into `f`.  image may be null (records only).
-int run_forward(rgs_ctx* ctx, Frame& f, Source src, const rgs_scene* scene, const void* dev_splats, int n_splats,
-                bool splats_monotone, const rgs_camera* cam, const double bg[3], unsigned flags, float* image,
-                bool flow_mode) {
-    cudaStream_t s = ctx->stream;
+// Enqueues the forward pipeline of one view into frame `f` on stream `s`.
+//
+// No host synchronisation in the steady state: the pair buffers have a capacity
+// (learned from the first view, grown on demand); a view whose pair count exceeds it
+// sets BinState::overflow, skips the pair work, and is re-rendered after a sync.  The
+// view's BinState is copied asynchronously to `host_stats`.  With `sync` the view is
+// resolved before returning (errors reported, overflow re-rendered).
+int run_forward(rgs_ctx* ctx, Frame& f, cudaStream_t s, Source src, const rgs_scene* scene, const void* dev_splats,
+                int n_splats, bool splats_monotone, const rgs_camera* cam, const double bg[3], unsigned flags,
+                float* image, bool flow_mode, bool sync, BinState* host_stats) {
     const DevCamera dc = make_dev_camera(cam);
     const int n = src == kFromScene ? scene->n : n_splats;
     const size_t npix = (size_t)cam->width * cam->height;
     const int ntiles = dc.tiles_x * dc.tiles_y;
+    if (dc.tiles_x > 256 || dc.tiles_y > 256)
+        return set_err(ctx, RGS_E_INVALID, "image too large: at most 4096x4096 pixels (256x256 tiles)");
     f.n = n;
     f.width = cam->width;
     f.height = cam->height;
@@ -340,135 +366,124 @@ int run_forward(rgs_ctx* ctx, Frame& f, Source src, const rgs_scene* scene, cons
         f.src.ensure(4 * (size_t)std::max(n, 1), s);
         f.have_src = true;
     }
-    DevStats init{kNoError, 0, 0, 0};
+    BinState init;
+    std::memset(&init, 0, sizeof init);
+    init.err = kNoError;
+    init.key_min = ~0ull;
+    init.pair_cap = (uint32_t)std::min<long long>(f.pair_cap, 0xffffffffll);
     CK(cudaMemcpyAsync(f.dstats(), &init, sizeof init, cudaMemcpyHostToDevice, s));
+    const int nb = rgs_launch::num_depth_buckets();
+    CK(cudaMemsetAsync(f.bucket_count.p, 0, 4 * (size_t)nb, s));
+    CK(cudaMemsetAsync(f.bucket_cur.p, 0, 4 * (size_t)nb, s));
     SplatArrays sa = f.arrays();
+    BinState* st_dev = f.dstats();
 
-    // K1
+    // K1: slice + project + SH (or host splats), depth keys, key range.
     {
-        StageTimer t(ctx, kStPreprocess);
+        StageTimer t(ctx, kStPreprocess, s);
         if (src == kFromScene)
-            rgs_launch::preprocess(scene->params, n, scene->sh_degree, dc, sa, &f.dstats()->err,
-                                   &f.dstats()->n_valid, s);
+            rgs_launch::preprocess(scene->params, n, scene->sh_degree, dc, sa, st_dev, s);
         else
-            rgs_launch::splats_from_host(dev_splats, n, dc, sa, &f.dstats()->n_valid, s);
+            rgs_launch::splats_from_host(dev_splats, n, dc, sa, st_dev, s);
         ctx->launches += 1;
     }
+    // Global (depth, index) ranks: depth-bucket histogram + scan, scatter, per-bucket sorts.
+    uint32_t* scan_tmp = f.scan_tmp.as<uint32_t>();
+    {
+        StageTimer t(ctx, kStDepthRank, s);
+        rgs_launch::bucket_hist(sa.valid, sa.depth_key, n, st_dev, f.bucket_count.as<uint32_t>(), s);
+        rgs_launch::exclusive_scan(f.bucket_count.as<uint32_t>(), nb, f.bucket_off.as<uint32_t>(), scan_tmp + 2048,
+                                   nullptr, s);
+        rgs_launch::depth_ranks(sa.valid, sa.depth_key, sa.tiles, n,
+                                (src == kFromSplats && !splats_monotone) ? sa.source_index : nullptr, st_dev,
+                                f.bucket_count.as<uint32_t>(), f.bucket_off.as<uint32_t>(),
+                                f.bucket_cur.as<uint32_t>(), f.ent_key.as<unsigned long long>(),
+                                f.ent_id.as<uint32_t>(), f.sorted_ids.as<uint32_t>(), f.sorted_tiles.as<uint32_t>(),
+                                f.big_list.as<uint32_t>(), f.big_scratch.p, s);
+        ctx->launches += 8;
+    }
+    // Pair offsets in rank order (exclusive scan of tiles-touched; total = pair count).
+    {
+        StageTimer t(ctx, kStHist, s);
+        rgs_launch::exclusive_scan(f.sorted_tiles.as<uint32_t>(), n, f.pair_off.as<uint32_t>(), scan_tmp,
+                                   &st_dev->n_pairs, s, &st_dev->n_valid);
+        ctx->launches += 3;
+    }
+    if (f.pair_cap == 0) {
+        // First view of this frame slot: learn the pair count once, size with headroom.
+        CK(cudaMemcpyAsync(f.host_stats, st_dev, sizeof(BinState), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        f.pair_cap = std::max<long long>(4096, (long long)f.host_stats->n_pairs * 5 / 4 + 1024);
+        const uint32_t cap = (uint32_t)std::min<long long>(f.pair_cap, 0xffffffffll);
+        CK(cudaMemcpyAsync(&st_dev->pair_cap, &cap, sizeof cap, cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    f.ensure_pairs(f.pair_cap, s);
+    rgs_launch::check_capacity(st_dev, s);
+    ctx->launches += 1;
 
-    // Depth order (stable; ties by index == source index for scenes).
-    cub::DoubleBuffer<unsigned long long> dk(f.dkey[0].as<unsigned long long>(), f.dkey[1].as<unsigned long long>());
-    cub::DoubleBuffer<uint32_t> dv(f.dval[0].as<uint32_t>(), f.dval[1].as<uint32_t>());
-    size_t need = 0, need_scan = 0;
+    // Duplicate-with-key in rank order, then the two stable tile-digit passes.
     {
-        StageTimer t(ctx, kStDepthSort);
-        if (src == kFromSplats && !splats_monotone) {
-            // Ties must break on source_index (rasterizer.cpp:70): stable pre-sort by it,
-            // then gather the depth keys in that order.
-            cub::DoubleBuffer<uint32_t> sk(f.counts.as<uint32_t>(), f.offsets.as<uint32_t>());
-            cub::DoubleBuffer<uint32_t> sv(f.dval[0].as<uint32_t>(), f.dval[1].as<uint32_t>());
-            rgs_launch::source_keys(f.src.as<int32_t>(), n, sk.Current(), sv.Current(), s);
-            CK(cub::DeviceRadixSort::SortPairs(nullptr, need, sk, sv, n, 0, 32, s));
-            f.cub_tmp.ensure(need, s);
-            CK(cub::DeviceRadixSort::SortPairs(f.cub_tmp.p, need, sk, sv, n, 0, 32, s));
-            uint32_t* ids_in = sv.Current();
-            uint32_t* ids_out = sv.Alternate();
-            rgs_gather_keys(f.dkey[0].as<unsigned long long>(), ids_in, n, f.dkey[1].as<unsigned long long>(),
-                            ids_out, s);
-            ctx->launches += 2;
-            dk = cub::DoubleBuffer<unsigned long long>(f.dkey[1].as<unsigned long long>(),
-                                                       f.dkey[0].as<unsigned long long>());
-            dv = cub::DoubleBuffer<uint32_t>(ids_out, ids_in);
-        }
-        need = 0;
-        CK(cub::DeviceRadixSort::SortPairs(nullptr, need, dk, dv, n, 0, 64, s));
-        CK(cub::DeviceScan::ExclusiveSum(nullptr, need_scan, f.counts.as<uint32_t>(), f.offsets.as<uint32_t>(), n,
-                                         s));
-        f.cub_tmp.ensure(std::max(need, need_scan), s);
-        if (n > 0) CK(cub::DeviceRadixSort::SortPairs(f.cub_tmp.p, need, dk, dv, n, 0, 64, s));
-    }
-    const uint32_t* sorted_ids = dv.Current();
-    {
-        StageTimer t(ctx, kStCounts);
-        rgs_launch::gather_counts(sorted_ids, f.tiles.as<uint32_t>(), n, f.counts.as<uint32_t>(), s);
-        if (n > 0)
-            CK(cub::DeviceScan::ExclusiveSum(f.cub_tmp.p, need_scan, f.counts.as<uint32_t>(),
-                                             f.offsets.as<uint32_t>(), n, s));
-        k_finish_counts<<<1, 32, 0, s>>>(f.offsets.as<uint32_t>(), f.counts.as<uint32_t>(), n, f.dstats());
-        ctx->launches += 2;
-    }
-    CK(cudaMemcpyAsync(ctx->host_stats, f.dstats(), sizeof(DevStats), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    const DevStats st = *ctx->host_stats;
-    if (st.err != kNoError) {
-        const int code = (int)(st.err & 0xff);
-        ctx->err_index = (int)(st.err >> 8);
-        return set_err(ctx, code, rotor_msg(code));
-    }
-    f.n_valid = st.n_valid;
-    f.n_pairs = st.n_pairs;
-
-    // Duplicate-with-key + stable sort by tile id.
-    f.ensure_pairs(f.n_pairs, s);
-    {
-        StageTimer t(ctx, kStDuplicate);
-        rgs_launch::duplicate(sorted_ids, f.offsets.as<uint32_t>(), f.counts.as<uint32_t>(), n,
-                              f.rect.as<ushort4>(), dc.tiles_x, f.tkey[0].as<uint32_t>(), f.pval[0].as<uint32_t>(), s);
+        StageTimer t(ctx, kStTileFill, s);
+        rgs_launch::duplicate(f.sorted_ids.as<uint32_t>(), f.pair_off.as<uint32_t>(), f.sorted_tiles.as<uint32_t>(),
+                              sa.rect, st_dev, n, dc.tiles_x, f.keys_a.as<uint32_t>(), f.pair_vals_buf.as<uint32_t>(),
+                              s);
         ctx->launches += 1;
     }
-    cub::DoubleBuffer<uint32_t> tk(f.tkey[0].as<uint32_t>(), f.tkey[1].as<uint32_t>());
-    cub::DoubleBuffer<uint32_t> tv(f.pval[0].as<uint32_t>(), f.pval[1].as<uint32_t>());
-    const int tbits = bits_for(ntiles);
-    if (f.n_pairs > 0) {
-        need = 0;
-        CK(cub::DeviceRadixSort::SortPairs(nullptr, need, tk, tv, (int)f.n_pairs, 0, tbits, s));
-        f.cub_tmp.ensure(need, s);
-        StageTimer t(ctx, kStTileSort);
-        CK(cub::DeviceRadixSort::SortPairs(f.cub_tmp.p, need, tk, tv, (int)f.n_pairs, 0, tbits, s));
-    }
-    f.pairs_sel = tv.Current() == f.pval[0].as<uint32_t>() ? 0 : 1;
     {
-        StageTimer t(ctx, kStRanges);
-        rgs_launch::tile_ranges(tk.Current(), f.n_pairs, ntiles, f.ranges.as<uint2>(), s);
-        ctx->launches += 1;
+        StageTimer t(ctx, kStTileSort, s);
+        rgs_launch::tile_radix_sort(f.keys_a.as<uint32_t>(), f.pair_vals_buf.as<uint32_t>(), f.keys_b.as<uint32_t>(),
+                                    f.vals_b.as<uint32_t>(), st_dev, f.pair_cap, dc.tiles_x, ntiles,
+                                    f.radix_counts.as<uint32_t>(), f.radix_offsets.as<uint32_t>(),
+                                    f.scan_tmp.as<uint32_t>(), f.ranges.as<uint2>(), s);
+        ctx->launches += 11;
     }
 
     // Blend.
     uint32_t* nc = flow_mode ? nullptr : f.n_contrib.as<uint32_t>();
     double* fT = flow_mode ? nullptr : f.final_T.as<double>();
     int* slow_count = &f.dstats()->slow_count;
+    if (!image) {
+        f.tmp_img.ensure(npix * 3 * sizeof(float), s);
+        image = f.tmp_img.as<float>();
+    }
     if (flags & RGS_FLAG_BLEND_FP64) {
         rgs_launch::mark_all_slow((int)npix, f.slow_list.as<uint32_t>(), slow_count, s);
         ctx->launches += 1;
-    } else if (image || !flow_mode) {
-        float* img = image;
-        if (!img) {
-            ctx->tmp_img.ensure(npix * 3 * sizeof(float), s);
-            img = ctx->tmp_img.as<float>();
-        }
-        image = img;
+    } else {
         unsigned long long* counters = nullptr;
-        if (ctx->count_evals && !flow_mode) {
-            ctx->counters.ensure(16, s);
-            counters = ctx->counters.as<unsigned long long>();
-        }
-        StageTimer t(ctx, kStBlend);
+        if (ctx->count_evals && !flow_mode) counters = ctx->counters.as<unsigned long long>();
+        StageTimer t(ctx, kStBlend, s);
         rgs_launch::blend_fp32(sa, f.pair_vals(), f.ranges.as<uint2>(), dc,
-                               make_float3((float)f.bg[0], (float)f.bg[1], (float)f.bg[2]), flow_mode ? 1 : 0, img,
+                               make_float3((float)f.bg[0], (float)f.bg[1], (float)f.bg[2]), flow_mode ? 1 : 0, image,
                                fT, nc, f.slow_list.as<uint32_t>(), slow_count, counters, s);
         ctx->launches += 1;
     }
-    if (!image) {
-        ctx->tmp_img.ensure(npix * 3 * sizeof(float), s);
-        image = ctx->tmp_img.as<float>();
-    }
     {
-        StageTimer t(ctx, kStFixup);
+        StageTimer t(ctx, kStFixup, s);
         rgs_launch::blend_fp64_pixels(sa, f.pair_vals(), f.ranges.as<uint2>(), dc,
                                       make_double3(f.bg[0], f.bg[1], f.bg[2]), flow_mode ? 1 : 0, image, fT, nc,
                                       f.slow_list.as<uint32_t>(), slow_count, (int)npix, s);
         ctx->launches += 1;
     }
     CK(cudaGetLastError());
+    BinState* hs = host_stats ? host_stats : f.host_stats;
+    CK(cudaMemcpyAsync(hs, st_dev, sizeof(BinState), cudaMemcpyDeviceToHost, s));
+    if (!sync) return RGS_OK;
+    CK(cudaStreamSynchronize(s));
+    const BinState st = *hs;
+    if (st.err != kNoError) {
+        const int code = (int)(st.err & 0xff);
+        ctx->err_index = (int)(st.err >> 8);
+        return set_err(ctx, code, rotor_msg(code));
+    }
+    if (st.overflow) {
+        f.pair_cap = (long long)st.n_pairs * 5 / 4 + 1024;
+        return run_forward(ctx, f, s, src, scene, dev_splats, n_splats, splats_monotone, cam, bg, flags, image,
+                           flow_mode, true, host_stats);
+    }
+    f.n_valid = st.n_valid;
+    f.n_pairs = st.n_pairs;
     return RGS_OK;
 }
 
@@ -487,20 +502,6 @@ int guarded(rgs_ctx* ctx, F&& fn) {
 }
 
 }  // namespace
-
-// Gather kernel used by the rasterize_forward source-index pre-sort.
-__global__ void k_gather_keys(const unsigned long long* keys, const uint32_t* ids, int n, unsigned long long* out,
-                              uint32_t* out_ids) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < n) {
-        out[k] = keys[ids[k]];
-        out_ids[k] = ids[k];
-    }
-}
-void rgs_gather_keys(const unsigned long long* keys, const uint32_t* ids, int n, unsigned long long* out,
-                     uint32_t* out_ids, cudaStream_t s) {
-    if (n > 0) k_gather_keys<<<(n + 255) / 256, 256, 0, s>>>(keys, ids, n, out, out_ids);
-}
 
 extern "C" {
 
@@ -526,7 +527,13 @@ int rgs_ctx_create(int device, rgs_ctx** out) {
         CK(cudaSetDevice(device));
         CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
         CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
-        CK(cudaMallocHost(&c->host_stats, sizeof(DevStats)));
+        CK(cudaMallocHost(&c->host_stats, sizeof(BinState)));
+        for (int k = 0; k < rgs_ctx::kSlots; ++k) {
+            CK(cudaStreamCreateWithFlags(&c->slot_stream[k], cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&c->slot_done[k], cudaEventDisableTiming));
+        }
+        CK(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
+        if (!rgs_launch::binning_init()) throw CudaError{cudaErrorInvalidValue, "binning_init"};
         // Keep freed blocks in the pool: frames re-grow without hitting the driver.
         cudaMemPool_t pool;
         CK(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -550,6 +557,16 @@ void rgs_ctx_destroy(rgs_ctx* c) {
     c->tmp_splats.release(c->stream);
     c->tmp_scan.release(c->stream);
     c->tmp_ids.release(c->stream);
+    for (int k = 0; k < rgs_ctx::kSlots; ++k) {
+        if (!c->slot_stream[k]) continue;
+        c->slot_frame[k].release(c->slot_stream[k]);
+        cudaStreamSynchronize(c->slot_stream[k]);
+        cudaStreamDestroy(c->slot_stream[k]);
+        cudaEventDestroy(c->slot_done[k]);
+    }
+    if (c->join_ev) cudaEventDestroy(c->join_ev);
+    if (c->view_stats) cudaFreeHost(c->view_stats);
+    for (size_t i = 0; i < c->ev_pool.size(); ++i) cudaEventDestroy(c->ev_pool[i]);
     cudaStreamSynchronize(c->stream);
     if (c->host_stats) cudaFreeHost(c->host_stats);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
@@ -576,8 +593,8 @@ int rgs_ctx_set_profiling(rgs_ctx* c, int timing, int count_evals) {
         c->timing = timing != 0;
         c->count_evals = count_evals != 0;
         if (c->count_evals) {
-            c->counters.ensure(16, c->stream);
-            CK(cudaMemsetAsync(c->counters.p, 0, 16, c->stream));
+            c->counters.ensure(32, c->stream);
+            CK(cudaMemsetAsync(c->counters.p, 0, 32, c->stream));
         }
         return RGS_OK;
     });
@@ -619,7 +636,7 @@ int rgs_ctx_profile_reset(rgs_ctx* c) {
             c->stage_ms[k] = 0;
             c->stage_n[k] = 0;
         }
-        if (c->counters.p) CK(cudaMemsetAsync(c->counters.p, 0, 16, c->stream));
+        if (c->counters.p) CK(cudaMemsetAsync(c->counters.p, 0, 32, c->stream));
         return RGS_OK;
     });
 }
@@ -632,9 +649,9 @@ int rgs_ctx_profile_read(rgs_ctx* c, double* stage_ms, long long* stage_launches
             if (stage_launches) stage_launches[k] = c->stage_n[k];
         }
         if (evals) {
-            evals[0] = evals[1] = 0;
+            evals[0] = evals[1] = evals[2] = 0;
             if (c->counters.p) {
-                CK(cudaMemcpyAsync(evals, c->counters.p, 16, cudaMemcpyDeviceToHost, c->stream));
+                CK(cudaMemcpyAsync(evals, c->counters.p, 24, cudaMemcpyDeviceToHost, c->stream));
                 CK(cudaStreamSynchronize(c->stream));
             }
         }
@@ -773,20 +790,18 @@ static int forward_common(rgs_ctx* c, Source src, const rgs_scene* scene, const 
                 CK(cudaMemcpyAsync(c->tmp_splats.p, splats, sizeof(rgs_splat) * (size_t)n_splats,
                                    host_io ? cudaMemcpyHostToDevice : cudaMemcpyDefault, c->stream));
             dsp = c->tmp_splats.p;
-            if (host_io || true) {
-                // monotone source indices -> index order already is the tie-break order
-                std::vector<rgs_splat> h;
-                const rgs_splat* hp = splats;
-                cudaPointerAttributes attr;
-                if (cudaPointerGetAttributes(&attr, splats) == cudaSuccess && attr.type == cudaMemoryTypeDevice) {
-                    h.resize(n_splats);
-                    CK(cudaMemcpy(h.data(), splats, sizeof(rgs_splat) * n_splats, cudaMemcpyDeviceToHost));
-                    hp = h.data();
-                }
-                cudaGetLastError();
-                for (int i = 1; i < n_splats; ++i)
-                    if (hp[i].source_index <= hp[i - 1].source_index) monotone = false;
+            // Monotone source indices: index order already is the tie-break order.
+            std::vector<rgs_splat> h;
+            const rgs_splat* hp = splats;
+            cudaPointerAttributes attr;
+            if (cudaPointerGetAttributes(&attr, splats) == cudaSuccess && attr.type == cudaMemoryTypeDevice) {
+                h.resize(n_splats);
+                CK(cudaMemcpy(h.data(), splats, sizeof(rgs_splat) * n_splats, cudaMemcpyDeviceToHost));
+                hp = h.data();
             }
+            cudaGetLastError();
+            for (int i = 1; i < n_splats; ++i)
+                if (hp[i].source_index <= hp[i - 1].source_index) monotone = false;
         }
         rgs_records* rec = nullptr;
         Frame* f = &c->scratch;
@@ -796,7 +811,8 @@ static int forward_common(rgs_ctx* c, Source src, const rgs_scene* scene, const 
             rec->retained = (flags & RGS_FLAG_RETAIN_RECORDS) ? 1 : 0;
             f = &rec->fb;
         }
-        rc = run_forward(c, *f, src, scene, dsp, n_splats, monotone, cam, bg, flags, dimg, flow);
+        rc = run_forward(c, *f, c->stream, src, scene, dsp, n_splats, monotone, cam, bg, flags, dimg, flow, true,
+                         nullptr);
         if (rc) {
             if (rec) {
                 rec->fb.release(c->stream);
@@ -832,24 +848,91 @@ int rgs_render_flow(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* cam, u
                           true);
 }
 
+}  // extern "C"
+
+namespace {
+
+// Views of a batch are spread round-robin over kSlots frame slots, each on its own
+// stream, so the small latency-bound kernels of one view overlap the blend of another.
+// No host synchronisation until the end of the batch; then every view's BinState is
+// checked (rotor errors reported, pair-buffer overflows re-rendered synchronously).
+// `copy_out` (optional) is called after each view is enqueued on its slot stream.
+template <typename CopyOut>
+int render_batch(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* cams, int n_views, const double bg[3],
+                 unsigned flags, float* (*image_for)(void*, int, int), void* user, CopyOut&& copy_out) {
+    for (int v = 0; v < n_views; ++v) {
+        const int rc = validate_camera(c, &cams[v]);
+        if (rc) return rc;
+    }
+    c->err_index = -1;
+    c->ensure_view_stats(n_views);
+    CK(cudaEventRecord(c->join_ev, c->stream));
+    for (int k = 0; k < rgs_ctx::kSlots; ++k) CK(cudaStreamWaitEvent(c->slot_stream[k], c->join_ev, 0));
+    for (int v = 0; v < n_views; ++v) {
+        const int k = v % rgs_ctx::kSlots;
+        cudaStream_t s = c->slot_stream[k];
+        const int rc = run_forward(c, c->slot_frame[k], s, kFromScene, scene, nullptr, 0, true, &cams[v], bg,
+                                   flags & ~RGS_FLAG_HOST_BUFFERS, image_for(user, v, k), false, false,
+                                   &c->view_stats[v]);
+        if (rc) return rc;
+        copy_out(v, k, s);
+    }
+    for (int k = 0; k < rgs_ctx::kSlots; ++k) {
+        CK(cudaEventRecord(c->slot_done[k], c->slot_stream[k]));
+        CK(cudaStreamWaitEvent(c->stream, c->slot_done[k], 0));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    for (int v = 0; v < n_views; ++v) {
+        const BinState& st = c->view_stats[v];
+        if (st.err != kNoError) {
+            const int code = (int)(st.err & 0xff);
+            c->err_index = (int)(st.err >> 8);
+            return set_err(c, code, rotor_msg(code));
+        }
+    }
+    for (int v = 0; v < n_views; ++v) {
+        if (!c->view_stats[v].overflow) continue;
+        Frame& f = c->slot_frame[0];
+        f.pair_cap = std::max<long long>(f.pair_cap, (long long)c->view_stats[v].n_pairs * 5 / 4 + 1024);
+        const int rc = run_forward(c, f, c->stream, kFromScene, scene, nullptr, 0, true, &cams[v], bg,
+                                   flags & ~RGS_FLAG_HOST_BUFFERS, image_for(user, v, 0), false, true, nullptr);
+        if (rc) return rc;
+        copy_out(v, 0, c->stream);
+        CK(cudaStreamSynchronize(c->stream));
+    }
+    return RGS_OK;
+}
+
+struct DeviceImages {
+    float* base;
+    size_t per;
+};
+float* device_image_for(void* u, int v, int) {
+    DeviceImages* d = static_cast<DeviceImages*>(u);
+    return d->base + d->per * (size_t)v;
+}
+
+}  // namespace
+
+extern "C" {
+
 int rgs_render_views(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* cams, int n_views, const double bg[3],
                      unsigned flags, float* images) {
     if (!scene || !cams || n_views < 0 || !images) return RGS_E_INVALID;
     for (int v = 0; v < n_views; ++v)
         if (cams[v].width != cams[0].width || cams[v].height != cams[0].height) return RGS_E_INVALID;
-    const size_t per = (size_t)cams[0].width * cams[0].height * 3;
-    for (int v = 0; v < n_views; ++v) {
-        int rc = forward_common(c, kFromScene, scene, nullptr, 0, &cams[v], bg, flags & ~RGS_FLAG_HOST_BUFFERS,
-                                images + per * v, nullptr, false);
-        if (rc) return rc;
-    }
-    return RGS_OK;
+    if (n_views == 0) return RGS_OK;
+    return guarded(c, [&]() -> int {
+        DeviceImages d{images, (size_t)cams[0].width * cams[0].height * 3};
+        return render_batch(c, scene, cams, n_views, bg, flags, device_image_for, &d, [](int, int, cudaStream_t) {});
+    });
 }
 
 int rgs_render_views_host(rgs_ctx* c, int n, int sh_degree, const float* mean, const float* ls, const float* rot,
                           const float* op, const float* sh, const rgs_camera* cams, int n_views, const double bg[3],
                           float* images_host) {
     if (!cams || n_views < 0 || !images_host) return RGS_E_INVALID;
+    if (n_views == 0) return RGS_OK;
     rgs_scene* scene = nullptr;
     int rc = rgs_scene_create(c, n, sh_degree, &scene);
     if (rc) return rc;
@@ -859,34 +942,35 @@ int rgs_render_views_host(rgs_ctx* c, int n, int sh_degree, const float* mean, c
         return rc;
     }
     rc = guarded(c, [&]() -> int {
+        // One device image per slot; each rendered view is copied to the host on the
+        // copy stream while the slot moves on (it waits for the copy before reuse).
         const size_t per = (size_t)cams[0].width * cams[0].height * 3;
-        DevBuf img[2];
-        cudaEvent_t rendered[2], copied[2];
-        for (int k = 0; k < 2; ++k) {
-            img[k].ensure(per * sizeof(float), c->stream);
-            CK(cudaEventCreateWithFlags(&rendered[k], cudaEventDisableTiming));
-            CK(cudaEventCreateWithFlags(&copied[k], cudaEventDisableTiming));
-            CK(cudaEventRecord(copied[k], c->copy_stream));
+        struct Slots {
+            DevBuf img[rgs_ctx::kSlots];
+            cudaEvent_t rendered[rgs_ctx::kSlots], copied[rgs_ctx::kSlots];
+        } sl;
+        for (int k = 0; k < rgs_ctx::kSlots; ++k) {
+            sl.img[k].ensure(per * sizeof(float), c->stream);
+            CK(cudaEventCreateWithFlags(&sl.rendered[k], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&sl.copied[k], cudaEventDisableTiming));
+            CK(cudaEventRecord(sl.copied[k], c->copy_stream));
+            CK(cudaStreamWaitEvent(c->slot_stream[k], sl.copied[k], 0));
         }
-        int r = RGS_OK;
-        for (int v = 0; v < n_views && r == RGS_OK; ++v) {
-            const int k = v & 1;
-            CK(cudaStreamWaitEvent(c->stream, copied[k], 0));
-            r = forward_common(c, kFromScene, scene, nullptr, 0, &cams[v], bg, 0, img[k].as<float>(), nullptr,
-                               false);
-            if (r) break;
-            CK(cudaEventRecord(rendered[k], c->stream));
-            CK(cudaStreamWaitEvent(c->copy_stream, rendered[k], 0));
-            CK(cudaMemcpyAsync(images_host + per * v, img[k].p, per * sizeof(float), cudaMemcpyDeviceToHost,
-                               c->copy_stream));
-            CK(cudaEventRecord(copied[k], c->copy_stream));
-        }
+        auto image_for = [](void* u, int, int k) -> float* { return static_cast<Slots*>(u)->img[k].as<float>(); };
+        const int r = render_batch(c, scene, cams, n_views, bg, 0, image_for, &sl, [&](int v, int k, cudaStream_t s) {
+            CK(cudaEventRecord(sl.rendered[k], s));
+            CK(cudaStreamWaitEvent(c->copy_stream, sl.rendered[k], 0));
+            CK(cudaMemcpyAsync(images_host + per * (size_t)v, sl.img[k].p, per * sizeof(float),
+                               cudaMemcpyDeviceToHost, c->copy_stream));
+            CK(cudaEventRecord(sl.copied[k], c->copy_stream));
+            CK(cudaStreamWaitEvent(s, sl.copied[k], 0));  // the slot's next view reuses img[k]
+        });
         CK(cudaStreamSynchronize(c->copy_stream));
         CK(cudaStreamSynchronize(c->stream));
-        for (int k = 0; k < 2; ++k) {
-            img[k].release(c->stream);
-            cudaEventDestroy(rendered[k]);
-            cudaEventDestroy(copied[k]);
+        for (int k = 0; k < rgs_ctx::kSlots; ++k) {
+            sl.img[k].release(c->stream);
+            cudaEventDestroy(sl.rendered[k]);
+            cudaEventDestroy(sl.copied[k]);
         }
         return r;
     });
@@ -906,7 +990,7 @@ int rgs_records_info_get(const rgs_records* r, rgs_records_info* info) {
     if (!r || !info) return RGS_E_INVALID;
     rgs_ctx* c = r->ctx;
     return guarded(c, [&] {
-        DevStats st;
+        BinState st;
         CK(cudaMemcpyAsync(c->host_stats, r->fb.dstats(), sizeof st, cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
         st = *c->host_stats;
@@ -936,12 +1020,10 @@ int rgs_records_export(rgs_ctx* c, const rgs_records* r, rgs_splat* splats, long
         uint32_t* v32 = c->tmp_scan.as<uint32_t>();
         uint32_t* scan = v32 + std::max(n, 1);
         rgs_launch::valid_to_u32(f.valid.as<uint8_t>(), n, v32, s);
-        size_t need = 0;
-        CK(cub::DeviceScan::ExclusiveSum(nullptr, need, v32, scan, n, s));
         DevBuf tmp;
-        tmp.ensure(std::max<size_t>(need, 16), s);
-        if (n > 0) CK(cub::DeviceScan::ExclusiveSum(tmp.p, need, v32, scan, n, s));
-        c->launches += 1;
+        tmp.ensure(4 * (size_t)(n / 1024 + 2), s);
+        rgs_launch::exclusive_scan(v32, n, scan, tmp.as<uint32_t>(), nullptr, s);
+        c->launches += 4;
         if (splats && f.n_valid > 0) {
             c->tmp_ids.ensure(4 * (size_t)f.n_valid, s);
             rgs_launch::compact_index(f.valid.as<uint8_t>(), scan, n, c->tmp_ids.as<uint32_t>(), s);
@@ -1001,12 +1083,12 @@ int rgs_render_backward(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* ca
         SplatArrays sa = f.arrays();
         const float3 bgf = make_float3((float)f.bg[0], (float)f.bg[1], (float)f.bg[2]);
         {
-            StageTimer t(c, kStBwdTiles);
+            StageTimer t(c, kStBwdTiles, s);
             rgs_launch::backward_fp32(sa, f.pair_vals(), f.ranges.as<uint2>(), dc, bgf, f.final_T.as<double>(),
                                       f.n_contrib.as<uint32_t>(), dL_dimage, c->sgrad.as<double>(), s);
         }
         {
-            StageTimer t(c, kStBwdFixup);
+            StageTimer t(c, kStBwdFixup, s);
             rgs_launch::backward_fp64_pixels(sa, f.pair_vals(), f.ranges.as<uint2>(), dc,
                                              make_double3(f.bg[0], f.bg[1], f.bg[2]), f.final_T.as<double>(),
                                              f.n_contrib.as<uint32_t>(), dL_dimage, f.slow_list.as<uint32_t>(),
@@ -1014,7 +1096,7 @@ int rgs_render_backward(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* ca
                                              c->sgrad.as<double>(), s);
         }
         {
-            StageTimer t(c, kStBwdGauss);
+            StageTimer t(c, kStBwdGauss, s);
             rgs_launch::gaussian_backward(scene->params, n, scene->sh_degree, dc, f.valid.as<uint8_t>(),
                                           c->sgrad.as<double>(), (flags & RGS_FLAG_ACCUMULATE) ? 1 : 0, grads,
                                           vnorm, visible, s);

@@ -53,16 +53,33 @@ struct SplatArrays {
     double4* color_depth;    // (r, g, b, depth) FP64
     double4* flow_radius;    // (flow_x, flow_y, radius, 0)
     ushort4* rect;           // tile rectangle (x0, x1, y0, y1), inclusive
-    float4* conic_f;         // (ca, cb, cc, alpha_base) FP32
-    float4* color_f;         // (r, g, b, p_alpha) FP32; p_alpha = log(1/(255 ab))
-    float2* guard_f;         // (c_s, p_clamp): error-bound slope and clamp-gate power
+    float4* conic_f;         // (ca2, cb2, cc2, alpha_base): -log2(e) * (A/2, B, C/2)
+    float4* color_f;         // (r, g, b, pa2): pa2 = log2(1/(255 ab))
+    float2* guard_f;         // (cs2n, pc2): error-bound slope, clamp-gate power log2(0.99/ab)
+    float4* ext_f;           // (ex, ey, gx2, gy2): alpha-ellipse bbox, max |grad p2| inside it
     int32_t* source_index;   // only for rasterize_forward (else NULL -> index)
-    unsigned long long* depth_key;  // sort key: depth bits, ~0 for invalid
-    uint32_t* depth_val;            // Gaussian index
+    unsigned long long* depth_key;  // order-preserving bits of the FP64 depth (valid splats)
 };
 
 // Error word: (index << 8) | code, minimum wins (lowest failing index).
 constexpr unsigned long long kNoError = ~0ull;
+
+// Per-view device counters shared by the preprocess and binning kernels; the host
+// reads it back once per view (after the tile-count scan).
+struct BinState {
+    unsigned long long err;      // rotor error word (kNoError if none)
+    unsigned long long key_min;  // min / max depth key over valid splats
+    unsigned long long key_max;
+    int n_valid;                 // splats produced (RenderRecords::splats.size())
+    int slow_count;              // pixels handed to the FP64 fix-up
+    int shift;                   // depth-bucket shift
+    uint32_t n_big;              // buckets too large for the per-thread sort
+    uint32_t n_pairs;            // total (tile, splat) pairs
+    uint32_t pair_cap;           // capacity of the pair buffers (set by the host)
+    uint32_t n_pairs_eff;        // n_pairs, or 0 when it exceeds pair_cap (overflow)
+    uint32_t overflow;           // 1: the view must be re-rendered with larger buffers
+    uint32_t pad2;
+};
 
 // Guard-band constants for the FP32 blend (DESIGN.md §"FP32 blend with FP64 re-decision").
 constexpr float kGuardFloor = 1e-6f;
@@ -78,14 +95,29 @@ namespace rgs_launch {
 using namespace rgs_dev;
 
 void preprocess(const float* params, int n, int sh_degree, const DevCamera& cam, const SplatArrays& out,
-                unsigned long long* err_word, int* n_valid, cudaStream_t s);
-void splats_from_host(const void* splats, int n, const DevCamera& cam, const SplatArrays& out,
-                      int* n_valid, cudaStream_t s);
-void gather_counts(const uint32_t* sorted_ids, const uint32_t* tiles, int n, uint32_t* counts,
-                   cudaStream_t s);
-void duplicate(const uint32_t* sorted_ids, const uint32_t* offsets, const uint32_t* counts, int n,
-               const ushort4* rect, int tiles_x, uint32_t* tile_keys, uint32_t* pair_vals, cudaStream_t s);
-void tile_ranges(const uint32_t* keys, long long n_pairs, int n_tiles, uint2* ranges, cudaStream_t s);
+                BinState* st, cudaStream_t s);
+void splats_from_host(const void* splats, int n, const DevCamera& cam, const SplatArrays& out, BinState* st,
+                      cudaStream_t s);
+// k_binning.cu
+int num_depth_buckets();
+bool binning_init();
+void exclusive_scan(const uint32_t* in, int n, uint32_t* out, uint32_t* scratch, uint32_t* total, cudaStream_t s,
+                    const int* n_dev = nullptr);
+void bucket_hist(const uint8_t* valid, const unsigned long long* key, int n, BinState* st, uint32_t* bucket_count,
+                 cudaStream_t s);
+void depth_ranks(const uint8_t* valid, const unsigned long long* key, const uint32_t* tiles, int n,
+                 const int32_t* src, BinState* st, const uint32_t* bucket_count, const uint32_t* bucket_off,
+                 uint32_t* bucket_cur, unsigned long long* ent_key, uint32_t* ent_id, uint32_t* sorted_ids,
+                 uint32_t* sorted_tiles, uint32_t* big_list, void* big_scratch, cudaStream_t s);
+void duplicate(const uint32_t* sorted_ids, const uint32_t* pair_off, const uint32_t* sorted_tiles,
+               const ushort4* rect, const BinState* st, int n, int tiles_x, uint32_t* keys, uint32_t* vals,
+               cudaStream_t s);
+void check_capacity(BinState* st, cudaStream_t s);
+int radix_blocks(long long n_pairs);
+size_t radix_count_entries(long long n_pairs);
+void tile_radix_sort(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32_t* vals_b, const BinState* st,
+                     long long n_pairs, int tiles_x, int n_tiles, uint32_t* counts, uint32_t* offsets,
+                     uint32_t* scratch, uint2* ranges, cudaStream_t s);
 void blend_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges, const DevCamera& cam,
                 float3 bg, int flow_mode, float* image, double* final_T, uint32_t* n_contrib,
                 uint32_t* slow_list, int* slow_count, unsigned long long* counters, cudaStream_t s);
@@ -112,7 +144,6 @@ void scene_pack(const float* mean, const float* ls, const float* rot, const floa
                 int n, float* params, cudaStream_t s);
 void scene_unpack(const float* params, int n, double* mean, double* ls, double* rot, double* op, double* sh,
                   cudaStream_t s);
-void source_keys(const int32_t* src, int n, uint32_t* keys, uint32_t* vals, cudaStream_t s);
 void valid_to_u32(const uint8_t* valid, int n, uint32_t* out, cudaStream_t s);
 double ffma_peak(float* out, int blocks, int iters, cudaStream_t s);
 }  // namespace rgs_launch

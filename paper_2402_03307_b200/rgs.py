@@ -403,14 +403,14 @@ class Context:
         self.check(self.L.rgs_ctx_profile_reset(self.h))
 
     def profile_read(self):
-        """{stage: (total_ms, launches)}, (E, B)."""
+        """{stage: (total_ms, launches)}, (E, B, E_kernel)."""
         k = self.L.rgs_profile_num_stages()
         ms = (ctypes.c_double * k)()
         cnt = (ctypes.c_longlong * k)()
-        ev = (ctypes.c_ulonglong * 2)()
+        ev = (ctypes.c_ulonglong * 3)()
         self.check(self.L.rgs_ctx_profile_read(self.h, ms, cnt, ev))
         names = [self.L.rgs_profile_stage_name(i).decode() for i in range(k)]
-        return {names[i]: (ms[i], cnt[i]) for i in range(k)}, (ev[0], ev[1])
+        return {names[i]: (ms[i], cnt[i]) for i in range(k)}, (ev[0], ev[1], ev[2])
 
     # --- scenes
     def scene(self, store: GaussianStore) -> "DeviceScene":

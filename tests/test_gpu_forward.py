@@ -139,6 +139,23 @@ def test_camera_and_rotor_errors(ctx):
         rgs.render_forward(nf, cam, ctx=ctx)
 
 
+def test_render_views_batch_matches_single_views(ctx):
+    """The multi-stream batch path (incl. a pair-buffer overflow re-render) equals per-view renders."""
+    import torch
+
+    store = scenes.synthetic_scene(20_000, 256, 192, seed=8)
+    scene = rgs.DeviceScene.from_store(ctx, store)
+    back = scenes.yaw_pose(180.0)  # sees nothing: slot 0 learns a tiny pair capacity first
+    cams = [scenes.bench_camera(256, 192, 0.5, back)] + scenes.sweep_cameras(256, 192, 8)
+    batch = ctx.render_views(scene, cams, (0.1, 0.2, 0.3))
+    torch.cuda.synchronize()
+    for v, cam in enumerate(cams):
+        img, rec = ctx.render_forward_device(scene, cam, (0.1, 0.2, 0.3), retain=False)
+        torch.cuda.synchronize()
+        assert torch.equal(batch[v], img), v
+    assert torch.all(batch[0] == torch.tensor([0.1, 0.2, 0.3], device=batch.device))
+
+
 def test_missing_records(ctx):
     st = scenes.random_scene(3, seed=2)
     cam = scenes.bench_camera(32, 32, 0.3)
