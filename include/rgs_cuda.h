@@ -53,6 +53,8 @@ typedef enum {
 #define RGS_FLAG_BLEND_FP64 2u     /* blend every pixel in FP64 (reference-KAT mode) */
 #define RGS_FLAG_ACCUMULATE 4u     /* backward: add into grads (StoreGrads::add, gaussian.cpp:199) */
 #define RGS_FLAG_HOST_BUFFERS 8u   /* image / splat pointers are host memory */
+#define RGS_FLAG_IMAGE_F64 16u     /* image is double* (implies RGS_FLAG_BLEND_FP64): the reference's Image */
+#define RGS_FLAG_DETERMINISTIC 32u /* backward: FP64, reference summation order, no atomics (bitwise reproducible) */
 
 typedef struct rgs_ctx rgs_ctx;
 typedef struct rgs_scene rgs_scene;
@@ -128,12 +130,19 @@ int rgs_measure_fp32_tflops(rgs_ctx* ctx, double* tflops);
  *   opacity_logit[N], sh[N*48] channel-major (sh[i*48 + ch*16 + k] = ShCoeffs(ch,k)).
  * Device storage is FP32 SoA (65 floats per Gaussian, see rgs_scene_params). */
 int rgs_scene_create(rgs_ctx* ctx, int n, int sh_degree, rgs_scene** out);
+/* Scene storage flags for rgs_scene_create_ex. */
+#define RGS_SCENE_F64 1u /* store parameters as float64 (exact for any GaussianStore) */
+/* As rgs_scene_create; RGS_SCENE_F64 keeps the 65 parameters per Gaussian in
+ * float64 (same element layout, rgs_scene_params_f64) so the preprocess and the
+ * parameter backward read the reference's double values unrounded. */
+int rgs_scene_create_ex(rgs_ctx* ctx, int n, int sh_degree, unsigned scene_flags, rgs_scene** out);
 void rgs_scene_destroy(rgs_scene* scene);
 int rgs_scene_size(const rgs_scene* scene);
 int rgs_scene_set_sh_degree(rgs_scene* scene, int sh_degree);
-/* Host float64 arrays; values are rounded to float32 (exact for checkpoint-loaded
- * stores, checkpoint.cpp:75-82).  *n_inexact (may be NULL) receives the number of
- * coefficients that were not float32-representable. */
+/* Host float64 arrays.  FP32 scenes round to float32 (exact for checkpoint-loaded
+ * stores, checkpoint.cpp:75-82) and *n_inexact (may be NULL) receives the number of
+ * coefficients that were not float32-representable; RGS_SCENE_F64 scenes store the
+ * values exactly (*n_inexact = 0). */
 int rgs_scene_upload_f64(rgs_ctx* ctx, rgs_scene* scene, const double* mean, const double* log_scales,
                          const double* rotor, const double* opacity_logit, const double* sh,
                          long long* n_inexact);
@@ -144,7 +153,8 @@ int rgs_scene_upload_f32(rgs_ctx* ctx, rgs_scene* scene, const float* mean, cons
  *   [0,4N) mean float4, [4N,8N) log_scales float4, [8N,12N) rotor(s,b01,b02,b03) float4,
  *   [12N,16N) rotor(b12,b13,b23,p) float4, [16N,64N) sh: 12 float4 blocks, block m
  *   holding coefficients j=4m..4m+3 with j = k*3+ch, [64N,65N) opacity_logit. */
-float* rgs_scene_params(rgs_scene* scene);
+float* rgs_scene_params(rgs_scene* scene);      /* NULL for RGS_SCENE_F64 scenes */
+double* rgs_scene_params_f64(rgs_scene* scene); /* NULL for FP32 scenes */
 /* Copy the device scene back to host arrays in the upload layout (float64). */
 int rgs_scene_download_f64(rgs_ctx* ctx, const rgs_scene* scene, double* mean, double* log_scales,
                            double* rotor, double* opacity_logit, double* sh);
@@ -188,7 +198,8 @@ int rgs_records_export(rgs_ctx* ctx, const rgs_records* rec, rgs_splat* splats,
                        int32_t* n_contrib);
 
 /* ---------------------------------------------------------------- backward */
-/* render_backward (rasterizer.cpp:320-397).  dL_dimage: H*W*3 floats (device).
+/* render_backward (rasterizer.cpp:320-397).  dL_dimage: H*W*3 floats (device; host with
+ * RGS_FLAG_HOST_BUFFERS, in which case grads / viewspace_norm / visible are host too).
  * grads: 65*N floats in the rgs_scene_params layout; viewspace_norm: N floats;
  * visible: N int32 (0/1, or a count with RGS_FLAG_ACCUMULATE, so visible>0
  * reproduces StoreGrads::add's OR).  Without RGS_FLAG_ACCUMULATE the outputs are
@@ -196,6 +207,13 @@ int rgs_records_export(rgs_ctx* ctx, const rgs_records* rec, rgs_splat* splats,
 int rgs_render_backward(rgs_ctx* ctx, const rgs_scene* scene, const rgs_camera* cam,
                         const rgs_records* records, const float* dL_dimage, unsigned flags,
                         float* grads, float* viewspace_norm, int32_t* visible);
+
+/* project() of one already-sliced Gaussian (rasterizer.hpp:52-54, rasterizer.cpp:215-276),
+ * evaluated on the device with the same FP64 code as the render path.  Host pointers:
+ * sliced = mean[3], cov[9] row-major, decay, speed[3]; sh48 channel-major.  *survived = 1 and
+ * *out filled (source_index = -1) when the splat passes the culls, 0 when culled. */
+int rgs_project_sliced(rgs_ctx* ctx, const double* sliced16, const rgs_camera* cam, const double* sh48,
+                       int sh_degree, double opacity_logit, rgs_splat* out, int* survived);
 
 /* ---------------------------------------------------------------- utilities */
 /* Camera::validate (camera.hpp:21-26) on the host; RGS_E_CAMERA with the

@@ -6,6 +6,8 @@
 // (see fp64_math.cuh), which is what makes tile rectangles, depths and culls
 // bit-identical to the CPU oracle.
 #include "fp64_math.cuh"
+#include <type_traits>
+
 #include "rgs_internal.cuh"
 
 namespace rgs_dev {
@@ -99,18 +101,21 @@ __device__ __forceinline__ void count_valid(bool ok, unsigned long long key, Bin
 
 // K1: slice + visibility gate + project + SH colour, one thread per Gaussian
 // (rasterizer.cpp:189-204, gaussian.cpp:32-47, rasterizer.cpp:215-276, sh.cpp:16-97).
+template <bool F64>
 __global__ void __launch_bounds__(128) k_preprocess(ParamView P, int sh_degree, DevCamera cam, SplatArrays out,
                                                     BinState* st) {
+    using ShT = typename std::conditional<F64, double, float>::type;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     bool ok = false;
     uint32_t ntiles = 0;
     unsigned long long key = ~0ull;
     if (i < P.n) {
-        const float4 m = P.mean()[i], l = P.ls()[i], r0 = P.rot0()[i], r1 = P.rot1()[i];
-        const double mean4[4] = {m.x, m.y, m.z, m.w};
-        const double ls[4] = {l.x, l.y, l.z, l.w};
-        const double rot[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
-        const double op = P.opacity()[i];
+        double mean4[4], ls[4], rot[8];
+        ld_block<F64>(P, 0, i, mean4);
+        ld_block<F64>(P, 1, i, ls);
+        ld_block<F64>(P, 2, i, rot);
+        ld_block<F64>(P, 3, i, rot + 4);
+        const double op = ld_opacity<F64>(P, i);
         SliceState s;
         const int rc = d_slice(mean4, ls, rot, cam.time, s);
         if (rc > 0) {
@@ -125,15 +130,14 @@ __global__ void __launch_bounds__(128) k_preprocess(ParamView P, int sh_degree, 
                 const int deg = sh_degree < 0 ? 0 : (sh_degree > 3 ? 3 : sh_degree);
                 const int K = (deg + 1) * (deg + 1);
                 const int nblk = (3 * K + 3) / 4;
-                float shv[48];
+                ShT shv[48];
 #pragma unroll
                 for (int b = 0; b < 12; ++b) {
-                    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (b < nblk) v = P.sh(b)[i];
-                    shv[4 * b + 0] = v.x;
-                    shv[4 * b + 1] = v.y;
-                    shv[4 * b + 2] = v.z;
-                    shv[4 * b + 3] = v.w;
+                    if (b < nblk) {
+                        ld_block<F64>(P, 4 + b, i, shv + 4 * b);
+                    } else {
+                        shv[4 * b + 0] = shv[4 * b + 1] = shv[4 * b + 2] = shv[4 * b + 3] = 0;
+                    }
                 }
                 double col[3];
 #pragma unroll
@@ -206,7 +210,7 @@ __global__ void k_splats_from_host(const HostSplat* sp, int n, DevCamera cam, Sp
 // sequential transmittance walk is then replayed identically by every lane.
 __global__ void __launch_bounds__(256) k_blend_fp64(SplatArrays sp, const uint32_t* __restrict__ vals,
                                                     const uint2* __restrict__ ranges, DevCamera cam, double3 bg,
-                                                    int flow_mode, float* image, double* final_T,
+                                                    int flow_mode, float* image, double* image64, double* final_T,
                                                     uint32_t* n_contrib, const uint32_t* __restrict__ list,
                                                     const int* __restrict__ count) {
     const int lane = threadIdx.x & 31;
@@ -270,18 +274,164 @@ __global__ void __launch_bounds__(256) k_blend_fp64(SplatArrays sp, const uint32
             acc0 = acc0 + T * bg.x;
             acc1 = acc1 + T * bg.y;
             acc2 = acc2 + T * bg.z;
-            if (flow_mode) {
-                image[(size_t)pix * 2 + 0] = (float)acc0;
-                image[(size_t)pix * 2 + 1] = (float)acc1;
+            const int ch = flow_mode ? 2 : 3;
+            if (image64) {  // RGS_FLAG_IMAGE_F64: the reference's double image, unrounded
+                image64[(size_t)pix * ch + 0] = acc0;
+                image64[(size_t)pix * ch + 1] = acc1;
+                if (!flow_mode) image64[(size_t)pix * 3 + 2] = acc2;
             } else {
-                image[(size_t)pix * 3 + 0] = (float)acc0;
-                image[(size_t)pix * 3 + 1] = (float)acc1;
-                image[(size_t)pix * 3 + 2] = (float)acc2;
+                image[(size_t)pix * ch + 0] = (float)acc0;
+                image[(size_t)pix * ch + 1] = (float)acc1;
+                if (!flow_mode) image[(size_t)pix * 3 + 2] = (float)acc2;
+            }
+            if (!flow_mode) {
                 if (final_T) final_T[pix] = T;
                 if (n_contrib) n_contrib[pix] = (uint32_t)contrib | kSlowBit;
             }
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// Deterministic backward (RGS_FLAG_DETERMINISTIC, the reference-KAT mode): the
+// reference's own order, FP64 throughout, no atomics.
+//   tiles:  one thread per tile replays its pixels row-major, positions descending,
+//           into per-(tile, position) accumulators (rasterizer.cpp:428-468);
+//   reduce: one thread per splat sums its accumulators over its tiles in increasing
+//           tile order (rasterizer.cpp:471-483), locating itself in each tile list by
+//           binary search on the depth rank.
+
+__global__ void k_inverse_rank(const uint32_t* __restrict__ sorted_ids, const int* __restrict__ n_valid,
+                               uint32_t* rank) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < *n_valid) rank[sorted_ids[r]] = (uint32_t)r;
+}
+
+__global__ void k_backward_det_tiles(SplatArrays sp, const uint32_t* __restrict__ vals,
+                                     const uint2* __restrict__ ranges, DevCamera cam, double3 bg,
+                                     const double* __restrict__ final_T, const uint32_t* __restrict__ n_contrib,
+                                     const float* __restrict__ dL, double* tile_grads) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= cam.tiles_x * cam.tiles_y) return;
+    const uint2 rg = ranges[t];
+    const int px0 = (t % cam.tiles_x) * kTile, py0 = (t / cam.tiles_x) * kTile;
+    const int px1 = min(px0 + kTile, cam.width), py1 = min(py0 + kTile, cam.height);
+    for (int y = py0; y < py1; ++y)
+        for (int x = px0; x < px1; ++x) {
+            const size_t pix = (size_t)y * cam.width + x;
+            const int contrib = (int)(n_contrib[pix] & ~kSlowBit);
+            if (contrib == 0) continue;
+            const double g0 = dL[pix * 3 + 0], g1 = dL[pix * 3 + 1], g2 = dL[pix * 3 + 2];
+            double T_run = final_T[pix];
+            double s0 = bg.x * final_T[pix], s1 = bg.y * final_T[pix], s2 = bg.z * final_T[pix];
+            for (int pos = contrib - 1; pos >= 0; --pos) {
+                const uint32_t id = vals[rg.x + pos];
+                const double2 m = sp.mean2[id];
+                const double4 cab = sp.conic_ab[id];
+                const double dx = (double)x - m.x, dy = (double)y - m.y;
+                const double power = -0.5 * (cab.x * dx * dx + cab.z * dy * dy) - cab.y * dx * dy;
+                if (power > 0) continue;
+                const double raw = cab.w * rgs_exp::glibc_exp(power);
+                const double a = smin(kAlphaClamp, raw);
+                if (a < kMinAlpha) continue;
+                const double T_before = T_run / (1 - a);
+                const double w = a * T_before;
+                double* o = tile_grads + (size_t)(rg.x + pos) * 9;
+                o[0] = o[0] + w * g0;
+                o[1] = o[1] + w * g1;
+                o[2] = o[2] + w * g2;
+                const double4 c = sp.color_depth[id];
+                double dL_da = g0 * (c.x * T_before - s0 / (1 - a));
+                dL_da += g1 * (c.y * T_before - s1 / (1 - a));
+                dL_da += g2 * (c.z * T_before - s2 / (1 - a));
+                if (raw <= kAlphaClamp) {
+                    o[8] += dL_da * (a / cab.w);
+                    const double dpow = dL_da * a;
+                    o[3] = o[3] + dpow * (-0.5 * dx * dx);
+                    o[4] = o[4] + dpow * (-dx * dy);
+                    o[5] = o[5] + dpow * (-0.5 * dy * dy);
+                    o[6] = o[6] + dpow * (cab.x * dx + cab.y * dy);
+                    o[7] = o[7] + dpow * (cab.y * dx + cab.z * dy);
+                }
+                s0 = s0 + c.x * w;
+                s1 = s1 + c.y * w;
+                s2 = s2 + c.z * w;
+                T_run = T_before;
+            }
+        }
+}
+
+__global__ void k_backward_det_reduce(SplatArrays sp, const uint32_t* __restrict__ vals,
+                                      const uint2* __restrict__ ranges, int tiles_x,
+                                      const uint32_t* __restrict__ rank, const double* __restrict__ tile_grads,
+                                      int n, double* sg) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || !sp.valid[i]) return;
+    const ushort4 q = sp.rect[i];
+    if (sp.tiles[i] == 0) return;
+    const uint32_t r = rank[i];
+    double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (int ty = q.z; ty <= q.w; ++ty)
+        for (int tx = q.x; tx <= q.y; ++tx) {
+            const uint2 rg = ranges[ty * tiles_x + tx];
+            uint32_t lo = rg.x, hi = rg.y;  // first position with rank >= r
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (rank[vals[mid]] < r) lo = mid + 1;
+                else hi = mid;
+            }
+            const double* g = tile_grads + (size_t)lo * 9;
+#pragma unroll
+            for (int k = 0; k < 9; ++k) acc[k] += g[k];
+        }
+#pragma unroll
+    for (int k = 0; k < 9; ++k) sg[(size_t)i * 9 + k] = acc[k];
+}
+
+// project() of one already-sliced Gaussian (rasterizer.cpp:215-276) for the C++
+// drop-in's single-Gaussian entry point; SH exactly as the reference (all 16 terms).
+__global__ void k_project_one(const double* __restrict__ sl, DevCamera cam, const double* __restrict__ sh,
+                              int sh_degree, double opacity_logit, HostSplat* out, int* survived) {
+    SliceState s;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) s.mean[k] = sl[k];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) s.cov[k] = sl[3 + k];
+    s.decay = sl[12];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) s.speed[k] = sl[13 + k];
+    ProjState o;
+    if (!d_project_geom(s, cam, opacity_logit, o)) {
+        *survived = 0;
+        return;
+    }
+    double basis[16];
+    d_sh_basis(o.dir, sh_degree, basis);
+    HostSplat h;
+    for (int ch = 0; ch < 3; ++ch) {
+        double a = sh[ch * 16] * basis[0];
+        for (int k = 1; k < 16; ++k) a += sh[ch * 16 + k] * basis[k];
+        const double c = a + 0.5;
+        h.color[ch] = c < 0 ? 0.0 : c;
+    }
+    for (int r = 0; r < 2; ++r) {
+        double a = o.T[r * 3 + 0] * s.speed[0];
+        a += o.T[r * 3 + 1] * s.speed[1];
+        a += o.T[r * 3 + 2] * s.speed[2];
+        h.flow2[r] = a;
+    }
+    h.mean2[0] = o.mean2[0];
+    h.mean2[1] = o.mean2[1];
+    h.conic[0] = o.conic[0];
+    h.conic[1] = o.conic[1];
+    h.conic[2] = o.conic[2];
+    h.depth = o.p[2];
+    h.alpha_base = o.alpha_base;
+    h.radius = o.radius;
+    h.source_index = -1;
+    h.pad = 0;
+    *out = h;
+    *survived = 1;
 }
 
 __global__ void k_mark_all_slow(int n, uint32_t* list, int* count) {
@@ -390,6 +540,7 @@ __global__ void __launch_bounds__(256) k_backward_fp64(SplatArrays sp, const uin
 // ---------------------------------------------------------------------------
 // K7: per-Gaussian backward (rasterizer.cpp:134-181, gaussian.cpp:57-101,
 // rotor.cpp:138-194).  Recomputes the forward chain from the parameters.
+template <bool F64>
 __global__ void __launch_bounds__(128) k_gaussian_backward(ParamView P, int sh_degree, DevCamera cam,
                                                            const uint8_t* __restrict__ valid,
                                                            const double* __restrict__ sgrad, int accumulate,
@@ -417,11 +568,12 @@ __global__ void __launch_bounds__(128) k_gaussian_backward(ParamView P, int sh_d
         }
         return;
     }
-    const float4 m = P.mean()[i], l = P.ls()[i], r0 = P.rot0()[i], r1 = P.rot1()[i];
-    const double mean4[4] = {m.x, m.y, m.z, m.w};
-    const double ls[4] = {l.x, l.y, l.z, l.w};
-    const double rot[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
-    const double op = P.opacity()[i];
+    double mean4[4], ls[4], rot[8];
+    ld_block<F64>(P, 0, i, mean4);
+    ld_block<F64>(P, 1, i, ls);
+    ld_block<F64>(P, 2, i, rot);
+    ld_block<F64>(P, 3, i, rot + 4);
+    const double op = ld_opacity<F64>(P, i);
     SliceState s;
     d_slice(mean4, ls, rot, cam.time, s);
     ProjState o;
@@ -442,15 +594,14 @@ __global__ void __launch_bounds__(128) k_gaussian_backward(ParamView P, int sh_d
     const int K = (deg + 1) * (deg + 1);
     double basis[16];
     d_sh_basis(o.dir, sh_degree, basis);
-    float shv[48];
+    typename std::conditional<F64, double, float>::type shv[48];
 #pragma unroll
     for (int b = 0; b < 12; ++b) {
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (b < (3 * K + 3) / 4) v = P.sh(b)[i];
-        shv[4 * b + 0] = v.x;
-        shv[4 * b + 1] = v.y;
-        shv[4 * b + 2] = v.z;
-        shv[4 * b + 3] = v.w;
+        if (b < (3 * K + 3) / 4) {
+            ld_block<F64>(P, 4 + b, i, shv + 4 * b);
+        } else {
+            shv[4 * b + 0] = shv[4 * b + 1] = shv[4 * b + 2] = shv[4 * b + 3] = 0;
+        }
     }
     double dL_ddir[3] = {0, 0, 0};
     {
@@ -737,11 +888,14 @@ using namespace rgs_dev;
 
 static inline int blocks(long long n, int t) { return (int)((n + t - 1) / t); }
 
-void preprocess(const float* params, int n, int sh_degree, const DevCamera& cam, const SplatArrays& out,
-                BinState* st, cudaStream_t s) {
+void preprocess(const float* params, const double* params64, int n, int sh_degree, const DevCamera& cam,
+                const SplatArrays& out, BinState* st, cudaStream_t s) {
     if (n <= 0) return;
-    ParamView P{params, n};
-    k_preprocess<<<blocks(n, 128), 128, 0, s>>>(P, sh_degree, cam, out, st);
+    ParamView P{params, n, params64};
+    if (params64)
+        k_preprocess<true><<<blocks(n, 128), 128, 0, s>>>(P, sh_degree, cam, out, st);
+    else
+        k_preprocess<false><<<blocks(n, 128), 128, 0, s>>>(P, sh_degree, cam, out, st);
 }
 
 void splats_from_host(const void* splats, int n, const DevCamera& cam, const SplatArrays& out, BinState* st,
@@ -762,11 +916,31 @@ static int persistent_blocks(int max_items) {
 }
 
 void blend_fp64_pixels(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges, const DevCamera& cam,
-                       double3 bg, int flow_mode, float* image, double* final_T, uint32_t* n_contrib,
+                       double3 bg, int flow_mode, float* image, double* image64, double* final_T, uint32_t* n_contrib,
                        const uint32_t* slow_list, const int* slow_count, int max_pixels, cudaStream_t s) {
     if (max_pixels <= 0) return;
     k_blend_fp64<<<persistent_blocks(max_pixels), 256, 0, s>>>(sp, pair_vals, ranges, cam, bg, flow_mode, image,
-                                                               final_T, n_contrib, slow_list, slow_count);
+                                                               image64, final_T, n_contrib, slow_list, slow_count);
+}
+
+void backward_deterministic(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges,
+                            const DevCamera& cam, double3 bg, const double* final_T, const uint32_t* n_contrib,
+                            const float* dL_dimage, const uint32_t* sorted_ids, const int* n_valid_dev, int n,
+                            uint32_t* rank, double* tile_grads, double* screen_grads, cudaStream_t s) {
+    const int ntiles = cam.tiles_x * cam.tiles_y;
+    if (n <= 0 || ntiles <= 0) return;
+    k_inverse_rank<<<blocks(n, 256), 256, 0, s>>>(sorted_ids, n_valid_dev, rank);
+    k_backward_det_tiles<<<blocks(ntiles, 64), 64, 0, s>>>(sp, pair_vals, ranges, cam, bg, final_T, n_contrib,
+                                                           dL_dimage, tile_grads);
+    k_backward_det_reduce<<<blocks(n, 128), 128, 0, s>>>(sp, pair_vals, ranges, cam.tiles_x, rank, tile_grads, n,
+                                                         screen_grads);
+}
+
+int project_one(const double* sliced16_dev, const DevCamera& cam, const double* sh48_dev, int sh_degree,
+                double opacity_logit, void* out_dev, int* survived_dev, cudaStream_t s) {
+    k_project_one<<<1, 1, 0, s>>>(sliced16_dev, cam, sh48_dev, sh_degree, opacity_logit,
+                                  reinterpret_cast<HostSplat*>(out_dev), survived_dev);
+    return 0;
 }
 
 void backward_fp64_pixels(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges,
@@ -778,13 +952,17 @@ void backward_fp64_pixels(const SplatArrays& sp, const uint32_t* pair_vals, cons
                                                                   dL_dimage, slow_list, slow_count, screen_grads);
 }
 
-void gaussian_backward(const float* params, int n, int sh_degree, const DevCamera& cam, const uint8_t* valid,
-                       const double* screen_grads, int accumulate, float* grads, float* vnorm, int32_t* visible,
-                       cudaStream_t s) {
+void gaussian_backward(const float* params, const double* params64, int n, int sh_degree, const DevCamera& cam,
+                       const uint8_t* valid, const double* screen_grads, int accumulate, float* grads, float* vnorm,
+                       int32_t* visible, cudaStream_t s) {
     if (n <= 0) return;
-    ParamView P{params, n};
-    k_gaussian_backward<<<blocks(n, 128), 128, 0, s>>>(P, sh_degree, cam, valid, screen_grads, accumulate, grads,
-                                                       vnorm, visible);
+    ParamView P{params, n, params64};
+    if (params64)
+        k_gaussian_backward<true><<<blocks(n, 128), 128, 0, s>>>(P, sh_degree, cam, valid, screen_grads, accumulate,
+                                                                 grads, vnorm, visible);
+    else
+        k_gaussian_backward<false><<<blocks(n, 128), 128, 0, s>>>(P, sh_degree, cam, valid, screen_grads,
+                                                                  accumulate, grads, vnorm, visible);
 }
 
 }  // namespace rgs_launch

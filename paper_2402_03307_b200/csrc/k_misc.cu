@@ -64,52 +64,50 @@ __global__ void k_valid_u32(const uint8_t* __restrict__ v, int n, uint32_t* out)
 }
 
 // Host upload layout -> device SoA blocks (see rgs_scene_params).
-__global__ void k_scene_pack(const float* __restrict__ mean, const float* __restrict__ ls,
-                             const float* __restrict__ rot, const float* __restrict__ op,
-                             const float* __restrict__ sh, int n, float* P) {
+template <typename T>
+__global__ void k_scene_pack(const T* __restrict__ mean, const T* __restrict__ ls, const T* __restrict__ rot,
+                             const T* __restrict__ op, const T* __restrict__ sh, int n, T* P) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    float4* pm = reinterpret_cast<float4*>(P);
-    float4* pl = reinterpret_cast<float4*>(P + 4 * (size_t)n);
-    float4* r0 = reinterpret_cast<float4*>(P + 8 * (size_t)n);
-    float4* r1 = reinterpret_cast<float4*>(P + 12 * (size_t)n);
-    pm[i] = make_float4(mean[4 * (size_t)i], mean[4 * (size_t)i + 1], mean[4 * (size_t)i + 2], mean[4 * (size_t)i + 3]);
-    pl[i] = make_float4(ls[4 * (size_t)i], ls[4 * (size_t)i + 1], ls[4 * (size_t)i + 2], ls[4 * (size_t)i + 3]);
-    const float* r = rot + 8 * (size_t)i;
-    r0[i] = make_float4(r[0], r[1], r[2], r[3]);
-    r1[i] = make_float4(r[4], r[5], r[6], r[7]);
-    const float* s = sh + 48 * (size_t)i;
-    float v[48];
+    // block b of 4 elements per Gaussian: mean, ls, rot0, rot1, sh[12] (j = k*3 + ch), then opacity
+    auto put = [&](int blk, T a, T b, T c, T d) {
+        T* q = P + 4 * (size_t)blk * n + 4 * (size_t)i;
+        q[0] = a; q[1] = b; q[2] = c; q[3] = d;
+    };
+    const T* m = mean + 4 * (size_t)i;
+    const T* l = ls + 4 * (size_t)i;
+    const T* r = rot + 8 * (size_t)i;
+    put(0, m[0], m[1], m[2], m[3]);
+    put(1, l[0], l[1], l[2], l[3]);
+    put(2, r[0], r[1], r[2], r[3]);
+    put(3, r[4], r[5], r[6], r[7]);
+    const T* s = sh + 48 * (size_t)i;
+    T v[48];
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch)
 #pragma unroll
         for (int k = 0; k < 16; ++k) v[k * 3 + ch] = s[ch * 16 + k];
 #pragma unroll
-    for (int b = 0; b < 12; ++b)
-        reinterpret_cast<float4*>(P + (16 + 4 * (size_t)b) * n)[i] =
-            make_float4(v[4 * b], v[4 * b + 1], v[4 * b + 2], v[4 * b + 3]);
+    for (int b = 0; b < 12; ++b) put(4 + b, v[4 * b], v[4 * b + 1], v[4 * b + 2], v[4 * b + 3]);
     P[64 * (size_t)n + i] = op[i];
 }
 
-__global__ void k_scene_unpack(const float* __restrict__ P, int n, double* mean, double* ls, double* rot,
-                               double* op, double* sh) {
+template <typename T>
+__global__ void k_scene_unpack(const T* __restrict__ P, int n, double* mean, double* ls, double* rot, double* op,
+                               double* sh) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const float4 m = reinterpret_cast<const float4*>(P)[i];
-    const float4 l = reinterpret_cast<const float4*>(P + 4 * (size_t)n)[i];
-    const float4 a = reinterpret_cast<const float4*>(P + 8 * (size_t)n)[i];
-    const float4 b = reinterpret_cast<const float4*>(P + 12 * (size_t)n)[i];
-    double* pm = mean + 4 * (size_t)i;
-    pm[0] = m.x; pm[1] = m.y; pm[2] = m.z; pm[3] = m.w;
-    double* pl = ls + 4 * (size_t)i;
-    pl[0] = l.x; pl[1] = l.y; pl[2] = l.z; pl[3] = l.w;
-    double* pr = rot + 8 * (size_t)i;
-    pr[0] = a.x; pr[1] = a.y; pr[2] = a.z; pr[3] = a.w;
-    pr[4] = b.x; pr[5] = b.y; pr[6] = b.z; pr[7] = b.w;
+    auto get = [&](int blk, int c) -> double { return P[4 * (size_t)blk * n + 4 * (size_t)i + c]; };
+    for (int c = 0; c < 4; ++c) {
+        mean[4 * (size_t)i + c] = get(0, c);
+        ls[4 * (size_t)i + c] = get(1, c);
+        rot[8 * (size_t)i + c] = get(2, c);
+        rot[8 * (size_t)i + 4 + c] = get(3, c);
+    }
     op[i] = P[64 * (size_t)n + i];
     for (int j = 0; j < 48; ++j) {
         const int k = j / 3, ch = j % 3;
-        sh[48 * (size_t)i + ch * 16 + k] = P[(16 + 4 * (size_t)(j / 4)) * n + 4 * (size_t)i + (j % 4)];
+        sh[48 * (size_t)i + ch * 16 + k] = get(4 + j / 4, j % 4);
     }
 }
 
@@ -139,12 +137,21 @@ void valid_to_u32(const uint8_t* valid, int n, uint32_t* out, cudaStream_t s) {
 
 void scene_pack(const float* mean, const float* ls, const float* rot, const float* op, const float* sh, int n,
                 float* params, cudaStream_t s) {
-    if (n > 0) k_scene_pack<<<blocks(n, 128), 128, 0, s>>>(mean, ls, rot, op, sh, n, params);
+    if (n > 0) k_scene_pack<float><<<blocks(n, 128), 128, 0, s>>>(mean, ls, rot, op, sh, n, params);
 }
 
-void scene_unpack(const float* params, int n, double* mean, double* ls, double* rot, double* op, double* sh,
-                  cudaStream_t s) {
-    if (n > 0) k_scene_unpack<<<blocks(n, 128), 128, 0, s>>>(params, n, mean, ls, rot, op, sh);
+void scene_pack64(const double* mean, const double* ls, const double* rot, const double* op, const double* sh,
+                  int n, double* params, cudaStream_t s) {
+    if (n > 0) k_scene_pack<double><<<blocks(n, 128), 128, 0, s>>>(mean, ls, rot, op, sh, n, params);
+}
+
+void scene_unpack(const float* params, const double* params64, int n, double* mean, double* ls, double* rot,
+                  double* op, double* sh, cudaStream_t s) {
+    if (n <= 0) return;
+    if (params64)
+        k_scene_unpack<double><<<blocks(n, 128), 128, 0, s>>>(params64, n, mean, ls, rot, op, sh);
+    else
+        k_scene_unpack<float><<<blocks(n, 128), 128, 0, s>>>(params, n, mean, ls, rot, op, sh);
 }
 
 }  // namespace rgs_launch

@@ -186,6 +186,7 @@ struct rgs_ctx {
     long long launches = 0;
     Frame scratch;
     DevBuf sgrad;     // N x 9 doubles (screen-space gradients)
+    DevBuf tile_grads;  // P x 9 doubles (deterministic backward: per (tile, position))
     DevBuf tmp_img;   // host-buffer staging
     DevBuf tmp_splats, tmp_scan, tmp_ids;
     BinState* host_stats = nullptr;  // pinned
@@ -265,7 +266,8 @@ struct rgs_scene {
     rgs_ctx* ctx = nullptr;
     int n = 0;
     int sh_degree = 0;
-    float* params = nullptr;
+    float* params = nullptr;     // FP32 storage
+    double* params64 = nullptr;  // RGS_SCENE_F64 storage
 };
 
 struct rgs_records {
@@ -382,7 +384,7 @@ int run_forward(rgs_ctx* ctx, Frame& f, cudaStream_t s, Source src, const rgs_sc
     {
         StageTimer t(ctx, kStPreprocess, s);
         if (src == kFromScene)
-            rgs_launch::preprocess(scene->params, n, scene->sh_degree, dc, sa, st_dev, s);
+            rgs_launch::preprocess(scene->params, scene->params64, n, scene->sh_degree, dc, sa, st_dev, s);
         else
             rgs_launch::splats_from_host(dev_splats, n, dc, sa, st_dev, s);
         ctx->launches += 1;
@@ -443,9 +445,12 @@ int run_forward(rgs_ctx* ctx, Frame& f, cudaStream_t s, Source src, const rgs_sc
     uint32_t* nc = flow_mode ? nullptr : f.n_contrib.as<uint32_t>();
     double* fT = flow_mode ? nullptr : f.final_T.as<double>();
     int* slow_count = &f.dstats()->slow_count;
-    if (!image) {
+    double* image64 = (flags & RGS_FLAG_IMAGE_F64) ? reinterpret_cast<double*>(image) : nullptr;
+    float* image32 = image64 ? nullptr : image;
+    if (image64) flags |= RGS_FLAG_BLEND_FP64;
+    if (!image32 && !image64) {
         f.tmp_img.ensure(npix * 3 * sizeof(float), s);
-        image = f.tmp_img.as<float>();
+        image32 = f.tmp_img.as<float>();
     }
     if (flags & RGS_FLAG_BLEND_FP64) {
         rgs_launch::mark_all_slow((int)npix, f.slow_list.as<uint32_t>(), slow_count, s);
@@ -455,15 +460,15 @@ int run_forward(rgs_ctx* ctx, Frame& f, cudaStream_t s, Source src, const rgs_sc
         if (ctx->count_evals && !flow_mode) counters = ctx->counters.as<unsigned long long>();
         StageTimer t(ctx, kStBlend, s);
         rgs_launch::blend_fp32(sa, f.pair_vals(), f.ranges.as<uint2>(), dc,
-                               make_float3((float)f.bg[0], (float)f.bg[1], (float)f.bg[2]), flow_mode ? 1 : 0, image,
-                               fT, nc, f.slow_list.as<uint32_t>(), slow_count, counters, s);
+                               make_float3((float)f.bg[0], (float)f.bg[1], (float)f.bg[2]), flow_mode ? 1 : 0,
+                               image32, fT, nc, f.slow_list.as<uint32_t>(), slow_count, counters, s);
         ctx->launches += 1;
     }
     {
         StageTimer t(ctx, kStFixup, s);
         rgs_launch::blend_fp64_pixels(sa, f.pair_vals(), f.ranges.as<uint2>(), dc,
-                                      make_double3(f.bg[0], f.bg[1], f.bg[2]), flow_mode ? 1 : 0, image, fT, nc,
-                                      f.slow_list.as<uint32_t>(), slow_count, (int)npix, s);
+                                      make_double3(f.bg[0], f.bg[1], f.bg[2]), flow_mode ? 1 : 0, image32, image64,
+                                      fT, nc, f.slow_list.as<uint32_t>(), slow_count, (int)npix, s);
         ctx->launches += 1;
     }
     CK(cudaGetLastError());
@@ -671,24 +676,35 @@ int rgs_camera_validate(rgs_ctx* c, const rgs_camera* cam) {
 }
 
 // ------------------------------------------------------------------ scene
-int rgs_scene_create(rgs_ctx* c, int n, int sh_degree, rgs_scene** out) {
-    if (!out || n < 0) return RGS_E_INVALID;
+int rgs_scene_create_ex(rgs_ctx* c, int n, int sh_degree, unsigned scene_flags, rgs_scene** out) {
+    if (!out || n < 0 || (scene_flags & ~RGS_SCENE_F64)) return RGS_E_INVALID;
     return guarded(c, [&] {
         rgs_scene* s = new rgs_scene;
         s->ctx = c;
         s->n = n;
         s->sh_degree = sh_degree;
-        CK(cudaMalloc(&s->params, sizeof(float) * 65 * (size_t)std::max(n, 1)));
-        CK(cudaMemsetAsync(s->params, 0, sizeof(float) * 65 * (size_t)std::max(n, 1), c->stream));
+        const size_t cnt = 65 * (size_t)std::max(n, 1);
+        if (scene_flags & RGS_SCENE_F64) {
+            CK(cudaMalloc(&s->params64, sizeof(double) * cnt));
+            CK(cudaMemsetAsync(s->params64, 0, sizeof(double) * cnt, c->stream));
+        } else {
+            CK(cudaMalloc(&s->params, sizeof(float) * cnt));
+            CK(cudaMemsetAsync(s->params, 0, sizeof(float) * cnt, c->stream));
+        }
         *out = s;
         return RGS_OK;
     });
+}
+
+int rgs_scene_create(rgs_ctx* c, int n, int sh_degree, rgs_scene** out) {
+    return rgs_scene_create_ex(c, n, sh_degree, 0u, out);
 }
 
 void rgs_scene_destroy(rgs_scene* s) {
     if (!s) return;
     cudaSetDevice(s->ctx->device);
     cudaFree(s->params);
+    cudaFree(s->params64);
     delete s;
 }
 int rgs_scene_size(const rgs_scene* s) { return s ? s->n : 0; }
@@ -698,6 +714,7 @@ int rgs_scene_set_sh_degree(rgs_scene* s, int d) {
     return RGS_OK;
 }
 float* rgs_scene_params(rgs_scene* s) { return s ? s->params : nullptr; }
+double* rgs_scene_params_f64(rgs_scene* s) { return s ? s->params64 : nullptr; }
 
 int rgs_scene_upload_f32(rgs_ctx* c, rgs_scene* s, const float* mean, const float* ls, const float* rot,
                          const float* op, const float* sh) {
@@ -705,6 +722,18 @@ int rgs_scene_upload_f32(rgs_ctx* c, rgs_scene* s, const float* mean, const floa
     return guarded(c, [&] {
         const size_t n = (size_t)s->n;
         if (n == 0) return RGS_OK;
+        if (s->params64) {  // widen on the host, then the exact FP64 upload
+            std::vector<double> d(65 * n);
+            std::vector<float> h(65 * n);
+            CK(cudaMemcpy(h.data(), mean, 16 * n, cudaMemcpyDefault));
+            CK(cudaMemcpy(h.data() + 4 * n, ls, 16 * n, cudaMemcpyDefault));
+            CK(cudaMemcpy(h.data() + 8 * n, rot, 32 * n, cudaMemcpyDefault));
+            CK(cudaMemcpy(h.data() + 16 * n, op, 4 * n, cudaMemcpyDefault));
+            CK(cudaMemcpy(h.data() + 17 * n, sh, 192 * n, cudaMemcpyDefault));
+            for (size_t k = 0; k < 65 * n; ++k) d[k] = h[k];
+            return (rgs_status)rgs_scene_upload_f64(c, s, d.data(), d.data() + 4 * n, d.data() + 8 * n, d.data() + 16 * n,
+                                        d.data() + 17 * n, nullptr);
+        }
         DevBuf tmp;
         tmp.ensure(sizeof(float) * 65 * n, c->stream);
         float* t = tmp.as<float>();
@@ -725,6 +754,26 @@ int rgs_scene_upload_f64(rgs_ctx* c, rgs_scene* s, const double* mean, const dou
                          const double* op, const double* sh, long long* n_inexact) {
     if (!s || !mean || !ls || !rot || !op || !sh) return RGS_E_INVALID;
     const size_t n = (size_t)s->n;
+    if (s->params64) {
+        if (n_inexact) *n_inexact = 0;
+        return guarded(c, [&] {
+            if (n == 0) return RGS_OK;
+            DevBuf tmp;
+            tmp.ensure(sizeof(double) * 65 * n, c->stream);
+            double* t = tmp.as<double>();
+            CK(cudaMemcpyAsync(t, mean, 32 * n, cudaMemcpyHostToDevice, c->stream));
+            CK(cudaMemcpyAsync(t + 4 * n, ls, 32 * n, cudaMemcpyHostToDevice, c->stream));
+            CK(cudaMemcpyAsync(t + 8 * n, rot, 64 * n, cudaMemcpyHostToDevice, c->stream));
+            CK(cudaMemcpyAsync(t + 16 * n, op, 8 * n, cudaMemcpyHostToDevice, c->stream));
+            CK(cudaMemcpyAsync(t + 17 * n, sh, 384 * n, cudaMemcpyHostToDevice, c->stream));
+            rgs_launch::scene_pack64(t, t + 4 * n, t + 8 * n, t + 16 * n, t + 17 * n, (int)n, s->params64,
+                                     c->stream);
+            c->launches += 1;
+            tmp.release(c->stream);
+            CK(cudaStreamSynchronize(c->stream));
+            return RGS_OK;
+        });
+    }
     std::vector<float> f(65 * std::max<size_t>(n, 1));
     long long inexact = 0;
     auto conv = [&](const double* src, size_t cnt, float* dst) {
@@ -752,7 +801,7 @@ int rgs_scene_download_f64(rgs_ctx* c, const rgs_scene* s, double* mean, double*
         DevBuf tmp;
         tmp.ensure(sizeof(double) * 65 * n, c->stream);
         double* t = tmp.as<double>();
-        rgs_launch::scene_unpack(s->params, (int)n, t, t + 4 * n, t + 8 * n, t + 16 * n, t + 17 * n, c->stream);
+        rgs_launch::scene_unpack(s->params, s->params64, (int)n, t, t + 4 * n, t + 8 * n, t + 16 * n, t + 17 * n, c->stream);
         c->launches += 1;
         if (mean) CK(cudaMemcpyAsync(mean, t, 32 * n, cudaMemcpyDeviceToHost, c->stream));
         if (ls) CK(cudaMemcpyAsync(ls, t + 4 * n, 32 * n, cudaMemcpyDeviceToHost, c->stream));
@@ -776,10 +825,11 @@ static int forward_common(rgs_ctx* c, Source src, const rgs_scene* scene, const 
         c->err_index = -1;
         const size_t npix = (size_t)cam->width * cam->height;
         const size_t chans = flow ? 2 : 3;
+        const size_t elem = (flags & RGS_FLAG_IMAGE_F64) ? sizeof(double) : sizeof(float);
         const bool host_io = (flags & RGS_FLAG_HOST_BUFFERS) != 0;
         float* dimg = image;
         if (host_io && image) {
-            c->tmp_img.ensure(npix * 3 * sizeof(float), c->stream);
+            c->tmp_img.ensure(npix * 3 * sizeof(double), c->stream);
             dimg = c->tmp_img.as<float>();
         }
         const void* dsp = nullptr;
@@ -821,7 +871,7 @@ static int forward_common(rgs_ctx* c, Source src, const rgs_scene* scene, const 
             return rc;
         }
         if (host_io && image) {
-            CK(cudaMemcpyAsync(image, dimg, npix * chans * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaMemcpyAsync(image, dimg, npix * chans * elem, cudaMemcpyDeviceToHost, c->stream));
             CK(cudaStreamSynchronize(c->stream));
         }
         if (records) *records = rec;
@@ -868,8 +918,11 @@ int render_batch(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* cams, int
     c->ensure_view_stats(n_views);
     CK(cudaEventRecord(c->join_ev, c->stream));
     for (int k = 0; k < rgs_ctx::kSlots; ++k) CK(cudaStreamWaitEvent(c->slot_stream[k], c->join_ev, 0));
+    // Profiling mode serialises the views (one slot) so per-stage event times are the
+    // kernels' own durations rather than shares of concurrently running views.
+    const int slots = c->timing ? 1 : rgs_ctx::kSlots;
     for (int v = 0; v < n_views; ++v) {
-        const int k = v % rgs_ctx::kSlots;
+        const int k = v % slots;
         cudaStream_t s = c->slot_stream[k];
         const int rc = run_forward(c, c->slot_frame[k], s, kFromScene, scene, nullptr, 0, true, &cams[v], bg,
                                    flags & ~RGS_FLAG_HOST_BUFFERS, image_for(user, v, k), false, false,
@@ -1071,6 +1124,33 @@ int rgs_render_backward(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* ca
     if (!scene || !cam || !r || !dL_dimage || !grads || !vnorm || !visible) return RGS_E_INVALID;
     if (!r->retained)
         return set_err(c, RGS_E_MISSING_RECORDS, "rasterize_backward: forward pass did not retain records");
+    if (flags & RGS_FLAG_HOST_BUFFERS) {
+        // Host in / host out: stage through device buffers on the context stream.
+        return guarded(c, [&]() -> int {
+            cudaStream_t s = c->stream;
+            const size_t n = (size_t)std::max(scene->n, 1), npix = (size_t)cam->width * cam->height;
+            DevBuf dl, g, vn, vis;
+            dl.ensure(npix * 3 * sizeof(float), s);
+            g.ensure(65 * n * sizeof(float), s);
+            vn.ensure(n * sizeof(float), s);
+            vis.ensure(n * sizeof(int32_t), s);
+            CK(cudaMemcpyAsync(dl.p, dL_dimage, npix * 3 * sizeof(float), cudaMemcpyHostToDevice, s));
+            if (flags & RGS_FLAG_ACCUMULATE) {
+                CK(cudaMemcpyAsync(g.p, grads, 65 * n * sizeof(float), cudaMemcpyHostToDevice, s));
+                CK(cudaMemcpyAsync(vn.p, vnorm, n * sizeof(float), cudaMemcpyHostToDevice, s));
+                CK(cudaMemcpyAsync(vis.p, visible, n * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+            }
+            const int rc = rgs_render_backward(c, scene, cam, r, dl.as<float>(), flags & ~RGS_FLAG_HOST_BUFFERS,
+                                               g.as<float>(), vn.as<float>(), vis.as<int32_t>());
+            if (rc) return rc;
+            CK(cudaMemcpyAsync(grads, g.p, 65 * n * sizeof(float), cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(vnorm, vn.p, n * sizeof(float), cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(visible, vis.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+            for (DevBuf* b : {&dl, &g, &vn, &vis}) b->release(s);
+            CK(cudaStreamSynchronize(s));
+            return RGS_OK;
+        });
+    }
     return guarded(c, [&]() -> int {
         const Frame& f = r->fb;
         if (cam->width != f.width || cam->height != f.height || scene->n != f.n)
@@ -1082,12 +1162,22 @@ int rgs_render_backward(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* ca
         CK(cudaMemsetAsync(c->sgrad.p, 0, sizeof(double) * 9 * (size_t)std::max(n, 1), s));
         SplatArrays sa = f.arrays();
         const float3 bgf = make_float3((float)f.bg[0], (float)f.bg[1], (float)f.bg[2]);
-        {
+        if (flags & RGS_FLAG_DETERMINISTIC) {
+            // Reference-order FP64 replay and tile-ordered reduction, no atomics.
+            c->tile_grads.ensure(sizeof(double) * 9 * (size_t)std::max<long long>(f.n_pairs, 1), s);
+            CK(cudaMemsetAsync(c->tile_grads.p, 0, sizeof(double) * 9 * (size_t)std::max<long long>(f.n_pairs, 1), s));
+            StageTimer t(c, kStBwdTiles, s);
+            rgs_launch::backward_deterministic(sa, f.pair_vals(), f.ranges.as<uint2>(), dc,
+                                               make_double3(f.bg[0], f.bg[1], f.bg[2]), f.final_T.as<double>(),
+                                               f.n_contrib.as<uint32_t>(), dL_dimage, f.sorted_ids.as<uint32_t>(),
+                                               &f.dstats()->n_valid, n, f.ent_id.as<uint32_t>(),
+                                               c->tile_grads.as<double>(), c->sgrad.as<double>(), s);
+        } else {
             StageTimer t(c, kStBwdTiles, s);
             rgs_launch::backward_fp32(sa, f.pair_vals(), f.ranges.as<uint2>(), dc, bgf, f.final_T.as<double>(),
                                       f.n_contrib.as<uint32_t>(), dL_dimage, c->sgrad.as<double>(), s);
         }
-        {
+        if (!(flags & RGS_FLAG_DETERMINISTIC)) {
             StageTimer t(c, kStBwdFixup, s);
             rgs_launch::backward_fp64_pixels(sa, f.pair_vals(), f.ranges.as<uint2>(), dc,
                                              make_double3(f.bg[0], f.bg[1], f.bg[2]), f.final_T.as<double>(),
@@ -1097,12 +1187,34 @@ int rgs_render_backward(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* ca
         }
         {
             StageTimer t(c, kStBwdGauss, s);
-            rgs_launch::gaussian_backward(scene->params, n, scene->sh_degree, dc, f.valid.as<uint8_t>(),
+            rgs_launch::gaussian_backward(scene->params, scene->params64, n, scene->sh_degree, dc, f.valid.as<uint8_t>(),
                                           c->sgrad.as<double>(), (flags & RGS_FLAG_ACCUMULATE) ? 1 : 0, grads,
                                           vnorm, visible, s);
         }
         c->launches += 3;
         CK(cudaGetLastError());
+        return RGS_OK;
+    });
+}
+
+int rgs_project_sliced(rgs_ctx* c, const double* sliced16, const rgs_camera* cam, const double* sh48, int sh_degree,
+                       double opacity_logit, rgs_splat* out, int* survived) {
+    if (!sliced16 || !cam || !sh48 || !out || !survived) return RGS_E_INVALID;
+    return guarded(c, [&]() -> int {
+        cudaStream_t s = c->stream;
+        DevBuf buf;
+        buf.ensure(sizeof(double) * 64 + sizeof(rgs_splat) + 16, s);
+        double* d = buf.as<double>();
+        rgs_splat* o = reinterpret_cast<rgs_splat*>(d + 64);
+        int* surv = reinterpret_cast<int*>(o + 1);
+        CK(cudaMemcpyAsync(d, sliced16, sizeof(double) * 16, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(d + 16, sh48, sizeof(double) * 48, cudaMemcpyHostToDevice, s));
+        rgs_launch::project_one(d, make_dev_camera(cam), d + 16, sh_degree, opacity_logit, o, surv, s);
+        c->launches += 1;
+        CK(cudaMemcpyAsync(out, o, sizeof(rgs_splat), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(survived, surv, sizeof(int), cudaMemcpyDeviceToHost, s));
+        buf.release(s);
+        CK(cudaStreamSynchronize(s));
         return RGS_OK;
     });
 }

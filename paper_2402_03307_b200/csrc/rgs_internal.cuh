@@ -29,10 +29,13 @@ struct DevCamera {
     double center[3];
 };
 
-// Offsets (in floats) of the SoA parameter blocks, see rgs_scene_params().
+// Offsets (in elements) of the SoA parameter blocks, see rgs_scene_params().  A scene
+// stores its parameters either as float (base) or, for RGS_SCENE_F64, as double
+// (base64) with the same element layout.
 struct ParamView {
     const float* base;
     int n;
+    const double* base64 = nullptr;
     __host__ __device__ const float4* mean() const { return reinterpret_cast<const float4*>(base); }
     __host__ __device__ const float4* ls() const { return reinterpret_cast<const float4*>(base + 4 * (size_t)n); }
     __host__ __device__ const float4* rot0() const { return reinterpret_cast<const float4*>(base + 8 * (size_t)n); }
@@ -42,6 +45,24 @@ struct ParamView {
     }
     __host__ __device__ const float* opacity() const { return base + 64 * (size_t)n; }
 };
+
+// Load one 4-wide parameter block (block b = elements [4bN, 4(b+1)N)) for Gaussian i.
+template <bool F64, typename T>
+__device__ __forceinline__ void ld_block(const ParamView& P, int blk, int i, T* v) {
+    if constexpr (F64) {
+        const double2* p = reinterpret_cast<const double2*>(P.base64 + 4 * (size_t)blk * P.n) + 2 * (size_t)i;
+        const double2 a = p[0], b = p[1];
+        v[0] = (T)a.x; v[1] = (T)a.y; v[2] = (T)b.x; v[3] = (T)b.y;
+    } else {
+        const float4 f = reinterpret_cast<const float4*>(P.base + 4 * (size_t)blk * P.n)[i];
+        v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+    }
+}
+template <bool F64>
+__device__ __forceinline__ double ld_opacity(const ParamView& P, int i) {
+    if constexpr (F64) return P.base64[64 * (size_t)P.n + i];
+    else return P.base[64 * (size_t)P.n + i];
+}
 
 // Per-Gaussian splat records written by the preprocess kernel (dense, indexed by
 // Gaussian / input-splat index; `valid` marks the ones that produced a splat).
@@ -94,7 +115,7 @@ constexpr uint32_t kSlowBit = 0x80000000u;
 namespace rgs_launch {
 using namespace rgs_dev;
 
-void preprocess(const float* params, int n, int sh_degree, const DevCamera& cam, const SplatArrays& out,
+void preprocess(const float* params, const double* params64, int n, int sh_degree, const DevCamera& cam, const SplatArrays& out,
                 BinState* st, cudaStream_t s);
 void splats_from_host(const void* splats, int n, const DevCamera& cam, const SplatArrays& out, BinState* st,
                       cudaStream_t s);
@@ -123,9 +144,15 @@ void blend_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* r
                 uint32_t* slow_list, int* slow_count, unsigned long long* counters, cudaStream_t s);
 void mark_all_slow(int n_pixels, uint32_t* slow_list, int* slow_count, cudaStream_t s);
 void blend_fp64_pixels(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges,
-                       const DevCamera& cam, double3 bg, int flow_mode, float* image, double* final_T,
-                       uint32_t* n_contrib, const uint32_t* slow_list, const int* slow_count,
+                       const DevCamera& cam, double3 bg, int flow_mode, float* image, double* image64,
+                       double* final_T, uint32_t* n_contrib, const uint32_t* slow_list, const int* slow_count,
                        int max_pixels, cudaStream_t s);
+void backward_deterministic(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges,
+                            const DevCamera& cam, double3 bg, const double* final_T, const uint32_t* n_contrib,
+                            const float* dL_dimage, const uint32_t* sorted_ids, const int* n_valid_dev, int n,
+                            uint32_t* rank, double* tile_grads, double* screen_grads, cudaStream_t s);
+int project_one(const double* sliced16_dev, const DevCamera& cam, const double* sh48_dev, int sh_degree,
+                double opacity_logit, void* out_dev, int* survived_dev, cudaStream_t s);
 void backward_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges,
                    const DevCamera& cam, float3 bg, const double* final_T, const uint32_t* n_contrib,
                    const float* dL_dimage, double* screen_grads, cudaStream_t s);
@@ -133,7 +160,7 @@ void backward_fp64_pixels(const SplatArrays& sp, const uint32_t* pair_vals, cons
                           const DevCamera& cam, double3 bg, const double* final_T, const uint32_t* n_contrib,
                           const float* dL_dimage, const uint32_t* slow_list, const int* slow_count,
                           int max_pixels, double* screen_grads, cudaStream_t s);
-void gaussian_backward(const float* params, int n, int sh_degree, const DevCamera& cam, const uint8_t* valid,
+void gaussian_backward(const float* params, const double* params64, int n, int sh_degree, const DevCamera& cam, const uint8_t* valid,
                        const double* screen_grads, int accumulate, float* grads, float* vnorm,
                        int32_t* visible, cudaStream_t s);
 void export_splats(const SplatArrays& sp, const uint32_t* compact_ids, int n_valid, void* out,
@@ -142,8 +169,10 @@ void compact_index(const uint8_t* valid, const uint32_t* scan, int n, uint32_t* 
 void map_ids(const uint32_t* pair_vals, long long n_pairs, const uint32_t* scan, int32_t* out, cudaStream_t s);
 void scene_pack(const float* mean, const float* ls, const float* rot, const float* op, const float* sh,
                 int n, float* params, cudaStream_t s);
-void scene_unpack(const float* params, int n, double* mean, double* ls, double* rot, double* op, double* sh,
-                  cudaStream_t s);
+void scene_pack64(const double* mean, const double* ls, const double* rot, const double* op, const double* sh,
+                  int n, double* params, cudaStream_t s);
+void scene_unpack(const float* params, const double* params64, int n, double* mean, double* ls, double* rot,
+                  double* op, double* sh, cudaStream_t s);
 void valid_to_u32(const uint8_t* valid, int n, uint32_t* out, cudaStream_t s);
 double ffma_peak(float* out, int blocks, int iters, cudaStream_t s);
 }  // namespace rgs_launch

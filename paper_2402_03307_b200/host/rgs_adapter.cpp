@@ -1,0 +1,265 @@
+// Drop-in C++ implementation of the reference's render entry points over the C ABI.
+//
+// A maintainer of /root/reference/proj compiles this file INSTEAD OF src/rasterizer.cpp
+// and links librgs_cuda.so: every declaration of include/rgs/rasterizer.hpp keeps its
+// signature, argument meaning and exceptions:
+//   project            rasterizer.hpp:52-54   -> rgs_project_sliced (device, FP64)
+//   render_forward     rasterizer.hpp:82-83   -> rgs_render_forward + rgs_records_export
+//   rasterize_forward  rasterizer.hpp:87-89   -> rgs_rasterize_forward
+//   render_backward    rasterizer.hpp:93-95   -> rgs_render_backward
+//   render_flow        rasterizer.hpp:99      -> rgs_render_flow
+// Behaviour differences: `threads` is ignored; ProjectCache / RenderRecords::caches are
+// not filled (the device backward recomputes what it needs; render_backward re-renders
+// the view from the store to rebuild its device records); rotor errors always throw.
+// Environment: RGS_DEVICE selects the CUDA device (default 0).  RGS_KAT_MODE=1 selects the
+// reference-KAT precision mode: FP64 blending with double images, and the deterministic
+// FP64 backward (reference summation order, bitwise reproducible).
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "rgs/rasterizer.hpp"
+#include "rgs_cuda.h"
+
+namespace rgs {
+namespace {
+
+rgs_ctx* context() {
+    static rgs_ctx* c = [] {
+        rgs_ctx* h = nullptr;
+        const char* dev = std::getenv("RGS_DEVICE");
+        const int rc = rgs_ctx_create(dev ? std::atoi(dev) : 0, &h);
+        if (rc != RGS_OK)
+            throw std::runtime_error("rgs_b200: no CUDA device (the B200 render path has no CPU fallback)");
+        return h;
+    }();
+    return c;
+}
+
+bool kat_mode() {
+    const char* v = std::getenv("RGS_KAT_MODE");
+    return v && v[0] == '1';
+}
+
+[[noreturn]] void raise(int rc) {
+    const std::string msg = rgs_ctx_last_error(context());
+    switch (rc) {
+        case RGS_E_CAMERA: throw std::runtime_error(msg);
+        case RGS_E_MISSING_RECORDS: throw MissingRecordsError();
+        case RGS_E_ZERO_ROTOR: throw ZeroRotorError();
+        case RGS_E_NONFINITE_ROTOR: throw NonFiniteRotorError();
+        default: throw std::runtime_error("rgs_b200: " + msg);
+    }
+}
+
+void check(int rc) {
+    if (rc != RGS_OK) raise(rc);
+}
+
+rgs_camera to_c(const Camera& cam) {
+    rgs_camera c;
+    c.width = cam.width;
+    c.height = cam.height;
+    c.fx = cam.fx;
+    c.fy = cam.fy;
+    c.cx = cam.cx;
+    c.cy = cam.cy;
+    for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j) c.world_to_camera[4 * i + j] = cam.world_to_camera(i, j);
+    c.time = cam.time;
+    return c;
+}
+
+Splat2D from_c(const rgs_splat& s) {
+    Splat2D o;
+    o.mean2 = Vec2(s.mean2[0], s.mean2[1]);
+    o.conic = Vec3(s.conic[0], s.conic[1], s.conic[2]);
+    o.depth = s.depth;
+    o.color = Vec3(s.color[0], s.color[1], s.color[2]);
+    o.alpha_base = s.alpha_base;
+    o.flow2 = Vec2(s.flow2[0], s.flow2[1]);
+    o.radius = s.radius;
+    o.source_index = s.source_index;
+    return o;
+}
+
+rgs_splat to_c(const Splat2D& s) {
+    rgs_splat o;
+    std::memset(&o, 0, sizeof o);
+    o.mean2[0] = s.mean2[0];
+    o.mean2[1] = s.mean2[1];
+    for (int k = 0; k < 3; ++k) o.conic[k] = s.conic[k];
+    o.depth = s.depth;
+    for (int k = 0; k < 3; ++k) o.color[k] = s.color[k];
+    o.alpha_base = s.alpha_base;
+    o.flow2[0] = s.flow2[0];
+    o.flow2[1] = s.flow2[1];
+    o.radius = s.radius;
+    o.source_index = s.source_index;
+    return o;
+}
+
+// GaussianStore (gaussian.hpp:79-103) -> a device scene.
+struct DeviceScene {
+    rgs_scene* s = nullptr;
+    explicit DeviceScene(const GaussianStore& store) {
+        const int n = store.size();
+        // FP64 storage: the store's double values reach the kernels unrounded.
+        check(rgs_scene_create_ex(context(), n, store.active_sh_degree, RGS_SCENE_F64, &s));
+        std::vector<double> mean(4 * (size_t)n), ls(4 * (size_t)n), rot(8 * (size_t)n), op(n), sh(48 * (size_t)n);
+        for (int i = 0; i < n; ++i) {
+            for (int a = 0; a < 4; ++a) mean[4 * i + a] = store.mean[i][a];
+            for (int a = 0; a < 4; ++a) ls[4 * i + a] = store.log_scales[i][a];
+            const Vec8 c = store.rotor[i].coeffs();
+            for (int a = 0; a < 8; ++a) rot[8 * i + a] = c[a];
+            op[i] = store.opacity_logit[i];
+            for (int ch = 0; ch < 3; ++ch)
+                for (int k = 0; k < 16; ++k) sh[48 * i + ch * 16 + k] = store.sh[i](ch, k);
+        }
+        check(rgs_scene_upload_f64(context(), s, mean.data(), ls.data(), rot.data(), op.data(), sh.data(), nullptr));
+    }
+    ~DeviceScene() { rgs_scene_destroy(s); }
+};
+
+struct RecordsHandle {
+    rgs_records* r = nullptr;
+    ~RecordsHandle() { rgs_records_destroy(r); }
+};
+
+unsigned image_flags() { return RGS_FLAG_HOST_BUFFERS | (kat_mode() ? RGS_FLAG_IMAGE_F64 : 0u); }
+
+// Renders into a reference Image (double, interleaved); FP32 device images are widened.
+template <typename Fn>
+void render_image(Image* image, int w, int h, int channels, Fn&& fn) {
+    *image = Image(w, h, channels);
+    if (kat_mode()) {
+        fn(reinterpret_cast<float*>(image->data.data()));
+    } else {
+        std::vector<float> tmp((size_t)w * h * channels);
+        fn(tmp.data());
+        for (size_t i = 0; i < tmp.size(); ++i) image->data[i] = tmp[i];
+    }
+}
+
+void export_records(const RecordsHandle& h, RenderRecords* rec, const Vec3& background) {
+    rgs_records_info info;
+    check(rgs_records_info_get(h.r, &info));
+    std::vector<rgs_splat> sp(info.n_splats);
+    const int nt = info.tiles_x * info.tiles_y;
+    std::vector<long long> off(nt + 1);
+    std::vector<int32_t> ids(std::max<long long>(info.n_pairs, 1));
+    rec->final_T.assign((size_t)info.width * info.height, 1);
+    std::vector<int32_t> nc((size_t)info.width * info.height);
+    check(rgs_records_export(context(), h.r, sp.data(), off.data(), ids.data(), rec->final_T.data(), nc.data()));
+    rec->splats.resize(sp.size());
+    for (size_t i = 0; i < sp.size(); ++i) rec->splats[i] = from_c(sp[i]);
+    rec->tile_splats.assign(nt, {});
+    for (int t = 0; t < nt; ++t) rec->tile_splats[t].assign(ids.begin() + off[t], ids.begin() + off[t + 1]);
+    rec->n_contrib.assign(nc.begin(), nc.end());
+    rec->tiles_x = info.tiles_x;
+    rec->tiles_y = info.tiles_y;
+    rec->background = background;
+}
+
+}  // namespace
+
+std::optional<Splat2D> project(const SlicedGaussian3D& s, const Camera& cam, const ShCoeffs& sh, int sh_degree,
+                               Scalar opacity_logit, ProjectCache* /*cache: not filled, see header comment*/) {
+    double sliced[16];
+    for (int a = 0; a < 3; ++a) sliced[a] = s.mean[a];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) sliced[3 + 3 * i + j] = s.cov(i, j);
+    sliced[12] = s.decay;
+    for (int a = 0; a < 3; ++a) sliced[13 + a] = s.speed[a];
+    double sh48[48];
+    for (int ch = 0; ch < 3; ++ch)
+        for (int k = 0; k < 16; ++k) sh48[ch * 16 + k] = sh(ch, k);
+    const rgs_camera c = to_c(cam);
+    rgs_splat out;
+    int survived = 0;
+    check(rgs_project_sliced(context(), sliced, &c, sh48, sh_degree, opacity_logit, &out, &survived));
+    if (!survived) return std::nullopt;
+    return from_c(out);
+}
+
+void rasterize_forward(const std::vector<Splat2D>& splats, const Camera& cam, const Vec3& background,
+                       int /*threads*/, Image* image, RenderRecords* records) {
+    std::vector<rgs_splat> sp(splats.size());
+    for (size_t i = 0; i < splats.size(); ++i) sp[i] = to_c(splats[i]);
+    const rgs_camera c = to_c(cam);
+    const double bg[3] = {background[0], background[1], background[2]};
+    RecordsHandle h;
+    render_image(image, cam.width, cam.height, 3, [&](float* img) {
+        check(rgs_rasterize_forward(context(), sp.data(), (int)sp.size(), &c, bg, image_flags(), img, &h.r));
+    });
+    if (records) {
+        export_records(h, records, background);
+        records->splats = splats;
+    }
+}
+
+RenderOutput render_forward(const GaussianStore& store, const Camera& cam, const RenderOptions& opts) {
+    cam.validate();
+    DeviceScene scene(store);
+    const rgs_camera c = to_c(cam);
+    const double bg[3] = {opts.background[0], opts.background[1], opts.background[2]};
+    RenderOutput out;
+    RecordsHandle h;
+    render_image(&out.image, cam.width, cam.height, 3, [&](float* img) {
+        check(rgs_render_forward(context(), scene.s, &c, bg, image_flags() | RGS_FLAG_RETAIN_RECORDS, img, &h.r));
+    });
+    export_records(h, &out.records, opts.background);
+    out.records.retained = opts.retain_records;
+    return out;
+}
+
+StoreGrads render_backward(const GaussianStore& store, const Camera& cam, const RenderRecords& rec,
+                           const Image& dL_dimage, int /*threads*/) {
+    if (!rec.retained) throw MissingRecordsError();
+    DeviceScene scene(store);
+    const rgs_camera c = to_c(cam);
+    const double bg[3] = {rec.background[0], rec.background[1], rec.background[2]};
+    // Rebuild the device records of this view (deterministic: same decisions as `rec`).
+    RecordsHandle h;
+    std::vector<double> img64((size_t)cam.width * cam.height * 3);
+    check(rgs_render_forward(context(), scene.s, &c, bg, image_flags() | RGS_FLAG_RETAIN_RECORDS,
+                             reinterpret_cast<float*>(img64.data()), &h.r));
+    const int n = store.size();
+    std::vector<float> dl(dL_dimage.data.begin(), dL_dimage.data.end());
+    std::vector<float> g(65 * (size_t)std::max(n, 1)), vn(std::max(n, 1));
+    std::vector<int32_t> vis(std::max(n, 1));
+    const unsigned flags = RGS_FLAG_HOST_BUFFERS | (kat_mode() ? RGS_FLAG_DETERMINISTIC : 0u);
+    check(rgs_render_backward(context(), scene.s, &c, h.r, dl.data(), flags, g.data(), vn.data(), vis.data()));
+    // device SoA (rgs_scene_params layout) -> per-Gaussian gradients
+    StoreGrads out;
+    out.resize(n);
+    const size_t N = (size_t)n;
+    for (int i = 0; i < n; ++i) {
+        GaussianParamGrad& p = out.g[i];
+        for (int a = 0; a < 4; ++a) p.d_mean[a] = g[4 * i + a];
+        for (int a = 0; a < 4; ++a) p.d_log_scales[a] = g[4 * N + 4 * i + a];
+        Vec8 r;
+        for (int a = 0; a < 4; ++a) r[a] = g[8 * N + 4 * i + a];
+        for (int a = 0; a < 4; ++a) r[4 + a] = g[12 * N + 4 * i + a];
+        p.d_rotor = r;
+        p.d_opacity_logit = g[64 * N + i];
+        for (int j = 0; j < 48; ++j) p.d_sh(j % 3, j / 3) = g[(16 + 4 * (size_t)(j / 4)) * N + 4 * i + (j % 4)];
+        out.viewspace_norm[i] = vn[i];
+        out.visible[i] = vis[i] > 0 ? 1 : 0;
+    }
+    return out;
+}
+
+Image render_flow(const GaussianStore& store, const Camera& cam, int /*threads*/) {
+    cam.validate();
+    DeviceScene scene(store);
+    const rgs_camera c = to_c(cam);
+    Image flow;
+    render_image(&flow, cam.width, cam.height, 2, [&](float* img) {
+        check(rgs_render_flow(context(), scene.s, &c, image_flags() | (kat_mode() ? RGS_FLAG_BLEND_FP64 : 0u), img));
+    });
+    return flow;
+}
+
+}  // namespace rgs

@@ -42,6 +42,9 @@ FLAG_RETAIN_RECORDS = 1
 FLAG_BLEND_FP64 = 2
 FLAG_ACCUMULATE = 4
 FLAG_HOST_BUFFERS = 8
+FLAG_IMAGE_F64 = 16
+FLAG_DETERMINISTIC = 32
+SCENE_F64 = 1  # rgs_scene_create_ex storage flag
 
 
 class RgsUnavailableError(RuntimeError):
@@ -130,7 +133,7 @@ EXPORTS = [
     "rgs_rasterize_forward", "rgs_render_flow", "rgs_records_destroy", "rgs_records_info_get",
     "rgs_records_export", "rgs_render_backward", "rgs_camera_validate", "rgs_profile_num_stages",
     "rgs_profile_stage_name", "rgs_ctx_set_profiling", "rgs_ctx_profile_reset", "rgs_ctx_profile_read",
-    "rgs_measure_fp32_tflops",
+    "rgs_measure_fp32_tflops", "rgs_project_sliced", "rgs_scene_create_ex", "rgs_scene_params_f64",
 ]
 
 
@@ -161,6 +164,8 @@ def load_library(path: str = LIB_PATH):
         "rgs_scene_upload_f64": (i, [p, p, p, p, p, p, p, p]),
         "rgs_scene_upload_f32": (i, [p, p, p, p, p, p, p]),
         "rgs_scene_params": (p, [p]),
+        "rgs_scene_create_ex": (i, [p, i, i, ctypes.c_uint, p]),
+        "rgs_scene_params_f64": (p, [p]),
         "rgs_scene_download_f64": (i, [p, p, p, p, p, p, p]),
         "rgs_render_forward": (i, [p, p, p, p, ctypes.c_uint, p, p]),
         "rgs_render_views": (i, [p, p, p, i, p, ctypes.c_uint, p]),
@@ -178,6 +183,7 @@ def load_library(path: str = LIB_PATH):
         "rgs_ctx_profile_reset": (i, [p]),
         "rgs_ctx_profile_read": (i, [p, p, p, p]),
         "rgs_measure_fp32_tflops": (i, [p, p]),
+        "rgs_project_sliced": (i, [p, p, p, p, i, d, p, p]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -478,17 +484,19 @@ class Context:
 
 
 class DeviceScene:
-    """A device-resident rgs_scene (FP32 SoA; rgs_scene_params layout)."""
+    """A device-resident rgs_scene (SoA, rgs_scene_params layout): FP32 storage, or
+    FP64 (``f64=True``, RGS_SCENE_F64) when the store's doubles must reach the
+    kernels unrounded."""
 
-    def __init__(self, ctx: Context, n: int, sh_degree: int):
+    def __init__(self, ctx: Context, n: int, sh_degree: int, f64: bool = False):
         h = _vp()
-        ctx.check(ctx.L.rgs_scene_create(ctx.h, n, sh_degree, ctypes.byref(h)))
-        self.ctx, self.h, self.n, self.sh_degree = ctx, h, n, sh_degree
+        ctx.check(ctx.L.rgs_scene_create_ex(ctx.h, n, sh_degree, SCENE_F64 if f64 else 0, ctypes.byref(h)))
+        self.ctx, self.h, self.n, self.sh_degree, self.f64 = ctx, h, n, sh_degree, f64
         self.n_inexact = 0
 
     @staticmethod
-    def from_store(ctx: Context, store: GaussianStore) -> "DeviceScene":
-        s = DeviceScene(ctx, store.size(), store.active_sh_degree)
+    def from_store(ctx: Context, store: GaussianStore, f64: bool = False) -> "DeviceScene":
+        s = DeviceScene(ctx, store.size(), store.active_sh_degree, f64=f64)
         s.upload(store)
         return s
 
@@ -501,8 +509,16 @@ class DeviceScene:
         self.sh_degree = store.active_sh_degree
         self.ctx.L.rgs_scene_set_sh_degree(self.h, store.active_sh_degree)
 
+    def download(self):
+        """Device scene -> (mean, log_scales, rotor, opacity_logit, sh) float64 host arrays."""
+        n = self.n
+        out = (np.zeros((n, 4)), np.zeros((n, 4)), np.zeros((n, 8)), np.zeros(n), np.zeros((n, 48)))
+        self.ctx.check(self.ctx.L.rgs_scene_download_f64(self.ctx.h, self.h, *[_vp(a.ctypes.data) for a in out]))
+        return out
+
     def params_ptr(self) -> int:
-        return int(self.ctx.L.rgs_scene_params(self.h) or 0)
+        fn =self.ctx.L.rgs_scene_params_f64 if self.f64 else self.ctx.L.rgs_scene_params
+        return int(fn(self.h) or 0)
 
     def close(self):
         if getattr(self, "h", None):
@@ -605,7 +621,7 @@ def render_forward(store: GaussianStore, cam: Camera, opts: RenderOptions = Rend
     """rasterizer.cpp:308-318.  Returns the image (float32) and the records."""
     ctx = ctx or default_context()
     cam.validate()
-    scene = DeviceScene.from_store(ctx, store)
+    scene = DeviceScene.from_store(ctx, store, f64=True)  # the store's doubles, unrounded
     img = np.zeros((cam.height, cam.width, 3), dtype=np.float32)
     c = cam.to_c()
     bg = (ctypes.c_double * 3)(*[float(b) for b in opts.background])
@@ -644,7 +660,7 @@ def render_backward(store: GaussianStore, cam: Camera, records: RenderRecords, d
     ctx = ctx or records.ctx
     scene = getattr(records, "_scene", None)
     if scene is None or scene.n != store.size():
-        scene = DeviceScene.from_store(ctx, store)
+        scene = DeviceScene.from_store(ctx, store, f64=True)
     n = store.size()
     dev = f"cuda:{ctx.device}"
     dl = torch.from_numpy(np.ascontiguousarray(dL_dimage, dtype=np.float32)).to(dev)
@@ -665,7 +681,7 @@ def render_flow(store: GaussianStore, cam: Camera, threads: int = 1, ctx: Option
     """rasterizer.cpp:399-425.  (H, W, 2) screen-space velocity image."""
     ctx = ctx or default_context()
     cam.validate()
-    scene = DeviceScene.from_store(ctx, store)
+    scene = DeviceScene.from_store(ctx, store, f64=True)
     import torch
 
     dev = f"cuda:{ctx.device}"

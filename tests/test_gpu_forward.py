@@ -188,3 +188,21 @@ def test_against_reference_golden(ctx, path):
     assert floored_rel_err(g.as_matrix(), z["grads"]).max() <= 1e-3
     flow = rgs.render_flow(store, cam, ctx=ctx)
     assert np.abs(flow - z["flow"]).max() <= 1e-4 * max(1.0, np.abs(z["flow"]).max())
+
+
+@pytest.mark.parametrize("seed", [3, 4])
+def test_unrounded_store_fp64_scene(ctx, orc, seed):
+    """Doubles that are not float32-representable: the drop-in stores them in an
+    RGS_SCENE_F64 scene, so the splat records stay bit-exact with the oracle."""
+    store = scenes.random_scene(70, sh_degree=3, seed=seed, f32=False)
+    cam = scenes.bench_camera(80, 64, 0.45, pose=scenes.yaw_pose(5.0, (0.03, 0.01, -0.05)))
+    cam.fx = cam.fy = 70.0
+    err, ncd, rec, ref, out = _compare_forward(ctx, orc, store, cam, bg=(0.2, 0.2, 0.1), fp64=True)
+    assert err <= 1e-6
+    assert ncd == 0
+    assert np.abs(rec.final_T - ref.final_T).max() <= 1e-12
+    scene = rgs.DeviceScene.from_store(ctx, store, f64=True)
+    assert scene.n_inexact == 0 and scene.params_ptr() != 0
+    back = scene.download()
+    for a, b in zip(back, store.arrays_f64()):
+        assert np.array_equal(np.asarray(a).reshape(-1), np.asarray(b).reshape(-1))
