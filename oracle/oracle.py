@@ -263,3 +263,178 @@ def reference_build() -> OracleLib:
 
 def reference_available() -> bool:
     return os.path.exists(REF_SO)
+
+
+# ----------------------------------------------------------------------------- training side
+class CAdamConfig(ctypes.Structure):
+    """TrainConfig subset used by adam_step (optim.hpp:17-63); defaults = the reference's."""
+
+    _fields_ = [
+        ("lr_position", ctypes.c_double),
+        ("lr_position_final", ctypes.c_double),
+        ("lr_scales", ctypes.c_double),
+        ("lr_rotor", ctypes.c_double),
+        ("lr_sh_dc", ctypes.c_double),
+        ("lr_sh_rest", ctypes.c_double),
+        ("lr_opacity", ctypes.c_double),
+        ("total_steps", ctypes.c_int),
+        ("static_mode", ctypes.c_int),
+    ]
+
+
+def adam_config(**kw) -> CAdamConfig:
+    c = CAdamConfig(1.6e-4, 1.6e-6, 5e-3, 1e-3, 2.5e-3, 1.25e-4, 0.05, 2000, 0)
+    for k, v in kw.items():
+        setattr(c, k, v)
+    return c
+
+
+class CLossWeights(ctypes.Structure):
+    """LossWeights (loss.hpp:11-16)."""
+
+    _fields_ = [
+        ("lambda_ssim", ctypes.c_double),
+        ("lambda_entropy", ctypes.c_double),
+        ("lambda_consistency", ctypes.c_double),
+        ("k_neighbors", ctypes.c_int),
+    ]
+
+
+def loss_weights(**kw) -> CLossWeights:
+    c = CLossWeights(0.2, 0.01, 0.05, 8)
+    for k, v in kw.items():
+        setattr(c, k, v)
+    return c
+
+
+def _d(x):
+    return np.ascontiguousarray(x, dtype=np.float64)
+
+
+class TrainOps:
+    """Training-side entry points of one oracle library (restatement `orc_` or reference `ref_`)."""
+
+    def __init__(self, lib: OracleLib):
+        self.o = lib
+        self.L = lib.lib
+        self.ref = lib.prefix == "ref"
+        f = lib._f
+        for name in ("psnr", "entropy_loss", "consistency_loss", "lr_schedule"):
+            f(name).restype = ctypes.c_double
+        f("lr_schedule").argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double]
+        if not self.ref:
+            f("l1_loss").restype = ctypes.c_double
+        self.f = f
+
+    def _check(self, rc):
+        if rc != 0:
+            name = "train_last_error" if self.ref else "last_error"
+            msg = getattr(self.L, f"{self.o.prefix}_{name}")
+            msg.restype = ctypes.c_char_p
+            raise OracleError(rc, msg().decode())
+
+    def l1_loss(self, rendered, target, want_grad=True):
+        a, b = _d(rendered), _d(target)
+        g = np.zeros_like(a) if want_grad else None
+        if self.ref:
+            loss = ctypes.c_double(0)
+            h, w = a.shape[:2]
+            self._check(self.f("l1_loss")(ctypes.c_int(w), ctypes.c_int(h), _p(a), _p(b), ctypes.byref(loss), _p(g)))
+            return loss.value, g
+        return self.f("l1_loss")(ctypes.c_longlong(a.size), _p(a), _p(b), _p(g)), g
+
+    def psnr(self, a, b):
+        a, b = _d(a), _d(b)
+        if self.ref:
+            h, w = a.shape[:2]
+            return self.f("psnr")(ctypes.c_int(w), ctypes.c_int(h), _p(a), _p(b))
+        return self.f("psnr")(ctypes.c_longlong(a.size), _p(a), _p(b))
+
+    def ssim_loss(self, rendered, target, want_grad=True):
+        a, b = _d(rendered), _d(target)
+        h, w = a.shape[:2]
+        g = np.zeros_like(a) if want_grad else None
+        loss = ctypes.c_double(0)
+        self._check(self.f("ssim_loss")(ctypes.c_int(w), ctypes.c_int(h), _p(a), _p(b), ctypes.byref(loss), _p(g)))
+        return loss.value, g
+
+    def entropy_loss(self, opacities, want_grad=True):
+        o = _d(opacities)
+        g = np.zeros_like(o) if want_grad else None
+        return self.f("entropy_loss")(ctypes.c_int(len(o)), _p(o), _p(g)), g
+
+    def consistency_loss(self, speeds, nbrs, want_grad=True):
+        s = _d(speeds)
+        nb = np.ascontiguousarray(nbrs, dtype=np.int32)
+        g = np.zeros_like(s) if want_grad else None
+        v = self.f("consistency_loss")(ctypes.c_int(len(s)), _p(s), ctypes.c_int(nb.shape[1]), _p(nb), _p(g))
+        return v, g
+
+    def scene_scales(self, mean):
+        m = _d(mean)
+        out = np.zeros(4)
+        self.f("scene_scales")(ctypes.c_int(len(m)), _p(m), _p(out))
+        return out
+
+    def knn4d(self, mean, k, scales, threads=4):
+        m = _d(mean)
+        out = np.zeros((len(m), k), dtype=np.int32)
+        name = "build_knn4d" if self.ref else "knn4d"
+        self._check(self.f(name)(ctypes.c_int(len(m)), _p(m), ctypes.c_int(k), _p(_d(scales)), ctypes.c_int(threads),
+                                 _p(out)))
+        return out
+
+    def gaussian_speeds(self, store):
+        mean, ls, rot, _, _ = OracleLib._scene(store)
+        out = np.zeros((len(mean), 3))
+        self._check(self.f("gaussian_speeds")(ctypes.c_int(len(mean)), _p(mean), _p(ls), _p(rot), _p(out)))
+        return out
+
+    def lr_schedule(self, step, total, lr_init, lr_final):
+        return self.f("lr_schedule")(step, total, lr_init, lr_final)
+
+    def adam_step(self, store, m, v, grads, cfg, step):
+        """In place on copies: returns (store', m', v')."""
+        mean, ls, rot, op, sh = [a.copy() for a in OracleLib._scene(store)]
+        m, v = _d(m).copy(), _d(v).copy()
+        g = _d(grads)
+        self._check(self.f("adam_step")(ctypes.c_int(len(op)), _p(mean), _p(ls), _p(rot), _p(op), _p(sh), _p(m), _p(v),
+                                        _p(g), ctypes.byref(cfg), ctypes.c_int(step)))
+        out = type(store)(mean, ls, rot, op, sh.reshape(store.sh.shape), store.active_sh_degree)
+        return out, m, v
+
+    def accumulate_stats(self, vnorm, visible, accum, count):
+        accum, count = _d(accum).copy(), np.ascontiguousarray(count, dtype=np.int32).copy()
+        vis = np.ascontiguousarray(visible, dtype=np.uint8)
+        self.f("accumulate_stats")(ctypes.c_int(len(accum)), _p(_d(vnorm)), _p(vis), _p(accum), _p(count))
+        return accum, count
+
+    def reset_opacity(self, op, m_op, v_op, value=0.01):
+        op, m_op, v_op = _d(op).copy(), _d(m_op).copy(), _d(v_op).copy()
+        self.f("reset_opacity")(ctypes.c_int(len(op)), _p(op), _p(m_op), _p(v_op), ctypes.c_double(value))
+        return op, m_op, v_op
+
+    def evaluate_loss(self, store, cams, targets, weights, background=(0.0, 0.0, 0.0), nbrs=None, threads=4,
+                      want_grads=True):
+        mean, ls, rot, op, sh = OracleLib._scene(store)
+        n = len(op)
+        arr = (CCamera * len(cams))(*[make_ccamera(c) for c in cams])
+        tg = np.ascontiguousarray(np.concatenate([_d(t).reshape(-1) for t in targets]))
+        losses = np.zeros(5)
+        g = np.zeros((n, 65)) if want_grads else None
+        vn = np.zeros(n) if want_grads else None
+        vis = np.zeros(n, dtype=np.uint8) if want_grads else None
+        nb = None if nbrs is None else np.ascontiguousarray(nbrs, dtype=np.int32)
+        bg = _d(background)
+        self._check(self.f("evaluate_loss")(ctypes.c_int(n), _p(mean), _p(ls), _p(rot), _p(op), _p(sh),
+                                            ctypes.c_int(store.active_sh_degree), ctypes.c_int(len(cams)), arr,
+                                            _p(tg), ctypes.byref(weights), _p(bg), _p(nb), ctypes.c_int(threads),
+                                            _p(losses), _p(g), _p(vn), _p(vis)))
+        return losses, g, vn, vis
+
+
+def train_ops(which: str = "orc") -> TrainOps:
+    key = "train_" + which
+    if key not in _cache:
+        _cache[key] = TrainOps(restatement() if which == "orc" else reference_build())
+    return _cache[key]

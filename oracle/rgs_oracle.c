@@ -1336,3 +1336,459 @@ int orc_project(const double* sliced, const orc_camera* cam, const double* sh48,
     if (r) out->source_index = -1;
     return r;
 }
+
+/* ======================================================================
+ * Training side: image losses, regularizers, the Adam
+ * step and densification statistics, and evaluate_loss's batch reduction.
+ * Pinned against oracle/_ref (image.cpp, ssim.cpp, loss.cpp, knn.cpp,
+ * optim.cpp, trainer.cpp compiled in place) by tests/test_oracle_train.py.
+ * ==================================================================== */
+
+/* image.cpp:7-18 */
+double orc_psnr(long long n_values, const double* a, const double* b) {
+    double mse = 0;
+    for (long long i = 0; i < n_values; ++i) {
+        double d = a[i] - b[i];
+        mse += d * d;
+    }
+    mse /= (double)n_values;
+    if (mse <= 0) return 100;
+    double v = 10 * log10(1 / mse);
+    return v < 100 ? v : 100;
+}
+
+/* image.cpp:20-36.  grad (may be NULL) = l1_loss_backward. */
+double orc_l1_loss(long long n_values, const double* rendered, const double* target, double* grad) {
+    double sum = 0;
+    for (long long i = 0; i < n_values; ++i) sum += fabs(rendered[i] - target[i]);
+    if (grad) {
+        double inv_n = 1 / (double)n_values;
+        for (long long i = 0; i < n_values; ++i) {
+            double d = rendered[i] - target[i];
+            grad[i] = d > 0 ? inv_n : (d < 0 ? -inv_n : 0);
+        }
+    }
+    return sum / (double)n_values;
+}
+
+/* ssim.cpp:15-31: normalised 11-tap Gaussian window, sigma 1.5. */
+enum { kWin = 11 };
+static void ssim_window(double* k) {
+    const double sigma = 1.5;
+    double sum = 0;
+    for (int i = 0; i < kWin; ++i) {
+        double d = i - (kWin - 1) / 2.0;
+        k[i] = exp(-d * d / (2 * sigma * sigma));
+        sum += k[i];
+    }
+    for (int i = 0; i < kWin; ++i) k[i] /= sum;
+}
+void orc_ssim_window(double* k11) { ssim_window(k11); }
+
+/* ssim.cpp:42-58: valid-region separable convolution (rows, then columns). */
+static void conv_valid(const double* k, const double* in, int w, int h, double* rows, double* out) {
+    int rw = w - kWin + 1, oh = h - kWin + 1;
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < rw; ++x) {
+            double s = 0;
+            for (int i = 0; i < kWin; ++i) s += k[i] * in[(size_t)y * w + x + i];
+            rows[(size_t)y * rw + x] = s;
+        }
+    for (int y = 0; y < oh; ++y)
+        for (int x = 0; x < rw; ++x) {
+            double s = 0;
+            for (int i = 0; i < kWin; ++i) s += k[i] * rows[(size_t)(y + i) * rw + x];
+            out[(size_t)y * rw + x] = s;
+        }
+}
+
+/* ssim.cpp:61-72: adjoint of conv_valid (scatter back to the input support). */
+static void conv_valid_adjoint(const double* k, const double* g, int gw, int gh, int in_w, int in_h,
+                               double* cols, double* out) {
+    memset(cols, 0, sizeof(double) * (size_t)gw * in_h);
+    for (int y = 0; y < gh; ++y)
+        for (int x = 0; x < gw; ++x)
+            for (int i = 0; i < kWin; ++i) cols[(size_t)(y + i) * gw + x] += k[i] * g[(size_t)y * gw + x];
+    memset(out, 0, sizeof(double) * (size_t)in_w * in_h);
+    for (int y = 0; y < in_h; ++y)
+        for (int x = 0; x < gw; ++x)
+            for (int i = 0; i < kWin; ++i) out[(size_t)y * in_w + x + i] += k[i] * cols[(size_t)y * gw + x];
+}
+
+/* ssim.cpp:74-142: 1 - mean SSIM over the valid region, channels 0..2; grad (may be
+ * NULL) = d loss / d rendered (zero outside the valid support). */
+int orc_ssim_loss(int w, int h, const double* xi, const double* yi, double* loss, double* grad) {
+    if (w < kWin || h < kWin) return fail(ORC_E_INVALID, "ssim: image smaller than the 11x11 window");
+    const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;
+    double k[kWin];
+    ssim_window(k);
+    const size_t np = (size_t)w * h;
+    const int vw = w - kWin + 1, vh = h - kWin + 1;
+    const size_t nv = (size_t)vw * vh;
+    double* f = (double*)malloc(sizeof(double) * np * 5);
+    double* m = (double*)malloc(sizeof(double) * nv * 5);
+    double* rows = (double*)malloc(sizeof(double) * (size_t)vw * h);
+    double* d = (double*)malloc(sizeof(double) * nv * 3);
+    double* adj = (double*)malloc(sizeof(double) * np * 3);
+    double* cols = (double*)malloc(sizeof(double) * (size_t)vw * h);
+    double total = 0;
+    size_t count = 0;
+    for (int ch = 0; ch < 3; ++ch) {
+        double *x = f, *y = f + np, *xx = f + 2 * np, *yy = f + 3 * np, *xy = f + 4 * np;
+        for (size_t p = 0; p < np; ++p) {
+            double a = xi[p * 3 + ch], b = yi[p * 3 + ch];
+            x[p] = a;
+            y[p] = b;
+            xx[p] = a * a;
+            yy[p] = b * b;
+            xy[p] = a * b;
+        }
+        for (int q = 0; q < 5; ++q) conv_valid(k, f + q * np, w, h, rows, m + q * nv);
+        const double *mx = m, *my = m + nv, *sxx = m + 2 * nv, *syy = m + 3 * nv, *sxy = m + 4 * nv;
+        for (size_t p = 0; p < nv; ++p) {
+            double ux = mx[p], uy = my[p];
+            double vx = sxx[p] - ux * ux;
+            double vy = syy[p] - uy * uy;
+            double vxy = sxy[p] - ux * uy;
+            double a1 = 2 * ux * uy + C1, a2 = 2 * vxy + C2;
+            double b1 = ux * ux + uy * uy + C1, b2 = vx + vy + C2;
+            double s = (a1 * a2) / (b1 * b2);
+            total += s;
+            ++count;
+            if (grad) {
+                double d_ssim = 1;
+                double d_a1 = d_ssim * a2 / (b1 * b2);
+                double d_a2 = d_ssim * a1 / (b1 * b2);
+                double d_b1 = -d_ssim * s / b1;
+                double d_b2 = -d_ssim * s / b2;
+                double d_ux = d_a1 * 2 * uy + d_b1 * 2 * ux;
+                double d_vx = d_b2;
+                double d_vxy = d_a2 * 2;
+                d_ux += -2 * ux * d_vx - uy * d_vxy;
+                d[p] = d_ux;
+                d[nv + p] = d_vx;
+                d[2 * nv + p] = d_vxy;
+            }
+        }
+        if (grad) {
+            for (int q = 0; q < 3; ++q) conv_valid_adjoint(k, d + q * nv, vw, vh, w, h, cols, adj + q * np);
+            for (size_t p = 0; p < np; ++p)
+                grad[p * 3 + ch] = adj[p] + 2 * x[p] * adj[np + p] + y[p] * adj[2 * np + p];
+        }
+    }
+    double mean = total / (double)count;
+    if (grad) {
+        double fct = -1 / (double)count;
+        for (size_t p = 0; p < np * 3; ++p) grad[p] *= fct;
+    }
+    *loss = 1 - mean;
+    free(f);
+    free(m);
+    free(rows);
+    free(d);
+    free(adj);
+    free(cols);
+    return ORC_OK;
+}
+
+/* loss.cpp:16-31 */
+double orc_entropy_loss(int n, const double* opacities, double* grad) {
+    const double clampv = 1e-6;
+    if (n == 0) return 0;
+    double total = 0;
+    const double inv_n = 1 / (double)n;
+    for (int i = 0; i < n; ++i) {
+        double o = opacities[i];
+        o = o < clampv ? clampv : (1 - clampv < o ? 1 - clampv : o); /* std::clamp */
+        total += -o * log(o);
+        if (grad) grad[i] = (opacities[i] > clampv && opacities[i] < 1 - clampv) ? -(log(o) + 1) * inv_n : 0;
+    }
+    return total * inv_n;
+}
+
+/* loss.cpp:33-58.  dspeed (may be NULL) n*3, zeroed then accumulated. */
+double orc_consistency_loss(int n, const double* speeds, int k, const int32_t* nbrs, double* dspeed) {
+    if (dspeed) memset(dspeed, 0, sizeof(double) * 3 * (size_t)n);
+    if (n == 0) return 0;
+    const double inv_n = 1 / (double)n;
+    double total = 0;
+    for (int i = 0; i < n; ++i) {
+        if (k <= 0) continue;
+        const double inv_k = 1 / (double)k;
+        double avg[3] = {0, 0, 0};
+        for (int j = 0; j < k; ++j)
+            for (int a = 0; a < 3; ++a) avg[a] += speeds[3 * (size_t)nbrs[(size_t)k * i + j] + a];
+        for (int a = 0; a < 3; ++a) avg[a] *= inv_k;
+        double diff[3], sgn[3];
+        for (int a = 0; a < 3; ++a) {
+            diff[a] = speeds[3 * (size_t)i + a] - avg[a];
+            sgn[a] = (double)(diff[a] > 0) - (double)(diff[a] < 0);
+        }
+        double s = fabs(diff[0]);
+        s += fabs(diff[1]);
+        s += fabs(diff[2]);
+        total += s;
+        if (dspeed) {
+            for (int a = 0; a < 3; ++a) dspeed[3 * (size_t)i + a] += inv_n * sgn[a];
+            for (int j = 0; j < k; ++j)
+                for (int a = 0; a < 3; ++a)
+                    dspeed[3 * (size_t)nbrs[(size_t)k * i + j] + a] -= inv_n * inv_k * sgn[a];
+        }
+    }
+    return total * inv_n;
+}
+
+/* trainer.cpp:12-20 */
+void orc_scene_scales(int n, const double* mean, double* out4) {
+    double lo[4] = {0, 0, 0, 0}, hi[4] = {0, 0, 0, 0};
+    if (n > 0)
+        for (int a = 0; a < 4; ++a) lo[a] = hi[a] = mean[a];
+    for (int i = 0; i < n; ++i)
+        for (int a = 0; a < 4; ++a) {
+            double v = mean[4 * (size_t)i + a];
+            lo[a] = v < lo[a] ? v : lo[a];
+            hi[a] = hi[a] < v ? v : hi[a];
+        }
+    for (int a = 0; a < 4; ++a) {
+        double e = hi[a] - lo[a];
+        out4[a] = e < 1e-3 ? 1e-3 : e;
+    }
+}
+
+/* knn.cpp:101-116: exact k nearest neighbours on mean / scales, excluding self, ordered by
+ * (squared distance, index) -- KdTree4's contract (knn.hpp:18-20), as a brute-force scan. */
+typedef struct {
+    int n, k;
+    const double* pts;
+    int32_t* nbrs;
+} knn_ctx;
+static void knn_body(int i, void* p) {
+    knn_ctx* c = (knn_ctx*)p;
+    const int k = c->k;
+    double bd[64];
+    int bi[64];
+    int cnt = 0;
+    const double* q = c->pts + 4 * (size_t)i;
+    for (int j = 0; j < c->n; ++j) {
+        if (j == i) continue;
+        const double* pj = c->pts + 4 * (size_t)j;
+        double d0 = pj[0] - q[0], d1 = pj[1] - q[1], d2 = pj[2] - q[2], d3 = pj[3] - q[3];
+        double dd = d0 * d0;
+        dd += d1 * d1;
+        dd += d2 * d2;
+        dd += d3 * d3;
+        if (cnt == k && !(dd < bd[k - 1] || (dd == bd[k - 1] && j < bi[k - 1]))) continue;
+        int pos = cnt < k ? cnt++ : k - 1;
+        while (pos > 0 && (dd < bd[pos - 1] || (dd == bd[pos - 1] && j < bi[pos - 1]))) {
+            bd[pos] = bd[pos - 1];
+            bi[pos] = bi[pos - 1];
+            --pos;
+        }
+        bd[pos] = dd;
+        bi[pos] = j;
+    }
+    for (int j = 0; j < k; ++j) c->nbrs[(size_t)k * i + j] = bi[j];
+}
+int orc_knn4d(int n, const double* mean, int k, const double* scales, int threads, int32_t* nbrs) {
+    if (n <= k) return fail(ORC_E_INVALID, "knn: need more points than neighbors");
+    if (k > 64) return fail(ORC_E_INVALID, "knn: k > 64 unsupported by the oracle");
+    double* pts = (double*)malloc(sizeof(double) * 4 * (size_t)n);
+    for (size_t i = 0; i < 4 * (size_t)n; ++i) pts[i] = mean[i] / scales[i % 4];
+    knn_ctx c = {n, k, pts, nbrs};
+    parallel_for(0, n, threads, knn_body, &c);
+    free(pts);
+    return ORC_OK;
+}
+
+/* gaussian.cpp:103-110 */
+int orc_gaussian_speeds(int n, const double* mean, const double* ls, const double* rot, double* speeds) {
+    (void)mean;
+    for (int i = 0; i < n; ++i) {
+        slice_cache c;
+        int rc = assemble_cache(ls + 4 * (size_t)i, rot + 8 * (size_t)i, &c);
+        if (rc) return rc;
+        if (c.W < kTemporalFloor) return fail(ORC_E_DEGENERATE_TIME, "slice: degenerate temporal variance");
+        for (int a = 0; a < 3; ++a) speeds[3 * (size_t)i + a] = c.V[a] / c.W;
+    }
+    return ORC_OK;
+}
+
+/* optim.cpp:47-51 */
+double orc_lr_schedule(int step, int total, double lr_init, double lr_final) {
+    if (total <= 0) return lr_init;
+    double u = (double)step / (double)total;
+    u = u < 0 ? 0 : (1 < u ? 1 : u);
+    return lr_init * pow(lr_final / lr_init, u);
+}
+
+/* optim.cpp:19-23 (kAdamBeta1/2, kAdamEps: optim.hpp:70-72) */
+static void adam_scalar(double* p, double* m, double* v, double g, double lr, double bc1, double bc2) {
+    const double b1 = 0.9, b2 = 0.999, eps = 1e-15;
+    *m = b1 * *m + (1 - b1) * g;
+    *v = b2 * *v + (1 - b2) * g * g;
+    *p -= lr * (*m / bc1) / (sqrt(*v / bc2) + eps);
+}
+
+/* optim.cpp:110-157.  m, v: n*65 in the gradient order; grads: n*65. */
+int orc_adam_step(int n, double* mean, double* ls, double* rot, double* op, double* sh, double* m, double* v,
+                  const double* grads, const orc_adam_config* cfg, int step) {
+    const double bc1 = 1 - pow(0.9, step);
+    const double bc2 = 1 - pow(0.999, step);
+    const double lr_pos = orc_lr_schedule(step, cfg->total_steps, cfg->lr_position, cfg->lr_position_final);
+    const int st = cfg->static_mode != 0;
+    for (int i = 0; i < n; ++i) {
+        const double* g = grads + 65 * (size_t)i;
+        double* mi = m + 65 * (size_t)i;
+        double* vi = v + 65 * (size_t)i;
+        for (int a = 0; a < 4; ++a) {
+            if (st && a == 3) continue;
+            adam_scalar(&mean[4 * (size_t)i + a], &mi[a], &vi[a], g[a], lr_pos, bc1, bc2);
+        }
+        for (int a = 0; a < (st ? 3 : 4); ++a)
+            adam_scalar(&ls[4 * (size_t)i + a], &mi[4 + a], &vi[4 + a], g[4 + a], cfg->lr_scales, bc1, bc2);
+        double rc[8];
+        for (int a = 0; a < 8; ++a) rc[a] = rot[8 * (size_t)i + a];
+        for (int a = 0; a < 8; ++a) {
+            if (st && (a == 3 || a == 5 || a == 6 || a == 7)) continue; /* kTemporalRotorIdx */
+            adam_scalar(&rc[a], &mi[8 + a], &vi[8 + a], g[8 + a], cfg->lr_rotor, bc1, bc2);
+        }
+        double nr[8];
+        int rcode = rotor_normalize(rc, nr);
+        if (rcode) return rcode;
+        if (st) nr[3] = nr[5] = nr[6] = nr[7] = 0;
+        for (int a = 0; a < 8; ++a) rot[8 * (size_t)i + a] = nr[a];
+        adam_scalar(&op[i], &mi[16], &vi[16], g[16], cfg->lr_opacity, bc1, bc2);
+        for (int c = 0; c < 16; ++c) {
+            double lr = c == 0 ? cfg->lr_sh_dc : cfg->lr_sh_rest;
+            for (int ch = 0; ch < 3; ++ch) {
+                int j = 17 + ch * 16 + c;
+                adam_scalar(&sh[48 * (size_t)i + ch * 16 + c], &mi[j], &vi[j], g[j], lr, bc1, bc2);
+            }
+        }
+    }
+    return ORC_OK;
+}
+
+/* optim.cpp:159-166 */
+void orc_accumulate_stats(int n, const double* vnorm, const uint8_t* visible, double* accum, int32_t* count) {
+    for (int i = 0; i < n; ++i) {
+        if (!visible[i]) continue;
+        accum[i] += vnorm[i];
+        count[i] += 1;
+    }
+}
+
+/* optim.cpp:236-243 */
+void orc_reset_opacity(int n, double* op, double* m_op, double* v_op, double value) {
+    for (int i = 0; i < n; ++i) {
+        double o = sigmoid(op[i]);
+        o = (value < o) ? value : o;
+        op[i] = log(o / (1 - o));
+        m_op[i] = 0;
+        v_op[i] = 0;
+    }
+}
+
+/* trainer.cpp:22-84: batch losses and summed gradients.  targets: n_frames images of
+ * H*W*3; nbrs (n*k) may be NULL (consistency skipped).  losses[5] = l1, ssim, entropy,
+ * consistency, total.  grads (n*65) / vnorm / visible may be NULL (no gradients). */
+int orc_evaluate_loss(int n, const double* mean, const double* ls, const double* rot, const double* op,
+                      const double* sh, int sh_degree, int n_frames, const orc_camera* cams,
+                      const double* targets, const orc_loss_weights* w, const double* bg, const int32_t* nbrs,
+                      int threads, double* losses, double* grads, double* vnorm, uint8_t* visible) {
+    double l1 = 0, ssim = 0, entropy = 0, consistency = 0;
+    const int want = grads != NULL;
+    if (want) {
+        memset(grads, 0, sizeof(double) * 65 * (size_t)n);
+        memset(vnorm, 0, sizeof(double) * (size_t)n);
+        memset(visible, 0, (size_t)n);
+    }
+    const double inv_b = n_frames == 0 ? 0 : 1 / (double)n_frames;
+    size_t off = 0;
+    for (int f = 0; f < n_frames; ++f) {
+        const orc_camera* cam = &cams[f];
+        const size_t nv = (size_t)cam->width * cam->height * 3;
+        const double* tgt = targets + off;
+        off += nv;
+        double* img = (double*)malloc(sizeof(double) * nv);
+        orc_records* rec = NULL;
+        int rc = orc_render_forward(n, mean, ls, rot, op, sh, sh_degree, cam, bg, threads, want, img, &rec);
+        if (rc) {
+            free(img);
+            return rc;
+        }
+        double sl = 0;
+        if (!want) {
+            l1 += orc_l1_loss((long long)nv, img, tgt, NULL) * inv_b;
+            rc = orc_ssim_loss(cam->width, cam->height, img, tgt, &sl, NULL);
+            if (rc) return rc;
+            ssim += sl * inv_b;
+        } else {
+            double* gl1 = (double*)malloc(sizeof(double) * nv);
+            double* gss = (double*)malloc(sizeof(double) * nv);
+            double lv = orc_l1_loss((long long)nv, img, tgt, gl1);
+            l1 += lv * inv_b;
+            rc = orc_ssim_loss(cam->width, cam->height, img, tgt, &sl, gss);
+            if (rc) return rc;
+            ssim += sl * inv_b;
+            const double wl1 = (1 - w->lambda_ssim) * inv_b;
+            const double wss = w->lambda_ssim * inv_b;
+            for (size_t i = 0; i < nv; ++i) gl1[i] = wl1 * gl1[i] + wss * gss[i];
+            double* fg = (double*)malloc(sizeof(double) * 65 * (size_t)n);
+            double* fv = (double*)malloc(sizeof(double) * (size_t)n);
+            uint8_t* fvis = (uint8_t*)malloc((size_t)n + 1);
+            rc = orc_render_backward(n, mean, ls, rot, op, sh, sh_degree, cam, rec, gl1, threads, fg, fv, fvis);
+            if (rc) return rc;
+            for (size_t i = 0; i < 65 * (size_t)n; ++i) grads[i] += fg[i];
+            for (int i = 0; i < n; ++i) {
+                vnorm[i] += fv[i];
+                visible[i] |= fvis[i];
+            }
+            free(fg);
+            free(fv);
+            free(fvis);
+            free(gl1);
+            free(gss);
+        }
+        orc_records_free(rec);
+        free(img);
+    }
+    if (w->lambda_entropy != 0) {
+        double* o = (double*)malloc(sizeof(double) * ((size_t)n + 1));
+        double* g = (double*)malloc(sizeof(double) * ((size_t)n + 1));
+        for (int i = 0; i < n; ++i) o[i] = sigmoid(op[i]);
+        entropy = orc_entropy_loss(n, o, want ? g : NULL);
+        if (want)
+            for (int i = 0; i < n; ++i)
+                grads[65 * (size_t)i + 16] += w->lambda_entropy * g[i] * o[i] * (1 - o[i]);
+        free(o);
+        free(g);
+    }
+    if (w->lambda_consistency != 0 && nbrs != NULL && n > 0) {
+        double* sp = (double*)malloc(sizeof(double) * 3 * (size_t)n);
+        double* gs = (double*)malloc(sizeof(double) * 3 * (size_t)n);
+        int rc = orc_gaussian_speeds(n, mean, ls, rot, sp);
+        if (rc) return rc;
+        consistency = orc_consistency_loss(n, sp, w->k_neighbors, nbrs, want ? gs : NULL);
+        if (want)
+            for (int i = 0; i < n; ++i) {
+                slice_cache c;
+                assemble_cache(ls + 4 * (size_t)i, rot + 8 * (size_t)i, &c);
+                c.dt = 0;
+                c.decay = 1; /* SliceCache default (gaussian.hpp:44) */
+                const double zero9[9] = {0}, zero3[3] = {0};
+                double ds[3];
+                for (int a = 0; a < 3; ++a) ds[a] = w->lambda_consistency * gs[3 * (size_t)i + a];
+                slice_backward(rot + 8 * (size_t)i, &c, zero9, zero3, 0, ds, grads + 65 * (size_t)i);
+            }
+        free(sp);
+        free(gs);
+    }
+    losses[0] = l1;
+    losses[1] = ssim;
+    losses[2] = entropy;
+    losses[3] = consistency;
+    losses[4] = (1 - w->lambda_ssim) * l1 + w->lambda_ssim * ssim + w->lambda_entropy * entropy +
+                w->lambda_consistency * consistency;
+    return ORC_OK;
+}

@@ -93,6 +93,39 @@ int orc_slice_at(const double* mean, const double* ls, const double* rot, double
 int orc_project(const double* sliced16, const orc_camera* cam, const double* sh48, int sh_degree,
                 double opacity_logit, orc_splat* out);
 
+/* ---- training side; image.cpp, ssim.cpp, loss.cpp, knn.cpp,
+ * optim.cpp, trainer.cpp.  65-vectors (gradients, Adam moments) are ordered mean4,
+ * log_scales4, rotor8, opacity_logit, sh48 channel-major. */
+typedef struct {
+    double lr_position, lr_position_final, lr_scales, lr_rotor, lr_sh_dc, lr_sh_rest, lr_opacity;
+    int total_steps;
+    int static_mode;
+} orc_adam_config; /* TrainConfig subset, optim.hpp:17-63 */
+
+typedef struct {
+    double lambda_ssim, lambda_entropy, lambda_consistency;
+    int k_neighbors;
+} orc_loss_weights; /* LossWeights, loss.hpp:11-16 */
+
+double orc_psnr(long long n_values, const double* a, const double* b);
+double orc_l1_loss(long long n_values, const double* rendered, const double* target, double* grad);
+void orc_ssim_window(double* k11);
+int orc_ssim_loss(int w, int h, const double* rendered, const double* target, double* loss, double* grad);
+double orc_entropy_loss(int n, const double* opacities, double* grad);
+double orc_consistency_loss(int n, const double* speeds, int k, const int32_t* nbrs, double* dspeed);
+void orc_scene_scales(int n, const double* mean, double* out4);
+int orc_knn4d(int n, const double* mean, int k, const double* scales, int threads, int32_t* nbrs);
+int orc_gaussian_speeds(int n, const double* mean, const double* ls, const double* rot, double* speeds);
+double orc_lr_schedule(int step, int total, double lr_init, double lr_final);
+int orc_adam_step(int n, double* mean, double* ls, double* rot, double* op, double* sh, double* m, double* v,
+                  const double* grads, const orc_adam_config* cfg, int step);
+void orc_accumulate_stats(int n, const double* vnorm, const uint8_t* visible, double* accum, int32_t* count);
+void orc_reset_opacity(int n, double* op, double* m_op, double* v_op, double value);
+int orc_evaluate_loss(int n, const double* mean, const double* ls, const double* rot, const double* op,
+                      const double* sh, int sh_degree, int n_frames, const orc_camera* cams,
+                      const double* targets, const orc_loss_weights* w, const double* bg, const int32_t* nbrs,
+                      int threads, double* losses, double* grads, double* vnorm, uint8_t* visible);
+
 #ifdef __cplusplus
 }
 #endif
