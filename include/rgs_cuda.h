@@ -45,6 +45,7 @@ typedef enum {
     RGS_E_NONFINITE_ROTOR = 4, /* NonFiniteRotorError (rotor.hpp:59-61, rotor.cpp:119,132-134) */
     RGS_E_CUDA = 5,            /* CUDA runtime failure */
     RGS_E_INVALID = 6,         /* bad argument (null pointer, size mismatch, ...) */
+    RGS_E_DEGENERATE_TIME = 7, /* DegenerateTimeError escaping gaussian_speed (gaussian.hpp:31-33) */
     RGS_E_NO_DEVICE = 8        /* no CUDA device: the product has no CPU fallback */
 } rgs_status;
 
@@ -55,6 +56,7 @@ typedef enum {
 #define RGS_FLAG_HOST_BUFFERS 8u   /* image / splat pointers are host memory */
 #define RGS_FLAG_IMAGE_F64 16u     /* image is double* (implies RGS_FLAG_BLEND_FP64): the reference's Image */
 #define RGS_FLAG_DETERMINISTIC 32u /* backward: FP64, reference summation order, no atomics (bitwise reproducible) */
+#define RGS_FLAG_ACCUMULATE_GRAD 64u /* rgs_image_loss: dL_dimage += instead of = */
 
 typedef struct rgs_ctx rgs_ctx;
 typedef struct rgs_scene rgs_scene;
@@ -219,6 +221,72 @@ int rgs_project_sliced(rgs_ctx* ctx, const double* sliced16, const rgs_camera* c
 /* Camera::validate (camera.hpp:21-26) on the host; RGS_E_CAMERA with the
  * reference's message on failure. */
 int rgs_camera_validate(rgs_ctx* ctx, const rgs_camera* cam);
+
+/* ---------------------------------------------------------------- training side
+ * The callers and data formats either side of the render path:
+ * evaluate_loss's image gradient (trainer.cpp:22-84), adam_step + accumulate_stats
+ * (optim.cpp:110-166), the entropy and consistency regularizers (loss.cpp:16-58) with
+ * their 4D KNN (knn.cpp:101-116), reset_opacity (optim.cpp:236-243) and scene_scales
+ * (trainer.cpp:12-20).  All device pointers; stream-ordered on the context stream. */
+
+/* Image losses and dL/dimage (image.cpp:20-36, ssim.cpp, trainer.cpp:41-50).
+ * rendered / target: H*W*3 floats.  dL_dimage (may be NULL: losses only) =
+ * w_l1 * d l1_loss/d rendered + w_ssim * d ssim_loss/d rendered (FP64 arithmetic in the
+ * reference's summation order, stored as float).  losses (may be NULL): [0] l1_loss,
+ * [1] ssim_loss = 1 - mean SSIM, [2] MSE (psnr = min(100, 10 log10(1/MSE)), image.cpp:7-18),
+ * each multiplied by loss_scale.  RGS_FLAG_ACCUMULATE adds into losses, RGS_FLAG_ACCUMULATE_GRAD
+ * into dL_dimage. */
+int rgs_image_loss(rgs_ctx* ctx, const float* rendered, const float* target, int width, int height,
+                   double w_l1, double w_ssim, double loss_scale, unsigned flags, float* dL_dimage,
+                   double* losses);
+
+/* TrainConfig subset of one optimizer step (optim.hpp:17-63) + the entropy weight
+ * (LossWeights::lambda_entropy, loss.hpp:12), folded into the step as trainer.cpp:55-64 does. */
+typedef struct {
+    double lr_position, lr_position_final, lr_scales, lr_rotor, lr_sh_dc, lr_sh_rest, lr_opacity;
+    int total_steps;
+    int static_mode;
+    double lambda_entropy;   /* 0: no entropy term */
+    int accumulate_stats;    /* 1: also accumulate_stats(vnorm, visible) (optim.cpp:159-166) */
+    unsigned flags;          /* RGS_FLAG_ACCUMULATE: losses[0] += entropy instead of = */
+} rgs_adam_config;
+
+/* Adam moments and densification statistics of one scene (GaussianStore::m_*, v_*,
+ * grad_accum, grad_count; gaussian.hpp:87-95), zero-initialised, in the scene's precision. */
+typedef struct rgs_optimizer rgs_optimizer;
+int rgs_optimizer_create(rgs_ctx* ctx, const rgs_scene* scene, rgs_optimizer** out);
+void rgs_optimizer_destroy(rgs_optimizer* opt);
+/* One bias-corrected Adam step (1-based `step`) over all 65 parameters, rotors
+ * re-normalised, static-mode masks (optim.cpp:110-157).  grads: 65*N floats (rgs_scene_params
+ * layout, e.g. rgs_render_backward with RGS_FLAG_ACCUMULATE over the batch); vnorm / visible as
+ * rgs_render_backward (needed with accumulate_stats).  losses (may be NULL): [0] = entropy_loss.
+ * Rotor errors are reported by rgs_optimizer_status (no host sync here). */
+int rgs_adam_step(rgs_ctx* ctx, rgs_scene* scene, rgs_optimizer* opt, const float* grads, const float* vnorm,
+                  const int32_t* visible, const rgs_adam_config* cfg, int step, double* losses);
+/* Synchronises; returns the ZeroRotor / NonFiniteRotor error of the steps since the last call. */
+int rgs_optimizer_status(rgs_ctx* ctx, rgs_optimizer* opt);
+/* Host arrays: m65 / v65 (N, 65) rows in the order mean4, log_scales4, rotor8, opacity_logit,
+ * sh48 channel-major; grad_accum N doubles; grad_count N ints.  Any may be NULL. */
+int rgs_optimizer_download(rgs_ctx* ctx, const rgs_optimizer* opt, double* m65, double* v65,
+                           double* grad_accum, int32_t* grad_count);
+int rgs_optimizer_upload(rgs_ctx* ctx, rgs_optimizer* opt, const double* m65, const double* v65,
+                         const double* grad_accum, const int32_t* grad_count);
+/* GaussianStore::reset_stats (gaussian.cpp:186-189). */
+int rgs_optimizer_reset_stats(rgs_ctx* ctx, rgs_optimizer* opt);
+/* reset_opacity (optim.cpp:236-243): opacity -> min(opacity, value), its moments zeroed. */
+int rgs_reset_opacity(rgs_ctx* ctx, rgs_scene* scene, rgs_optimizer* opt, double value);
+
+/* scene_scales (trainer.cpp:12-20) -> host out4.  Synchronises. */
+int rgs_scene_scales(rgs_ctx* ctx, const rgs_scene* scene, double* out4);
+/* build_knn4d (knn.cpp:101-116): neighbors[N*k] (device int32), exact, ordered by (distance,
+ * index) on mean / scales; scales = NULL uses rgs_scene_scales.  k in {1, 2, 4, 8, 16}. */
+int rgs_knn_build(rgs_ctx* ctx, const rgs_scene* scene, int k, const double* scales, int32_t* neighbors);
+/* consistency_loss (loss.cpp:33-58) over gaussian_speed (gaussian.cpp:103-110) and its
+ * gradient through slice_backward (trainer.cpp:66-77): grads (may be NULL) += lambda *
+ * dL/dparams; losses (may be NULL): [0] = consistency_loss (+= with RGS_FLAG_ACCUMULATE).
+ * Synchronises (DegenerateTimeError / rotor errors are reported). */
+int rgs_consistency(rgs_ctx* ctx, const rgs_scene* scene, const int32_t* neighbors, int k, double lambda,
+                    unsigned flags, float* grads, double* losses);
 
 #ifdef __cplusplus
 }

@@ -35,6 +35,7 @@ SOURCES = [
     ("k_raster.cu", []),
     ("k_binning.cu", []),
     ("k_misc.cu", []),
+    ("k_train.cu", ["-fmad=false"]),
     ("rgs_capi.cu", []),
 ]
 

@@ -383,4 +383,108 @@ __device__ __forceinline__ bool d_project_geom(const SliceState& s, const DevCam
     return true;
 }
 
+
+// gaussian.cpp:84-100 + rotor.cpp:138-194: the tail of slice_backward shared by the
+// render backward (K7) and the consistency regularizer -- from the 4x4 covariance
+// gradient G4 to d log_scales (out[4..7]) and d rotor (out[8..15], w.r.t. the stored,
+// pre-normalisation coefficients `rot`), accumulated.
+__device__ __forceinline__ void d_g4_backward(const SliceState& s, const double* rot, const double* G4,
+                                              double* out) {
+    // d log_scales: 2 q_k (R^T G4 R)_kk
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        double acc = 0;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            double ga = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) ga += G4[a * 4 + b] * s.R[b * 4 + k];
+            acc += s.R[a * 4 + k] * ga;
+        }
+        out[4 + k] += 2 * s.q[k] * acc;
+    }
+    // dL/dR = (G4 + G4^T) R diag(q)
+    double dR[16];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            double a = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) a += (G4[r * 4 + k] + G4[k * 4 + r]) * s.R[k * 4 + c];
+            dR[r * 4 + c] = a * s.q[c];
+        }
+    // through the quadratic forms (to_matrix_jacobian, rotor.cpp:183-194)
+    const double* v = s.nrm;
+    double drn[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#define RGS_JT(e, a, b, c)               \
+drn[a] += dR[e] * (c) * v[b];         \
+drn[b] += dR[e] * (c) * v[a];
+    RGS_JT(0, 0, 0, 1.0) RGS_JT(0, 1, 1, -1.0) RGS_JT(0, 2, 2, -1.0) RGS_JT(0, 3, 3, -1.0)
+    RGS_JT(0, 4, 4, 1.0) RGS_JT(0, 5, 5, 1.0) RGS_JT(0, 6, 6, 1.0) RGS_JT(0, 7, 7, -1.0)
+    RGS_JT(1, 1, 0, 2.0) RGS_JT(1, 2, 4, -2.0) RGS_JT(1, 3, 5, -2.0) RGS_JT(1, 6, 7, 2.0)
+    RGS_JT(2, 1, 4, 2.0) RGS_JT(2, 2, 0, 2.0) RGS_JT(2, 3, 6, -2.0) RGS_JT(2, 5, 7, -2.0)
+    RGS_JT(3, 1, 5, 2.0) RGS_JT(3, 2, 6, 2.0) RGS_JT(3, 3, 0, 2.0) RGS_JT(3, 4, 7, 2.0)
+    RGS_JT(4, 1, 0, -2.0) RGS_JT(4, 2, 4, -2.0) RGS_JT(4, 3, 5, -2.0) RGS_JT(4, 6, 7, -2.0)
+    RGS_JT(5, 0, 0, 1.0) RGS_JT(5, 1, 1, -1.0) RGS_JT(5, 2, 2, 1.0) RGS_JT(5, 3, 3, 1.0)
+    RGS_JT(5, 4, 4, -1.0) RGS_JT(5, 5, 5, -1.0) RGS_JT(5, 6, 6, 1.0) RGS_JT(5, 7, 7, -1.0)
+    RGS_JT(6, 1, 2, -2.0) RGS_JT(6, 3, 7, 2.0) RGS_JT(6, 4, 0, 2.0) RGS_JT(6, 5, 6, -2.0)
+    RGS_JT(7, 1, 3, -2.0) RGS_JT(7, 2, 7, -2.0) RGS_JT(7, 4, 6, 2.0) RGS_JT(7, 5, 0, 2.0)
+    RGS_JT(8, 1, 4, 2.0) RGS_JT(8, 2, 0, -2.0) RGS_JT(8, 3, 6, -2.0) RGS_JT(8, 5, 7, 2.0)
+    RGS_JT(9, 1, 2, -2.0) RGS_JT(9, 3, 7, -2.0) RGS_JT(9, 4, 0, -2.0) RGS_JT(9, 5, 6, -2.0)
+    RGS_JT(10, 0, 0, 1.0) RGS_JT(10, 1, 1, 1.0) RGS_JT(10, 2, 2, -1.0) RGS_JT(10, 3, 3, 1.0)
+    RGS_JT(10, 4, 4, -1.0) RGS_JT(10, 5, 5, 1.0) RGS_JT(10, 6, 6, -1.0) RGS_JT(10, 7, 7, -1.0)
+    RGS_JT(11, 1, 7, 2.0) RGS_JT(11, 2, 3, -2.0) RGS_JT(11, 4, 5, -2.0) RGS_JT(11, 6, 0, 2.0)
+    RGS_JT(12, 1, 5, 2.0) RGS_JT(12, 2, 6, 2.0) RGS_JT(12, 3, 0, -2.0) RGS_JT(12, 4, 7, -2.0)
+    RGS_JT(13, 1, 3, -2.0) RGS_JT(13, 2, 7, 2.0) RGS_JT(13, 4, 6, 2.0) RGS_JT(13, 5, 0, -2.0)
+    RGS_JT(14, 1, 7, -2.0) RGS_JT(14, 2, 3, -2.0) RGS_JT(14, 4, 5, -2.0) RGS_JT(14, 6, 0, -2.0)
+    RGS_JT(15, 0, 0, 1.0) RGS_JT(15, 1, 1, 1.0) RGS_JT(15, 2, 2, 1.0) RGS_JT(15, 3, 3, -1.0)
+    RGS_JT(15, 4, 4, 1.0) RGS_JT(15, 5, 5, -1.0) RGS_JT(15, 6, 6, -1.0) RGS_JT(15, 7, 7, -1.0)
+#undef RGS_JT
+    // normalize_jacobian^T (rotor.cpp:138-168): Jn^T w = j1^T (j2^T w), j2 symmetric.
+    double l2 = sqnorm8(rot);
+    double eps = rotor_epsilon(rot);
+    double grad[8], upd[8];
+    epsilon_gradient(rot, grad);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) upd[k] = rot[k];
+    double delta = 0, ddr[8];
+    const bool branch = fabs(eps) >= kEpsBranch;
+    if (branch) {
+        const double rad = smax(l2 * l2 - 4 * eps * eps, 0.0);
+        const double sq = smax(sqrt(rad), 1e-30);
+        const double den = l2 + sq;
+        delta = -2 * eps / den;
+        const double dde = -2 / den - 8 * eps * eps / (sq * den * den);
+        const double ddl = 2 * eps * (1 + l2 / sq) / (den * den);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            ddr[k] = dde * grad[k] + ddl * 2 * rot[k];
+            upd[k] = rot[k] + delta * grad[k];
+        }
+    }
+    const double len = sqrt(sqnorm8(upd));
+    double u[8], w2[8];
+    double udot = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        u[k] = upd[k] / len;
+        udot += u[k] * drn[k];
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) w2[k] = (drn[k] - u[k] * udot) / len;
+    double gdot = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) gdot += grad[k] * w2[k];
+    // epsilon Hessian pairs: (0,7)=+1, (1,6)=-1, (2,5)=+1, (3,4)=-1
+    const double Hw[8] = {w2[7], -w2[6], w2[5], -w2[4], -w2[3], w2[2], -w2[1], w2[0]};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        double r;
+        if (branch) r = w2[k] + ddr[k] * gdot + delta * Hw[k];
+        else r = w2[k] - grad[k] * gdot / l2;
+        out[8 + k] += r;
+    }
+}
+
 }  // namespace rgs_dev

@@ -1,0 +1,739 @@
+// Training-side kernels either side of the render path:
+//
+//   K8a k_ssim_fields   SSIM forward on the valid region + the per-position adjoint
+//                       seeds (ssim.cpp:74-125), block partial sums of SSIM
+//   K8b k_image_grad    adjoint convolutions (ssim.cpp:61-72, as gathers in the
+//                       reference's summation order) + L1 gradient (image.cpp:27-36)
+//                       -> dL/dimage = w_l1 g_l1 + w_ssim g_ssim (trainer.cpp:41-50),
+//                       block partial sums of |d| and d^2 (l1_loss, psnr)
+//   K9  k_adam_step     optim.cpp:110-166 fused: entropy gradient (loss.cpp:16-31,
+//                       trainer.cpp:55-64), accumulate_stats, Adam on all 65
+//                       parameters, rotor re-normalisation, static-mode masks
+//   K10 k_speeds / k_consistency / k_speed_backward
+//                       consistency regularizer (loss.cpp:33-58, trainer.cpp:66-77)
+//   K11 k_knn           exact 4D k-nearest neighbours (knn.cpp:101-116), brute force
+//       k_reset_opacity optim.cpp:236-243
+//
+// This TU is compiled with -fmad=false and keeps the reference's expression order, so
+// on identical inputs the SSIM/L1 image gradient, the Adam update (FP64 scenes) and the
+// neighbour lists are bit-identical to the reference; only block reductions of loss
+// scalars (fixed-order trees) and libm log in the entropy term differ in the last ulps.
+#include "fp64_math.cuh"
+#include "rgs_train.cuh"
+
+namespace rgs_dev {
+
+__constant__ double c_win[kSsimWin];
+
+// ---------------------------------------------------------------------------
+// Deterministic block reduction of one double (256 threads).
+__device__ __forceinline__ double block_sum(double v, double* red) {
+    const int t = threadIdx.x;
+    red[t] = v;
+    __syncthreads();
+#pragma unroll
+    for (int s = 128; s > 0; s >>= 1) {
+        if (t < s) red[t] = red[t] + red[t + s];
+        __syncthreads();
+    }
+    const double r = red[0];
+    __syncthreads();
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// K8a: SSIM forward over one tile of valid positions and one channel.
+// Tile: kSsimTX x kSsimTY valid positions; input footprint (TX+10) x (TY+10).
+__global__ void __launch_bounds__(256) k_ssim_fields(const float* __restrict__ img, const float* __restrict__ tgt,
+                                                     int W, int H, int want_grad, double* __restrict__ dfield,
+                                                     double* __restrict__ part_ssim) {
+    constexpr int TX = kSsimTX, TY = kSsimTY, IX = TX + kSsimWin - 1, IY = TY + kSsimWin - 1;
+    __shared__ float sa[IY][IX + 1];
+    __shared__ float sb[IY][IX + 1];
+    __shared__ double rows[5][IY][TX];
+    __shared__ double red[256];
+    const int vw = W - kSsimWin + 1, vh = H - kSsimWin + 1;
+    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY, ch = blockIdx.z;
+    const int t = threadIdx.x;
+    for (int e = t; e < IY * IX; e += 256) {
+        const int r = e / IX, c = e % IX;
+        const int gx = x0 + c, gy = y0 + r;
+        float a = 0.f, b = 0.f;
+        if (gx < W && gy < H) {
+            const size_t p = ((size_t)gy * W + gx) * 3 + ch;
+            a = img[p];
+            b = tgt[p];
+        }
+        sa[r][c] = a;
+        sb[r][c] = b;
+    }
+    __syncthreads();
+    // Horizontal pass (ssim.cpp:44-49): rows(x, y) = sum_i k_i in(x + i, y), from 0.
+    for (int e = t; e < IY * TX; e += 256) {
+        const int r = e / TX, c = e % TX;
+        double s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0;
+#pragma unroll
+        for (int i = 0; i < kSsimWin; ++i) {
+            const double a = sa[r][c + i], b = sb[r][c + i];
+            const double k = c_win[i];
+            s0 += k * a;
+            s1 += k * b;
+            s2 += k * (a * a);
+            s3 += k * (b * b);
+            s4 += k * (a * b);
+        }
+        rows[0][r][c] = s0;
+        rows[1][r][c] = s1;
+        rows[2][r][c] = s2;
+        rows[3][r][c] = s3;
+        rows[4][r][c] = s4;
+    }
+    __syncthreads();
+    const int c = t % TX, r = t / TX;
+    const int vx = x0 + c, vy = y0 + r;
+    double ssim = 0;
+    if (vx < vw && vy < vh) {
+        double m[5];
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            double s = 0;
+#pragma unroll
+            for (int i = 0; i < kSsimWin; ++i) s += c_win[i] * rows[q][r + i][c];
+            m[q] = s;
+        }
+        const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;
+        const double ux = m[0], uy = m[1];
+        const double vx2 = m[2] - ux * ux;
+        const double vy2 = m[3] - uy * uy;
+        const double vxy = m[4] - ux * uy;
+        const double a1 = 2 * ux * uy + C1, a2 = 2 * vxy + C2;
+        const double b1 = ux * ux + uy * uy + C1, b2 = vx2 + vy2 + C2;
+        ssim = (a1 * a2) / (b1 * b2);
+        if (want_grad) {
+            // ssim.cpp:104-120
+            const double d_ssim = 1;
+            const double d_a1 = d_ssim * a2 / (b1 * b2);
+            const double d_a2 = d_ssim * a1 / (b1 * b2);
+            const double d_b1 = -d_ssim * ssim / b1;
+            const double d_b2 = -d_ssim * ssim / b2;
+            double d_ux = d_a1 * 2 * uy + d_b1 * 2 * ux;
+            const double d_vx = d_b2;
+            const double d_vxy = d_a2 * 2;
+            d_ux += -2 * ux * d_vx - uy * d_vxy;
+            const size_t nv = (size_t)vw * vh, p = (size_t)vy * vw + vx;
+            double* base = dfield + (size_t)ch * 3 * nv;
+            base[p] = d_ux;
+            base[nv + p] = d_vx;
+            base[2 * nv + p] = d_vxy;
+        }
+    }
+    const double s = block_sum(ssim, red);
+    if (t == 0)
+        part_ssim[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = s;
+}
+
+// K8b: per output pixel and channel: adjoint convolutions of the three seeds, the SSIM
+// gradient, the L1 gradient and their weighted sum (FP32 dL/dimage for render_backward).
+__global__ void __launch_bounds__(256) k_image_grad(const float* __restrict__ img, const float* __restrict__ tgt,
+                                                    int W, int H, const double* __restrict__ dfield,
+                                                    ImageGradArgs a, float* __restrict__ dl,
+                                                    double* __restrict__ part_l1, double* __restrict__ part_sq) {
+    constexpr int TX = kSsimTX, TY = kSsimTY, DX = TX + kSsimWin - 1, DY = TY + kSsimWin - 1;
+    __shared__ double sd[3][DY][DX];
+    __shared__ double cols[3][TY][DX];
+    __shared__ double red[256];
+    const int vw = W - kSsimWin + 1, vh = H - kSsimWin + 1;
+    const int X0 = blockIdx.x * TX, Y0 = blockIdx.y * TY, ch = blockIdx.z;
+    const int dx0 = X0 - (kSsimWin - 1), dy0 = Y0 - (kSsimWin - 1);
+    const int t = threadIdx.x;
+    const bool grad = dl != nullptr;
+    if (grad && a.w_ssim != 0) {
+        const size_t nv = (size_t)vw * vh;
+        const double* base = dfield + (size_t)ch * 3 * nv;
+        for (int e = t; e < 3 * DY * DX; e += 256) {
+            const int q = e / (DY * DX), rem = e % (DY * DX), r = rem / DX, c = rem % DX;
+            const int x = dx0 + c, y = dy0 + r;
+            sd[q][r][c] = (x >= 0 && y >= 0 && x < vw && y < vh) ? base[q * nv + (size_t)y * vw + x] : 0.0;
+        }
+        __syncthreads();
+        // cols(x, Y) = sum over y ascending of k[Y - y] g(x, y)   (ssim.cpp:64-67)
+        for (int e = t; e < 3 * TY * DX; e += 256) {
+            const int q = e / (TY * DX), rem = e % (TY * DX), r = rem / DX, c = rem % DX;
+            const int Y = Y0 + r;
+            const int ylo = max(0, Y - (kSsimWin - 1)), yhi = min(vh - 1, Y);
+            double s = 0;
+            for (int y = ylo; y <= yhi; ++y) s += c_win[Y - y] * sd[q][y - dy0][c];
+            cols[q][r][c] = s;
+        }
+        __syncthreads();
+    }
+    const int c = t % TX, r = t / TX;
+    const int X = X0 + c, Y = Y0 + r;
+    double l1 = 0, sq = 0;
+    if (X < W && Y < H) {
+        const size_t p = ((size_t)Y * W + X) * 3 + ch;
+        const double xv = img[p], yv = tgt[p];
+        const double d = xv - yv;
+        l1 = fabs(d);
+        sq = d * d;
+        if (grad) {
+            double g_ssim = 0;
+            if (a.w_ssim != 0) {
+                // out(X, y) = sum over x ascending of k[X - x] cols(x, y)   (ssim.cpp:68-71)
+                const int xlo = max(0, X - (kSsimWin - 1)), xhi = min(vw - 1, X);
+                double g[3];
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    double s = 0;
+                    for (int x = xlo; x <= xhi; ++x) s += c_win[X - x] * cols[q][r][x - dx0];
+                    g[q] = s;
+                }
+                g_ssim = g[0] + 2 * xv * g[1] + yv * g[2];  // ssim.cpp:124-125
+                g_ssim *= a.ssim_scale;                     // -1 / count (ssim.cpp:131-134)
+            }
+            const double g_l1 = d > 0 ? a.inv_n : (d < 0 ? -a.inv_n : 0);  // image.cpp:33
+            const double v = a.w_l1 * g_l1 + a.w_ssim * g_ssim;            // trainer.cpp:47-49
+            dl[p] = a.accumulate ? (float)((double)dl[p] + v) : (float)v;
+        }
+    }
+    const double s1 = block_sum(l1, red);
+    const double s2 = block_sum(sq, red);
+    if (t == 0) {
+        const size_t b = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+        part_l1[b] = s1;
+        part_sq[b] = s2;
+    }
+}
+
+// Fixed-order sum of block partials -> losses[slot] (+)= scale * sum / denom.
+__global__ void __launch_bounds__(256) k_finalize(const double* __restrict__ parts, int n_parts, double denom,
+                                                  double scale, int one_minus, int accumulate, double* out) {
+    __shared__ double red[256];
+    double s = 0;
+    for (int i = threadIdx.x; i < n_parts; i += 256) s += parts[i];
+    const double tot = block_sum(s, red);
+    if (threadIdx.x == 0) {
+        double v = tot / denom;
+        if (one_minus) v = 1 - v;
+        v = v * scale;
+        *out = accumulate ? *out + v : v;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K9: fused optimizer step, one thread per Gaussian (optim.cpp:110-166).
+__device__ __forceinline__ void adam_scalar(double& p, double& m, double& v, double g, double lr, double bc1,
+                                            double bc2) {
+    // optim.cpp:19-23 (kAdamBeta1 = 0.9, kAdamBeta2 = 0.999, kAdamEps = 1e-15)
+    m = 0.9 * m + (1 - 0.9) * g;
+    v = 0.999 * v + (1 - 0.999) * g * g;
+    p -= lr * (m / bc1) / (sqrt(v / bc2) + 1e-15);
+}
+
+template <bool F64>
+struct StoreT {
+    using T = typename std::conditional<F64, double, float>::type;
+};
+
+template <bool F64>
+__device__ __forceinline__ void ld4(const void* base, int n, int blk, int i, double* v) {
+    if constexpr (F64) {
+        const double2* p = reinterpret_cast<const double2*>(static_cast<const double*>(base) + 4 * (size_t)blk * n) +
+                           2 * (size_t)i;
+        const double2 a = p[0], b = p[1];
+        v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+    } else {
+        const float4 f = reinterpret_cast<const float4*>(static_cast<const float*>(base) + 4 * (size_t)blk * n)[i];
+        v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+    }
+}
+template <bool F64>
+__device__ __forceinline__ void st4(void* base, int n, int blk, int i, const double* v) {
+    if constexpr (F64) {
+        double2* p = reinterpret_cast<double2*>(static_cast<double*>(base) + 4 * (size_t)blk * n) + 2 * (size_t)i;
+        p[0] = make_double2(v[0], v[1]);
+        p[1] = make_double2(v[2], v[3]);
+    } else {
+        reinterpret_cast<float4*>(static_cast<float*>(base) + 4 * (size_t)blk * n)[i] =
+            make_float4((float)v[0], (float)v[1], (float)v[2], (float)v[3]);
+    }
+}
+template <bool F64>
+__device__ __forceinline__ double ld1(const void* base, size_t idx) {
+    if constexpr (F64) return static_cast<const double*>(base)[idx];
+    else return static_cast<const float*>(base)[idx];
+}
+template <bool F64>
+__device__ __forceinline__ void st1(void* base, size_t idx, double v) {
+    if constexpr (F64) static_cast<double*>(base)[idx] = v;
+    else static_cast<float*>(base)[idx] = (float)v;
+}
+
+template <bool F64>
+__global__ void __launch_bounds__(128) k_adam_step(void* params, void* mom1, void* mom2, const float* __restrict__ grads,
+                                                   const float* __restrict__ vnorm, const int32_t* __restrict__ visible,
+                                                   double* __restrict__ accum, int32_t* __restrict__ count, int n,
+                                                   AdamArgs a, unsigned long long* err, double* part_entropy) {
+    __shared__ double red[256];
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    double ent = 0;
+    if (i < n) {
+        // accumulate_stats (optim.cpp:159-166), on the batch-summed view statistics.
+        if (a.stats && visible[i] > 0) {
+            accum[i] += (double)vnorm[i];
+            count[i] += 1;
+        }
+        double p[4], m[4], v[4], g[4];
+        // mean (x, y, z, t): lr_position schedule; static mode freezes t
+        ld4<F64>(params, n, 0, i, p);
+        ld4<F64>(mom1, n, 0, i, m);
+        ld4<F64>(mom2, n, 0, i, v);
+        ld4<false>(grads, n, 0, i, g);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (!(a.static_mode && k == 3)) adam_scalar(p[k], m[k], v[k], g[k], a.lr_pos, a.bc1, a.bc2);
+        st4<F64>(params, n, 0, i, p);
+        st4<F64>(mom1, n, 0, i, m);
+        st4<F64>(mom2, n, 0, i, v);
+        // log scales
+        ld4<F64>(params, n, 1, i, p);
+        ld4<F64>(mom1, n, 1, i, m);
+        ld4<F64>(mom2, n, 1, i, v);
+        ld4<false>(grads, n, 1, i, g);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (!(a.static_mode && k == 3)) adam_scalar(p[k], m[k], v[k], g[k], a.lr_scales, a.bc1, a.bc2);
+        st4<F64>(params, n, 1, i, p);
+        st4<F64>(mom1, n, 1, i, m);
+        st4<F64>(mom2, n, 1, i, v);
+        // rotor: Adam on the 8 stored coefficients, then normalize (rotor.cpp:117-136)
+        {
+            double rc[8], rm[8], rv[8], rg[8];
+            ld4<F64>(params, n, 2, i, rc);
+            ld4<F64>(params, n, 3, i, rc + 4);
+            ld4<F64>(mom1, n, 2, i, rm);
+            ld4<F64>(mom1, n, 3, i, rm + 4);
+            ld4<F64>(mom2, n, 2, i, rv);
+            ld4<F64>(mom2, n, 3, i, rv + 4);
+            ld4<false>(grads, n, 2, i, rg);
+            ld4<false>(grads, n, 3, i, rg + 4);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const bool temporal = (k == 3 || k == 5 || k == 6 || k == 7);  // kTemporalRotorIdx
+                if (!(a.static_mode && temporal)) adam_scalar(rc[k], rm[k], rv[k], rg[k], a.lr_rotor, a.bc1, a.bc2);
+            }
+            double nr[8];
+            const int code = d_normalize(rc, nr);
+            if (code) {
+                atomicMin(err, ((unsigned long long)i << 8) | (unsigned long long)code);
+            } else {
+                if (a.static_mode) nr[3] = nr[5] = nr[6] = nr[7] = 0;
+                st4<F64>(params, n, 2, i, nr);
+                st4<F64>(params, n, 3, i, nr + 4);
+            }
+            st4<F64>(mom1, n, 2, i, rm);
+            st4<F64>(mom1, n, 3, i, rm + 4);
+            st4<F64>(mom2, n, 2, i, rv);
+            st4<F64>(mom2, n, 3, i, rv + 4);
+        }
+        // opacity (+ entropy regularizer, loss.cpp:16-31 folded as trainer.cpp:55-64)
+        {
+            const size_t io = 64 * (size_t)n + i;
+            double po = ld1<F64>(params, io), mo = ld1<F64>(mom1, io), vo = ld1<F64>(mom2, io);
+            double go = grads[io];
+            if (a.lambda_entropy != 0) {
+                const double o = 1 / (1 + rgs_exp::glibc_exp(-po));  // GaussianStore::opacity
+                const double lo = 1e-6, hi = 1 - 1e-6;
+                const double oc = o < lo ? lo : (hi < o ? hi : o);
+                const double lg = log(oc);
+                ent = -oc * lg;
+                const double ge = (o > lo && o < hi) ? -(lg + 1) * a.inv_n : 0;
+                go = go + a.lambda_entropy * ge * o * (1 - o);
+            }
+            adam_scalar(po, mo, vo, go, a.lr_opacity, a.bc1, a.bc2);
+            st1<F64>(params, io, po);
+            st1<F64>(mom1, io, mo);
+            st1<F64>(mom2, io, vo);
+        }
+        // SH: block b holds coefficients j = 4b..4b+3, j = k*3 + ch; DC (k = 0) is j < 3
+#pragma unroll 1
+        for (int b = 0; b < 12; ++b) {
+            ld4<F64>(params, n, 4 + b, i, p);
+            ld4<F64>(mom1, n, 4 + b, i, m);
+            ld4<F64>(mom2, n, 4 + b, i, v);
+            ld4<false>(grads, n, 4 + b, i, g);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const double lr = (4 * b + e) < 3 ? a.lr_sh_dc : a.lr_sh_rest;
+                adam_scalar(p[e], m[e], v[e], g[e], lr, a.bc1, a.bc2);
+            }
+            st4<F64>(params, n, 4 + b, i, p);
+            st4<F64>(mom1, n, 4 + b, i, m);
+            st4<F64>(mom2, n, 4 + b, i, v);
+        }
+    }
+    if (part_entropy) {
+        // 128-thread blocks: pad the reduction buffer.
+        const int t = threadIdx.x;
+        red[t] = ent;
+        red[t + 128] = 0;
+        __syncthreads();
+        for (int s = 128; s > 0; s >>= 1) {
+            if (t < s) red[t] = red[t] + red[t + s];
+            __syncthreads();
+        }
+        if (t == 0) part_entropy[blockIdx.x] = red[0];
+    }
+}
+
+// optim.cpp:236-243: opacity -> min(opacity, value) in probability space; its moments zeroed.
+template <bool F64>
+__global__ void k_reset_opacity(void* params, void* mom1, void* mom2, int n, double value) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const size_t io = 64 * (size_t)n + i;
+    const double x = ld1<F64>(params, io);
+    double o = 1 / (1 + rgs_exp::glibc_exp(-x));
+    o = (value < o) ? value : o;  // std::min
+    st1<F64>(params, io, log(o / (1 - o)));
+    st1<F64>(mom1, io, 0.0);
+    st1<F64>(mom2, io, 0.0);
+}
+
+// ---------------------------------------------------------------------------
+// K10: consistency regularizer.
+// gaussian_speed (gaussian.cpp:103-110): V / W of the normalised 4D covariance.
+template <bool F64>
+__global__ void __launch_bounds__(128) k_speeds(ParamView P, double* __restrict__ speeds,
+                                                unsigned long long* err) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.n) return;
+    double mean4[4], ls[4], rot[8];
+    ld_block<F64>(P, 0, i, mean4);
+    ld_block<F64>(P, 1, i, ls);
+    ld_block<F64>(P, 2, i, rot);
+    ld_block<F64>(P, 3, i, rot + 4);
+    SliceState s;
+    const int code = d_slice(mean4, ls, rot, 0.0, s);
+    if (code > 0) {
+        atomicMin(err, ((unsigned long long)i << 8) | (unsigned long long)code);
+        return;
+    }
+    if (code < 0) {  // DegenerateTimeError escapes evaluate_loss in the reference
+        atomicMin(err, ((unsigned long long)i << 8) | (unsigned long long)kErrDegenerateTime);
+        return;
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) speeds[3 * (size_t)i + a] = s.V[a] / s.W;
+}
+
+// loss.cpp:33-58: loss partials and dL/dspeed (own term written, neighbour terms
+// scattered with FP64 atomics).
+__global__ void __launch_bounds__(256) k_consistency(const double* __restrict__ speeds,
+                                                     const int32_t* __restrict__ nbrs, int n, int k,
+                                                     double* __restrict__ dspeed, double* part) {
+    __shared__ double red[256];
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    double tot = 0;
+    if (i < n && k > 0) {
+        const double inv_n = 1 / (double)n, inv_k = 1 / (double)k;
+        double avg[3] = {0, 0, 0};
+        for (int j = 0; j < k; ++j) {
+            const int q = nbrs[(size_t)k * i + j];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) avg[a] += speeds[3 * (size_t)q + a];
+        }
+        double diff[3], sgn[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            avg[a] *= inv_k;
+            diff[a] = speeds[3 * (size_t)i + a] - avg[a];
+            sgn[a] = (double)(diff[a] > 0) - (double)(diff[a] < 0);
+        }
+        double s = fabs(diff[0]);
+        s += fabs(diff[1]);
+        s += fabs(diff[2]);
+        tot = s;
+        if (dspeed) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) atomicAdd(&dspeed[3 * (size_t)i + a], inv_n * sgn[a]);
+            for (int j = 0; j < k; ++j) {
+                const int q = nbrs[(size_t)k * i + j];
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+                    if (sgn[a] != 0) atomicAdd(&dspeed[3 * (size_t)q + a], -(inv_n * inv_k * sgn[a]));
+            }
+        }
+    }
+    const double s = block_sum(tot, red);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// slice_backward with only dL/dspeed (trainer.cpp:72-76): the speed gradient enters
+// G4 through V and W; added into the FP32 gradient block (log scales, rotor).
+template <bool F64>
+__global__ void __launch_bounds__(128) k_speed_backward(ParamView P, const double* __restrict__ dspeed,
+                                                        double lambda, float* grads) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.n) return;
+    double ds[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) ds[a] = lambda * dspeed[3 * (size_t)i + a];
+    if (ds[0] == 0 && ds[1] == 0 && ds[2] == 0) return;
+    double mean4[4], ls[4], rot[8];
+    ld_block<F64>(P, 0, i, mean4);
+    ld_block<F64>(P, 1, i, ls);
+    ld_block<F64>(P, 2, i, rot);
+    ld_block<F64>(P, 3, i, rot + 4);
+    SliceState s;
+    if (d_slice(mean4, ls, rot, 0.0, s) != 0) return;
+    const double W = s.W;
+    double G4[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) G4[e] = 0;
+    // gaussian.cpp:70-77 with dL_dmean3 = 0, dL_ddecay = 0, dL_dcov3 = 0
+    double vds = s.V[0] * ds[0];
+    vds += s.V[1] * ds[1];
+    vds += s.V[2] * ds[2];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) G4[a * 4 + 3] = ds[a] / W;
+    G4[15] = -vds / (W * W);
+    double out[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) out[e] = 0;
+    d_g4_backward(s, rot, G4, out);
+    const int n = P.n;
+    float4* gl = reinterpret_cast<float4*>(grads + 4 * (size_t)n) + i;
+    float4* g0 = reinterpret_cast<float4*>(grads + 8 * (size_t)n) + i;
+    float4* g1 = reinterpret_cast<float4*>(grads + 12 * (size_t)n) + i;
+    float4 t = *gl;
+    *gl = make_float4((float)((double)t.x + out[4]), (float)((double)t.y + out[5]), (float)((double)t.z + out[6]),
+                      (float)((double)t.w + out[7]));
+    t = *g0;
+    *g0 = make_float4((float)((double)t.x + out[8]), (float)((double)t.y + out[9]), (float)((double)t.z + out[10]),
+                      (float)((double)t.w + out[11]));
+    t = *g1;
+    *g1 = make_float4((float)((double)t.x + out[12]), (float)((double)t.y + out[13]), (float)((double)t.z + out[14]),
+                      (float)((double)t.w + out[15]));
+}
+
+// ---------------------------------------------------------------------------
+// K11: exact k nearest neighbours in scaled 4D coordinates (knn.cpp:101-116), ordered by
+// (squared distance, index) as KdTree4 guarantees (knn.hpp:18-20).  One thread per query,
+// candidates streamed through shared memory in tiles; top-k kept sorted in registers.
+template <int K>
+__global__ void __launch_bounds__(kKnnThreads) k_knn(const double4* __restrict__ pts, int n, int32_t* __restrict__ out) {
+    __shared__ double4 tile[kKnnTile];
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const double4 q = i < n ? pts[i] : make_double4(0, 0, 0, 0);
+    double bd[K];
+    int bi[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        bd[j] = INFINITY;
+        bi[j] = 0x7fffffff;
+    }
+    for (int base = 0; base < n; base += kKnnTile) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < kKnnTile; e += blockDim.x)
+            tile[e] = base + e < n ? pts[base + e] : make_double4(INFINITY, INFINITY, INFINITY, INFINITY);
+        __syncthreads();
+        const int lim = min(kKnnTile, n - base);
+        for (int e = 0; e < lim; ++e) {
+            const double4 p = tile[e];
+            const double d0 = p.x - q.x, d1 = p.y - q.y, d2 = p.z - q.z, d3 = p.w - q.w;
+            double dd = d0 * d0;
+            dd += d1 * d1;
+            dd += d2 * d2;
+            dd += d3 * d3;
+            const int j = base + e;
+            // j ascends, so a tie with the current worst never enters (index order kept).
+            if (dd < bd[K - 1] && j != i) {
+                double cd = dd;
+                int ci = j;
+#pragma unroll
+                for (int s = 0; s < K; ++s) {
+                    // insertion: keep (bd, bi) sorted by (distance, index)
+                    const bool less = cd < bd[s] || (cd == bd[s] && ci < bi[s]);
+                    const double td = bd[s];
+                    const int ti = bi[s];
+                    bd[s] = less ? cd : td;
+                    bi[s] = less ? ci : ti;
+                    cd = less ? td : cd;
+                    ci = less ? ti : ci;
+                }
+            }
+        }
+    }
+    if (i < n)
+#pragma unroll
+        for (int j = 0; j < K; ++j) out[(size_t)K * i + j] = bi[j];
+}
+
+// Scaled 4D points (mean / scene scales, knn.cpp:106).
+template <bool F64>
+__global__ void k_knn_points(ParamView P, double4 scales, double4* pts) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.n) return;
+    double m[4];
+    ld_block<F64>(P, 0, i, m);
+    pts[i] = make_double4(m[0] / scales.x, m[1] / scales.y, m[2] / scales.z, m[3] / scales.w);
+}
+
+// trainer.cpp:12-20: per-block min / max of the means (reduced on the host in order).
+template <bool F64>
+__global__ void __launch_bounds__(256) k_mean_extent(ParamView P, double* part_lo, double* part_hi) {
+    __shared__ double lo[4][256], hi[4][256];
+    const int i = blockIdx.x * blockDim.x + threadIdx.x, t = threadIdx.x;
+    double m[4];
+    if (i < P.n) {
+        ld_block<F64>(P, 0, i, m);
+    } else {
+        ld_block<F64>(P, 0, blockIdx.x * blockDim.x, m);  // block's first Gaussian: neutral for min/max
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) lo[a][t] = hi[a][t] = m[a];
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if (t < s)
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const double l = lo[a][t + s], h = hi[a][t + s];
+                lo[a][t] = l < lo[a][t] ? l : lo[a][t];
+                hi[a][t] = hi[a][t] < h ? h : hi[a][t];
+            }
+        __syncthreads();
+    }
+    if (t < 4) {
+        part_lo[4 * (size_t)blockIdx.x + t] = lo[t][0];
+        part_hi[4 * (size_t)blockIdx.x + t] = hi[t][0];
+    }
+}
+
+}  // namespace rgs_dev
+
+// ---------------------------------------------------------------------------
+namespace rgs_launch {
+using namespace rgs_dev;
+
+static inline int nblk(long long n, int t) { return (int)((n + t - 1) / t); }
+
+void set_ssim_window(const double* k11, cudaStream_t s) {
+    cudaMemcpyToSymbolAsync(c_win, k11, sizeof(double) * kSsimWin, 0, cudaMemcpyHostToDevice, s);
+}
+
+ImageLossGrid image_loss_grid(int W, int H) {
+    ImageLossGrid g;
+    const int vw = W - kSsimWin + 1, vh = H - kSsimWin + 1;
+    g.a_x = nblk(vw, kSsimTX);
+    g.a_y = nblk(vh, kSsimTY);
+    g.b_x = nblk(W, kSsimTX);
+    g.b_y = nblk(H, kSsimTY);
+    g.n_a = 3 * g.a_x * g.a_y;
+    g.n_b = 3 * g.b_x * g.b_y;
+    return g;
+}
+
+void image_loss(const float* img, const float* tgt, int W, int H, const ImageGradArgs& a, float* dl,
+                double* dfield, double* parts, double* losses, double loss_scale, int accumulate, cudaStream_t s) {
+    const ImageLossGrid g = image_loss_grid(W, H);
+    const double count = 3.0 * (double)(W - kSsimWin + 1) * (double)(H - kSsimWin + 1);
+    const double nvals = 3.0 * (double)W * (double)H;
+    double* pa = parts;
+    double* pl1 = parts + g.n_a;
+    double* psq = pl1 + g.n_b;
+    k_ssim_fields<<<dim3(g.a_x, g.a_y, 3), 256, 0, s>>>(img, tgt, W, H, dl != nullptr, dfield, pa);
+    k_image_grad<<<dim3(g.b_x, g.b_y, 3), 256, 0, s>>>(img, tgt, W, H, dfield, a, dl, pl1, psq);
+    if (losses) {
+        k_finalize<<<1, 256, 0, s>>>(pl1, g.n_b, nvals, loss_scale, 0, accumulate, losses + 0);
+        k_finalize<<<1, 256, 0, s>>>(pa, g.n_a, count, loss_scale, 1, accumulate, losses + 1);
+        k_finalize<<<1, 256, 0, s>>>(psq, g.n_b, nvals, loss_scale, 0, accumulate, losses + 2);
+    }
+}
+
+void adam_step(bool f64, void* params, void* m1, void* m2, const float* grads, const float* vnorm,
+               const int32_t* visible, double* accum, int32_t* count, int n, const AdamArgs& a,
+               unsigned long long* err, double* part_entropy, double* losses_entropy, int accumulate, cudaStream_t s) {
+    const int nb = nblk(n, 128);
+    if (f64)
+        k_adam_step<true><<<nb, 128, 0, s>>>(params, m1, m2, grads, vnorm, visible, accum, count, n, a, err,
+                                            part_entropy);
+    else
+        k_adam_step<false><<<nb, 128, 0, s>>>(params, m1, m2, grads, vnorm, visible, accum, count, n, a, err,
+                                             part_entropy);
+    if (part_entropy && losses_entropy)
+        k_finalize<<<1, 256, 0, s>>>(part_entropy, nb, (double)n, 1.0, 0, accumulate, losses_entropy);
+}
+
+int adam_blocks(int n) { return nblk(n, 128); }
+
+void reset_opacity(bool f64, void* params, void* m1, void* m2, int n, double value, cudaStream_t s) {
+    if (f64)
+        k_reset_opacity<true><<<nblk(n, 256), 256, 0, s>>>(params, m1, m2, n, value);
+    else
+        k_reset_opacity<false><<<nblk(n, 256), 256, 0, s>>>(params, m1, m2, n, value);
+}
+
+void speeds(const float* params, const double* params64, int n, double* out, unsigned long long* err,
+            cudaStream_t s) {
+    ParamView P{params, n, params64};
+    if (params64)
+        k_speeds<true><<<nblk(n, 128), 128, 0, s>>>(P, out, err);
+    else
+        k_speeds<false><<<nblk(n, 128), 128, 0, s>>>(P, out, err);
+}
+
+void consistency(const double* speeds, const int32_t* nbrs, int n, int k, double* dspeed, double* parts,
+                 double* losses_slot, int accumulate, cudaStream_t s) {
+    const int nb = nblk(n, 256);
+    k_consistency<<<nb, 256, 0, s>>>(speeds, nbrs, n, k, dspeed, parts);
+    if (losses_slot) k_finalize<<<1, 256, 0, s>>>(parts, nb, (double)n, 1.0, 0, accumulate, losses_slot);
+}
+
+int consistency_blocks(int n) { return nblk(n, 256); }
+
+void speed_backward(const float* params, const double* params64, int n, const double* dspeed, double lambda,
+                    float* grads, cudaStream_t s) {
+    ParamView P{params, n, params64};
+    if (params64)
+        k_speed_backward<true><<<nblk(n, 128), 128, 0, s>>>(P, dspeed, lambda, grads);
+    else
+        k_speed_backward<false><<<nblk(n, 128), 128, 0, s>>>(P, dspeed, lambda, grads);
+}
+
+void knn_points(const float* params, const double* params64, int n, const double* scales, double* pts4,
+                cudaStream_t s) {
+    ParamView P{params, n, params64};
+    const double4 sc = make_double4(scales[0], scales[1], scales[2], scales[3]);
+    if (params64)
+        k_knn_points<true><<<nblk(n, 256), 256, 0, s>>>(P, sc, reinterpret_cast<double4*>(pts4));
+    else
+        k_knn_points<false><<<nblk(n, 256), 256, 0, s>>>(P, sc, reinterpret_cast<double4*>(pts4));
+}
+
+int knn(const double* pts4, int n, int k, int32_t* out, cudaStream_t s) {
+    const double4* p = reinterpret_cast<const double4*>(pts4);
+    const int nb = nblk(n, kKnnThreads);
+    switch (k) {
+        case 1: k_knn<1><<<nb, kKnnThreads, 0, s>>>(p, n, out); break;
+        case 2: k_knn<2><<<nb, kKnnThreads, 0, s>>>(p, n, out); break;
+        case 4: k_knn<4><<<nb, kKnnThreads, 0, s>>>(p, n, out); break;
+        case 8: k_knn<8><<<nb, kKnnThreads, 0, s>>>(p, n, out); break;
+        case 16: k_knn<16><<<nb, kKnnThreads, 0, s>>>(p, n, out); break;
+        default: return -1;
+    }
+    return 0;
+}
+
+int extent_blocks(int n) { return nblk(n, 256); }
+
+void mean_extent(const float* params, const double* params64, int n, double* part_lo, double* part_hi,
+                 cudaStream_t s) {
+    ParamView P{params, n, params64};
+    if (params64)
+        k_mean_extent<true><<<nblk(n, 256), 256, 0, s>>>(P, part_lo, part_hi);
+    else
+        k_mean_extent<false><<<nblk(n, 256), 256, 0, s>>>(P, part_lo, part_hi);
+}
+
+}  // namespace rgs_launch

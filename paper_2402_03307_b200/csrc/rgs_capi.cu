@@ -1220,3 +1220,378 @@ int rgs_project_sliced(rgs_ctx* c, const double* sliced16, const rgs_camera* cam
 }
 
 }  // extern "C"
+
+// ===========================================================================
+// Training side: image losses, Adam, regularizers, KNN.
+#include "rgs_train.cuh"
+
+struct rgs_optimizer {
+    rgs_ctx* ctx = nullptr;
+    int n = 0;
+    bool f64 = false;
+    void* m1 = nullptr;              // Adam first moments, scene SoA layout and precision
+    void* m2 = nullptr;              // second moments
+    double* accum = nullptr;         // GaussianStore::grad_accum
+    int32_t* count = nullptr;        // GaussianStore::grad_count
+    unsigned long long* err = nullptr;  // rotor error word of the steps since the last status call
+    DevBuf part;                     // block partials (entropy)
+};
+
+namespace {
+
+// Host (N, 65) rows in the reference order -> the five upload arrays (and back).
+void split65(const double* r, size_t n, std::vector<double>& d) {
+    d.assign(65 * n, 0.0);
+    for (size_t i = 0; i < n; ++i) {
+        const double* s = r + 65 * i;
+        for (int a = 0; a < 4; ++a) d[4 * i + a] = s[a];
+        for (int a = 0; a < 4; ++a) d[4 * n + 4 * i + a] = s[4 + a];
+        for (int a = 0; a < 8; ++a) d[8 * n + 8 * i + a] = s[8 + a];
+        d[16 * n + i] = s[16];
+        for (int a = 0; a < 48; ++a) d[17 * n + 48 * i + a] = s[17 + a];
+    }
+}
+void join65(const std::vector<double>& d, size_t n, double* r) {
+    for (size_t i = 0; i < n; ++i) {
+        double* s = r + 65 * i;
+        for (int a = 0; a < 4; ++a) s[a] = d[4 * i + a];
+        for (int a = 0; a < 4; ++a) s[4 + a] = d[4 * n + 4 * i + a];
+        for (int a = 0; a < 8; ++a) s[8 + a] = d[8 * n + 8 * i + a];
+        s[16] = d[16 * n + i];
+        for (int a = 0; a < 48; ++a) s[17 + a] = d[17 * n + 48 * i + a];
+    }
+}
+
+// SoA device block (float or double) <-> host (N, 65) rows.
+void soa_upload(rgs_ctx* c, size_t n, bool f64, const double* rows, void* dst) {
+    std::vector<double> d;
+    split65(rows, n, d);
+    DevBuf tmp;
+    cudaStream_t s = c->stream;
+    if (f64) {
+        tmp.ensure(sizeof(double) * 65 * n, s);
+        double* t = tmp.as<double>();
+        CK(cudaMemcpyAsync(t, d.data(), sizeof(double) * 65 * n, cudaMemcpyHostToDevice, s));
+        rgs_launch::scene_pack64(t, t + 4 * n, t + 8 * n, t + 16 * n, t + 17 * n, (int)n, (double*)dst, s);
+    } else {
+        std::vector<float> f(d.begin(), d.end());
+        tmp.ensure(sizeof(float) * 65 * n, s);
+        float* t = tmp.as<float>();
+        CK(cudaMemcpyAsync(t, f.data(), sizeof(float) * 65 * n, cudaMemcpyHostToDevice, s));
+        rgs_launch::scene_pack(t, t + 4 * n, t + 8 * n, t + 16 * n, t + 17 * n, (int)n, (float*)dst, s);
+    }
+    c->launches += 1;
+    CK(cudaStreamSynchronize(s));
+    tmp.release(s);
+}
+void soa_download(rgs_ctx* c, size_t n, bool f64, const void* src, double* rows) {
+    DevBuf tmp;
+    cudaStream_t s = c->stream;
+    tmp.ensure(sizeof(double) * 65 * n, s);
+    double* t = tmp.as<double>();
+    rgs_launch::scene_unpack(f64 ? nullptr : (const float*)src, f64 ? (const double*)src : nullptr, (int)n, t,
+                             t + 4 * n, t + 8 * n, t + 16 * n, t + 17 * n, s);
+    c->launches += 1;
+    std::vector<double> d(65 * n);
+    CK(cudaMemcpyAsync(d.data(), t, sizeof(double) * 65 * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    tmp.release(s);
+    join65(d, n, rows);
+}
+
+// ssim.cpp:15-31 on the host (glibc exp), uploaded once per context.
+void ensure_ssim_window(rgs_ctx* c) {
+    static thread_local int done_device = -1;
+    if (done_device == c->device) return;
+    double k[kSsimWin], sum = 0;
+    for (int i = 0; i < kSsimWin; ++i) {
+        const double d = i - (kSsimWin - 1) / 2.0;
+        k[i] = std::exp(-d * d / (2 * 1.5 * 1.5));
+        sum += k[i];
+    }
+    for (double& v : k) v /= sum;
+    rgs_launch::set_ssim_window(k, c->stream);
+    CK(cudaStreamSynchronize(c->stream));
+    done_device = c->device;
+}
+
+struct TrainScratch {
+    DevBuf dfield, parts, speeds, dspeed, pts, lo, hi;
+};
+TrainScratch& train_scratch(rgs_ctx* c) {
+    // One scratch set per context (kept alongside the context's other buffers).
+    static thread_local std::vector<std::pair<rgs_ctx*, TrainScratch*>> reg;
+    for (auto& p : reg)
+        if (p.first == c) return *p.second;
+    reg.push_back({c, new TrainScratch});
+    return *reg.back().second;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rgs_image_loss(rgs_ctx* c, const float* rendered, const float* target, int width, int height, double w_l1,
+                   double w_ssim, double loss_scale, unsigned flags, float* dL_dimage, double* losses) {
+    if (!rendered || !target || width <= 0 || height <= 0) return RGS_E_INVALID;
+    if (width < kSsimWin || height < kSsimWin)
+        return set_err(c, RGS_E_INVALID, "ssim: image smaller than the 11x11 window");
+    return guarded(c, [&]() -> int {
+        cudaStream_t s = c->stream;
+        ensure_ssim_window(c);
+        TrainScratch& ts = train_scratch(c);
+        const ImageLossGrid g = rgs_launch::image_loss_grid(width, height);
+        const size_t nv = (size_t)(width - kSsimWin + 1) * (height - kSsimWin + 1);
+        if (dL_dimage) ts.dfield.ensure(sizeof(double) * 9 * nv, s);
+        ts.parts.ensure(sizeof(double) * (g.n_a + 2 * g.n_b + 16), s);
+        ImageGradArgs a;
+        a.w_l1 = w_l1;
+        a.w_ssim = w_ssim;
+        a.inv_n = 1 / (3.0 * (double)width * (double)height);
+        a.ssim_scale = -1 / (3.0 * (double)nv);
+        a.accumulate = (flags & RGS_FLAG_ACCUMULATE_GRAD) ? 1 : 0;
+        rgs_launch::image_loss(rendered, target, width, height, a, dL_dimage, ts.dfield.as<double>(),
+                               ts.parts.as<double>(), losses, loss_scale, (flags & RGS_FLAG_ACCUMULATE) ? 1 : 0, s);
+        c->launches += losses ? 5 : 2;
+        CK(cudaGetLastError());
+        return RGS_OK;
+    });
+}
+
+int rgs_optimizer_create(rgs_ctx* c, const rgs_scene* scene, rgs_optimizer** out) {
+    if (!scene || !out) return RGS_E_INVALID;
+    return guarded(c, [&]() -> int {
+        rgs_optimizer* o = new rgs_optimizer;
+        o->ctx = c;
+        o->n = scene->n;
+        o->f64 = scene->params64 != nullptr;
+        const size_t n1 = (size_t)std::max(scene->n, 1);
+        const size_t eb = o->f64 ? sizeof(double) : sizeof(float);
+        CK(cudaMalloc(&o->m1, 65 * n1 * eb));
+        CK(cudaMalloc(&o->m2, 65 * n1 * eb));
+        CK(cudaMalloc(&o->accum, n1 * sizeof(double)));
+        CK(cudaMalloc(&o->count, n1 * sizeof(int32_t)));
+        CK(cudaMalloc(&o->err, sizeof(unsigned long long)));
+        CK(cudaMemsetAsync(o->m1, 0, 65 * n1 * eb, c->stream));
+        CK(cudaMemsetAsync(o->m2, 0, 65 * n1 * eb, c->stream));
+        CK(cudaMemsetAsync(o->accum, 0, n1 * sizeof(double), c->stream));
+        CK(cudaMemsetAsync(o->count, 0, n1 * sizeof(int32_t), c->stream));
+        CK(cudaMemsetAsync(o->err, 0xff, sizeof(unsigned long long), c->stream));
+        o->part.ensure(sizeof(double) * (rgs_launch::adam_blocks(scene->n) + 16), c->stream);
+        CK(cudaStreamSynchronize(c->stream));
+        *out = o;
+        return RGS_OK;
+    });
+}
+
+void rgs_optimizer_destroy(rgs_optimizer* o) {
+    if (!o) return;
+    cudaSetDevice(o->ctx->device);
+    cudaStreamSynchronize(o->ctx->stream);
+    cudaFree(o->m1);
+    cudaFree(o->m2);
+    cudaFree(o->accum);
+    cudaFree(o->count);
+    cudaFree(o->err);
+    o->part.release(o->ctx->stream);
+    delete o;
+}
+
+int rgs_adam_step(rgs_ctx* c, rgs_scene* scene, rgs_optimizer* o, const float* grads, const float* vnorm,
+                  const int32_t* visible, const rgs_adam_config* cfg, int step, double* losses) {
+    if (!scene || !o || !grads || !cfg || step < 1) return RGS_E_INVALID;
+    if (o->n != scene->n || o->f64 != (scene->params64 != nullptr))
+        return set_err(c, RGS_E_INVALID, "adam_step: gradients not aligned with store");
+    if (cfg->accumulate_stats && (!vnorm || !visible)) return RGS_E_INVALID;
+    return guarded(c, [&]() -> int {
+        if (scene->n == 0) return RGS_OK;
+        // optim.cpp:112-115 on the host: std::pow, lr_schedule (optim.cpp:47-51)
+        AdamArgs a;
+        a.bc1 = 1 - std::pow(0.9, step);
+        a.bc2 = 1 - std::pow(0.999, step);
+        double lr_pos = cfg->lr_position;
+        if (cfg->total_steps > 0) {
+            double u = (double)step / (double)cfg->total_steps;
+            u = std::clamp(u, 0.0, 1.0);
+            lr_pos = cfg->lr_position * std::pow(cfg->lr_position_final / cfg->lr_position, u);
+        }
+        a.lr_pos = lr_pos;
+        a.lr_scales = cfg->lr_scales;
+        a.lr_rotor = cfg->lr_rotor;
+        a.lr_sh_dc = cfg->lr_sh_dc;
+        a.lr_sh_rest = cfg->lr_sh_rest;
+        a.lr_opacity = cfg->lr_opacity;
+        a.lambda_entropy = cfg->lambda_entropy;
+        a.inv_n = 1 / (double)scene->n;
+        a.static_mode = cfg->static_mode ? 1 : 0;
+        a.stats = cfg->accumulate_stats ? 1 : 0;
+        void* params = scene->params64 ? (void*)scene->params64 : (void*)scene->params;
+        const bool ent = losses && cfg->lambda_entropy != 0;
+        rgs_launch::adam_step(o->f64, params, o->m1, o->m2, grads, vnorm, visible, o->accum, o->count, scene->n, a,
+                              o->err, ent ? o->part.as<double>() : nullptr, ent ? losses : nullptr,
+                              (cfg->flags & RGS_FLAG_ACCUMULATE) ? 1 : 0, c->stream);
+        c->launches += ent ? 2 : 1;
+        CK(cudaGetLastError());
+        return RGS_OK;
+    });
+}
+
+int rgs_optimizer_status(rgs_ctx* c, rgs_optimizer* o) {
+    if (!o) return RGS_E_INVALID;
+    return guarded(c, [&]() -> int {
+        unsigned long long e = 0;
+        CK(cudaMemcpyAsync(&e, o->err, sizeof e, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (e == kNoError) return RGS_OK;
+        CK(cudaMemsetAsync(o->err, 0xff, sizeof(unsigned long long), c->stream));
+        const int code = (int)(e & 0xff);
+        c->err_index = (int)(e >> 8);
+        return set_err(c, code, rotor_msg(code));
+    });
+}
+
+int rgs_optimizer_download(rgs_ctx* c, const rgs_optimizer* o, double* m65, double* v65, double* grad_accum,
+                           int32_t* grad_count) {
+    if (!o) return RGS_E_INVALID;
+    return guarded(c, [&]() -> int {
+        const size_t n = (size_t)o->n;
+        if (n == 0) return RGS_OK;
+        if (m65) soa_download(c, n, o->f64, o->m1, m65);
+        if (v65) soa_download(c, n, o->f64, o->m2, v65);
+        if (grad_accum) CK(cudaMemcpyAsync(grad_accum, o->accum, 8 * n, cudaMemcpyDeviceToHost, c->stream));
+        if (grad_count) CK(cudaMemcpyAsync(grad_count, o->count, 4 * n, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        return RGS_OK;
+    });
+}
+
+int rgs_optimizer_upload(rgs_ctx* c, rgs_optimizer* o, const double* m65, const double* v65,
+                         const double* grad_accum, const int32_t* grad_count) {
+    if (!o) return RGS_E_INVALID;
+    return guarded(c, [&]() -> int {
+        const size_t n = (size_t)o->n;
+        if (n == 0) return RGS_OK;
+        if (m65) soa_upload(c, n, o->f64, m65, o->m1);
+        if (v65) soa_upload(c, n, o->f64, v65, o->m2);
+        if (grad_accum) CK(cudaMemcpyAsync(o->accum, grad_accum, 8 * n, cudaMemcpyHostToDevice, c->stream));
+        if (grad_count) CK(cudaMemcpyAsync(o->count, grad_count, 4 * n, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        return RGS_OK;
+    });
+}
+
+int rgs_optimizer_reset_stats(rgs_ctx* c, rgs_optimizer* o) {
+    if (!o) return RGS_E_INVALID;
+    return guarded(c, [&]() -> int {
+        const size_t n1 = (size_t)std::max(o->n, 1);
+        CK(cudaMemsetAsync(o->accum, 0, n1 * sizeof(double), c->stream));
+        CK(cudaMemsetAsync(o->count, 0, n1 * sizeof(int32_t), c->stream));
+        return RGS_OK;
+    });
+}
+
+int rgs_reset_opacity(rgs_ctx* c, rgs_scene* scene, rgs_optimizer* o, double value) {
+    if (!scene || !o || o->n != scene->n) return RGS_E_INVALID;
+    return guarded(c, [&]() -> int {
+        if (scene->n == 0) return RGS_OK;
+        void* params = scene->params64 ? (void*)scene->params64 : (void*)scene->params;
+        rgs_launch::reset_opacity(o->f64, params, o->m1, o->m2, scene->n, value, c->stream);
+        c->launches += 1;
+        CK(cudaGetLastError());
+        return RGS_OK;
+    });
+}
+
+int rgs_scene_scales(rgs_ctx* c, const rgs_scene* scene, double* out4) {
+    if (!scene || !out4) return RGS_E_INVALID;
+    return guarded(c, [&]() -> int {
+        const int n = scene->n;
+        if (n == 0) {
+            for (int a = 0; a < 4; ++a) out4[a] = 1e-3;  // (0 - 0).cwiseMax(1e-3)
+            return RGS_OK;
+        }
+        TrainScratch& ts = train_scratch(c);
+        const int nb = rgs_launch::extent_blocks(n);
+        ts.lo.ensure(sizeof(double) * 4 * nb, c->stream);
+        ts.hi.ensure(sizeof(double) * 4 * nb, c->stream);
+        rgs_launch::mean_extent(scene->params, scene->params64, n, ts.lo.as<double>(), ts.hi.as<double>(), c->stream);
+        c->launches += 1;
+        std::vector<double> lo(4 * (size_t)nb), hi(4 * (size_t)nb);
+        CK(cudaMemcpyAsync(lo.data(), ts.lo.p, sizeof(double) * 4 * nb, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(hi.data(), ts.hi.p, sizeof(double) * 4 * nb, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        for (int a = 0; a < 4; ++a) {
+            double l = lo[a], h = hi[a];
+            for (int b = 1; b < nb; ++b) {
+                l = std::min(l, lo[4 * (size_t)b + a]);
+                h = std::max(h, hi[4 * (size_t)b + a]);
+            }
+            out4[a] = std::max(h - l, 1e-3);  // trainer.cpp:19
+        }
+        return RGS_OK;
+    });
+}
+
+int rgs_knn_build(rgs_ctx* c, const rgs_scene* scene, int k, const double* scales, int32_t* neighbors) {
+    if (!scene || !neighbors || k <= 0) return RGS_E_INVALID;
+    if (scene->n <= k) return set_err(c, RGS_E_INVALID, "knn: need more points than neighbors");
+    if (!(k == 1 || k == 2 || k == 4 || k == 8 || k == 16))
+        return set_err(c, RGS_E_INVALID, "knn: k must be 1, 2, 4, 8 or 16");
+    return guarded(c, [&]() -> int {
+        double sc[4];
+        if (scales) {
+            for (int a = 0; a < 4; ++a) sc[a] = scales[a];
+        } else {
+            const int rc = rgs_scene_scales(c, scene, sc);
+            if (rc) return rc;
+        }
+        TrainScratch& ts = train_scratch(c);
+        ts.pts.ensure(sizeof(double) * 4 * (size_t)scene->n, c->stream);
+        rgs_launch::knn_points(scene->params, scene->params64, scene->n, sc, ts.pts.as<double>(), c->stream);
+        if (rgs_launch::knn(ts.pts.as<double>(), scene->n, k, neighbors, c->stream))
+            return set_err(c, RGS_E_INVALID, "knn: unsupported k");
+        c->launches += 2;
+        CK(cudaGetLastError());
+        return RGS_OK;
+    });
+}
+
+int rgs_consistency(rgs_ctx* c, const rgs_scene* scene, const int32_t* neighbors, int k, double lambda,
+                    unsigned flags, float* grads, double* losses) {
+    if (!scene || !neighbors || k <= 0) return RGS_E_INVALID;
+    return guarded(c, [&]() -> int {
+        const int n = scene->n;
+        if (n == 0) return RGS_OK;
+        cudaStream_t s = c->stream;
+        TrainScratch& ts = train_scratch(c);
+        ts.speeds.ensure(sizeof(double) * 3 * (size_t)n, s);
+        ts.parts.ensure(sizeof(double) * (rgs_launch::consistency_blocks(n) + 16), s);
+        DevBuf err;
+        err.ensure(sizeof(unsigned long long), s);
+        CK(cudaMemsetAsync(err.p, 0xff, sizeof(unsigned long long), s));
+        rgs_launch::speeds(scene->params, scene->params64, n, ts.speeds.as<double>(), err.as<unsigned long long>(), s);
+        double* dspeed = nullptr;
+        if (grads) {
+            ts.dspeed.ensure(sizeof(double) * 3 * (size_t)n, s);
+            CK(cudaMemsetAsync(ts.dspeed.p, 0, sizeof(double) * 3 * (size_t)n, s));
+            dspeed = ts.dspeed.as<double>();
+        }
+        rgs_launch::consistency(ts.speeds.as<double>(), neighbors, n, k, dspeed, ts.parts.as<double>(), losses,
+                                (flags & RGS_FLAG_ACCUMULATE) ? 1 : 0, s);
+        if (grads) rgs_launch::speed_backward(scene->params, scene->params64, n, dspeed, lambda, grads, s);
+        c->launches += 2 + (losses ? 1 : 0) + (grads ? 1 : 0);
+        unsigned long long e = 0;
+        CK(cudaMemcpyAsync(&e, err.p, sizeof e, cudaMemcpyDeviceToHost, s));
+        err.release(s);
+        CK(cudaStreamSynchronize(s));
+        if (e != kNoError) {
+            const int code = (int)(e & 0xff);
+            c->err_index = (int)(e >> 8);
+            if (code == kErrDegenerateTime) return set_err(c, RGS_E_DEGENERATE_TIME, "slice_at: temporal scale collapsed (W < 1e-12)");
+            return set_err(c, code, rotor_msg(code));
+        }
+        return RGS_OK;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,64 @@
+// Shared declarations of the training-side kernels (k_train.cu) and the C-ABI host code.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rgs_dev {
+
+constexpr int kSsimWin = 11;  // ssim.cpp:12
+constexpr int kSsimTX = 32;   // tile of valid positions / pixels per block (x)
+constexpr int kSsimTY = 8;    // (y); 256 threads
+constexpr int kKnnThreads = 128;
+constexpr int kKnnTile = 1024;
+constexpr int kErrDegenerateTime = 7;
+
+// dL/dimage assembly (trainer.cpp:41-50): w_l1 * l1_grad + w_ssim * ssim_grad.
+struct ImageGradArgs {
+    double w_l1, w_ssim;
+    double inv_n;       // 1 / (3 W H)               (image.cpp:31)
+    double ssim_scale;  // -1 / (3 (W-10) (H-10))    (ssim.cpp:131-134)
+    int accumulate;     // dL/dimage += instead of =
+};
+
+struct ImageLossGrid {
+    int a_x, a_y, b_x, b_y, n_a, n_b;
+};
+
+// One Adam step (optim.cpp:110-157); learning rate and bias corrections computed on the
+// host with the reference's std::pow.
+struct AdamArgs {
+    double lr_pos, lr_scales, lr_rotor, lr_sh_dc, lr_sh_rest, lr_opacity;
+    double bc1, bc2;
+    double lambda_entropy, inv_n;
+    int static_mode;
+    int stats;
+};
+
+}  // namespace rgs_dev
+
+namespace rgs_launch {
+using namespace rgs_dev;
+void set_ssim_window(const double* k11, cudaStream_t s);
+ImageLossGrid image_loss_grid(int W, int H);
+void image_loss(const float* img, const float* tgt, int W, int H, const ImageGradArgs& a, float* dl,
+                double* dfield, double* parts, double* losses, double loss_scale, int accumulate, cudaStream_t s);
+void adam_step(bool f64, void* params, void* m1, void* m2, const float* grads, const float* vnorm,
+               const int32_t* visible, double* accum, int32_t* count, int n, const AdamArgs& a,
+               unsigned long long* err, double* part_entropy, double* losses_entropy, int accumulate, cudaStream_t s);
+int adam_blocks(int n);
+void reset_opacity(bool f64, void* params, void* m1, void* m2, int n, double value, cudaStream_t s);
+void speeds(const float* params, const double* params64, int n, double* out, unsigned long long* err,
+            cudaStream_t s);
+void consistency(const double* speeds, const int32_t* nbrs, int n, int k, double* dspeed, double* parts,
+                 double* losses_slot, int accumulate, cudaStream_t s);
+int consistency_blocks(int n);
+void speed_backward(const float* params, const double* params64, int n, const double* dspeed, double lambda,
+                    float* grads, cudaStream_t s);
+void knn_points(const float* params, const double* params64, int n, const double* scales, double* pts4,
+                cudaStream_t s);
+int knn(const double* pts4, int n, int k, int32_t* out, cudaStream_t s);
+int extent_blocks(int n);
+void mean_extent(const float* params, const double* params64, int n, double* part_lo, double* part_hi,
+                 cudaStream_t s);
+}  // namespace rgs_launch

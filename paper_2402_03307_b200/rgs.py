@@ -36,6 +36,7 @@ RGS_E_ZERO_ROTOR = 3
 RGS_E_NONFINITE_ROTOR = 4
 RGS_E_CUDA = 5
 RGS_E_INVALID = 6
+RGS_E_DEGENERATE_TIME = 7
 RGS_E_NO_DEVICE = 8
 
 FLAG_RETAIN_RECORDS = 1
@@ -44,6 +45,7 @@ FLAG_ACCUMULATE = 4
 FLAG_HOST_BUFFERS = 8
 FLAG_IMAGE_F64 = 16
 FLAG_DETERMINISTIC = 32
+FLAG_ACCUMULATE_GRAD = 64
 SCENE_F64 = 1  # rgs_scene_create_ex storage flag
 
 
@@ -77,6 +79,14 @@ class NonFiniteRotorError(RuntimeError):
 
 class CameraError(RuntimeError):
     """std::runtime_error thrown by Camera::validate (camera.hpp:21-26)."""
+
+
+class DegenerateTimeError(RuntimeError):
+    """gaussian.hpp:31-33 (escapes gaussian_speed in the consistency term)."""
+
+    def __init__(self, msg="slice_at: temporal scale collapsed (W < 1e-12)", index=-1):
+        super().__init__(msg)
+        self.index = index
 
 
 # ----------------------------------------------------------------------------- ctypes
@@ -134,6 +144,10 @@ EXPORTS = [
     "rgs_records_export", "rgs_render_backward", "rgs_camera_validate", "rgs_profile_num_stages",
     "rgs_profile_stage_name", "rgs_ctx_set_profiling", "rgs_ctx_profile_reset", "rgs_ctx_profile_read",
     "rgs_measure_fp32_tflops", "rgs_project_sliced", "rgs_scene_create_ex", "rgs_scene_params_f64",
+    # training side (train.py)
+    "rgs_image_loss", "rgs_optimizer_create", "rgs_optimizer_destroy", "rgs_adam_step", "rgs_optimizer_status",
+    "rgs_optimizer_download", "rgs_optimizer_upload", "rgs_optimizer_reset_stats", "rgs_reset_opacity",
+    "rgs_scene_scales", "rgs_knn_build", "rgs_consistency",
 ]
 
 
@@ -184,6 +198,18 @@ def load_library(path: str = LIB_PATH):
         "rgs_ctx_profile_read": (i, [p, p, p, p]),
         "rgs_measure_fp32_tflops": (i, [p, p]),
         "rgs_project_sliced": (i, [p, p, p, p, i, d, p, p]),
+        "rgs_image_loss": (i, [p, p, p, i, i, d, d, d, ctypes.c_uint, p, p]),
+        "rgs_optimizer_create": (i, [p, p, p]),
+        "rgs_optimizer_destroy": (None, [p]),
+        "rgs_adam_step": (i, [p, p, p, p, p, p, p, i, p]),
+        "rgs_optimizer_status": (i, [p, p]),
+        "rgs_optimizer_download": (i, [p, p, p, p, p, p]),
+        "rgs_optimizer_upload": (i, [p, p, p, p, p, p]),
+        "rgs_optimizer_reset_stats": (i, [p, p]),
+        "rgs_reset_opacity": (i, [p, p, p, d]),
+        "rgs_scene_scales": (i, [p, p, p]),
+        "rgs_knn_build": (i, [p, p, i, p, p]),
+        "rgs_consistency": (i, [p, p, p, i, d, ctypes.c_uint, p, p]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -389,6 +415,8 @@ class Context:
             raise NonFiniteRotorError(msg, idx)
         if rc == RGS_E_CAMERA:
             raise CameraError(msg)
+        if rc == RGS_E_DEGENERATE_TIME:
+            raise DegenerateTimeError(msg, idx)
         if rc == RGS_E_NO_DEVICE:
             raise RgsUnavailableError(msg)
         raise RgsCudaError(f"[{rc}] {msg}")

@@ -1,0 +1,353 @@
+"""Training-side mirror of the reference over the CUDA C-ABI.
+
+Same names, argument meaning and defaults as /root/reference/proj/include/rgs:
+  TrainConfig / LossWeights / LossBreakdown         optim.hpp:17-63, loss.hpp:11-30
+  evaluate_loss(...)                                trainer.cpp:22-84
+  adam_step / accumulate_stats / reset_opacity      optim.cpp:110-166, 236-243
+  scene_scales / build_knn4d                        trainer.cpp:12-20, knn.cpp:101-116
+  l1_loss / ssim_loss / psnr                        image.cpp, ssim.cpp
+
+Everything runs on the device: the render forward / backward, the FP64 L1 + SSIM image
+gradient (rgs_image_loss), the fused Adam + entropy + statistics kernel (rgs_adam_step),
+the consistency regularizer (rgs_consistency) and its exact 4D KNN (rgs_knn_build).
+``Trainer`` is the step loop of train_from (trainer.cpp:102-189) for a replicated scene:
+under torch.distributed every rank renders its own views and one NCCL all-reduce(sum) of
+the [65 grads | viewspace_norm] block (+ the visible counts and the image losses)
+reproduces the single-process batch reduction of evaluate_loss (StoreGrads::add with
+visible as a count, gaussian.cpp:199-209); Adam then runs identically on every rank.
+torch supplies device memory, streams and the collective; it is plumbing, not the product.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import rgs
+from .rgs import CCamera, Camera, Context, DeviceScene, _ptr, _vp
+
+
+@dataclass
+class LossWeights:
+    """loss.hpp:11-16"""
+
+    lambda_ssim: float = 0.2
+    lambda_entropy: float = 0.01
+    lambda_consistency: float = 0.05
+    k_neighbors: int = 8
+
+
+@dataclass
+class LossBreakdown:
+    """loss.hpp:25-28"""
+
+    l1: float = 0.0
+    ssim: float = 0.0
+    entropy: float = 0.0
+    consistency: float = 0.0
+    total: float = 0.0
+    mse: float = 0.0  # of the batch (psnr = min(100, 10 log10(1 / mse)))
+
+
+def combine_losses(w: LossWeights, l1, ssim, entropy, consistency) -> float:
+    """loss.cpp:60-64"""
+    return (1 - w.lambda_ssim) * l1 + w.lambda_ssim * ssim + w.lambda_entropy * entropy + \
+        w.lambda_consistency * consistency
+
+
+@dataclass
+class TrainConfig:
+    """optim.hpp:17-63 (the fields the device step uses; dataset / densify fields kept for parity)."""
+
+    lr_position: float = 1.6e-4
+    lr_position_final: float = 1.6e-6
+    lr_scales: float = 5e-3
+    lr_rotor: float = 1e-3
+    lr_sh_dc: float = 2.5e-3
+    lr_sh_rest: float = 1.25e-4
+    lr_opacity: float = 0.05
+    total_steps: int = 2000
+    batch: int = 3
+    densify_grad_threshold: float = 2e-4
+    densify_from: int = 500
+    densify_until: int = 15000
+    densify_interval: int = 100
+    opacity_reset_interval: int = 3000
+    prune_opacity: float = 0.005
+    percent_dense: float = 0.01
+    split_factor: float = 1.6
+    reset_opacity_value: float = 0.01
+    min_gaussians: int = 16
+    max_gaussians: int = 200000
+    loss: LossWeights = field(default_factory=LossWeights)
+    background: Sequence[float] = (0.0, 0.0, 0.0)
+    static_mode: bool = False
+    knn_rebuild_interval: int = 100
+    sh_unlock_interval: int = 1000
+    log_interval: int = 50
+
+    def validate(self):
+        """optim.cpp:27-45 (the checks that concern the device step)."""
+        pos = lambda v: v > 0 and math.isfinite(v)  # noqa: E731
+        if not all(pos(v) for v in (self.lr_position, self.lr_position_final, self.lr_scales, self.lr_rotor,
+                                    self.lr_sh_dc, self.lr_sh_rest, self.lr_opacity)):
+            raise ValueError("TrainConfig: learning rates must be positive")
+        if self.total_steps < 0 or self.batch < 1:
+            raise ValueError("TrainConfig: batch must be >= 1")
+        if min(self.densify_interval, self.opacity_reset_interval, self.knn_rebuild_interval,
+               self.sh_unlock_interval) <= 0:
+            raise ValueError("TrainConfig: intervals must be positive")
+
+
+def lr_schedule(step: int, total: int, lr_init: float, lr_final: float) -> float:
+    """optim.cpp:47-51"""
+    if total <= 0:
+        return lr_init
+    u = min(max(step / total, 0.0), 1.0)
+    return lr_init * (lr_final / lr_init) ** u
+
+
+class CAdamConfig(ctypes.Structure):
+    """rgs_adam_config (include/rgs_cuda.h)."""
+
+    _fields_ = [
+        ("lr_position", ctypes.c_double),
+        ("lr_position_final", ctypes.c_double),
+        ("lr_scales", ctypes.c_double),
+        ("lr_rotor", ctypes.c_double),
+        ("lr_sh_dc", ctypes.c_double),
+        ("lr_sh_rest", ctypes.c_double),
+        ("lr_opacity", ctypes.c_double),
+        ("total_steps", ctypes.c_int),
+        ("static_mode", ctypes.c_int),
+        ("lambda_entropy", ctypes.c_double),
+        ("accumulate_stats", ctypes.c_int),
+        ("flags", ctypes.c_uint),
+    ]
+
+    @staticmethod
+    def from_config(cfg: TrainConfig, lambda_entropy: float = 0.0, accumulate_stats: bool = True,
+                    accumulate: bool = False) -> "CAdamConfig":
+        return CAdamConfig(cfg.lr_position, cfg.lr_position_final, cfg.lr_scales, cfg.lr_rotor, cfg.lr_sh_dc,
+                           cfg.lr_sh_rest, cfg.lr_opacity, int(cfg.total_steps), int(bool(cfg.static_mode)),
+                           float(lambda_entropy), int(bool(accumulate_stats)),
+                           rgs.FLAG_ACCUMULATE if accumulate else 0)
+
+
+class DeviceOptimizer:
+    """Adam moments + densification statistics of one DeviceScene (rgs_optimizer)."""
+
+    def __init__(self, ctx: Context, scene: DeviceScene):
+        h = _vp()
+        ctx.check(ctx.L.rgs_optimizer_create(ctx.h, scene.h, ctypes.byref(h)))
+        self.ctx, self.scene, self.h = ctx, scene, h
+
+    def step(self, grads, vnorm, visible, cfg: CAdamConfig, step: int, losses=None):
+        """adam_step (+ accumulate_stats, + entropy) on device buffers; no host sync."""
+        self.ctx.sync_stream()
+        self.ctx.check(self.ctx.L.rgs_adam_step(self.ctx.h, self.scene.h, self.h, _vp(_ptr(grads)),
+                                                _vp(_ptr(vnorm)) if vnorm is not None else None,
+                                                _vp(_ptr(visible)) if visible is not None else None,
+                                                ctypes.byref(cfg), int(step),
+                                                _vp(_ptr(losses)) if losses is not None else None))
+
+    def status(self):
+        """Raises the rotor error of the steps since the last call (synchronises)."""
+        self.ctx.check(self.ctx.L.rgs_optimizer_status(self.ctx.h, self.h))
+
+    def download(self):
+        n = self.scene.n
+        m, v = np.zeros((n, 65)), np.zeros((n, 65))
+        acc, cnt = np.zeros(n), np.zeros(n, dtype=np.int32)
+        self.ctx.check(self.ctx.L.rgs_optimizer_download(self.ctx.h, self.h, _vp(m.ctypes.data), _vp(v.ctypes.data),
+                                                         _vp(acc.ctypes.data), _vp(cnt.ctypes.data)))
+        return m, v, acc, cnt
+
+    def upload(self, m=None, v=None, accum=None, count=None):
+        def p(a, dt):
+            return None if a is None else np.ascontiguousarray(a, dtype=dt)
+
+        m, v, accum, count = p(m, np.float64), p(v, np.float64), p(accum, np.float64), p(count, np.int32)
+        self.ctx.check(self.ctx.L.rgs_optimizer_upload(
+            self.ctx.h, self.h, *[(_vp(a.ctypes.data) if a is not None else None) for a in (m, v, accum, count)]))
+
+    def reset_stats(self):
+        self.ctx.check(self.ctx.L.rgs_optimizer_reset_stats(self.ctx.h, self.h))
+
+    def reset_opacity(self, value: float = 0.01):
+        """optim.cpp:236-243"""
+        self.ctx.sync_stream()
+        self.ctx.check(self.ctx.L.rgs_reset_opacity(self.ctx.h, self.scene.h, self.h, float(value)))
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.L.rgs_optimizer_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def image_loss(ctx: Context, rendered, target, w_l1: float = 1.0, w_ssim: float = 0.0, dL_dimage=None,
+               losses=None, loss_scale: float = 1.0, accumulate: bool = False, accumulate_grad: bool = False):
+    """L1 + SSIM losses and dL/dimage on device tensors (rgs_image_loss).  ``accumulate``: losses
+    +=; ``accumulate_grad``: dL_dimage +=."""
+    h, w = int(rendered.shape[0]), int(rendered.shape[1])
+    ctx.sync_stream()
+    flags = (rgs.FLAG_ACCUMULATE if accumulate else 0) | (rgs.FLAG_ACCUMULATE_GRAD if accumulate_grad else 0)
+    ctx.check(ctx.L.rgs_image_loss(ctx.h, _vp(_ptr(rendered)), _vp(_ptr(target)), w, h, float(w_l1), float(w_ssim),
+                                   float(loss_scale), flags,
+                                   _vp(_ptr(dL_dimage)) if dL_dimage is not None else None,
+                                   _vp(_ptr(losses)) if losses is not None else None))
+
+
+def scene_scales(ctx: Context, scene: DeviceScene) -> np.ndarray:
+    """trainer.cpp:12-20"""
+    out = np.zeros(4)
+    ctx.check(ctx.L.rgs_scene_scales(ctx.h, scene.h, _vp(out.ctypes.data)))
+    return out
+
+
+def build_knn4d(ctx: Context, scene: DeviceScene, k: int, scales=None, out=None):
+    """knn.cpp:101-116 -> device int32 tensor (N, k)."""
+    import torch
+
+    if out is None:
+        out = torch.empty((scene.n, k), dtype=torch.int32, device=f"cuda:{ctx.device}")
+    sc = None if scales is None else np.ascontiguousarray(scales, dtype=np.float64)
+    ctx.sync_stream()
+    ctx.check(ctx.L.rgs_knn_build(ctx.h, scene.h, int(k), _vp(sc.ctypes.data) if sc is not None else None,
+                                  _vp(_ptr(out))))
+    return out
+
+
+def consistency(ctx: Context, scene: DeviceScene, nbrs, lam: float, grads=None, losses=None, accumulate=False):
+    """consistency_loss + its gradient through slice_backward (trainer.cpp:66-77)."""
+    ctx.sync_stream()
+    ctx.check(ctx.L.rgs_consistency(ctx.h, scene.h, _vp(_ptr(nbrs)), int(nbrs.shape[1]), float(lam),
+                                    rgs.FLAG_ACCUMULATE if accumulate else 0,
+                                    _vp(_ptr(grads)) if grads is not None else None,
+                                    _vp(_ptr(losses)) if losses is not None else None))
+
+
+# ----------------------------------------------------------------------------- multi-GPU plumbing
+def allreduce_step_buffers(gbuf, visible, losses_img, dist=None):
+    """The batch reduction across ranks: sum of [65 grads | viewspace_norm] (one NCCL call),
+    of the visible counts and of the three image-loss slots.  A no-op on one process.
+    Works on any backend (gloo on CPU in the tests, NCCL over NVLink on the GPUs)."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return
+    dist.all_reduce(gbuf)
+    dist.all_reduce(visible)
+    dist.all_reduce(losses_img)
+
+
+class Trainer:
+    """evaluate_loss + accumulate_stats + adam_step of train_from (trainer.cpp:121-150) on a
+    device-resident scene.  ``dist``: torch.distributed (initialised) for the multi-GPU
+    batch (each rank passes its own views; the batch size is views_per_rank * world)."""
+
+    def __init__(self, ctx: Context, scene: DeviceScene, config: TrainConfig, dist=None):
+        import torch
+
+        config.validate()
+        self.ctx, self.scene, self.cfg, self.dist = ctx, scene, config, dist
+        self.world = dist.get_world_size() if (dist is not None and dist.is_initialized()) else 1
+        dev = f"cuda:{ctx.device}"
+        n = scene.n
+        self.opt = DeviceOptimizer(ctx, scene)
+        self.gbuf = torch.zeros(66 * n, dtype=torch.float32, device=dev)  # [65 grads | viewspace_norm]
+        self.grads = self.gbuf[: 65 * n]
+        self.vnorm = self.gbuf[65 * n:]
+        self.visible = torch.zeros(n, dtype=torch.int32, device=dev)
+        self.losses = torch.zeros(8, dtype=torch.float64, device=dev)  # l1, ssim, mse, entropy, consistency
+        self.losses_host = torch.zeros(8, dtype=torch.float64).pin_memory()
+        self.nbrs = None
+        self.step_count = 0
+        self._img = None
+        self._dl = None
+
+    # trainer.cpp:107-113
+    def rebuild_knn(self):
+        w = self.cfg.loss
+        if w.lambda_consistency != 0 and self.scene.n > w.k_neighbors:
+            self.nbrs = build_knn4d(self.ctx, self.scene, w.k_neighbors, out=self.nbrs)
+        else:
+            self.nbrs = None
+
+    def _buffers(self, cam: Camera):
+        import torch
+
+        shape = (cam.height, cam.width, 3)
+        if self._img is None or tuple(self._img.shape) != shape:
+            dev = f"cuda:{self.ctx.device}"
+            self._img = torch.empty(shape, dtype=torch.float32, device=dev)
+            self._dl = torch.empty(shape, dtype=torch.float32, device=dev)
+        return self._img, self._dl
+
+    def evaluate_loss(self, cams: Sequence[Camera], targets, want_grads: bool = True):
+        """trainer.cpp:22-84 for this rank's views (device tensors); leaves the batch-reduced
+        gradients in self.grads / vnorm / visible and the losses in self.losses (device)."""
+        w = self.cfg.loss
+        ctx, scene = self.ctx, self.scene
+        self.gbuf.zero_()
+        self.visible.zero_()
+        self.losses.zero_()
+        inv_b = 1.0 / (len(cams) * self.world) if cams else 0.0
+        wl1, wss = (1 - w.lambda_ssim) * inv_b, w.lambda_ssim * inv_b
+        for cam, tgt in zip(cams, targets):
+            img, dl = self._buffers(cam)
+            img, rec = ctx.render_forward_device(scene, cam, self.cfg.background, retain=want_grads, image=img)
+            image_loss(ctx, img, tgt, wl1, wss, dl if want_grads else None, self.losses, loss_scale=inv_b,
+                       accumulate=True)
+            if want_grads:
+                ctx.render_backward_device(scene, cam, rec, dl, self.grads, self.vnorm, self.visible, accumulate=True)
+            rec.close()
+        allreduce_step_buffers(self.gbuf, self.visible, self.losses[:3], self.dist)
+        if w.lambda_consistency != 0 and self.nbrs is not None and scene.n > 0:
+            consistency(ctx, scene, self.nbrs, w.lambda_consistency, self.grads if want_grads else None,
+                        self.losses[4:5])
+
+    def step(self, cams: Sequence[Camera], targets) -> LossBreakdown:
+        """One train_from iteration minus densification (trainer.cpp:115-150): SH unlock, batch
+        loss + gradients, accumulate_stats, Adam, opacity reset and KNN rebuild schedules.
+        One host synchronisation: the loss scalars (and the rotor-error word) per step."""
+        cfg, w = self.cfg, self.cfg.loss
+        self.step_count += 1
+        step = self.step_count
+        sh = min(3, (step - 1) // cfg.sh_unlock_interval)
+        if sh != self.scene.sh_degree:
+            self.ctx.L.rgs_scene_set_sh_degree(self.scene.h, sh)
+            self.scene.sh_degree = sh
+        if self.nbrs is None and step == 1:
+            self.rebuild_knn()
+        self.evaluate_loss(cams, targets, True)
+        acfg = CAdamConfig.from_config(cfg, w.lambda_entropy, True)
+        self.opt.step(self.grads, self.vnorm, self.visible, acfg, step, self.losses[3:4])
+        if step % cfg.opacity_reset_interval == 0:
+            self.opt.reset_opacity(cfg.reset_opacity_value)
+        if step % cfg.knn_rebuild_interval == 0:
+            self.rebuild_knn()
+        return self.read_losses()
+
+    def read_losses(self) -> LossBreakdown:
+        self.losses_host.copy_(self.losses, non_blocking=True)
+        self.opt.status()  # synchronises the stream; raises rotor errors
+        h = self.losses_host.numpy()
+        w = self.cfg.loss
+        out = LossBreakdown(float(h[0]), float(h[1]), float(h[3]), float(h[4]), 0.0, float(h[2]))
+        out.total = combine_losses(w, out.l1, out.ssim, out.entropy, out.consistency)
+        return out
+
+
+def psnr_from_mse(mse: float) -> float:
+    """image.cpp:7-18"""
+    if mse <= 0:
+        return 100.0
+    return min(100.0, 10 * math.log10(1 / mse))

@@ -1,0 +1,261 @@
+"""GPU parity of the training side through the C ABI against the CPU
+oracle (oracle/rgs_oracle.c, pinned bit-exact to the reference's own training sources by
+tests/test_oracle_train.py).
+
+Bars: the image gradient (L1 + SSIM, FP64 in the reference order) is bit-identical to
+float(reference) on the same rendered image; Adam on FP64 scenes is bit-identical, on FP32
+scenes equal to the reference step rounded to float; KNN lists are identical; loss scalars
+within 1e-12 relative (fixed-order tree sums); the entropy term within 1e-12 (libm log);
+the consistency and full evaluate_loss gradients within relative 1e-3 (floored at
+1e-3 * max |column|, as the render backward)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2402_03307_b200 import rgs, scenes, train
+from paper_2402_03307_b200.rgs import DeviceScene
+
+from parity import floored_rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def T():
+    return O.train_ops("orc")
+
+
+def _t(a, dtype=None):
+    import torch
+
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype).cuda()
+
+
+@pytest.mark.parametrize("shape", [(37, 45), (200, 160), (800, 800)])
+def test_image_loss_bit_exact(ctx, T, shape):
+    import torch
+
+    h, w = shape
+    r = np.random.default_rng(h)
+    a = r.uniform(0, 1, (h, w, 3)).astype(np.float32)
+    b = np.clip(a + r.normal(0, 0.1, a.shape), 0, 1).astype(np.float32)
+    b[5, 7] = a[5, 7]
+    wl1, wss = 0.8 / 3, 0.2 / 3
+    dl = torch.zeros((h, w, 3), dtype=torch.float32, device="cuda")
+    losses = torch.zeros(4, dtype=torch.float64, device="cuda")
+    train.image_loss(ctx, _t(a), _t(b), wl1, wss, dl, losses, loss_scale=1.0)
+    torch.cuda.synchronize()
+    l1, g1 = T.l1_loss(a.astype(np.float64), b.astype(np.float64))
+    ss, gs = T.ssim_loss(a.astype(np.float64), b.astype(np.float64))
+    ref = (wl1 * g1 + wss * gs).astype(np.float32)
+    got = dl.cpu().numpy()
+    assert np.array_equal(got, ref), f"{np.count_nonzero(got != ref)} of {got.size} differ"
+    L = losses.cpu().numpy()
+    assert abs(L[0] - l1) <= 1e-12 * abs(l1)
+    assert abs(L[1] - ss) <= 1e-12 * max(abs(ss), 1e-3)
+    mse = float(np.mean((a.astype(np.float64) - b) ** 2))
+    assert abs(L[2] - mse) <= 1e-12 * mse
+    # losses only (no gradient buffer) and accumulation
+    train.image_loss(ctx, _t(a), _t(b), losses=losses, loss_scale=0.5, accumulate=True)
+    torch.cuda.synchronize()
+    assert abs(losses.cpu().numpy()[0] - 1.5 * l1) <= 1e-12 * l1
+
+
+def test_image_loss_rejects_small_images(ctx):
+    import torch
+
+    a = torch.zeros((10, 40, 3), dtype=torch.float32, device="cuda")
+    with pytest.raises(rgs.RgsCudaError):
+        train.image_loss(ctx, a, a)
+
+
+def _store_and_grads(n, seed, static=False):
+    store = scenes.random_scene(n, sh_degree=3, seed=seed)
+    if static:
+        store.rotor[:, [3, 5, 6, 7]] = 0.0
+    r = np.random.default_rng(seed)
+    g = r.normal(0, 1e-2, (n, 65)).astype(np.float32).astype(np.float64)
+    m = r.normal(0, 1e-3, (n, 65)).astype(np.float32).astype(np.float64)
+    v = r.uniform(0, 1e-5, (n, 65)).astype(np.float32).astype(np.float64)
+    return store, g, m, v
+
+
+def _grads_soa(g, n):
+    """(N, 65) reference order -> rgs_scene_params SoA float32 layout."""
+    out = np.zeros(65 * n, dtype=np.float32)
+    out[: 4 * n] = g[:, 0:4].reshape(-1)
+    out[4 * n: 8 * n] = g[:, 4:8].reshape(-1)
+    out[8 * n: 12 * n] = g[:, 8:12].reshape(-1)
+    out[12 * n: 16 * n] = g[:, 12:16].reshape(-1)
+    sh = g[:, 17:65].reshape(n, 3, 16).transpose(0, 2, 1).reshape(n, 48)  # j = k*3 + ch
+    out[16 * n: 64 * n] = sh.reshape(n, 12, 4).transpose(1, 0, 2).reshape(-1)
+    out[64 * n:] = g[:, 16]
+    return out
+
+
+@pytest.mark.parametrize("f64", [True, False])
+@pytest.mark.parametrize("static", [0, 1])
+def test_adam_step_matches_reference(ctx, T, f64, static):
+    import torch
+
+    n = 3000
+    store, g, m, v = _store_and_grads(n, 40 + static, bool(static))
+    sc = DeviceScene.from_store(ctx, store, f64=f64)
+    opt = train.DeviceOptimizer(ctx, sc)
+    opt.upload(m, v, np.zeros(n), np.zeros(n, dtype=np.int32))
+    cfg = train.TrainConfig(static_mode=bool(static), total_steps=500)
+    vis = torch.as_tensor(np.random.default_rng(1).integers(0, 3, n).astype(np.int32)).cuda()
+    vn = torch.as_tensor(np.random.default_rng(2).uniform(0, 1, n).astype(np.float32)).cuda()
+    opt.step(_t(_grads_soa(g, n)), vn, vis, train.CAdamConfig.from_config(cfg), 7)
+    opt.status()
+    ref_store, rm, rv = T.adam_step(store, m, v, g, O.adam_config(static_mode=static, total_steps=500), 7)
+    got = sc.download()
+    gm, gv, acc, cnt = opt.download()
+    want = O.OracleLib._scene(ref_store)
+    if f64:
+        for x, y in zip(got, want):
+            assert np.array_equal(x, y.reshape(x.shape))
+        assert np.array_equal(gm, rm) and np.array_equal(gv, rv)
+    else:
+        for x, y in zip(got, want):
+            assert np.array_equal(x, y.reshape(x.shape).astype(np.float32).astype(np.float64))
+        assert np.array_equal(gm, rm.astype(np.float32).astype(np.float64))
+        assert np.array_equal(gv, rv.astype(np.float32).astype(np.float64))
+    vis_h, vn_h = vis.cpu().numpy(), vn.cpu().numpy().astype(np.float64)
+    a2, c2 = T.accumulate_stats(vn_h, (vis_h > 0).astype(np.uint8), np.zeros(n), np.zeros(n, dtype=np.int32))
+    assert np.array_equal(acc, a2) and np.array_equal(cnt, c2)
+
+
+def test_adam_entropy_and_opacity_reset(ctx, T):
+    import torch
+
+    n = 2000
+    store, g, m, v = _store_and_grads(n, 77)
+    store.opacity_logit[:2] = [30.0, -30.0]  # clamp edges of the entropy term
+    sc = DeviceScene.from_store(ctx, store, f64=True)
+    opt = train.DeviceOptimizer(ctx, sc)
+    lam = 0.01
+    losses = torch.zeros(2, dtype=torch.float64, device="cuda")
+    cfg = train.CAdamConfig.from_config(train.TrainConfig(), lambda_entropy=lam, accumulate_stats=False)
+    opt.step(_t(_grads_soa(g, n)), None, None, cfg, 1, losses)
+    opt.status()
+    o = 1 / (1 + np.exp(-store.opacity_logit))
+    ent, ge = T.entropy_loss(o)
+    g2 = g.copy()
+    g2[:, 16] = g[:, 16] + lam * ge * o * (1 - o)
+    ref_store, _, _ = T.adam_step(store, np.zeros((n, 65)), np.zeros((n, 65)), g2, O.adam_config(), 1)
+    got_op = sc.download()[3]
+    assert np.allclose(got_op, ref_store.opacity_logit, rtol=0, atol=1e-12)
+    assert abs(losses.cpu().numpy()[0] - ent) <= 1e-12 * ent
+    opt.reset_opacity(0.01)
+    op2, m2, v2 = T.reset_opacity(sc.download()[3], np.ones(n), np.ones(n), 0.01)
+    assert np.allclose(sc.download()[3], op2, rtol=1e-14, atol=1e-14)
+    gm, gv, _, _ = opt.download()
+    assert not gm[:, 16].any() and not gv[:, 16].any()
+
+
+def test_adam_zero_rotor_error(ctx):
+    n = 50
+    store = scenes.random_scene(n, sh_degree=0, seed=3)
+    store.rotor[17] = 0.0
+    sc = DeviceScene.from_store(ctx, store)
+    opt = train.DeviceOptimizer(ctx, sc)
+    opt.step(_t(np.zeros(65 * n, np.float32)), None, None,
+             train.CAdamConfig.from_config(train.TrainConfig(), accumulate_stats=False), 1)
+    with pytest.raises(rgs.ZeroRotorError) as e:
+        opt.status()
+    assert e.value.index == 17
+    opt.status()  # cleared
+
+
+@pytest.mark.parametrize("k", [4, 8])
+def test_knn_and_scene_scales(ctx, T, k):
+    store = scenes.random_scene(3000, sh_degree=0, seed=k)
+    sc = DeviceScene.from_store(ctx, store, f64=True)
+    scales = train.scene_scales(ctx, sc)
+    assert np.array_equal(scales, T.scene_scales(store.mean))
+    nb = train.build_knn4d(ctx, sc, k).cpu().numpy()
+    assert np.array_equal(nb, T.knn4d(store.mean, k, scales, threads=8))
+
+
+def test_knn_ties(ctx, T):
+    store = scenes.random_scene(64, sh_degree=0, seed=1)
+    store.mean[:] = np.round(store.mean * 2) / 2  # many exact distance ties
+    sc = DeviceScene.from_store(ctx, store, f64=True)
+    nb = train.build_knn4d(ctx, sc, 8).cpu().numpy()
+    assert np.array_equal(nb, T.knn4d(store.mean, 8, train.scene_scales(ctx, sc)))
+
+
+def test_consistency_matches_reference(ctx, T):
+    import torch
+
+    n = 1500
+    store = scenes.random_scene(n, sh_degree=0, seed=9)
+    sc = DeviceScene.from_store(ctx, store, f64=True)
+    nb = train.build_knn4d(ctx, sc, 8)
+    grads = torch.zeros(65 * n, dtype=torch.float32, device="cuda")
+    losses = torch.zeros(1, dtype=torch.float64, device="cuda")
+    train.consistency(ctx, sc, nb, 0.05, grads, losses)
+    w = O.loss_weights(lambda_ssim=0.2, lambda_entropy=0.0, lambda_consistency=0.05)
+    L, g, _, _ = T.evaluate_loss(store, [], [], w, nbrs=nb.cpu().numpy())
+    assert abs(losses.cpu().numpy()[0] - L[3]) <= 1e-12 * L[3]
+    mean, ls, rot, op, sh = rgs.grads_from_soa(grads.cpu().numpy(), n)
+    got = np.concatenate([mean, ls, rot, op[:, None], sh.reshape(n, 48)], axis=1)
+    err = floored_rel_err(got, g)
+    assert err.max() <= 1e-3, err.max()
+
+
+def _training_case(n=2500, views=3, w=96, h=72, seed=5):
+    store = scenes.synthetic_scene(n, w, h, seed=seed)
+    cams = [scenes.bench_camera(w, h, 0.2 + 0.3 * k, scenes.yaw_pose(4.0 * k, (0.03, -0.01, 0.05)))
+            for k in range(views)]
+    truth = store.copy()
+    r = np.random.default_rng(seed)
+    store.mean[:, :3] += r.normal(0, 0.01, (n, 3)).astype(np.float32)
+    store.sh[:, :, 0] += r.normal(0, 0.1, (n, 3)).astype(np.float32)
+    return store, truth, cams
+
+
+def test_evaluate_loss_matches_reference(ctx, T):
+    """trainer.cpp:22-84 end to end on the device (render fwd, L1 + SSIM gradient, render bwd,
+    batch sum, entropy and consistency) against the oracle on the same scene and targets."""
+    import torch
+
+    store, truth, cams = _training_case()
+    tsc = DeviceScene.from_store(ctx, truth)
+    targets = [ctx.render_forward_device(tsc, c, retain=False)[0].clone() for c in cams]
+    sc = DeviceScene.from_store(ctx, store)
+    tr = train.Trainer(ctx, sc, train.TrainConfig())
+    tr.rebuild_knn()
+    tr.evaluate_loss(cams, targets)
+    torch.cuda.synchronize()
+    # entropy is folded into the Adam step on the device: compare it separately
+    w = O.loss_weights(lambda_entropy=0.0)
+    L, g, vn, vis = T.evaluate_loss(store, cams, [t.cpu().numpy().astype(np.float64) for t in targets], w,
+                                    nbrs=tr.nbrs.cpu().numpy(), threads=8)
+    got = tr.losses.cpu().numpy()
+    assert abs(got[0] - L[0]) <= 1e-5 * L[0]  # L1 of the float image vs the double image
+    assert abs(got[1] - L[1]) <= 1e-5 * max(L[1], 1e-3)
+    assert abs(got[4] - L[3]) <= 1e-9 * L[3]
+    n = store.size()
+    mean, ls, rot, op, sh = rgs.grads_from_soa(tr.grads.cpu().numpy(), n)
+    gg = np.concatenate([mean, ls, rot, op[:, None], sh.reshape(n, 48)], axis=1)
+    err = floored_rel_err(gg, g)
+    assert np.mean(err <= 1e-3) >= 0.999, (np.mean(err <= 1e-3), err.max())
+    assert np.array_equal(tr.visible.cpu().numpy() > 0, vis.astype(bool))
+    assert np.allclose(tr.vnorm.cpu().numpy(), vn, rtol=1e-3, atol=1e-3 * vn.max())
+
+
+def test_trainer_reduces_loss(ctx):
+    """A few device steps of train_from's loop lower the loss toward the target renders."""
+    store, truth, cams = _training_case(n=3000, views=4)
+    tsc = DeviceScene.from_store(ctx, truth)
+    targets = [ctx.render_forward_device(tsc, c, retain=False)[0].clone() for c in cams]
+    sc = DeviceScene.from_store(ctx, store)
+    tr = train.Trainer(ctx, sc, train.TrainConfig(total_steps=50, lr_sh_dc=2e-2))
+    first = tr.step(cams, targets)
+    for _ in range(30):
+        last = tr.step(cams, targets)
+    assert np.isfinite(last.total) and last.total < first.total
+    m, v, acc, cnt = tr.opt.download()
+    assert cnt.max() == 31 and acc.max() > 0

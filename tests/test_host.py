@@ -109,3 +109,48 @@ def test_bench_multi_rank_plumbing_gloo():
     assert [r[1] for r in res] == [11.0, 11.0]
     assert all(r[2] == 300 for r in res)
     assert res[0][3] != res[1][3]  # distinct camera poses per rank
+
+
+def _train_worker(rank, world, port, q):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2402_03307_b200 import train
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n = 5
+    # per-rank partial batch sums: grads|vnorm, visible counts, image losses
+    gbuf = torch.arange(66 * n, dtype=torch.float32) * (rank + 1)
+    vis = torch.tensor([1, 0, 0, 1, 0], dtype=torch.int32) if rank == 0 else torch.tensor([0, 0, 1, 1, 0],
+                                                                                           dtype=torch.int32)
+    losses = torch.zeros(8, dtype=torch.float64)
+    losses[:3] = torch.tensor([0.1, 0.2, 0.3], dtype=torch.float64) * (rank + 1)
+    losses[3] = 7.0  # entropy: replicated, must not be summed
+    train.allreduce_step_buffers(gbuf, vis, losses[:3], dist)
+    q.put((rank, gbuf.tolist(), vis.tolist(), losses.tolist()))
+    dist.destroy_process_group()
+
+
+def test_training_batch_reduction_gloo():
+    """Multi-GPU training plumbing (world 2, gloo): the all-reduce reproduces the single-process
+    batch reduction -- grads and viewspace norms summed, visible counted (> 0 == OR,
+    gaussian.cpp:199-209), image losses summed, replicated regularizer slots untouched."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_train_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    n = 5
+    for _, g, vis, losses in res:
+        assert g == [3.0 * k for k in range(66 * n)]
+        assert [v > 0 for v in vis] == [True, False, True, True, False]
+        assert np.allclose(losses[:3], [0.3, 0.6, 0.9]) and losses[3] == 7.0
