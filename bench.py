@@ -38,6 +38,13 @@ METRIC = "render FPS at 1352×1014 (300K 4D Gaussians)"
 WORKLOAD = "C2: 300K 4D rotor Gaussians, SH deg 3, 1352x1014, 300-timestamp forward-render sweep"
 L2_FLUSH_BYTES = 256 << 20
 
+# Training leg (config C3, reported under "train"): D-NeRF-shaped 800x800, 200K Gaussians,
+# TrainConfig's default batch of 3 camera x timestamp views per step and rank.
+TRAIN_N, TRAIN_W, TRAIN_H, TRAIN_BATCH, TRAIN_SEED, TRAIN_VIEWS = 200_000, 800, 800, 3, 3, 24
+TRAIN_WORKLOAD = ("C3: 200K 4D rotor Gaussians, SH deg 3, 800x800, batch of 3 camera x timestamp views per rank "
+                  "and step: render fwd + L1/SSIM image gradient + render bwd + batch all-reduce + entropy + "
+                  "consistency (exact 4D KNN, k=8) + accumulate_stats + Adam")
+
 
 def parse():
     ap = argparse.ArgumentParser()
@@ -48,6 +55,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="one warm sweep, no JSON (for ncu)")
+    ap.add_argument("--no-train", action="store_true", help="skip the C3 training leg")
+    ap.add_argument("--train-only", action="store_true", help="only the C3 training leg (profiling)")
+    ap.add_argument("--train-steps", type=int, default=10)
     return ap.parse_args()
 
 
@@ -174,6 +184,141 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- training leg
+def train_views(rank):
+    """TRAIN_VIEWS camera x timestamp views of rank `rank` (8 yaws x 3 times; distinct per rank)."""
+    from paper_2402_03307_b200 import scenes
+
+    cams = []
+    for v in range(TRAIN_VIEWS):
+        yaw = -6.0 + 12.0 * (v % 8) / 7 + 1.0 * rank
+        t = (v // 8 + 0.5) / 3
+        cams.append(scenes.bench_camera(TRAIN_W, TRAIN_H, t, scenes.yaw_pose(yaw, (0.02 * (v % 3), 0.0, 0.03))))
+    return cams
+
+
+def train_case():
+    """Ground-truth C3 scene (targets) and the perturbed copy that is trained."""
+    from paper_2402_03307_b200 import scenes
+
+    truth = scenes.synthetic_scene(TRAIN_N, TRAIN_W, TRAIN_H, seed=TRAIN_SEED)
+    store = truth.copy()
+    r = np.random.default_rng(TRAIN_SEED)
+    store.mean[:, :3] += r.normal(0, 0.01, (TRAIN_N, 3)).astype(np.float32)
+    store.sh[:, :, 0] += r.normal(0, 0.1, (TRAIN_N, 3)).astype(np.float32)
+    store.opacity_logit += r.normal(0, 0.2, TRAIN_N).astype(np.float32)
+    return truth, store
+
+
+def run_train_leg(args, ctx, dev, dist, rank, world, flush):
+    import torch
+
+    from paper_2402_03307_b200 import rgs, train
+
+    truth, store = train_case()
+    cams = train_views(rank)
+    tsc = rgs.DeviceScene.from_store(ctx, truth)
+    targets = torch.empty((TRAIN_VIEWS, TRAIN_H, TRAIN_W, 3), dtype=torch.float32, device=dev)
+    ctx.render_views(tsc, cams, (0.0, 0.0, 0.0), out=targets)
+    tsc.close()
+    scene = rgs.DeviceScene.from_store(ctx, store)
+    cfg = train.TrainConfig(batch=TRAIN_BATCH, total_steps=2000)
+    tr = train.Trainer(ctx, scene, cfg, dist)
+    stream = torch.cuda.current_stream(dev)
+    B = TRAIN_BATCH
+
+    def batch(k):
+        idx = [(k * B + j) % TRAIN_VIEWS for j in range(B)]
+        return [cams[i] for i in idx], [targets[i] for i in idx]
+
+    first = None
+    for k in range(max(args.warmup, 1)):
+        c, t = batch(k)
+        lb = tr.step(c, t)
+        first = first or lb
+    knn0 = time.perf_counter()
+    tr.rebuild_knn()
+    torch.cuda.synchronize(dev)
+    knn_ms = 1e3 * (time.perf_counter() - knn0)
+    launches0 = ctx.kernel_launches
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    flush.zero_()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for k in range(args.train_steps):
+        c, t = batch(args.warmup + k)
+        last = tr.step(c, t)
+    b.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = max_over_ranks(a.elapsed_time(b), dist, dev)
+    launches = ctx.kernel_launches - launches0
+    its = args.train_steps / (ms / 1e3)
+
+    # per-stage breakdown of one step (serialised CUDA events on the launching stream)
+    ctx.set_profiling(timing=True, count_evals=False)
+    ctx.profile_reset()
+    c, t = batch(0)
+    tr.step(c, t)
+    stages, _ = ctx.profile_read()
+    ctx.set_profiling(False, False)
+    stage_ms = {k: v[0] for k, v in stages.items() if v[1]}
+
+    # e2e: the same steps through the public API with each step's target images copied
+    # H2D from pinned host memory and the loss scalars read back (Trainer.step's D2H).
+    host_t = targets.cpu().pin_memory()
+    dev_t = torch.empty((B, TRAIN_H, TRAIN_W, 3), dtype=torch.float32, device=dev)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for k in range(args.train_steps):
+        idx = [(k * B + j) % TRAIN_VIEWS for j in range(B)]
+        for j, i in enumerate(idx):
+            dev_t[j].copy_(host_t[i], non_blocking=True)
+        tr.step([cams[i] for i in idx], [dev_t[j] for j in range(B)])
+    torch.cuda.synchronize(dev)
+    e2e_s = max_over_ranks(time.perf_counter() - t0, dist, dev)
+    e2e = {"value": args.train_steps / e2e_s, "unit": "it/s", "h2d_bytes_per_step": int(B * TRAIN_H * TRAIN_W * 12),
+           "d2h_bytes_per_step": 64, "steps": args.train_steps,
+           "note": "Trainer.step with the batch's target images H2D from pinned host memory each step and the "
+                   "loss scalars D2H (one host sync per step)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle
+
+        ops = oracle.train_ops("ref" if oracle.reference_available() else "orc")
+        threads = os.cpu_count() or 1
+        c, t = batch(0)
+        tg = [x.cpu().numpy().astype(np.float64) for x in t]
+        w = oracle.loss_weights()
+        t0 = time.perf_counter()
+        L, g, vn, vis = ops.evaluate_loss(store, c, tg, w, (0.0, 0.0, 0.0), None, threads=threads)
+        n = store.size()
+        ops.adam_step(store, np.zeros((n, 65)), np.zeros((n, 65)), g, oracle.adam_config(), 1)
+        cpu_s = time.perf_counter() - t0
+        cpu = {"value": 1.0 / cpu_s, "unit": "it/s", "cores": threads,
+               "kind": "reference" if ops.ref else "port",
+               "sample": f"1 training step (evaluate_loss over {B} views without the consistency KNN + adam_step), "
+                         f"{threads} threads, {cpu_model()}"}
+    return {
+        "metric": "train it/s", "value": its, "unit": "it/s", "ms_per_step": ms / args.train_steps,
+        "steps": args.train_steps, "warmup": max(args.warmup, 1), "n_gpus": world,
+        "views_per_step": B * world,
+        "config": {"workload": TRAIN_WORKLOAD, "n_gaussians": TRAIN_N, "width": TRAIN_W, "height": TRAIN_H,
+                   "batch_per_rank": B, "parallelism": f"dp{world}: replicated scene, NCCL all-reduce of "
+                                                         "[65 grads | viewspace norm | visible | image losses]",
+                   "l2": "256 MiB flush before the timed steps; per-step working set > L2"},
+        "loss_first": first.total, "loss_last": last.total, "psnr_last": train.psnr_from_mse(last.mse),
+        "knn_rebuild_ms": knn_ms, "stage_ms_one_step": stage_ms, "gpu_launches": launches,
+        "e2e": e2e, "cpu_baseline": cpu,
+    }
+
+
 # ----------------------------------------------------------------------------- ours
 def run_ours(args, rank, local_rank, world):
     import torch
@@ -188,9 +333,17 @@ def run_ours(args, rank, local_rank, world):
 
         dist.init_process_group("nccl", device_id=dev)
 
+    ctx = rgs.Context(local_rank)
+    if args.train_only:
+        flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+        res = run_train_leg(args, ctx, dev, dist, rank, world, flush)
+        if rank == 0:
+            print(json.dumps({"train": res}), flush=True)
+        if dist:
+            dist.destroy_process_group()
+        return
     store = scenes.synthetic_scene(N_GAUSS, W, H, seed=SEED)
     cams = sweep_for_rank(rank)
-    ctx = rgs.Context(local_rank)
     scene = rgs.DeviceScene.from_store(ctx, store)
     images = torch.empty((N_TIMES, H, W, 3), dtype=torch.float32, device=dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
@@ -335,6 +488,12 @@ def run_ours(args, rank, local_rank, world):
                "sample": f"{len(picks)} frames (t index {picks}) of the same sweep, full 1352x1014, "
                          f"{threads} threads, {cpu_model()}"}
 
+    train_res = None
+    if not args.no_train:
+        del images
+        torch.cuda.empty_cache()
+        train_res = run_train_leg(args, ctx, dev, dist, rank, world, flush)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
@@ -352,7 +511,7 @@ def run_ours(args, rank, local_rank, world):
             "stages_note": "per-stage CUDA events from a serialised profiling sweep after the timed region "
                            "(the timed sweeps pipeline 3 views over 3 streams, so stages overlap there)",
             "fp32_peak_tflops": fp32_peak, "clocks": clocks, "gpu_launches": launches,
-            "e2e": e2e, "cpu_baseline": cpu,
+            "e2e": e2e, "cpu_baseline": cpu, "train": train_res,
         }
         print(json.dumps(line), flush=True)
     if dist:

@@ -419,7 +419,7 @@ class TrainOps:
         mean, ls, rot, op, sh = OracleLib._scene(store)
         n = len(op)
         arr = (CCamera * len(cams))(*[make_ccamera(c) for c in cams])
-        tg = np.ascontiguousarray(np.concatenate([_d(t).reshape(-1) for t in targets]))
+        tg = np.ascontiguousarray(np.concatenate([_d(t).reshape(-1) for t in targets])) if len(targets) else np.zeros(1)
         losses = np.zeros(5)
         g = np.zeros((n, 65)) if want_grads else None
         vn = np.zeros(n) if want_grads else None

@@ -387,6 +387,12 @@ class Context:
         except ImportError:
             pass
 
+    def fence(self):
+        """Order later torch-stream work after this context's stream: a no-op when the context
+        runs on torch's current stream, a stream synchronisation otherwise."""
+        if not self._torch_stream:
+            self.synchronize()
+
     def close(self):
         if getattr(self, "h", None):
             self.L.rgs_ctx_destroy(self.h)

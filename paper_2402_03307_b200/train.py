@@ -205,6 +205,7 @@ def image_loss(ctx: Context, rendered, target, w_l1: float = 1.0, w_ssim: float 
                                    float(loss_scale), flags,
                                    _vp(_ptr(dL_dimage)) if dL_dimage is not None else None,
                                    _vp(_ptr(losses)) if losses is not None else None))
+    ctx.fence()
 
 
 def scene_scales(ctx: Context, scene: DeviceScene) -> np.ndarray:
@@ -224,6 +225,7 @@ def build_knn4d(ctx: Context, scene: DeviceScene, k: int, scales=None, out=None)
     ctx.sync_stream()
     ctx.check(ctx.L.rgs_knn_build(ctx.h, scene.h, int(k), _vp(sc.ctypes.data) if sc is not None else None,
                                   _vp(_ptr(out))))
+    ctx.fence()
     return out
 
 
@@ -296,6 +298,7 @@ class Trainer:
         gradients in self.grads / vnorm / visible and the losses in self.losses (device)."""
         w = self.cfg.loss
         ctx, scene = self.ctx, self.scene
+        ctx.fence()
         self.gbuf.zero_()
         self.visible.zero_()
         self.losses.zero_()
@@ -309,7 +312,13 @@ class Trainer:
             if want_grads:
                 ctx.render_backward_device(scene, cam, rec, dl, self.grads, self.vnorm, self.visible, accumulate=True)
             rec.close()
-        allreduce_step_buffers(self.gbuf, self.visible, self.losses[:3], self.dist)
+        if self.world > 1:
+            ctx.fence()
+            allreduce_step_buffers(self.gbuf, self.visible, self.losses[:3], self.dist)
+            if not ctx._torch_stream:
+                import torch
+
+                torch.cuda.current_stream(ctx.device).synchronize()
         if w.lambda_consistency != 0 and self.nbrs is not None and scene.n > 0:
             consistency(ctx, scene, self.nbrs, w.lambda_consistency, self.grads if want_grads else None,
                         self.losses[4:5])
@@ -337,6 +346,7 @@ class Trainer:
         return self.read_losses()
 
     def read_losses(self) -> LossBreakdown:
+        self.ctx.fence()
         self.losses_host.copy_(self.losses, non_blocking=True)
         self.opt.status()  # synchronises the stream; raises rotor errors
         h = self.losses_host.numpy()
