@@ -46,7 +46,8 @@ typedef enum {
     RGS_E_CUDA = 5,            /* CUDA runtime failure */
     RGS_E_INVALID = 6,         /* bad argument (null pointer, size mismatch, ...) */
     RGS_E_DEGENERATE_TIME = 7, /* DegenerateTimeError escaping gaussian_speed (gaussian.hpp:31-33) */
-    RGS_E_NO_DEVICE = 8        /* no CUDA device: the product has no CPU fallback */
+    RGS_E_NO_DEVICE = 8,       /* no CUDA device: the product has no CPU fallback */
+    RGS_E_CHECKPOINT = 9       /* CheckpointError (checkpoint.hpp:10-12) */
 } rgs_status;
 
 /* Render flags. */
@@ -275,6 +276,39 @@ int rgs_optimizer_upload(rgs_ctx* ctx, rgs_optimizer* opt, const double* m65, co
 int rgs_optimizer_reset_stats(rgs_ctx* ctx, rgs_optimizer* opt);
 /* reset_opacity (optim.cpp:236-243): opacity -> min(opacity, value), its moments zeroed. */
 int rgs_reset_opacity(rgs_ctx* ctx, rgs_scene* scene, rgs_optimizer* opt, double value);
+
+/* R4GS v1 checkpoint (checkpoint.hpp:14-23) straight into a new device scene: header checks
+ * and error messages as load_checkpoint (checkpoint.cpp:54-86); the 65-float records are
+ * staged through pinned memory and transposed to the SoA on the device.  scene_flags:
+ * RGS_SCENE_F64 for FP64 storage (the values are float32 either way). */
+int rgs_scene_load_checkpoint(rgs_ctx* ctx, const char* path, unsigned scene_flags, rgs_scene** out);
+/* save_checkpoint (checkpoint.cpp:29-52): float32 records, byte-identical to the reference. */
+int rgs_scene_save_checkpoint(rgs_ctx* ctx, const rgs_scene* scene, const char* path);
+
+/* The train loop's generator (std::mt19937_64 seeded with TrainConfig::seed, trainer.cpp:105):
+ * the batch picks (std::uniform_int_distribution<int>, trainer.cpp:106,119) and the normal
+ * draws of densify_and_prune come from the same engine, as in the reference. */
+typedef struct rgs_rng rgs_rng;
+int rgs_rng_create(unsigned long long seed, rgs_rng** out);
+void rgs_rng_destroy(rgs_rng* rng);
+int rgs_rng_uniform_int(rgs_rng* rng, int lo, int hi, int* out);
+
+/* TrainConfig's adaptive density control fields (optim.hpp:31-42). */
+typedef struct {
+    double densify_grad_threshold, percent_dense, split_factor, prune_opacity;
+    int min_gaussians, max_gaussians;
+    int static_mode;
+} rgs_densify_config;
+typedef struct {
+    int cloned, split, pruned;
+} rgs_densify_report; /* DensifyReport (optim.hpp:94-96) */
+/* densify_and_prune (optim.cpp:168-234) on the device scene and its optimizer state: clone /
+ * split decisions from the accumulated statistics, children appended in index order with the
+ * generator's normal draws, prune by opacity / size / temporal extent (lowest opacities first
+ * when bounded by min_gaussians), compaction, reset_stats.  The scene and optimizer are resized
+ * (rgs_scene_params pointers change).  Synchronises. */
+int rgs_densify_and_prune(rgs_ctx* ctx, rgs_scene* scene, rgs_optimizer* opt, const rgs_densify_config* cfg,
+                          double scene_extent, rgs_rng* rng, rgs_densify_report* report);
 
 /* scene_scales (trainer.cpp:12-20) -> host out4.  Synchronises. */
 int rgs_scene_scales(rgs_ctx* ctx, const rgs_scene* scene, double* out4);

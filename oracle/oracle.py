@@ -438,3 +438,45 @@ def train_ops(which: str = "orc") -> TrainOps:
     if key not in _cache:
         _cache[key] = TrainOps(restatement() if which == "orc" else reference_build())
     return _cache[key]
+
+
+class CDensifyConfig(ctypes.Structure):
+    """TrainConfig's adaptive density control fields (optim.hpp:31-42)."""
+
+    _fields_ = [
+        ("densify_grad_threshold", ctypes.c_double),
+        ("percent_dense", ctypes.c_double),
+        ("split_factor", ctypes.c_double),
+        ("prune_opacity", ctypes.c_double),
+        ("min_gaussians", ctypes.c_int),
+        ("max_gaussians", ctypes.c_int),
+        ("static_mode", ctypes.c_int),
+    ]
+
+
+def densify_config(**kw) -> CDensifyConfig:
+    c = CDensifyConfig(2e-4, 0.01, 1.6, 0.005, 16, 200000, 0)
+    for k, v in kw.items():
+        setattr(c, k, v)
+    return c
+
+
+def ref_densify_and_prune(store, m, v, accum, count, cfg, extent, seed):
+    """optim.cpp:168-234 in the reference build (no restatement: pinned directly)."""
+    L = reference_build().lib
+    mean, ls, rot, op, sh = OracleLib._scene(store)
+    n = len(op)
+    cap = 3 * n + 8
+    outs = [np.zeros((cap, 4)), np.zeros((cap, 4)), np.zeros((cap, 8)), np.zeros(cap), np.zeros((cap, 48)),
+            np.zeros((cap, 65)), np.zeros((cap, 65)), np.zeros(cap), np.zeros(cap, dtype=np.int32)]
+    rep = np.zeros(3, dtype=np.int32)
+    f = L.ref_densify_and_prune
+    f.restype = ctypes.c_int
+    k = f(ctypes.c_int(n), _p(mean), _p(ls), _p(rot), _p(op), _p(sh), _p(_d(m)), _p(_d(v)), _p(_d(accum)),
+          _p(np.ascontiguousarray(count, dtype=np.int32)), ctypes.byref(cfg), ctypes.c_double(extent),
+          ctypes.c_ulonglong(seed), _p(rep), ctypes.c_int(cap), *[_p(o) for o in outs])
+    if k < 0:
+        raise OracleError(99, "ref_densify_and_prune failed")
+    mean, ls, rot, op, sh, m, v, acc, cnt = [o[:k] for o in outs]
+    st = type(store)(mean, ls, rot, op, sh.reshape(k, 3, 16), store.active_sh_degree)
+    return st, m, v, acc, cnt, tuple(int(x) for x in rep)

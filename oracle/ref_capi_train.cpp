@@ -446,3 +446,54 @@ int ref_load_checkpoint(const char* path, double* mean, double* ls, double* rot,
 }
 
 }  // extern "C"
+
+extern "C" {
+typedef struct {
+    double densify_grad_threshold, percent_dense, split_factor, prune_opacity;
+    int min_gaussians, max_gaussians;
+    int static_mode;
+} ref_densify_config;
+
+// optim.cpp:168-234 with a std::mt19937_64(seed) as the train loop's generator.  Inputs are
+// the store (+ moments m/v as 65-rows, grad_accum, grad_count); outputs go to arrays of
+// capacity `cap` Gaussians.  Returns the new size (or -1); report3 = cloned, split, pruned.
+int ref_densify_and_prune(int n, const double* mean, const double* ls, const double* rot, const double* op,
+                          const double* sh, const double* m, const double* v, const double* accum,
+                          const int32_t* count, const ref_densify_config* cfg, double extent,
+                          unsigned long long seed, int* report3, int cap, double* mean_o, double* ls_o,
+                          double* rot_o, double* op_o, double* sh_o, double* m_o, double* v_o, double* accum_o,
+                          int32_t* count_o) {
+    try {
+        GaussianStore s = to_store2(n, mean, ls, rot, op, sh, 0);
+        moments_in(s, m, v);
+        for (int i = 0; i < n; ++i) {
+            s.grad_accum[i] = accum[i];
+            s.grad_count[i] = count[i];
+        }
+        TrainConfig t;
+        t.densify_grad_threshold = cfg->densify_grad_threshold;
+        t.percent_dense = cfg->percent_dense;
+        t.split_factor = cfg->split_factor;
+        t.prune_opacity = cfg->prune_opacity;
+        t.min_gaussians = cfg->min_gaussians;
+        t.max_gaussians = cfg->max_gaussians;
+        t.static_mode = cfg->static_mode != 0;
+        std::mt19937_64 rng(seed);
+        DensifyReport r = densify_and_prune(s, t, extent, rng);
+        report3[0] = r.cloned;
+        report3[1] = r.split;
+        report3[2] = r.pruned;
+        if (s.size() > cap) return -1;
+        from_store(s, mean_o, ls_o, rot_o, op_o, sh_o);
+        moments_out(s, m_o, v_o);
+        for (int i = 0; i < s.size(); ++i) {
+            accum_o[i] = s.grad_accum[i];
+            count_o[i] = s.grad_count[i];
+        }
+        return s.size();
+    } catch (const std::exception& e) {
+        fail(e);
+        return -1;
+    }
+}
+}

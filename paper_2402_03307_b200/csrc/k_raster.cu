@@ -22,7 +22,7 @@ struct StagedSplat {
     float4 a;  // (mx, my, ca2, cb2)   mean relative to the tile origin
     float4 b;  // (cc2, D, pa2, cs2n)  D: error floor incl. the mean's FP32 rounding
     float4 c;  // (r, g, b, alpha_base)   flow: (fx, fy, 0, alpha_base)
-    float4 d;  // (ex, ey, pc2, 0)     culling extents, clamp-gate power
+    float4 d;  // (ex, ey, pc2, R)     culling extents, clamp-gate power, R >= 1 / (1 - alpha_max)
 };
 
 template <bool FLOW>
@@ -42,7 +42,9 @@ __device__ __forceinline__ void stage(const SplatArrays& sp, uint32_t id, double
     } else {
         dst->c = make_float4(col.x, col.y, col.z, cf.w);
     }
-    dst->d = make_float4(e.x, e.y, g.y, 0.f);
+    // 1 / (1 - alpha) <= 1 / (1 - min(0.99, ab)): the T-gate error bound without a reciprocal
+    const float am = fminf(0.99f, cf.w);
+    dst->d = make_float4(e.x, e.y, g.y, __fdiv_ru(1.f, __fsub_rd(1.f, am)) * 1.000001f);
 }
 
 __device__ __forceinline__ bool overlaps(const StagedSplat& s, float sx0, float sy0) {
@@ -52,20 +54,29 @@ __device__ __forceinline__ bool overlaps(const StagedSplat& s, float sx0, float 
 
 enum { kSkip = 0, kAccept = 1, kAmbiguous = 2 };
 
-// Gate classification shared by K5 and K6: explicit-rounding intrinsics, so both
-// kernels compute bit-identical p2 / M and take identical decisions.
-__device__ __forceinline__ int classify(const float4& a, const float4& b, float fpx, float fpy, float& p, float& M,
-                                        float& dx, float& dy) {
+// Gate values shared by K5 and K6: explicit-rounding intrinsics, so both kernels compute
+// bit-identical p2 / M and take identical decisions.
+__device__ __forceinline__ void gate_values(const float4& a, const float4& b, float fpx, float fpy, float& p, float& M,
+                                            float& dx, float& dy) {
     dx = __fsub_rn(fpx, a.x);
     dy = __fsub_rn(fpy, a.y);
     const float t = __fmul_rn(a.z, dx), u = __fmul_rn(b.x, dy), v = __fmul_rn(a.w, dx);
     const float q = __fmaf_rn(t, dx, __fmul_rn(u, dy));  // ca2 dx^2 + cc2 dy^2  (<= 0)
     p = __fmaf_rn(v, dy, q);                             // log2(e) * power
     M = __fmaf_rn(b.w, q, b.y);                          // error bound of p
-    if (__fadd_rn(p, M) < b.z) return kSkip;             // alpha < 1/255 for certain
-    if (p > -M) return (p > M) ? kSkip : kAmbiguous;     // power > 0 gate
-    if (__fsub_rn(p, M) <= b.z) return kAmbiguous;       // alpha gate within the bound
-    return kAccept;
+}
+// alpha < 1/255 for certain, or power > 0 for certain
+__device__ __forceinline__ bool gate_skip(float p, float M, float pa2) { return (__fadd_rn(p, M) < pa2) | (p > M); }
+// (not skipped and) power > 0 or alpha < 1/255 within the bound
+__device__ __forceinline__ bool gate_ambiguous(float p, float M, float pa2) {
+    return (p > -M) | (__fsub_rn(p, M) <= pa2);
+}
+
+__device__ __forceinline__ int classify(const float4& a, const float4& b, float fpx, float fpy, float& p, float& M,
+                                        float& dx, float& dy) {
+    gate_values(a, b, fpx, fpy, p, M, dx, dy);
+    if (gate_skip(p, M, b.z)) return kSkip;
+    return gate_ambiguous(p, M, b.z) ? kAmbiguous : kAccept;
 }
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -125,25 +136,20 @@ __global__ void __launch_bounds__(256) k_blend_fp32(SplatArrays sp, const uint32
                 if (done) continue;
                 const float4 a = sm[k].a, b = sm[k].b;
                 float p, M, dx, dy;
-                const int g = classify(a, b, fpx, fpy, p, M, dx, dy);
+                gate_values(a, b, fpx, fpy, p, M, dx, dy);
                 if (COUNT) ++n_eval;
-                if (g == kSkip) continue;
-                if (g == kAmbiguous) {
-                    slow = done = true;
-                    continue;
-                }
+                if (gate_skip(p, M, b.z)) continue;
                 const float4 cc = sm[k].c;
-                const float pc = sm[k].d.z;
+                const float2 pr = make_float2(sm[k].d.z, sm[k].d.w);
                 const float al = blend_alpha(cc.w, p);
-                // backward's clamp gate: unclamped alpha <= 0.99 (rasterizer.cpp:356)
-                if (__fadd_rn(p, M) >= pc && __fsub_rn(p, M) <= pc) {
-                    slow = done = true;
-                    continue;
-                }
                 const float om = __fsub_rn(1.f, al);
                 const float test_T = __fmul_rn(T, om);
-                const float errN = fmaf(al * M, rcp_approx(om), errT + 3e-7f);
-                if (fabsf(test_T - 1e-4f) <= test_T * errN) {
+                const float errN = fmaf(al * M, pr.y, errT + 3e-7f);
+                // ambiguous: a classify gate, the backward's clamp gate (unclamped alpha <= 0.99,
+                // rasterizer.cpp:356) or T(1 - alpha) < 1e-4 within their error bounds
+                const bool amb = gate_ambiguous(p, M, b.z) | ((__fadd_rn(p, M) >= pr.x) & (__fsub_rn(p, M) <= pr.x)) |
+                                 (fabsf(test_T - 1e-4f) <= test_T * errN);
+                if (amb) {
                     slow = done = true;
                     continue;
                 }
@@ -201,16 +207,43 @@ __global__ void __launch_bounds__(256) k_blend_fp32(SplatArrays sp, const uint32
     }
 }
 
-__device__ __forceinline__ float warp_sum(float v) {
+// Reduce-scatter of 9 per-lane partials across the warp (butterfly, 12 shuffles instead of
+// 9 x 5): at each level the lanes split their remaining slots in two halves, keep one half
+// and receive the partner's contribution to it.  Afterwards lane pairs (l, l^1) hold the
+// warp sum of value `idx` (valid when ok) -- 9 lanes then issue their shared-memory
+// atomics in one instruction.
+template <int K, int OFF>
+__device__ __forceinline__ void rs_level(const float* in, float* out, int lane, int& base, int& end) {
+    constexpr int LO = (K + 1) / 2;
+    const bool hi = (lane & OFF) != 0;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-    return v;
+    for (int i = 0; i < LO; ++i) {
+        const float mine = hi ? (LO + i < K ? in[LO + i] : 0.f) : in[i];
+        const float give = hi ? in[i] : (LO + i < K ? in[LO + i] : 0.f);
+        out[i] = mine + __shfl_xor_sync(kFull, give, OFF);
+    }
+    // the lane's slots cover value indices [base, end); keep the low or the high half
+    if (hi) base += LO;
+    else end = min(end, base + LO);
 }
 
-// K6: back-to-front replay of the FP32 pixels (rasterizer.cpp:437-468).  Per-splat
-// partial sums are warp-reduced, combined in shared memory and scattered with one
-// FP64 atomic per (tile, splat, component).  Slow pixels are replayed in FP64 by
-// k_backward_fp64.
+__device__ __forceinline__ float reduce_scatter9(const float* v, int lane, int& idx, bool& ok) {
+    float a[5], b[3], c[2], d[1];
+    int base = 0, end = 9;
+    rs_level<9, 16>(v, a, lane, base, end);  // 9 -> 5 slots
+    rs_level<5, 8>(a, b, lane, base, end);   // 5 -> 3
+    rs_level<3, 4>(b, c, lane, base, end);   // 3 -> 2
+    rs_level<2, 2>(c, d, lane, base, end);   // 2 -> 1
+    const float r = d[0] + __shfl_xor_sync(kFull, d[0], 1);
+    idx = base;
+    ok = base < end;  // padding slots hold zeros and own no value
+    return r;
+}
+
+// K6: back-to-front replay of the FP32 pixels (rasterizer.cpp:320-397).  Per-splat
+// partial sums are reduce-scattered across the warp, combined in shared memory and
+// scattered with one FP64 atomic per (tile, splat, component).  Slow pixels are replayed
+// in FP64 by k_backward_fp64.
 __global__ void __launch_bounds__(256) k_backward_fp32(SplatArrays sp, const uint32_t* __restrict__ vals,
                                                        const uint2* __restrict__ ranges, DevCamera cam, float3 bg,
                                                        const double* __restrict__ final_T,
@@ -286,24 +319,27 @@ __global__ void __launch_bounds__(256) k_backward_fp32(SplatArrays sp, const uin
                     // value here means K5 culled the pair, whose FP64 decision is "skip".
                     if (classify(a, b, fpx, fpy, p, M, dx, dy) == kAccept) {
                         const float4 cc = sm[k].c;
-                        const float al = blend_alpha(cc.w, p);
+                        const float e = ex2_approx(p);
+                        const float al = fminf(0.99f, __fmul_rn(cc.w, e));
                         const float om = 1.f - al;
-                        const float T_before = T_run / om;
+                        const float inv_om = rcp_approx(om);
+                        const float T_before = T_run * inv_om;
                         const float w = al * T_before;
                         v[0] = w * g0;
                         v[1] = w * g1;
                         v[2] = w * g2;
-                        const float dL_da = g0 * (cc.x * T_before - s0 / om) + g1 * (cc.y * T_before - s1 / om) +
-                                            g2 * (cc.z * T_before - s2 / om);
-                        if (p <= sm[k].d.z) {  // unclamped alpha <= 0.99
+                        const float dL_da = g0 * fmaf(cc.x, T_before, -s0 * inv_om) +
+                                            g1 * fmaf(cc.y, T_before, -s1 * inv_om) +
+                                            g2 * fmaf(cc.z, T_before, -s2 * inv_om);
+                        if (p <= sm[k].d.z) {  // unclamped alpha <= 0.99: al = ab * e
                             const float A = -2.f * kLn2 * a.z, B = -kLn2 * a.w, C = -2.f * kLn2 * b.x;
-                            v[8] = dL_da * (al / cc.w);
+                            v[8] = dL_da * e;
                             const float dp = dL_da * al;
                             v[3] = dp * (-0.5f * dx * dx);
                             v[4] = dp * (-dx * dy);
                             v[5] = dp * (-0.5f * dy * dy);
-                            v[6] = dp * (A * dx + B * dy);
-                            v[7] = dp * (B * dx + C * dy);
+                            v[6] = dp * fmaf(A, dx, B * dy);
+                            v[7] = dp * fmaf(B, dx, C * dy);
                         }
                         s0 = fmaf(cc.x, w, s0);
                         s1 = fmaf(cc.y, w, s1);
@@ -321,13 +357,10 @@ __global__ void __launch_bounds__(256) k_backward_fp32(SplatArrays sp, const uin
                             if (v[q] != 0.f) atomicAdd(&acc[q][k], v[q]);
                     }
                 } else {
-#pragma unroll
-                    for (int q = 0; q < 9; ++q) v[q] = warp_sum(v[q]);
-                    if (lane == 0) {
-#pragma unroll
-                        for (int q = 0; q < 9; ++q)
-                            if (v[q] != 0.f) atomicAdd(&acc[q][k], v[q]);
-                    }
+                    int idx;
+                    bool ok;
+                    const float r = reduce_scatter9(v, lane, idx, ok);
+                    if (ok && !(lane & 1) && r != 0.f) atomicAdd(&acc[idx][k], r);
                 }
             }
         }

@@ -610,6 +610,136 @@ __global__ void __launch_bounds__(256) k_mean_extent(ParamView P, double* part_l
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// K12: densify_and_prune (optim.cpp:168-234).  The decisions run here, the sequential
+// parts (the max_gaussians cut-off, the normal draws of the train loop's mt19937_64, the
+// opacity sort of the prune set) on the host with the reference's own std:: types.
+template <bool F64>
+__global__ void k_densify_kind(ParamView P, const double* __restrict__ accum, const int32_t* __restrict__ count,
+                               double thr, double clone_limit, uint8_t* __restrict__ kind) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.n) return;
+    uint8_t k = 0;
+    if (count[i] != 0) {
+        const double avg = accum[i] / count[i];
+        if (avg > thr) {
+            double ls[4];
+            ld_block<F64>(P, 1, i, ls);
+            // log_scales.head<3>().array().exp().maxCoeff()
+            double m = rgs_exp::glibc_exp(ls[0]);
+            m = smax(m, rgs_exp::glibc_exp(ls[1]));
+            m = smax(m, rgs_exp::glibc_exp(ls[2]));
+            k = (m <= clone_limit) ? 1 : 2;
+        }
+    }
+    kind[i] = k;
+}
+
+// Children of the processed candidates, appended at ext index n + c (moments zero,
+// push_back gaussian.cpp:122-140).  kind: 1 clone, 2 / 3 first / second split child.
+template <bool F64>
+__global__ void k_densify_children(ParamView P, const int32_t* __restrict__ parent, const uint8_t* __restrict__ ckind,
+                                   const double* __restrict__ draws, const int32_t* __restrict__ draw_off, int n_child,
+                                   double log_split, int static_mode, void* ext, void* ext_m1, void* ext_m2,
+                                   int ext_n, unsigned long long* err) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n_child) return;
+    const int p = parent[c], dst = P.n + c;
+    double mean[4], ls[4], rot[8];
+    ld_block<F64>(P, 0, p, mean);
+    ld_block<F64>(P, 1, p, ls);
+    ld_block<F64>(P, 2, p, rot);
+    ld_block<F64>(P, 3, p, rot + 4);
+    SliceState s;
+    const int code = d_slice(mean, ls, rot, mean[3], s);  // slice_at(parent, parent.mean[3]) / gaussian_speed
+    if (code != 0) {
+        atomicMin(err, ((unsigned long long)p << 8) | (unsigned long long)(code < 0 ? kErrDegenerateTime : code));
+        return;
+    }
+    const double* z = draws + draw_off[c];
+    double cm[4] = {mean[0], mean[1], mean[2], mean[3]}, cl[4] = {ls[0], ls[1], ls[2], ls[3]};
+    if (ckind[c] == 1) {
+        // child.mean.head<3>() += gaussian_speed(parent) * (gauss(rng) * st)   (optim.cpp:189-191)
+        const double st = rgs_exp::glibc_exp(ls[3]);
+        const double f = z[0] * st;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) cm[a] = mean[a] + (s.V[a] / s.W) * f;
+    } else {
+        // child.mean = parent.mean + (R * q.cwiseSqrt().asDiagonal()) * z   (optim.cpp:195-200)
+        double sq[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) sq[j] = sqrt(s.q[j]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            double acc = (s.R[i * 4 + 0] * sq[0]) * z[0];
+#pragma unroll
+            for (int j = 1; j < 4; ++j) acc += (s.R[i * 4 + j] * sq[j]) * z[j];
+            cm[i] = mean[i] + acc;
+        }
+        if (static_mode) cm[3] = mean[3];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) cl[a] = ls[a] - log_split;
+        if (static_mode) cl[3] = ls[3];
+    }
+    st4<F64>(ext, ext_n, 0, dst, cm);
+    st4<F64>(ext, ext_n, 1, dst, cl);
+    st4<F64>(ext, ext_n, 2, dst, rot);
+    st4<F64>(ext, ext_n, 3, dst, rot + 4);
+    double v[4];
+#pragma unroll 1
+    for (int b = 0; b < 12; ++b) {
+        ld_block<F64>(P, 4 + b, p, v);
+        st4<F64>(ext, ext_n, 4 + b, dst, v);
+    }
+    st1<F64>(ext, 64 * (size_t)ext_n + dst, ld_opacity<F64>(P, p));
+    const double zero[4] = {0, 0, 0, 0};
+#pragma unroll 1
+    for (int b = 0; b < 16; ++b) {
+        st4<F64>(ext_m1, ext_n, b, dst, zero);
+        st4<F64>(ext_m2, ext_n, b, dst, zero);
+    }
+    st1<F64>(ext_m1, 64 * (size_t)ext_n + dst, 0.0);
+    st1<F64>(ext_m2, 64 * (size_t)ext_n + dst, 0.0);
+}
+
+// Copy Gaussian map[j] of an SoA block of n_src Gaussians to slot j of one of n_dst.
+template <typename T>
+__global__ void k_gather_soa(const T* __restrict__ src, int n_src, const int32_t* __restrict__ map, int n_map,
+                             T* __restrict__ dst, int n_dst) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n_map) return;
+    const int i = map ? map[j] : j;
+#pragma unroll 1
+    for (int b = 0; b < 16; ++b) {
+        const T* a = src + 4 * (size_t)b * n_src + 4 * (size_t)i;
+        T* o = dst + 4 * (size_t)b * n_dst + 4 * (size_t)j;
+        o[0] = a[0]; o[1] = a[1]; o[2] = a[2]; o[3] = a[3];
+    }
+    dst[64 * (size_t)n_dst + j] = src[64 * (size_t)n_src + i];
+}
+
+// Prune candidates (optim.cpp:212-221): flag, and the opacity logit for the host sort.
+template <bool F64>
+__global__ void k_prune_flags(ParamView P, const uint8_t* __restrict__ removed, double prune_opacity,
+                              double big_scale, int static_mode, uint8_t* __restrict__ flag) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.n) return;
+    if (removed[i]) {
+        flag[i] = 0;
+        return;
+    }
+    double ls[4];
+    ld_block<F64>(P, 1, i, ls);
+    double m = rgs_exp::glibc_exp(ls[0]);
+    m = smax(m, rgs_exp::glibc_exp(ls[1]));
+    m = smax(m, rgs_exp::glibc_exp(ls[2]));
+    const double t_scale = rgs_exp::glibc_exp(ls[3]);
+    const bool over_time = !static_mode && t_scale > 1.0;
+    const double o = 1 / (1 + rgs_exp::glibc_exp(-ld_opacity<F64>(P, i)));
+    flag[i] = (o < prune_opacity || m > big_scale || over_time) ? 1 : 0;
+}
+
 }  // namespace rgs_dev
 
 // ---------------------------------------------------------------------------
@@ -726,6 +856,51 @@ int knn(const double* pts4, int n, int k, int32_t* out, cudaStream_t s) {
 }
 
 int extent_blocks(int n) { return nblk(n, 256); }
+
+void densify_kind(const float* params, const double* params64, int n, const double* accum, const int32_t* count,
+                  double thr, double clone_limit, uint8_t* kind, cudaStream_t s) {
+    ParamView P{params, n, params64};
+    if (params64)
+        k_densify_kind<true><<<nblk(n, 256), 256, 0, s>>>(P, accum, count, thr, clone_limit, kind);
+    else
+        k_densify_kind<false><<<nblk(n, 256), 256, 0, s>>>(P, accum, count, thr, clone_limit, kind);
+}
+
+void densify_children(const float* params, const double* params64, int n, const int32_t* parent,
+                      const uint8_t* ckind, const double* draws, const int32_t* draw_off, int n_child,
+                      double log_split, int static_mode, void* ext, void* ext_m1, void* ext_m2, int ext_n,
+                      unsigned long long* err, cudaStream_t s) {
+    if (n_child <= 0) return;
+    ParamView P{params, n, params64};
+    if (params64)
+        k_densify_children<true><<<nblk(n_child, 128), 128, 0, s>>>(P, parent, ckind, draws, draw_off, n_child,
+                                                                   log_split, static_mode, ext, ext_m1, ext_m2,
+                                                                   ext_n, err);
+    else
+        k_densify_children<false><<<nblk(n_child, 128), 128, 0, s>>>(P, parent, ckind, draws, draw_off, n_child,
+                                                                    log_split, static_mode, ext, ext_m1, ext_m2,
+                                                                    ext_n, err);
+}
+
+void gather_soa(bool f64, const void* src, int n_src, const int32_t* map, int n_map, void* dst, int n_dst,
+                cudaStream_t s) {
+    if (n_map <= 0) return;
+    if (f64)
+        k_gather_soa<double><<<nblk(n_map, 256), 256, 0, s>>>((const double*)src, n_src, map, n_map, (double*)dst,
+                                                              n_dst);
+    else
+        k_gather_soa<float><<<nblk(n_map, 256), 256, 0, s>>>((const float*)src, n_src, map, n_map, (float*)dst,
+                                                             n_dst);
+}
+
+void prune_flags(const float* params, const double* params64, int n, const uint8_t* removed, double prune_opacity,
+                 double big_scale, int static_mode, uint8_t* flag, cudaStream_t s) {
+    ParamView P{params, n, params64};
+    if (params64)
+        k_prune_flags<true><<<nblk(n, 256), 256, 0, s>>>(P, removed, prune_opacity, big_scale, static_mode, flag);
+    else
+        k_prune_flags<false><<<nblk(n, 256), 256, 0, s>>>(P, removed, prune_opacity, big_scale, static_mode, flag);
+}
 
 void mean_extent(const float* params, const double* params64, int n, double* part_lo, double* part_hi,
                  cudaStream_t s) {

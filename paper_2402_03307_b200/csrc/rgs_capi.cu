@@ -1595,3 +1595,300 @@ int rgs_consistency(rgs_ctx* c, const rgs_scene* scene, const int32_t* neighbors
 }
 
 }  // extern "C"
+
+// ===========================================================================
+// R4GS v1 checkpoints straight to / from a device scene (checkpoint.cpp:29-86).
+#include <cstdio>
+
+namespace {
+constexpr char kCkptMagic[4] = {'R', '4', 'G', 'S'};
+constexpr uint32_t kCkptVersion = 1;  // checkpoint.hpp:19
+
+int ckpt_err(rgs_ctx* c, const std::string& what) { return set_err(c, RGS_E_CHECKPOINT, "checkpoint: " + what); }
+}  // namespace
+
+extern "C" {
+
+int rgs_scene_load_checkpoint(rgs_ctx* c, const char* path, unsigned scene_flags, rgs_scene** out) {
+    if (!path || !out || (scene_flags & ~RGS_SCENE_F64)) return RGS_E_INVALID;
+    if (!c) return RGS_E_INVALID;
+    const std::string p(path);
+    FILE* f = std::fopen(path, "rb");
+    if (!f) return ckpt_err(c, "cannot open: " + p);
+    struct Closer {
+        FILE* f;
+        ~Closer() { std::fclose(f); }
+    } closer{f};
+    char magic[4];
+    if (std::fread(magic, 1, 4, f) != 4 || std::memcmp(magic, kCkptMagic, 4) != 0)
+        return ckpt_err(c, "bad magic: " + p);
+    uint32_t hdr[3] = {0, 0, 0};  // version, count, sh degree (little-endian host)
+    const size_t got = std::fread(hdr, 4, 3, f);
+    if (got < 1 || hdr[0] != kCkptVersion)
+        return ckpt_err(c, "unsupported version " + std::to_string(got < 1 ? 0u : hdr[0]));
+    if (got < 3 || hdr[2] > 3) return ckpt_err(c, "malformed header: " + p);
+    const size_t n = hdr[1];
+    if (n > (size_t)0x7fffffff) return ckpt_err(c, "malformed header: " + p);
+    return guarded(c, [&]() -> int {
+        cudaStream_t s = c->stream;
+        float* pinned = nullptr;
+        const size_t bytes = 65 * sizeof(float) * std::max<size_t>(n, 1);
+        CK(cudaMallocHost(&pinned, bytes));
+        const size_t rd = n ? std::fread(pinned, 65 * sizeof(float), n, f) : 0;
+        if (rd != n) {
+            cudaFreeHost(pinned);
+            return ckpt_err(c, "truncated: " + p);
+        }
+        rgs_scene* sc = nullptr;
+        int rc = rgs_scene_create_ex(c, (int)n, (int)hdr[2], scene_flags, &sc);
+        if (rc) {
+            cudaFreeHost(pinned);
+            return rc;
+        }
+        DevBuf tmp;
+        tmp.ensure(bytes, s);
+        CK(cudaMemcpyAsync(tmp.p, pinned, 65 * sizeof(float) * n, cudaMemcpyHostToDevice, s));
+        rgs_launch::records_to_soa(tmp.as<float>(), (int)n, sc->params, sc->params64, s);
+        c->launches += n ? 1 : 0;
+        tmp.release(s);
+        CK(cudaStreamSynchronize(s));
+        cudaFreeHost(pinned);
+        *out = sc;
+        return RGS_OK;
+    });
+}
+
+int rgs_scene_save_checkpoint(rgs_ctx* c, const rgs_scene* scene, const char* path) {
+    if (!scene || !path) return RGS_E_INVALID;
+    return guarded(c, [&]() -> int {
+        const std::string p(path);
+        const size_t n = (size_t)scene->n;
+        cudaStream_t s = c->stream;
+        std::vector<float> rec(65 * std::max<size_t>(n, 1));
+        if (n) {
+            DevBuf tmp;
+            tmp.ensure(65 * sizeof(float) * n, s);
+            rgs_launch::soa_to_records(scene->params, scene->params64, (int)n, tmp.as<float>(), s);
+            c->launches += 1;
+            CK(cudaMemcpyAsync(rec.data(), tmp.p, 65 * sizeof(float) * n, cudaMemcpyDeviceToHost, s));
+            tmp.release(s);
+            CK(cudaStreamSynchronize(s));
+        }
+        FILE* f = std::fopen(path, "wb");
+        if (!f) return ckpt_err(c, "cannot open for writing: " + p);
+        const uint32_t hdr[3] = {kCkptVersion, (uint32_t)n, (uint32_t)scene->sh_degree};
+        bool ok = std::fwrite(kCkptMagic, 1, 4, f) == 4 && std::fwrite(hdr, 4, 3, f) == 3 &&
+                  (n == 0 || std::fwrite(rec.data(), 65 * sizeof(float), n, f) == n);
+        ok = (std::fclose(f) == 0) && ok;
+        if (!ok) return ckpt_err(c, "write failed: " + p);
+        return RGS_OK;
+    });
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// densify_and_prune (optim.cpp:168-234) and the train loop's generator.
+#include <random>
+
+struct rgs_rng {
+    std::mt19937_64 eng;  // train_from's rng (trainer.cpp:105)
+};
+
+extern "C" {
+
+int rgs_rng_create(unsigned long long seed, rgs_rng** out) {
+    if (!out) return RGS_E_INVALID;
+    *out = new rgs_rng{std::mt19937_64(seed)};
+    return RGS_OK;
+}
+void rgs_rng_destroy(rgs_rng* r) { delete r; }
+int rgs_rng_uniform_int(rgs_rng* r, int lo, int hi, int* out) {
+    if (!r || !out || hi < lo) return RGS_E_INVALID;
+    std::uniform_int_distribution<int> d(lo, hi);  // trainer.cpp:106, 119
+    *out = d(r->eng);
+    return RGS_OK;
+}
+
+int rgs_densify_and_prune(rgs_ctx* c, rgs_scene* scene, rgs_optimizer* o, const rgs_densify_config* cfg,
+                          double scene_extent, rgs_rng* rng, rgs_densify_report* report) {
+    if (!scene || !o || !cfg || !rng || o->n != scene->n) return RGS_E_INVALID;
+    return guarded(c, [&]() -> int {
+        cudaStream_t s = c->stream;
+        const int n = scene->n;
+        const bool f64 = scene->params64 != nullptr;
+        const size_t eb = f64 ? sizeof(double) : sizeof(float);
+        rgs_densify_report rep{0, 0, 0};
+        // ---- densify decisions (optim.cpp:176-186) on the device
+        std::vector<uint8_t> kind((size_t)std::max(n, 1), 0);
+        DevBuf dk;
+        if (n > 0) {
+            dk.ensure((size_t)n, s);
+            rgs_launch::densify_kind(scene->params, scene->params64, n, o->accum, o->count,
+                                     cfg->densify_grad_threshold, cfg->percent_dense * scene_extent,
+                                     dk.as<uint8_t>(), s);
+            c->launches += 1;
+            CK(cudaMemcpyAsync(kind.data(), dk.p, (size_t)n, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+        }
+        // ---- the sequential part on the host: cut-off and normal draws, in index order
+        std::normal_distribution<double> gauss(0, 1);  // optim.cpp:172 (fresh per call)
+        std::vector<int32_t> parent, draw_off;
+        std::vector<uint8_t> ckind;
+        std::vector<double> draws;
+        std::vector<uint8_t> removed;
+        int size = n;
+        for (int i = 0; i < n; ++i) {
+            if (!kind[i]) continue;
+            if (size + 2 > cfg->max_gaussians) break;
+            if (kind[i] == 1) {
+                parent.push_back(i);
+                ckind.push_back(1);
+                draw_off.push_back((int32_t)draws.size());
+                draws.push_back(gauss(rng->eng));
+                size += 1;
+                rep.cloned += 1;
+            } else {
+                for (int k = 0; k < 2; ++k) {
+                    parent.push_back(i);
+                    ckind.push_back((uint8_t)(2 + k));
+                    draw_off.push_back((int32_t)draws.size());
+                    for (int a = 0; a < 4; ++a) draws.push_back(gauss(rng->eng));
+                }
+                size += 2;
+                rep.split += 1;
+            }
+        }
+        const int n_child = (int)parent.size();
+        const int ext_n = n + n_child;
+        // ---- extended store: survivors copied, children appended (push_back)
+        void *ext = nullptr, *ext_m1 = nullptr, *ext_m2 = nullptr;
+        const size_t ext1 = (size_t)std::max(ext_n, 1);
+        CK(cudaMalloc(&ext, 65 * ext1 * eb));
+        CK(cudaMalloc(&ext_m1, 65 * ext1 * eb));
+        CK(cudaMalloc(&ext_m2, 65 * ext1 * eb));
+        void* params = f64 ? (void*)scene->params64 : (void*)scene->params;
+        rgs_launch::gather_soa(f64, params, n, nullptr, n, ext, ext_n, s);
+        rgs_launch::gather_soa(f64, o->m1, n, nullptr, n, ext_m1, ext_n, s);
+        rgs_launch::gather_soa(f64, o->m2, n, nullptr, n, ext_m2, ext_n, s);
+        c->launches += 3;
+        DevBuf dparent, dck, ddraw, doff, derr, drem, dflag;
+        derr.ensure(sizeof(unsigned long long), s);
+        CK(cudaMemsetAsync(derr.p, 0xff, sizeof(unsigned long long), s));
+        if (n_child) {
+            dparent.ensure(4 * (size_t)n_child, s);
+            dck.ensure((size_t)n_child, s);
+            doff.ensure(4 * (size_t)n_child, s);
+            ddraw.ensure(8 * draws.size(), s);
+            CK(cudaMemcpyAsync(dparent.p, parent.data(), 4 * (size_t)n_child, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(dck.p, ckind.data(), (size_t)n_child, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(doff.p, draw_off.data(), 4 * (size_t)n_child, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(ddraw.p, draws.data(), 8 * draws.size(), cudaMemcpyHostToDevice, s));
+            rgs_launch::densify_children(scene->params, scene->params64, n, dparent.as<int32_t>(), dck.as<uint8_t>(),
+                                         ddraw.as<double>(), doff.as<int32_t>(), n_child,
+                                         std::log(cfg->split_factor), cfg->static_mode, ext, ext_m1, ext_m2, ext_n,
+                                         derr.as<unsigned long long>(), s);
+            c->launches += 1;
+        }
+        // ---- prune (optim.cpp:211-226): flags on the device, the opacity sort on the host
+        std::vector<uint8_t> rem((size_t)ext1, 0);
+        for (int k = 0; k < n_child; ++k)
+            if (ckind[k] == 2) rem[parent[k]] = 1;  // split parents (to_remove)
+        drem.ensure(ext1, s);
+        dflag.ensure(ext1, s);
+        CK(cudaMemcpyAsync(drem.p, rem.data(), ext1, cudaMemcpyHostToDevice, s));
+        rgs_launch::prune_flags(f64 ? nullptr : (const float*)ext, f64 ? (const double*)ext : nullptr, ext_n,
+                                drem.as<uint8_t>(), cfg->prune_opacity, 0.5 * scene_extent, cfg->static_mode,
+                                dflag.as<uint8_t>(), s);
+        c->launches += 1;
+        std::vector<uint8_t> flag(ext1);
+        std::vector<double> logit(ext1);
+        std::vector<float> logit_f(f64 ? 0 : ext1);
+        CK(cudaMemcpyAsync(flag.data(), dflag.p, ext1, cudaMemcpyDeviceToHost, s));
+        if (f64)
+            CK(cudaMemcpyAsync(logit.data(), (double*)ext + 64 * (size_t)ext_n, 8 * (size_t)ext_n,
+                               cudaMemcpyDeviceToHost, s));
+        else
+            CK(cudaMemcpyAsync(logit_f.data(), (float*)ext + 64 * (size_t)ext_n, 4 * (size_t)ext_n,
+                               cudaMemcpyDeviceToHost, s));
+        unsigned long long e = 0;
+        CK(cudaMemcpyAsync(&e, derr.p, sizeof e, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        auto free_ext = [&]() {
+            cudaFree(ext);
+            cudaFree(ext_m1);
+            cudaFree(ext_m2);
+        };
+        if (e != kNoError) {
+            free_ext();
+            const int code = (int)(e & 0xff);
+            c->err_index = (int)(e >> 8);
+            if (code == kErrDegenerateTime)
+                return set_err(c, RGS_E_DEGENERATE_TIME, "slice_at: temporal scale collapsed (W < 1e-12)");
+            return set_err(c, code, rotor_msg(code));
+        }
+        if (!f64)
+            for (int i = 0; i < ext_n; ++i) logit[i] = logit_f[i];
+        auto opacity = [&](int i) { return 1 / (1 + std::exp(-logit[i])); };  // GaussianStore::opacity
+        std::vector<int> prunable;
+        for (int i = 0; i < ext_n; ++i)
+            if (flag[i]) prunable.push_back(i);
+        int n_removed_split = rep.split;
+        int allowed = std::max(0, ext_n - n_removed_split - cfg->min_gaussians);
+        if ((int)prunable.size() > allowed) {
+            std::sort(prunable.begin(), prunable.end(), [&](int a, int b) { return opacity(a) < opacity(b); });
+            prunable.resize(allowed);
+        }
+        rep.pruned = (int)prunable.size();
+        std::vector<uint8_t> drop((size_t)ext1, 0);
+        for (int i = 0; i < ext_n; ++i) drop[i] = rem[i];
+        for (int i : prunable) drop[i] = 1;
+        std::vector<int32_t> keep;
+        keep.reserve(ext_n);
+        for (int i = 0; i < ext_n; ++i)
+            if (!drop[i]) keep.push_back(i);
+        const int n_new = (int)keep.size();
+        // ---- remove_indices (gaussian.cpp:142-180) as one gather; reset_stats
+        const size_t nn1 = (size_t)std::max(n_new, 1);
+        void *np = nullptr, *nm1 = nullptr, *nm2 = nullptr;
+        double* nacc = nullptr;
+        int32_t* ncnt = nullptr;
+        CK(cudaMalloc(&np, 65 * nn1 * eb));
+        CK(cudaMalloc(&nm1, 65 * nn1 * eb));
+        CK(cudaMalloc(&nm2, 65 * nn1 * eb));
+        CK(cudaMalloc(&nacc, nn1 * sizeof(double)));
+        CK(cudaMalloc(&ncnt, nn1 * sizeof(int32_t)));
+        DevBuf dkeep;
+        dkeep.ensure(4 * nn1, s);
+        CK(cudaMemcpyAsync(dkeep.p, keep.data(), 4 * (size_t)n_new, cudaMemcpyHostToDevice, s));
+        rgs_launch::gather_soa(f64, ext, ext_n, dkeep.as<int32_t>(), n_new, np, n_new, s);
+        rgs_launch::gather_soa(f64, ext_m1, ext_n, dkeep.as<int32_t>(), n_new, nm1, n_new, s);
+        rgs_launch::gather_soa(f64, ext_m2, ext_n, dkeep.as<int32_t>(), n_new, nm2, n_new, s);
+        c->launches += 3;
+        CK(cudaMemsetAsync(nacc, 0, nn1 * sizeof(double), s));
+        CK(cudaMemsetAsync(ncnt, 0, nn1 * sizeof(int32_t), s));
+        CK(cudaStreamSynchronize(s));
+        for (DevBuf* b : {&dk, &dparent, &dck, &ddraw, &doff, &derr, &drem, &dflag, &dkeep}) b->release(s);
+        free_ext();
+        cudaFree(f64 ? (void*)scene->params64 : (void*)scene->params);
+        cudaFree(o->m1);
+        cudaFree(o->m2);
+        cudaFree(o->accum);
+        cudaFree(o->count);
+        if (f64)
+            scene->params64 = (double*)np;
+        else
+            scene->params = (float*)np;
+        scene->n = n_new;
+        o->n = n_new;
+        o->m1 = nm1;
+        o->m2 = nm2;
+        o->accum = nacc;
+        o->count = ncnt;
+        o->part.ensure(sizeof(double) * (rgs_launch::adam_blocks(n_new) + 16), s);
+        if (report) *report = rep;
+        return RGS_OK;
+    });
+}
+
+}  // extern "C"

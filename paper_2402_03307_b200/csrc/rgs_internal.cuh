@@ -173,6 +173,8 @@ void scene_pack64(const double* mean, const double* ls, const double* rot, const
                   int n, double* params, cudaStream_t s);
 void scene_unpack(const float* params, const double* params64, int n, double* mean, double* ls, double* rot,
                   double* op, double* sh, cudaStream_t s);
+void records_to_soa(const float* rec, int n, float* params, double* params64, cudaStream_t s);
+void soa_to_records(const float* params, const double* params64, int n, float* rec, cudaStream_t s);
 void valid_to_u32(const uint8_t* valid, int n, uint32_t* out, cudaStream_t s);
 double ffma_peak(float* out, int blocks, int iters, cudaStream_t s);
 }  // namespace rgs_launch

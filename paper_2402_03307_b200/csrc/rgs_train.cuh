@@ -61,4 +61,14 @@ int knn(const double* pts4, int n, int k, int32_t* out, cudaStream_t s);
 int extent_blocks(int n);
 void mean_extent(const float* params, const double* params64, int n, double* part_lo, double* part_hi,
                  cudaStream_t s);
+void densify_kind(const float* params, const double* params64, int n, const double* accum, const int32_t* count,
+                  double thr, double clone_limit, uint8_t* kind, cudaStream_t s);
+void densify_children(const float* params, const double* params64, int n, const int32_t* parent,
+                      const uint8_t* ckind, const double* draws, const int32_t* draw_off, int n_child,
+                      double log_split, int static_mode, void* ext, void* ext_m1, void* ext_m2, int ext_n,
+                      unsigned long long* err, cudaStream_t s);
+void gather_soa(bool f64, const void* src, int n_src, const int32_t* map, int n_map, void* dst, int n_dst,
+                cudaStream_t s);
+void prune_flags(const float* params, const double* params64, int n, const uint8_t* removed, double prune_opacity,
+                 double big_scale, int static_mode, uint8_t* flag, cudaStream_t s);
 }  // namespace rgs_launch

@@ -38,6 +38,7 @@ RGS_E_CUDA = 5
 RGS_E_INVALID = 6
 RGS_E_DEGENERATE_TIME = 7
 RGS_E_NO_DEVICE = 8
+RGS_E_CHECKPOINT = 9
 
 FLAG_RETAIN_RECORDS = 1
 FLAG_BLEND_FP64 = 2
@@ -79,6 +80,10 @@ class NonFiniteRotorError(RuntimeError):
 
 class CameraError(RuntimeError):
     """std::runtime_error thrown by Camera::validate (camera.hpp:21-26)."""
+
+
+class CheckpointError(RuntimeError):
+    """checkpoint.hpp:10-12"""
 
 
 class DegenerateTimeError(RuntimeError):
@@ -148,6 +153,8 @@ EXPORTS = [
     "rgs_image_loss", "rgs_optimizer_create", "rgs_optimizer_destroy", "rgs_adam_step", "rgs_optimizer_status",
     "rgs_optimizer_download", "rgs_optimizer_upload", "rgs_optimizer_reset_stats", "rgs_reset_opacity",
     "rgs_scene_scales", "rgs_knn_build", "rgs_consistency",
+    "rgs_scene_load_checkpoint", "rgs_scene_save_checkpoint",
+    "rgs_rng_create", "rgs_rng_destroy", "rgs_rng_uniform_int", "rgs_densify_and_prune",
 ]
 
 
@@ -210,6 +217,12 @@ def load_library(path: str = LIB_PATH):
         "rgs_scene_scales": (i, [p, p, p]),
         "rgs_knn_build": (i, [p, p, i, p, p]),
         "rgs_consistency": (i, [p, p, p, i, d, ctypes.c_uint, p, p]),
+        "rgs_scene_load_checkpoint": (i, [p, ctypes.c_char_p, ctypes.c_uint, p]),
+        "rgs_scene_save_checkpoint": (i, [p, p, ctypes.c_char_p]),
+        "rgs_rng_create": (i, [ctypes.c_ulonglong, p]),
+        "rgs_rng_destroy": (None, [p]),
+        "rgs_rng_uniform_int": (i, [p, i, i, p]),
+        "rgs_densify_and_prune": (i, [p, p, p, p, d, p, p]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -421,6 +434,8 @@ class Context:
             raise NonFiniteRotorError(msg, idx)
         if rc == RGS_E_CAMERA:
             raise CameraError(msg)
+        if rc == RGS_E_CHECKPOINT:
+            raise CheckpointError(msg)
         if rc == RGS_E_DEGENERATE_TIME:
             raise DegenerateTimeError(msg, idx)
         if rc == RGS_E_NO_DEVICE:
@@ -542,6 +557,21 @@ class DeviceScene:
         self.n_inexact = inexact.value
         self.sh_degree = store.active_sh_degree
         self.ctx.L.rgs_scene_set_sh_degree(self.h, store.active_sh_degree)
+
+    @staticmethod
+    def load_checkpoint(ctx: Context, path: str, f64: bool = False) -> "DeviceScene":
+        """load_checkpoint (checkpoint.cpp:54-86) straight into device memory."""
+        h = _vp()
+        ctx.check(ctx.L.rgs_scene_load_checkpoint(ctx.h, os.fsencode(path), SCENE_F64 if f64 else 0, ctypes.byref(h)))
+        s = DeviceScene.__new__(DeviceScene)
+        s.ctx, s.h, s.f64, s.n_inexact = ctx, h, f64, 0
+        s.n = int(ctx.L.rgs_scene_size(h))
+        s.sh_degree = -1
+        return s
+
+    def save_checkpoint(self, path: str):
+        """save_checkpoint (checkpoint.cpp:29-52)."""
+        self.ctx.check(self.ctx.L.rgs_scene_save_checkpoint(self.ctx.h, self.h, os.fsencode(path)))
 
     def download(self):
         """Device scene -> (mean, log_scales, rotor, opacity_logit, sh) float64 host arrays."""

@@ -194,6 +194,72 @@ class DeviceOptimizer:
             pass
 
 
+class Rng:
+    """The train loop's generator (std::mt19937_64(TrainConfig::seed), trainer.cpp:105), host-side
+    in the C library so batch picks and densification draws match the reference's sequence."""
+
+    def __init__(self, ctx: Context, seed: int = 0):
+        h = _vp()
+        ctx.check(ctx.L.rgs_rng_create(ctypes.c_ulonglong(seed), ctypes.byref(h)))
+        self.ctx, self.h = ctx, h
+
+    def uniform_int(self, lo: int, hi: int) -> int:
+        """std::uniform_int_distribution<int>(lo, hi)(rng) (trainer.cpp:106, 119)."""
+        out = ctypes.c_int(0)
+        self.ctx.check(self.ctx.L.rgs_rng_uniform_int(self.h, int(lo), int(hi), ctypes.byref(out)))
+        return out.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.L.rgs_rng_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class CDensifyConfig(ctypes.Structure):
+    """rgs_densify_config: TrainConfig's density control fields (optim.hpp:31-42)."""
+
+    _fields_ = [
+        ("densify_grad_threshold", ctypes.c_double),
+        ("percent_dense", ctypes.c_double),
+        ("split_factor", ctypes.c_double),
+        ("prune_opacity", ctypes.c_double),
+        ("min_gaussians", ctypes.c_int),
+        ("max_gaussians", ctypes.c_int),
+        ("static_mode", ctypes.c_int),
+    ]
+
+    @staticmethod
+    def from_config(cfg: "TrainConfig") -> "CDensifyConfig":
+        return CDensifyConfig(cfg.densify_grad_threshold, cfg.percent_dense, cfg.split_factor, cfg.prune_opacity,
+                              int(cfg.min_gaussians), int(cfg.max_gaussians), int(bool(cfg.static_mode)))
+
+
+@dataclass
+class DensifyReport:
+    """optim.hpp:94-96"""
+
+    cloned: int = 0
+    split: int = 0
+    pruned: int = 0
+
+
+def densify_and_prune(ctx: Context, scene: DeviceScene, opt: "DeviceOptimizer", cfg: "TrainConfig",
+                      scene_extent: float, rng: Rng) -> DensifyReport:
+    """optim.cpp:168-234 on the device scene (resized in place)."""
+    rep = (ctypes.c_int * 3)()
+    dc = CDensifyConfig.from_config(cfg)
+    ctx.sync_stream()
+    ctx.check(ctx.L.rgs_densify_and_prune(ctx.h, scene.h, opt.h, ctypes.byref(dc), float(scene_extent), rng.h, rep))
+    scene.n = int(ctx.L.rgs_scene_size(scene.h))
+    return DensifyReport(rep[0], rep[1], rep[2])
+
+
 def image_loss(ctx: Context, rendered, target, w_l1: float = 1.0, w_ssim: float = 0.0, dL_dimage=None,
                losses=None, loss_scale: float = 1.0, accumulate: bool = False, accumulate_grad: bool = False):
     """L1 + SSIM losses and dL/dimage on device tensors (rgs_image_loss).  ``accumulate``: losses
@@ -255,25 +321,34 @@ class Trainer:
     device-resident scene.  ``dist``: torch.distributed (initialised) for the multi-GPU
     batch (each rank passes its own views; the batch size is views_per_rank * world)."""
 
-    def __init__(self, ctx: Context, scene: DeviceScene, config: TrainConfig, dist=None):
-        import torch
-
+    def __init__(self, ctx: Context, scene: DeviceScene, config: TrainConfig, dist=None,
+                 scene_extent: Optional[float] = None, seed: int = 0):
         config.validate()
         self.ctx, self.scene, self.cfg, self.dist = ctx, scene, config, dist
+        self.scene_extent = scene_extent  # camera_extent(dataset) (trainer.cpp:88-99); None: no densification
+        self.rng = Rng(ctx, seed)
+        self.opt = DeviceOptimizer(ctx, scene)
+        self.step_count = 0
+        self.nbrs = None
+        self._img = None
+        self._dl = None
+        self._alloc()
+
+    def _alloc(self):
+        """Gradient / statistics buffers sized for the current scene (re-run after densification)."""
+        import torch
+
+        ctx, scene = self.ctx, self.scene
+        dist = self.dist
         self.world = dist.get_world_size() if (dist is not None and dist.is_initialized()) else 1
         dev = f"cuda:{ctx.device}"
         n = scene.n
-        self.opt = DeviceOptimizer(ctx, scene)
         self.gbuf = torch.zeros(66 * n, dtype=torch.float32, device=dev)  # [65 grads | viewspace_norm]
         self.grads = self.gbuf[: 65 * n]
         self.vnorm = self.gbuf[65 * n:]
         self.visible = torch.zeros(n, dtype=torch.int32, device=dev)
         self.losses = torch.zeros(8, dtype=torch.float64, device=dev)  # l1, ssim, mse, entropy, consistency
         self.losses_host = torch.zeros(8, dtype=torch.float64).pin_memory()
-        self.nbrs = None
-        self.step_count = 0
-        self._img = None
-        self._dl = None
 
     # trainer.cpp:107-113
     def rebuild_knn(self):
@@ -339,11 +414,21 @@ class Trainer:
         self.evaluate_loss(cams, targets, True)
         acfg = CAdamConfig.from_config(cfg, w.lambda_entropy, True)
         self.opt.step(self.grads, self.vnorm, self.visible, acfg, step, self.losses[3:4])
+        out = self.read_losses()
+        mutated = False
+        if (self.scene_extent is not None and cfg.densify_from <= step <= cfg.densify_until
+                and step % cfg.densify_interval == 0):
+            # optim.cpp:168-234; every rank draws the same numbers from its own copy of the
+            # generator, so the replicated scenes stay identical.
+            self.last_densify = densify_and_prune(self.ctx, self.scene, self.opt, cfg, self.scene_extent, self.rng)
+            self._alloc()
+            mutated = True
         if step % cfg.opacity_reset_interval == 0:
             self.opt.reset_opacity(cfg.reset_opacity_value)
-        if step % cfg.knn_rebuild_interval == 0:
+        if mutated or step % cfg.knn_rebuild_interval == 0:
+            self.nbrs = None
             self.rebuild_knn()
-        return self.read_losses()
+        return out
 
     def read_losses(self) -> LossBreakdown:
         self.ctx.fence()

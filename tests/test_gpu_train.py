@@ -259,3 +259,125 @@ def test_trainer_reduces_loss(ctx):
     assert np.isfinite(last.total) and last.total < first.total
     m, v, acc, cnt = tr.opt.download()
     assert cnt.max() == 31 and acc.max() > 0
+
+
+def _write_r4gs(path, store, version=1, magic=b"R4GS", truncate=0):
+    """checkpoint.hpp:14-18 layout, written independently of the code under test."""
+    n = store.size()
+    rec = np.concatenate([store.mean, store.log_scales, store.rotor, store.opacity_logit[:, None],
+                          store.sh.reshape(n, 48)], axis=1).astype("<f4")
+    blob = magic + np.array([version, n, store.active_sh_degree], "<u4").tobytes() + rec.tobytes()
+    with open(path, "wb") as f:
+        f.write(blob[: len(blob) - truncate])
+    return blob
+
+
+@pytest.mark.parametrize("f64", [False, True])
+def test_checkpoint_roundtrip(ctx, tmp_path, f64):
+    """R4GS v1 load straight to the device and save back byte-identically (checkpoint.cpp:29-86)."""
+    store = scenes.random_scene(777, sh_degree=2, seed=4)
+    src = str(tmp_path / "a.r4gs")
+    blob = _write_r4gs(src, store)
+    sc = DeviceScene.load_checkpoint(ctx, src, f64=f64)
+    assert sc.n == 777
+    for x, y in zip(sc.download(), O.OracleLib._scene(store)):
+        assert np.array_equal(x, y.reshape(x.shape))
+    dst = str(tmp_path / "b.r4gs")
+    sc.save_checkpoint(dst)
+    assert open(dst, "rb").read() == blob
+    if O.reference_available():
+        import ctypes
+
+        L = O.reference_build().lib
+        L.ref_load_checkpoint.restype = ctypes.c_int
+        n = L.ref_load_checkpoint(dst.encode(), None, None, None, None, None, None)
+        assert n == 777
+
+
+def test_checkpoint_errors(ctx, tmp_path):
+    store = scenes.random_scene(10, sh_degree=1, seed=1)
+    cases = [
+        (dict(magic=b"R4GX"), "checkpoint: bad magic: "),
+        (dict(version=2), "checkpoint: unsupported version 2"),
+        (dict(truncate=8), "checkpoint: truncated: "),
+    ]
+    for kw, msg in cases:
+        p = str(tmp_path / "bad.r4gs")
+        _write_r4gs(p, store, **kw)
+        with pytest.raises(rgs.CheckpointError) as e:
+            DeviceScene.load_checkpoint(ctx, p)
+        assert str(e.value).startswith(msg), str(e.value)
+    store.active_sh_degree = 4
+    p = str(tmp_path / "deg.r4gs")
+    _write_r4gs(p, store)
+    with pytest.raises(rgs.CheckpointError, match="malformed header"):
+        DeviceScene.load_checkpoint(ctx, p)
+    with pytest.raises(rgs.CheckpointError, match="cannot open"):
+        DeviceScene.load_checkpoint(ctx, str(tmp_path / "missing.r4gs"))
+
+
+def _densify_case(n, seed):
+    store = scenes.random_scene(n, sh_degree=3, seed=seed)
+    r = np.random.default_rng(seed)
+    m = r.normal(0, 1e-3, (n, 65))
+    v = r.uniform(0, 1e-5, (n, 65))
+    count = r.integers(0, 4, n).astype(np.int32)
+    accum = r.uniform(0, 1.5e-3, n) * count
+    return store, m, v, accum, count
+
+
+@pytest.mark.skipif(not O.reference_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("case", ["generic", "max_cut", "min_bound", "static"])
+def test_densify_and_prune_matches_reference(ctx, case):
+    """optim.cpp:168-234 on the device (FP64 scene) against the reference build with the same
+    mt19937_64 seed: identical store, moments, statistics reset and report."""
+    n = 2500
+    store, m, v, accum, count = _densify_case(n, {"generic": 1, "max_cut": 2, "min_bound": 3, "static": 4}[case])
+    kw = dict(percent_dense=0.02, prune_opacity=0.3)
+    if case == "max_cut":
+        kw["max_gaussians"] = n + 40
+    if case == "min_bound":
+        kw.update(prune_opacity=0.9, min_gaussians=n - 300)
+    if case == "static":
+        kw["static_mode"] = 1
+        store.rotor[:, [3, 5, 6, 7]] = 0.0
+    extent = 8.0
+    cfg = train.TrainConfig(**{k: v2 for k, v2 in kw.items() if k != "static_mode"}, static_mode=bool(kw.get("static_mode")))
+    sc = DeviceScene.from_store(ctx, store, f64=True)
+    opt = train.DeviceOptimizer(ctx, sc)
+    opt.upload(m, v, accum, count)
+    rng = train.Rng(ctx, seed=1234)
+    rep = train.densify_and_prune(ctx, sc, opt, cfg, extent, rng)
+    ref_store, rm, rv, racc, rcnt, rrep = O.ref_densify_and_prune(store, m, v, accum, count,
+                                                                   O.densify_config(**kw), extent, 1234)
+    assert (rep.cloned, rep.split, rep.pruned) == rrep
+    assert rep.cloned > 0 and rep.split > 0 and rep.pruned > 0
+    assert sc.n == ref_store.size()
+    for x, y in zip(sc.download(), O.OracleLib._scene(ref_store)):
+        assert np.array_equal(x, y.reshape(x.shape))
+    gm, gv, gacc, gcnt = opt.download()
+    assert np.array_equal(gm, rm) and np.array_equal(gv, rv)
+    assert not gacc.any() and not gcnt.any()
+
+
+def test_rng_matches_std_mt19937_64(ctx):
+    """The batch picks come from std::uniform_int_distribution over std::mt19937_64 (trainer.cpp:106)."""
+    rng = train.Rng(ctx, seed=0)
+    got = [rng.uniform_int(0, 9) for _ in range(8)]
+    assert all(0 <= g <= 9 for g in got) and len(set(got)) > 1
+    rng2 = train.Rng(ctx, seed=0)
+    assert [rng2.uniform_int(0, 9) for _ in range(8)] == got
+
+
+def test_trainer_densifies(ctx):
+    store, truth, cams = _training_case(n=3000, views=3)
+    tsc = DeviceScene.from_store(ctx, truth)
+    targets = [ctx.render_forward_device(tsc, c, retain=False)[0].clone() for c in cams]
+    sc = DeviceScene.from_store(ctx, store)
+    cfg = train.TrainConfig(densify_from=2, densify_interval=3, densify_grad_threshold=1e-6, total_steps=20)
+    tr = train.Trainer(ctx, sc, cfg, scene_extent=4.0)
+    n0 = sc.n
+    for _ in range(7):
+        lb = tr.step(cams, targets)
+    assert np.isfinite(lb.total)
+    assert sc.n != n0 and tr.grads.numel() == 65 * sc.n
