@@ -585,45 +585,69 @@ __global__ void __launch_bounds__(128) k_gaussian_backward(ParamView P, int sh_d
     const double dm2[2] = {g9[6], g9[7]};
     const double dab = g9[8];
 
-    double out[65];
+    // out[0..16]: mean4, ls4, rotor8, opacity; the 48 SH gradients are written directly.
+    double out[17];
 #pragma unroll
-    for (int k = 0; k < 65; ++k) out[k] = 0;
+    for (int k = 0; k < 17; ++k) out[k] = 0;
 
-    // ---- colour path: SH coefficients and view direction (rasterizer.cpp:137-147)
+    // ---- colour path: SH coefficients and view direction (rasterizer.cpp:137-147).
+    // The SH blocks are streamed once: the colour (for the clamp flags) and, per channel,
+    // t[ch][ax] = sum_k bgrad[k][ax] sh[k][ch] accumulate in the reference's k order.
     const int deg = sh_degree < 0 ? 0 : (sh_degree > 3 ? 3 : sh_degree);
     const int K = (deg + 1) * (deg + 1);
     double basis[16];
     d_sh_basis(o.dir, sh_degree, basis);
-    typename std::conditional<F64, double, float>::type shv[48];
+    double bgrad[48];
+    d_sh_basis_grad(o.dir, sh_degree, bgrad);
+    double acol[3] = {0, 0, 0}, tg[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+    const int nblocks = (3 * K + 3) / 4;
 #pragma unroll
     for (int b = 0; b < 12; ++b) {
-        if (b < (3 * K + 3) / 4) {
-            ld_block<F64>(P, 4 + b, i, shv + 4 * b);
-        } else {
-            shv[4 * b + 0] = shv[4 * b + 1] = shv[4 * b + 2] = shv[4 * b + 3] = 0;
+        if (b >= nblocks) break;
+        double v4[4];
+        ld_block<F64>(P, 4 + b, i, v4);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int j = 4 * b + e, k = j / 3, ch = j - 3 * k;
+            if (k >= K) break;
+            const double v = v4[e];
+            if (k == 0) {
+                acol[ch] = v * basis[0];
+#pragma unroll
+                for (int ax = 0; ax < 3; ++ax) tg[ch][ax] = bgrad[ax] * v;
+            } else {
+                acol[ch] += v * basis[k];
+#pragma unroll
+                for (int ax = 0; ax < 3; ++ax) tg[ch][ax] += bgrad[k * 3 + ax] * v;
+            }
         }
     }
+    bool live[3];
     double dL_ddir[3] = {0, 0, 0};
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+        const bool clamped = (acol[ch] + 0.5) < 0;
+        live[ch] = !(clamped || dcol[ch] == 0);
+        if (!live[ch]) continue;
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) dL_ddir[ax] += dcol[ch] * tg[ch][ax];
+    }
     {
-        double bgrad[48];
-        d_sh_basis_grad(o.dir, sh_degree, bgrad);
+        // SH gradients (rasterizer.cpp:139): d_sh(ch, k) = dcol[ch] basis[k] unless clamped
 #pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-            double a = (double)shv[ch] * basis[0];
+        for (int b = 0; b < 12; ++b) {
+            float f4[4];
 #pragma unroll
-            for (int k = 1; k < 16; ++k)
-                if (k < K) a += (double)shv[k * 3 + ch] * basis[k];
-            const bool clamped = (a + 0.5) < 0;
-            if (clamped || dcol[ch] == 0) continue;
-#pragma unroll
-            for (int k = 0; k < 16; ++k) out[17 + ch * 16 + k] += dcol[ch] * basis[k];
-#pragma unroll
-            for (int ax = 0; ax < 3; ++ax) {
-                double t = bgrad[ax] * (double)shv[ch];
-#pragma unroll
-                for (int k = 1; k < 16; ++k)
-                    if (k < K) t += bgrad[k * 3 + ax] * (double)shv[k * 3 + ch];
-                dL_ddir[ax] += dcol[ch] * t;
+            for (int e = 0; e < 4; ++e) {
+                const int j = 4 * b + e, k = j / 3, ch = j - 3 * k;
+                f4[e] = live[ch] ? (float)(0.0 + dcol[ch] * basis[k]) : 0.f;
+            }
+            float4* pb = reinterpret_cast<float4*>(grads + (16 + 4 * (size_t)b) * n) + i;
+            if (accumulate) {
+                const float4 t = *pb;
+                *pb = make_float4(t.x + f4[0], t.y + f4[1], t.z + f4[2], t.w + f4[3]);
+            } else {
+                *pb = make_float4(f4[0], f4[1], f4[2], f4[3]);
             }
         }
     }
@@ -743,18 +767,13 @@ __global__ void __launch_bounds__(128) k_gaussian_backward(ParamView P, int sh_d
         d_g4_backward(s, rot, G4, out);
     }
     // ---- write (scene SoA layout)
-    float f[65];
+    float f[17];
 #pragma unroll
-    for (int k = 0; k < 65; ++k) f[k] = (float)out[k];
+    for (int k = 0; k < 17; ++k) f[k] = (float)out[k];
     float4 om = make_float4(f[0], f[1], f[2], f[3]);
     float4 ol = make_float4(f[4], f[5], f[6], f[7]);
     float4 o0 = make_float4(f[8], f[9], f[10], f[11]);
     float4 o1 = make_float4(f[12], f[13], f[14], f[15]);
-    float shg[48];
-#pragma unroll
-    for (int ch = 0; ch < 3; ++ch)
-#pragma unroll
-        for (int k = 0; k < 16; ++k) shg[k * 3 + ch] = f[17 + ch * 16 + k];
     const float vn = (float)sqrt(dm2[0] * dm2[0] + dm2[1] * dm2[1]);
     if (accumulate) {
         float4 t;
@@ -762,12 +781,6 @@ __global__ void __launch_bounds__(128) k_gaussian_backward(ParamView P, int sh_d
         t = gl[i]; gl[i] = make_float4(t.x + ol.x, t.y + ol.y, t.z + ol.z, t.w + ol.w);
         t = gr0[i]; gr0[i] = make_float4(t.x + o0.x, t.y + o0.y, t.z + o0.z, t.w + o0.w);
         t = gr1[i]; gr1[i] = make_float4(t.x + o1.x, t.y + o1.y, t.z + o1.z, t.w + o1.w);
-#pragma unroll
-        for (int b = 0; b < 12; ++b) {
-            float4* p = reinterpret_cast<float4*>(grads + (16 + 4 * (size_t)b) * n) + i;
-            t = *p;
-            *p = make_float4(t.x + shg[4 * b], t.y + shg[4 * b + 1], t.z + shg[4 * b + 2], t.w + shg[4 * b + 3]);
-        }
         gop[i] += f[16];
         vnorm[i] += vn;
         visible[i] += 1;
@@ -776,10 +789,6 @@ __global__ void __launch_bounds__(128) k_gaussian_backward(ParamView P, int sh_d
         gl[i] = ol;
         gr0[i] = o0;
         gr1[i] = o1;
-#pragma unroll
-        for (int b = 0; b < 12; ++b)
-            reinterpret_cast<float4*>(grads + (16 + 4 * (size_t)b) * n)[i] =
-                make_float4(shg[4 * b], shg[4 * b + 1], shg[4 * b + 2], shg[4 * b + 3]);
         gop[i] = f[16];
         vnorm[i] = vn;
         visible[i] = 1;

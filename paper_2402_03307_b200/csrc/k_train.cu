@@ -570,6 +570,168 @@ __global__ void __launch_bounds__(kKnnThreads) k_knn(const double4* __restrict__
         for (int j = 0; j < K; ++j) out[(size_t)K * i + j] = bi[j];
 }
 
+
+// ---------------------------------------------------------------------------
+// K11b: exact KNN through a uniform 4D grid.  Points are counting-sorted by cell; a query
+// scans the (2r+1)^4 block of cells around its own, shell by shell, until its k-th
+// distance is below the distance to the unscanned region (with a relative safety margin
+// for the rounding of that bound), or the block covers the grid.  The top-k insertion is
+// lexicographic in (distance, index), so the result does not depend on the scan order and
+// equals the brute-force / KdTree4 answer.
+struct KnnGrid {
+    double lo[4], cell[4];
+    int G;  // cells per dimension
+};
+
+__device__ __forceinline__ int knn_cell_coord(double v, double lo, double cell, int G) {
+    int c = (int)floor((v - lo) / cell);
+    return c < 0 ? 0 : (c >= G ? G - 1 : c);
+}
+__device__ __forceinline__ int knn_cell_id(const double4& p, const KnnGrid& g) {
+    const int a = knn_cell_coord(p.x, g.lo[0], g.cell[0], g.G), b = knn_cell_coord(p.y, g.lo[1], g.cell[1], g.G);
+    const int c = knn_cell_coord(p.z, g.lo[2], g.cell[2], g.G), d = knn_cell_coord(p.w, g.lo[3], g.cell[3], g.G);
+    return ((d * g.G + c) * g.G + b) * g.G + a;
+}
+
+__global__ void k_knn_bounds(const double4* __restrict__ pts, int n, double* part) {
+    __shared__ double lo[4][256], hi[4][256];
+    const int t = threadIdx.x;
+    double l[4] = {INFINITY, INFINITY, INFINITY, INFINITY}, h[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    for (int i = blockIdx.x * 256 + t; i < n; i += gridDim.x * 256) {
+        const double4 p = pts[i];
+        const double v[4] = {p.x, p.y, p.z, p.w};
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            l[a] = fmin(l[a], v[a]);
+            h[a] = fmax(h[a], v[a]);
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        lo[a][t] = l[a];
+        hi[a][t] = h[a];
+    }
+    __syncthreads();
+    for (int s2 = 128; s2 > 0; s2 >>= 1) {
+        if (t < s2)
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                lo[a][t] = fmin(lo[a][t], lo[a][t + s2]);
+                hi[a][t] = fmax(hi[a][t], hi[a][t + s2]);
+            }
+        __syncthreads();
+    }
+    if (t < 4) {
+        part[8 * blockIdx.x + t] = lo[t][0];
+        part[8 * blockIdx.x + 4 + t] = hi[t][0];
+    }
+}
+
+__global__ void k_knn_cells(const double4* __restrict__ pts, int n, KnnGrid g, uint32_t* __restrict__ cell,
+                            uint32_t* __restrict__ count) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t c = (uint32_t)knn_cell_id(pts[i], g);
+    cell[i] = c;
+    atomicAdd(&count[c], 1u);
+}
+
+__global__ void k_knn_scatter(const double4* __restrict__ pts, int n, const uint32_t* __restrict__ cell,
+                              const uint32_t* __restrict__ start, uint32_t* __restrict__ cursor,
+                              double4* __restrict__ spts, int32_t* __restrict__ sidx) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t c = cell[i];
+    const uint32_t pos = start[c] + atomicAdd(&cursor[c], 1u);
+    spts[pos] = pts[i];
+    sidx[pos] = i;
+}
+
+template <int K>
+__device__ __forceinline__ void topk_insert(double* bd, int* bi, double dd, int j) {
+    if (!(dd < bd[K - 1] || (dd == bd[K - 1] && j < bi[K - 1]))) return;
+    double cd = dd;
+    int ci = j;
+#pragma unroll
+    for (int s = 0; s < K; ++s) {
+        const bool less = cd < bd[s] || (cd == bd[s] && ci < bi[s]);
+        const double td = bd[s];
+        const int ti = bi[s];
+        bd[s] = less ? cd : td;
+        bi[s] = less ? ci : ti;
+        cd = less ? td : cd;
+        ci = less ? ti : ci;
+    }
+}
+
+template <int K>
+__global__ void __launch_bounds__(128) k_knn_grid(const double4* __restrict__ spts, const int32_t* __restrict__ sidx,
+                                                  const uint32_t* __restrict__ start, int n, KnnGrid g,
+                                                  int32_t* __restrict__ out) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const double4 q = spts[t];
+    const int qi = sidx[t];
+    const int G = g.G;
+    const int qc[4] = {knn_cell_coord(q.x, g.lo[0], g.cell[0], G), knn_cell_coord(q.y, g.lo[1], g.cell[1], G),
+                       knn_cell_coord(q.z, g.lo[2], g.cell[2], G), knn_cell_coord(q.w, g.lo[3], g.cell[3], G)};
+    const double qv[4] = {q.x, q.y, q.z, q.w};
+    double bd[K];
+    int bi[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        bd[j] = INFINITY;
+        bi[j] = 0x7fffffff;
+    }
+    for (int r = 0;; ++r) {
+        int lo[4], hi[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            lo[a] = max(qc[a] - r, 0);
+            hi[a] = min(qc[a] + r, G - 1);
+        }
+        for (int d = lo[3]; d <= hi[3]; ++d)
+            for (int c = lo[2]; c <= hi[2]; ++c)
+                for (int b = lo[1]; b <= hi[1]; ++b)
+                    for (int a = lo[0]; a <= hi[0]; ++a) {
+                        // only the shell at Chebyshev distance r from the query's cell
+                        const int cheb = max(max(abs(a - qc[0]), abs(b - qc[1])), max(abs(c - qc[2]), abs(d - qc[3])));
+                        if (cheb != r) continue;
+                        const int cid = ((d * G + c) * G + b) * G + a;
+                        const uint32_t e0 = start[cid], e1 = start[cid + 1];
+                        for (uint32_t e = e0; e < e1; ++e) {
+                            const int j = sidx[e];
+                            if (j == qi) continue;
+                            const double4 p = spts[e];
+                            const double d0 = p.x - q.x, d1 = p.y - q.y, d2 = p.z - q.z, d3 = p.w - q.w;
+                            double dd = d0 * d0;
+                            dd += d1 * d1;
+                            dd += d2 * d2;
+                            dd += d3 * d3;
+                            topk_insert<K>(bd, bi, dd, j);
+                        }
+                    }
+        // distance from q to the unscanned region (sides at the grid edge are closed)
+        double bound = INFINITY;
+        bool all = true;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            if (qc[a] - r > 0) {
+                bound = fmin(bound, qv[a] - (g.lo[a] + (double)(qc[a] - r) * g.cell[a]));
+                all = false;
+            }
+            if (qc[a] + r < G - 1) {
+                bound = fmin(bound, (g.lo[a] + (double)(qc[a] + r + 1) * g.cell[a]) - qv[a]);
+                all = false;
+            }
+        }
+        if (all) break;
+        if (bi[K - 1] != 0x7fffffff && bound > 0 && bd[K - 1] < bound * bound * (1 - 1e-9)) break;
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j) out[(size_t)K * qi + j] = bi[j];
+}
+
 // Scaled 4D points (mean / scene scales, knn.cpp:106).
 template <bool F64>
 __global__ void k_knn_points(ParamView P, double4 scales, double4* pts) {
@@ -853,6 +1015,68 @@ int knn(const double* pts4, int n, int k, int32_t* out, cudaStream_t s) {
         default: return -1;
     }
     return 0;
+}
+
+int knn_grid(const double* pts4, int n, int k, int32_t* out, void* scratch, size_t scratch_bytes, cudaStream_t s) {
+    const double4* p = reinterpret_cast<const double4*>(pts4);
+    // grid resolution: ~2 points per cell on average
+    int G = (int)floor(pow(n / 2.0, 0.25));
+    G = G < 1 ? 1 : (G > 48 ? 48 : G);
+    const size_t ncell = (size_t)G * G * G * G;
+    // scratch layout: part[8*64] | cell[n] u32 | count[ncell+1] | start[ncell+1] | cursor[ncell] |
+    //                 scan tmp[ncell/1024+4096] | spts[n] double4 | sidx[n]
+    char* base = static_cast<char*>(scratch);
+    auto take = [&](size_t bytes) {
+        char* r = base;
+        base += (bytes + 255) & ~size_t(255);
+        return r;
+    };
+    double* part = (double*)take(8 * 64 * sizeof(double));
+    uint32_t* cell = (uint32_t*)take(4 * (size_t)n);
+    uint32_t* count = (uint32_t*)take(4 * (ncell + 1));
+    uint32_t* start = (uint32_t*)take(4 * (ncell + 1));
+    uint32_t* cursor = (uint32_t*)take(4 * ncell);
+    uint32_t* tmp = (uint32_t*)take(4 * (ncell / 1024 + 4096));
+    double4* spts = (double4*)take(32 * (size_t)n);
+    int32_t* sidx = (int32_t*)take(4 * (size_t)n);
+    if ((size_t)(base - static_cast<char*>(scratch)) > scratch_bytes) return -2;
+    k_knn_bounds<<<64, 256, 0, s>>>(p, n, part);
+    double hp[8 * 64];
+    cudaMemcpyAsync(hp, part, sizeof hp, cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return -3;
+    KnnGrid g;
+    g.G = G;
+    for (int a = 0; a < 4; ++a) {
+        double lo = INFINITY, hi = -INFINITY;
+        for (int b = 0; b < 64; ++b) {
+            lo = fmin(lo, hp[8 * b + a]);
+            hi = fmax(hi, hp[8 * b + 4 + a]);
+        }
+        g.lo[a] = lo;
+        g.cell[a] = (hi > lo && isfinite(hi - lo)) ? (hi - lo) / G : 1.0;
+    }
+    cudaMemsetAsync(count, 0, 4 * (ncell + 1), s);
+    cudaMemsetAsync(cursor, 0, 4 * ncell, s);
+    k_knn_cells<<<nblk(n, 256), 256, 0, s>>>(p, n, g, cell, count);
+    exclusive_scan(count, (int)ncell + 1, start, tmp, nullptr, s);
+    k_knn_scatter<<<nblk(n, 256), 256, 0, s>>>(p, n, cell, start, cursor, spts, sidx);
+    const int nb = nblk(n, 128);
+    switch (k) {
+        case 1: k_knn_grid<1><<<nb, 128, 0, s>>>(spts, sidx, start, n, g, out); break;
+        case 2: k_knn_grid<2><<<nb, 128, 0, s>>>(spts, sidx, start, n, g, out); break;
+        case 4: k_knn_grid<4><<<nb, 128, 0, s>>>(spts, sidx, start, n, g, out); break;
+        case 8: k_knn_grid<8><<<nb, 128, 0, s>>>(spts, sidx, start, n, g, out); break;
+        case 16: k_knn_grid<16><<<nb, 128, 0, s>>>(spts, sidx, start, n, g, out); break;
+        default: return -1;
+    }
+    return 0;
+}
+
+size_t knn_grid_scratch(int n) {
+    int G = (int)floor(pow(n / 2.0, 0.25));
+    G = G < 1 ? 1 : (G > 48 ? 48 : G);
+    const size_t ncell = (size_t)G * G * G * G;
+    return 8 * 64 * 8 + 4 * (size_t)n + 3 * 4 * (ncell + 1) + 4 * (ncell / 1024 + 4096) + 36 * (size_t)n + 8 * 256;
 }
 
 int extent_blocks(int n) { return nblk(n, 256); }

@@ -1316,7 +1316,7 @@ void ensure_ssim_window(rgs_ctx* c) {
 }
 
 struct TrainScratch {
-    DevBuf dfield, parts, speeds, dspeed, pts, lo, hi;
+    DevBuf dfield, parts, speeds, dspeed, pts, lo, hi, knn;
 };
 TrainScratch& train_scratch(rgs_ctx* c) {
     // One scratch set per context (kept alongside the context's other buffers).
@@ -1548,9 +1548,13 @@ int rgs_knn_build(rgs_ctx* c, const rgs_scene* scene, int k, const double* scale
         TrainScratch& ts = train_scratch(c);
         ts.pts.ensure(sizeof(double) * 4 * (size_t)scene->n, c->stream);
         rgs_launch::knn_points(scene->params, scene->params64, scene->n, sc, ts.pts.as<double>(), c->stream);
-        if (rgs_launch::knn(ts.pts.as<double>(), scene->n, k, neighbors, c->stream))
-            return set_err(c, RGS_E_INVALID, "knn: unsupported k");
-        c->launches += 2;
+        const size_t need = rgs_launch::knn_grid_scratch(scene->n);
+        ts.knn.ensure(need, c->stream);
+        const int rc = rgs_launch::knn_grid(ts.pts.as<double>(), scene->n, k, neighbors, ts.knn.p, ts.knn.bytes,
+                                            c->stream);
+        if (rc == -1) return set_err(c, RGS_E_INVALID, "knn: unsupported k");
+        if (rc) return set_err(c, RGS_E_CUDA, "knn: grid build failed");
+        c->launches += 9;
         CK(cudaGetLastError());
         return RGS_OK;
     });

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "rgs_internal.cuh"
+
 namespace rgs_dev {
 
 constexpr int kSsimWin = 11;  // ssim.cpp:12
@@ -58,6 +60,8 @@ void speed_backward(const float* params, const double* params64, int n, const do
 void knn_points(const float* params, const double* params64, int n, const double* scales, double* pts4,
                 cudaStream_t s);
 int knn(const double* pts4, int n, int k, int32_t* out, cudaStream_t s);
+int knn_grid(const double* pts4, int n, int k, int32_t* out, void* scratch, size_t scratch_bytes, cudaStream_t s);
+size_t knn_grid_scratch(int n);
 int extent_blocks(int n);
 void mean_extent(const float* params, const double* params64, int n, double* part_lo, double* part_hi,
                  cudaStream_t s);

@@ -178,6 +178,21 @@ def test_knn_and_scene_scales(ctx, T, k):
     assert np.array_equal(nb, T.knn4d(store.mean, k, scales, threads=8))
 
 
+def test_knn_grid_large_and_clustered(ctx, T):
+    """The grid KNN on a frustum-shaped synthetic scene (non-uniform density) and on a
+    clustered one: identical lists to the brute-force oracle."""
+    store = scenes.synthetic_scene(40000, 320, 240, seed=12)
+    sc = DeviceScene.from_store(ctx, store)
+    scales = train.scene_scales(ctx, sc)
+    nb = train.build_knn4d(ctx, sc, 8).cpu().numpy()
+    assert np.array_equal(nb, T.knn4d(store.mean, 8, scales, threads=16))
+    cl = scenes.random_scene(6000, sh_degree=0, seed=2)
+    cl.mean[:3000, :3] = cl.mean[:3000, :3] * 1e-3 + 0.5  # a dense cluster inside a sparse cloud
+    sc2 = DeviceScene.from_store(ctx, cl, f64=True)
+    nb2 = train.build_knn4d(ctx, sc2, 16).cpu().numpy()
+    assert np.array_equal(nb2, T.knn4d(cl.mean, 16, train.scene_scales(ctx, sc2), threads=16))
+
+
 def test_knn_ties(ctx, T):
     store = scenes.random_scene(64, sh_degree=0, seed=1)
     store.mean[:] = np.round(store.mean * 2) / 2  # many exact distance ties
