@@ -240,18 +240,24 @@ __device__ __forceinline__ float reduce_scatter9(const float* v, int lane, int& 
     return r;
 }
 
-// K6: back-to-front replay of the FP32 pixels (rasterizer.cpp:320-397).  Per-splat
-// partial sums are reduce-scattered across the warp, combined in shared memory and
-// scattered with one FP64 atomic per (tile, splat, component).  Slow pixels are replayed
-// in FP64 by k_backward_fp64.
+// K6: back-to-front replay of the FP32 pixels (rasterizer.cpp:320-397).  Splats are staged
+// kBwdBatch at a time.  Each warp reduce-scatters its per-splat partials and its owner lanes
+// store them with plain shared-memory stores into the warp's private slot (a warp visits a
+// staged splat at most once, so no atomics -- shared float atomics are CAS loops on this
+// architecture); after the batch the 8 warp slots are summed per (splat, component) and
+// scattered with one FP64 atomic each.  Slow pixels are replayed in FP64 by k_backward_fp64.
+constexpr int kBwdBatch = 128;
+constexpr int kBwdWarps = kTilePixels / 32;
+
 __global__ void __launch_bounds__(256) k_backward_fp32(SplatArrays sp, const uint32_t* __restrict__ vals,
                                                        const uint2* __restrict__ ranges, DevCamera cam, float3 bg,
                                                        const double* __restrict__ final_T,
                                                        const uint32_t* __restrict__ n_contrib,
                                                        const float* __restrict__ dL, double* sg) {
-    __shared__ StagedSplat sm[kTilePixels];
-    __shared__ uint32_t sid[kTilePixels];
-    __shared__ float acc[9][kTilePixels];
+    extern __shared__ float4 dyn_smem[];
+    StagedSplat* sm = reinterpret_cast<StagedSplat*>(dyn_smem);                   // [kBwdBatch]
+    uint32_t* sid = reinterpret_cast<uint32_t*>(sm + kBwdBatch);                   // [kBwdBatch]
+    float* accw = reinterpret_cast<float*>(sid + kBwdBatch);                       // [warps][batch][9]
     __shared__ int s_max;
     const int tile = blockIdx.x;
     const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
@@ -264,10 +270,12 @@ __global__ void __launch_bounds__(256) k_backward_fp32(SplatArrays sp, const uin
     const double px0 = tx * kTile, py0 = ty * kTile;
     const float fpx = (float)lx, fpy = (float)ly, fsx0 = (float)sx0, fsy0 = (float)sy0;
     constexpr float kLn2 = 0.69314718055994531f;
+    float* myacc = accw + (size_t)warp * kBwdBatch * 9;
 
     int contrib = 0;
     float T_run = 1.f, g0 = 0.f, g1 = 0.f, g2 = 0.f, s0 = 0.f, s1 = 0.f, s2 = 0.f;
     if (threadIdx.x == 0) s_max = 0;
+    for (int e = threadIdx.x; e < kBwdWarps * kBwdBatch * 9; e += kTilePixels) accw[e] = 0.f;
     if (inside) {
         const uint32_t pix = (uint32_t)py * cam.width + px;
         const uint32_t c = n_contrib[pix];
@@ -289,93 +297,98 @@ __global__ void __launch_bounds__(256) k_backward_fp32(SplatArrays sp, const uin
     __syncthreads();
     const int max_contrib = s_max;
 
-    for (int end = max_contrib; end > 0; end -= kTilePixels) {
-        const int beg = end > kTilePixels ? end - kTilePixels : 0;
+    for (int end = max_contrib; end > 0; end -= kBwdBatch) {
+        const int beg = end > kBwdBatch ? end - kBwdBatch : 0;
         const int cnt = end - beg;
         if ((int)threadIdx.x < cnt) {
             const uint32_t id = vals[rg.x + beg + threadIdx.x];
             sid[threadIdx.x] = id;
             stage<false>(sp, id, px0, py0, &sm[threadIdx.x]);
         }
-#pragma unroll
-        for (int q = 0; q < 9; ++q) acc[q][threadIdx.x] = 0.f;
         __syncthreads();
-        for (int c = ((cnt - 1) >> 5) << 5; c >= 0; c -= 32) {
-            const int k0 = c + lane;
-            unsigned mask =
-                __ballot_sync(kFull, k0 < cnt && beg + k0 < wmax && overlaps(sm[k0], fsx0, fsy0));
-            while (mask) {
-                const int j = 31 - __clz(mask);
-                mask &= ~(1u << j);
-                const int k = c + j;
-                float v[9];
+        if (beg < wmax) {
+            for (int c = ((cnt - 1) >> 5) << 5; c >= 0; c -= 32) {
+                const int k0 = c + lane;
+                unsigned mask =
+                    __ballot_sync(kFull, k0 < cnt && beg + k0 < wmax && overlaps(sm[k0], fsx0, fsy0));
+                while (mask) {
+                    const int j = 31 - __clz(mask);
+                    mask &= ~(1u << j);
+                    const int k = c + j;
+                    float v[9];
 #pragma unroll
-                for (int q = 0; q < 9; ++q) v[q] = 0.f;
-                bool act = false;
-                if (beg + k < contrib) {
-                    const float4 a = sm[k].a, b = sm[k].b;
-                    float p, M, dx, dy;
-                    // Non-slow pixels: every kept decision was certain in K5; an ambiguous
-                    // value here means K5 culled the pair, whose FP64 decision is "skip".
-                    if (classify(a, b, fpx, fpy, p, M, dx, dy) == kAccept) {
-                        const float4 cc = sm[k].c;
-                        const float e = ex2_approx(p);
-                        const float al = fminf(0.99f, __fmul_rn(cc.w, e));
-                        const float om = 1.f - al;
-                        const float inv_om = rcp_approx(om);
-                        const float T_before = T_run * inv_om;
-                        const float w = al * T_before;
-                        v[0] = w * g0;
-                        v[1] = w * g1;
-                        v[2] = w * g2;
-                        const float dL_da = g0 * fmaf(cc.x, T_before, -s0 * inv_om) +
-                                            g1 * fmaf(cc.y, T_before, -s1 * inv_om) +
-                                            g2 * fmaf(cc.z, T_before, -s2 * inv_om);
-                        if (p <= sm[k].d.z) {  // unclamped alpha <= 0.99: al = ab * e
-                            const float A = -2.f * kLn2 * a.z, B = -kLn2 * a.w, C = -2.f * kLn2 * b.x;
-                            v[8] = dL_da * e;
-                            const float dp = dL_da * al;
-                            v[3] = dp * (-0.5f * dx * dx);
-                            v[4] = dp * (-dx * dy);
-                            v[5] = dp * (-0.5f * dy * dy);
-                            v[6] = dp * fmaf(A, dx, B * dy);
-                            v[7] = dp * fmaf(B, dx, C * dy);
+                    for (int q = 0; q < 9; ++q) v[q] = 0.f;
+                    bool act = false;
+                    if (beg + k < contrib) {
+                        const float4 a = sm[k].a, b = sm[k].b;
+                        float p, M, dx, dy;
+                        // Non-slow pixels: every kept decision was certain in K5; an ambiguous
+                        // value here means K5 culled the pair, whose FP64 decision is "skip".
+                        if (classify(a, b, fpx, fpy, p, M, dx, dy) == kAccept) {
+                            const float4 cc = sm[k].c;
+                            const float e = ex2_approx(p);
+                            const float al = fminf(0.99f, __fmul_rn(cc.w, e));
+                            const float om = 1.f - al;
+                            const float inv_om = rcp_approx(om);
+                            const float T_before = T_run * inv_om;
+                            const float w = al * T_before;
+                            v[0] = w * g0;
+                            v[1] = w * g1;
+                            v[2] = w * g2;
+                            const float dL_da = g0 * fmaf(cc.x, T_before, -s0 * inv_om) +
+                                                g1 * fmaf(cc.y, T_before, -s1 * inv_om) +
+                                                g2 * fmaf(cc.z, T_before, -s2 * inv_om);
+                            if (p <= sm[k].d.z) {  // unclamped alpha <= 0.99: al = ab * e
+                                const float A = -2.f * kLn2 * a.z, B = -kLn2 * a.w, C = -2.f * kLn2 * b.x;
+                                v[8] = dL_da * e;
+                                const float dp = dL_da * al;
+                                v[3] = dp * (-0.5f * dx * dx);
+                                v[4] = dp * (-dx * dy);
+                                v[5] = dp * (-0.5f * dy * dy);
+                                v[6] = dp * fmaf(A, dx, B * dy);
+                                v[7] = dp * fmaf(B, dx, C * dy);
+                            }
+                            s0 = fmaf(cc.x, w, s0);
+                            s1 = fmaf(cc.y, w, s1);
+                            s2 = fmaf(cc.z, w, s2);
+                            T_run = T_before;
+                            act = true;
                         }
-                        s0 = fmaf(cc.x, w, s0);
-                        s1 = fmaf(cc.y, w, s1);
-                        s2 = fmaf(cc.z, w, s2);
-                        T_run = T_before;
-                        act = true;
                     }
-                }
-                const unsigned am = __ballot_sync(kFull, act);
-                if (am == 0) continue;
-                if (__popc(am) == 1) {
-                    if (act) {
+                    const unsigned am = __ballot_sync(kFull, act);
+                    if (am == 0) continue;
+                    float* slot = myacc + (size_t)k * 9;
+                    if (__popc(am) == 1) {
+                        if (act) {
 #pragma unroll
-                        for (int q = 0; q < 9; ++q)
-                            if (v[q] != 0.f) atomicAdd(&acc[q][k], v[q]);
+                            for (int q = 0; q < 9; ++q) slot[q] = v[q];
+                        }
+                    } else {
+                        int idx;
+                        bool ok;
+                        const float r = reduce_scatter9(v, lane, idx, ok);
+                        if (ok && !(lane & 1)) slot[idx] = r;
                     }
-                } else {
-                    int idx;
-                    bool ok;
-                    const float r = reduce_scatter9(v, lane, idx, ok);
-                    if (ok && !(lane & 1) && r != 0.f) atomicAdd(&acc[idx][k], r);
                 }
             }
         }
         __syncthreads();
-        if ((int)threadIdx.x < cnt) {
-            double* o = sg + (size_t)sid[threadIdx.x] * 9;
+        for (int e = threadIdx.x; e < cnt * 9; e += kTilePixels) {
+            float sum = 0.f;
 #pragma unroll
-            for (int q = 0; q < 9; ++q) {
-                const float val = acc[q][threadIdx.x];
-                if (val != 0.f) atomicAdd(o + q, (double)val);
+            for (int w = 0; w < kBwdWarps; ++w) {
+                float* pw = accw + (size_t)w * kBwdBatch * 9 + e;
+                sum += *pw;
+                *pw = 0.f;
             }
+            if (sum != 0.f) atomicAdd(sg + (size_t)sid[e / 9] * 9 + (e % 9), (double)sum);
         }
         __syncthreads();
     }
 }
+
+constexpr size_t kBwdSmem = sizeof(StagedSplat) * kBwdBatch + sizeof(uint32_t) * kBwdBatch +
+                            sizeof(float) * kBwdWarps * kBwdBatch * 9;
 
 }  // namespace rgs_dev
 
@@ -401,8 +414,13 @@ void backward_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2
                    float3 bg, const double* final_T, const uint32_t* n_contrib, const float* dL_dimage,
                    double* screen_grads, cudaStream_t s) {
     const int tiles = cam.tiles_x * cam.tiles_y;
-    k_backward_fp32<<<tiles, kTilePixels, 0, s>>>(sp, pair_vals, ranges, cam, bg, final_T, n_contrib, dL_dimage,
-                                                  screen_grads);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_backward_fp32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSmem);
+        attr = true;
+    }
+    k_backward_fp32<<<tiles, kTilePixels, kBwdSmem, s>>>(sp, pair_vals, ranges, cam, bg, final_T, n_contrib,
+                                                         dL_dimage, screen_grads);
 }
 
 }  // namespace rgs_launch

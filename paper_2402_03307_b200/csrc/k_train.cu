@@ -269,6 +269,9 @@ __device__ __forceinline__ void st1(void* base, size_t idx, double v) {
     else static_cast<float*>(base)[idx] = (float)v;
 }
 
+// One thread per (Gaussian, parameter group): blockIdx.y = 0 mean, 1 log scales, 2 rotor
+// (both blocks + normalize), 3 opacity (+ entropy, + accumulate_stats), 4..15 SH blocks.
+// Every group is independent, so the 16x wider grid hides the FP64 divide / sqrt latency.
 template <bool F64>
 __global__ void __launch_bounds__(128) k_adam_step(void* params, void* mom1, void* mom2, const float* __restrict__ grads,
                                                    const float* __restrict__ vnorm, const int32_t* __restrict__ visible,
@@ -276,38 +279,25 @@ __global__ void __launch_bounds__(128) k_adam_step(void* params, void* mom1, voi
                                                    AdamArgs a, unsigned long long* err, double* part_entropy) {
     __shared__ double red[256];
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int grp = blockIdx.y;
     double ent = 0;
     if (i < n) {
-        // accumulate_stats (optim.cpp:159-166), on the batch-summed view statistics.
-        if (a.stats && visible[i] > 0) {
-            accum[i] += (double)vnorm[i];
-            count[i] += 1;
-        }
         double p[4], m[4], v[4], g[4];
-        // mean (x, y, z, t): lr_position schedule; static mode freezes t
-        ld4<F64>(params, n, 0, i, p);
-        ld4<F64>(mom1, n, 0, i, m);
-        ld4<F64>(mom2, n, 0, i, v);
-        ld4<false>(grads, n, 0, i, g);
+        if (grp == 0 || grp == 1) {
+            // mean (lr_position schedule) / log scales; static mode freezes t
+            const double lr = grp == 0 ? a.lr_pos : a.lr_scales;
+            ld4<F64>(params, n, grp, i, p);
+            ld4<F64>(mom1, n, grp, i, m);
+            ld4<F64>(mom2, n, grp, i, v);
+            ld4<false>(grads, n, grp, i, g);
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-            if (!(a.static_mode && k == 3)) adam_scalar(p[k], m[k], v[k], g[k], a.lr_pos, a.bc1, a.bc2);
-        st4<F64>(params, n, 0, i, p);
-        st4<F64>(mom1, n, 0, i, m);
-        st4<F64>(mom2, n, 0, i, v);
-        // log scales
-        ld4<F64>(params, n, 1, i, p);
-        ld4<F64>(mom1, n, 1, i, m);
-        ld4<F64>(mom2, n, 1, i, v);
-        ld4<false>(grads, n, 1, i, g);
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-            if (!(a.static_mode && k == 3)) adam_scalar(p[k], m[k], v[k], g[k], a.lr_scales, a.bc1, a.bc2);
-        st4<F64>(params, n, 1, i, p);
-        st4<F64>(mom1, n, 1, i, m);
-        st4<F64>(mom2, n, 1, i, v);
-        // rotor: Adam on the 8 stored coefficients, then normalize (rotor.cpp:117-136)
-        {
+            for (int k = 0; k < 4; ++k)
+                if (!(a.static_mode && k == 3)) adam_scalar(p[k], m[k], v[k], g[k], lr, a.bc1, a.bc2);
+            st4<F64>(params, n, grp, i, p);
+            st4<F64>(mom1, n, grp, i, m);
+            st4<F64>(mom2, n, grp, i, v);
+        } else if (grp == 2) {
+            // rotor: Adam on the 8 stored coefficients, then normalize (rotor.cpp:117-136)
             double rc[8], rm[8], rv[8], rg[8];
             ld4<F64>(params, n, 2, i, rc);
             ld4<F64>(params, n, 3, i, rc + 4);
@@ -335,9 +325,13 @@ __global__ void __launch_bounds__(128) k_adam_step(void* params, void* mom1, voi
             st4<F64>(mom1, n, 3, i, rm + 4);
             st4<F64>(mom2, n, 2, i, rv);
             st4<F64>(mom2, n, 3, i, rv + 4);
-        }
-        // opacity (+ entropy regularizer, loss.cpp:16-31 folded as trainer.cpp:55-64)
-        {
+        } else if (grp == 3) {
+            // accumulate_stats (optim.cpp:159-166) on the batch-summed view statistics
+            if (a.stats && visible[i] > 0) {
+                accum[i] += (double)vnorm[i];
+                count[i] += 1;
+            }
+            // opacity (+ entropy regularizer, loss.cpp:16-31 folded as trainer.cpp:55-64)
             const size_t io = 64 * (size_t)n + i;
             double po = ld1<F64>(params, io), mo = ld1<F64>(mom1, io), vo = ld1<F64>(mom2, io);
             double go = grads[io];
@@ -354,32 +348,31 @@ __global__ void __launch_bounds__(128) k_adam_step(void* params, void* mom1, voi
             st1<F64>(params, io, po);
             st1<F64>(mom1, io, mo);
             st1<F64>(mom2, io, vo);
-        }
-        // SH: block b holds coefficients j = 4b..4b+3, j = k*3 + ch; DC (k = 0) is j < 3
-#pragma unroll 1
-        for (int b = 0; b < 12; ++b) {
-            ld4<F64>(params, n, 4 + b, i, p);
-            ld4<F64>(mom1, n, 4 + b, i, m);
-            ld4<F64>(mom2, n, 4 + b, i, v);
-            ld4<false>(grads, n, 4 + b, i, g);
+        } else {
+            // SH block b = grp - 4 holds coefficients j = 4b..4b+3, j = k*3 + ch; DC is j < 3
+            const int b = grp - 4;
+            ld4<F64>(params, n, grp, i, p);
+            ld4<F64>(mom1, n, grp, i, m);
+            ld4<F64>(mom2, n, grp, i, v);
+            ld4<false>(grads, n, grp, i, g);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const double lr = (4 * b + e) < 3 ? a.lr_sh_dc : a.lr_sh_rest;
                 adam_scalar(p[e], m[e], v[e], g[e], lr, a.bc1, a.bc2);
             }
-            st4<F64>(params, n, 4 + b, i, p);
-            st4<F64>(mom1, n, 4 + b, i, m);
-            st4<F64>(mom2, n, 4 + b, i, v);
+            st4<F64>(params, n, grp, i, p);
+            st4<F64>(mom1, n, grp, i, m);
+            st4<F64>(mom2, n, grp, i, v);
         }
     }
-    if (part_entropy) {
+    if (part_entropy && grp == 3) {
         // 128-thread blocks: pad the reduction buffer.
         const int t = threadIdx.x;
         red[t] = ent;
         red[t + 128] = 0;
         __syncthreads();
-        for (int s = 128; s > 0; s >>= 1) {
-            if (t < s) red[t] = red[t] + red[t + s];
+        for (int s2 = 128; s2 > 0; s2 >>= 1) {
+            if (t < s2) red[t] = red[t] + red[t + s2];
             __syncthreads();
         }
         if (t == 0) part_entropy[blockIdx.x] = red[0];
@@ -948,10 +941,10 @@ void adam_step(bool f64, void* params, void* m1, void* m2, const float* grads, c
                unsigned long long* err, double* part_entropy, double* losses_entropy, int accumulate, cudaStream_t s) {
     const int nb = nblk(n, 128);
     if (f64)
-        k_adam_step<true><<<nb, 128, 0, s>>>(params, m1, m2, grads, vnorm, visible, accum, count, n, a, err,
+        k_adam_step<true><<<dim3(nb, 16), 128, 0, s>>>(params, m1, m2, grads, vnorm, visible, accum, count, n, a, err,
                                             part_entropy);
     else
-        k_adam_step<false><<<nb, 128, 0, s>>>(params, m1, m2, grads, vnorm, visible, accum, count, n, a, err,
+        k_adam_step<false><<<dim3(nb, 16), 128, 0, s>>>(params, m1, m2, grads, vnorm, visible, accum, count, n, a, err,
                                              part_entropy);
     if (part_entropy && losses_entropy)
         k_finalize<<<1, 256, 0, s>>>(part_entropy, nb, (double)n, 1.0, 0, accumulate, losses_entropy);
