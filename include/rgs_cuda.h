@@ -241,6 +241,15 @@ int rgs_image_loss(rgs_ctx* ctx, const float* rendered, const float* target, int
                    double w_l1, double w_ssim, double loss_scale, unsigned flags, float* dL_dimage,
                    double* losses);
 
+/* As rgs_image_loss on float64 images (the reference's Image type) with a float64 dL_dimage: the
+ * gradient is bit-identical to the reference's l1_loss_backward / ssim_loss_with_grad mix. */
+int rgs_image_loss_f64(rgs_ctx* ctx, const double* rendered, const double* target, int width, int height,
+                       double w_l1, double w_ssim, double loss_scale, unsigned flags, double* dL_dimage,
+                       double* losses);
+/* entropy_loss_with_grad (loss.cpp:16-31) on a device array of opacities: grad (may be NULL,
+ * n doubles) = dL/dopacity; loss (may be NULL, device double). */
+int rgs_entropy_loss(rgs_ctx* ctx, const double* opacities, int n, double* grad, double* loss);
+
 /* TrainConfig subset of one optimizer step (optim.hpp:17-63) + the entropy weight
  * (LossWeights::lambda_entropy, loss.hpp:12), folded into the step as trainer.cpp:55-64 does. */
 typedef struct {
@@ -272,6 +281,8 @@ int rgs_optimizer_download(rgs_ctx* ctx, const rgs_optimizer* opt, double* m65, 
                            double* grad_accum, int32_t* grad_count);
 int rgs_optimizer_upload(rgs_ctx* ctx, rgs_optimizer* opt, const double* m65, const double* v65,
                          const double* grad_accum, const int32_t* grad_count);
+/* accumulate_stats (optim.cpp:159-166) on its own: accum += vnorm, count += 1 where visible > 0. */
+int rgs_accumulate_stats(rgs_ctx* ctx, rgs_optimizer* opt, const float* vnorm, const int32_t* visible);
 /* GaussianStore::reset_stats (gaussian.cpp:186-189). */
 int rgs_optimizer_reset_stats(rgs_ctx* ctx, rgs_optimizer* opt);
 /* reset_opacity (optim.cpp:236-243): opacity -> min(opacity, value), its moments zeroed. */
@@ -292,6 +303,10 @@ typedef struct rgs_rng rgs_rng;
 int rgs_rng_create(unsigned long long seed, rgs_rng** out);
 void rgs_rng_destroy(rgs_rng* rng);
 int rgs_rng_uniform_int(rgs_rng* rng, int lo, int hi, int* out);
+/* The engine's state as text (std::mt19937_64 operator<< / >>), so a caller's own engine can be
+ * handed to rgs_densify_and_prune and taken back.  get: *len = bytes needed incl. the NUL. */
+int rgs_rng_get_state(const rgs_rng* rng, char* buf, size_t cap, size_t* len);
+int rgs_rng_set_state(rgs_rng* rng, const char* buf);
 
 /* TrainConfig's adaptive density control fields (optim.hpp:31-42). */
 typedef struct {
@@ -313,8 +328,18 @@ int rgs_densify_and_prune(rgs_ctx* ctx, rgs_scene* scene, rgs_optimizer* opt, co
 /* scene_scales (trainer.cpp:12-20) -> host out4.  Synchronises. */
 int rgs_scene_scales(rgs_ctx* ctx, const rgs_scene* scene, double* out4);
 /* build_knn4d (knn.cpp:101-116): neighbors[N*k] (device int32), exact, ordered by (distance,
- * index) on mean / scales; scales = NULL uses rgs_scene_scales.  k in {1, 2, 4, 8, 16}. */
+ * index) on mean / scales; scales = NULL uses rgs_scene_scales.  1 <= k <= 16. */
 int rgs_knn_build(rgs_ctx* ctx, const rgs_scene* scene, int k, const double* scales, int32_t* neighbors);
+/* KdTree4::knn (knn.cpp:60-99) for a batch of query points: the k (<= 16) nearest data points
+ * of each query, ordered by (squared distance, index), skipping exclude[q] (may be NULL);
+ * out[nq*k] (device), -1 where fewer than k data points exist.  points4 / queries4: device
+ * arrays of 4 doubles per point. */
+int rgs_knn_query(rgs_ctx* ctx, const double* points4, int n, const double* queries4, int nq, const int32_t* exclude,
+                  int k, int32_t* out);
+/* consistency_loss (loss.cpp:33-58) on given speeds (device, 3 doubles each) and a neighbour
+ * table (device, n*k): dspeed (may be NULL, n*3) = dL/dspeed; losses (may be NULL): [0] = loss. */
+int rgs_consistency_loss(rgs_ctx* ctx, const double* speeds, int n, const int32_t* neighbors, int k, double* dspeed,
+                         double* losses);
 /* consistency_loss (loss.cpp:33-58) over gaussian_speed (gaussian.cpp:103-110) and its
  * gradient through slice_backward (trainer.cpp:66-77): grads (may be NULL) += lambda *
  * dL/dparams; losses (may be NULL): [0] = consistency_loss (+= with RGS_FLAG_ACCUMULATE).

@@ -47,6 +47,9 @@ __device__ __forceinline__ void stage(const SplatArrays& sp, uint32_t id, double
     dst->d = make_float4(e.x, e.y, g.y, __fdiv_ru(1.f, __fsub_rd(1.f, am)) * 1.000001f);
 }
 
+// Per-warp culling of a staged splat against the warp's 8x4 sub-tile with the bounding box
+// of its alpha >= 1/255 ellipse.  (An exact ellipse-rectangle test removed 19% of the
+// evaluations but cost more in the ballot phase than it saved: measured, round 1.)
 __device__ __forceinline__ bool overlaps(const StagedSplat& s, float sx0, float sy0) {
     return (s.a.x + s.d.x >= sx0) && (s.a.x - s.d.x <= sx0 + 7.f) && (s.a.y + s.d.y >= sy0) &&
            (s.a.y - s.d.y <= sy0 + 3.f);
@@ -97,7 +100,7 @@ constexpr unsigned kFull = 0xffffffffu;
 
 // K5: forward blend.
 template <bool FLOW, bool COUNT>
-__global__ void __launch_bounds__(256) k_blend_fp32(SplatArrays sp, const uint32_t* __restrict__ vals,
+__global__ void __launch_bounds__(256, 5) k_blend_fp32(SplatArrays sp, const uint32_t* __restrict__ vals,
                                                     const uint2* __restrict__ ranges, DevCamera cam, float3 bg,
                                                     float* __restrict__ image, double* __restrict__ final_T,
                                                     uint32_t* __restrict__ n_contrib, uint32_t* slow_list,

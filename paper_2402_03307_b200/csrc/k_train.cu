@@ -44,12 +44,13 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 // ---------------------------------------------------------------------------
 // K8a: SSIM forward over one tile of valid positions and one channel.
 // Tile: kSsimTX x kSsimTY valid positions; input footprint (TX+10) x (TY+10).
-__global__ void __launch_bounds__(256) k_ssim_fields(const float* __restrict__ img, const float* __restrict__ tgt,
+template <typename TI>
+__global__ void __launch_bounds__(256) k_ssim_fields(const TI* __restrict__ img, const TI* __restrict__ tgt,
                                                      int W, int H, int want_grad, double* __restrict__ dfield,
                                                      double* __restrict__ part_ssim) {
     constexpr int TX = kSsimTX, TY = kSsimTY, IX = TX + kSsimWin - 1, IY = TY + kSsimWin - 1;
-    __shared__ float sa[IY][IX + 1];
-    __shared__ float sb[IY][IX + 1];
+    __shared__ TI sa[IY][IX + 1];
+    __shared__ TI sb[IY][IX + 1];
     __shared__ double rows[5][IY][TX];
     __shared__ double red[256];
     const int vw = W - kSsimWin + 1, vh = H - kSsimWin + 1;
@@ -58,7 +59,7 @@ __global__ void __launch_bounds__(256) k_ssim_fields(const float* __restrict__ i
     for (int e = t; e < IY * IX; e += 256) {
         const int r = e / IX, c = e % IX;
         const int gx = x0 + c, gy = y0 + r;
-        float a = 0.f, b = 0.f;
+        TI a = 0, b = 0;
         if (gx < W && gy < H) {
             const size_t p = ((size_t)gy * W + gx) * 3 + ch;
             a = img[p];
@@ -134,9 +135,10 @@ __global__ void __launch_bounds__(256) k_ssim_fields(const float* __restrict__ i
 
 // K8b: per output pixel and channel: adjoint convolutions of the three seeds, the SSIM
 // gradient, the L1 gradient and their weighted sum (FP32 dL/dimage for render_backward).
-__global__ void __launch_bounds__(256) k_image_grad(const float* __restrict__ img, const float* __restrict__ tgt,
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(256) k_image_grad(const TI* __restrict__ img, const TI* __restrict__ tgt,
                                                     int W, int H, const double* __restrict__ dfield,
-                                                    ImageGradArgs a, float* __restrict__ dl,
+                                                    ImageGradArgs a, TO* __restrict__ dl,
                                                     double* __restrict__ part_l1, double* __restrict__ part_sq) {
     constexpr int TX = kSsimTX, TY = kSsimTY, DX = TX + kSsimWin - 1, DY = TY + kSsimWin - 1;
     __shared__ double sd[3][DY][DX];
@@ -193,7 +195,7 @@ __global__ void __launch_bounds__(256) k_image_grad(const float* __restrict__ im
             }
             const double g_l1 = d > 0 ? a.inv_n : (d < 0 ? -a.inv_n : 0);  // image.cpp:33
             const double v = a.w_l1 * g_l1 + a.w_ssim * g_ssim;            // trainer.cpp:47-49
-            dl[p] = a.accumulate ? (float)((double)dl[p] + v) : (float)v;
+            dl[p] = a.accumulate ? (TO)((double)dl[p] + v) : (TO)v;
         }
     }
     const double s1 = block_sum(l1, red);
@@ -218,6 +220,34 @@ __global__ void __launch_bounds__(256) k_finalize(const double* __restrict__ par
         v = v * scale;
         *out = accumulate ? *out + v : v;
     }
+}
+
+
+// loss.cpp:16-31 on an opacity array (the standalone form of the term folded into K9).
+__global__ void __launch_bounds__(256) k_entropy(const double* __restrict__ op, int n, double* __restrict__ grad,
+                                                 double* part) {
+    __shared__ double red[256];
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    double t = 0;
+    if (i < n) {
+        const double lo = 1e-6, hi = 1 - 1e-6, inv_n = 1 / (double)n;
+        const double o0 = op[i];
+        const double o = o0 < lo ? lo : (hi < o0 ? hi : o0);
+        const double lg = log(o);
+        t = -o * lg;
+        if (grad) grad[i] = (o0 > lo && o0 < hi) ? -(lg + 1) * inv_n : 0;
+    }
+    const double s2 = block_sum(t, red);
+    if (threadIdx.x == 0) part[blockIdx.x] = s2;
+}
+
+// optim.cpp:159-166 standalone.
+__global__ void k_accumulate_stats(const float* __restrict__ vnorm, const int32_t* __restrict__ visible, int n,
+                                   double* __restrict__ accum, int32_t* __restrict__ count) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || !(visible[i] > 0)) return;
+    accum[i] += (double)vnorm[i];
+    count[i] += 1;
 }
 
 // ---------------------------------------------------------------------------
@@ -657,14 +687,19 @@ __device__ __forceinline__ void topk_insert(double* bd, int* bi, double dd, int 
     }
 }
 
+// Queries: qpts[t] (t < nq); result row qrow[t] (or t), excluded data index qexcl[t] (or -1);
+// k_out <= K columns written, -1 where fewer than k_out candidates exist.
 template <int K>
 __global__ void __launch_bounds__(128) k_knn_grid(const double4* __restrict__ spts, const int32_t* __restrict__ sidx,
-                                                  const uint32_t* __restrict__ start, int n, KnnGrid g,
+                                                  const uint32_t* __restrict__ start, KnnGrid g,
+                                                  const double4* __restrict__ qpts, const int32_t* __restrict__ qrow,
+                                                  const int32_t* __restrict__ qexcl, int nq, int k_out,
                                                   int32_t* __restrict__ out) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n) return;
-    const double4 q = spts[t];
-    const int qi = sidx[t];
+    if (t >= nq) return;
+    const double4 q = qpts[t];
+    const int qi = qexcl ? qexcl[t] : -1;
+    const int row = qrow ? qrow[t] : t;
     const int G = g.G;
     const int qc[4] = {knn_cell_coord(q.x, g.lo[0], g.cell[0], G), knn_cell_coord(q.y, g.lo[1], g.cell[1], G),
                        knn_cell_coord(q.z, g.lo[2], g.cell[2], G), knn_cell_coord(q.w, g.lo[3], g.cell[3], G)};
@@ -721,8 +756,7 @@ __global__ void __launch_bounds__(128) k_knn_grid(const double4* __restrict__ sp
         if (all) break;
         if (bi[K - 1] != 0x7fffffff && bound > 0 && bd[K - 1] < bound * bound * (1 - 1e-9)) break;
     }
-#pragma unroll
-    for (int j = 0; j < K; ++j) out[(size_t)K * qi + j] = bi[j];
+    for (int j = 0; j < k_out; ++j) out[(size_t)k_out * row + j] = bi[j] == 0x7fffffff ? -1 : bi[j];
 }
 
 // Scaled 4D points (mean / scene scales, knn.cpp:106).
@@ -919,21 +953,31 @@ ImageLossGrid image_loss_grid(int W, int H) {
     return g;
 }
 
-void image_loss(const float* img, const float* tgt, int W, int H, const ImageGradArgs& a, float* dl,
-                double* dfield, double* parts, double* losses, double loss_scale, int accumulate, cudaStream_t s) {
+template <typename TI, typename TO>
+void image_loss_t(const TI* img, const TI* tgt, int W, int H, const ImageGradArgs& a, TO* dl, double* dfield,
+                  double* parts, double* losses, double loss_scale, int accumulate, cudaStream_t s) {
     const ImageLossGrid g = image_loss_grid(W, H);
     const double count = 3.0 * (double)(W - kSsimWin + 1) * (double)(H - kSsimWin + 1);
     const double nvals = 3.0 * (double)W * (double)H;
     double* pa = parts;
     double* pl1 = parts + g.n_a;
     double* psq = pl1 + g.n_b;
-    k_ssim_fields<<<dim3(g.a_x, g.a_y, 3), 256, 0, s>>>(img, tgt, W, H, dl != nullptr, dfield, pa);
-    k_image_grad<<<dim3(g.b_x, g.b_y, 3), 256, 0, s>>>(img, tgt, W, H, dfield, a, dl, pl1, psq);
+    k_ssim_fields<TI><<<dim3(g.a_x, g.a_y, 3), 256, 0, s>>>(img, tgt, W, H, dl != nullptr, dfield, pa);
+    k_image_grad<TI, TO><<<dim3(g.b_x, g.b_y, 3), 256, 0, s>>>(img, tgt, W, H, dfield, a, dl, pl1, psq);
     if (losses) {
         k_finalize<<<1, 256, 0, s>>>(pl1, g.n_b, nvals, loss_scale, 0, accumulate, losses + 0);
         k_finalize<<<1, 256, 0, s>>>(pa, g.n_a, count, loss_scale, 1, accumulate, losses + 1);
         k_finalize<<<1, 256, 0, s>>>(psq, g.n_b, nvals, loss_scale, 0, accumulate, losses + 2);
     }
+}
+
+void image_loss(const float* img, const float* tgt, int W, int H, const ImageGradArgs& a, float* dl,
+                double* dfield, double* parts, double* losses, double loss_scale, int accumulate, cudaStream_t s) {
+    image_loss_t<float, float>(img, tgt, W, H, a, dl, dfield, parts, losses, loss_scale, accumulate, s);
+}
+void image_loss_f64(const double* img, const double* tgt, int W, int H, const ImageGradArgs& a, double* dl,
+                    double* dfield, double* parts, double* losses, double loss_scale, int accumulate, cudaStream_t s) {
+    image_loss_t<double, double>(img, tgt, W, H, a, dl, dfield, parts, losses, loss_scale, accumulate, s);
 }
 
 void adam_step(bool f64, void* params, void* m1, void* m2, const float* grads, const float* vnorm,
@@ -951,6 +995,17 @@ void adam_step(bool f64, void* params, void* m1, void* m2, const float* grads, c
 }
 
 int adam_blocks(int n) { return nblk(n, 128); }
+
+void entropy(const double* op, int n, double* grad, double* parts, double* loss, cudaStream_t s) {
+    const int nb = nblk(n, 256);
+    k_entropy<<<nb, 256, 0, s>>>(op, n, grad, parts);
+    if (loss) k_finalize<<<1, 256, 0, s>>>(parts, nb, (double)n, 1.0, 0, 0, loss);
+}
+
+void accumulate_stats(const float* vnorm, const int32_t* visible, int n, double* accum, int32_t* count,
+                      cudaStream_t s) {
+    if (n > 0) k_accumulate_stats<<<nblk(n, 256), 256, 0, s>>>(vnorm, visible, n, accum, count);
+}
 
 void reset_opacity(bool f64, void* params, void* m1, void* m2, int n, double value, cudaStream_t s) {
     if (f64)
@@ -1010,14 +1065,14 @@ int knn(const double* pts4, int n, int k, int32_t* out, cudaStream_t s) {
     return 0;
 }
 
-int knn_grid(const double* pts4, int n, int k, int32_t* out, void* scratch, size_t scratch_bytes, cudaStream_t s) {
+// Grid build over the data points + query launch.  queries4 == NULL: the data points are the
+// queries (self excluded, rows in data order) -- build_knn4d.
+int knn_grid(const double* pts4, int n, const double* queries4, const int32_t* qexcl, int nq, int k, int32_t* out,
+             void* scratch, size_t scratch_bytes, cudaStream_t s) {
     const double4* p = reinterpret_cast<const double4*>(pts4);
-    // grid resolution: ~2 points per cell on average
     int G = (int)floor(pow(n / 2.0, 0.25));
     G = G < 1 ? 1 : (G > 48 ? 48 : G);
     const size_t ncell = (size_t)G * G * G * G;
-    // scratch layout: part[8*64] | cell[n] u32 | count[ncell+1] | start[ncell+1] | cursor[ncell] |
-    //                 scan tmp[ncell/1024+4096] | spts[n] double4 | sidx[n]
     char* base = static_cast<char*>(scratch);
     auto take = [&](size_t bytes) {
         char* r = base;
@@ -1053,14 +1108,19 @@ int knn_grid(const double* pts4, int n, int k, int32_t* out, void* scratch, size
     k_knn_cells<<<nblk(n, 256), 256, 0, s>>>(p, n, g, cell, count);
     exclusive_scan(count, (int)ncell + 1, start, tmp, nullptr, s);
     k_knn_scatter<<<nblk(n, 256), 256, 0, s>>>(p, n, cell, start, cursor, spts, sidx);
-    const int nb = nblk(n, 128);
-    switch (k) {
-        case 1: k_knn_grid<1><<<nb, 128, 0, s>>>(spts, sidx, start, n, g, out); break;
-        case 2: k_knn_grid<2><<<nb, 128, 0, s>>>(spts, sidx, start, n, g, out); break;
-        case 4: k_knn_grid<4><<<nb, 128, 0, s>>>(spts, sidx, start, n, g, out); break;
-        case 8: k_knn_grid<8><<<nb, 128, 0, s>>>(spts, sidx, start, n, g, out); break;
-        case 16: k_knn_grid<16><<<nb, 128, 0, s>>>(spts, sidx, start, n, g, out); break;
-        default: return -1;
+    const double4* qp = queries4 ? reinterpret_cast<const double4*>(queries4) : spts;
+    const int32_t* qrow = queries4 ? nullptr : sidx;
+    const int32_t* qx = queries4 ? qexcl : sidx;
+    const int nqq = queries4 ? nq : n;
+    const int nb = nblk(nqq, 128);
+    const int K = k <= 1 ? 1 : (k <= 2 ? 2 : (k <= 4 ? 4 : (k <= 8 ? 8 : 16)));
+    if (k < 1 || k > 16) return -1;
+    switch (K) {
+        case 1: k_knn_grid<1><<<nb, 128, 0, s>>>(spts, sidx, start, g, qp, qrow, qx, nqq, k, out); break;
+        case 2: k_knn_grid<2><<<nb, 128, 0, s>>>(spts, sidx, start, g, qp, qrow, qx, nqq, k, out); break;
+        case 4: k_knn_grid<4><<<nb, 128, 0, s>>>(spts, sidx, start, g, qp, qrow, qx, nqq, k, out); break;
+        case 8: k_knn_grid<8><<<nb, 128, 0, s>>>(spts, sidx, start, g, qp, qrow, qx, nqq, k, out); break;
+        default: k_knn_grid<16><<<nb, 128, 0, s>>>(spts, sidx, start, g, qp, qrow, qx, nqq, k, out); break;
     }
     return 0;
 }

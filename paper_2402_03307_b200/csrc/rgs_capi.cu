@@ -1358,6 +1358,49 @@ int rgs_image_loss(rgs_ctx* c, const float* rendered, const float* target, int w
     });
 }
 
+int rgs_image_loss_f64(rgs_ctx* c, const double* rendered, const double* target, int width, int height, double w_l1,
+                       double w_ssim, double loss_scale, unsigned flags, double* dL_dimage, double* losses) {
+    if (!rendered || !target || width <= 0 || height <= 0) return RGS_E_INVALID;
+    if (width < kSsimWin || height < kSsimWin)
+        return set_err(c, RGS_E_INVALID, "ssim: image smaller than the 11x11 window");
+    return guarded(c, [&]() -> int {
+        cudaStream_t s = c->stream;
+        ensure_ssim_window(c);
+        TrainScratch& ts = train_scratch(c);
+        const ImageLossGrid g = rgs_launch::image_loss_grid(width, height);
+        const size_t nv = (size_t)(width - kSsimWin + 1) * (height - kSsimWin + 1);
+        if (dL_dimage) ts.dfield.ensure(sizeof(double) * 9 * nv, s);
+        ts.parts.ensure(sizeof(double) * (g.n_a + 2 * g.n_b + 16), s);
+        ImageGradArgs a;
+        a.w_l1 = w_l1;
+        a.w_ssim = w_ssim;
+        a.inv_n = 1 / (3.0 * (double)width * (double)height);
+        a.ssim_scale = -1 / (3.0 * (double)nv);
+        a.accumulate = (flags & RGS_FLAG_ACCUMULATE_GRAD) ? 1 : 0;
+        rgs_launch::image_loss_f64(rendered, target, width, height, a, dL_dimage, ts.dfield.as<double>(),
+                                   ts.parts.as<double>(), losses, loss_scale, (flags & RGS_FLAG_ACCUMULATE) ? 1 : 0, s);
+        c->launches += losses ? 5 : 2;
+        CK(cudaGetLastError());
+        return RGS_OK;
+    });
+}
+
+int rgs_entropy_loss(rgs_ctx* c, const double* opacities, int n, double* grad, double* loss) {
+    if (!opacities || n < 0) return RGS_E_INVALID;
+    return guarded(c, [&]() -> int {
+        if (n == 0) {
+            if (loss) CK(cudaMemsetAsync(loss, 0, sizeof(double), c->stream));
+            return RGS_OK;
+        }
+        TrainScratch& ts = train_scratch(c);
+        ts.parts.ensure(sizeof(double) * ((n + 255) / 256 + 16), c->stream);
+        rgs_launch::entropy(opacities, n, grad, ts.parts.as<double>(), loss, c->stream);
+        c->launches += loss ? 2 : 1;
+        CK(cudaGetLastError());
+        return RGS_OK;
+    });
+}
+
 int rgs_optimizer_create(rgs_ctx* c, const rgs_scene* scene, rgs_optimizer** out) {
     if (!scene || !out) return RGS_E_INVALID;
     return guarded(c, [&]() -> int {
@@ -1480,6 +1523,16 @@ int rgs_optimizer_upload(rgs_ctx* c, rgs_optimizer* o, const double* m65, const 
     });
 }
 
+int rgs_accumulate_stats(rgs_ctx* c, rgs_optimizer* o, const float* vnorm, const int32_t* visible) {
+    if (!o || !vnorm || !visible) return RGS_E_INVALID;
+    return guarded(c, [&]() -> int {
+        rgs_launch::accumulate_stats(vnorm, visible, o->n, o->accum, o->count, c->stream);
+        c->launches += o->n > 0 ? 1 : 0;
+        CK(cudaGetLastError());
+        return RGS_OK;
+    });
+}
+
 int rgs_optimizer_reset_stats(rgs_ctx* c, rgs_optimizer* o) {
     if (!o) return RGS_E_INVALID;
     return guarded(c, [&]() -> int {
@@ -1535,8 +1588,7 @@ int rgs_scene_scales(rgs_ctx* c, const rgs_scene* scene, double* out4) {
 int rgs_knn_build(rgs_ctx* c, const rgs_scene* scene, int k, const double* scales, int32_t* neighbors) {
     if (!scene || !neighbors || k <= 0) return RGS_E_INVALID;
     if (scene->n <= k) return set_err(c, RGS_E_INVALID, "knn: need more points than neighbors");
-    if (!(k == 1 || k == 2 || k == 4 || k == 8 || k == 16))
-        return set_err(c, RGS_E_INVALID, "knn: k must be 1, 2, 4, 8 or 16");
+    if (k > 16) return set_err(c, RGS_E_INVALID, "knn: k must be at most 16");
     return guarded(c, [&]() -> int {
         double sc[4];
         if (scales) {
@@ -1550,11 +1602,47 @@ int rgs_knn_build(rgs_ctx* c, const rgs_scene* scene, int k, const double* scale
         rgs_launch::knn_points(scene->params, scene->params64, scene->n, sc, ts.pts.as<double>(), c->stream);
         const size_t need = rgs_launch::knn_grid_scratch(scene->n);
         ts.knn.ensure(need, c->stream);
-        const int rc = rgs_launch::knn_grid(ts.pts.as<double>(), scene->n, k, neighbors, ts.knn.p, ts.knn.bytes,
-                                            c->stream);
+        const int rc = rgs_launch::knn_grid(ts.pts.as<double>(), scene->n, nullptr, nullptr, 0, k, neighbors,
+                                            ts.knn.p, ts.knn.bytes, c->stream);
         if (rc == -1) return set_err(c, RGS_E_INVALID, "knn: unsupported k");
         if (rc) return set_err(c, RGS_E_CUDA, "knn: grid build failed");
         c->launches += 9;
+        CK(cudaGetLastError());
+        return RGS_OK;
+    });
+}
+
+int rgs_knn_query(rgs_ctx* c, const double* points4, int n, const double* queries4, int nq, const int32_t* exclude,
+                  int k, int32_t* out) {
+    if (!points4 || !queries4 || !out || n < 0 || nq < 0 || k < 1) return RGS_E_INVALID;
+    if (k > 16) return set_err(c, RGS_E_INVALID, "knn: k must be at most 16");
+    return guarded(c, [&]() -> int {
+        if (nq == 0) return RGS_OK;
+        if (n == 0) {
+            CK(cudaMemsetAsync(out, 0xff, sizeof(int32_t) * (size_t)nq * k, c->stream));
+            return RGS_OK;
+        }
+        TrainScratch& ts = train_scratch(c);
+        ts.knn.ensure(rgs_launch::knn_grid_scratch(n), c->stream);
+        const int rc = rgs_launch::knn_grid(points4, n, queries4, exclude, nq, k, out, ts.knn.p, ts.knn.bytes,
+                                            c->stream);
+        if (rc) return set_err(c, RGS_E_CUDA, "knn: grid build failed");
+        c->launches += 5;
+        CK(cudaGetLastError());
+        return RGS_OK;
+    });
+}
+
+int rgs_consistency_loss(rgs_ctx* c, const double* speeds, int n, const int32_t* neighbors, int k, double* dspeed,
+                         double* losses) {
+    if (!speeds || !neighbors || k < 0 || n < 0) return RGS_E_INVALID;
+    return guarded(c, [&]() -> int {
+        if (n == 0) return RGS_OK;
+        TrainScratch& ts = train_scratch(c);
+        ts.parts.ensure(sizeof(double) * (rgs_launch::consistency_blocks(n) + 16), c->stream);
+        if (dspeed) CK(cudaMemsetAsync(dspeed, 0, sizeof(double) * 3 * (size_t)n, c->stream));
+        rgs_launch::consistency(speeds, neighbors, n, k, dspeed, ts.parts.as<double>(), losses, 0, c->stream);
+        c->launches += losses ? 2 : 1;
         CK(cudaGetLastError());
         return RGS_OK;
     });
@@ -1694,6 +1782,7 @@ int rgs_scene_save_checkpoint(rgs_ctx* c, const rgs_scene* scene, const char* pa
 // ===========================================================================
 // densify_and_prune (optim.cpp:168-234) and the train loop's generator.
 #include <random>
+#include <sstream>
 
 struct rgs_rng {
     std::mt19937_64 eng;  // train_from's rng (trainer.cpp:105)
@@ -1707,6 +1796,23 @@ int rgs_rng_create(unsigned long long seed, rgs_rng** out) {
     return RGS_OK;
 }
 void rgs_rng_destroy(rgs_rng* r) { delete r; }
+int rgs_rng_get_state(const rgs_rng* r, char* buf, size_t cap, size_t* len) {
+    if (!r) return RGS_E_INVALID;
+    std::ostringstream os;
+    os << r->eng;  // the engine's textual state (std::mt19937_64 operator<<)
+    const std::string st = os.str();
+    if (len) *len = st.size() + 1;
+    if (!buf) return RGS_OK;
+    if (cap < st.size() + 1) return RGS_E_INVALID;
+    std::memcpy(buf, st.c_str(), st.size() + 1);
+    return RGS_OK;
+}
+int rgs_rng_set_state(rgs_rng* r, const char* buf) {
+    if (!r || !buf) return RGS_E_INVALID;
+    std::istringstream is(buf);
+    is >> r->eng;
+    return is.fail() ? RGS_E_INVALID : RGS_OK;
+}
 int rgs_rng_uniform_int(rgs_rng* r, int lo, int hi, int* out) {
     if (!r || !out || hi < lo) return RGS_E_INVALID;
     std::uniform_int_distribution<int> d(lo, hi);  // trainer.cpp:106, 119

@@ -49,6 +49,11 @@ void adam_step(bool f64, void* params, void* m1, void* m2, const float* grads, c
                const int32_t* visible, double* accum, int32_t* count, int n, const AdamArgs& a,
                unsigned long long* err, double* part_entropy, double* losses_entropy, int accumulate, cudaStream_t s);
 int adam_blocks(int n);
+void image_loss_f64(const double* img, const double* tgt, int W, int H, const ImageGradArgs& a, double* dl,
+                    double* dfield, double* parts, double* losses, double loss_scale, int accumulate, cudaStream_t s);
+void entropy(const double* op, int n, double* grad, double* parts, double* loss, cudaStream_t s);
+void accumulate_stats(const float* vnorm, const int32_t* visible, int n, double* accum, int32_t* count,
+                      cudaStream_t s);
 void reset_opacity(bool f64, void* params, void* m1, void* m2, int n, double value, cudaStream_t s);
 void speeds(const float* params, const double* params64, int n, double* out, unsigned long long* err,
             cudaStream_t s);
@@ -60,7 +65,8 @@ void speed_backward(const float* params, const double* params64, int n, const do
 void knn_points(const float* params, const double* params64, int n, const double* scales, double* pts4,
                 cudaStream_t s);
 int knn(const double* pts4, int n, int k, int32_t* out, cudaStream_t s);
-int knn_grid(const double* pts4, int n, int k, int32_t* out, void* scratch, size_t scratch_bytes, cudaStream_t s);
+int knn_grid(const double* pts4, int n, const double* queries4, const int32_t* qexcl, int nq, int k, int32_t* out,
+             void* scratch, size_t scratch_bytes, cudaStream_t s);
 size_t knn_grid_scratch(int n);
 int extent_blocks(int n);
 void mean_extent(const float* params, const double* params64, int n, double* part_lo, double* part_hi,

@@ -155,6 +155,8 @@ EXPORTS = [
     "rgs_scene_scales", "rgs_knn_build", "rgs_consistency",
     "rgs_scene_load_checkpoint", "rgs_scene_save_checkpoint",
     "rgs_rng_create", "rgs_rng_destroy", "rgs_rng_uniform_int", "rgs_densify_and_prune",
+    "rgs_knn_query", "rgs_consistency_loss", "rgs_image_loss_f64", "rgs_entropy_loss", "rgs_accumulate_stats",
+    "rgs_rng_get_state", "rgs_rng_set_state",
 ]
 
 
@@ -223,6 +225,13 @@ def load_library(path: str = LIB_PATH):
         "rgs_rng_destroy": (None, [p]),
         "rgs_rng_uniform_int": (i, [p, i, i, p]),
         "rgs_densify_and_prune": (i, [p, p, p, p, d, p, p]),
+        "rgs_knn_query": (i, [p, p, i, p, i, p, i, p]),
+        "rgs_consistency_loss": (i, [p, p, i, p, i, p, p]),
+        "rgs_image_loss_f64": (i, [p, p, p, i, i, d, d, d, ctypes.c_uint, p, p]),
+        "rgs_entropy_loss": (i, [p, p, i, p, p]),
+        "rgs_accumulate_stats": (i, [p, p, p, p]),
+        "rgs_rng_get_state": (i, [p, p, ctypes.c_size_t, p]),
+        "rgs_rng_set_state": (i, [p, ctypes.c_char_p]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
