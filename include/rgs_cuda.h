@@ -219,6 +219,12 @@ int rgs_project_sliced(rgs_ctx* ctx, const double* sliced16, const rgs_camera* c
                        int sh_degree, double opacity_logit, rgs_splat* out, int* survived);
 
 /* ---------------------------------------------------------------- utilities */
+/* Device memory for FFI callers without the CUDA runtime (the C++ drop-ins use these):
+ * rgs_malloc returns NULL on failure; rgs_memcpy copies in any direction (cudaMemcpyDefault)
+ * on the context stream and synchronises. */
+void* rgs_malloc(rgs_ctx* ctx, size_t bytes);
+void rgs_free(rgs_ctx* ctx, void* ptr);
+int rgs_memcpy(rgs_ctx* ctx, void* dst, const void* src, size_t bytes);
 /* Camera::validate (camera.hpp:21-26) on the host; RGS_E_CAMERA with the
  * reference's message on failure. */
 int rgs_camera_validate(rgs_ctx* ctx, const rgs_camera* cam);
@@ -236,7 +242,8 @@ int rgs_camera_validate(rgs_ctx* ctx, const rgs_camera* cam);
  * reference's summation order, stored as float).  losses (may be NULL): [0] l1_loss,
  * [1] ssim_loss = 1 - mean SSIM, [2] MSE (psnr = min(100, 10 log10(1/MSE)), image.cpp:7-18),
  * each multiplied by loss_scale.  RGS_FLAG_ACCUMULATE adds into losses, RGS_FLAG_ACCUMULATE_GRAD
- * into dL_dimage. */
+ * into dL_dimage.  Images smaller than the 11x11 window have no SSIM: losses[1] is NaN and
+ * w_ssim must be 0 (else the reference's "ssim: image smaller than the 11x11 window"). */
 int rgs_image_loss(rgs_ctx* ctx, const float* rendered, const float* target, int width, int height,
                    double w_l1, double w_ssim, double loss_scale, unsigned flags, float* dL_dimage,
                    double* losses);
@@ -283,6 +290,8 @@ int rgs_optimizer_upload(rgs_ctx* ctx, rgs_optimizer* opt, const double* m65, co
                          const double* grad_accum, const int32_t* grad_count);
 /* accumulate_stats (optim.cpp:159-166) on its own: accum += vnorm, count += 1 where visible > 0. */
 int rgs_accumulate_stats(rgs_ctx* ctx, rgs_optimizer* opt, const float* vnorm, const int32_t* visible);
+/* As rgs_accumulate_stats with float64 view-space norms (the reference's StoreGrads). */
+int rgs_accumulate_stats_f64(rgs_ctx* ctx, rgs_optimizer* opt, const double* vnorm, const int32_t* visible);
 /* GaussianStore::reset_stats (gaussian.cpp:186-189). */
 int rgs_optimizer_reset_stats(rgs_ctx* ctx, rgs_optimizer* opt);
 /* reset_opacity (optim.cpp:236-243): opacity -> min(opacity, value), its moments zeroed. */

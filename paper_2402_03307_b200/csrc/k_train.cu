@@ -242,7 +242,8 @@ __global__ void __launch_bounds__(256) k_entropy(const double* __restrict__ op, 
 }
 
 // optim.cpp:159-166 standalone.
-__global__ void k_accumulate_stats(const float* __restrict__ vnorm, const int32_t* __restrict__ visible, int n,
+template <typename TV>
+__global__ void k_accumulate_stats(const TV* __restrict__ vnorm, const int32_t* __restrict__ visible, int n,
                                    double* __restrict__ accum, int32_t* __restrict__ count) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n || !(visible[i] > 0)) return;
@@ -944,8 +945,8 @@ void set_ssim_window(const double* k11, cudaStream_t s) {
 ImageLossGrid image_loss_grid(int W, int H) {
     ImageLossGrid g;
     const int vw = W - kSsimWin + 1, vh = H - kSsimWin + 1;
-    g.a_x = nblk(vw, kSsimTX);
-    g.a_y = nblk(vh, kSsimTY);
+    g.a_x = vw > 0 ? nblk(vw, kSsimTX) : 0;
+    g.a_y = vh > 0 ? nblk(vh, kSsimTY) : 0;
     g.b_x = nblk(W, kSsimTX);
     g.b_y = nblk(H, kSsimTY);
     g.n_a = 3 * g.a_x * g.a_y;
@@ -962,11 +963,17 @@ void image_loss_t(const TI* img, const TI* tgt, int W, int H, const ImageGradArg
     double* pa = parts;
     double* pl1 = parts + g.n_a;
     double* psq = pl1 + g.n_b;
-    k_ssim_fields<TI><<<dim3(g.a_x, g.a_y, 3), 256, 0, s>>>(img, tgt, W, H, dl != nullptr, dfield, pa);
-    k_image_grad<TI, TO><<<dim3(g.b_x, g.b_y, 3), 256, 0, s>>>(img, tgt, W, H, dfield, a, dl, pl1, psq);
+    // Images smaller than the window have no SSIM (the caller rejects w_ssim != 0 for them):
+    // stage A is skipped and the SSIM slot is NaN.
+    const bool has_ssim = W >= kSsimWin && H >= kSsimWin;
+    if (has_ssim) k_ssim_fields<TI><<<dim3(g.a_x, g.a_y, 3), 256, 0, s>>>(img, tgt, W, H, dl != nullptr, dfield, pa);
+    ImageGradArgs a2 = a;
+    if (!has_ssim) a2.w_ssim = 0;
+    k_image_grad<TI, TO><<<dim3(g.b_x, g.b_y, 3), 256, 0, s>>>(img, tgt, W, H, dfield, a2, dl, pl1, psq);
     if (losses) {
         k_finalize<<<1, 256, 0, s>>>(pl1, g.n_b, nvals, loss_scale, 0, accumulate, losses + 0);
-        k_finalize<<<1, 256, 0, s>>>(pa, g.n_a, count, loss_scale, 1, accumulate, losses + 1);
+        if (has_ssim) k_finalize<<<1, 256, 0, s>>>(pa, g.n_a, count, loss_scale, 1, accumulate, losses + 1);
+        else k_finalize<<<1, 256, 0, s>>>(pa, 0, 0.0, loss_scale, 0, 0, losses + 1);  // 0 / 0 = NaN
         k_finalize<<<1, 256, 0, s>>>(psq, g.n_b, nvals, loss_scale, 0, accumulate, losses + 2);
     }
 }
@@ -1004,7 +1011,11 @@ void entropy(const double* op, int n, double* grad, double* parts, double* loss,
 
 void accumulate_stats(const float* vnorm, const int32_t* visible, int n, double* accum, int32_t* count,
                       cudaStream_t s) {
-    if (n > 0) k_accumulate_stats<<<nblk(n, 256), 256, 0, s>>>(vnorm, visible, n, accum, count);
+    if (n > 0) k_accumulate_stats<float><<<nblk(n, 256), 256, 0, s>>>(vnorm, visible, n, accum, count);
+}
+void accumulate_stats_f64(const double* vnorm, const int32_t* visible, int n, double* accum, int32_t* count,
+                          cudaStream_t s) {
+    if (n > 0) k_accumulate_stats<double><<<nblk(n, 256), 256, 0, s>>>(vnorm, visible, n, accum, count);
 }
 
 void reset_opacity(bool f64, void* params, void* m1, void* m2, int n, double value, cudaStream_t s) {

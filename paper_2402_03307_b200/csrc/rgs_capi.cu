@@ -670,6 +670,30 @@ int rgs_ctx_synchronize(rgs_ctx* c) {
     });
 }
 
+void* rgs_malloc(rgs_ctx* c, size_t bytes) {
+    if (!c) return nullptr;
+    void* p = nullptr;
+    if (cudaSetDevice(c->device) != cudaSuccess || cudaMalloc(&p, std::max<size_t>(bytes, 1)) != cudaSuccess) {
+        set_err(c, RGS_E_CUDA, "rgs_malloc: out of device memory");
+        return nullptr;
+    }
+    return p;
+}
+void rgs_free(rgs_ctx* c, void* p) {
+    if (!c || !p) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    cudaFree(p);
+}
+int rgs_memcpy(rgs_ctx* c, void* dst, const void* src, size_t bytes) {
+    if (!dst || !src) return RGS_E_INVALID;
+    return guarded(c, [&]() -> int {
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        return RGS_OK;
+    });
+}
+
 int rgs_camera_validate(rgs_ctx* c, const rgs_camera* cam) {
     if (!cam) return RGS_E_INVALID;
     return validate_camera(c, cam);
@@ -1334,21 +1358,21 @@ extern "C" {
 int rgs_image_loss(rgs_ctx* c, const float* rendered, const float* target, int width, int height, double w_l1,
                    double w_ssim, double loss_scale, unsigned flags, float* dL_dimage, double* losses) {
     if (!rendered || !target || width <= 0 || height <= 0) return RGS_E_INVALID;
-    if (width < kSsimWin || height < kSsimWin)
+    if ((width < kSsimWin || height < kSsimWin) && w_ssim != 0)
         return set_err(c, RGS_E_INVALID, "ssim: image smaller than the 11x11 window");
     return guarded(c, [&]() -> int {
         cudaStream_t s = c->stream;
         ensure_ssim_window(c);
         TrainScratch& ts = train_scratch(c);
         const ImageLossGrid g = rgs_launch::image_loss_grid(width, height);
-        const size_t nv = (size_t)(width - kSsimWin + 1) * (height - kSsimWin + 1);
+        const size_t nv = (size_t)std::max(width - kSsimWin + 1, 0) * (size_t)std::max(height - kSsimWin + 1, 0);
         if (dL_dimage) ts.dfield.ensure(sizeof(double) * 9 * nv, s);
         ts.parts.ensure(sizeof(double) * (g.n_a + 2 * g.n_b + 16), s);
         ImageGradArgs a;
         a.w_l1 = w_l1;
         a.w_ssim = w_ssim;
         a.inv_n = 1 / (3.0 * (double)width * (double)height);
-        a.ssim_scale = -1 / (3.0 * (double)nv);
+        a.ssim_scale = nv ? -1 / (3.0 * (double)nv) : 0.0;
         a.accumulate = (flags & RGS_FLAG_ACCUMULATE_GRAD) ? 1 : 0;
         rgs_launch::image_loss(rendered, target, width, height, a, dL_dimage, ts.dfield.as<double>(),
                                ts.parts.as<double>(), losses, loss_scale, (flags & RGS_FLAG_ACCUMULATE) ? 1 : 0, s);
@@ -1361,21 +1385,21 @@ int rgs_image_loss(rgs_ctx* c, const float* rendered, const float* target, int w
 int rgs_image_loss_f64(rgs_ctx* c, const double* rendered, const double* target, int width, int height, double w_l1,
                        double w_ssim, double loss_scale, unsigned flags, double* dL_dimage, double* losses) {
     if (!rendered || !target || width <= 0 || height <= 0) return RGS_E_INVALID;
-    if (width < kSsimWin || height < kSsimWin)
+    if ((width < kSsimWin || height < kSsimWin) && w_ssim != 0)
         return set_err(c, RGS_E_INVALID, "ssim: image smaller than the 11x11 window");
     return guarded(c, [&]() -> int {
         cudaStream_t s = c->stream;
         ensure_ssim_window(c);
         TrainScratch& ts = train_scratch(c);
         const ImageLossGrid g = rgs_launch::image_loss_grid(width, height);
-        const size_t nv = (size_t)(width - kSsimWin + 1) * (height - kSsimWin + 1);
+        const size_t nv = (size_t)std::max(width - kSsimWin + 1, 0) * (size_t)std::max(height - kSsimWin + 1, 0);
         if (dL_dimage) ts.dfield.ensure(sizeof(double) * 9 * nv, s);
         ts.parts.ensure(sizeof(double) * (g.n_a + 2 * g.n_b + 16), s);
         ImageGradArgs a;
         a.w_l1 = w_l1;
         a.w_ssim = w_ssim;
         a.inv_n = 1 / (3.0 * (double)width * (double)height);
-        a.ssim_scale = -1 / (3.0 * (double)nv);
+        a.ssim_scale = nv ? -1 / (3.0 * (double)nv) : 0.0;
         a.accumulate = (flags & RGS_FLAG_ACCUMULATE_GRAD) ? 1 : 0;
         rgs_launch::image_loss_f64(rendered, target, width, height, a, dL_dimage, ts.dfield.as<double>(),
                                    ts.parts.as<double>(), losses, loss_scale, (flags & RGS_FLAG_ACCUMULATE) ? 1 : 0, s);
@@ -1527,6 +1551,16 @@ int rgs_accumulate_stats(rgs_ctx* c, rgs_optimizer* o, const float* vnorm, const
     if (!o || !vnorm || !visible) return RGS_E_INVALID;
     return guarded(c, [&]() -> int {
         rgs_launch::accumulate_stats(vnorm, visible, o->n, o->accum, o->count, c->stream);
+        c->launches += o->n > 0 ? 1 : 0;
+        CK(cudaGetLastError());
+        return RGS_OK;
+    });
+}
+
+int rgs_accumulate_stats_f64(rgs_ctx* c, rgs_optimizer* o, const double* vnorm, const int32_t* visible) {
+    if (!o || !vnorm || !visible) return RGS_E_INVALID;
+    return guarded(c, [&]() -> int {
+        rgs_launch::accumulate_stats_f64(vnorm, visible, o->n, o->accum, o->count, c->stream);
         c->launches += o->n > 0 ? 1 : 0;
         CK(cudaGetLastError());
         return RGS_OK;

@@ -54,6 +54,8 @@ void image_loss_f64(const double* img, const double* tgt, int W, int H, const Im
 void entropy(const double* op, int n, double* grad, double* parts, double* loss, cudaStream_t s);
 void accumulate_stats(const float* vnorm, const int32_t* visible, int n, double* accum, int32_t* count,
                       cudaStream_t s);
+void accumulate_stats_f64(const double* vnorm, const int32_t* visible, int n, double* accum, int32_t* count,
+                          cudaStream_t s);
 void reset_opacity(bool f64, void* params, void* m1, void* m2, int n, double value, cudaStream_t s);
 void speeds(const float* params, const double* params64, int n, double* out, unsigned long long* err,
             cudaStream_t s);

@@ -156,7 +156,8 @@ EXPORTS = [
     "rgs_scene_load_checkpoint", "rgs_scene_save_checkpoint",
     "rgs_rng_create", "rgs_rng_destroy", "rgs_rng_uniform_int", "rgs_densify_and_prune",
     "rgs_knn_query", "rgs_consistency_loss", "rgs_image_loss_f64", "rgs_entropy_loss", "rgs_accumulate_stats",
-    "rgs_rng_get_state", "rgs_rng_set_state",
+    "rgs_rng_get_state", "rgs_rng_set_state", "rgs_malloc", "rgs_free", "rgs_memcpy",
+    "rgs_accumulate_stats_f64",
 ]
 
 
@@ -230,8 +231,12 @@ def load_library(path: str = LIB_PATH):
         "rgs_image_loss_f64": (i, [p, p, p, i, i, d, d, d, ctypes.c_uint, p, p]),
         "rgs_entropy_loss": (i, [p, p, i, p, p]),
         "rgs_accumulate_stats": (i, [p, p, p, p]),
+        "rgs_accumulate_stats_f64": (i, [p, p, p, p]),
         "rgs_rng_get_state": (i, [p, p, ctypes.c_size_t, p]),
         "rgs_rng_set_state": (i, [p, ctypes.c_char_p]),
+        "rgs_malloc": (p, [p, ctypes.c_size_t]),
+        "rgs_free": (None, [p, p]),
+        "rgs_memcpy": (i, [p, p, p, ctypes.c_size_t]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

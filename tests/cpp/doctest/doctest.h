@@ -107,6 +107,27 @@ inline int run_all() {
         ::doctest::check(doctest_ok, "throws " #T ": " #expr, __FILE__, __LINE__); \
     } while (0)
 
+#define CHECK_THROWS(expr)                                                   \
+    do {                                                                     \
+        bool doctest_ok = false;                                             \
+        try {                                                                \
+            (void)(expr);                                                    \
+        } catch (...) {                                                      \
+            doctest_ok = true;                                               \
+        }                                                                    \
+        ::doctest::check(doctest_ok, "throws: " #expr, __FILE__, __LINE__);  \
+    } while (0)
+#define CHECK_NOTHROW(expr)                                                  \
+    do {                                                                     \
+        bool doctest_ok = true;                                              \
+        try {                                                                \
+            (void)(expr);                                                    \
+        } catch (...) {                                                      \
+            doctest_ok = false;                                              \
+        }                                                                    \
+        ::doctest::check(doctest_ok, "nothrow: " #expr, __FILE__, __LINE__); \
+    } while (0)
+
 #ifdef DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN
 int main() { return ::doctest::run_all(); }
 #endif

@@ -41,3 +41,18 @@ def test_reference_render_suite_fast_mode():
     r = _run(kat=False)
     passed = [l for l in r.stdout.splitlines() if l.startswith("[PASS]")]
     assert len(passed) >= 7, r.stdout[-4000:]
+
+
+TRAIN_BIN = os.path.join(ROOT, "tests", "cpp", "_build", "ref_test_train_gpu")
+
+
+def test_reference_loss_and_optim_suites():
+    """The reference's own tests/test_loss.cpp and tests/test_optim.cpp, unmodified, against
+    host/rgs_train_adapter.cpp: L1 / SSIM / entropy / consistency / KdTree4 / build_knn4d /
+    initialize_scene / adam_step / accumulate_stats / densify_and_prune / reset_opacity all run
+    on the device."""
+    if not os.path.exists(TRAIN_BIN):
+        pytest.fail(f"{TRAIN_BIN} not built (make -C tests/cpp where /root/reference exists)")
+    r = subprocess.run([TRAIN_BIN], capture_output=True, text=True, timeout=900)
+    print(r.stdout[-4000:])
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]

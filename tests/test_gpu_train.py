@@ -61,12 +61,22 @@ def test_image_loss_bit_exact(ctx, T, shape):
     assert abs(losses.cpu().numpy()[0] - 1.5 * l1) <= 1e-12 * l1
 
 
-def test_image_loss_rejects_small_images(ctx):
+def test_image_loss_small_images(ctx, T):
+    """Below the 11x11 window: SSIM is rejected (ssim.cpp:81-82), the L1 part still works."""
     import torch
 
-    a = torch.zeros((10, 40, 3), dtype=torch.float32, device="cuda")
-    with pytest.raises(rgs.RgsCudaError):
-        train.image_loss(ctx, a, a)
+    a = torch.rand((10, 40, 3), dtype=torch.float32, device="cuda")
+    b = torch.rand((10, 40, 3), dtype=torch.float32, device="cuda")
+    with pytest.raises(rgs.RgsCudaError, match="smaller than the 11x11 window"):
+        train.image_loss(ctx, a, b, 0.8, 0.2, torch.zeros_like(a))
+    dl = torch.zeros_like(a)
+    losses = torch.zeros(3, dtype=torch.float64, device="cuda")
+    train.image_loss(ctx, a, b, 1.0, 0.0, dl, losses)
+    torch.cuda.synchronize()
+    l1, g1 = T.l1_loss(a.cpu().numpy().astype(np.float64), b.cpu().numpy().astype(np.float64))
+    assert np.array_equal(dl.cpu().numpy(), g1.astype(np.float32))
+    L = losses.cpu().numpy()
+    assert abs(L[0] - l1) <= 1e-12 * l1 and np.isnan(L[1])
 
 
 def _store_and_grads(n, seed, static=False):
