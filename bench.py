@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="one warm sweep, no JSON (for ncu)")
     ap.add_argument("--no-train", action="store_true", help="skip the C3 training leg")
+    ap.add_argument("--no-c4", action="store_true", help="skip the C4 4K batch leg")
     ap.add_argument("--train-only", action="store_true", help="only the C3 training leg (profiling)")
     ap.add_argument("--train-steps", type=int, default=10)
     return ap.parse_args()
@@ -182,6 +183,55 @@ def run_reference(args, rank, world):
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- C4 batch leg
+C4_N, C4_W, C4_H, C4_SEED, C4_VIEWS = 2_000_000, 3840, 2160, 4, 64
+
+
+def run_c4_leg(args, ctx, dev, dist, rank, world, flush):
+    """Config C4: 2M Gaussians, 3840x2160, a 64-view camera x timestamp batch (8 orbit yaws x 8
+    times) sharded across the ranks ("strong" scaling: the batch is fixed as N grows)."""
+    import torch
+
+    from paper_2402_03307_b200 import rgs, scenes
+
+    store = scenes.synthetic_scene(C4_N, C4_W, C4_H, seed=C4_SEED)
+    cams_all = scenes.orbit_cameras(C4_W, C4_H, 8, 8)
+    lo, hi = rank * C4_VIEWS // world, (rank + 1) * C4_VIEWS // world
+    cams = cams_all[lo:hi]
+    scene = rgs.DeviceScene.from_store(ctx, store)
+    images = torch.empty((len(cams), C4_H, C4_W, 3), dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    ctx.render_views(scene, cams, (0.0, 0.0, 0.0), out=images)  # warm-up (also sizes the pair buffers)
+    steps = 2
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    total = 0.0
+    for _ in range(steps):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        ctx.render_views(scene, cams, (0.0, 0.0, 0.0), out=images)
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        total += a.elapsed_time(b)
+    ms = max_over_ranks(total, dist, dev)
+    _, rec = ctx.render_forward_device(scene, cams[len(cams) // 2], retain=False)
+    n_pairs, n_vis = rec.n_pairs, rec._n_splats
+    rec.close()
+    del images
+    scene.close()
+    torch.cuda.empty_cache()
+    return {"metric": "batch FPS at 3840x2160 (2M 4D Gaussians, 64-view batch)", "value": C4_VIEWS * steps / (ms / 1e3),
+            "unit": "frames/s", "scaling": "strong", "n_gpus": world, "views_per_rank": len(cams), "steps": steps,
+            "ms_per_batch": ms / steps,
+            "config": {"workload": "C4: 2M 4D rotor Gaussians, SH deg 3, 3840x2160, 64 views = 8 orbit yaws x 8 "
+                                   "timestamps, views sharded contiguously across ranks",
+                       "n_gaussians": C4_N, "width": C4_W, "height": C4_H, "n_pairs_mid_view": n_pairs,
+                       "n_visible_mid_view": n_vis, "l2": "256 MiB flush before each timed batch"}}
 
 
 # ----------------------------------------------------------------------------- training leg
@@ -472,9 +522,20 @@ def run_ours(args, rank, local_rank, world):
             ctx.render_views_host([p.numpy() for p in pinned], store.active_sh_degree, cams, (0, 0, 0),
                                   host_imgs.numpy())
         dt = max_over_ranks(time.perf_counter() - t0, dist, dev)
+        # raw PCIe D2H rate into the same pinned buffer (diagnostic for the e2e bound)
+        src = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        dst = host_imgs.view(-1).view(torch.uint8)[: 256 << 20]
+        torch.cuda.synchronize(dev)
+        t1 = time.perf_counter()
+        for _ in range(4):
+            dst.copy_(src, non_blocking=True)
+        torch.cuda.synchronize(dev)
+        d2h_gbs = 4 * (256 << 20) / (time.perf_counter() - t1) / 1e9
+        del src
         e2e = {"value": N_TIMES * reps * world / dt, "unit": "frames/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "steps": reps,
-               "note": "rgs_render_views_host: pinned host scene -> HBM, 300 renders, 300 images -> pinned host"}
+               "d2h_bytes_per_step": d2h, "steps": reps, "pcie_d2h_gbs_measured": d2h_gbs,
+               "note": "rgs_render_views_host: pinned host scene -> HBM, 300 renders, 300 images -> pinned host; "
+                       "bound by the D2H of 4.9 GB of float32 images per sweep"}
 
     # ---- CPU baseline (rank 0, N=1 only, bounded sample)
     cpu = None
@@ -488,10 +549,12 @@ def run_ours(args, rank, local_rank, world):
                "sample": f"{len(picks)} frames (t index {picks}) of the same sweep, full 1352x1014, "
                          f"{threads} threads, {cpu_model()}"}
 
-    train_res = None
+    train_res = c4_res = None
+    del images
+    torch.cuda.empty_cache()
+    if not args.no_c4:
+        c4_res = run_c4_leg(args, ctx, dev, dist, rank, world, flush)
     if not args.no_train:
-        del images
-        torch.cuda.empty_cache()
         train_res = run_train_leg(args, ctx, dev, dist, rank, world, flush)
 
     if rank == 0:
@@ -511,7 +574,7 @@ def run_ours(args, rank, local_rank, world):
             "stages_note": "per-stage CUDA events from a serialised profiling sweep after the timed region "
                            "(the timed sweeps pipeline 3 views over 3 streams, so stages overlap there)",
             "fp32_peak_tflops": fp32_peak, "clocks": clocks, "gpu_launches": launches,
-            "e2e": e2e, "cpu_baseline": cpu, "train": train_res,
+            "e2e": e2e, "cpu_baseline": cpu, "c4": c4_res, "train": train_res,
         }
         print(json.dumps(line), flush=True)
     if dist:

@@ -60,6 +60,17 @@ def test_c2_frame(ctx, orc):
               f" slow_pixels={rec.n_slow_pixels}")
 
 
+def test_c4_view(ctx, orc):
+    """Config C4 shape: 2M Gaussians at 3840x2160 (240x135 tiles), one orbit view of the
+    64-view batch: bit-exact tile lists, n_contrib identical, image <= 1e-4."""
+    store = scenes.synthetic_scene(2_000_000, 3840, 2160, seed=4)
+    cam = scenes.orbit_cameras(3840, 2160, 8, 8)[2 * 8 + 5]
+    err, ncd, rec, ref, out = _compare_forward(ctx, orc, store, cam, threads=32)
+    assert err <= 1e-4, err
+    assert ncd == 0
+    print(f"C4: splats={len(ref.splats)} pairs={len(ref.tile_ids)} max_err={err:.3e} slow_pixels={rec.n_slow_pixels}")
+
+
 def test_fp64_mode_matches_oracle_tightly(ctx, orc):
     store = scenes.random_scene(40, sh_degree=2, seed=11)
     cam = scenes.bench_camera(64, 48, 0.4)
