@@ -52,7 +52,10 @@ __device__ __forceinline__ void d_blend_record(const SplatArrays& out, int i, do
                                                double ab, double r, double g, double b, double s00, double s11) {
     const double pa = log(kMinAlpha / ab);  // natural-log alpha threshold (<= 0)
     const double kappa = fabs(cb) / sqrt(ca * cc);
-    double cs = (kappa < 0.999) ? 1.5e-6 * (1 + kappa) / (1 - kappa) : 1e30;
+    // FP32 p2 = fma(v, dy, fma(t, dx, u dy)) with rounded coefficients carries <= ~5 u
+    // (u = 2^-24) relative error on each of |ca2 dx^2|, |cc2 dy^2|, |cb2 dx dy| <= kappa |q| / 2,
+    // i.e. <= 3.0e-7 (1 + kappa / 2) |q|; 6e-7 (1 + kappa) / (1 - kappa) keeps a 2x margin.
+    double cs = (kappa < 0.999) ? 6e-7 * (1 + kappa) / (1 - kappa) : 1e30;
     if (!(ca > 0) || !(cc > 0)) cs = 1e30;
     const double L = fabs(pa) * 2;
     const double ex = sqrt(L * fmax(s00, 0.0)) * (1 + 1e-3) + 1e-2;

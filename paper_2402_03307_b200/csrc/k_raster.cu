@@ -150,8 +150,15 @@ __global__ void __launch_bounds__(256, 5) k_blend_fp32(SplatArrays sp, const uin
                 const float errN = fmaf(al * M, pr.y, errT + 3e-7f);
                 // ambiguous: a classify gate, the backward's clamp gate (unclamped alpha <= 0.99,
                 // rasterizer.cpp:356) or T(1 - alpha) < 1e-4 within their error bounds
-                const bool amb = gate_ambiguous(p, M, b.z) | ((__fadd_rn(p, M) >= pr.x) & (__fsub_rn(p, M) <= pr.x)) |
-                                 (fabsf(test_T - 1e-4f) <= test_T * errN);
+                const bool amb_g = gate_ambiguous(p, M, b.z);
+                const bool amb_c = (__fadd_rn(p, M) >= pr.x) & (__fsub_rn(p, M) <= pr.x);
+                const bool amb_t = fabsf(test_T - 1e-4f) <= test_T * errN;
+                const bool amb = amb_g | amb_c | amb_t;
+                if (COUNT && amb) {
+                    // slow-pixel reasons: power > 0 / alpha gate, clamp gate, transmittance gate
+                    const int r = amb_g ? ((p > -M) ? 3 : 4) : (amb_c ? 5 : 6);
+                    atomicAdd(counters + r, 1ull);
+                }
                 if (amb) {
                     slow = done = true;
                     continue;

@@ -209,6 +209,7 @@ struct rgs_ctx {
     cudaStream_t slot_stream[kSlots] = {};
     cudaEvent_t slot_done[kSlots] = {};
     cudaEvent_t join_ev = nullptr;
+    std::vector<void*> frame_pool;   // PooledFrame* of destroyed records
     BinState* view_stats = nullptr;  // pinned, one per view of the current batch
     size_t view_stats_cap = 0;
     void ensure_view_stats(size_t n) {
@@ -270,14 +271,45 @@ struct rgs_scene {
     double* params64 = nullptr;  // RGS_SCENE_F64 storage
 };
 
+// A retained view's device state, recycled through the context's pool (rgs_records_destroy
+// returns it with an event marking the end of its last use, the next user waits on it), so
+// a training loop that creates and destroys one record per view allocates nothing per view.
+struct PooledFrame {
+    Frame f;
+    cudaEvent_t free_ev = nullptr;
+};
+
 struct rgs_records {
     rgs_ctx* ctx = nullptr;
-    Frame fb;
+    PooledFrame* pf = nullptr;
+    Frame* fb = nullptr;
     int retained = 0;
     int n_slow = -1;
 };
 
 namespace {
+
+constexpr size_t kFramePoolMax = 8;
+
+PooledFrame* frame_get(rgs_ctx* c, cudaStream_t s) {
+    if (c->frame_pool.empty()) return new PooledFrame;
+    PooledFrame* pf = static_cast<PooledFrame*>(c->frame_pool.back());
+    c->frame_pool.pop_back();
+    if (pf->free_ev) cudaStreamWaitEvent(s, pf->free_ev, 0);  // its last user is done
+    return pf;
+}
+
+void frame_put(rgs_ctx* c, PooledFrame* pf) {
+    if (c->frame_pool.size() >= kFramePoolMax) {
+        pf->f.release(c->stream);
+        if (pf->free_ev) cudaEventDestroy(pf->free_ev);
+        delete pf;
+        return;
+    }
+    if (!pf->free_ev) cudaEventCreateWithFlags(&pf->free_ev, cudaEventDisableTiming);
+    cudaEventRecord(pf->free_ev, c->stream);
+    c->frame_pool.push_back(pf);
+}
 
 int set_err(rgs_ctx* ctx, int code, const std::string& msg) {
     if (ctx) ctx->err = msg;
@@ -364,10 +396,8 @@ int run_forward(rgs_ctx* ctx, Frame& f, cudaStream_t s, Source src, const rgs_sc
     for (int k = 0; k < 3; ++k) f.bg[k] = bg ? bg[k] : 0.0;
     f.ensure_gaussians(n, s);
     f.ensure_pixels(npix, ntiles, s);
-    if (src == kFromSplats) {
-        f.src.ensure(4 * (size_t)std::max(n, 1), s);
-        f.have_src = true;
-    }
+    f.have_src = src == kFromSplats;  // frames are recycled between scene and splat renders
+    if (f.have_src) f.src.ensure(4 * (size_t)std::max(n, 1), s);
     BinState init;
     std::memset(&init, 0, sizeof init);
     init.err = kNoError;
@@ -562,6 +592,13 @@ void rgs_ctx_destroy(rgs_ctx* c) {
     c->tmp_splats.release(c->stream);
     c->tmp_scan.release(c->stream);
     c->tmp_ids.release(c->stream);
+    for (void* v : c->frame_pool) {
+        PooledFrame* pf = static_cast<PooledFrame*>(v);
+        pf->f.release(c->stream);
+        if (pf->free_ev) cudaEventDestroy(pf->free_ev);
+        delete pf;
+    }
+    c->frame_pool.clear();
     for (int k = 0; k < rgs_ctx::kSlots; ++k) {
         if (!c->slot_stream[k]) continue;
         c->slot_frame[k].release(c->slot_stream[k]);
@@ -598,8 +635,8 @@ int rgs_ctx_set_profiling(rgs_ctx* c, int timing, int count_evals) {
         c->timing = timing != 0;
         c->count_evals = count_evals != 0;
         if (c->count_evals) {
-            c->counters.ensure(32, c->stream);
-            CK(cudaMemsetAsync(c->counters.p, 0, 32, c->stream));
+            c->counters.ensure(64, c->stream);
+            CK(cudaMemsetAsync(c->counters.p, 0, 64, c->stream));
         }
         return RGS_OK;
     });
@@ -641,7 +678,7 @@ int rgs_ctx_profile_reset(rgs_ctx* c) {
             c->stage_ms[k] = 0;
             c->stage_n[k] = 0;
         }
-        if (c->counters.p) CK(cudaMemsetAsync(c->counters.p, 0, 32, c->stream));
+        if (c->counters.p) CK(cudaMemsetAsync(c->counters.p, 0, 64, c->stream));
         return RGS_OK;
     });
 }
@@ -663,6 +700,17 @@ int rgs_ctx_profile_read(rgs_ctx* c, double* stage_ms, long long* stage_launches
         return RGS_OK;
     });
 }
+int rgs_ctx_profile_slow_reasons(rgs_ctx* c, unsigned long long* out4) {
+    if (!out4) return RGS_E_INVALID;
+    return guarded(c, [&]() -> int {
+        for (int k = 0; k < 4; ++k) out4[k] = 0;
+        if (!c->counters.p) return RGS_OK;
+        CK(cudaMemcpyAsync(out4, c->counters.as<unsigned long long>() + 3, 32, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        return RGS_OK;
+    });
+}
+
 int rgs_ctx_synchronize(rgs_ctx* c) {
     return guarded(c, [&] {
         CK(cudaStreamSynchronize(c->stream));
@@ -883,13 +931,15 @@ static int forward_common(rgs_ctx* c, Source src, const rgs_scene* scene, const 
             rec = new rgs_records;
             rec->ctx = c;
             rec->retained = (flags & RGS_FLAG_RETAIN_RECORDS) ? 1 : 0;
-            f = &rec->fb;
+            rec->pf = frame_get(c, c->stream);
+            rec->fb = &rec->pf->f;
+            f = rec->fb;
         }
         rc = run_forward(c, *f, c->stream, src, scene, dsp, n_splats, monotone, cam, bg, flags, dimg, flow, true,
                          nullptr);
         if (rc) {
             if (rec) {
-                rec->fb.release(c->stream);
+                frame_put(c, rec->pf);
                 delete rec;
             }
             return rc;
@@ -1059,7 +1109,7 @@ int rgs_render_views_host(rgs_ctx* c, int n, int sh_degree, const float* mean, c
 void rgs_records_destroy(rgs_records* r) {
     if (!r) return;
     cudaSetDevice(r->ctx->device);
-    r->fb.release(r->ctx->stream);
+    frame_put(r->ctx, r->pf);
     delete r;
 }
 
@@ -1068,17 +1118,17 @@ int rgs_records_info_get(const rgs_records* r, rgs_records_info* info) {
     rgs_ctx* c = r->ctx;
     return guarded(c, [&] {
         BinState st;
-        CK(cudaMemcpyAsync(c->host_stats, r->fb.dstats(), sizeof st, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(c->host_stats, r->fb->dstats(), sizeof st, cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
         st = *c->host_stats;
-        info->n_splats = r->fb.n_valid;
-        info->tiles_x = r->fb.tiles_x;
-        info->tiles_y = r->fb.tiles_y;
+        info->n_splats = r->fb->n_valid;
+        info->tiles_x = r->fb->tiles_x;
+        info->tiles_y = r->fb->tiles_y;
         info->retained = r->retained;
-        info->n_pairs = r->fb.n_pairs;
+        info->n_pairs = r->fb->n_pairs;
         info->n_slow_pixels = st.slow_count;
-        info->width = r->fb.width;
-        info->height = r->fb.height;
+        info->width = r->fb->width;
+        info->height = r->fb->height;
         return RGS_OK;
     });
 }
@@ -1087,7 +1137,7 @@ int rgs_records_export(rgs_ctx* c, const rgs_records* r, rgs_splat* splats, long
                        double* final_T, int32_t* n_contrib) {
     if (!r) return RGS_E_INVALID;
     return guarded(c, [&] {
-        const Frame& f = r->fb;
+        const Frame& f = *r->fb;
         cudaStream_t s = c->stream;
         const int n = f.n;
         const size_t npix = (size_t)f.width * f.height;
@@ -1176,7 +1226,7 @@ int rgs_render_backward(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* ca
         });
     }
     return guarded(c, [&]() -> int {
-        const Frame& f = r->fb;
+        const Frame& f = *r->fb;
         if (cam->width != f.width || cam->height != f.height || scene->n != f.n)
             return set_err(c, RGS_E_INVALID, "render_backward: camera/scene does not match the records");
         cudaStream_t s = c->stream;

@@ -157,7 +157,7 @@ EXPORTS = [
     "rgs_rng_create", "rgs_rng_destroy", "rgs_rng_uniform_int", "rgs_densify_and_prune",
     "rgs_knn_query", "rgs_consistency_loss", "rgs_image_loss_f64", "rgs_entropy_loss", "rgs_accumulate_stats",
     "rgs_rng_get_state", "rgs_rng_set_state", "rgs_malloc", "rgs_free", "rgs_memcpy",
-    "rgs_accumulate_stats_f64",
+    "rgs_accumulate_stats_f64", "rgs_ctx_profile_slow_reasons",
 ]
 
 
@@ -232,6 +232,7 @@ def load_library(path: str = LIB_PATH):
         "rgs_entropy_loss": (i, [p, p, i, p, p]),
         "rgs_accumulate_stats": (i, [p, p, p, p]),
         "rgs_accumulate_stats_f64": (i, [p, p, p, p]),
+        "rgs_ctx_profile_slow_reasons": (i, [p, p]),
         "rgs_rng_get_state": (i, [p, p, ctypes.c_size_t, p]),
         "rgs_rng_set_state": (i, [p, ctypes.c_char_p]),
         "rgs_malloc": (p, [p, ctypes.c_size_t]),
@@ -462,6 +463,12 @@ class Context:
     # --- profiling (CUDA events per pipeline stage, on the launching stream)
     def set_profiling(self, timing: bool = True, count_evals: bool = False):
         self.check(self.L.rgs_ctx_set_profiling(self.h, int(timing), int(count_evals)))
+
+    def slow_reasons(self):
+        """{reason: count} of the FP32 blend's slow-pixel decisions (count_evals profiling)."""
+        out = (ctypes.c_ulonglong * 4)()
+        self.check(self.L.rgs_ctx_profile_slow_reasons(self.h, out))
+        return dict(zip(("power_gate", "alpha_gate", "clamp_gate", "T_gate"), [int(x) for x in out]))
 
     def measure_fp32_tflops(self) -> float:
         v = ctypes.c_double(0)

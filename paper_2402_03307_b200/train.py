@@ -332,6 +332,8 @@ class Trainer:
         self.nbrs = None
         self._img = None
         self._dl = None
+        self._streams = None
+        self.overlap = True  # forward of view v+1 alongside the backward of view v
         self._alloc()
 
     def _alloc(self):
@@ -358,19 +360,25 @@ class Trainer:
         else:
             self.nbrs = None
 
-    def _buffers(self, cam: Camera):
+    def _buffers(self, cam: Camera, slot: int = 0):
         import torch
 
         shape = (cam.height, cam.width, 3)
-        if self._img is None or tuple(self._img.shape) != shape:
+        if self._img is None or tuple(self._img[0].shape) != shape:
             dev = f"cuda:{self.ctx.device}"
-            self._img = torch.empty(shape, dtype=torch.float32, device=dev)
-            self._dl = torch.empty(shape, dtype=torch.float32, device=dev)
-        return self._img, self._dl
+            self._img = [torch.empty(shape, dtype=torch.float32, device=dev) for _ in range(2)]
+            self._dl = [torch.empty(shape, dtype=torch.float32, device=dev) for _ in range(2)]
+        return self._img[slot], self._dl[slot]
 
     def evaluate_loss(self, cams: Sequence[Camera], targets, want_grads: bool = True):
         """trainer.cpp:22-84 for this rank's views (device tensors); leaves the batch-reduced
-        gradients in self.grads / vnorm / visible and the losses in self.losses (device)."""
+        gradients in self.grads / vnorm / visible and the losses in self.losses (device).
+
+        With ``overlap`` (default) the forward of view v+1 runs on a side stream while the loss
+        and backward of view v run on the main stream; the backward passes stay in view order
+        on the main stream (they accumulate into one gradient buffer)."""
+        import torch
+
         w = self.cfg.loss
         ctx, scene = self.ctx, self.scene
         ctx.fence()
@@ -379,20 +387,42 @@ class Trainer:
         self.losses.zero_()
         inv_b = 1.0 / (len(cams) * self.world) if cams else 0.0
         wl1, wss = (1 - w.lambda_ssim) * inv_b, w.lambda_ssim * inv_b
-        for cam, tgt in zip(cams, targets):
-            img, dl = self._buffers(cam)
-            img, rec = ctx.render_forward_device(scene, cam, self.cfg.background, retain=want_grads, image=img)
+        overlap = self.overlap and ctx._torch_stream and len(cams) > 1
+        main = torch.cuda.current_stream(ctx.device)
+        if overlap and self._streams is None:
+            self._streams = [torch.cuda.Stream(ctx.device), torch.cuda.Stream(ctx.device)]
+        # per buffer slot: event after its last use on the main stream; initially the end of the
+        # previous step (its Adam update of the scene) and of the buffer zeroing above
+        start = main.record_event() if overlap else None
+        free = [start, start]
+        recs = []
+        for v, (cam, tgt) in enumerate(zip(cams, targets)):
+            slot = v % 2 if overlap else 0
+            img, dl = self._buffers(cam, slot)
+            if overlap:
+                side = self._streams[slot]
+                if free[slot] is not None:
+                    side.wait_event(free[slot])
+                with torch.cuda.stream(side):
+                    img, rec = ctx.render_forward_device(scene, cam, self.cfg.background, retain=want_grads,
+                                                         image=img)
+                main.wait_stream(side)
+                ctx.sync_stream()
+            else:
+                img, rec = ctx.render_forward_device(scene, cam, self.cfg.background, retain=want_grads, image=img)
             image_loss(ctx, img, tgt, wl1, wss, dl if want_grads else None, self.losses, loss_scale=inv_b,
                        accumulate=True)
             if want_grads:
                 ctx.render_backward_device(scene, cam, rec, dl, self.grads, self.vnorm, self.visible, accumulate=True)
+            if overlap:
+                free[slot] = main.record_event()
+            recs.append(rec)
+        for rec in recs:  # returned to the context's frame pool (stream-ordered, no host sync)
             rec.close()
         if self.world > 1:
             ctx.fence()
             allreduce_step_buffers(self.gbuf, self.visible, self.losses[:3], self.dist)
             if not ctx._torch_stream:
-                import torch
-
                 torch.cuda.current_stream(ctx.device).synchronize()
         if w.lambda_consistency != 0 and self.nbrs is not None and scene.n > 0:
             consistency(ctx, scene, self.nbrs, w.lambda_consistency, self.grads if want_grads else None,
