@@ -255,7 +255,12 @@ __global__ void __launch_bounds__(256) k_blend_fp64(SplatArrays sp, const uint32
                     }
                 }
             }
+            // The transmittance walk (the only sequential part) is replayed by every lane with
+            // one shuffle per accepted entry; each lane keeps the T in front of its own entry
+            // and adds its colour contribution itself (summed over the warp at the end).
             unsigned mask = __ballot_sync(0xffffffffu, accept);
+            double myT = 0;
+            int stop_lane = 32;
             while (mask) {
                 const int l = __ffs(mask) - 1;
                 mask &= mask - 1;
@@ -263,15 +268,25 @@ __global__ void __launch_bounds__(256) k_blend_fp64(SplatArrays sp, const uint32
                 const double test_T = T * (1 - al);
                 if (test_T < kStopT) {
                     done = true;
+                    stop_lane = l;
                     break;
                 }
-                const double wgt = al * T;
-                acc0 = acc0 + __shfl_sync(0xffffffffu, c0, l) * wgt;
-                acc1 = acc1 + __shfl_sync(0xffffffffu, c1, l) * wgt;
-                acc2 = acc2 + __shfl_sync(0xffffffffu, c2, l) * wgt;
+                if (lane == l) myT = T;
                 T = test_T;
                 contrib = (int)(base + l - rg.x) + 1;
             }
+            if (accept && lane < stop_lane) {
+                const double wgt = a * myT;
+                acc0 = acc0 + c0 * wgt;
+                acc1 = acc1 + c1 * wgt;
+                acc2 = acc2 + c2 * wgt;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            acc0 += __shfl_xor_sync(0xffffffffu, acc0, o);
+            acc1 += __shfl_xor_sync(0xffffffffu, acc1, o);
+            acc2 += __shfl_xor_sync(0xffffffffu, acc2, o);
         }
         if (lane == 0) {
             acc0 = acc0 + T * bg.x;
