@@ -11,9 +11,10 @@
 //      ranks gives each splat its pair offset; warps emit the (tile, splat) pairs of 32
 //      consecutive ranks cooperatively (coalesced stores).
 //   3. LSD radix sort of the pairs on the packed key (ty << 8 | tx), as two stable 8-bit
-//      digit passes (tx, then ty).  Each pass: per-block digit histogram, exclusive scan
-//      of the [digit][block] counts, and a scatter that ranks each block's elements with
-//      warp __match_any_sync peer groups, sorts them by digit in shared memory and writes
+//      digit passes (tx, then ty), one kernel each: the global digit histograms come from
+//      the duplicate kernel (per splat rectangle, not per pair), a block's offset inside each
+//      digit from a decoupled look-back; the block ranks its elements with warp
+//      __match_any_sync peer groups, sorts them by digit in shared memory and writes
 //      contiguous per-digit runs.
 //
 // Stable passes over pairs emitted in rank order leave every tile's list in
@@ -70,6 +71,13 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* t
     if (total) *total = warp_sums[(blockDim.x >> 5) - 1];
     __syncthreads();
     return before;
+}
+
+// Inclusive prefix sum over the block of one int per thread (a difference array -> values).
+__device__ __forceinline__ int block_inclusive_diff(int v) {
+    uint32_t total;
+    const uint32_t ex = block_exclusive_scan((uint32_t)v, &total);
+    return (int)(ex + (uint32_t)v);
 }
 
 // `n_dev` (optional) overrides n with a device-side count.
@@ -252,25 +260,9 @@ __global__ void __launch_bounds__(512) k_bucket_sort_big(const uint32_t* __restr
 }
 
 // --------------------------------------------------------------------------- duplicate
-// Warp-cooperative: the pairs of 32 consecutive ranks are written as one contiguous
-// run (lane l writes pair l, l+32, ...).  key = tile id, value = splat id.
-__global__ void __launch_bounds__(256) k_duplicate(const uint32_t* __restrict__ sorted_ids,
-                                                   const uint32_t* __restrict__ pair_off,
-                                                   const uint32_t* __restrict__ sorted_tiles,
-                                                   const ushort4* __restrict__ rect, const BinState* __restrict__ st,
-                                                   int tiles_x, uint32_t* keys, uint32_t* vals) {
-    const int lane = threadIdx.x & 31;
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    const int nv = st->n_valid;
-    if (st->overflow || r - lane >= nv) return;  // buffers too small / whole warp past the end
-    uint32_t id = 0, cnt = 0, off = 0;
-    ushort4 q = make_ushort4(0, 0, 0, 0);
-    if (r < nv) {
-        id = sorted_ids[r];
-        cnt = sorted_tiles[r];
-        off = pair_off[r];
-        if (cnt) q = rect[id];
-    }
+// Pair emission of one warp (32 consecutive ranks) for k_duplicate.
+__device__ __forceinline__ void emit_pairs(uint32_t id, uint32_t cnt, uint32_t off, ushort4 q, int lane,
+                                                uint32_t* keys, uint32_t* vals) {
     // inclusive prefix of counts within the warp
     uint32_t incl = cnt;
 #pragma unroll
@@ -306,6 +298,46 @@ __global__ void __launch_bounds__(256) k_duplicate(const uint32_t* __restrict__ 
     }
 }
 
+// Warp-cooperative: the pairs of 32 consecutive ranks are written as one contiguous
+// run (lane l writes pair l, l+32, ...).  key = tile id, value = splat id.
+// It also builds the two radix passes' global digit histograms per splat, not per pair: a
+// rectangle [x0, x1] x [y0, y1] adds its height to tx digits x0..x1 and its width to ty digits
+// y0..y1 -- difference arrays in shared memory, flushed with 2 x 257 global atomics per block.
+__global__ void __launch_bounds__(256) k_duplicate(const uint32_t* __restrict__ sorted_ids,
+                                                   const uint32_t* __restrict__ pair_off,
+                                                   const uint32_t* __restrict__ sorted_tiles,
+                                                   const ushort4* __restrict__ rect, const BinState* __restrict__ st,
+                                                   int tiles_x, uint32_t* keys, uint32_t* vals, int* hist_diff) {
+    __shared__ int sdx[257], sdy[257];
+    for (int e = threadIdx.x; e < 257; e += blockDim.x) sdx[e] = sdy[e] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nv = st->n_valid;
+    const bool warp_live = !st->overflow && r - lane < nv;  // buffers large enough, warp not past the end
+    uint32_t id = 0, cnt = 0, off = 0;
+    ushort4 q = make_ushort4(0, 0, 0, 0);
+    if (warp_live && r < nv) {
+        id = sorted_ids[r];
+        cnt = sorted_tiles[r];
+        off = pair_off[r];
+        if (cnt) {
+            q = rect[id];
+            const int h = q.w - q.z + 1, wd = q.y - q.x + 1;
+            atomicAdd(&sdx[q.x], h);
+            atomicAdd(&sdx[q.y + 1], -h);
+            atomicAdd(&sdy[q.z], wd);
+            atomicAdd(&sdy[q.w + 1], -wd);
+        }
+    }
+    if (warp_live) emit_pairs(id, cnt, off, q, lane, keys, vals);
+    __syncthreads();
+    for (int e = threadIdx.x; e < 257; e += blockDim.x) {
+        if (sdx[e]) atomicAdd(&hist_diff[e], sdx[e]);
+        if (sdy[e]) atomicAdd(&hist_diff[257 + e], sdy[e]);
+    }
+}
+
 // --------------------------------------------------------------------------- LSD digit pass
 // Stable counting-sort pass on one byte of the packed key (ty << 8 | tx): tx for pass 0,
 // ty for pass 1.  A block sorts a tile of kBlockTile consecutive elements locally:
@@ -321,46 +353,33 @@ constexpr int kRadixRounds = 8;
 constexpr int kBlockTile = kRadixThreads * kRadixRounds;  // 2048
 constexpr int kRadixDigits = 256;
 
-// counts layout: [digit][block], so one exclusive scan yields every (digit, block) offset.
-__global__ void __launch_bounds__(kRadixThreads) k_radix_hist(const uint32_t* __restrict__ keys,
-                                                              const BinState* __restrict__ st, int shift, int n_blocks,
-                                                              uint32_t* counts) {
-    __shared__ uint32_t h[kRadixDigits];
-    h[threadIdx.x] = 0;
-    __syncthreads();
-    const uint32_t n = st->n_pairs_eff;
-    const uint32_t base = (uint32_t)blockIdx.x * kBlockTile;
-    uint32_t d[kRadixRounds];
-#pragma unroll
-    for (int j = 0; j < kRadixRounds; ++j) {
-        const uint32_t e = base + j * kRadixThreads + threadIdx.x;
-        d[j] = e < n ? (keys[e] >> shift) & 0xffu : 0xffffffffu;
-    }
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int j = 0; j < kRadixRounds; ++j) {
-        const unsigned peers = __match_any_sync(0xffffffffu, d[j]);
-        if (d[j] != 0xffffffffu && (peers & ((1u << lane) - 1u)) == 0) atomicAdd(&h[d[j]], __popc(peers));
-    }
-    __syncthreads();
-    counts[(size_t)threadIdx.x * n_blocks + blockIdx.x] = h[threadIdx.x];
-}
+// One-sweep digit pass: the global digit
+// starts come from the histograms k_duplicate built, and each block's offset inside a digit
+// from a decoupled look-back over its predecessors' published per-digit counts.  Blocks take
+// their tile index from an atomic ticket, so every predecessor has started (and publishes its
+// aggregate before looking back itself): the spin-wait always terminates.
+constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kCountMask = (1u << 30) - 1u;
 
-__global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(const uint32_t* __restrict__ keys_in,
-                                                                 const uint32_t* __restrict__ vals_in,
-                                                                 const BinState* __restrict__ st, int shift,
-                                                                 int n_blocks, const uint32_t* __restrict__ offsets,
-                                                                 uint32_t* keys_out, uint32_t* vals_out) {
-    __shared__ uint32_t wcnt[kRadixWarps][kRadixDigits];  // per-warp counts -> per-warp starts
-    __shared__ uint32_t dstart[kRadixDigits];             // digit start inside the sorted tile
-    __shared__ uint32_t gbase[kRadixDigits];              // global offset of (digit, block)
+__global__ void __launch_bounds__(kRadixThreads) k_radix_onesweep(const uint32_t* __restrict__ keys_in,
+                                                                  const uint32_t* __restrict__ vals_in,
+                                                                  const BinState* __restrict__ st, int shift,
+                                                                  const int* __restrict__ hist_diff,
+                                                                  uint32_t* status, uint32_t* ticket,
+                                                                  uint32_t* keys_out, uint32_t* vals_out) {
+    __shared__ uint32_t wcnt[kRadixWarps][kRadixDigits];
+    __shared__ uint32_t dstart[kRadixDigits];
+    __shared__ uint32_t gbase[kRadixDigits];
     __shared__ uint32_t skey[kBlockTile], sval[kBlockTile];
+    __shared__ uint32_t s_bid;
+    if (threadIdx.x == 0) s_bid = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const uint32_t bid = s_bid;
+    const uint32_t n = st->n_pairs_eff;
+    if (bid * (uint32_t)kBlockTile >= n) return;  // past the end (all later tickets too)
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
     for (int k = 0; k < kRadixWarps; ++k) wcnt[k][threadIdx.x] = 0;
-    gbase[threadIdx.x] = offsets[(size_t)threadIdx.x * n_blocks + blockIdx.x];
-    const uint32_t n = st->n_pairs_eff;
-    const uint32_t base = (uint32_t)blockIdx.x * kBlockTile + w * (kBlockTile / kRadixWarps);
+    const uint32_t base = bid * kBlockTile + w * (kBlockTile / kRadixWarps);
     uint32_t key[kRadixRounds], val[kRadixRounds], rk[kRadixRounds];
 #pragma unroll
     for (int j = 0; j < kRadixRounds; ++j) {
@@ -369,7 +388,6 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(const uint32_t*
         val[j] = e < n ? vals_in[e] : 0u;
     }
     __syncthreads();
-    // warp-local ranks (element order within the warp's 256 elements)
 #pragma unroll
     for (int j = 0; j < kRadixRounds; ++j) {
         const uint32_t d = key[j] != 0xffffffffu ? (key[j] >> shift) & 0xffu : 0xffffffffu;
@@ -383,24 +401,45 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(const uint32_t*
         rk[j] = r;
     }
     __syncthreads();
-    // per digit: prefix over warps, and the digit's start in the sorted tile
-    {
-        const int dd = threadIdx.x;
-        uint32_t tot = 0;
+    const int dd = threadIdx.x;
+    uint32_t tot = 0;
 #pragma unroll
-        for (int k = 0; k < kRadixWarps; ++k) {
-            const uint32_t c = wcnt[k][dd];
-            wcnt[k][dd] = tot;
-            tot += c;
+    for (int k = 0; k < kRadixWarps; ++k) {
+        const uint32_t c = wcnt[k][dd];
+        wcnt[k][dd] = tot;
+        tot += c;
+    }
+    // publish this block's count of digit dd, then look back for its exclusive prefix
+    volatile uint32_t* vs = status;
+    if (bid == 0) {
+        vs[dd] = kFlagInc | tot;
+    } else {
+        vs[(size_t)bid * kRadixDigits + dd] = kFlagAgg | tot;
+        uint32_t excl = 0;
+        for (int64_t p = (int64_t)bid - 1; p >= 0;) {
+            const uint32_t v = vs[(size_t)p * kRadixDigits + dd];
+            if (!(v & (kFlagAgg | kFlagInc))) continue;  // predecessor not published yet
+            excl += v & kCountMask;
+            if (v & kFlagInc) break;
+            --p;
         }
-        dstart[dd] = tot;  // digit total for now; scanned below
+        vs[(size_t)bid * kRadixDigits + dd] = kFlagInc | (excl + tot);
+        dstart[dd] = excl;  // temporarily: exclusive offset of this block inside the digit
+    }
+    if (bid == 0) dstart[dd] = 0;
+    // global digit start: exclusive prefix over digits of the histogram (difference array)
+    {
+        uint32_t t2;
+        const uint32_t h = (uint32_t)block_inclusive_diff(hist_diff[dd]);
+        const uint32_t ex = block_exclusive_scan(h, &t2);
+        gbase[dd] = ex + dstart[dd];
     }
     __syncthreads();
     {
         uint32_t total;
-        const uint32_t ex = block_exclusive_scan(dstart[threadIdx.x], &total);
+        const uint32_t ex = block_exclusive_scan(tot, &total);
         __syncthreads();
-        dstart[threadIdx.x] = ex;
+        dstart[dd] = ex;
     }
     __syncthreads();
 #pragma unroll
@@ -412,9 +451,7 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(const uint32_t*
         sval[p] = val[j];
     }
     __syncthreads();
-    const uint32_t valid_in_tile = n > (uint32_t)blockIdx.x * kBlockTile
-                                       ? min((uint32_t)kBlockTile, n - (uint32_t)blockIdx.x * kBlockTile)
-                                       : 0u;
+    const uint32_t valid_in_tile = min((uint32_t)kBlockTile, n - bid * (uint32_t)kBlockTile);
     for (uint32_t i = threadIdx.x; i < valid_in_tile; i += kRadixThreads) {
         const uint32_t k = skey[i];
         const uint32_t d = (k >> shift) & 0xffu;
@@ -482,36 +519,32 @@ void depth_ranks(const uint8_t* valid, const unsigned long long* key, const uint
 
 void duplicate(const uint32_t* sorted_ids, const uint32_t* pair_off, const uint32_t* sorted_tiles,
                const ushort4* rect, const BinState* st, int n, int tiles_x, uint32_t* keys, uint32_t* vals,
-               cudaStream_t s) {
+               int* aux, cudaStream_t s) {
+    cudaMemsetAsync(aux, 0, sizeof(int) * 528, s);
     if (n > 0)
         k_duplicate<<<blocks(n, 256), 256, 0, s>>>(sorted_ids, pair_off, sorted_tiles, rect, st, tiles_x, keys,
-                                                    vals);
+                                                    vals, aux);
 }
 
 int radix_blocks(long long n_pairs) { return std::max(blocks(n_pairs, kBlockTile), 1); }
 size_t radix_count_entries(long long n_pairs) { return (size_t)kRadixDigits * radix_blocks(n_pairs); }
 
 // Two stable byte passes (tx, then ty); the sorted pairs end back in (keys_a, vals_a).
-// counts/offsets: radix_count_entries() u32 each; scratch for the scan: entries/1024 + 1 u32.
+// aux: [0, 514) the digit-histogram difference arrays k_duplicate filled, [520, 522) tickets;
+// status_a / status_b: radix_count_entries() u32 each (decoupled look-back state).
 void tile_radix_sort(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32_t* vals_b, const BinState* st,
-                     long long n_pairs, int tiles_x, int n_tiles, uint32_t* counts, uint32_t* offsets,
-                     uint32_t* scratch, uint2* ranges, cudaStream_t s) {
+                     long long n_pairs, int tiles_x, int n_tiles, uint32_t* status_a, uint32_t* status_b,
+                     int* aux, uint2* ranges, cudaStream_t s) {
     const int nb = radix_blocks(n_pairs);
-    const int entries = kRadixDigits * nb;
-    uint32_t* kin = keys_a;
-    uint32_t* vin = vals_a;
-    uint32_t* kout = keys_b;
-    uint32_t* vout = vals_b;
-    for (int pass = 0; pass < 2; ++pass) {
-        const int shift = pass == 0 ? 0 : 8;
-        k_radix_hist<<<nb, kRadixThreads, 0, s>>>(kin, st, shift, nb, counts);
-        exclusive_scan(counts, entries, offsets, scratch, nullptr, s, nullptr);
-        k_radix_scatter<<<nb, kRadixThreads, 0, s>>>(kin, vin, st, shift, nb, offsets, kout, vout);
-        std::swap(kin, kout);
-        std::swap(vin, vout);
-    }
+    const size_t entries = (size_t)kRadixDigits * nb;
+    cudaMemsetAsync(status_a, 0, 4 * entries, s);
+    cudaMemsetAsync(status_b, 0, 4 * entries, s);
+    uint32_t* tickets = reinterpret_cast<uint32_t*>(aux + 520);
+    k_radix_onesweep<<<nb, kRadixThreads, 0, s>>>(keys_a, vals_a, st, 0, aux, status_a, tickets, keys_b, vals_b);
+    k_radix_onesweep<<<nb, kRadixThreads, 0, s>>>(keys_b, vals_b, st, 8, aux + 257, status_b, tickets + 1, keys_a,
+                                                   vals_a);
     cudaMemsetAsync(ranges, 0, sizeof(uint2) * (size_t)n_tiles, s);
-    k_tile_ranges<<<std::max(blocks(n_pairs, 256), 1), 256, 0, s>>>(kin, st, tiles_x, ranges);
+    k_tile_ranges<<<std::max(blocks(n_pairs, 256), 1), 256, 0, s>>>(keys_a, st, tiles_x, ranges);
 }
 
 void check_capacity(BinState* st, cudaStream_t s) { k_check_capacity<<<1, 1, 0, s>>>(st); }

@@ -457,9 +457,10 @@ int run_forward(rgs_ctx* ctx, Frame& f, cudaStream_t s, Source src, const rgs_sc
     // Duplicate-with-key in rank order, then the two stable tile-digit passes.
     {
         StageTimer t(ctx, kStTileFill, s);
+        // scan_tmp is free again after the pair-offset scan: it holds the digit histograms
         rgs_launch::duplicate(f.sorted_ids.as<uint32_t>(), f.pair_off.as<uint32_t>(), f.sorted_tiles.as<uint32_t>(),
                               sa.rect, st_dev, n, dc.tiles_x, f.keys_a.as<uint32_t>(), f.pair_vals_buf.as<uint32_t>(),
-                              s);
+                              f.scan_tmp.as<int>(), s);
         ctx->launches += 1;
     }
     {
@@ -467,8 +468,8 @@ int run_forward(rgs_ctx* ctx, Frame& f, cudaStream_t s, Source src, const rgs_sc
         rgs_launch::tile_radix_sort(f.keys_a.as<uint32_t>(), f.pair_vals_buf.as<uint32_t>(), f.keys_b.as<uint32_t>(),
                                     f.vals_b.as<uint32_t>(), st_dev, f.pair_cap, dc.tiles_x, ntiles,
                                     f.radix_counts.as<uint32_t>(), f.radix_offsets.as<uint32_t>(),
-                                    f.scan_tmp.as<uint32_t>(), f.ranges.as<uint2>(), s);
-        ctx->launches += 11;
+                                    f.scan_tmp.as<int>(), f.ranges.as<uint2>(), s);
+        ctx->launches += 3;
     }
 
     // Blend.

@@ -132,13 +132,13 @@ void depth_ranks(const uint8_t* valid, const unsigned long long* key, const uint
                  uint32_t* sorted_tiles, uint32_t* big_list, void* big_scratch, cudaStream_t s);
 void duplicate(const uint32_t* sorted_ids, const uint32_t* pair_off, const uint32_t* sorted_tiles,
                const ushort4* rect, const BinState* st, int n, int tiles_x, uint32_t* keys, uint32_t* vals,
-               cudaStream_t s);
+               int* aux, cudaStream_t s);
 void check_capacity(BinState* st, cudaStream_t s);
 int radix_blocks(long long n_pairs);
 size_t radix_count_entries(long long n_pairs);
 void tile_radix_sort(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32_t* vals_b, const BinState* st,
-                     long long n_pairs, int tiles_x, int n_tiles, uint32_t* counts, uint32_t* offsets,
-                     uint32_t* scratch, uint2* ranges, cudaStream_t s);
+                     long long n_pairs, int tiles_x, int n_tiles, uint32_t* status_a, uint32_t* status_b,
+                     int* aux, uint2* ranges, cudaStream_t s);
 void blend_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges, const DevCamera& cam,
                 float3 bg, int flow_mode, float* image, double* final_T, uint32_t* n_contrib,
                 uint32_t* slow_list, int* slow_count, unsigned long long* counters, cudaStream_t s);
