@@ -73,6 +73,65 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* t
     return before;
 }
 
+
+// Single-pass exclusive scan (decoupled look-back): one kernel instead of sums / scan of sums /
+// apply.  Status words: bit 63 inclusive, bit 62 aggregate, low 32 bits the value.  Tiles of
+// kScan1Tile items; blocks take tile indices from an atomic ticket.
+constexpr int kScan1Items = 8;
+constexpr int kScan1Tile = kScanThreads * kScan1Items;
+constexpr unsigned long long kScanInc = 1ull << 63, kScanAgg = 1ull << 62;
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_1p(const uint32_t* __restrict__ in, int n,
+                                                          const int* __restrict__ n_dev, uint32_t* out,
+                                                          uint32_t* total, unsigned long long* status,
+                                                          uint32_t* ticket) {
+    __shared__ uint32_t s_bid, s_excl;
+    if (threadIdx.x == 0) s_bid = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const int bid = (int)s_bid;
+    if (n_dev) n = min(n, *n_dev);
+    const int base = bid * kScan1Tile;
+    if (base >= n && !(bid == 0 && total)) return;
+    uint32_t v[kScan1Items];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int k = 0; k < kScan1Items; ++k) {
+        const int e = base + threadIdx.x * kScan1Items + k;
+        v[k] = e < n ? in[e] : 0u;
+        sum += v[k];
+    }
+    uint32_t agg;
+    const uint32_t ex = block_exclusive_scan(sum, &agg);
+    if (threadIdx.x == 0) {
+        volatile unsigned long long* vs = status;
+        uint32_t excl = 0;
+        if (bid == 0) {
+            vs[0] = kScanInc | agg;
+        } else {
+            vs[bid] = kScanAgg | agg;
+            for (int p = bid - 1; p >= 0;) {
+                const unsigned long long w = vs[p];
+                if (!(w & (kScanInc | kScanAgg))) continue;
+                excl += (uint32_t)w;
+                if (w & kScanInc) break;
+                --p;
+            }
+            vs[bid] = kScanInc | (unsigned long long)(excl + agg);
+        }
+        s_excl = excl;
+        const bool last = base + kScan1Tile >= n;
+        if (last && total) *total = excl + agg;
+    }
+    __syncthreads();
+    uint32_t run = s_excl + ex;
+#pragma unroll
+    for (int k = 0; k < kScan1Items; ++k) {
+        const int e = base + threadIdx.x * kScan1Items + k;
+        if (e < n) out[e] = run;
+        run += v[k];
+    }
+}
+
 // Inclusive prefix sum over the block of one int per thread (a difference array -> values).
 __device__ __forceinline__ int block_inclusive_diff(int v) {
     uint32_t total;
@@ -461,6 +520,32 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_onesweep(const uint32_t
     }
 }
 
+// Per-view reset of the binning state in one launch (instead of a pageable H2D copy of the
+// initial BinState and two memsets): counters, depth-key range, capacity, bucket arrays.
+__global__ void k_frame_init(BinState* st, uint32_t pair_cap, uint32_t* bucket_count, uint32_t* bucket_cur, int nb) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) {
+        BinState z;
+        z.err = kNoError;
+        z.key_min = ~0ull;
+        z.key_max = 0;
+        z.n_valid = 0;
+        z.slow_count = 0;
+        z.shift = 0;
+        z.n_big = 0;
+        z.n_pairs = 0;
+        z.pair_cap = pair_cap;
+        z.n_pairs_eff = 0;
+        z.overflow = 0;
+        z.pad2 = 0;
+        *st = z;
+    }
+    if (i < nb) {
+        bucket_count[i] = 0;
+        bucket_cur[i] = 0;
+    }
+}
+
 // Pair total vs buffer capacity: an overflowing view does no pair work and is re-rendered.
 __global__ void k_check_capacity(BinState* st) {
     const bool over = st->n_pairs > st->pair_cap;
@@ -488,6 +573,17 @@ using namespace rgs_dev;
 static inline int blocks(long long n, int t) { return (int)((n + t - 1) / t); }
 
 int num_depth_buckets() { return kNumBuckets; }
+
+// Single-pass variant; scratch: scan1_scratch_words(n) u32 (status words + ticket).
+size_t scan1_scratch_words(int n) { return 2 * (size_t)(blocks(std::max(n, 1), kScan1Tile) + 1) + 4; }
+void exclusive_scan_1p(const uint32_t* in, int n, uint32_t* out, uint32_t* scratch, uint32_t* total, cudaStream_t s,
+                       const int* n_dev) {
+    const int nb = blocks(std::max(n, 1), kScan1Tile);
+    unsigned long long* status = reinterpret_cast<unsigned long long*>(scratch);
+    uint32_t* ticket = scratch + 2 * (size_t)nb;
+    cudaMemsetAsync(scratch, 0, 4 * (2 * (size_t)nb + 1), s);
+    k_scan_1p<<<nb, kScanThreads, 0, s>>>(in, n, n_dev, out, total, status, ticket);
+}
 
 void exclusive_scan(const uint32_t* in, int n, uint32_t* out, uint32_t* scratch, uint32_t* total, cudaStream_t s,
                     const int* n_dev) {
@@ -548,6 +644,10 @@ void tile_radix_sort(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint3
 }
 
 void check_capacity(BinState* st, cudaStream_t s) { k_check_capacity<<<1, 1, 0, s>>>(st); }
+
+void frame_init(BinState* st, uint32_t pair_cap, uint32_t* bucket_count, uint32_t* bucket_cur, cudaStream_t s) {
+    k_frame_init<<<blocks(kNumBuckets, 256), 256, 0, s>>>(st, pair_cap, bucket_count, bucket_cur, kNumBuckets);
+}
 
 bool binning_init() {
     return cudaFuncSetAttribute(k_bucket_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize,

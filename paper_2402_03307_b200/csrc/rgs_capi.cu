@@ -128,7 +128,7 @@ struct Frame {
         bucket_cur.ensure(4 * nb, s);
         big_list.ensure(4 * nb, s);
         stats.ensure(sizeof(BinState), s);
-        scan_tmp.ensure(4 * 4096, s);
+        scan_tmp.ensure(4 * (4096 + rgs_launch::scan1_scratch_words((int)n1)), s);
         if (!host_stats) CK(cudaMallocHost(&host_stats, sizeof(BinState)));
     }
     void ensure_pixels(size_t npix, int ntiles, cudaStream_t s) {
@@ -398,15 +398,10 @@ int run_forward(rgs_ctx* ctx, Frame& f, cudaStream_t s, Source src, const rgs_sc
     f.ensure_pixels(npix, ntiles, s);
     f.have_src = src == kFromSplats;  // frames are recycled between scene and splat renders
     if (f.have_src) f.src.ensure(4 * (size_t)std::max(n, 1), s);
-    BinState init;
-    std::memset(&init, 0, sizeof init);
-    init.err = kNoError;
-    init.key_min = ~0ull;
-    init.pair_cap = (uint32_t)std::min<long long>(f.pair_cap, 0xffffffffll);
-    CK(cudaMemcpyAsync(f.dstats(), &init, sizeof init, cudaMemcpyHostToDevice, s));
     const int nb = rgs_launch::num_depth_buckets();
-    CK(cudaMemsetAsync(f.bucket_count.p, 0, 4 * (size_t)nb, s));
-    CK(cudaMemsetAsync(f.bucket_cur.p, 0, 4 * (size_t)nb, s));
+    rgs_launch::frame_init(f.dstats(), (uint32_t)std::min<long long>(f.pair_cap, 0xffffffffll),
+                           f.bucket_count.as<uint32_t>(), f.bucket_cur.as<uint32_t>(), s);
+    ctx->launches += 1;
     SplatArrays sa = f.arrays();
     BinState* st_dev = f.dstats();
 
@@ -424,7 +419,7 @@ int run_forward(rgs_ctx* ctx, Frame& f, cudaStream_t s, Source src, const rgs_sc
     {
         StageTimer t(ctx, kStDepthRank, s);
         rgs_launch::bucket_hist(sa.valid, sa.depth_key, n, st_dev, f.bucket_count.as<uint32_t>(), s);
-        rgs_launch::exclusive_scan(f.bucket_count.as<uint32_t>(), nb, f.bucket_off.as<uint32_t>(), scan_tmp + 2048,
+        rgs_launch::exclusive_scan_1p(f.bucket_count.as<uint32_t>(), nb, f.bucket_off.as<uint32_t>(), scan_tmp + 2048,
                                    nullptr, s);
         rgs_launch::depth_ranks(sa.valid, sa.depth_key, sa.tiles, n,
                                 (src == kFromSplats && !splats_monotone) ? sa.source_index : nullptr, st_dev,
@@ -432,14 +427,14 @@ int run_forward(rgs_ctx* ctx, Frame& f, cudaStream_t s, Source src, const rgs_sc
                                 f.bucket_cur.as<uint32_t>(), f.ent_key.as<unsigned long long>(),
                                 f.ent_id.as<uint32_t>(), f.sorted_ids.as<uint32_t>(), f.sorted_tiles.as<uint32_t>(),
                                 f.big_list.as<uint32_t>(), f.big_scratch.p, s);
-        ctx->launches += 8;
+        ctx->launches += 6;
     }
     // Pair offsets in rank order (exclusive scan of tiles-touched; total = pair count).
     {
         StageTimer t(ctx, kStHist, s);
-        rgs_launch::exclusive_scan(f.sorted_tiles.as<uint32_t>(), n, f.pair_off.as<uint32_t>(), scan_tmp,
+        rgs_launch::exclusive_scan_1p(f.sorted_tiles.as<uint32_t>(), n, f.pair_off.as<uint32_t>(), scan_tmp + 4096,
                                    &st_dev->n_pairs, s, &st_dev->n_valid);
-        ctx->launches += 3;
+        ctx->launches += 1;
     }
     if (f.pair_cap == 0) {
         // First view of this frame slot: learn the pair count once, size with headroom.

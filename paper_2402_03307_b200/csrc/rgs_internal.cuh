@@ -124,6 +124,9 @@ int num_depth_buckets();
 bool binning_init();
 void exclusive_scan(const uint32_t* in, int n, uint32_t* out, uint32_t* scratch, uint32_t* total, cudaStream_t s,
                     const int* n_dev = nullptr);
+size_t scan1_scratch_words(int n);
+void exclusive_scan_1p(const uint32_t* in, int n, uint32_t* out, uint32_t* scratch, uint32_t* total, cudaStream_t s,
+                       const int* n_dev = nullptr);
 void bucket_hist(const uint8_t* valid, const unsigned long long* key, int n, BinState* st, uint32_t* bucket_count,
                  cudaStream_t s);
 void depth_ranks(const uint8_t* valid, const unsigned long long* key, const uint32_t* tiles, int n,
@@ -134,6 +137,7 @@ void duplicate(const uint32_t* sorted_ids, const uint32_t* pair_off, const uint3
                const ushort4* rect, const BinState* st, int n, int tiles_x, uint32_t* keys, uint32_t* vals,
                int* aux, cudaStream_t s);
 void check_capacity(BinState* st, cudaStream_t s);
+void frame_init(BinState* st, uint32_t pair_cap, uint32_t* bucket_count, uint32_t* bucket_cur, cudaStream_t s);
 int radix_blocks(long long n_pairs);
 size_t radix_count_entries(long long n_pairs);
 void tile_radix_sort(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32_t* vals_b, const BinState* st,
