@@ -474,13 +474,29 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_onesweep(const uint32_t
         vs[dd] = kFlagInc | tot;
     } else {
         vs[(size_t)bid * kRadixDigits + dd] = kFlagAgg | tot;
+        // Look back in windows of kLookback predecessors: their loads are issued together, so
+        // a long run of aggregate-only predecessors (the first wave starts all at once) costs
+        // one memory round trip per window rather than per block.
+        constexpr int kLookback = 16;
         uint32_t excl = 0;
-        for (int64_t p = (int64_t)bid - 1; p >= 0;) {
-            const uint32_t v = vs[(size_t)p * kRadixDigits + dd];
-            if (!(v & (kFlagAgg | kFlagInc))) continue;  // predecessor not published yet
-            excl += v & kCountMask;
-            if (v & kFlagInc) break;
-            --p;
+        int64_t p = (int64_t)bid - 1;
+        while (p >= 0) {
+            uint32_t win[kLookback];
+#pragma unroll
+            for (int j = 0; j < kLookback; ++j) win[j] = p - j >= 0 ? (uint32_t)vs[(size_t)(p - j) * kRadixDigits + dd] : (uint32_t)kFlagInc;
+            bool stop = false;
+            int used = 0;
+#pragma unroll
+            for (int j = 0; j < kLookback; ++j) {
+                if (stop) break;
+                const uint32_t v = win[j];
+                if (!(v & (kFlagAgg | kFlagInc))) break;  // not published yet: reload from here
+                if (p - j >= 0) excl += v & kCountMask;
+                ++used;
+                if (v & kFlagInc) stop = true;
+            }
+            if (stop) break;
+            p -= used;
         }
         vs[(size_t)bid * kRadixDigits + dd] = kFlagInc | (excl + tot);
         dstart[dd] = excl;  // temporarily: exclusive offset of this block inside the digit

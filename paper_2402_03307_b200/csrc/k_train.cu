@@ -42,6 +42,22 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 }
 
 // ---------------------------------------------------------------------------
+// Deterministic block reduction of one double over NT threads.
+template <int NT>
+__device__ __forceinline__ double block_sum_n(double v, double* red) {
+    const int t = threadIdx.x;
+    red[t] = v;
+    __syncthreads();
+#pragma unroll
+    for (int s = NT / 2; s > 0; s >>= 1) {
+        if (t < s) red[t] = red[t] + red[t + s];
+        __syncthreads();
+    }
+    const double r = red[0];
+    __syncthreads();
+    return r;
+}
+
 // K8a: SSIM forward over one tile of valid positions and one channel.
 // Tile: kSsimTX x kSsimTY valid positions; input footprint (TX+10) x (TY+10).
 template <typename TI>
@@ -136,14 +152,14 @@ __global__ void __launch_bounds__(256) k_ssim_fields(const TI* __restrict__ img,
 // K8b: per output pixel and channel: adjoint convolutions of the three seeds, the SSIM
 // gradient, the L1 gradient and their weighted sum (FP32 dL/dimage for render_backward).
 template <typename TI, typename TO>
-__global__ void __launch_bounds__(256) k_image_grad(const TI* __restrict__ img, const TI* __restrict__ tgt,
+__global__ void __launch_bounds__(kSsimAThreads) k_image_grad(const TI* __restrict__ img, const TI* __restrict__ tgt,
                                                     int W, int H, const double* __restrict__ dfield,
                                                     ImageGradArgs a, TO* __restrict__ dl,
                                                     double* __restrict__ part_l1, double* __restrict__ part_sq) {
-    constexpr int TX = kSsimTX, TY = kSsimTY, DX = TX + kSsimWin - 1, DY = TY + kSsimWin - 1;
+    constexpr int TX = kSsimTX, TY = kSsimATY, DX = TX + kSsimWin - 1, DY = TY + kSsimWin - 1;
     __shared__ double sd[3][DY][DX];
     __shared__ double cols[3][TY][DX];
-    __shared__ double red[256];
+    __shared__ double red[kSsimAThreads];
     const int vw = W - kSsimWin + 1, vh = H - kSsimWin + 1;
     const int X0 = blockIdx.x * TX, Y0 = blockIdx.y * TY, ch = blockIdx.z;
     const int dx0 = X0 - (kSsimWin - 1), dy0 = Y0 - (kSsimWin - 1);
@@ -152,14 +168,14 @@ __global__ void __launch_bounds__(256) k_image_grad(const TI* __restrict__ img, 
     if (grad && a.w_ssim != 0) {
         const size_t nv = (size_t)vw * vh;
         const double* base = dfield + (size_t)ch * 3 * nv;
-        for (int e = t; e < 3 * DY * DX; e += 256) {
+        for (int e = t; e < 3 * DY * DX; e += kSsimAThreads) {
             const int q = e / (DY * DX), rem = e % (DY * DX), r = rem / DX, c = rem % DX;
             const int x = dx0 + c, y = dy0 + r;
             sd[q][r][c] = (x >= 0 && y >= 0 && x < vw && y < vh) ? base[q * nv + (size_t)y * vw + x] : 0.0;
         }
         __syncthreads();
         // cols(x, Y) = sum over y ascending of k[Y - y] g(x, y)   (ssim.cpp:64-67)
-        for (int e = t; e < 3 * TY * DX; e += 256) {
+        for (int e = t; e < 3 * TY * DX; e += kSsimAThreads) {
             const int q = e / (TY * DX), rem = e % (TY * DX), r = rem / DX, c = rem % DX;
             const int Y = Y0 + r;
             const int ylo = max(0, Y - (kSsimWin - 1)), yhi = min(vh - 1, Y);
@@ -198,8 +214,8 @@ __global__ void __launch_bounds__(256) k_image_grad(const TI* __restrict__ img, 
             dl[p] = a.accumulate ? (TO)((double)dl[p] + v) : (TO)v;
         }
     }
-    const double s1 = block_sum(l1, red);
-    const double s2 = block_sum(sq, red);
+    const double s1 = block_sum_n<kSsimAThreads>(l1, red);
+    const double s2 = block_sum_n<kSsimAThreads>(sq, red);
     if (t == 0) {
         const size_t b = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
         part_l1[b] = s1;
@@ -948,7 +964,7 @@ ImageLossGrid image_loss_grid(int W, int H) {
     g.a_x = vw > 0 ? nblk(vw, kSsimTX) : 0;
     g.a_y = vh > 0 ? nblk(vh, kSsimTY) : 0;
     g.b_x = nblk(W, kSsimTX);
-    g.b_y = nblk(H, kSsimTY);
+    g.b_y = nblk(H, kSsimATY);
     g.n_a = 3 * g.a_x * g.a_y;
     g.n_b = 3 * g.b_x * g.b_y;
     return g;
@@ -969,7 +985,7 @@ void image_loss_t(const TI* img, const TI* tgt, int W, int H, const ImageGradArg
     if (has_ssim) k_ssim_fields<TI><<<dim3(g.a_x, g.a_y, 3), 256, 0, s>>>(img, tgt, W, H, dl != nullptr, dfield, pa);
     ImageGradArgs a2 = a;
     if (!has_ssim) a2.w_ssim = 0;
-    k_image_grad<TI, TO><<<dim3(g.b_x, g.b_y, 3), 256, 0, s>>>(img, tgt, W, H, dfield, a2, dl, pl1, psq);
+    k_image_grad<TI, TO><<<dim3(g.b_x, g.b_y, 3), kSsimAThreads, 0, s>>>(img, tgt, W, H, dfield, a2, dl, pl1, psq);
     if (losses) {
         k_finalize<<<1, 256, 0, s>>>(pl1, g.n_b, nvals, loss_scale, 0, accumulate, losses + 0);
         if (has_ssim) k_finalize<<<1, 256, 0, s>>>(pa, g.n_a, count, loss_scale, 1, accumulate, losses + 1);

@@ -10,7 +10,9 @@ namespace rgs_dev {
 
 constexpr int kSsimWin = 11;  // ssim.cpp:12
 constexpr int kSsimTX = 32;   // tile of valid positions / pixels per block (x)
-constexpr int kSsimTY = 8;    // (y); 256 threads
+constexpr int kSsimTY = 8;    // (y); 256 threads (K8b)
+constexpr int kSsimATY = 16;  // K8a tile height; 512 threads
+constexpr int kSsimAThreads = kSsimTX * kSsimATY;
 constexpr int kKnnThreads = 128;
 constexpr int kKnnTile = 1024;
 constexpr int kErrDegenerateTime = 7;
