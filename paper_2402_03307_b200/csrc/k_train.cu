@@ -11,7 +11,7 @@
 //                       parameters, rotor re-normalisation, static-mode masks
 //   K10 k_speeds / k_consistency / k_speed_backward
 //                       consistency regularizer (loss.cpp:33-58, trainer.cpp:66-77)
-//   K11 k_knn           exact 4D k-nearest neighbours (knn.cpp:101-116), brute force
+//   K11 k_knn_grid      exact 4D k-nearest neighbours (knn.cpp:101-116) through a uniform grid
 //       k_reset_opacity optim.cpp:236-243
 //
 // This TU is compiled with -fmad=false and keeps the reference's expression order, so
@@ -558,61 +558,7 @@ __global__ void __launch_bounds__(128) k_speed_backward(ParamView P, const doubl
 }
 
 // ---------------------------------------------------------------------------
-// K11: exact k nearest neighbours in scaled 4D coordinates (knn.cpp:101-116), ordered by
-// (squared distance, index) as KdTree4 guarantees (knn.hpp:18-20).  One thread per query,
-// candidates streamed through shared memory in tiles; top-k kept sorted in registers.
-template <int K>
-__global__ void __launch_bounds__(kKnnThreads) k_knn(const double4* __restrict__ pts, int n, int32_t* __restrict__ out) {
-    __shared__ double4 tile[kKnnTile];
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const double4 q = i < n ? pts[i] : make_double4(0, 0, 0, 0);
-    double bd[K];
-    int bi[K];
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-        bd[j] = INFINITY;
-        bi[j] = 0x7fffffff;
-    }
-    for (int base = 0; base < n; base += kKnnTile) {
-        __syncthreads();
-        for (int e = threadIdx.x; e < kKnnTile; e += blockDim.x)
-            tile[e] = base + e < n ? pts[base + e] : make_double4(INFINITY, INFINITY, INFINITY, INFINITY);
-        __syncthreads();
-        const int lim = min(kKnnTile, n - base);
-        for (int e = 0; e < lim; ++e) {
-            const double4 p = tile[e];
-            const double d0 = p.x - q.x, d1 = p.y - q.y, d2 = p.z - q.z, d3 = p.w - q.w;
-            double dd = d0 * d0;
-            dd += d1 * d1;
-            dd += d2 * d2;
-            dd += d3 * d3;
-            const int j = base + e;
-            // j ascends, so a tie with the current worst never enters (index order kept).
-            if (dd < bd[K - 1] && j != i) {
-                double cd = dd;
-                int ci = j;
-#pragma unroll
-                for (int s = 0; s < K; ++s) {
-                    // insertion: keep (bd, bi) sorted by (distance, index)
-                    const bool less = cd < bd[s] || (cd == bd[s] && ci < bi[s]);
-                    const double td = bd[s];
-                    const int ti = bi[s];
-                    bd[s] = less ? cd : td;
-                    bi[s] = less ? ci : ti;
-                    cd = less ? td : cd;
-                    ci = less ? ti : ci;
-                }
-            }
-        }
-    }
-    if (i < n)
-#pragma unroll
-        for (int j = 0; j < K; ++j) out[(size_t)K * i + j] = bi[j];
-}
-
-
-// ---------------------------------------------------------------------------
-// K11b: exact KNN through a uniform 4D grid.  Points are counting-sorted by cell; a query
+// K11: exact KNN through a uniform 4D grid.  Points are counting-sorted by cell; a query
 // scans the (2r+1)^4 block of cells around its own, shell by shell, until its k-th
 // distance is below the distance to the unscanned region (with a relative safety margin
 // for the rounding of that bound), or the block covers the grid.  The top-k insertion is
@@ -1076,20 +1022,6 @@ void knn_points(const float* params, const double* params64, int n, const double
         k_knn_points<true><<<nblk(n, 256), 256, 0, s>>>(P, sc, reinterpret_cast<double4*>(pts4));
     else
         k_knn_points<false><<<nblk(n, 256), 256, 0, s>>>(P, sc, reinterpret_cast<double4*>(pts4));
-}
-
-int knn(const double* pts4, int n, int k, int32_t* out, cudaStream_t s) {
-    const double4* p = reinterpret_cast<const double4*>(pts4);
-    const int nb = nblk(n, kKnnThreads);
-    switch (k) {
-        case 1: k_knn<1><<<nb, kKnnThreads, 0, s>>>(p, n, out); break;
-        case 2: k_knn<2><<<nb, kKnnThreads, 0, s>>>(p, n, out); break;
-        case 4: k_knn<4><<<nb, kKnnThreads, 0, s>>>(p, n, out); break;
-        case 8: k_knn<8><<<nb, kKnnThreads, 0, s>>>(p, n, out); break;
-        case 16: k_knn<16><<<nb, kKnnThreads, 0, s>>>(p, n, out); break;
-        default: return -1;
-    }
-    return 0;
 }
 
 // Grid build over the data points + query launch.  queries4 == NULL: the data points are the

@@ -13,8 +13,6 @@ constexpr int kSsimTX = 32;   // tile of valid positions / pixels per block (x)
 constexpr int kSsimTY = 8;    // (y); 256 threads (K8b)
 constexpr int kSsimATY = 16;  // K8a tile height; 512 threads
 constexpr int kSsimAThreads = kSsimTX * kSsimATY;
-constexpr int kKnnThreads = 128;
-constexpr int kKnnTile = 1024;
 constexpr int kErrDegenerateTime = 7;
 
 // dL/dimage assembly (trainer.cpp:41-50): w_l1 * l1_grad + w_ssim * ssim_grad.
@@ -68,7 +66,6 @@ void speed_backward(const float* params, const double* params64, int n, const do
                     float* grads, cudaStream_t s);
 void knn_points(const float* params, const double* params64, int n, const double* scales, double* pts4,
                 cudaStream_t s);
-int knn(const double* pts4, int n, int k, int32_t* out, cudaStream_t s);
 int knn_grid(const double* pts4, int n, const double* queries4, const int32_t* qexcl, int nq, int k, int32_t* out,
              void* scratch, size_t scratch_bytes, cudaStream_t s);
 size_t knn_grid_scratch(int n);
