@@ -83,6 +83,9 @@ __device__ __forceinline__ int d_normalize(const double* in, double* v) {
 // (zero-coefficient slots included so signed zeros match).
 #define RGS_QT(a, b, c) val += (c) * v[a] * v[b]
 #define RGS_QZ val += 0.0 * v[0] * v[0]
+// Four zero-coefficient terms: each adds 0.0 * v0 * v0 = +0 (v is finite after normalize), and
+// adding +0 four times equals adding it once (it only turns -0 into +0).
+#define RGS_QZ4 val += 0.0
 __device__ __forceinline__ void d_to_matrix(const double* v, double* m) {
     double val;
     // R00
@@ -90,52 +93,53 @@ __device__ __forceinline__ void d_to_matrix(const double* v, double* m) {
     RGS_QT(4, 4, 1.0); RGS_QT(5, 5, 1.0); RGS_QT(6, 6, 1.0); RGS_QT(7, 7, -1.0); m[0] = val;
     // R01
     val = 0; RGS_QT(1, 0, 2.0); RGS_QT(2, 4, -2.0); RGS_QT(3, 5, -2.0); RGS_QT(6, 7, 2.0);
-    RGS_QZ; RGS_QZ; RGS_QZ; RGS_QZ; m[1] = val;
+    RGS_QZ4; m[1] = val;
     // R02
     val = 0; RGS_QT(1, 4, 2.0); RGS_QT(2, 0, 2.0); RGS_QT(3, 6, -2.0); RGS_QT(5, 7, -2.0);
-    RGS_QZ; RGS_QZ; RGS_QZ; RGS_QZ; m[2] = val;
+    RGS_QZ4; m[2] = val;
     // R03
     val = 0; RGS_QT(1, 5, 2.0); RGS_QT(2, 6, 2.0); RGS_QT(3, 0, 2.0); RGS_QT(4, 7, 2.0);
-    RGS_QZ; RGS_QZ; RGS_QZ; RGS_QZ; m[3] = val;
+    RGS_QZ4; m[3] = val;
     // R10
     val = 0; RGS_QT(1, 0, -2.0); RGS_QT(2, 4, -2.0); RGS_QT(3, 5, -2.0); RGS_QT(6, 7, -2.0);
-    RGS_QZ; RGS_QZ; RGS_QZ; RGS_QZ; m[4] = val;
+    RGS_QZ4; m[4] = val;
     // R11
     val = 0; RGS_QT(0, 0, 1.0); RGS_QT(1, 1, -1.0); RGS_QT(2, 2, 1.0); RGS_QT(3, 3, 1.0);
     RGS_QT(4, 4, -1.0); RGS_QT(5, 5, -1.0); RGS_QT(6, 6, 1.0); RGS_QT(7, 7, -1.0); m[5] = val;
     // R12
     val = 0; RGS_QT(1, 2, -2.0); RGS_QT(3, 7, 2.0); RGS_QT(4, 0, 2.0); RGS_QT(5, 6, -2.0);
-    RGS_QZ; RGS_QZ; RGS_QZ; RGS_QZ; m[6] = val;
+    RGS_QZ4; m[6] = val;
     // R13
     val = 0; RGS_QT(1, 3, -2.0); RGS_QT(2, 7, -2.0); RGS_QT(4, 6, 2.0); RGS_QT(5, 0, 2.0);
-    RGS_QZ; RGS_QZ; RGS_QZ; RGS_QZ; m[7] = val;
+    RGS_QZ4; m[7] = val;
     // R20
     val = 0; RGS_QT(1, 4, 2.0); RGS_QT(2, 0, -2.0); RGS_QT(3, 6, -2.0); RGS_QT(5, 7, 2.0);
-    RGS_QZ; RGS_QZ; RGS_QZ; RGS_QZ; m[8] = val;
+    RGS_QZ4; m[8] = val;
     // R21
     val = 0; RGS_QT(1, 2, -2.0); RGS_QT(3, 7, -2.0); RGS_QT(4, 0, -2.0); RGS_QT(5, 6, -2.0);
-    RGS_QZ; RGS_QZ; RGS_QZ; RGS_QZ; m[9] = val;
+    RGS_QZ4; m[9] = val;
     // R22
     val = 0; RGS_QT(0, 0, 1.0); RGS_QT(1, 1, 1.0); RGS_QT(2, 2, -1.0); RGS_QT(3, 3, 1.0);
     RGS_QT(4, 4, -1.0); RGS_QT(5, 5, 1.0); RGS_QT(6, 6, -1.0); RGS_QT(7, 7, -1.0); m[10] = val;
     // R23
     val = 0; RGS_QT(1, 7, 2.0); RGS_QT(2, 3, -2.0); RGS_QT(4, 5, -2.0); RGS_QT(6, 0, 2.0);
-    RGS_QZ; RGS_QZ; RGS_QZ; RGS_QZ; m[11] = val;
+    RGS_QZ4; m[11] = val;
     // R30
     val = 0; RGS_QT(1, 5, 2.0); RGS_QT(2, 6, 2.0); RGS_QT(3, 0, -2.0); RGS_QT(4, 7, -2.0);
-    RGS_QZ; RGS_QZ; RGS_QZ; RGS_QZ; m[12] = val;
+    RGS_QZ4; m[12] = val;
     // R31
     val = 0; RGS_QT(1, 3, -2.0); RGS_QT(2, 7, 2.0); RGS_QT(4, 6, 2.0); RGS_QT(5, 0, -2.0);
-    RGS_QZ; RGS_QZ; RGS_QZ; RGS_QZ; m[13] = val;
+    RGS_QZ4; m[13] = val;
     // R32
     val = 0; RGS_QT(1, 7, -2.0); RGS_QT(2, 3, -2.0); RGS_QT(4, 5, -2.0); RGS_QT(6, 0, -2.0);
-    RGS_QZ; RGS_QZ; RGS_QZ; RGS_QZ; m[14] = val;
+    RGS_QZ4; m[14] = val;
     // R33
     val = 0; RGS_QT(0, 0, 1.0); RGS_QT(1, 1, 1.0); RGS_QT(2, 2, 1.0); RGS_QT(3, 3, -1.0);
     RGS_QT(4, 4, 1.0); RGS_QT(5, 5, -1.0); RGS_QT(6, 6, -1.0); RGS_QT(7, 7, -1.0); m[15] = val;
 }
 #undef RGS_QT
 #undef RGS_QZ
+#undef RGS_QZ4
 
 // SliceCache (gaussian.hpp:36-45) restricted to what the device needs.
 struct SliceState {
