@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--profile-only", action="store_true", help="one warm sweep, no JSON (for ncu)")
     ap.add_argument("--no-train", action="store_true", help="skip the C3 training leg")
     ap.add_argument("--no-c4", action="store_true", help="skip the C4 4K batch leg")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 1M-Gaussian training leg")
     ap.add_argument("--train-only", action="store_true", help="only the C3 training leg (profiling)")
     ap.add_argument("--train-steps", type=int, default=10)
     return ap.parse_args()
@@ -232,6 +233,66 @@ def run_c4_leg(args, ctx, dev, dist, rank, world, flush):
                                    "timestamps, views sharded contiguously across ranks",
                        "n_gaussians": C4_N, "width": C4_W, "height": C4_H, "n_pairs_mid_view": n_pairs,
                        "n_visible_mid_view": n_vis, "l2": "256 MiB flush before each timed batch"}}
+
+
+# ----------------------------------------------------------------------------- C5 training leg
+C5_N, C5_W, C5_H, C5_SEED, C5_VIEWS = 1_000_000, 1352, 1014, 5, 8
+
+
+def run_c5_leg(args, ctx, dev, dist, rank, world, flush):
+    """Config C5: multi-view training, 1M Gaussians, an 8-view batch per rank, the batch reduced
+    with one NCCL all-reduce per step (replicated scene, weak scaling in views)."""
+    import torch
+
+    from paper_2402_03307_b200 import rgs, scenes, train
+
+    truth = scenes.synthetic_scene(C5_N, C5_W, C5_H, seed=C5_SEED)
+    store = truth.copy()
+    r = np.random.default_rng(C5_SEED)
+    store.mean[:, :3] += r.normal(0, 0.01, (C5_N, 3)).astype(np.float32)
+    store.sh[:, :, 0] += r.normal(0, 0.1, (C5_N, 3)).astype(np.float32)
+    cams = [scenes.bench_camera(C5_W, C5_H, (v + 0.5) / C5_VIEWS,
+                                scenes.yaw_pose(-4.0 + 8.0 * v / (C5_VIEWS - 1) + 0.7 * rank, (0.02, 0.0, 0.03)))
+            for v in range(C5_VIEWS)]
+    tsc = rgs.DeviceScene.from_store(ctx, truth)
+    targets = torch.empty((C5_VIEWS, C5_H, C5_W, 3), dtype=torch.float32, device=dev)
+    ctx.render_views(tsc, cams, (0.0, 0.0, 0.0), out=targets)
+    tsc.close()
+    del truth
+    scene = rgs.DeviceScene.from_store(ctx, store)
+    tr = train.Trainer(ctx, scene, train.TrainConfig(batch=C5_VIEWS, total_steps=2000, max_gaussians=2_000_000),
+                       dist)
+    tlist = [targets[v] for v in range(C5_VIEWS)]
+    for _ in range(2):
+        tr.step(cams, tlist)
+    stream = torch.cuda.current_stream(dev)
+    steps = 5
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    flush.zero_()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        last = tr.step(cams, tlist)
+    b.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = max_over_ranks(a.elapsed_time(b), dist, dev)
+    its = steps / (ms / 1e3)
+    out = {"metric": "train it/s (C5)", "value": its, "unit": "it/s", "n_gpus": world, "steps": steps,
+           "ms_per_step": ms / steps, "views_per_step": C5_VIEWS * world, "views_per_s": its * C5_VIEWS * world,
+           "scaling": "weak",
+           "allreduce_bytes_per_step": (66 * C5_N + C5_N) * 4 + 3 * 8 if world > 1 else 0,
+           "loss_last": last.total,
+           "config": {"workload": "C5: 1M 4D rotor Gaussians, SH deg 3, 1352x1014, 8 camera x timestamp views per rank "
+                                  "and step, full training step, batch reduced by NCCL all-reduce",
+                      "n_gaussians": C5_N, "width": C5_W, "height": C5_H, "views_per_rank": C5_VIEWS}}
+    tr = None
+    scene.close()
+    del targets, tlist
+    torch.cuda.empty_cache()
+    return out
 
 
 # ----------------------------------------------------------------------------- training leg
@@ -557,13 +618,15 @@ def run_ours(args, rank, local_rank, world):
                "sample": f"{len(picks)} frames (t index {picks}) of the same sweep, full 1352x1014, "
                          f"{threads} threads, {cpu_model()}"}
 
-    train_res = c4_res = None
+    train_res = c4_res = c5_res = None
     del images
     torch.cuda.empty_cache()
     if not args.no_c4:
         c4_res = run_c4_leg(args, ctx, dev, dist, rank, world, flush)
     if not args.no_train:
         train_res = run_train_leg(args, ctx, dev, dist, rank, world, flush)
+    if not args.no_c5:
+        c5_res = run_c5_leg(args, ctx, dev, dist, rank, world, flush)
 
     if rank == 0:
         line = {
@@ -583,7 +646,7 @@ def run_ours(args, rank, local_rank, world):
             "stages_note": "per-stage CUDA events from a serialised profiling sweep after the timed region "
                            "(the timed sweeps pipeline 3 views over 3 streams, so stages overlap there)",
             "fp32_peak_tflops": fp32_peak, "clocks": clocks, "gpu_launches": launches,
-            "e2e": e2e, "cpu_baseline": cpu, "c4": c4_res, "train": train_res,
+            "e2e": e2e, "cpu_baseline": cpu, "c4": c4_res, "train": train_res, "train_c5": c5_res,
         }
         print(json.dumps(line), flush=True)
     if dist:

@@ -177,10 +177,11 @@ __global__ void __launch_bounds__(kSsimAThreads) k_image_grad(const TI* __restri
         // cols(x, Y) = sum over y ascending of k[Y - y] g(x, y)   (ssim.cpp:64-67)
         for (int e = t; e < 3 * TY * DX; e += kSsimAThreads) {
             const int q = e / (TY * DX), rem = e % (TY * DX), r = rem / DX, c = rem % DX;
-            const int Y = Y0 + r;
-            const int ylo = max(0, Y - (kSsimWin - 1)), yhi = min(vh - 1, Y);
+            // y = Y - 10 + i ascending; rows outside the valid region are zero in sd, so the
+            // fixed 11 taps add +0 there and the sum equals the reference's clipped one
             double s = 0;
-            for (int y = ylo; y <= yhi; ++y) s += c_win[Y - y] * sd[q][y - dy0][c];
+#pragma unroll
+            for (int i = 0; i < kSsimWin; ++i) s += c_win[kSsimWin - 1 - i] * sd[q][r + i][c];
             cols[q][r][c] = s;
         }
         __syncthreads();
@@ -198,12 +199,13 @@ __global__ void __launch_bounds__(kSsimAThreads) k_image_grad(const TI* __restri
             double g_ssim = 0;
             if (a.w_ssim != 0) {
                 // out(X, y) = sum over x ascending of k[X - x] cols(x, y)   (ssim.cpp:68-71)
-                const int xlo = max(0, X - (kSsimWin - 1)), xhi = min(vw - 1, X);
+                // x = X - 10 + i ascending; columns outside the valid region are zero in cols
                 double g[3];
 #pragma unroll
                 for (int q = 0; q < 3; ++q) {
                     double s = 0;
-                    for (int x = xlo; x <= xhi; ++x) s += c_win[X - x] * cols[q][r][x - dx0];
+#pragma unroll
+                    for (int i = 0; i < kSsimWin; ++i) s += c_win[kSsimWin - 1 - i] * cols[q][r][c + i];
                     g[q] = s;
                 }
                 g_ssim = g[0] + 2 * xv * g[1] + yv * g[2];  // ssim.cpp:124-125
