@@ -508,26 +508,36 @@ __global__ void __launch_bounds__(256) k_backward_fp64(SplatArrays sp, const uin
                     c2 = c.z;
                 }
             }
-            // Sequential recursion over lanes 0..31 (= descending positions).
-            double my_Tb = 0, my_s0 = 0, my_s1 = 0, my_s2 = 0;
-            unsigned mask = __ballot_sync(0xffffffffu, pass);
-            while (mask) {
-                const int l = __ffs(mask) - 1;
-                mask &= mask - 1;
-                const double al = __shfl_sync(0xffffffffu, a, l);
-                const double T_before = T_run / (1 - al);
-                const double wgt = al * T_before;
-                if (lane == l) {
-                    my_Tb = T_before;
-                    my_s0 = s0;
-                    my_s1 = s1;
-                    my_s2 = s2;
-                }
-                s0 = s0 + __shfl_sync(0xffffffffu, c0, l) * wgt;
-                s1 = s1 + __shfl_sync(0xffffffffu, c1, l) * wgt;
-                s2 = s2 + __shfl_sync(0xffffffffu, c2, l) * wgt;
-                T_run = T_before;
+            // The back-to-front recursion T_before = T_run / (1 - a), suffix += c a T_before over
+            // lanes 0..31 (= descending positions) as warp scans: an inclusive product of (1 - a)
+            // and an exclusive sum of the colour contributions.  No decision depends on T here
+            // (the forward fixed contrib), so the ~1-ulp reassociation only reaches the values.
+            double f = pass ? 1 - a : 1.0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double y = __shfl_up_sync(0xffffffffu, f, o);
+                if (lane >= o) f *= y;
             }
+            const double my_Tb = T_run / f;
+            const double wl = pass ? a * my_Tb : 0.0;
+            double e0 = c0 * wl, e1 = c1 * wl, e2 = c2 * wl;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double y0 = __shfl_up_sync(0xffffffffu, e0, o);
+                const double y1 = __shfl_up_sync(0xffffffffu, e1, o);
+                const double y2 = __shfl_up_sync(0xffffffffu, e2, o);
+                if (lane >= o) {
+                    e0 += y0;
+                    e1 += y1;
+                    e2 += y2;
+                }
+            }
+            // exclusive prefix = inclusive - own contribution
+            const double my_s0 = s0 + (e0 - c0 * wl), my_s1 = s1 + (e1 - c1 * wl), my_s2 = s2 + (e2 - c2 * wl);
+            T_run = T_run / __shfl_sync(0xffffffffu, f, 31);
+            s0 = s0 + __shfl_sync(0xffffffffu, e0, 31);
+            s1 = s1 + __shfl_sync(0xffffffffu, e1, 31);
+            s2 = s2 + __shfl_sync(0xffffffffu, e2, 31);
             if (pass) {
                 const double T_before = my_Tb;
                 const double wgt = a * T_before;

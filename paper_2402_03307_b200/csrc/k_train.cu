@@ -59,20 +59,22 @@ __device__ __forceinline__ double block_sum_n(double v, double* red) {
 }
 
 // K8a: SSIM forward over one tile of valid positions and one channel.
-// Tile: kSsimTX x kSsimTY valid positions; input footprint (TX+10) x (TY+10).
+// Tile: kSsimTX x kSsimATY valid positions (512 threads); input footprint (TX+10) x (TY+10).
 template <typename TI>
-__global__ void __launch_bounds__(256) k_ssim_fields(const TI* __restrict__ img, const TI* __restrict__ tgt,
+__global__ void __launch_bounds__(kSsimAThreads) k_ssim_fields(const TI* __restrict__ img, const TI* __restrict__ tgt,
                                                      int W, int H, int want_grad, double* __restrict__ dfield,
                                                      double* __restrict__ part_ssim) {
-    constexpr int TX = kSsimTX, TY = kSsimTY, IX = TX + kSsimWin - 1, IY = TY + kSsimWin - 1;
-    __shared__ TI sa[IY][IX + 1];
-    __shared__ TI sb[IY][IX + 1];
-    __shared__ double rows[5][IY][TX];
-    __shared__ double red[256];
+    constexpr int TX = kSsimTX, TY = kSsimATY, IX = TX + kSsimWin - 1, IY = TY + kSsimWin - 1;
+    // dynamic shared memory: rows[5][IY][TX] and red[] (double), then sa / sb [IY][IX + 1] (TI)
+    extern __shared__ double k8a_smem[];
+    auto rows = reinterpret_cast<double (*)[IY][TX]>(k8a_smem);
+    double* red = k8a_smem + 5 * IY * TX;
+    auto sa = reinterpret_cast<TI (*)[IX + 1]>(red + kSsimAThreads);
+    auto sb = reinterpret_cast<TI (*)[IX + 1]>(reinterpret_cast<TI*>(red + kSsimAThreads) + IY * (IX + 1));
     const int vw = W - kSsimWin + 1, vh = H - kSsimWin + 1;
     const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY, ch = blockIdx.z;
     const int t = threadIdx.x;
-    for (int e = t; e < IY * IX; e += 256) {
+    for (int e = t; e < IY * IX; e += kSsimAThreads) {
         const int r = e / IX, c = e % IX;
         const int gx = x0 + c, gy = y0 + r;
         TI a = 0, b = 0;
@@ -86,7 +88,7 @@ __global__ void __launch_bounds__(256) k_ssim_fields(const TI* __restrict__ img,
     }
     __syncthreads();
     // Horizontal pass (ssim.cpp:44-49): rows(x, y) = sum_i k_i in(x + i, y), from 0.
-    for (int e = t; e < IY * TX; e += 256) {
+    for (int e = t; e < IY * TX; e += kSsimAThreads) {
         const int r = e / TX, c = e % TX;
         double s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0;
 #pragma unroll
@@ -144,7 +146,7 @@ __global__ void __launch_bounds__(256) k_ssim_fields(const TI* __restrict__ img,
             base[2 * nv + p] = d_vxy;
         }
     }
-    const double s = block_sum(ssim, red);
+    const double s = block_sum_n<kSsimAThreads>(ssim, red);
     if (t == 0)
         part_ssim[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = s;
 }
@@ -910,7 +912,7 @@ ImageLossGrid image_loss_grid(int W, int H) {
     ImageLossGrid g;
     const int vw = W - kSsimWin + 1, vh = H - kSsimWin + 1;
     g.a_x = vw > 0 ? nblk(vw, kSsimTX) : 0;
-    g.a_y = vh > 0 ? nblk(vh, kSsimTY) : 0;
+    g.a_y = vh > 0 ? nblk(vh, kSsimATY) : 0;
     g.b_x = nblk(W, kSsimTX);
     g.b_y = nblk(H, kSsimATY);
     g.n_a = 3 * g.a_x * g.a_y;
@@ -930,7 +932,15 @@ void image_loss_t(const TI* img, const TI* tgt, int W, int H, const ImageGradArg
     // Images smaller than the window have no SSIM (the caller rejects w_ssim != 0 for them):
     // stage A is skipped and the SSIM slot is NaN.
     const bool has_ssim = W >= kSsimWin && H >= kSsimWin;
-    if (has_ssim) k_ssim_fields<TI><<<dim3(g.a_x, g.a_y, 3), 256, 0, s>>>(img, tgt, W, H, dl != nullptr, dfield, pa);
+    constexpr int IY = kSsimATY + kSsimWin - 1, IX = kSsimTX + kSsimWin - 1;
+    const size_t smem = sizeof(double) * (5 * IY * kSsimTX + kSsimAThreads) + sizeof(TI) * 2 * IY * (IX + 1);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_ssim_fields<TI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    if (has_ssim)
+        k_ssim_fields<TI><<<dim3(g.a_x, g.a_y, 3), kSsimAThreads, smem, s>>>(img, tgt, W, H, dl != nullptr, dfield, pa);
     ImageGradArgs a2 = a;
     if (!has_ssim) a2.w_ssim = 0;
     k_image_grad<TI, TO><<<dim3(g.b_x, g.b_y, 3), kSsimAThreads, 0, s>>>(img, tgt, W, H, dfield, a2, dl, pl1, psq);

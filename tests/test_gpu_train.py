@@ -406,3 +406,42 @@ def test_trainer_densifies(ctx):
         lb = tr.step(cams, targets)
     assert np.isfinite(lb.total)
     assert sc.n != n0 and tr.grads.numel() == 65 * sc.n
+
+
+def test_trainer_overlap_matches_serial(ctx):
+    """The overlapped multi-stream evaluate_loss (forward of view v+1 beside the backward of
+    view v) gives the serial result: same losses, gradients equal up to FP64-atomic order."""
+    import torch
+
+    store, truth, cams = _training_case(n=3000, views=4)
+    tsc = DeviceScene.from_store(ctx, truth)
+    targets = [ctx.render_forward_device(tsc, c, retain=False)[0].clone() for c in cams]
+    tctx = rgs.Context(0)  # on torch's stream: the overlap path needs it
+    out = []
+    for overlap in (False, True):
+        sc = DeviceScene.from_store(tctx, store)
+        tr = train.Trainer(tctx, sc, train.TrainConfig())
+        tr.overlap = overlap
+        tr.rebuild_knn()
+        tr.evaluate_loss(cams, targets)
+        torch.cuda.synchronize()
+        out.append((tr.losses.cpu().numpy().copy(), tr.grads.cpu().numpy().copy(), tr.visible.cpu().numpy().copy()))
+    (l0, g0, v0), (l1, g1, v1) = out
+    assert np.allclose(l0, l1, rtol=1e-12, atol=0)
+    assert np.array_equal(v0, v1)
+    scale = np.abs(g0).max()
+    assert np.abs(g0 - g1).max() <= 1e-5 * scale
+
+
+def test_render_views_host_matches_device(ctx):
+    """The e2e entry point (host scene in, host images out) renders what the device path does."""
+    import torch
+
+    store = scenes.synthetic_scene(20000, 320, 240, seed=8)
+    cams = scenes.sweep_cameras(320, 240, 7)
+    sc = DeviceScene.from_store(ctx, store)
+    dev = ctx.render_views(sc, cams)
+    torch.cuda.synchronize()
+    host = torch.empty((7, 240, 320, 3), dtype=torch.float32).pin_memory()
+    ctx.render_views_host(store.arrays_f32(), store.active_sh_degree, cams, (0, 0, 0), host.numpy())
+    assert np.array_equal(host.numpy(), dev.cpu().numpy())
