@@ -438,15 +438,22 @@ def run_ours(args, rank, local_rank, world):
 
     from paper_2402_03307_b200 import rgs, scenes
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # RGS_BENCH_SHARE_GPU=1 (test harness only): every rank on device 0 over gloo, to exercise
+    # the multi-rank code paths on a one-GPU box.  The driver's runs use one GPU per rank + NCCL.
+    shared = os.environ.get("RGS_BENCH_SHARE_GPU") == "1"
+    dev_index = 0 if shared else local_rank
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
-    ctx = rgs.Context(local_rank)
+    ctx = rgs.Context(dev_index)
     if args.train_only:
         flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
         res = run_train_leg(args, ctx, dev, dist, rank, world, flush)
