@@ -136,12 +136,12 @@ __global__ void __launch_bounds__(256, 5) k_blend_fp32(SplatArrays sp, const uin
             while (mask) {
                 const int k = c + __ffs(mask) - 1;
                 mask &= mask - 1;
+                if (done) continue;
                 const float4 a = sm[k].a, b = sm[k].b;
                 float p, M, dx, dy;
                 gate_values(a, b, fpx, fpy, p, M, dx, dy);
-                if (COUNT) n_eval += !done;
-                // finished lanes ride along in SIMT anyway: fold them into the skip predicate
-                if (done | gate_skip(p, M, b.z)) continue;
+                if (COUNT) ++n_eval;
+                if (gate_skip(p, M, b.z)) continue;
                 const float4 cc = sm[k].c;
                 const float2 pr = make_float2(sm[k].d.z, sm[k].d.w);
                 const float al = blend_alpha(cc.w, p);
@@ -149,12 +149,10 @@ __global__ void __launch_bounds__(256, 5) k_blend_fp32(SplatArrays sp, const uin
                 const float test_T = __fmul_rn(T, om);
                 const float errN = fmaf(al * M, pr.y, errT + 3e-7f);
                 // ambiguous: a classify gate, the backward's clamp gate (unclamped alpha <= 0.99,
-                // rasterizer.cpp:356) or T(1 - alpha) < 1e-4 within their error bounds.  Far above
-                // 1e-4 (the common case) neither the T gate's bound nor the stop test can fire.
+                // rasterizer.cpp:356) or T(1 - alpha) < 1e-4 within their error bounds
                 const bool amb_g = gate_ambiguous(p, M, b.z);
                 const bool amb_c = (__fadd_rn(p, M) >= pr.x) & (__fsub_rn(p, M) <= pr.x);
-                const bool near_stop = !(test_T > fmaf(2e-4f, errN, 1e-4f));
-                const bool amb_t = near_stop && (fabsf(test_T - 1e-4f) <= test_T * errN);
+                const bool amb_t = fabsf(test_T - 1e-4f) <= test_T * errN;
                 const bool amb = amb_g | amb_c | amb_t;
                 if (COUNT && amb) {
                     // slow-pixel reasons: power > 0 / alpha gate, clamp gate, transmittance gate
@@ -165,7 +163,7 @@ __global__ void __launch_bounds__(256, 5) k_blend_fp32(SplatArrays sp, const uin
                     slow = done = true;
                     continue;
                 }
-                if (near_stop && test_T < 1e-4f) {  // rasterizer.cpp:111: the splat is not blended
+                if (test_T < 1e-4f) {  // rasterizer.cpp:111: the splat is not blended
                     done = stopped = true;
                     if (COUNT) n_ref = start - rg.x + k + 1;
                     continue;
