@@ -420,15 +420,16 @@ void blend_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* r
                                                                   n_contrib, slow_list, slow_count, counters);
 }
 
+// Per-device kernel attributes (called from rgs_ctx_create on the context's device).
+bool raster_init() {
+    return cudaFuncSetAttribute(k_backward_fp32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSmem) ==
+           cudaSuccess;
+}
+
 void backward_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges, const DevCamera& cam,
                    float3 bg, const double* final_T, const uint32_t* n_contrib, const float* dL_dimage,
                    double* screen_grads, cudaStream_t s) {
     const int tiles = cam.tiles_x * cam.tiles_y;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_backward_fp32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSmem);
-        attr = true;
-    }
     k_backward_fp32<<<tiles, kTilePixels, kBwdSmem, s>>>(sp, pair_vals, ranges, cam, bg, final_T, n_contrib,
                                                          dL_dimage, screen_grads);
 }

@@ -908,6 +908,17 @@ void set_ssim_window(const double* k11, cudaStream_t s) {
     cudaMemcpyToSymbolAsync(c_win, k11, sizeof(double) * kSsimWin, 0, cudaMemcpyHostToDevice, s);
 }
 
+// Per-device kernel attributes (called from rgs_ctx_create on the context's device).
+bool train_init() {
+    constexpr int IY = kSsimATY + kSsimWin - 1, IX = kSsimTX + kSsimWin - 1;
+    const size_t s32 = sizeof(double) * (5 * IY * kSsimTX + kSsimAThreads) + sizeof(float) * 2 * IY * (IX + 1);
+    const size_t s64 = sizeof(double) * (5 * IY * kSsimTX + kSsimAThreads) + sizeof(double) * 2 * IY * (IX + 1);
+    return cudaFuncSetAttribute(k_ssim_fields<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s32) ==
+               cudaSuccess &&
+           cudaFuncSetAttribute(k_ssim_fields<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s64) ==
+               cudaSuccess;
+}
+
 ImageLossGrid image_loss_grid(int W, int H) {
     ImageLossGrid g;
     const int vw = W - kSsimWin + 1, vh = H - kSsimWin + 1;
@@ -934,11 +945,6 @@ void image_loss_t(const TI* img, const TI* tgt, int W, int H, const ImageGradArg
     const bool has_ssim = W >= kSsimWin && H >= kSsimWin;
     constexpr int IY = kSsimATY + kSsimWin - 1, IX = kSsimTX + kSsimWin - 1;
     const size_t smem = sizeof(double) * (5 * IY * kSsimTX + kSsimAThreads) + sizeof(TI) * 2 * IY * (IX + 1);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_ssim_fields<TI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
     if (has_ssim)
         k_ssim_fields<TI><<<dim3(g.a_x, g.a_y, 3), kSsimAThreads, smem, s>>>(img, tgt, W, H, dl != nullptr, dfield, pa);
     ImageGradArgs a2 = a;

@@ -210,6 +210,8 @@ struct rgs_ctx {
     cudaEvent_t slot_done[kSlots] = {};
     cudaEvent_t join_ev = nullptr;
     std::vector<void*> frame_pool;   // PooledFrame* of destroyed records
+    void* train = nullptr;           // TrainScratch (training-side buffers), created on first use
+    void (*train_free)(void*, cudaStream_t) = nullptr;
     BinState* view_stats = nullptr;  // pinned, one per view of the current batch
     size_t view_stats_cap = 0;
     void ensure_view_stats(size_t n) {
@@ -565,6 +567,8 @@ int rgs_ctx_create(int device, rgs_ctx** out) {
         }
         CK(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
         if (!rgs_launch::binning_init()) throw CudaError{cudaErrorInvalidValue, "binning_init"};
+        if (!rgs_launch::raster_init()) throw CudaError{cudaErrorInvalidValue, "raster_init"};
+        if (!rgs_launch::train_init()) throw CudaError{cudaErrorInvalidValue, "train_init"};
         // Keep freed blocks in the pool: frames re-grow without hitting the driver.
         cudaMemPool_t pool;
         CK(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -595,6 +599,7 @@ void rgs_ctx_destroy(rgs_ctx* c) {
         delete pf;
     }
     c->frame_pool.clear();
+    if (c->train && c->train_free) c->train_free(c->train, c->stream);
     for (int k = 0; k < rgs_ctx::kSlots; ++k) {
         if (!c->slot_stream[k]) continue;
         c->slot_frame[k].release(c->slot_stream[k]);
@@ -1388,13 +1393,20 @@ void ensure_ssim_window(rgs_ctx* c) {
 struct TrainScratch {
     DevBuf dfield, parts, speeds, dspeed, pts, lo, hi, knn;
 };
+void train_scratch_free(void* p, cudaStream_t s) {
+    TrainScratch* ts = static_cast<TrainScratch*>(p);
+    for (DevBuf* b : {&ts->dfield, &ts->parts, &ts->speeds, &ts->dspeed, &ts->pts, &ts->lo, &ts->hi, &ts->knn})
+        b->release(s);
+    delete ts;
+}
+
+// One scratch set per context, released with it (rgs_ctx_destroy).
 TrainScratch& train_scratch(rgs_ctx* c) {
-    // One scratch set per context (kept alongside the context's other buffers).
-    static thread_local std::vector<std::pair<rgs_ctx*, TrainScratch*>> reg;
-    for (auto& p : reg)
-        if (p.first == c) return *p.second;
-    reg.push_back({c, new TrainScratch});
-    return *reg.back().second;
+    if (!c->train) {
+        c->train = new TrainScratch;
+        c->train_free = train_scratch_free;
+    }
+    return *static_cast<TrainScratch*>(c->train);
 }
 
 }  // namespace

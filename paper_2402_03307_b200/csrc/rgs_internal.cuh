@@ -122,6 +122,8 @@ void splats_from_host(const void* splats, int n, const DevCamera& cam, const Spl
 // k_binning.cu
 int num_depth_buckets();
 bool binning_init();
+bool raster_init();  // k_raster.cu
+bool train_init();   // k_train.cu
 void exclusive_scan(const uint32_t* in, int n, uint32_t* out, uint32_t* scratch, uint32_t* total, cudaStream_t s,
                     const int* n_dev = nullptr);
 size_t scan1_scratch_words(int n);

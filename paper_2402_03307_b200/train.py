@@ -428,10 +428,13 @@ class Trainer:
             consistency(ctx, scene, self.nbrs, w.lambda_consistency, self.grads if want_grads else None,
                         self.losses[4:5])
 
-    def step(self, cams: Sequence[Camera], targets) -> LossBreakdown:
+    def step(self, cams: Sequence[Camera], targets, read: bool = True) -> Optional[LossBreakdown]:
         """One train_from iteration minus densification (trainer.cpp:115-150): SH unlock, batch
         loss + gradients, accumulate_stats, Adam, opacity reset and KNN rebuild schedules.
-        One host synchronisation: the loss scalars (and the rotor-error word) per step."""
+        ``read``: one host synchronisation per step for the loss scalars (and the rotor-error
+        word), as train_from's per-step loss check.  ``read=False`` only queues the copy of the
+        losses (no sync, so the next step's work is enqueued without a bubble); `last_losses()`
+        returns them and raises a deferred rotor error."""
         cfg, w = self.cfg, self.cfg.loss
         self.step_count += 1
         step = self.step_count
@@ -444,7 +447,12 @@ class Trainer:
         self.evaluate_loss(cams, targets, True)
         acfg = CAdamConfig.from_config(cfg, w.lambda_entropy, True)
         self.opt.step(self.grads, self.vnorm, self.visible, acfg, step, self.losses[3:4])
-        out = self.read_losses()
+        if read:
+            out = self.read_losses()
+        else:
+            self.ctx.fence()
+            self.losses_host.copy_(self.losses, non_blocking=True)
+            out = None
         mutated = False
         if (self.scene_extent is not None and cfg.densify_from <= step <= cfg.densify_until
                 and step % cfg.densify_interval == 0):
@@ -463,6 +471,10 @@ class Trainer:
     def read_losses(self) -> LossBreakdown:
         self.ctx.fence()
         self.losses_host.copy_(self.losses, non_blocking=True)
+        return self.last_losses()
+
+    def last_losses(self) -> LossBreakdown:
+        """The most recently queued loss copy (synchronises; raises pending rotor errors)."""
         self.opt.status()  # synchronises the stream; raises rotor errors
         h = self.losses_host.numpy()
         w = self.cfg.loss
