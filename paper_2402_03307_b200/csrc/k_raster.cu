@@ -26,7 +26,8 @@ struct StagedSplat {
 };
 
 template <bool FLOW>
-__device__ __forceinline__ void stage(const SplatArrays& sp, uint32_t id, double px0, double py0, StagedSplat* dst) {
+__device__ __forceinline__ void stage(const SplatArrays& sp, uint32_t id, double px0, double py0, StagedSplat* dst,
+                                      float* lmax = nullptr) {
     const double2 m = sp.mean2[id];
     const float mx = (float)(m.x - px0), my = (float)(m.y - py0);
     const float4 cf = sp.conic_f[id];
@@ -45,6 +46,14 @@ __device__ __forceinline__ void stage(const SplatArrays& sp, uint32_t id, double
     // 1 / (1 - alpha) <= 1 / (1 - min(0.99, ab)): the T-gate error bound without a reciprocal
     const float am = fminf(0.99f, cf.w);
     dst->d = make_float4(e.x, e.y, g.y, __fdiv_ru(1.f, __fsub_rd(1.f, am)) * 1.000001f);
+    if (lmax) {
+        // Largest eigenvalue of the (negative definite) log2-power form [[ca2, cb2/2], [cb2/2, cc2]]
+        // plus a slack far above its FP32 rounding: p2 <= lmax d^2 at Euclidean distance d from
+        // the mean.  Near-degenerate conics get lmax >= 0 (no culling from it).
+        const float h = 0.5f * (cf.x + cf.z), dd = 0.5f * (cf.x - cf.z), o = 0.5f * cf.y;
+        const float lm = h + sqrtf(fmaf(dd, dd, o * o));
+        *lmax = lm + 1e-5f * (fabsf(cf.x) + fabsf(cf.z) + fabsf(cf.y));
+    }
 }
 
 // Per-warp culling of a staged splat against the warp's 8x4 sub-tile with the bounding box
@@ -53,6 +62,16 @@ __device__ __forceinline__ void stage(const SplatArrays& sp, uint32_t id, double
 __device__ __forceinline__ bool overlaps(const StagedSplat& s, float sx0, float sy0) {
     return (s.a.x + s.d.x >= sx0) && (s.a.x - s.d.x <= sx0 + 7.f) && (s.a.y + s.d.y >= sy0) &&
            (s.a.y - s.d.y <= sy0 + 3.f);
+}
+// ... and a radial bound: p2 <= lmax d^2 with d the distance from the mean to the sub-tile's
+// pixel rectangle (shrunk by 1e-3 px).  With the error floor D and a 1e-3 margin below the
+// alpha threshold, every pixel of the sub-tile certainly skips the splat in FP64, so K5 and K6
+// (which cull identically) drop it without changing any gate decision.
+__device__ __forceinline__ bool overlaps_radial(const StagedSplat& s, float lmax, float sx0, float sy0) {
+    if (!overlaps(s, sx0, sy0)) return false;
+    const float ddx = fmaxf(fmaxf(sx0 - s.a.x, s.a.x - (sx0 + 7.f)) - 1e-3f, 0.f);
+    const float ddy = fmaxf(fmaxf(sy0 - s.a.y, s.a.y - (sy0 + 3.f)) - 1e-3f, 0.f);
+    return lmax * fmaf(ddx, ddx, ddy * ddy) >= s.b.z - s.b.y - 1e-3f;
 }
 
 enum { kSkip = 0, kAccept = 1, kAmbiguous = 2 };
@@ -106,6 +125,7 @@ __global__ void __launch_bounds__(256, 5) k_blend_fp32(SplatArrays sp, const uin
                                                     uint32_t* __restrict__ n_contrib, uint32_t* slow_list,
                                                     int* slow_count, unsigned long long* counters) {
     __shared__ StagedSplat sm[kTilePixels];
+    __shared__ float slm[kTilePixels];
     const int tile = blockIdx.x;
     const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -126,13 +146,13 @@ __global__ void __launch_bounds__(256, 5) k_blend_fp32(SplatArrays sp, const uin
     for (uint32_t start = rg.x; start < rg.y; start += kTilePixels) {
         if (__syncthreads_count(done) == kTilePixels) break;
         const uint32_t j = start + threadIdx.x;
-        if (j < rg.y) stage<FLOW>(sp, vals[j], px0, py0, &sm[threadIdx.x]);
+        if (j < rg.y) stage<FLOW>(sp, vals[j], px0, py0, &sm[threadIdx.x], &slm[threadIdx.x]);
         __syncthreads();
         const int n = (int)min((uint32_t)kTilePixels, rg.y - start);
         if (warp_done) continue;
         for (int c = 0; c < n; c += 32) {
             const int k0 = c + lane;
-            unsigned mask = __ballot_sync(kFull, k0 < n && overlaps(sm[k0], fsx0, fsy0));
+            unsigned mask = __ballot_sync(kFull, k0 < n && overlaps_radial(sm[k0], slm[k0], fsx0, fsy0));
             while (mask) {
                 const int k = c + __ffs(mask) - 1;
                 mask &= mask - 1;
@@ -267,7 +287,8 @@ __global__ void __launch_bounds__(256) k_backward_fp32(SplatArrays sp, const uin
     extern __shared__ float4 dyn_smem[];
     StagedSplat* sm = reinterpret_cast<StagedSplat*>(dyn_smem);                   // [kBwdBatch]
     uint32_t* sid = reinterpret_cast<uint32_t*>(sm + kBwdBatch);                   // [kBwdBatch]
-    float* accw = reinterpret_cast<float*>(sid + kBwdBatch);                       // [warps][batch][9]
+    float* slm = reinterpret_cast<float*>(sid + kBwdBatch);                        // [kBwdBatch]
+    float* accw = slm + kBwdBatch;                                                 // [warps][batch][9]
     __shared__ int s_max;
     const int tile = blockIdx.x;
     const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
@@ -313,14 +334,14 @@ __global__ void __launch_bounds__(256) k_backward_fp32(SplatArrays sp, const uin
         if ((int)threadIdx.x < cnt) {
             const uint32_t id = vals[rg.x + beg + threadIdx.x];
             sid[threadIdx.x] = id;
-            stage<false>(sp, id, px0, py0, &sm[threadIdx.x]);
+            stage<false>(sp, id, px0, py0, &sm[threadIdx.x], &slm[threadIdx.x]);
         }
         __syncthreads();
         if (beg < wmax) {
             for (int c = ((cnt - 1) >> 5) << 5; c >= 0; c -= 32) {
                 const int k0 = c + lane;
                 unsigned mask =
-                    __ballot_sync(kFull, k0 < cnt && beg + k0 < wmax && overlaps(sm[k0], fsx0, fsy0));
+                    __ballot_sync(kFull, k0 < cnt && beg + k0 < wmax && overlaps_radial(sm[k0], slm[k0], fsx0, fsy0));
                 while (mask) {
                     const int j = 31 - __clz(mask);
                     mask &= ~(1u << j);
@@ -397,7 +418,7 @@ __global__ void __launch_bounds__(256) k_backward_fp32(SplatArrays sp, const uin
     }
 }
 
-constexpr size_t kBwdSmem = sizeof(StagedSplat) * kBwdBatch + sizeof(uint32_t) * kBwdBatch +
+constexpr size_t kBwdSmem = sizeof(StagedSplat) * kBwdBatch + sizeof(uint32_t) * kBwdBatch + sizeof(float) * kBwdBatch +
                             sizeof(float) * kBwdWarps * kBwdBatch * 9;
 
 }  // namespace rgs_dev
