@@ -59,18 +59,20 @@ __device__ __forceinline__ void stage(const SplatArrays& sp, uint32_t id, double
 // Per-warp culling of a staged splat against the warp's 8x4 sub-tile with the bounding box
 // of its alpha >= 1/255 ellipse.  (An exact ellipse-rectangle test removed 19% of the
 // evaluations but cost more in the ballot phase than it saved: measured, round 1.)
+template <int H = 3>
 __device__ __forceinline__ bool overlaps(const StagedSplat& s, float sx0, float sy0) {
     return (s.a.x + s.d.x >= sx0) && (s.a.x - s.d.x <= sx0 + 7.f) && (s.a.y + s.d.y >= sy0) &&
-           (s.a.y - s.d.y <= sy0 + 3.f);
+           (s.a.y - s.d.y <= sy0 + (float)H);
 }
 // ... and a radial bound: p2 <= lmax d^2 with d the distance from the mean to the sub-tile's
 // pixel rectangle (shrunk by 1e-3 px).  With the error floor D and a 1e-3 margin below the
 // alpha threshold, every pixel of the sub-tile certainly skips the splat in FP64, so K5 and K6
 // (which cull identically) drop it without changing any gate decision.
+template <int H = 3>
 __device__ __forceinline__ bool overlaps_radial(const StagedSplat& s, float lmax, float sx0, float sy0) {
-    if (!overlaps(s, sx0, sy0)) return false;
+    if (!overlaps<H>(s, sx0, sy0)) return false;
     const float ddx = fmaxf(fmaxf(sx0 - s.a.x, s.a.x - (sx0 + 7.f)) - 1e-3f, 0.f);
-    const float ddy = fmaxf(fmaxf(sy0 - s.a.y, s.a.y - (sy0 + 3.f)) - 1e-3f, 0.f);
+    const float ddy = fmaxf(fmaxf(sy0 - s.a.y, s.a.y - (sy0 + (float)H)) - 1e-3f, 0.f);
     return lmax * fmaf(ddx, ddx, ddy * ddy) >= s.b.z - s.b.y - 1e-3f;
 }
 
@@ -270,20 +272,25 @@ __device__ __forceinline__ float reduce_scatter9(const float* v, int lane, int& 
     return r;
 }
 
-// K6: back-to-front replay of the FP32 pixels (rasterizer.cpp:320-397).  Splats are staged
-// kBwdBatch at a time.  Each warp reduce-scatters its per-splat partials and its owner lanes
+// K6: back-to-front replay of the FP32 pixels (rasterizer.cpp:320-397).  128 threads per tile,
+// each lane replays two pixels (rows y and y + 4 of its warp's 8x8 sub-tile), so the per-splat
+// loop overhead and the warp reduction are shared by 64 pixels.  Splats are staged kBwdBatch
+// at a time.  Each warp sums its lanes' two partials, reduce-scatters them and its owner lanes
 // store them with plain shared-memory stores into the warp's private slot (a warp visits a
 // staged splat at most once, so no atomics -- shared float atomics are CAS loops on this
-// architecture); after the batch the 8 warp slots are summed per (splat, component) and
+// architecture); after the batch the warp slots are summed per (splat, component) and
 // scattered with one FP64 atomic each.  Slow pixels are replayed in FP64 by k_backward_fp64.
+// The 8x8 cull is the union of K5's two 8x4 culls, so every pair K5 evaluated is evaluated
+// here with the same FP32 numbers and the same decision.
 constexpr int kBwdBatch = 128;
-constexpr int kBwdWarps = kTilePixels / 32;
+constexpr int kBwdThreads = 128;
+constexpr int kBwdWarps = kBwdThreads / 32;
 
-__global__ void __launch_bounds__(256) k_backward_fp32(SplatArrays sp, const uint32_t* __restrict__ vals,
-                                                       const uint2* __restrict__ ranges, DevCamera cam, float3 bg,
-                                                       const double* __restrict__ final_T,
-                                                       const uint32_t* __restrict__ n_contrib,
-                                                       const float* __restrict__ dL, double* sg) {
+__global__ void __launch_bounds__(kBwdThreads) k_backward_fp32(SplatArrays sp, const uint32_t* __restrict__ vals,
+                                                               const uint2* __restrict__ ranges, DevCamera cam,
+                                                               float3 bg, const double* __restrict__ final_T,
+                                                               const uint32_t* __restrict__ n_contrib,
+                                                               const float* __restrict__ dL, double* sg) {
     extern __shared__ float4 dyn_smem[];
     StagedSplat* sm = reinterpret_cast<StagedSplat*>(dyn_smem);                   // [kBwdBatch]
     uint32_t* sid = reinterpret_cast<uint32_t*>(sm + kBwdBatch);                   // [kBwdBatch]
@@ -293,37 +300,43 @@ __global__ void __launch_bounds__(256) k_backward_fp32(SplatArrays sp, const uin
     const int tile = blockIdx.x;
     const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int sx0 = (warp & 1) * 8, sy0 = (warp >> 1) * 4;
+    const int sx0 = (warp & 1) * 8, sy0 = (warp >> 1) * 8;
     const int lx = sx0 + (lane & 7), ly = sy0 + (lane >> 3);
-    const int px = tx * kTile + lx, py = ty * kTile + ly;
-    const bool inside = px < cam.width && py < cam.height;
-    const uint2 rg = ranges[tile];
     const double px0 = tx * kTile, py0 = ty * kTile;
-    const float fpx = (float)lx, fpy = (float)ly, fsx0 = (float)sx0, fsy0 = (float)sy0;
+    const uint2 rg = ranges[tile];
+    const float fpx = (float)lx, fsx0 = (float)sx0, fsy0 = (float)sy0;
     constexpr float kLn2 = 0.69314718055994531f;
     float* myacc = accw + (size_t)warp * kBwdBatch * 9;
 
-    int contrib = 0;
-    float T_run = 1.f, g0 = 0.f, g1 = 0.f, g2 = 0.f, s0 = 0.f, s1 = 0.f, s2 = 0.f;
+    int contrib[2];
+    float fpy[2], T_run[2], g0[2], g1[2], g2[2], s0[2], s1[2], s2[2];
     if (threadIdx.x == 0) s_max = 0;
-    for (int e = threadIdx.x; e < kBwdWarps * kBwdBatch * 9; e += kTilePixels) accw[e] = 0.f;
-    if (inside) {
-        const uint32_t pix = (uint32_t)py * cam.width + px;
-        const uint32_t c = n_contrib[pix];
-        if (!(c & kSlowBit)) {
-            contrib = (int)c;
-            const float fT = (float)final_T[pix];
-            T_run = fT;
-            g0 = dL[(size_t)pix * 3 + 0];
-            g1 = dL[(size_t)pix * 3 + 1];
-            g2 = dL[(size_t)pix * 3 + 2];
-            s0 = bg.x * fT;
-            s1 = bg.y * fT;
-            s2 = bg.z * fT;
+    for (int e = threadIdx.x; e < kBwdWarps * kBwdBatch * 9; e += kBwdThreads) accw[e] = 0.f;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int px = tx * kTile + lx, py = ty * kTile + ly + 4 * h;
+        fpy[h] = (float)(ly + 4 * h);
+        contrib[h] = 0;
+        T_run[h] = 1.f;
+        g0[h] = g1[h] = g2[h] = s0[h] = s1[h] = s2[h] = 0.f;
+        if (px < cam.width && py < cam.height) {
+            const uint32_t pix = (uint32_t)py * cam.width + px;
+            const uint32_t c = n_contrib[pix];
+            if (!(c & kSlowBit)) {
+                contrib[h] = (int)c;
+                const float fT = (float)final_T[pix];
+                T_run[h] = fT;
+                g0[h] = dL[(size_t)pix * 3 + 0];
+                g1[h] = dL[(size_t)pix * 3 + 1];
+                g2[h] = dL[(size_t)pix * 3 + 2];
+                s0[h] = bg.x * fT;
+                s1[h] = bg.y * fT;
+                s2[h] = bg.z * fT;
+            }
         }
     }
     __syncthreads();
-    const int wmax = __reduce_max_sync(kFull, contrib);
+    const int wmax = __reduce_max_sync(kFull, max(contrib[0], contrib[1]));
     if (lane == 0 && wmax > 0) atomicMax(&s_max, wmax);
     __syncthreads();
     const int max_contrib = s_max;
@@ -340,8 +353,8 @@ __global__ void __launch_bounds__(256) k_backward_fp32(SplatArrays sp, const uin
         if (beg < wmax) {
             for (int c = ((cnt - 1) >> 5) << 5; c >= 0; c -= 32) {
                 const int k0 = c + lane;
-                unsigned mask =
-                    __ballot_sync(kFull, k0 < cnt && beg + k0 < wmax && overlaps_radial(sm[k0], slm[k0], fsx0, fsy0));
+                unsigned mask = __ballot_sync(
+                    kFull, k0 < cnt && beg + k0 < wmax && overlaps_radial<7>(sm[k0], slm[k0], fsx0, fsy0));
                 while (mask) {
                     const int j = 31 - __clz(mask);
                     mask &= ~(1u << j);
@@ -350,41 +363,42 @@ __global__ void __launch_bounds__(256) k_backward_fp32(SplatArrays sp, const uin
 #pragma unroll
                     for (int q = 0; q < 9; ++q) v[q] = 0.f;
                     bool act = false;
-                    if (beg + k < contrib) {
-                        const float4 a = sm[k].a, b = sm[k].b;
+                    const float4 a = sm[k].a, b = sm[k].b;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        if (beg + k >= contrib[h]) continue;
                         float p, M, dx, dy;
                         // Non-slow pixels: every kept decision was certain in K5; an ambiguous
                         // value here means K5 culled the pair, whose FP64 decision is "skip".
-                        if (classify(a, b, fpx, fpy, p, M, dx, dy) == kAccept) {
-                            const float4 cc = sm[k].c;
-                            const float e = ex2_approx(p);
-                            const float al = fminf(0.99f, __fmul_rn(cc.w, e));
-                            const float om = 1.f - al;
-                            const float inv_om = rcp_approx(om);
-                            const float T_before = T_run * inv_om;
-                            const float w = al * T_before;
-                            v[0] = w * g0;
-                            v[1] = w * g1;
-                            v[2] = w * g2;
-                            const float dL_da = g0 * fmaf(cc.x, T_before, -s0 * inv_om) +
-                                                g1 * fmaf(cc.y, T_before, -s1 * inv_om) +
-                                                g2 * fmaf(cc.z, T_before, -s2 * inv_om);
-                            if (p <= sm[k].d.z) {  // unclamped alpha <= 0.99: al = ab * e
-                                const float A = -2.f * kLn2 * a.z, B = -kLn2 * a.w, C = -2.f * kLn2 * b.x;
-                                v[8] = dL_da * e;
-                                const float dp = dL_da * al;
-                                v[3] = dp * (-0.5f * dx * dx);
-                                v[4] = dp * (-dx * dy);
-                                v[5] = dp * (-0.5f * dy * dy);
-                                v[6] = dp * fmaf(A, dx, B * dy);
-                                v[7] = dp * fmaf(B, dx, C * dy);
-                            }
-                            s0 = fmaf(cc.x, w, s0);
-                            s1 = fmaf(cc.y, w, s1);
-                            s2 = fmaf(cc.z, w, s2);
-                            T_run = T_before;
-                            act = true;
+                        if (classify(a, b, fpx, fpy[h], p, M, dx, dy) != kAccept) continue;
+                        const float4 cc = sm[k].c;
+                        const float e = ex2_approx(p);
+                        const float al = fminf(0.99f, __fmul_rn(cc.w, e));
+                        const float om = 1.f - al;
+                        const float inv_om = rcp_approx(om);
+                        const float T_before = T_run[h] * inv_om;
+                        const float w = al * T_before;
+                        v[0] = fmaf(w, g0[h], v[0]);
+                        v[1] = fmaf(w, g1[h], v[1]);
+                        v[2] = fmaf(w, g2[h], v[2]);
+                        const float dL_da = g0[h] * fmaf(cc.x, T_before, -s0[h] * inv_om) +
+                                            g1[h] * fmaf(cc.y, T_before, -s1[h] * inv_om) +
+                                            g2[h] * fmaf(cc.z, T_before, -s2[h] * inv_om);
+                        if (p <= sm[k].d.z) {  // unclamped alpha <= 0.99: al = ab * e
+                            const float A = -2.f * kLn2 * a.z, B = -kLn2 * a.w, C = -2.f * kLn2 * b.x;
+                            v[8] = fmaf(dL_da, e, v[8]);
+                            const float dp = dL_da * al;
+                            v[3] = fmaf(dp, -0.5f * dx * dx, v[3]);
+                            v[4] = fmaf(dp, -dx * dy, v[4]);
+                            v[5] = fmaf(dp, -0.5f * dy * dy, v[5]);
+                            v[6] = fmaf(dp, fmaf(A, dx, B * dy), v[6]);
+                            v[7] = fmaf(dp, fmaf(B, dx, C * dy), v[7]);
                         }
+                        s0[h] = fmaf(cc.x, w, s0[h]);
+                        s1[h] = fmaf(cc.y, w, s1[h]);
+                        s2[h] = fmaf(cc.z, w, s2[h]);
+                        T_run[h] = T_before;
+                        act = true;
                     }
                     const unsigned am = __ballot_sync(kFull, act);
                     if (am == 0) continue;
@@ -404,7 +418,7 @@ __global__ void __launch_bounds__(256) k_backward_fp32(SplatArrays sp, const uin
             }
         }
         __syncthreads();
-        for (int e = threadIdx.x; e < cnt * 9; e += kTilePixels) {
+        for (int e = threadIdx.x; e < cnt * 9; e += kBwdThreads) {
             float sum = 0.f;
 #pragma unroll
             for (int w = 0; w < kBwdWarps; ++w) {
@@ -451,7 +465,7 @@ void backward_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2
                    float3 bg, const double* final_T, const uint32_t* n_contrib, const float* dL_dimage,
                    double* screen_grads, cudaStream_t s) {
     const int tiles = cam.tiles_x * cam.tiles_y;
-    k_backward_fp32<<<tiles, kTilePixels, kBwdSmem, s>>>(sp, pair_vals, ranges, cam, bg, final_T, n_contrib,
+    k_backward_fp32<<<tiles, kBwdThreads, kBwdSmem, s>>>(sp, pair_vals, ranges, cam, bg, final_T, n_contrib,
                                                          dL_dimage, screen_grads);
 }
 
