@@ -273,8 +273,9 @@ __device__ __forceinline__ float reduce_scatter9(const float* v, int lane, int& 
 }
 
 // K6: back-to-front replay of the FP32 pixels (rasterizer.cpp:320-397).  128 threads per tile,
-// each lane replays two pixels (rows y and y + 4 of its warp's 8x8 sub-tile), so the per-splat
-// loop overhead and the warp reduction are shared by 64 pixels.  Splats are staged kBwdBatch
+// each lane replays kBwdPx = 2 pixels (rows y and y + 4 of its warp's 8x8 sub-tile), so the
+// per-splat loop overhead and the warp reduction are shared by 64 pixels (measured: 2 pixels
+// 1.10 ms / C3 step, 1 pixel 1.36 ms, 4 pixels 1.28 ms; 48-register cap 1.25 ms).  Splats are staged kBwdBatch
 // at a time.  Each warp sums its lanes' two partials, reduce-scatters them and its owner lanes
 // store them with plain shared-memory stores into the warp's private slot (a warp visits a
 // staged splat at most once, so no atomics -- shared float atomics are CAS loops on this
@@ -282,8 +283,9 @@ __device__ __forceinline__ float reduce_scatter9(const float* v, int lane, int& 
 // scattered with one FP64 atomic each.  Slow pixels are replayed in FP64 by k_backward_fp64.
 // The 8x8 cull is the union of K5's two 8x4 culls, so every pair K5 evaluated is evaluated
 // here with the same FP32 numbers and the same decision.
-constexpr int kBwdBatch = 128;
-constexpr int kBwdThreads = 128;
+constexpr int kBwdBatch = 64;
+constexpr int kBwdPx = 2;                          // pixels per lane, rows y + 4 i
+constexpr int kBwdThreads = kTilePixels / kBwdPx;
 constexpr int kBwdWarps = kBwdThreads / 32;
 
 __global__ void __launch_bounds__(kBwdThreads) k_backward_fp32(SplatArrays sp, const uint32_t* __restrict__ vals,
@@ -300,7 +302,7 @@ __global__ void __launch_bounds__(kBwdThreads) k_backward_fp32(SplatArrays sp, c
     const int tile = blockIdx.x;
     const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int sx0 = (warp & 1) * 8, sy0 = (warp >> 1) * 8;
+    const int sx0 = (warp & 1) * 8, sy0 = (warp >> 1) * 4 * kBwdPx;
     const int lx = sx0 + (lane & 7), ly = sy0 + (lane >> 3);
     const double px0 = tx * kTile, py0 = ty * kTile;
     const uint2 rg = ranges[tile];
@@ -308,12 +310,13 @@ __global__ void __launch_bounds__(kBwdThreads) k_backward_fp32(SplatArrays sp, c
     constexpr float kLn2 = 0.69314718055994531f;
     float* myacc = accw + (size_t)warp * kBwdBatch * 9;
 
-    int contrib[2];
-    float fpy[2], T_run[2], g0[2], g1[2], g2[2], s0[2], s1[2], s2[2];
+    int contrib[kBwdPx];
+    float fpy[kBwdPx], T_run[kBwdPx], g0[kBwdPx], g1[kBwdPx], g2[kBwdPx], s0[kBwdPx], s1[kBwdPx], s2[kBwdPx];
     if (threadIdx.x == 0) s_max = 0;
     for (int e = threadIdx.x; e < kBwdWarps * kBwdBatch * 9; e += kBwdThreads) accw[e] = 0.f;
+    int cmax = 0;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < kBwdPx; ++h) {
         const int px = tx * kTile + lx, py = ty * kTile + ly + 4 * h;
         fpy[h] = (float)(ly + 4 * h);
         contrib[h] = 0;
@@ -334,9 +337,10 @@ __global__ void __launch_bounds__(kBwdThreads) k_backward_fp32(SplatArrays sp, c
                 s2[h] = bg.z * fT;
             }
         }
+        cmax = max(cmax, contrib[h]);
     }
     __syncthreads();
-    const int wmax = __reduce_max_sync(kFull, max(contrib[0], contrib[1]));
+    const int wmax = __reduce_max_sync(kFull, cmax);
     if (lane == 0 && wmax > 0) atomicMax(&s_max, wmax);
     __syncthreads();
     const int max_contrib = s_max;
@@ -344,17 +348,17 @@ __global__ void __launch_bounds__(kBwdThreads) k_backward_fp32(SplatArrays sp, c
     for (int end = max_contrib; end > 0; end -= kBwdBatch) {
         const int beg = end > kBwdBatch ? end - kBwdBatch : 0;
         const int cnt = end - beg;
-        if ((int)threadIdx.x < cnt) {
-            const uint32_t id = vals[rg.x + beg + threadIdx.x];
-            sid[threadIdx.x] = id;
-            stage<false>(sp, id, px0, py0, &sm[threadIdx.x], &slm[threadIdx.x]);
+        for (int q = threadIdx.x; q < cnt; q += kBwdThreads) {
+            const uint32_t id = vals[rg.x + beg + q];
+            sid[q] = id;
+            stage<false>(sp, id, px0, py0, &sm[q], &slm[q]);
         }
         __syncthreads();
         if (beg < wmax) {
             for (int c = ((cnt - 1) >> 5) << 5; c >= 0; c -= 32) {
                 const int k0 = c + lane;
                 unsigned mask = __ballot_sync(
-                    kFull, k0 < cnt && beg + k0 < wmax && overlaps_radial<7>(sm[k0], slm[k0], fsx0, fsy0));
+                    kFull, k0 < cnt && beg + k0 < wmax && overlaps_radial<4 * kBwdPx - 1>(sm[k0], slm[k0], fsx0, fsy0));
                 while (mask) {
                     const int j = 31 - __clz(mask);
                     mask &= ~(1u << j);
@@ -365,7 +369,7 @@ __global__ void __launch_bounds__(kBwdThreads) k_backward_fp32(SplatArrays sp, c
                     bool act = false;
                     const float4 a = sm[k].a, b = sm[k].b;
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
+                    for (int h = 0; h < kBwdPx; ++h) {
                         if (beg + k >= contrib[h]) continue;
                         float p, M, dx, dy;
                         // Non-slow pixels: every kept decision was certain in K5; an ambiguous
