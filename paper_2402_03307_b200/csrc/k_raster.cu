@@ -275,30 +275,28 @@ __device__ __forceinline__ float reduce_scatter9(const float* v, int lane, int& 
 // K6: back-to-front replay of the FP32 pixels (rasterizer.cpp:320-397).  128 threads per tile,
 // each lane replays kBwdPx = 2 pixels (rows y and y + 4 of its warp's 8x8 sub-tile), so the
 // per-splat loop overhead and the warp reduction are shared by 64 pixels (measured: 2 pixels
-// 1.10 ms / C3 step, 1 pixel 1.36 ms, 4 pixels 1.28 ms; 48-register cap 1.25 ms).  Splats are staged kBwdBatch
-// at a time.  Each warp sums its lanes' two partials, reduce-scatters them and its owner lanes
-// store them with plain shared-memory stores into the warp's private slot (a warp visits a
-// staged splat at most once, so no atomics -- shared float atomics are CAS loops on this
-// architecture); after the batch the warp slots are summed per (splat, component) and
-// scattered with one FP64 atomic each.  Slow pixels are replayed in FP64 by k_backward_fp64.
-// The 8x8 cull is the union of K5's two 8x4 culls, so every pair K5 evaluated is evaluated
-// here with the same FP32 numbers and the same decision.
-constexpr int kBwdBatch = 64;
-constexpr int kBwdPx = 2;                          // pixels per lane, rows y + 4 i
+// 1.10 ms / C3 step, 1 pixel 1.36 ms, 4 pixels 1.28 ms; 48-register cap 1.25 ms).  Warps are
+// independent: each stages its own 32-splat windows (no block barriers -- a block-shared
+// staging with per-warp shared-memory slots summed per batch measured the same), sums its
+// lanes' two partials, reduce-scatters them across the warp and the 9 owner lanes issue one
+// FP64 atomic each.  Slow pixels are replayed in FP64 by k_backward_fp64.  The 8x8 cull is
+// the union of K5's two 8x4 culls, so every pair K5 evaluated is evaluated here with the same
+// FP32 numbers and the same decision.
+//
+// Per pixel the colour terms fold into scalars: with G = sum_c dL/dc_c * colour_c (per pair)
+// and S = sum_c dL/dc_c * s_c (per pixel, s = colour accumulated behind the splat),
+// dL/dalpha = T_before G - S / (1 - alpha) and S += w G.
+constexpr int kBwdPx = 2;  // pixels per lane, rows y + 4 i
 constexpr int kBwdThreads = kTilePixels / kBwdPx;
 constexpr int kBwdWarps = kBwdThreads / 32;
 
 __global__ void __launch_bounds__(kBwdThreads) k_backward_fp32(SplatArrays sp, const uint32_t* __restrict__ vals,
-                                                               const uint2* __restrict__ ranges, DevCamera cam,
-                                                               float3 bg, const double* __restrict__ final_T,
-                                                               const uint32_t* __restrict__ n_contrib,
-                                                               const float* __restrict__ dL, double* sg) {
-    extern __shared__ float4 dyn_smem[];
-    StagedSplat* sm = reinterpret_cast<StagedSplat*>(dyn_smem);                   // [kBwdBatch]
-    uint32_t* sid = reinterpret_cast<uint32_t*>(sm + kBwdBatch);                   // [kBwdBatch]
-    float* slm = reinterpret_cast<float*>(sid + kBwdBatch);                        // [kBwdBatch]
-    float* accw = slm + kBwdBatch;                                                 // [warps][batch][9]
-    __shared__ int s_max;
+                                                                const uint2* __restrict__ ranges, DevCamera cam,
+                                                                float3 bg, const double* __restrict__ final_T,
+                                                                const uint32_t* __restrict__ n_contrib,
+                                                                const float* __restrict__ dL, double* sg) {
+    __shared__ StagedSplat smw[kBwdWarps][32];
+    __shared__ float slmw[kBwdWarps][32];
     const int tile = blockIdx.x;
     const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -308,12 +306,11 @@ __global__ void __launch_bounds__(kBwdThreads) k_backward_fp32(SplatArrays sp, c
     const uint2 rg = ranges[tile];
     const float fpx = (float)lx, fsx0 = (float)sx0, fsy0 = (float)sy0;
     constexpr float kLn2 = 0.69314718055994531f;
-    float* myacc = accw + (size_t)warp * kBwdBatch * 9;
+    StagedSplat* sm = smw[warp];
+    float* slm = slmw[warp];
 
     int contrib[kBwdPx];
-    float fpy[kBwdPx], T_run[kBwdPx], g0[kBwdPx], g1[kBwdPx], g2[kBwdPx], s0[kBwdPx], s1[kBwdPx], s2[kBwdPx];
-    if (threadIdx.x == 0) s_max = 0;
-    for (int e = threadIdx.x; e < kBwdWarps * kBwdBatch * 9; e += kBwdThreads) accw[e] = 0.f;
+    float fpy[kBwdPx], T_run[kBwdPx], g0[kBwdPx], g1[kBwdPx], g2[kBwdPx], S[kBwdPx];
     int cmax = 0;
 #pragma unroll
     for (int h = 0; h < kBwdPx; ++h) {
@@ -321,7 +318,7 @@ __global__ void __launch_bounds__(kBwdThreads) k_backward_fp32(SplatArrays sp, c
         fpy[h] = (float)(ly + 4 * h);
         contrib[h] = 0;
         T_run[h] = 1.f;
-        g0[h] = g1[h] = g2[h] = s0[h] = s1[h] = s2[h] = 0.f;
+        g0[h] = g1[h] = g2[h] = S[h] = 0.f;
         if (px < cam.width && py < cam.height) {
             const uint32_t pix = (uint32_t)py * cam.width + px;
             const uint32_t c = n_contrib[pix];
@@ -332,112 +329,81 @@ __global__ void __launch_bounds__(kBwdThreads) k_backward_fp32(SplatArrays sp, c
                 g0[h] = dL[(size_t)pix * 3 + 0];
                 g1[h] = dL[(size_t)pix * 3 + 1];
                 g2[h] = dL[(size_t)pix * 3 + 2];
-                s0[h] = bg.x * fT;
-                s1[h] = bg.y * fT;
-                s2[h] = bg.z * fT;
+                S[h] = fmaf(g0[h], bg.x * fT, fmaf(g1[h], bg.y * fT, g2[h] * (bg.z * fT)));
             }
         }
         cmax = max(cmax, contrib[h]);
     }
-    __syncthreads();
     const int wmax = __reduce_max_sync(kFull, cmax);
-    if (lane == 0 && wmax > 0) atomicMax(&s_max, wmax);
-    __syncthreads();
-    const int max_contrib = s_max;
 
-    for (int end = max_contrib; end > 0; end -= kBwdBatch) {
-        const int beg = end > kBwdBatch ? end - kBwdBatch : 0;
+    for (int end = wmax; end > 0; end -= 32) {
+        const int beg = end > 32 ? end - 32 : 0;
         const int cnt = end - beg;
-        for (int q = threadIdx.x; q < cnt; q += kBwdThreads) {
-            const uint32_t id = vals[rg.x + beg + q];
-            sid[q] = id;
-            stage<false>(sp, id, px0, py0, &sm[q], &slm[q]);
+        uint32_t myid = 0;
+        __syncwarp();
+        if (lane < cnt) {
+            myid = vals[rg.x + beg + lane];
+            stage<false>(sp, myid, px0, py0, &sm[lane], &slm[lane]);
         }
-        __syncthreads();
-        if (beg < wmax) {
-            for (int c = ((cnt - 1) >> 5) << 5; c >= 0; c -= 32) {
-                const int k0 = c + lane;
-                unsigned mask = __ballot_sync(
-                    kFull, k0 < cnt && beg + k0 < wmax && overlaps_radial<4 * kBwdPx - 1>(sm[k0], slm[k0], fsx0, fsy0));
-                while (mask) {
-                    const int j = 31 - __clz(mask);
-                    mask &= ~(1u << j);
-                    const int k = c + j;
-                    float v[9];
+        __syncwarp();
+        unsigned mask = __ballot_sync(kFull, lane < cnt && overlaps_radial<4 * kBwdPx - 1>(sm[lane], slm[lane], fsx0, fsy0));
+        while (mask) {
+            const int k = 31 - __clz(mask);
+            mask &= ~(1u << k);
+            float v[9];
 #pragma unroll
-                    for (int q = 0; q < 9; ++q) v[q] = 0.f;
-                    bool act = false;
-                    const float4 a = sm[k].a, b = sm[k].b;
+            for (int q = 0; q < 9; ++q) v[q] = 0.f;
+            bool act = false;
+            const float4 a = sm[k].a, b = sm[k].b;
 #pragma unroll
-                    for (int h = 0; h < kBwdPx; ++h) {
-                        if (beg + k >= contrib[h]) continue;
-                        float p, M, dx, dy;
-                        // Non-slow pixels: every kept decision was certain in K5; an ambiguous
-                        // value here means K5 culled the pair, whose FP64 decision is "skip".
-                        if (classify(a, b, fpx, fpy[h], p, M, dx, dy) != kAccept) continue;
-                        const float4 cc = sm[k].c;
-                        const float e = ex2_approx(p);
-                        const float al = fminf(0.99f, __fmul_rn(cc.w, e));
-                        const float om = 1.f - al;
-                        const float inv_om = rcp_approx(om);
-                        const float T_before = T_run[h] * inv_om;
-                        const float w = al * T_before;
-                        v[0] = fmaf(w, g0[h], v[0]);
-                        v[1] = fmaf(w, g1[h], v[1]);
-                        v[2] = fmaf(w, g2[h], v[2]);
-                        const float dL_da = g0[h] * fmaf(cc.x, T_before, -s0[h] * inv_om) +
-                                            g1[h] * fmaf(cc.y, T_before, -s1[h] * inv_om) +
-                                            g2[h] * fmaf(cc.z, T_before, -s2[h] * inv_om);
-                        if (p <= sm[k].d.z) {  // unclamped alpha <= 0.99: al = ab * e
-                            const float A = -2.f * kLn2 * a.z, B = -kLn2 * a.w, C = -2.f * kLn2 * b.x;
-                            v[8] = fmaf(dL_da, e, v[8]);
-                            const float dp = dL_da * al;
-                            v[3] = fmaf(dp, -0.5f * dx * dx, v[3]);
-                            v[4] = fmaf(dp, -dx * dy, v[4]);
-                            v[5] = fmaf(dp, -0.5f * dy * dy, v[5]);
-                            v[6] = fmaf(dp, fmaf(A, dx, B * dy), v[6]);
-                            v[7] = fmaf(dp, fmaf(B, dx, C * dy), v[7]);
-                        }
-                        s0[h] = fmaf(cc.x, w, s0[h]);
-                        s1[h] = fmaf(cc.y, w, s1[h]);
-                        s2[h] = fmaf(cc.z, w, s2[h]);
-                        T_run[h] = T_before;
-                        act = true;
-                    }
-                    const unsigned am = __ballot_sync(kFull, act);
-                    if (am == 0) continue;
-                    float* slot = myacc + (size_t)k * 9;
-                    if (__popc(am) == 1) {
-                        if (act) {
-#pragma unroll
-                            for (int q = 0; q < 9; ++q) slot[q] = v[q];
-                        }
-                    } else {
-                        int idx;
-                        bool ok;
-                        const float r = reduce_scatter9(v, lane, idx, ok);
-                        if (ok && !(lane & 1)) slot[idx] = r;
-                    }
+            for (int h = 0; h < kBwdPx; ++h) {
+                if (beg + k >= contrib[h]) continue;
+                float p, M, dx, dy;
+                if (classify(a, b, fpx, fpy[h], p, M, dx, dy) != kAccept) continue;
+                const float4 cc = sm[k].c;
+                const float e = ex2_approx(p);
+                const float al = fminf(0.99f, __fmul_rn(cc.w, e));
+                const float om = 1.f - al;
+                const float inv_om = rcp_approx(om);
+                const float T_before = T_run[h] * inv_om;
+                const float w = al * T_before;
+                v[0] = fmaf(w, g0[h], v[0]);
+                v[1] = fmaf(w, g1[h], v[1]);
+                v[2] = fmaf(w, g2[h], v[2]);
+                const float G = fmaf(g0[h], cc.x, fmaf(g1[h], cc.y, g2[h] * cc.z));
+                const float dL_da = fmaf(T_before, G, -S[h] * inv_om);
+                if (p <= sm[k].d.z) {  // unclamped alpha <= 0.99: al = ab * e
+                    const float A = -2.f * kLn2 * a.z, B = -kLn2 * a.w, C = -2.f * kLn2 * b.x;
+                    v[8] = fmaf(dL_da, e, v[8]);
+                    const float dp = dL_da * al;
+                    v[3] = fmaf(dp, -0.5f * dx * dx, v[3]);
+                    v[4] = fmaf(dp, -dx * dy, v[4]);
+                    v[5] = fmaf(dp, -0.5f * dy * dy, v[5]);
+                    v[6] = fmaf(dp, fmaf(A, dx, B * dy), v[6]);
+                    v[7] = fmaf(dp, fmaf(B, dx, C * dy), v[7]);
                 }
+                S[h] = fmaf(w, G, S[h]);
+                T_run[h] = T_before;
+                act = true;
             }
-        }
-        __syncthreads();
-        for (int e = threadIdx.x; e < cnt * 9; e += kBwdThreads) {
-            float sum = 0.f;
+            const unsigned am = __ballot_sync(kFull, act);
+            if (am == 0) continue;
+            double* o = sg + (size_t)__shfl_sync(kFull, myid, k) * 9;
+            if (__popc(am) == 1) {
+                if (act) {
 #pragma unroll
-            for (int w = 0; w < kBwdWarps; ++w) {
-                float* pw = accw + (size_t)w * kBwdBatch * 9 + e;
-                sum += *pw;
-                *pw = 0.f;
+                    for (int q = 0; q < 9; ++q)
+                        if (v[q] != 0.f) atomicAdd(o + q, (double)v[q]);
+                }
+            } else {
+                int idx;
+                bool ok;
+                const float r = reduce_scatter9(v, lane, idx, ok);
+                if (ok && !(lane & 1) && r != 0.f) atomicAdd(o + idx, (double)r);
             }
-            if (sum != 0.f) atomicAdd(sg + (size_t)sid[e / 9] * 9 + (e % 9), (double)sum);
         }
-        __syncthreads();
     }
 }
-
-constexpr size_t kBwdSmem = sizeof(StagedSplat) * kBwdBatch + sizeof(uint32_t) * kBwdBatch + sizeof(float) * kBwdBatch +
-                            sizeof(float) * kBwdWarps * kBwdBatch * 9;
 
 }  // namespace rgs_dev
 
@@ -460,17 +426,14 @@ void blend_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* r
 }
 
 // Per-device kernel attributes (called from rgs_ctx_create on the context's device).
-bool raster_init() {
-    return cudaFuncSetAttribute(k_backward_fp32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSmem) ==
-           cudaSuccess;
-}
+bool raster_init() { return true; }
 
 void backward_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges, const DevCamera& cam,
                    float3 bg, const double* final_T, const uint32_t* n_contrib, const float* dL_dimage,
                    double* screen_grads, cudaStream_t s) {
     const int tiles = cam.tiles_x * cam.tiles_y;
-    k_backward_fp32<<<tiles, kBwdThreads, kBwdSmem, s>>>(sp, pair_vals, ranges, cam, bg, final_T, n_contrib,
-                                                         dL_dimage, screen_grads);
+    k_backward_fp32<<<tiles, kBwdThreads, 0, s>>>(sp, pair_vals, ranges, cam, bg, final_T, n_contrib, dL_dimage,
+                                                  screen_grads);
 }
 
 }  // namespace rgs_launch
