@@ -384,22 +384,26 @@ def run_train_leg(args, ctx, dev, dist, rank, world, flush):
     # e2e: the same steps through the public API with each step's target images copied
     # H2D from pinned host memory and the loss scalars read back (Trainer.step's D2H).
     host_t = targets.cpu().pin_memory()
-    dev_t = torch.empty((B, TRAIN_H, TRAIN_W, 3), dtype=torch.float32, device=dev)
+    stager = train.TargetStager(dev, B, TRAIN_H, TRAIN_W)
+    views = lambda k: [(k * B + j) % TRAIN_VIEWS for j in range(B)]  # noqa: E731
     if dist:
         dist.barrier()
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
+    stager.put([host_t[i] for i in views(0)])
     for k in range(args.train_steps):
-        idx = [(k * B + j) % TRAIN_VIEWS for j in range(B)]
-        for j, i in enumerate(idx):
-            dev_t[j].copy_(host_t[i], non_blocking=True)
-        tr.step([cams[i] for i in idx], [dev_t[j] for j in range(B)])
+        tg = stager.take()
+        if k + 1 < args.train_steps:  # the next step's targets cross PCIe during this step
+            stager.put([host_t[i] for i in views(k + 1)])
+        tr.step([cams[i] for i in views(k)], tg)
+        stager.release(ctx)
     torch.cuda.synchronize(dev)
     e2e_s = max_over_ranks(time.perf_counter() - t0, dist, dev)
     e2e = {"value": args.train_steps / e2e_s, "unit": "it/s", "h2d_bytes_per_step": int(B * TRAIN_H * TRAIN_W * 12),
            "d2h_bytes_per_step": 64, "steps": args.train_steps,
-           "note": "Trainer.step with the batch's target images H2D from pinned host memory each step and the "
-                   "loss scalars D2H (one host sync per step)"}
+           "note": "Trainer.step with the batch's target images H2D from pinned host memory each step "
+                   "(train.TargetStager: step k+1's copy overlaps step k) and the loss scalars D2H "
+                   "(one host sync per step)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

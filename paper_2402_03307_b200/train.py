@@ -316,6 +316,76 @@ def allreduce_step_buffers(gbuf, visible, losses_img, dist=None):
     dist.all_reduce(losses_img)
 
 
+class TargetStager:
+    """Double-buffered host -> device staging of a step's target images on a copy stream, so
+    the PCIe transfer of step k+1 overlaps the compute of step k.  (The reference keeps its
+    dataset in host memory and reads the images in place, dataset.cpp / trainer.cpp:22-84; on
+    the GPU every step's targets cross PCIe once.)
+
+    ``put(host_images)`` queues the copies of one step (pinned host tensors of shape (H, W, 3),
+    float32); ``take()`` returns that step's device views and orders torch's current stream
+    after their copy; ``release()`` -- after the step that consumed them is enqueued -- lets
+    the buffer be refilled."""
+
+    def __init__(self, device, batch: int, height: int, width: int, depth: int = 2):
+        import collections
+
+        import torch
+
+        self.device = torch.device(device)
+        self.bufs = [torch.empty((batch, height, width, 3), dtype=torch.float32, device=self.device)
+                     for _ in range(depth)]
+        self.ready = [None] * depth
+        self.free = [None] * depth
+        self.stream = torch.cuda.Stream(self.device)
+        self.queue = collections.deque()
+        self.next = 0
+        self.taken = None
+        self.bytes_per_put = 0
+
+    def put(self, host_images) -> None:
+        import torch
+
+        if len(self.queue) >= len(self.bufs):
+            raise RuntimeError("TargetStager: every buffer is queued; take() one first")
+        i = self.next
+        if i == self.taken:
+            raise RuntimeError("TargetStager: release() the taken buffer before refilling it")
+        if len(host_images) > self.bufs[i].shape[0]:
+            raise ValueError("TargetStager: more images than the batch size")
+        self.next = (i + 1) % len(self.bufs)
+        with torch.cuda.stream(self.stream):
+            if self.free[i] is not None:
+                self.stream.wait_event(self.free[i])
+            nbytes = 0
+            for j, h in enumerate(host_images):
+                self.bufs[i][j].copy_(h, non_blocking=True)
+                nbytes += h.numel() * h.element_size()
+            self.ready[i] = self.stream.record_event()
+        self.bytes_per_put = nbytes
+        self.queue.append((i, len(host_images)))
+
+    def take(self):
+        import torch
+
+        if self.taken is not None:
+            raise RuntimeError("TargetStager: release() the previous batch first")
+        i, n = self.queue.popleft()
+        torch.cuda.current_stream(self.device).wait_event(self.ready[i])
+        self.taken = i
+        return [self.bufs[i][j] for j in range(n)]
+
+    def release(self, ctx: Optional[Context] = None) -> None:
+        import torch
+
+        if self.taken is None:
+            return
+        if ctx is not None:
+            ctx.fence()
+        self.free[self.taken] = torch.cuda.current_stream(self.device).record_event()
+        self.taken = None
+
+
 class Trainer:
     """evaluate_loss + accumulate_stats + adam_step of train_from (trainer.cpp:121-150) on a
     device-resident scene.  ``dist``: torch.distributed (initialised) for the multi-GPU

@@ -433,6 +433,46 @@ def test_trainer_overlap_matches_serial(ctx):
     assert np.abs(g0 - g1).max() <= 1e-5 * scale
 
 
+def test_target_stager_pipeline(ctx):
+    """train.TargetStager: step k+1's targets copied during step k arrive intact, and the
+    staged steps give the losses of the same steps fed straight from device tensors."""
+    import torch
+
+    store, truth, cams = _training_case(n=3000, views=4)
+    tctx = rgs.Context(0)
+    tsc = DeviceScene.from_store(tctx, truth)
+    dev_t = [tctx.render_forward_device(tsc, c, retain=False)[0].clone() for c in cams]
+    torch.cuda.synchronize()
+    host = [t.cpu().pin_memory() for t in dev_t]
+    batches = [[0, 1], [2, 3], [1, 2], [3, 0], [0, 2]]
+    out = []
+    for staged in (False, True):
+        sc = DeviceScene.from_store(tctx, store)
+        tr = train.Trainer(tctx, sc, train.TrainConfig(batch=2))
+        st = train.TargetStager(0, 2, host[0].shape[0], host[0].shape[1])
+        losses = []
+        if staged:
+            st.put([host[i] for i in batches[0]])
+        for k, b in enumerate(batches):
+            if staged:
+                tg = st.take()
+                if k + 1 < len(batches):
+                    st.put([host[i] for i in batches[k + 1]])
+                for t, i in zip(tg, b):
+                    assert torch.equal(t, dev_t[i])
+            else:
+                tg = [dev_t[i] for i in b]
+            losses.append(tr.step([cams[i] for i in b], tg).total)
+            if staged:
+                st.release(tctx)
+        out.append(losses)
+    assert np.allclose(out[0], out[1], rtol=1e-6, atol=0)  # FP64-atomic order only
+    st = train.TargetStager(0, 1, 4, 4, depth=1)
+    st.put([torch.zeros((4, 4, 3)).pin_memory()])
+    with pytest.raises(RuntimeError):
+        st.put([torch.zeros((4, 4, 3)).pin_memory()])
+
+
 def test_render_views_host_matches_device(ctx):
     """The e2e entry point (host scene in, host images out) renders what the device path does."""
     import torch
