@@ -984,7 +984,7 @@ namespace {
 // `copy_out` (optional) is called after each view is enqueued on its slot stream.
 template <typename CopyOut>
 int render_batch(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* cams, int n_views, const double bg[3],
-                 unsigned flags, float* (*image_for)(void*, int, int), void* user, CopyOut&& copy_out) {
+                 unsigned flags, float* (*image_for)(void*, int, cudaStream_t), void* user, CopyOut&& copy_out) {
     for (int v = 0; v < n_views; ++v) {
         const int rc = validate_camera(c, &cams[v]);
         if (rc) return rc;
@@ -1000,7 +1000,7 @@ int render_batch(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* cams, int
         const int k = v % slots;
         cudaStream_t s = c->slot_stream[k];
         const int rc = run_forward(c, c->slot_frame[k], s, kFromScene, scene, nullptr, 0, true, &cams[v], bg,
-                                   flags & ~RGS_FLAG_HOST_BUFFERS, image_for(user, v, k), false, false,
+                                   flags & ~RGS_FLAG_HOST_BUFFERS, image_for(user, v, s), false, false,
                                    &c->view_stats[v]);
         if (rc) return rc;
         copy_out(v, k, s);
@@ -1023,7 +1023,8 @@ int render_batch(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* cams, int
         Frame& f = c->slot_frame[0];
         f.pair_cap = std::max<long long>(f.pair_cap, (long long)c->view_stats[v].n_pairs * 5 / 4 + 1024);
         const int rc = run_forward(c, f, c->stream, kFromScene, scene, nullptr, 0, true, &cams[v], bg,
-                                   flags & ~RGS_FLAG_HOST_BUFFERS, image_for(user, v, 0), false, true, nullptr);
+                                   flags & ~RGS_FLAG_HOST_BUFFERS, image_for(user, v, c->stream), false, true,
+                                   nullptr);
         if (rc) return rc;
         copy_out(v, 0, c->stream);
         CK(cudaStreamSynchronize(c->stream));
@@ -1035,7 +1036,7 @@ struct DeviceImages {
     float* base;
     size_t per;
 };
-float* device_image_for(void* u, int v, int) {
+float* device_image_for(void* u, int v, cudaStream_t) {
     DeviceImages* d = static_cast<DeviceImages*>(u);
     return d->base + d->per * (size_t)v;
 }
@@ -1070,32 +1071,37 @@ int rgs_render_views_host(rgs_ctx* c, int n, int sh_degree, const float* mean, c
         return rc;
     }
     rc = guarded(c, [&]() -> int {
-        // One device image per slot; each rendered view is copied to the host on the
-        // copy stream while the slot moves on (it waits for the copy before reuse).
+        // A ring of 2 x kSlots device images: view v renders into img[v % R] once the copy of
+        // view v - R out of it is done, and is copied to the host on the copy stream while
+        // the slot moves on to its next view (which no longer waits for this copy).
+        constexpr int R = 2 * rgs_ctx::kSlots;
         const size_t per = (size_t)cams[0].width * cams[0].height * 3;
-        struct Slots {
-            DevBuf img[rgs_ctx::kSlots];
-            cudaEvent_t rendered[rgs_ctx::kSlots], copied[rgs_ctx::kSlots];
+        struct Ring {
+            DevBuf img[R];
+            cudaEvent_t rendered[R], copied[R];
         } sl;
-        for (int k = 0; k < rgs_ctx::kSlots; ++k) {
+        for (int k = 0; k < R; ++k) {
             sl.img[k].ensure(per * sizeof(float), c->stream);
             CK(cudaEventCreateWithFlags(&sl.rendered[k], cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&sl.copied[k], cudaEventDisableTiming));
-            CK(cudaEventRecord(sl.copied[k], c->copy_stream));
-            CK(cudaStreamWaitEvent(c->slot_stream[k], sl.copied[k], 0));
+            CK(cudaEventRecord(sl.copied[k], c->stream));  // after the allocations
         }
-        auto image_for = [](void* u, int, int k) -> float* { return static_cast<Slots*>(u)->img[k].as<float>(); };
-        const int r = render_batch(c, scene, cams, n_views, bg, 0, image_for, &sl, [&](int v, int k, cudaStream_t s) {
-            CK(cudaEventRecord(sl.rendered[k], s));
-            CK(cudaStreamWaitEvent(c->copy_stream, sl.rendered[k], 0));
-            CK(cudaMemcpyAsync(images_host + per * (size_t)v, sl.img[k].p, per * sizeof(float),
+        auto image_for = [](void* u, int v, cudaStream_t s) -> float* {
+            Ring* r = static_cast<Ring*>(u);
+            CK(cudaStreamWaitEvent(s, r->copied[v % R], 0));
+            return r->img[v % R].as<float>();
+        };
+        const int r = render_batch(c, scene, cams, n_views, bg, 0, image_for, &sl, [&](int v, int, cudaStream_t s) {
+            const int q = v % R;
+            CK(cudaEventRecord(sl.rendered[q], s));
+            CK(cudaStreamWaitEvent(c->copy_stream, sl.rendered[q], 0));
+            CK(cudaMemcpyAsync(images_host + per * (size_t)v, sl.img[q].p, per * sizeof(float),
                                cudaMemcpyDeviceToHost, c->copy_stream));
-            CK(cudaEventRecord(sl.copied[k], c->copy_stream));
-            CK(cudaStreamWaitEvent(s, sl.copied[k], 0));  // the slot's next view reuses img[k]
+            CK(cudaEventRecord(sl.copied[q], c->copy_stream));
         });
         CK(cudaStreamSynchronize(c->copy_stream));
         CK(cudaStreamSynchronize(c->stream));
-        for (int k = 0; k < rgs_ctx::kSlots; ++k) {
+        for (int k = 0; k < R; ++k) {
             sl.img[k].release(c->stream);
             cudaEventDestroy(sl.rendered[k]);
             cudaEventDestroy(sl.copied[k]);

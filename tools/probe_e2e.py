@@ -25,7 +25,7 @@ f32 = store.arrays_f32()
 pinned = [torch.from_numpy(a).pin_memory() for a in f32]
 host = torch.empty((300, H, W, 3), dtype=torch.float32, pin_memory=True)
 host.zero_()  # touch pages
-for rep in range(3):
+for rep in range(6):
     t = time.perf_counter()
     ctx.render_views_host([p.numpy() for p in pinned], 3, cams, (0, 0, 0), host.numpy())
     print("host sweep 300 rep", rep, "%.1f ms" % (1e3 * (time.perf_counter() - t)))
