@@ -408,8 +408,8 @@ __global__ void __launch_bounds__(256) k_duplicate(const uint32_t* __restrict__ 
 // round, lane) order = element order.
 constexpr int kRadixThreads = 256;
 constexpr int kRadixWarps = kRadixThreads / 32;
-constexpr int kRadixRounds = 8;
-constexpr int kBlockTile = kRadixThreads * kRadixRounds;  // 2048
+constexpr int kRadixRounds = 16;
+constexpr int kBlockTile = kRadixThreads * kRadixRounds;  // 4096
 constexpr int kRadixDigits = 256;
 
 // One-sweep digit pass: the global digit
@@ -569,15 +569,36 @@ __global__ void k_check_capacity(BinState* st) {
     st->n_pairs_eff = over ? 0u : st->n_pairs;
 }
 
-__global__ void k_tile_ranges(const uint32_t* __restrict__ keys, const BinState* __restrict__ st, int tiles_x,
-                              uint2* ranges) {
+// Per-tile [start, end) from the sorted keys: grid-stride, four keys per thread (one 16-byte
+// load) compared with their neighbours; sized by the device-side pair count.
+__global__ void __launch_bounds__(256) k_tile_ranges(const uint32_t* __restrict__ keys, const BinState* __restrict__ st,
+                                                     int tiles_x, uint2* ranges) {
     const uint32_t n = st->n_pairs_eff;
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const uint32_t k = keys[i];
-    const uint32_t t = (k >> 8) * (uint32_t)tiles_x + (k & 0xffu);
-    if (i == 0 || keys[i - 1] != k) ranges[t].x = i;
-    if (i == n - 1 || keys[i + 1] != k) ranges[t].y = i + 1;
+    constexpr uint32_t kNone = 0xffffffffu;  // never a tile key (ty, tx < 2^8)
+    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; 4 * q < n; q += gridDim.x * blockDim.x) {
+        const uint32_t i0 = 4 * q;
+        uint32_t k[6];
+        k[0] = i0 > 0 ? keys[i0 - 1] : kNone;
+        if (i0 + 4 <= n) {
+            const uint4 v = *reinterpret_cast<const uint4*>(keys + i0);
+            k[1] = v.x;
+            k[2] = v.y;
+            k[3] = v.z;
+            k[4] = v.w;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) k[1 + j] = i0 + j < n ? keys[i0 + j] : kNone;
+        }
+        k[5] = i0 + 4 < n ? keys[i0 + 4] : kNone;
+#pragma unroll
+        for (int j = 1; j <= 4; ++j) {
+            if (k[j] == kNone) break;
+            const uint32_t t = (k[j] >> 8) * (uint32_t)tiles_x + (k[j] & 0xffu);
+            const uint32_t i = i0 + j - 1;
+            if (k[j - 1] != k[j]) ranges[t].x = i;
+            if (k[j + 1] != k[j]) ranges[t].y = i + 1;
+        }
+    }
 }
 
 }  // namespace rgs_dev
@@ -656,7 +677,7 @@ void tile_radix_sort(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint3
     k_radix_onesweep<<<nb, kRadixThreads, 0, s>>>(keys_b, vals_b, st, 8, aux + 257, status_b, tickets + 1, keys_a,
                                                    vals_a);
     cudaMemsetAsync(ranges, 0, sizeof(uint2) * (size_t)n_tiles, s);
-    k_tile_ranges<<<std::max(blocks(n_pairs, 256), 1), 256, 0, s>>>(keys_a, st, tiles_x, ranges);
+    k_tile_ranges<<<std::max(std::min(blocks(n_pairs, 4 * 256), 148 * 8), 1), 256, 0, s>>>(keys_a, st, tiles_x, ranges);
 }
 
 void check_capacity(BinState* st, cudaStream_t s) { k_check_capacity<<<1, 1, 0, s>>>(st); }
