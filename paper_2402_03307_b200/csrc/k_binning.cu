@@ -217,39 +217,31 @@ __global__ void k_bucket_scatter(const uint8_t* __restrict__ valid, const unsign
     ent_id[pos] = (uint32_t)i;
 }
 
-// One thread per bucket: insertion sort of small buckets in place, big ones deferred.
+// One thread per scattered entry: its rank inside its (small) bucket by counting the
+// bucket's entries that order before it -- (key, tie) is a total order -- and a direct
+// write to the sorted position.  Buckets above kSmallBucket are deferred to the big sort
+// (queued once, by their first entry).
 __global__ void k_bucket_sort_small(const uint32_t* __restrict__ bucket_count, const uint32_t* __restrict__ bucket_off,
-                                    unsigned long long* ent_key, uint32_t* ent_id, const int32_t* __restrict__ src,
+                                    const unsigned long long* __restrict__ ent_key,
+                                    const uint32_t* __restrict__ ent_id, const int32_t* __restrict__ src,
                                     const uint32_t* __restrict__ tiles, uint32_t* sorted_ids,
                                     uint32_t* sorted_tiles, BinState* st, uint32_t* big_list) {
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= kNumBuckets) return;
-    const uint32_t cnt = bucket_count[b];
-    if (cnt == 0) return;
-    const uint32_t off = bucket_off[b];
+    const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+    if (pos >= st->n_valid) return;
+    const unsigned long long k = ent_key[pos];
+    const uint32_t b = (uint32_t)((k - st->key_min) >> st->shift);
+    const uint32_t cnt = bucket_count[b], off = bucket_off[b];
     if (cnt > kSmallBucket) {
-        big_list[atomicAdd(&st->n_big, 1u)] = (uint32_t)b;
+        if ((uint32_t)pos == off) big_list[atomicAdd(&st->n_big, 1u)] = b;
         return;
     }
-    unsigned long long* K = ent_key + off;
-    uint32_t* I = ent_id + off;
-    for (uint32_t a = 1; a < cnt; ++a) {
-        const unsigned long long kv = K[a];
-        const uint32_t iv = I[a];
-        const uint32_t tv = tie_of(src, iv);
-        int j = (int)a - 1;
-        while (j >= 0 && key_less(kv, tv, K[j], tie_of(src, I[j]))) {
-            K[j + 1] = K[j];
-            I[j + 1] = I[j];
-            --j;
-        }
-        K[j + 1] = kv;
-        I[j + 1] = iv;
-    }
-    for (uint32_t a = 0; a < cnt; ++a) {
-        sorted_ids[off + a] = I[a];
-        sorted_tiles[off + a] = tiles[I[a]];
-    }
+    const uint32_t id = ent_id[pos];
+    const uint32_t t = tie_of(src, id);
+    uint32_t rank = 0;
+    for (uint32_t q = off; q < off + cnt; ++q)
+        if (q != (uint32_t)pos) rank += key_less(ent_key[q], tie_of(src, ent_id[q]), k, t) ? 1u : 0u;
+    sorted_ids[off + rank] = id;
+    sorted_tiles[off + rank] = tiles[id];
 }
 
 struct SortRec {
@@ -643,8 +635,8 @@ void depth_ranks(const uint8_t* valid, const unsigned long long* key, const uint
                  uint32_t* sorted_tiles, uint32_t* big_list, void* big_scratch, cudaStream_t s) {
     if (n <= 0) return;
     k_bucket_scatter<<<blocks(n, 256), 256, 0, s>>>(valid, key, n, st, bucket_off, bucket_cur, ent_key, ent_id);
-    k_bucket_sort_small<<<blocks(kNumBuckets, 256), 256, 0, s>>>(bucket_count, bucket_off, ent_key, ent_id, src,
-                                                                 tiles, sorted_ids, sorted_tiles, st, big_list);
+    k_bucket_sort_small<<<blocks(n, 256), 256, 0, s>>>(bucket_count, bucket_off, ent_key, ent_id, src, tiles,
+                                                        sorted_ids, sorted_tiles, st, big_list);
     k_bucket_sort_big<<<148, 512, kBigSmem * sizeof(SortRec), s>>>(bucket_count, bucket_off, ent_key, ent_id, src,
                                                                    tiles, st, big_list, sorted_ids, sorted_tiles,
                                                                    reinterpret_cast<SortRec*>(big_scratch));
