@@ -102,25 +102,36 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_1p(const uint32_t* __rest
     }
     uint32_t agg;
     const uint32_t ex = block_exclusive_scan(sum, &agg);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {
+        // warp-wide look-back: lane j reads predecessor p - j, 32 status words per round trip
+        const int lane = threadIdx.x;
         volatile unsigned long long* vs = status;
         uint32_t excl = 0;
         if (bid == 0) {
-            vs[0] = kScanInc | agg;
+            if (lane == 0) vs[0] = kScanInc | agg;
         } else {
-            vs[bid] = kScanAgg | agg;
+            if (lane == 0) vs[bid] = kScanAgg | agg;
             for (int p = bid - 1; p >= 0;) {
-                const unsigned long long w = vs[p];
-                if (!(w & (kScanInc | kScanAgg))) continue;
-                excl += (uint32_t)w;
-                if (w & kScanInc) break;
-                --p;
+                const unsigned long long w = p - lane >= 0 ? vs[p - lane] : (unsigned long long)(kScanInc | 0ull);
+                const unsigned inc = __ballot_sync(kFullMask, (w & kScanInc) != 0);
+                const unsigned ready = __ballot_sync(kFullMask, (w & (kScanInc | kScanAgg)) != 0);
+                const int last = inc ? __ffs(inc) - 1 : 31;  // nearest inclusive predecessor
+                const unsigned need = last == 31 ? kFullMask : ((2u << last) - 1u);
+                if ((ready & need) != need) continue;  // a predecessor has not published yet
+                uint32_t x = lane <= last && p - lane >= 0 ? (uint32_t)w : 0u;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(kFullMask, x, o);
+                excl += x;
+                if (inc) break;
+                p -= 32;
             }
-            vs[bid] = kScanInc | (unsigned long long)(excl + agg);
+            if (lane == 0) vs[bid] = kScanInc | (unsigned long long)(excl + agg);
         }
-        s_excl = excl;
-        const bool last = base + kScan1Tile >= n;
-        if (last && total) *total = excl + agg;
+        if (lane == 0) {
+            s_excl = excl;
+            const bool last_tile = base + kScan1Tile >= n;
+            if (last_tile && total) *total = excl + agg;
+        }
     }
     __syncthreads();
     uint32_t run = s_excl + ex;
