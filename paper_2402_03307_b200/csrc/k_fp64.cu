@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(128) k_preprocess(ParamView P, int sh_degree, 
                             col[0], col[1], col[2], o.p[2], flow[0], flow[1], o.radius, cam.tiles_x, cam.tiles_y,
                             &ntiles, o.cov2[0], o.cov2[3]);
                 key = order_key(o.p[2]);
+                if (out.dir_dist) out.dir_dist[i] = make_double4(o.dir[0], o.dir[1], o.dir[2], o.dist);
             }
         }
         out.valid[i] = ok ? 1 : 0;
@@ -565,59 +566,25 @@ __global__ void __launch_bounds__(256) k_backward_fp64(SplatArrays sp, const uin
     }
 }
 
-// ---------------------------------------------------------------------------
-// K7: per-Gaussian backward (rasterizer.cpp:134-181, gaussian.cpp:57-101,
-// rotor.cpp:138-194).  Recomputes the forward chain from the parameters.
+// K7a: colour path of the per-Gaussian backward (rasterizer.cpp:137-147): SH gradients and
+// the view-direction term of d mean3, from the forward's direction (K1 stores it; the chain
+// is recomputed bit-identically either way).  Split from K7b so neither kernel carries the
+// SH basis gradients and the slice state at once (K7 was 255 registers with spills).
 template <bool F64>
-__global__ void __launch_bounds__(128) k_gaussian_backward(ParamView P, int sh_degree, DevCamera cam,
-                                                           const uint8_t* __restrict__ valid,
-                                                           const double* __restrict__ sgrad, int accumulate,
-                                                           float* grads, float* vnorm, int32_t* visible) {
+__global__ void __launch_bounds__(128) k_color_backward(ParamView P, int sh_degree, const uint8_t* __restrict__ valid,
+                                                        const double4* __restrict__ dir_dist,
+                                                        const double* __restrict__ sgrad, int accumulate,
+                                                        float* grads, double* cdm3) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= P.n) return;
+    if (i >= P.n || !valid[i]) return;
     const int n = P.n;
-    float4* gm = reinterpret_cast<float4*>(grads);
-    float4* gl = reinterpret_cast<float4*>(grads + 4 * (size_t)n);
-    float4* gr0 = reinterpret_cast<float4*>(grads + 8 * (size_t)n);
-    float4* gr1 = reinterpret_cast<float4*>(grads + 12 * (size_t)n);
-    float* gop = grads + 64 * (size_t)n;
-    if (!valid[i]) {
-        if (!accumulate) {
-            const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-            gm[i] = z;
-            gl[i] = z;
-            gr0[i] = z;
-            gr1[i] = z;
-#pragma unroll
-            for (int b = 0; b < 12; ++b) reinterpret_cast<float4*>(grads + (16 + 4 * (size_t)b) * n)[i] = z;
-            gop[i] = 0.f;
-            vnorm[i] = 0.f;
-            visible[i] = 0;
-        }
-        return;
-    }
-    double mean4[4], ls[4], rot[8];
-    ld_block<F64>(P, 0, i, mean4);
-    ld_block<F64>(P, 1, i, ls);
-    ld_block<F64>(P, 2, i, rot);
-    ld_block<F64>(P, 3, i, rot + 4);
-    const double op = ld_opacity<F64>(P, i);
-    SliceState s;
-    d_slice(mean4, ls, rot, cam.time, s);
-    ProjState o;
-    d_project_geom(s, cam, op, o);
-
+    const double4 dd = dir_dist[i];
+    struct {
+        double dir[3];
+        double dist;
+    } o = {{dd.x, dd.y, dd.z}, dd.w};
     const double* g9 = sgrad + (size_t)i * 9;
     const double dcol[3] = {g9[0], g9[1], g9[2]};
-    const double dcon[3] = {g9[3], g9[4], g9[5]};
-    const double dm2[2] = {g9[6], g9[7]};
-    const double dab = g9[8];
-
-    // out[0..16]: mean4, ls4, rotor8, opacity; the 48 SH gradients are written directly.
-    double out[17];
-#pragma unroll
-    for (int k = 0; k < 17; ++k) out[k] = 0;
-
     // ---- colour path: SH coefficients and view direction (rasterizer.cpp:137-147).
     // The SH blocks are streamed once: the colour (for the clamp flags) and, per channel,
     // t[ch][ax] = sum_k bgrad[k][ax] sh[k][ch] accumulate in the reference's k order.
@@ -689,6 +656,69 @@ __global__ void __launch_bounds__(128) k_gaussian_backward(ParamView P, int sh_d
             dmean3[r] += a;
         }
     }
+    cdm3[(size_t)i * 3 + 0] = dmean3[0];
+    cdm3[(size_t)i * 3 + 1] = dmean3[1];
+    cdm3[(size_t)i * 3 + 2] = dmean3[2];
+}
+
+// ---------------------------------------------------------------------------
+// K7b: per-Gaussian backward (rasterizer.cpp:134-181, gaussian.cpp:57-101,
+// rotor.cpp:138-194).  Recomputes the forward chain from the parameters.
+template <bool F64>
+__global__ void __launch_bounds__(128, 3) k_gaussian_backward(ParamView P, int sh_degree, DevCamera cam,
+                                                           const uint8_t* __restrict__ valid,
+                                                           const double* __restrict__ sgrad,
+                                                           const double* __restrict__ cdm3, int accumulate,
+                                                           float* grads, float* vnorm, int32_t* visible) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.n) return;
+    const int n = P.n;
+    float4* gm = reinterpret_cast<float4*>(grads);
+    float4* gl = reinterpret_cast<float4*>(grads + 4 * (size_t)n);
+    float4* gr0 = reinterpret_cast<float4*>(grads + 8 * (size_t)n);
+    float4* gr1 = reinterpret_cast<float4*>(grads + 12 * (size_t)n);
+    float* gop = grads + 64 * (size_t)n;
+    if (!valid[i]) {
+        if (!accumulate) {
+            const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+            gm[i] = z;
+            gl[i] = z;
+            gr0[i] = z;
+            gr1[i] = z;
+#pragma unroll
+            for (int b = 0; b < 12; ++b) reinterpret_cast<float4*>(grads + (16 + 4 * (size_t)b) * n)[i] = z;
+            gop[i] = 0.f;
+            vnorm[i] = 0.f;
+            visible[i] = 0;
+        }
+        return;
+    }
+    double mean4[4], ls[4], rot[8];
+    ld_block<F64>(P, 0, i, mean4);
+    ld_block<F64>(P, 1, i, ls);
+    ld_block<F64>(P, 2, i, rot);
+    ld_block<F64>(P, 3, i, rot + 4);
+    const double op = ld_opacity<F64>(P, i);
+    SliceState s;
+    d_slice(mean4, ls, rot, cam.time, s);
+    ProjState o;
+    d_project_geom(s, cam, op, o);
+
+    const double* g9 = sgrad + (size_t)i * 9;
+    const double dcol[3] = {g9[0], g9[1], g9[2]};
+    const double dcon[3] = {g9[3], g9[4], g9[5]};
+    const double dm2[2] = {g9[6], g9[7]};
+    const double dab = g9[8];
+
+    // out[0..16]: mean4, ls4, rotor8, opacity; the 48 SH gradients are written directly.
+    double out[17];
+#pragma unroll
+    for (int k = 0; k < 17; ++k) out[k] = 0;
+
+    // ---- colour path: K7a (k_color_backward) left its d mean3 term in cdm3
+    double dmean3[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) dmean3[r] = 0.0 + cdm3[(size_t)i * 3 + r];
     // ---- alpha_base = opacity * decay
     const double dL_ddecay = dab * o.opacity;
     out[16] += dab * s.decay * o.opacity * (1 - o.opacity);
@@ -896,16 +926,21 @@ void backward_fp64_pixels(const SplatArrays& sp, const uint32_t* pair_vals, cons
 }
 
 void gaussian_backward(const float* params, const double* params64, int n, int sh_degree, const DevCamera& cam,
-                       const uint8_t* valid, const double* screen_grads, int accumulate, float* grads, float* vnorm,
-                       int32_t* visible, cudaStream_t s) {
+                       const double4* dir_dist, double* color_dmean3, const uint8_t* valid, const double* screen_grads,
+                       int accumulate, float* grads, float* vnorm, int32_t* visible, cudaStream_t s) {
     if (n <= 0) return;
     ParamView P{params, n, params64};
-    if (params64)
-        k_gaussian_backward<true><<<blocks(n, 128), 128, 0, s>>>(P, sh_degree, cam, valid, screen_grads, accumulate,
-                                                                 grads, vnorm, visible);
-    else
+    if (params64) {
+        k_color_backward<true><<<blocks(n, 128), 128, 0, s>>>(P, sh_degree, valid, dir_dist, screen_grads, accumulate,
+                                                               grads, color_dmean3);
+        k_gaussian_backward<true><<<blocks(n, 128), 128, 0, s>>>(P, sh_degree, cam, valid, screen_grads, color_dmean3,
+                                                                 accumulate, grads, vnorm, visible);
+    } else {
+        k_color_backward<false><<<blocks(n, 128), 128, 0, s>>>(P, sh_degree, valid, dir_dist, screen_grads,
+                                                                accumulate, grads, color_dmean3);
         k_gaussian_backward<false><<<blocks(n, 128), 128, 0, s>>>(P, sh_degree, cam, valid, screen_grads,
-                                                                  accumulate, grads, vnorm, visible);
+                                                                  color_dmean3, accumulate, grads, vnorm, visible);
+    }
 }
 
 }  // namespace rgs_launch

@@ -63,7 +63,8 @@ struct DevBuf {
 // All per-view device state (one set per render in flight / per retained record).
 struct Frame {
     // per Gaussian / input splat
-    DevBuf valid, tiles, mean2, conic_ab, color_depth, flow_radius, rect, conic_f, color_f, guard_f, ext_f, src, key;
+    DevBuf valid, tiles, mean2, conic_ab, color_depth, flow_radius, rect, conic_f, color_f, guard_f, ext_f, src, key,
+        dir_dist;
     DevBuf ent_key, ent_id, sorted_ids, sorted_tiles, pair_off;
     // depth buckets
     DevBuf bucket_count, bucket_off, bucket_cur, big_list, big_scratch;
@@ -97,6 +98,7 @@ struct Frame {
         a.ext_f = ext_f.as<float4>();
         a.source_index = have_src ? src.as<int32_t>() : nullptr;
         a.depth_key = key.as<unsigned long long>();
+        a.dir_dist = dir_dist.as<double4>();
         return a;
     }
     const uint32_t* pair_vals() const { return pair_vals_buf.as<uint32_t>(); }
@@ -115,6 +117,7 @@ struct Frame {
         color_f.ensure(16 * n1, s);
         guard_f.ensure(8 * n1, s);
         ext_f.ensure(16 * n1, s);
+        dir_dist.ensure(32 * n1, s);
         key.ensure(8 * n1, s);
         ent_key.ensure(8 * n1, s);
         ent_id.ensure(4 * n1, s);
@@ -151,7 +154,7 @@ struct Frame {
     }
     void release(cudaStream_t s) {
         DevBuf* all[] = {&valid, &tiles, &mean2, &conic_ab, &color_depth, &flow_radius, &rect, &conic_f,
-                         &color_f, &guard_f, &ext_f, &src, &key, &ent_key, &ent_id, &sorted_ids, &sorted_tiles,
+                         &color_f, &guard_f, &ext_f, &src, &key, &dir_dist, &ent_key, &ent_id, &sorted_ids, &sorted_tiles,
                          &pair_off, &bucket_count, &bucket_off, &bucket_cur, &big_list, &big_scratch, &ranges,
                          &keys_a, &pair_vals_buf, &keys_b, &vals_b, &radix_counts, &radix_offsets, &final_T,
                          &n_contrib, &slow_list, &stats, &scan_tmp, &tmp_img};
@@ -186,6 +189,7 @@ struct rgs_ctx {
     long long launches = 0;
     Frame scratch;
     DevBuf sgrad;     // N x 9 doubles (screen-space gradients)
+    DevBuf cgrad;     // N x 3 doubles (the colour path's d mean3, K7a -> K7b)
     DevBuf tile_grads;  // P x 9 doubles (deterministic backward: per (tile, position))
     DevBuf tmp_img;   // host-buffer staging
     DevBuf tmp_splats, tmp_scan, tmp_ids;
@@ -588,6 +592,7 @@ void rgs_ctx_destroy(rgs_ctx* c) {
     cudaSetDevice(c->device);
     c->scratch.release(c->stream);
     c->sgrad.release(c->stream);
+    c->cgrad.release(c->stream);
     c->tmp_img.release(c->stream);
     c->tmp_splats.release(c->stream);
     c->tmp_scan.release(c->stream);
@@ -1268,11 +1273,13 @@ int rgs_render_backward(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* ca
         }
         {
             StageTimer t(c, kStBwdGauss, s);
-            rgs_launch::gaussian_backward(scene->params, scene->params64, n, scene->sh_degree, dc, f.valid.as<uint8_t>(),
+            c->cgrad.ensure(sizeof(double) * 3 * (size_t)std::max(n, 1), s);
+            rgs_launch::gaussian_backward(scene->params, scene->params64, n, scene->sh_degree, dc,
+                                          f.dir_dist.as<double4>(), c->cgrad.as<double>(), f.valid.as<uint8_t>(),
                                           c->sgrad.as<double>(), (flags & RGS_FLAG_ACCUMULATE) ? 1 : 0, grads,
                                           vnorm, visible, s);
         }
-        c->launches += 3;
+        c->launches += 4;
         CK(cudaGetLastError());
         return RGS_OK;
     });

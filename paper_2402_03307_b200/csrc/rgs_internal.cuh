@@ -80,6 +80,7 @@ struct SplatArrays {
     float4* ext_f;           // (ex, ey, gx2, gy2): alpha-ellipse bbox, max |grad p2| inside it
     int32_t* source_index;   // only for rasterize_forward (else NULL -> index)
     unsigned long long* depth_key;  // order-preserving bits of the FP64 depth (valid splats)
+    double4* dir_dist;              // (view direction, distance) of valid splats (scene renders)
 };
 
 // Error word: (index << 8) | code, minimum wins (lowest failing index).
@@ -166,7 +167,8 @@ void backward_fp64_pixels(const SplatArrays& sp, const uint32_t* pair_vals, cons
                           const DevCamera& cam, double3 bg, const double* final_T, const uint32_t* n_contrib,
                           const float* dL_dimage, const uint32_t* slow_list, const int* slow_count,
                           int max_pixels, double* screen_grads, cudaStream_t s);
-void gaussian_backward(const float* params, const double* params64, int n, int sh_degree, const DevCamera& cam, const uint8_t* valid,
+void gaussian_backward(const float* params, const double* params64, int n, int sh_degree, const DevCamera& cam,
+                       const double4* dir_dist, double* color_dmean3, const uint8_t* valid,
                        const double* screen_grads, int accumulate, float* grads, float* vnorm,
                        int32_t* visible, cudaStream_t s);
 void export_splats(const SplatArrays& sp, const uint32_t* compact_ids, int n_valid, void* out,
