@@ -60,12 +60,21 @@ __device__ __forceinline__ double block_sum_n(double v, double* red) {
 
 // K8a: SSIM forward over one tile of valid positions and one channel.
 // Tile: kSsimTX x kSsimATY valid positions (512 threads); input footprint (TX+10) x (TY+10).
+// K8a dynamic shared memory (see the layout in the kernel).
+template <typename TI>
+constexpr size_t k8a_smem_bytes() {
+    constexpr int IY = kSsimATY + kSsimWin - 1, IX = kSsimTX + kSsimWin - 1;
+    return sizeof(double) * (5 * IY * kSsimTX + kSsimAThreads) + sizeof(TI) * 2 * IY * (IX + 1);
+}
+
 template <typename TI>
 __global__ void __launch_bounds__(kSsimAThreads) k_ssim_fields(const TI* __restrict__ img, const TI* __restrict__ tgt,
                                                      int W, int H, int want_grad, double* __restrict__ dfield,
                                                      double* __restrict__ part_ssim) {
     constexpr int TX = kSsimTX, TY = kSsimATY, IX = TX + kSsimWin - 1, IY = TY + kSsimWin - 1;
     // dynamic shared memory: rows[5][IY][TX] and red[] (double), then sa / sb [IY][IX + 1] (TI)
+    // (the products a*a, b*b, a*b are formed per tap in registers: staging them in shared
+    // memory as doubles measured 13% slower -- the taps are shared-memory bound, not FP64)
     extern __shared__ double k8a_smem[];
     auto rows = reinterpret_cast<double (*)[IY][TX]>(k8a_smem);
     double* red = k8a_smem + 5 * IY * TX;
@@ -242,6 +251,30 @@ __global__ void __launch_bounds__(256) k_finalize(const double* __restrict__ par
     }
 }
 
+
+// The image loss's three finalisations (L1, SSIM, squared error) in one launch, one block each.
+struct FinalizeJob {
+    const double* parts;
+    int n_parts, one_minus, accumulate;
+    double denom;
+    double* out;
+};
+struct FinalizeJobs {
+    FinalizeJob j[3];
+};
+__global__ void __launch_bounds__(256) k_finalize3(FinalizeJobs jobs, double scale) {
+    const FinalizeJob& f = jobs.j[blockIdx.x];
+    __shared__ double red[256];
+    double s = 0;
+    for (int i = threadIdx.x; i < f.n_parts; i += 256) s += f.parts[i];
+    const double tot = block_sum(s, red);
+    if (threadIdx.x == 0) {
+        double v = tot / f.denom;
+        if (f.one_minus) v = 1 - v;
+        v = v * scale;
+        *f.out = f.accumulate ? *f.out + v : v;
+    }
+}
 
 // loss.cpp:16-31 on an opacity array (the standalone form of the term folded into K9).
 __global__ void __launch_bounds__(256) k_entropy(const double* __restrict__ op, int n, double* __restrict__ grad,
@@ -910,9 +943,7 @@ void set_ssim_window(const double* k11, cudaStream_t s) {
 
 // Per-device kernel attributes (called from rgs_ctx_create on the context's device).
 bool train_init() {
-    constexpr int IY = kSsimATY + kSsimWin - 1, IX = kSsimTX + kSsimWin - 1;
-    const size_t s32 = sizeof(double) * (5 * IY * kSsimTX + kSsimAThreads) + sizeof(float) * 2 * IY * (IX + 1);
-    const size_t s64 = sizeof(double) * (5 * IY * kSsimTX + kSsimAThreads) + sizeof(double) * 2 * IY * (IX + 1);
+    const size_t s32 = k8a_smem_bytes<float>(), s64 = k8a_smem_bytes<double>();
     return cudaFuncSetAttribute(k_ssim_fields<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s32) ==
                cudaSuccess &&
            cudaFuncSetAttribute(k_ssim_fields<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s64) ==
@@ -943,18 +974,19 @@ void image_loss_t(const TI* img, const TI* tgt, int W, int H, const ImageGradArg
     // Images smaller than the window have no SSIM (the caller rejects w_ssim != 0 for them):
     // stage A is skipped and the SSIM slot is NaN.
     const bool has_ssim = W >= kSsimWin && H >= kSsimWin;
-    constexpr int IY = kSsimATY + kSsimWin - 1, IX = kSsimTX + kSsimWin - 1;
-    const size_t smem = sizeof(double) * (5 * IY * kSsimTX + kSsimAThreads) + sizeof(TI) * 2 * IY * (IX + 1);
+    const size_t smem = k8a_smem_bytes<TI>();
     if (has_ssim)
         k_ssim_fields<TI><<<dim3(g.a_x, g.a_y, 3), kSsimAThreads, smem, s>>>(img, tgt, W, H, dl != nullptr, dfield, pa);
     ImageGradArgs a2 = a;
     if (!has_ssim) a2.w_ssim = 0;
     k_image_grad<TI, TO><<<dim3(g.b_x, g.b_y, 3), kSsimAThreads, 0, s>>>(img, tgt, W, H, dfield, a2, dl, pl1, psq);
     if (losses) {
-        k_finalize<<<1, 256, 0, s>>>(pl1, g.n_b, nvals, loss_scale, 0, accumulate, losses + 0);
-        if (has_ssim) k_finalize<<<1, 256, 0, s>>>(pa, g.n_a, count, loss_scale, 1, accumulate, losses + 1);
-        else k_finalize<<<1, 256, 0, s>>>(pa, 0, 0.0, loss_scale, 0, 0, losses + 1);  // 0 / 0 = NaN
-        k_finalize<<<1, 256, 0, s>>>(psq, g.n_b, nvals, loss_scale, 0, accumulate, losses + 2);
+        FinalizeJobs jobs;
+        jobs.j[0] = FinalizeJob{pl1, g.n_b, 0, accumulate, nvals, losses + 0};
+        jobs.j[1] = has_ssim ? FinalizeJob{pa, g.n_a, 1, accumulate, count, losses + 1}
+                             : FinalizeJob{pa, 0, 0, 0, 0.0, losses + 1};  // 0 / 0 = NaN
+        jobs.j[2] = FinalizeJob{psq, g.n_b, 0, accumulate, nvals, losses + 2};
+        k_finalize3<<<3, 256, 0, s>>>(jobs, loss_scale);
     }
 }
 

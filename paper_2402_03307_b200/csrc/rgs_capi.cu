@@ -1447,7 +1447,7 @@ int rgs_image_loss(rgs_ctx* c, const float* rendered, const float* target, int w
         a.accumulate = (flags & RGS_FLAG_ACCUMULATE_GRAD) ? 1 : 0;
         rgs_launch::image_loss(rendered, target, width, height, a, dL_dimage, ts.dfield.as<double>(),
                                ts.parts.as<double>(), losses, loss_scale, (flags & RGS_FLAG_ACCUMULATE) ? 1 : 0, s);
-        c->launches += losses ? 5 : 2;
+        c->launches += losses ? 3 : 2;
         CK(cudaGetLastError());
         return RGS_OK;
     });
@@ -1474,7 +1474,7 @@ int rgs_image_loss_f64(rgs_ctx* c, const double* rendered, const double* target,
         a.accumulate = (flags & RGS_FLAG_ACCUMULATE_GRAD) ? 1 : 0;
         rgs_launch::image_loss_f64(rendered, target, width, height, a, dL_dimage, ts.dfield.as<double>(),
                                    ts.parts.as<double>(), losses, loss_scale, (flags & RGS_FLAG_ACCUMULATE) ? 1 : 0, s);
-        c->launches += losses ? 5 : 2;
+        c->launches += losses ? 3 : 2;
         CK(cudaGetLastError());
         return RGS_OK;
     });
