@@ -593,7 +593,7 @@ def run_ours(args, rank, local_rank, world):
         ctx.render_views_host([p.numpy() for p in pinned], store.active_sh_degree, cams, (0, 0, 0), host_imgs.numpy())
         # Each rep timed on its own; the median is reported (the host PCIe link of the shared
         # pool's boxes occasionally drops to a fraction of its rate for a sweep).
-        reps = 5
+        reps = 9
         rep_s = []
         for _ in range(reps):
             if dist:
