@@ -356,6 +356,40 @@ __device__ __forceinline__ void st1(void* base, size_t idx, double v) {
 // One thread per (Gaussian, parameter group): blockIdx.y = 0 mean, 1 log scales, 2 rotor
 // (both blocks + normalize), 3 opacity (+ entropy, + accumulate_stats), 4..15 SH blocks.
 // Every group is independent, so the 16x wider grid hides the FP64 divide / sqrt latency.
+// K9a: the plain Adam groups -- mean, log scales and the 12 SH blocks (14 of the 16 groups,
+// 56 of the 65 parameters): four independent scalar updates per thread, few registers, so
+// the FP64 divide / sqrt latency is hidden by occupancy.  Same arithmetic as k_adam_step.
+template <bool F64>
+__global__ void __launch_bounds__(128) k_adam_plain(void* params, void* mom1, void* mom2,
+                                                    const float* __restrict__ grads, int n, AdamArgs a) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int grp = blockIdx.y < 2 ? blockIdx.y : blockIdx.y + 2;
+    double p[4], m[4], v[4], g[4];
+    ld4<F64>(params, n, grp, i, p);
+    ld4<F64>(mom1, n, grp, i, m);
+    ld4<F64>(mom2, n, grp, i, v);
+    ld4<false>(grads, n, grp, i, g);
+    if (grp < 2) {
+        // mean (lr_position schedule) / log scales; static mode freezes t
+        const double lr = grp == 0 ? a.lr_pos : a.lr_scales;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (!(a.static_mode && k == 3)) adam_scalar(p[k], m[k], v[k], g[k], lr, a.bc1, a.bc2);
+    } else {
+        // SH block b = grp - 4 holds coefficients j = 4b..4b+3, j = k*3 + ch; DC is j < 3
+        const int b = grp - 4;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const double lr = (4 * b + e) < 3 ? a.lr_sh_dc : a.lr_sh_rest;
+            adam_scalar(p[e], m[e], v[e], g[e], lr, a.bc1, a.bc2);
+        }
+    }
+    st4<F64>(params, n, grp, i, p);
+    st4<F64>(mom1, n, grp, i, m);
+    st4<F64>(mom2, n, grp, i, v);
+}
+
 template <bool F64>
 __global__ void __launch_bounds__(128) k_adam_step(void* params, void* mom1, void* mom2, const float* __restrict__ grads,
                                                    const float* __restrict__ vnorm, const int32_t* __restrict__ visible,
@@ -363,24 +397,10 @@ __global__ void __launch_bounds__(128) k_adam_step(void* params, void* mom1, voi
                                                    AdamArgs a, unsigned long long* err, double* part_entropy) {
     __shared__ double red[256];
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const int grp = blockIdx.y;
+    const int grp = 2 + blockIdx.y;  // groups 2 (rotor) and 3 (opacity / stats); k_adam_plain does the rest
     double ent = 0;
     if (i < n) {
-        double p[4], m[4], v[4], g[4];
-        if (grp == 0 || grp == 1) {
-            // mean (lr_position schedule) / log scales; static mode freezes t
-            const double lr = grp == 0 ? a.lr_pos : a.lr_scales;
-            ld4<F64>(params, n, grp, i, p);
-            ld4<F64>(mom1, n, grp, i, m);
-            ld4<F64>(mom2, n, grp, i, v);
-            ld4<false>(grads, n, grp, i, g);
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                if (!(a.static_mode && k == 3)) adam_scalar(p[k], m[k], v[k], g[k], lr, a.bc1, a.bc2);
-            st4<F64>(params, n, grp, i, p);
-            st4<F64>(mom1, n, grp, i, m);
-            st4<F64>(mom2, n, grp, i, v);
-        } else if (grp == 2) {
+        if (grp == 2) {
             // rotor: Adam on the 8 stored coefficients, then normalize (rotor.cpp:117-136)
             double rc[8], rm[8], rv[8], rg[8];
             ld4<F64>(params, n, 2, i, rc);
@@ -432,21 +452,6 @@ __global__ void __launch_bounds__(128) k_adam_step(void* params, void* mom1, voi
             st1<F64>(params, io, po);
             st1<F64>(mom1, io, mo);
             st1<F64>(mom2, io, vo);
-        } else {
-            // SH block b = grp - 4 holds coefficients j = 4b..4b+3, j = k*3 + ch; DC is j < 3
-            const int b = grp - 4;
-            ld4<F64>(params, n, grp, i, p);
-            ld4<F64>(mom1, n, grp, i, m);
-            ld4<F64>(mom2, n, grp, i, v);
-            ld4<false>(grads, n, grp, i, g);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const double lr = (4 * b + e) < 3 ? a.lr_sh_dc : a.lr_sh_rest;
-                adam_scalar(p[e], m[e], v[e], g[e], lr, a.bc1, a.bc2);
-            }
-            st4<F64>(params, n, grp, i, p);
-            st4<F64>(mom1, n, grp, i, m);
-            st4<F64>(mom2, n, grp, i, v);
         }
     }
     if (part_entropy && grp == 3) {
@@ -1003,12 +1008,15 @@ void adam_step(bool f64, void* params, void* m1, void* m2, const float* grads, c
                const int32_t* visible, double* accum, int32_t* count, int n, const AdamArgs& a,
                unsigned long long* err, double* part_entropy, double* losses_entropy, int accumulate, cudaStream_t s) {
     const int nb = nblk(n, 128);
-    if (f64)
-        k_adam_step<true><<<dim3(nb, 16), 128, 0, s>>>(params, m1, m2, grads, vnorm, visible, accum, count, n, a, err,
-                                            part_entropy);
-    else
-        k_adam_step<false><<<dim3(nb, 16), 128, 0, s>>>(params, m1, m2, grads, vnorm, visible, accum, count, n, a, err,
-                                             part_entropy);
+    if (f64) {
+        k_adam_plain<true><<<dim3(nb, 14), 128, 0, s>>>(params, m1, m2, grads, n, a);
+        k_adam_step<true><<<dim3(nb, 2), 128, 0, s>>>(params, m1, m2, grads, vnorm, visible, accum, count, n, a, err,
+                                                      part_entropy);
+    } else {
+        k_adam_plain<false><<<dim3(nb, 14), 128, 0, s>>>(params, m1, m2, grads, n, a);
+        k_adam_step<false><<<dim3(nb, 2), 128, 0, s>>>(params, m1, m2, grads, vnorm, visible, accum, count, n, a,
+                                                       err, part_entropy);
+    }
     if (part_entropy && losses_entropy)
         k_finalize<<<1, 256, 0, s>>>(part_entropy, nb, (double)n, 1.0, 0, accumulate, losses_entropy);
 }

@@ -1568,7 +1568,7 @@ int rgs_adam_step(rgs_ctx* c, rgs_scene* scene, rgs_optimizer* o, const float* g
         rgs_launch::adam_step(o->f64, params, o->m1, o->m2, grads, vnorm, visible, o->accum, o->count, scene->n, a,
                               o->err, ent ? o->part.as<double>() : nullptr, ent ? losses : nullptr,
                               (cfg->flags & RGS_FLAG_ACCUMULATE) ? 1 : 0, c->stream);
-        c->launches += ent ? 2 : 1;
+        c->launches += ent ? 3 : 2;
         CK(cudaGetLastError());
         return RGS_OK;
     });
