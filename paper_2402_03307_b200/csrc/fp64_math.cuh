@@ -291,6 +291,81 @@ __device__ __forceinline__ void d_sh_basis_grad(const double* dir, int degree, d
     }
 }
 
+// Row k of d_sh_basis_grad (the same expressions, so the same values), for loops that want
+// one row at a time instead of the 48-entry array (K7a).
+template <int K>
+__device__ __forceinline__ void d_sh_basis_grad_row(double x, double y, double z, int degree, double* g) {
+    g[0] = g[1] = g[2] = 0;
+    if constexpr (K >= 1 && K <= 3) {
+        if (degree >= 1) {
+            if constexpr (K == 1) g[1] = -kC1;
+            if constexpr (K == 2) g[2] = kC1;
+            if constexpr (K == 3) g[0] = -kC1;
+        }
+    } else if constexpr (K >= 4 && K <= 8) {
+        if (degree >= 2) {
+            if constexpr (K == 4) {
+                g[0] = kC2_0 * y;
+                g[1] = kC2_0 * x;
+            }
+            if constexpr (K == 5) {
+                g[1] = kC2_1 * z;
+                g[2] = kC2_1 * y;
+            }
+            if constexpr (K == 6) {
+                g[0] = kC2_2 * -2 * x;
+                g[1] = kC2_2 * -2 * y;
+                g[2] = kC2_2 * 4 * z;
+            }
+            if constexpr (K == 7) {
+                g[0] = kC2_3 * z;
+                g[2] = kC2_3 * x;
+            }
+            if constexpr (K == 8) {
+                g[0] = kC2_4 * 2 * x;
+                g[1] = kC2_4 * -2 * y;
+            }
+        }
+    } else if constexpr (K >= 9) {
+        if (degree >= 3) {
+            const double xx = x * x, yy = y * y, zz = z * z;
+            if constexpr (K == 9) {
+                g[0] = kC3_0 * 6 * x * y;
+                g[1] = kC3_0 * (3 * xx - 3 * yy);
+            }
+            if constexpr (K == 10) {
+                g[0] = kC3_1 * y * z;
+                g[1] = kC3_1 * x * z;
+                g[2] = kC3_1 * x * y;
+            }
+            if constexpr (K == 11) {
+                g[0] = kC3_2 * -2 * x * y;
+                g[1] = kC3_2 * (4 * zz - xx - 3 * yy);
+                g[2] = kC3_2 * 8 * y * z;
+            }
+            if constexpr (K == 12) {
+                g[0] = kC3_3 * -6 * x * z;
+                g[1] = kC3_3 * -6 * y * z;
+                g[2] = kC3_3 * (6 * zz - 3 * xx - 3 * yy);
+            }
+            if constexpr (K == 13) {
+                g[0] = kC3_4 * (4 * zz - 3 * xx - yy);
+                g[1] = kC3_4 * -2 * x * y;
+                g[2] = kC3_4 * 8 * x * z;
+            }
+            if constexpr (K == 14) {
+                g[0] = kC3_5 * 2 * x * z;
+                g[1] = kC3_5 * -2 * y * z;
+                g[2] = kC3_5 * (xx - yy);
+            }
+            if constexpr (K == 15) {
+                g[0] = kC3_6 * (3 * xx - 3 * yy);
+                g[1] = kC3_6 * -6 * x * y;
+            }
+        }
+    }
+}
+
 // ProjectCache subset (rasterizer.hpp:33-48) + the Splat2D outputs.
 struct ProjState {
     double p[3];

@@ -566,6 +566,33 @@ __global__ void __launch_bounds__(256) k_backward_fp64(SplatArrays sp, const uin
     }
 }
 
+// K7a's SH loop, one row k per step (compile-time k): loads the row's three coefficients
+// (j = 3k + ch) and accumulates acol[ch] += v basis[k], tg[ch][ax] += g_k[ax] v.
+template <bool F64, int Kr>
+__device__ __forceinline__ void sh_rows(const ParamView& P, int i, int K, const double* dir,
+                                        int sh_degree, const double* basis, double* acol, double (*tg)[3]) {
+    if constexpr (Kr < 16) {
+        if (Kr >= K) return;
+        double g3[3];
+        d_sh_basis_grad_row<Kr>(dir[0], dir[1], dir[2], sh_degree, g3);
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+            const int j = 3 * Kr + ch;
+            const double v = ld_coef<F64>(P, i, j);
+            if (Kr == 0) {
+                acol[ch] = v * basis[0];
+#pragma unroll
+                for (int ax = 0; ax < 3; ++ax) tg[ch][ax] = g3[ax] * v;
+            } else {
+                acol[ch] += v * basis[Kr];
+#pragma unroll
+                for (int ax = 0; ax < 3; ++ax) tg[ch][ax] += g3[ax] * v;
+            }
+        }
+        sh_rows<F64, Kr + 1>(P, i, K, dir, sh_degree, basis, acol, tg);
+    }
+}
+
 // K7a: colour path of the per-Gaussian backward (rasterizer.cpp:137-147): SH gradients and
 // the view-direction term of d mean3, from the forward's direction (K1 stores it; the chain
 // is recomputed bit-identically either way).  Split from K7b so neither kernel carries the
@@ -592,31 +619,11 @@ __global__ void __launch_bounds__(128) k_color_backward(ParamView P, int sh_degr
     const int K = (deg + 1) * (deg + 1);
     double basis[16];
     d_sh_basis(o.dir, sh_degree, basis);
-    double bgrad[48];
-    d_sh_basis_grad(o.dir, sh_degree, bgrad);
     double acol[3] = {0, 0, 0}, tg[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-    const int nblocks = (3 * K + 3) / 4;
-#pragma unroll
-    for (int b = 0; b < 12; ++b) {
-        if (b >= nblocks) break;
-        double v4[4];
-        ld_block<F64>(P, 4 + b, i, v4);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const int j = 4 * b + e, k = j / 3, ch = j - 3 * k;
-            if (k >= K) break;
-            const double v = v4[e];
-            if (k == 0) {
-                acol[ch] = v * basis[0];
-#pragma unroll
-                for (int ax = 0; ax < 3; ++ax) tg[ch][ax] = bgrad[ax] * v;
-            } else {
-                acol[ch] += v * basis[k];
-#pragma unroll
-                for (int ax = 0; ax < 3; ++ax) tg[ch][ax] += bgrad[k * 3 + ax] * v;
-            }
-        }
-    }
+    // one SH row k at a time: its three coefficients (one per channel) and its basis-gradient
+    // row (computed on the spot, not a 48-entry array); per channel the k order is the
+    // reference's, as in the 48-entry form
+    sh_rows<F64, 0>(P, i, K, o.dir, sh_degree, basis, acol, tg);
     bool live[3];
     double dL_ddir[3] = {0, 0, 0};
 #pragma unroll

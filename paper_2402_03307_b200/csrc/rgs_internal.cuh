@@ -58,6 +58,13 @@ __device__ __forceinline__ void ld_block(const ParamView& P, int blk, int i, T* 
         v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
     }
 }
+// SH coefficient j (= 3k + ch) of Gaussian i: element j % 4 of block 4 + j / 4.
+template <bool F64>
+__device__ __forceinline__ double ld_coef(const ParamView& P, int i, int j) {
+    const size_t off = 4 * (size_t)(4 + (j >> 2)) * P.n + 4 * (size_t)i + (j & 3);
+    if constexpr (F64) return P.base64[off];
+    else return P.base[off];
+}
 template <bool F64>
 __device__ __forceinline__ double ld_opacity(const ParamView& P, int i) {
     if constexpr (F64) return P.base64[64 * (size_t)P.n + i];
