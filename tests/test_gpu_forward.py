@@ -116,6 +116,33 @@ def test_flow(ctx, orc):
     assert np.abs(got - ref).max() <= 1e-4 * scale
 
 
+@pytest.mark.parametrize("n", [3000, 6000])
+def test_equal_depth_ties(ctx, orc, n):
+    """Every splat at the same depth: one depth bucket far above the small-bucket limit (the
+    shared-memory bitonic path at 3000, the global-scratch path above 4096); the tile lists
+    must come out in index order, as the reference's (depth, index) sort."""
+    store = scenes.synthetic_scene(n, 320, 240, seed=11)
+    store.mean[:, :2] *= 4.0 / store.mean[:, 2:3]  # same screen positions at depth 4
+    store.mean[:, :2] = store.mean[:, :2].astype(np.float32)
+    store.mean[:, 2] = 4.0
+    store.rotor[:] = 0
+    store.rotor[:, 0] = 1.0  # identity rotors: no space-time coupling, depth = z exactly
+    cam = scenes.bench_camera(320, 240, 0.5)
+    err, ncd, rec, ref, out = _compare_forward(ctx, orc, store, cam)
+    assert len(ref.splats) > 0.9 * n
+    assert err <= 1e-4 and ncd == 0
+
+
+def test_max_image_4096(ctx, orc):
+    """The largest supported image (4096 x 4096 = 256 x 256 tiles, the two byte passes' range)
+    on a sparse scene: records, tile lists and image against the oracle."""
+    store = scenes.synthetic_scene(4000, 4096, 4096, seed=12)
+    cam = scenes.bench_camera(4096, 4096, 0.4, scenes.yaw_pose(3.0, (0.02, 0.0, 0.05)))
+    err, ncd, rec, ref, out = _compare_forward(ctx, orc, store, cam, threads=16)
+    assert rec.tiles_x == 256 and rec.tiles_y == 256
+    assert err <= 1e-4 and ncd == 0
+
+
 def test_empty_and_offscreen(ctx, orc):
     empty = rgs.GaussianStore.empty(0, 0)
     cam = scenes.bench_camera(40, 24, 0.5)
