@@ -67,6 +67,30 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
 
 
+def replicate_scene(ctx, store, dist, rank, world, dev):
+    """The scene replica of every rank: on one rank an upload; on N ranks
+    rank 0 uploads and the device parameter buffer is broadcast (NCCL over NVLink), timed and
+    reported (setup, outside the timed region)."""
+    import torch
+
+    from paper_2402_03307_b200 import rgs
+
+    if dist is None or world == 1:
+        return rgs.DeviceScene.from_store(ctx, store), None
+    scene = rgs.DeviceScene(ctx, store.size(), store.active_sh_degree)
+    if rank == 0:
+        scene.upload(store)
+    ctx.synchronize()
+    buf = scene.params_tensor()
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    dist.broadcast(buf, src=0)
+    torch.cuda.synchronize(dev)
+    ms = 1e3 * max_over_ranks(time.perf_counter() - t0, dist, dev)
+    return scene, {"bytes": buf.numel() * buf.element_size(), "ms": ms, "collective": "broadcast from rank 0"}
+
+
 def max_over_ranks(value: float, dist=None, device=None) -> float:
     """Max of a per-rank time over all ranks (the multi-GPU timing rule)."""
     if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
@@ -201,7 +225,7 @@ def run_c4_leg(args, ctx, dev, dist, rank, world, flush):
     cams_all = scenes.orbit_cameras(C4_W, C4_H, 8, 8)
     lo, hi = rank * C4_VIEWS // world, (rank + 1) * C4_VIEWS // world
     cams = cams_all[lo:hi]
-    scene = rgs.DeviceScene.from_store(ctx, store)
+    scene, bcast = replicate_scene(ctx, store, dist, rank, world, dev)
     images = torch.empty((len(cams), C4_H, C4_W, 3), dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
     ctx.render_views(scene, cams, (0.0, 0.0, 0.0), out=images)  # warm-up (also sizes the pair buffers)
@@ -228,7 +252,7 @@ def run_c4_leg(args, ctx, dev, dist, rank, world, flush):
     torch.cuda.empty_cache()
     return {"metric": "batch FPS at 3840x2160 (2M 4D Gaussians, 64-view batch)", "value": C4_VIEWS * steps / (ms / 1e3),
             "unit": "frames/s", "scaling": "strong", "n_gpus": world, "views_per_rank": len(cams), "steps": steps,
-            "ms_per_batch": ms / steps,
+            "ms_per_batch": ms / steps, "scene_broadcast": bcast,
             "config": {"workload": "C4: 2M 4D rotor Gaussians, SH deg 3, 3840x2160, 64 views = 8 orbit yaws x 8 "
                                    "timestamps, views sharded contiguously across ranks",
                        "n_gaussians": C4_N, "width": C4_W, "height": C4_H, "n_pairs_mid_view": n_pairs,

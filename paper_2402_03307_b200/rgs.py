@@ -601,6 +601,19 @@ class DeviceScene:
         self.ctx.check(self.ctx.L.rgs_scene_download_f64(self.ctx.h, self.h, *[_vp(a.ctypes.data) for a in out]))
         return out
 
+    def params_tensor(self):
+        """The device parameter buffer (rgs_scene_params layout: 65 x N float32, or float64 for
+        FP64 scenes) as a torch tensor view -- e.g. to broadcast a replica with NCCL."""
+        import torch
+
+        class _View:
+            pass
+
+        v = _View()
+        v.__cuda_array_interface__ = {"shape": (65 * self.n,), "typestr": "<f8" if self.f64 else "<f4",
+                                      "data": (self.params_ptr(), False), "version": 3}
+        return torch.as_tensor(v, device=f"cuda:{self.ctx.device}")
+
     def params_ptr(self) -> int:
         fn =self.ctx.L.rgs_scene_params_f64 if self.f64 else self.ctx.L.rgs_scene_params
         return int(fn(self.h) or 0)

@@ -143,6 +143,26 @@ def test_max_image_4096(ctx, orc):
     assert err <= 1e-4 and ncd == 0
 
 
+def test_scene_params_tensor_view(ctx):
+    """DeviceScene.params_tensor is a live view of the device SoA: writing through it (as an
+    NCCL broadcast into a replica does) changes what the renderer sees."""
+    import torch
+
+    store = scenes.random_scene(300, sh_degree=3, seed=4)
+    a = rgs.DeviceScene.from_store(ctx, store)
+    b = rgs.DeviceScene(ctx, store.size(), store.active_sh_degree)
+    ctx.synchronize()
+    b.params_tensor().copy_(a.params_tensor())
+    torch.cuda.synchronize()
+    for x, y in zip(a.download(), b.download()):
+        assert np.array_equal(x, y)
+    cam = scenes.bench_camera(96, 64, 0.5)
+    ia = ctx.render_forward_device(a, cam, retain=False)[0]
+    ib = ctx.render_forward_device(b, cam, retain=False)[0]
+    torch.cuda.synchronize()
+    assert torch.equal(ia, ib)
+
+
 def test_empty_and_offscreen(ctx, orc):
     empty = rgs.GaussianStore.empty(0, 0)
     cam = scenes.bench_camera(40, 24, 0.5)
