@@ -128,6 +128,7 @@ __global__ void __launch_bounds__(256, 5) k_blend_fp32(SplatArrays sp, const uin
                                                     int* slow_count, unsigned long long* counters) {
     __shared__ StagedSplat sm[kTilePixels];
     __shared__ float slm[kTilePixels];
+    __shared__ uint8_t wlist[kTilePixels / 32][32];
     const int tile = blockIdx.x;
     const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -154,10 +155,15 @@ __global__ void __launch_bounds__(256, 5) k_blend_fp32(SplatArrays sp, const uin
         if (warp_done) continue;
         for (int c = 0; c < n; c += 32) {
             const int k0 = c + lane;
-            unsigned mask = __ballot_sync(kFull, k0 < n && overlaps_radial(sm[k0], slm[k0], fsx0, fsy0));
-            while (mask) {
-                const int k = c + __ffs(mask) - 1;
-                mask &= mask - 1;
+            // the window's survivors, compacted in order into the warp's list: the walk below
+            // is a uniform counted loop (index, address and trip count in uniform registers)
+            const bool surv = k0 < n && overlaps_radial(sm[k0], slm[k0], fsx0, fsy0);
+            const unsigned m = __ballot_sync(kFull, surv);
+            if (surv) wlist[warp][__popc(m & ((1u << lane) - 1u))] = (uint8_t)lane;
+            __syncwarp();
+            const int ns = __popc(m);
+            for (int q = 0; q < ns; ++q) {
+                const int k = c + wlist[warp][q];
                 if (done) continue;
                 const float4 a = sm[k].a, b = sm[k].b;
                 float p, M, dx, dy;
@@ -199,6 +205,7 @@ __global__ void __launch_bounds__(256, 5) k_blend_fp32(SplatArrays sp, const uin
                 contrib = (int)(start - rg.x) + k + 1;
                 if (COUNT) ++n_blend;
             }
+            __syncwarp();  // the list is rewritten by the next window
             if (__all_sync(kFull, done)) {
                 warp_done = true;
                 break;
