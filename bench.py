@@ -415,19 +415,24 @@ def run_train_leg(args, ctx, dev, dist, rank, world, flush):
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
     stager.put([host_t[i] for i in views(0)])
+    e2e_losses = []
     for k in range(args.train_steps):
         tg = stager.take()
         if k + 1 < args.train_steps:  # the next step's targets cross PCIe during this step
             stager.put([host_t[i] for i in views(k + 1)])
-        tr.step([cams[i] for i in views(k)], tg)
+        tr.step([cams[i] for i in views(k)], tg, read=False)
         stager.release(ctx)
+        if k > 0:  # step k-1's losses reach the host while step k runs
+            e2e_losses.append(tr.pop_losses().total)
+    e2e_losses.append(tr.pop_losses().total)
     torch.cuda.synchronize(dev)
     e2e_s = max_over_ranks(time.perf_counter() - t0, dist, dev)
+    assert len(e2e_losses) == args.train_steps and all(np.isfinite(e2e_losses))
     e2e = {"value": args.train_steps / e2e_s, "unit": "it/s", "h2d_bytes_per_step": int(B * TRAIN_H * TRAIN_W * 12),
-           "d2h_bytes_per_step": 64, "steps": args.train_steps,
+           "d2h_bytes_per_step": 64 + 8, "steps": args.train_steps,
            "note": "Trainer.step with the batch's target images H2D from pinned host memory each step "
-                   "(train.TargetStager: step k+1's copy overlaps step k) and the loss scalars D2H "
-                   "(one host sync per step)"}
+                   "(train.TargetStager: step k+1's copy overlaps step k) and every step's loss scalars "
+                   "and rotor-error word D2H, read on the host one step behind (Trainer.pop_losses)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

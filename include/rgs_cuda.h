@@ -285,6 +285,11 @@ int rgs_adam_step(rgs_ctx* ctx, rgs_scene* scene, rgs_optimizer* opt, const floa
                   const int32_t* visible, const rgs_adam_config* cfg, int step, double* losses);
 /* Synchronises; returns the ZeroRotor / NonFiniteRotor error of the steps since the last call. */
 int rgs_optimizer_status(rgs_ctx* ctx, rgs_optimizer* opt);
+/* Queues (no host sync) a copy of the optimizer's error word into *word (pinned host memory):
+ * ~0 when no rotor error occurred since the last rgs_optimizer_status, else (index << 8) | code.
+ * Lets a training loop read step k's status while step k+1 runs; rgs_optimizer_status then
+ * raises and clears a reported error. */
+int rgs_optimizer_status_async(rgs_ctx* ctx, rgs_optimizer* opt, unsigned long long* word);
 /* Host arrays: m65 / v65 (N, 65) rows in the order mean4, log_scales4, rotor8, opacity_logit,
  * sh48 channel-major; grad_accum N doubles; grad_count N ints.  Any may be NULL. */
 int rgs_optimizer_download(rgs_ctx* ctx, const rgs_optimizer* opt, double* m65, double* v65,

@@ -1588,6 +1588,14 @@ int rgs_optimizer_status(rgs_ctx* c, rgs_optimizer* o) {
     });
 }
 
+int rgs_optimizer_status_async(rgs_ctx* c, rgs_optimizer* o, unsigned long long* word) {
+    if (!o || !word) return RGS_E_INVALID;
+    return guarded(c, [&]() -> int {
+        CK(cudaMemcpyAsync(word, o->err, sizeof *word, cudaMemcpyDeviceToHost, c->stream));
+        return RGS_OK;
+    });
+}
+
 int rgs_optimizer_download(rgs_ctx* c, const rgs_optimizer* o, double* m65, double* v65, double* grad_accum,
                            int32_t* grad_count) {
     if (!o) return RGS_E_INVALID;

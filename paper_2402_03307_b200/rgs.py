@@ -151,7 +151,7 @@ EXPORTS = [
     "rgs_measure_fp32_tflops", "rgs_project_sliced", "rgs_scene_create_ex", "rgs_scene_params_f64",
     # training side (train.py)
     "rgs_image_loss", "rgs_optimizer_create", "rgs_optimizer_destroy", "rgs_adam_step", "rgs_optimizer_status",
-    "rgs_optimizer_download", "rgs_optimizer_upload", "rgs_optimizer_reset_stats", "rgs_reset_opacity",
+    "rgs_optimizer_status_async", "rgs_optimizer_download", "rgs_optimizer_upload", "rgs_optimizer_reset_stats", "rgs_reset_opacity",
     "rgs_scene_scales", "rgs_knn_build", "rgs_consistency",
     "rgs_scene_load_checkpoint", "rgs_scene_save_checkpoint",
     "rgs_rng_create", "rgs_rng_destroy", "rgs_rng_uniform_int", "rgs_densify_and_prune",
@@ -213,6 +213,7 @@ def load_library(path: str = LIB_PATH):
         "rgs_optimizer_destroy": (None, [p]),
         "rgs_adam_step": (i, [p, p, p, p, p, p, p, i, p]),
         "rgs_optimizer_status": (i, [p, p]),
+        "rgs_optimizer_status_async": (i, [p, p, p]),
         "rgs_optimizer_download": (i, [p, p, p, p, p, p]),
         "rgs_optimizer_upload": (i, [p, p, p, p, p, p]),
         "rgs_optimizer_reset_stats": (i, [p, p]),

@@ -158,6 +158,11 @@ class DeviceOptimizer:
         """Raises the rotor error of the steps since the last call (synchronises)."""
         self.ctx.check(self.ctx.L.rgs_optimizer_status(self.ctx.h, self.h))
 
+    def status_async(self, word) -> None:
+        """Queues the error word's copy into ``word`` (a pinned int64 tensor of one element);
+        no synchronisation.  ~0 (-1 as int64) means no rotor error."""
+        self.ctx.check(self.ctx.L.rgs_optimizer_status_async(self.ctx.h, self.h, _vp(word.data_ptr())))
+
     def download(self):
         n = self.scene.n
         m, v = np.zeros((n, 65)), np.zeros((n, 65))
@@ -421,6 +426,15 @@ class Trainer:
         self.visible = torch.zeros(n, dtype=torch.int32, device=dev)
         self.losses = torch.zeros(8, dtype=torch.float64, device=dev)  # l1, ssim, mse, entropy, consistency
         self.losses_host = torch.zeros(8, dtype=torch.float64).pin_memory()
+        # queued (read=False) loss copies: a ring of two pinned slots with the rotor-error word
+        # and an event each, so step k's losses are read while step k+1 runs (pop_losses)
+        import collections
+
+        self._ring = [torch.zeros(8, dtype=torch.float64).pin_memory() for _ in range(2)]
+        self._ring_err = [torch.zeros(1, dtype=torch.int64).pin_memory() for _ in range(2)]
+        self._ring_ev = [None, None]
+        self._ring_next = 0
+        self._pending = collections.deque()
 
     # trainer.cpp:107-113
     def rebuild_knn(self):
@@ -503,8 +517,9 @@ class Trainer:
         loss + gradients, accumulate_stats, Adam, opacity reset and KNN rebuild schedules.
         ``read``: one host synchronisation per step for the loss scalars (and the rotor-error
         word), as train_from's per-step loss check.  ``read=False`` only queues the copy of the
-        losses (no sync, so the next step's work is enqueued without a bubble); `last_losses()`
-        returns them and raises a deferred rotor error."""
+        losses and of the rotor-error word (no sync, so the next step's work is enqueued without
+        a bubble); `pop_losses()` returns the oldest queued step's (waiting for that step only),
+        `last_losses()` the newest; both raise a deferred rotor error."""
         cfg, w = self.cfg, self.cfg.loss
         self.step_count += 1
         step = self.step_count
@@ -520,8 +535,7 @@ class Trainer:
         if read:
             out = self.read_losses()
         else:
-            self.ctx.fence()
-            self.losses_host.copy_(self.losses, non_blocking=True)
+            self._queue_losses()
             out = None
         mutated = False
         if (self.scene_extent is not None and cfg.densify_from <= step <= cfg.densify_until
@@ -538,19 +552,51 @@ class Trainer:
             self.rebuild_knn()
         return out
 
-    def read_losses(self) -> LossBreakdown:
-        self.ctx.fence()
-        self.losses_host.copy_(self.losses, non_blocking=True)
-        return self.last_losses()
+    def _queue_losses(self):
+        import torch
 
-    def last_losses(self) -> LossBreakdown:
-        """The most recently queued loss copy (synchronises; raises pending rotor errors)."""
-        self.opt.status()  # synchronises the stream; raises rotor errors
-        h = self.losses_host.numpy()
+        slot = self._ring_next
+        self._ring_next ^= 1
+        if slot in self._pending:  # never popped: the oldest queued read is dropped
+            self._pending.remove(slot)
+        self.ctx.fence()
+        self._ring[slot].copy_(self.losses, non_blocking=True)
+        self.opt.status_async(self._ring_err[slot])
+        self._ring_ev[slot] = torch.cuda.current_stream(self.ctx.device).record_event()
+        self._pending.append(slot)
+
+    def _breakdown(self, h) -> LossBreakdown:
         w = self.cfg.loss
         out = LossBreakdown(float(h[0]), float(h[1]), float(h[3]), float(h[4]), 0.0, float(h[2]))
         out.total = combine_losses(w, out.l1, out.ssim, out.entropy, out.consistency)
         return out
+
+    def pop_losses(self) -> LossBreakdown:
+        """The oldest queued (``read=False``) step's losses: waits for that step only (later
+        steps keep running) and raises its rotor error, if any."""
+        slot = self._pending.popleft()
+        self._ring_ev[slot].synchronize()
+        if int(self._ring_err[slot].item()) != -1:
+            self.opt.status()  # raises (and clears) the reported rotor error
+        return self._breakdown(self._ring[slot].numpy())
+
+    def read_losses(self) -> LossBreakdown:
+        """The current losses (synchronises; raises pending rotor errors)."""
+        self.ctx.fence()
+        self.losses_host.copy_(self.losses, non_blocking=True)
+        self.opt.status()  # synchronises the stream; raises rotor errors
+        self._pending.clear()
+        return self._breakdown(self.losses_host.numpy())
+
+    def last_losses(self) -> LossBreakdown:
+        """The most recent loss copy -- a synchronous read or the newest queued one
+        (synchronises; raises pending rotor errors; drops older queued reads)."""
+        self.opt.status()  # synchronises the stream; raises rotor errors
+        if self._pending:
+            slot = self._pending[-1]
+            self._pending.clear()
+            return self._breakdown(self._ring[slot].numpy())
+        return self._breakdown(self.losses_host.numpy())
 
 
 def psnr_from_mse(mse: float) -> float:

@@ -172,10 +172,19 @@ def test_adam_zero_rotor_error(ctx):
     opt = train.DeviceOptimizer(ctx, sc)
     opt.step(_t(np.zeros(65 * n, np.float32)), None, None,
              train.CAdamConfig.from_config(train.TrainConfig(), accumulate_stats=False), 1)
+    import torch
+
+    word = torch.zeros(1, dtype=torch.int64).pin_memory()
+    opt.status_async(word)
+    torch.cuda.synchronize()
+    assert int(word.item()) >> 8 == 17  # (index << 8) | code, queued without a host sync
     with pytest.raises(rgs.ZeroRotorError) as e:
         opt.status()
     assert e.value.index == 17
     opt.status()  # cleared
+    opt.status_async(word)
+    torch.cuda.synchronize()
+    assert int(word.item()) == -1
 
 
 @pytest.mark.parametrize("k", [4, 8])
@@ -471,6 +480,36 @@ def test_target_stager_pipeline(ctx):
     st.put([torch.zeros((4, 4, 3)).pin_memory()])
     with pytest.raises(RuntimeError):
         st.put([torch.zeros((4, 4, 3)).pin_memory()])
+
+
+def test_pipelined_loss_reads(ctx):
+    """read=False + pop_losses (step k's losses read while step k+1 runs) returns the losses
+    the synchronous read returns for the same steps."""
+    store, truth, cams = _training_case(n=3000, views=4)
+    tctx = rgs.Context(0)
+    tsc = DeviceScene.from_store(tctx, truth)
+    targets = [tctx.render_forward_device(tsc, c, retain=False)[0].clone() for c in cams]
+    out = []
+    for pipelined in (False, True):
+        sc = DeviceScene.from_store(tctx, store)
+        tr = train.Trainer(tctx, sc, train.TrainConfig(batch=2))
+        got = []
+        for k in range(5):
+            b = [k % 4, (k + 1) % 4]
+            args = ([cams[i] for i in b], [targets[i] for i in b])
+            if not pipelined:
+                got.append(tr.step(*args).total)
+                continue
+            tr.step(*args, read=False)
+            if k > 0:
+                got.append(tr.pop_losses().total)
+        if pipelined:
+            got.append(tr.pop_losses().total)
+            with pytest.raises(IndexError):
+                tr.pop_losses()
+        out.append(got)
+    assert len(out[1]) == 5
+    assert np.allclose(out[0], out[1], rtol=1e-6, atol=0)  # FP64-atomic order only
 
 
 def test_render_views_host_matches_device(ctx):
