@@ -47,7 +47,8 @@ typedef enum {
     RGS_E_INVALID = 6,         /* bad argument (null pointer, size mismatch, ...) */
     RGS_E_DEGENERATE_TIME = 7, /* DegenerateTimeError escaping gaussian_speed (gaussian.hpp:31-33) */
     RGS_E_NO_DEVICE = 8,       /* no CUDA device: the product has no CPU fallback */
-    RGS_E_CHECKPOINT = 9       /* CheckpointError (checkpoint.hpp:10-12) */
+    RGS_E_CHECKPOINT = 9,      /* CheckpointError (checkpoint.hpp:10-12) */
+    RGS_E_OVERFLOW = 10        /* a deferred-check forward outgrew its pair buffers (re-run it checked) */
 } rgs_status;
 
 /* Render flags. */
@@ -58,6 +59,10 @@ typedef enum {
 #define RGS_FLAG_IMAGE_F64 16u     /* image is double* (implies RGS_FLAG_BLEND_FP64): the reference's Image */
 #define RGS_FLAG_DETERMINISTIC 32u /* backward: FP64, reference summation order, no atomics (bitwise reproducible) */
 #define RGS_FLAG_ACCUMULATE_GRAD 64u /* rgs_image_loss: dL_dimage += instead of = */
+#define RGS_FLAG_DEFER_CHECKS 128u  /* rgs_render_forward / rgs_consistency: no host synchronisation;
+                                       rotor / degenerate-time errors and pair-buffer overflow are
+                                       folded into the context's deferred status word
+                                       (rgs_ctx_status / rgs_ctx_status_async) */
 
 typedef struct rgs_ctx rgs_ctx;
 typedef struct rgs_scene rgs_scene;
@@ -283,6 +288,12 @@ void rgs_optimizer_destroy(rgs_optimizer* opt);
  * Rotor errors are reported by rgs_optimizer_status (no host sync here). */
 int rgs_adam_step(rgs_ctx* ctx, rgs_scene* scene, rgs_optimizer* opt, const float* grads, const float* vnorm,
                   const int32_t* visible, const rgs_adam_config* cfg, int step, double* losses);
+/* The context's deferred status word (RGS_FLAG_DEFER_CHECKS calls): rgs_ctx_status synchronises
+ * and returns (then clears) the first error, with its index in rgs_ctx_error_index;
+ * rgs_ctx_status_async queues a copy of the raw word ((index << 8) | code, ~0 when clean; an
+ * overflow reports code RGS_E_OVERFLOW) into pinned host memory without synchronising. */
+int rgs_ctx_status(rgs_ctx* ctx);
+int rgs_ctx_status_async(rgs_ctx* ctx, unsigned long long* word);
 /* Synchronises; returns the ZeroRotor / NonFiniteRotor error of the steps since the last call. */
 int rgs_optimizer_status(rgs_ctx* ctx, rgs_optimizer* opt);
 /* Queues (no host sync) a copy of the optimizer's error word into *word (pinned host memory):

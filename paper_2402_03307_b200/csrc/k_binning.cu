@@ -539,6 +539,13 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_onesweep(const uint32_t
     }
 }
 
+// RGS_FLAG_DEFER_CHECKS: the view's rotor error / pair-buffer overflow into the context's
+// deferred status word (min wins: the lowest failing index, as the synchronous check).
+__global__ void k_fold_status(const BinState* st, unsigned long long* word, unsigned long long overflow_word) {
+    if (st->err != kNoError) atomicMin(word, st->err);
+    if (st->overflow) atomicMin(word, overflow_word);
+}
+
 // Per-view reset of the binning state in one launch (instead of a pageable H2D copy of the
 // initial BinState and two memsets): counters, depth-key range, capacity, bucket arrays.
 __global__ void k_frame_init(BinState* st, uint32_t pair_cap, uint32_t* bucket_count, uint32_t* bucket_cur, int nb) {
@@ -684,6 +691,10 @@ void tile_radix_sort(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint3
 }
 
 void check_capacity(BinState* st, cudaStream_t s) { k_check_capacity<<<1, 1, 0, s>>>(st); }
+
+void fold_status(const BinState* st, unsigned long long* word, unsigned long long overflow_word, cudaStream_t s) {
+    k_fold_status<<<1, 1, 0, s>>>(st, word, overflow_word);
+}
 
 void frame_init(BinState* st, uint32_t pair_cap, uint32_t* bucket_count, uint32_t* bucket_cur, cudaStream_t s) {
     k_frame_init<<<blocks(kNumBuckets, 256), 256, 0, s>>>(st, pair_cap, bucket_count, bucket_cur, kNumBuckets);

@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <unordered_set>
 #include <vector>
 
 #include "../../include/rgs_cuda.h"
@@ -179,6 +180,7 @@ static const char* kStageNames[kNumStages] = {
     "preprocess_k1", "depth_rank", "pair_offsets_scan", "duplicate_k3", "tile_radix_sort_k4", "blend_fp32_k5",
     "blend_fp64_fixup", "backward_tiles_k6", "backward_fp64_fixup", "backward_gauss_k7"};
 
+struct rgs_records;
 struct rgs_ctx {
     int device = 0;
     cudaStream_t own_stream = nullptr;
@@ -188,6 +190,9 @@ struct rgs_ctx {
     int err_index = -1;
     long long launches = 0;
     Frame scratch;
+    std::unordered_set<rgs_records*> live_records;  // orphaned (not freed) when the context goes first
+    DevBuf deferred;  // u64 deferred status word (RGS_FLAG_DEFER_CHECKS), ~0 when clean
+    unsigned long long* host_word = nullptr;  // pinned
     DevBuf sgrad;     // N x 9 doubles (screen-space gradients)
     DevBuf cgrad;     // N x 3 doubles (the colour path's d mean3, K7a -> K7b)
     DevBuf tile_grads;  // P x 9 doubles (deterministic backward: per (tile, position))
@@ -291,6 +296,10 @@ struct rgs_records {
     Frame* fb = nullptr;
     int retained = 0;
     int n_slow = -1;
+    // RGS_FLAG_DEFER_CHECKS: the forward's BinState copy is in flight (fb->host_stats, complete
+    // at `ready`); resolve() reads it when host-side counts are first needed
+    mutable bool pending = false;
+    cudaEvent_t ready = nullptr;
 };
 
 namespace {
@@ -320,6 +329,22 @@ void frame_put(rgs_ctx* c, PooledFrame* pf) {
 int set_err(rgs_ctx* ctx, int code, const std::string& msg) {
     if (ctx) ctx->err = msg;
     return code;
+}
+
+// Deferred status word of a pair-buffer overflow: index 0, so it reports before rotor errors.
+constexpr unsigned long long kOverflowWord = (unsigned long long)RGS_E_OVERFLOW;
+
+// A deferred-check record's host-side counts (and its overflow), read when first needed.
+int resolve(rgs_ctx* c, const rgs_records* r) {
+    if (!r->pending) return RGS_OK;
+    CK(cudaEventSynchronize(r->ready));
+    const BinState st = *r->fb->host_stats;
+    r->pending = false;
+    r->fb->n_valid = st.n_valid;
+    r->fb->n_pairs = st.n_pairs;
+    if (st.overflow)
+        return set_err(c, RGS_E_OVERFLOW, "deferred-check forward outgrew its pair buffers; re-run it checked");
+    return RGS_OK;
 }
 
 int cuda_fail(rgs_ctx* ctx, const CudaError& e) {
@@ -565,6 +590,7 @@ int rgs_ctx_create(int device, rgs_ctx** out) {
         CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
         CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
         CK(cudaMallocHost(&c->host_stats, sizeof(BinState)));
+        CK(cudaMallocHost(&c->host_word, sizeof(unsigned long long)));
         for (int k = 0; k < rgs_ctx::kSlots; ++k) {
             CK(cudaStreamCreateWithFlags(&c->slot_stream[k], cudaStreamNonBlocking));
             CK(cudaEventCreateWithFlags(&c->slot_done[k], cudaEventDisableTiming));
@@ -578,6 +604,9 @@ int rgs_ctx_create(int device, rgs_ctx** out) {
         CK(cudaDeviceGetDefaultMemPool(&pool, device));
         unsigned long long thresh = ~0ull;
         CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+        c->deferred.ensure(sizeof(unsigned long long), c->own_stream);
+        CK(cudaMemsetAsync(c->deferred.p, 0xff, sizeof(unsigned long long), c->own_stream));
+        CK(cudaStreamSynchronize(c->own_stream));
     } catch (const CudaError& e) {
         delete c;
         return RGS_E_CUDA;
@@ -590,7 +619,20 @@ int rgs_ctx_create(int device, rgs_ctx** out) {
 void rgs_ctx_destroy(rgs_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    for (rgs_records* r : c->live_records) {  // records outliving their context: orphaned
+        r->pf->f.release(c->stream);
+        if (r->pf->free_ev) cudaEventDestroy(r->pf->free_ev);
+        delete r->pf;
+        r->pf = nullptr;
+        r->fb = nullptr;
+        if (r->ready) cudaEventDestroy(r->ready);
+        r->ready = nullptr;
+        r->ctx = nullptr;
+    }
+    c->live_records.clear();
     c->scratch.release(c->stream);
+    c->deferred.release(c->stream);
     c->sgrad.release(c->stream);
     c->cgrad.release(c->stream);
     c->tmp_img.release(c->stream);
@@ -617,6 +659,7 @@ void rgs_ctx_destroy(rgs_ctx* c) {
     for (size_t i = 0; i < c->ev_pool.size(); ++i) cudaEventDestroy(c->ev_pool[i]);
     cudaStreamSynchronize(c->stream);
     if (c->host_stats) cudaFreeHost(c->host_stats);
+    if (c->host_word) cudaFreeHost(c->host_word);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     delete c;
@@ -936,13 +979,29 @@ static int forward_common(rgs_ctx* c, Source src, const rgs_scene* scene, const 
         if (records) {
             rec = new rgs_records;
             rec->ctx = c;
+            c->live_records.insert(rec);
             rec->retained = (flags & RGS_FLAG_RETAIN_RECORDS) ? 1 : 0;
             rec->pf = frame_get(c, c->stream);
             rec->fb = &rec->pf->f;
             f = rec->fb;
         }
-        rc = run_forward(c, *f, c->stream, src, scene, dsp, n_splats, monotone, cam, bg, flags, dimg, flow, true,
+        // Deferred checks (a retained record whose frame already knows its pair capacity): no
+        // host synchronisation; errors and overflow go to the context's deferred status word.
+        const bool defer = (flags & RGS_FLAG_DEFER_CHECKS) && rec && !host_io && f->pair_cap > 0;
+        if (defer) {
+            // no re-render is possible after the fact: 2x headroom over the frame's last checked
+            // pair count (an overflow is still reported, as RGS_E_OVERFLOW, never silent)
+            f->pair_cap = std::max<long long>(f->pair_cap, 2 * f->n_pairs + 1024);
+        }
+        rc = run_forward(c, *f, c->stream, src, scene, dsp, n_splats, monotone, cam, bg, flags, dimg, flow, !defer,
                          nullptr);
+        if (defer && !rc) {
+            rgs_launch::fold_status(f->dstats(), c->deferred.as<unsigned long long>(), kOverflowWord, c->stream);
+            c->launches += 1;
+            if (!rec->ready) CK(cudaEventCreateWithFlags(&rec->ready, cudaEventDisableTiming));
+            CK(cudaEventRecord(rec->ready, c->stream));
+            rec->pending = true;
+        }
         if (rc) {
             if (rec) {
                 frame_put(c, rec->pf);
@@ -1120,15 +1179,23 @@ int rgs_render_views_host(rgs_ctx* c, int n, int sh_degree, const float* mean, c
 // ------------------------------------------------------------------ records
 void rgs_records_destroy(rgs_records* r) {
     if (!r) return;
+    if (!r->ctx) {  // its context was destroyed first and already freed the frame
+        delete r;
+        return;
+    }
     cudaSetDevice(r->ctx->device);
+    r->ctx->live_records.erase(r);
     frame_put(r->ctx, r->pf);
+    if (r->ready) cudaEventDestroy(r->ready);
     delete r;
 }
 
 int rgs_records_info_get(const rgs_records* r, rgs_records_info* info) {
-    if (!r || !info) return RGS_E_INVALID;
+    if (!r || !info || !r->ctx) return RGS_E_INVALID;
     rgs_ctx* c = r->ctx;
-    return guarded(c, [&] {
+    return guarded(c, [&]() -> int {
+        const int rc = resolve(c, r);
+        if (rc) return rc;
         BinState st;
         CK(cudaMemcpyAsync(c->host_stats, r->fb->dstats(), sizeof st, cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
@@ -1147,8 +1214,10 @@ int rgs_records_info_get(const rgs_records* r, rgs_records_info* info) {
 
 int rgs_records_export(rgs_ctx* c, const rgs_records* r, rgs_splat* splats, long long* tile_offsets, int32_t* tile_ids,
                        double* final_T, int32_t* n_contrib) {
-    if (!r) return RGS_E_INVALID;
-    return guarded(c, [&] {
+    if (!r || r->ctx != c) return RGS_E_INVALID;
+    return guarded(c, [&]() -> int {
+        const int rc = resolve(c, r);
+        if (rc) return rc;
         const Frame& f = *r->fb;
         cudaStream_t s = c->stream;
         const int n = f.n;
@@ -1207,7 +1276,7 @@ int rgs_records_export(rgs_ctx* c, const rgs_records* r, rgs_splat* splats, long
 // ------------------------------------------------------------------ backward
 int rgs_render_backward(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* cam, const rgs_records* r,
                         const float* dL_dimage, unsigned flags, float* grads, float* vnorm, int32_t* visible) {
-    if (!scene || !cam || !r || !dL_dimage || !grads || !vnorm || !visible) return RGS_E_INVALID;
+    if (!scene || !cam || !r || !dL_dimage || !grads || !vnorm || !visible || r->ctx != c) return RGS_E_INVALID;
     if (!r->retained)
         return set_err(c, RGS_E_MISSING_RECORDS, "rasterize_backward: forward pass did not retain records");
     if (flags & RGS_FLAG_HOST_BUFFERS) {
@@ -1249,6 +1318,8 @@ int rgs_render_backward(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* ca
         SplatArrays sa = f.arrays();
         const float3 bgf = make_float3((float)f.bg[0], (float)f.bg[1], (float)f.bg[2]);
         if (flags & RGS_FLAG_DETERMINISTIC) {
+            const int rc = resolve(c, r);
+            if (rc) return rc;
             // Reference-order FP64 replay and tile-ordered reduction, no atomics.
             c->tile_grads.ensure(sizeof(double) * 9 * (size_t)std::max<long long>(f.n_pairs, 1), s);
             CK(cudaMemsetAsync(c->tile_grads.p, 0, sizeof(double) * 9 * (size_t)std::max<long long>(f.n_pairs, 1), s));
@@ -1588,6 +1659,32 @@ int rgs_optimizer_status(rgs_ctx* c, rgs_optimizer* o) {
     });
 }
 
+int rgs_ctx_status(rgs_ctx* c) {
+    return guarded(c, [&]() -> int {
+        unsigned long long e = 0;
+        CK(cudaMemcpyAsync(c->host_word, c->deferred.p, sizeof e, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        e = *c->host_word;
+        if (e == kNoError) return RGS_OK;
+        CK(cudaMemsetAsync(c->deferred.p, 0xff, sizeof(unsigned long long), c->stream));
+        const int code = (int)(e & 0xff);
+        c->err_index = (int)(e >> 8);
+        if (code == RGS_E_OVERFLOW)
+            return set_err(c, code, "deferred-check forward outgrew its pair buffers; re-run it checked");
+        if (code == kErrDegenerateTime)
+            return set_err(c, RGS_E_DEGENERATE_TIME, "slice_at: temporal scale collapsed (W < 1e-12)");
+        return set_err(c, code, rotor_msg(code));
+    });
+}
+
+int rgs_ctx_status_async(rgs_ctx* c, unsigned long long* word) {
+    if (!word) return RGS_E_INVALID;
+    return guarded(c, [&]() -> int {
+        CK(cudaMemcpyAsync(word, c->deferred.p, sizeof *word, cudaMemcpyDeviceToHost, c->stream));
+        return RGS_OK;
+    });
+}
+
 int rgs_optimizer_status_async(rgs_ctx* c, rgs_optimizer* o, unsigned long long* word) {
     if (!o || !word) return RGS_E_INVALID;
     return guarded(c, [&]() -> int {
@@ -1771,10 +1868,14 @@ int rgs_consistency(rgs_ctx* c, const rgs_scene* scene, const int32_t* neighbors
         TrainScratch& ts = train_scratch(c);
         ts.speeds.ensure(sizeof(double) * 3 * (size_t)n, s);
         ts.parts.ensure(sizeof(double) * (rgs_launch::consistency_blocks(n) + 16), s);
+        const bool defer = (flags & RGS_FLAG_DEFER_CHECKS) != 0;
         DevBuf err;
-        err.ensure(sizeof(unsigned long long), s);
-        CK(cudaMemsetAsync(err.p, 0xff, sizeof(unsigned long long), s));
-        rgs_launch::speeds(scene->params, scene->params64, n, ts.speeds.as<double>(), err.as<unsigned long long>(), s);
+        if (!defer) {
+            err.ensure(sizeof(unsigned long long), s);
+            CK(cudaMemsetAsync(err.p, 0xff, sizeof(unsigned long long), s));
+        }
+        unsigned long long* errp = defer ? c->deferred.as<unsigned long long>() : err.as<unsigned long long>();
+        rgs_launch::speeds(scene->params, scene->params64, n, ts.speeds.as<double>(), errp, s);
         double* dspeed = nullptr;
         if (grads) {
             ts.dspeed.ensure(sizeof(double) * 3 * (size_t)n, s);
@@ -1785,6 +1886,7 @@ int rgs_consistency(rgs_ctx* c, const rgs_scene* scene, const int32_t* neighbors
                                 (flags & RGS_FLAG_ACCUMULATE) ? 1 : 0, s);
         if (grads) rgs_launch::speed_backward(scene->params, scene->params64, n, dspeed, lambda, grads, s);
         c->launches += 2 + (losses ? 1 : 0) + (grads ? 1 : 0);
+        if (defer) return RGS_OK;  // the speeds' error is in the deferred status word
         unsigned long long e = 0;
         CK(cudaMemcpyAsync(&e, err.p, sizeof e, cudaMemcpyDeviceToHost, s));
         err.release(s);

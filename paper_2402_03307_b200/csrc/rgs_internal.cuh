@@ -147,6 +147,7 @@ void duplicate(const uint32_t* sorted_ids, const uint32_t* pair_off, const uint3
                const ushort4* rect, const BinState* st, int n, int tiles_x, uint32_t* keys, uint32_t* vals,
                int* aux, cudaStream_t s);
 void check_capacity(BinState* st, cudaStream_t s);
+void fold_status(const BinState* st, unsigned long long* word, unsigned long long overflow_word, cudaStream_t s);
 void frame_init(BinState* st, uint32_t pair_cap, uint32_t* bucket_count, uint32_t* bucket_cur, cudaStream_t s);
 int radix_blocks(long long n_pairs);
 size_t radix_count_entries(long long n_pairs);

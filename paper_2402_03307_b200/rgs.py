@@ -39,6 +39,7 @@ RGS_E_INVALID = 6
 RGS_E_DEGENERATE_TIME = 7
 RGS_E_NO_DEVICE = 8
 RGS_E_CHECKPOINT = 9
+RGS_E_OVERFLOW = 10
 
 FLAG_RETAIN_RECORDS = 1
 FLAG_BLEND_FP64 = 2
@@ -47,6 +48,9 @@ FLAG_HOST_BUFFERS = 8
 FLAG_IMAGE_F64 = 16
 FLAG_DETERMINISTIC = 32
 FLAG_ACCUMULATE_GRAD = 64
+FLAG_DEFER_CHECKS = 128
+
+_CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy
 SCENE_F64 = 1  # rgs_scene_create_ex storage flag
 
 
@@ -84,6 +88,11 @@ class CameraError(RuntimeError):
 
 class CheckpointError(RuntimeError):
     """checkpoint.hpp:10-12"""
+
+
+class PairOverflowError(RuntimeError):
+    """A deferred-check forward (FLAG_DEFER_CHECKS) outgrew its pair buffers: its records are
+    incomplete and the work that used them must be re-run with checks."""
 
 
 class DegenerateTimeError(RuntimeError):
@@ -142,6 +151,7 @@ _lib = None
 EXPORTS = [
     "rgs_abi_version", "rgs_device_count", "rgs_ctx_create", "rgs_ctx_destroy", "rgs_ctx_set_stream",
     "rgs_ctx_stream", "rgs_ctx_last_error", "rgs_ctx_error_index", "rgs_ctx_synchronize",
+    "rgs_ctx_status", "rgs_ctx_status_async",
     "rgs_ctx_kernel_launches", "rgs_scene_create", "rgs_scene_destroy", "rgs_scene_size",
     "rgs_scene_set_sh_degree", "rgs_scene_upload_f64", "rgs_scene_upload_f32", "rgs_scene_params",
     "rgs_scene_download_f64", "rgs_render_forward", "rgs_render_views", "rgs_render_views_host",
@@ -178,6 +188,8 @@ def load_library(path: str = LIB_PATH):
         "rgs_ctx_set_stream": (i, [p, p]),
         "rgs_ctx_stream": (p, [p]),
         "rgs_ctx_last_error": (ctypes.c_char_p, [p]),
+        "rgs_ctx_status": (i, [p]),
+        "rgs_ctx_status_async": (i, [p, p]),
         "rgs_ctx_error_index": (i, [p]),
         "rgs_ctx_synchronize": (i, [p]),
         "rgs_ctx_kernel_launches": (ll, [p]),
@@ -412,9 +424,22 @@ class Context:
 
             if torch.cuda.is_available():
                 s = torch.cuda.current_stream(self.device).cuda_stream
-                self.L.rgs_ctx_set_stream(self.h, _vp(s) if s else None)
+                # torch's default stream is the legacy default stream (handle 0): pass
+                # cudaStreamLegacy (0x1) -- NULL would select the context's own stream, which is
+                # not ordered with torch's work on the legacy stream
+                self.L.rgs_ctx_set_stream(self.h, _vp(s if s else _CUDA_STREAM_LEGACY))
         except ImportError:
             pass
+
+    def status(self):
+        """Raises (and clears) the first error of the deferred-check calls since the last call
+        (FLAG_DEFER_CHECKS forwards / consistency); synchronises."""
+        self.check(self.L.rgs_ctx_status(self.h))
+
+    def status_async(self, word) -> None:
+        """Queues a copy of the deferred status word into ``word`` (pinned int64 tensor of one
+        element; -1 = clean), no synchronisation."""
+        self.check(self.L.rgs_ctx_status_async(self.h, _vp(word.data_ptr())))
 
     def fence(self):
         """Order later torch-stream work after this context's stream: a no-op when the context
@@ -422,8 +447,23 @@ class Context:
         if not self._torch_stream:
             self.synchronize()
 
+    def adopt(self, child) -> None:
+        """Registers a handle owner (scene, records, optimizer) to be closed before this
+        context: in a garbage cycle the finalisers run in any order, and a child's destroy
+        call needs its context alive."""
+        import weakref
+
+        if getattr(self, "_children", None) is None:
+            self._children = weakref.WeakSet()
+        self._children.add(child)
+
     def close(self):
         if getattr(self, "h", None):
+            for child in list(getattr(self, "_children", None) or ()):
+                try:
+                    child.close()
+                except Exception:
+                    pass
             self.L.rgs_ctx_destroy(self.h)
             self.h = None
 
@@ -450,6 +490,8 @@ class Context:
             raise NonFiniteRotorError(msg, idx)
         if rc == RGS_E_CAMERA:
             raise CameraError(msg)
+        if rc == RGS_E_OVERFLOW:
+            raise PairOverflowError(msg)
         if rc == RGS_E_CHECKPOINT:
             raise CheckpointError(msg)
         if rc == RGS_E_DEGENERATE_TIME:
@@ -521,7 +563,7 @@ class Context:
         return images_host
 
     def render_forward_device(self, scene: "DeviceScene", cam: Camera, background=(0.0, 0.0, 0.0), retain=True,
-                              blend_fp64=False, image=None):
+                              blend_fp64=False, image=None, defer_checks=False):
         import torch
 
         self.sync_stream()
@@ -530,6 +572,8 @@ class Context:
         c = cam.to_c()
         bg = (ctypes.c_double * 3)(*[float(b) for b in background])
         flags = (FLAG_RETAIN_RECORDS if retain else 0) | (FLAG_BLEND_FP64 if blend_fp64 else 0)
+        if defer_checks:  # no host sync: errors / overflow via status() / status_async()
+            flags |= FLAG_DEFER_CHECKS
         h = _vp()
         self.check(self.L.rgs_render_forward(self.h, scene.h, ctypes.byref(c), bg, flags, _vp(_ptr(image)),
                                              ctypes.byref(h)))
@@ -563,6 +607,7 @@ class DeviceScene:
         h = _vp()
         ctx.check(ctx.L.rgs_scene_create_ex(ctx.h, n, sh_degree, SCENE_F64 if f64 else 0, ctypes.byref(h)))
         self.ctx, self.h, self.n, self.sh_degree, self.f64 = ctx, h, n, sh_degree, f64
+        ctx.adopt(self)
         self.n_inexact = 0
 
     @staticmethod
@@ -587,6 +632,7 @@ class DeviceScene:
         ctx.check(ctx.L.rgs_scene_load_checkpoint(ctx.h, os.fsencode(path), SCENE_F64 if f64 else 0, ctypes.byref(h)))
         s = DeviceScene.__new__(DeviceScene)
         s.ctx, s.h, s.f64, s.n_inexact = ctx, h, f64, 0
+        ctx.adopt(s)
         s.n = int(ctx.L.rgs_scene_size(h))
         s.sh_degree = -1
         return s
@@ -621,7 +667,8 @@ class DeviceScene:
 
     def close(self):
         if getattr(self, "h", None):
-            self.ctx.L.rgs_scene_destroy(self.h)
+            if getattr(self.ctx, "h", None):  # (a closed context already freed it)
+                self.ctx.L.rgs_scene_destroy(self.h)
             self.h = None
 
     def __del__(self):
@@ -639,13 +686,23 @@ class RenderRecords:
         self.background = np.asarray(background, dtype=np.float64)
         self.retained = bool(retained)
         self._cache = None
-        info = CRecordsInfo()
-        ctx.check(ctx.L.rgs_records_info_get(handle, ctypes.byref(info)))
-        self.tiles_x, self.tiles_y = info.tiles_x, info.tiles_y
-        self.n_pairs = info.n_pairs
-        self.n_slow_pixels = info.n_slow_pixels
-        self.width, self.height = info.width, info.height
-        self._n_splats = info.n_splats
+        self._info = None  # read on first use (the read synchronises)
+        ctx.adopt(self)
+
+    def _get_info(self):
+        if self._info is None:
+            info = CRecordsInfo()
+            self.ctx.check(self.ctx.L.rgs_records_info_get(self.h, ctypes.byref(info)))
+            self._info = info
+        return self._info
+
+    tiles_x = property(lambda self: self._get_info().tiles_x)
+    tiles_y = property(lambda self: self._get_info().tiles_y)
+    n_pairs = property(lambda self: self._get_info().n_pairs)
+    n_slow_pixels = property(lambda self: self._get_info().n_slow_pixels)
+    width = property(lambda self: self._get_info().width)
+    height = property(lambda self: self._get_info().height)
+    _n_splats = property(lambda self: self._get_info().n_splats)
 
     def _export(self):
         if self._cache is None:
@@ -688,7 +745,7 @@ class RenderRecords:
 
     def close(self):
         if getattr(self, "h", None):
-            self.ctx.L.rgs_records_destroy(self.h)
+            self.ctx.L.rgs_records_destroy(self.h)  # safe after the context: orphaned records
             self.h = None
 
     def __del__(self):

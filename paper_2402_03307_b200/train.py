@@ -144,6 +144,7 @@ class DeviceOptimizer:
         h = _vp()
         ctx.check(ctx.L.rgs_optimizer_create(ctx.h, scene.h, ctypes.byref(h)))
         self.ctx, self.scene, self.h = ctx, scene, h
+        ctx.adopt(self)
 
     def step(self, grads, vnorm, visible, cfg: CAdamConfig, step: int, losses=None):
         """adam_step (+ accumulate_stats, + entropy) on device buffers; no host sync."""
@@ -189,7 +190,8 @@ class DeviceOptimizer:
 
     def close(self):
         if getattr(self, "h", None):
-            self.ctx.L.rgs_optimizer_destroy(self.h)
+            if getattr(self.ctx, "h", None):  # (a closed context already freed it)
+                self.ctx.L.rgs_optimizer_destroy(self.h)
             self.h = None
 
     def __del__(self):
@@ -300,11 +302,13 @@ def build_knn4d(ctx: Context, scene: DeviceScene, k: int, scales=None, out=None)
     return out
 
 
-def consistency(ctx: Context, scene: DeviceScene, nbrs, lam: float, grads=None, losses=None, accumulate=False):
-    """consistency_loss + its gradient through slice_backward (trainer.cpp:66-77)."""
+def consistency(ctx: Context, scene: DeviceScene, nbrs, lam: float, grads=None, losses=None, accumulate=False,
+                defer_checks=False):
+    """consistency_loss + its gradient through slice_backward (trainer.cpp:66-77).
+    ``defer_checks``: no host sync; a rotor / degenerate-time error goes to ctx.status()."""
     ctx.sync_stream()
-    ctx.check(ctx.L.rgs_consistency(ctx.h, scene.h, _vp(_ptr(nbrs)), int(nbrs.shape[1]), float(lam),
-                                    rgs.FLAG_ACCUMULATE if accumulate else 0,
+    flags = (rgs.FLAG_ACCUMULATE if accumulate else 0) | (rgs.FLAG_DEFER_CHECKS if defer_checks else 0)
+    ctx.check(ctx.L.rgs_consistency(ctx.h, scene.h, _vp(_ptr(nbrs)), int(nbrs.shape[1]), float(lam), flags,
                                     _vp(_ptr(grads)) if grads is not None else None,
                                     _vp(_ptr(losses)) if losses is not None else None))
 
@@ -409,6 +413,12 @@ class Trainer:
         self._dl = None
         self._streams = None
         self.overlap = True  # forward of view v+1 alongside the backward of view v
+        # Deferred checks: the step's forwards and consistency term do not synchronise; their
+        # rotor / degenerate-time errors and pair-buffer overflows surface at the step's loss
+        # read (read_losses / pop_losses / last_losses).  The first step and the step after a
+        # densification run checked (they size the pair buffers).
+        self.defer_checks = True
+        self._checked_next = True
         self._alloc()
 
     def _alloc(self):
@@ -432,6 +442,7 @@ class Trainer:
 
         self._ring = [torch.zeros(8, dtype=torch.float64).pin_memory() for _ in range(2)]
         self._ring_err = [torch.zeros(1, dtype=torch.int64).pin_memory() for _ in range(2)]
+        self._ring_ctx = [torch.zeros(1, dtype=torch.int64).pin_memory() for _ in range(2)]
         self._ring_ev = [None, None]
         self._ring_next = 0
         self._pending = collections.deque()
@@ -454,13 +465,14 @@ class Trainer:
             self._dl = [torch.empty(shape, dtype=torch.float32, device=dev) for _ in range(2)]
         return self._img[slot], self._dl[slot]
 
-    def evaluate_loss(self, cams: Sequence[Camera], targets, want_grads: bool = True):
+    def evaluate_loss(self, cams: Sequence[Camera], targets, want_grads: bool = True, defer: bool = False):
         """trainer.cpp:22-84 for this rank's views (device tensors); leaves the batch-reduced
         gradients in self.grads / vnorm / visible and the losses in self.losses (device).
 
         With ``overlap`` (default) the forward of view v+1 runs on a side stream while the loss
         and backward of view v run on the main stream; the backward passes stay in view order
-        on the main stream (they accumulate into one gradient buffer)."""
+        on the main stream (they accumulate into one gradient buffer).  ``defer``: the forwards
+        and the consistency term skip their host synchronisation (errors via ctx.status())."""
         import torch
 
         w = self.cfg.loss
@@ -489,11 +501,12 @@ class Trainer:
                     side.wait_event(free[slot])
                 with torch.cuda.stream(side):
                     img, rec = ctx.render_forward_device(scene, cam, self.cfg.background, retain=want_grads,
-                                                         image=img)
+                                                         image=img, defer_checks=defer)
                 main.wait_stream(side)
                 ctx.sync_stream()
             else:
-                img, rec = ctx.render_forward_device(scene, cam, self.cfg.background, retain=want_grads, image=img)
+                img, rec = ctx.render_forward_device(scene, cam, self.cfg.background, retain=want_grads, image=img,
+                                                     defer_checks=defer)
             image_loss(ctx, img, tgt, wl1, wss, dl if want_grads else None, self.losses, loss_scale=inv_b,
                        accumulate=True)
             if want_grads:
@@ -510,7 +523,7 @@ class Trainer:
                 torch.cuda.current_stream(ctx.device).synchronize()
         if w.lambda_consistency != 0 and self.nbrs is not None and scene.n > 0:
             consistency(ctx, scene, self.nbrs, w.lambda_consistency, self.grads if want_grads else None,
-                        self.losses[4:5])
+                        self.losses[4:5], defer_checks=defer)
 
     def step(self, cams: Sequence[Camera], targets, read: bool = True) -> Optional[LossBreakdown]:
         """One train_from iteration minus densification (trainer.cpp:115-150): SH unlock, batch
@@ -529,7 +542,9 @@ class Trainer:
             self.scene.sh_degree = sh
         if self.nbrs is None and step == 1:
             self.rebuild_knn()
-        self.evaluate_loss(cams, targets, True)
+        defer = self.defer_checks and not self._checked_next
+        self._checked_next = False
+        self.evaluate_loss(cams, targets, True, defer=defer)
         acfg = CAdamConfig.from_config(cfg, w.lambda_entropy, True)
         self.opt.step(self.grads, self.vnorm, self.visible, acfg, step, self.losses[3:4])
         if read:
@@ -545,6 +560,7 @@ class Trainer:
             self.last_densify = densify_and_prune(self.ctx, self.scene, self.opt, cfg, self.scene_extent, self.rng)
             self._alloc()
             mutated = True
+            self._checked_next = True  # the scene changed size: re-learn the pair capacities
         if step % cfg.opacity_reset_interval == 0:
             self.opt.reset_opacity(cfg.reset_opacity_value)
         if mutated or step % cfg.knn_rebuild_interval == 0:
@@ -562,6 +578,7 @@ class Trainer:
         self.ctx.fence()
         self._ring[slot].copy_(self.losses, non_blocking=True)
         self.opt.status_async(self._ring_err[slot])
+        self.ctx.status_async(self._ring_ctx[slot])
         self._ring_ev[slot] = torch.cuda.current_stream(self.ctx.device).record_event()
         self._pending.append(slot)
 
@@ -576,6 +593,8 @@ class Trainer:
         steps keep running) and raises its rotor error, if any."""
         slot = self._pending.popleft()
         self._ring_ev[slot].synchronize()
+        if int(self._ring_ctx[slot].item()) != -1:
+            self.ctx.status()  # raises (and clears) a deferred forward / consistency error
         if int(self._ring_err[slot].item()) != -1:
             self.opt.status()  # raises (and clears) the reported rotor error
         return self._breakdown(self._ring[slot].numpy())
@@ -584,14 +603,16 @@ class Trainer:
         """The current losses (synchronises; raises pending rotor errors)."""
         self.ctx.fence()
         self.losses_host.copy_(self.losses, non_blocking=True)
-        self.opt.status()  # synchronises the stream; raises rotor errors
+        self.ctx.status()  # synchronises; raises deferred forward / consistency errors
+        self.opt.status()  # raises rotor errors of the Adam step
         self._pending.clear()
         return self._breakdown(self.losses_host.numpy())
 
     def last_losses(self) -> LossBreakdown:
         """The most recent loss copy -- a synchronous read or the newest queued one
         (synchronises; raises pending rotor errors; drops older queued reads)."""
-        self.opt.status()  # synchronises the stream; raises rotor errors
+        self.ctx.status()  # synchronises; raises deferred forward / consistency errors
+        self.opt.status()  # raises rotor errors of the Adam step
         if self._pending:
             slot = self._pending[-1]
             self._pending.clear()

@@ -163,6 +163,48 @@ def test_scene_params_tensor_view(ctx):
     assert torch.equal(ia, ib)
 
 
+def test_deferred_checks(ctx):
+    """FLAG_DEFER_CHECKS forwards: no host sync, same image and records as a checked forward;
+    a rotor error and a pair-buffer overflow surface through the context status (and the
+    records), never silently."""
+    import torch
+
+    tctx = rgs.Context(0)
+    store = scenes.synthetic_scene(3000, 160, 120, seed=5)
+    cam = scenes.bench_camera(160, 120, 0.5)
+    sc = rgs.DeviceScene.from_store(tctx, store)
+    img0, rec0 = tctx.render_forward_device(sc, cam)  # checked: sizes the pooled frame
+    ref = (img0.clone(), rec0.n_pairs, rec0.tile_ids.copy())
+    rec0.close()
+    img1, rec1 = tctx.render_forward_device(sc, cam, defer_checks=True)
+    tctx.status()
+    assert torch.equal(img1, ref[0]) and rec1.n_pairs == ref[1]
+    assert np.array_equal(rec1.tile_ids, ref[2])
+    rec1.close()
+    # rotor error: reported by status(), not by the call
+    bad = store.copy()
+    bad.rotor[21] = 0
+    bsc = rgs.DeviceScene.from_store(tctx, bad)
+    _, rec2 = tctx.render_forward_device(bsc, cam, defer_checks=True)
+    with pytest.raises(rgs.ZeroRotorError) as e:
+        tctx.status()
+    assert e.value.index == 21
+    tctx.status()  # cleared
+    rec2.close()
+    # overflow: a pooled frame sized by the scenes above, then a ~7x denser one without checks
+    sparse = rgs.DeviceScene.from_store(tctx, scenes.synthetic_scene(200, 160, 120, seed=6))
+    _, r = tctx.render_forward_device(sparse, cam)
+    r.close()
+    dense = rgs.DeviceScene.from_store(tctx, scenes.synthetic_scene(20000, 160, 120, seed=7))
+    _, r = tctx.render_forward_device(dense, cam, defer_checks=True)
+    with pytest.raises(rgs.PairOverflowError):
+        tctx.status()
+    with pytest.raises(rgs.PairOverflowError):
+        r.n_pairs
+    r.close()
+    tctx.status()
+
+
 def test_empty_and_offscreen(ctx, orc):
     empty = rgs.GaussianStore.empty(0, 0)
     cam = scenes.bench_camera(40, 24, 0.5)
