@@ -469,9 +469,9 @@ class Trainer:
         """trainer.cpp:22-84 for this rank's views (device tensors); leaves the batch-reduced
         gradients in self.grads / vnorm / visible and the losses in self.losses (device).
 
-        With ``overlap`` (default) the forward of view v+1 runs on a side stream while the loss
-        and backward of view v run on the main stream; the backward passes stay in view order
-        on the main stream (they accumulate into one gradient buffer).  ``defer``: the forwards
+        With ``overlap`` (default) the forward and image loss of view v+1 run on a side stream
+        while the backward of view v runs on the main stream; the losses and the backward
+        passes each stay in view order (they accumulate into one buffer).  ``defer``: the forwards
         and the consistency term skip their host synchronisation (errors via ctx.status())."""
         import torch
 
@@ -492,23 +492,31 @@ class Trainer:
         start = main.record_event() if overlap else None
         free = [start, start]
         recs = []
+        loss_done = None  # the previous view's image loss (its scratch and the loss slots are shared)
         for v, (cam, tgt) in enumerate(zip(cams, targets)):
             slot = v % 2 if overlap else 0
             img, dl = self._buffers(cam, slot)
             if overlap:
+                # side stream: forward of view v, then its image loss (FP64, SSIM) -- so the loss
+                # overlaps the FP32 backward of view v - 1 on the main stream
                 side = self._streams[slot]
                 if free[slot] is not None:
                     side.wait_event(free[slot])
                 with torch.cuda.stream(side):
                     img, rec = ctx.render_forward_device(scene, cam, self.cfg.background, retain=want_grads,
                                                          image=img, defer_checks=defer)
+                    if loss_done is not None:
+                        side.wait_event(loss_done)
+                    image_loss(ctx, img, tgt, wl1, wss, dl if want_grads else None, self.losses, loss_scale=inv_b,
+                               accumulate=True)
+                    loss_done = side.record_event()
                 main.wait_stream(side)
                 ctx.sync_stream()
             else:
                 img, rec = ctx.render_forward_device(scene, cam, self.cfg.background, retain=want_grads, image=img,
                                                      defer_checks=defer)
-            image_loss(ctx, img, tgt, wl1, wss, dl if want_grads else None, self.losses, loss_scale=inv_b,
-                       accumulate=True)
+                image_loss(ctx, img, tgt, wl1, wss, dl if want_grads else None, self.losses, loss_scale=inv_b,
+                           accumulate=True)
             if want_grads:
                 ctx.render_backward_device(scene, cam, rec, dl, self.grads, self.vnorm, self.visible, accumulate=True)
             if overlap:
