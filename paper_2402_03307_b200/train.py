@@ -491,6 +491,12 @@ class Trainer:
         # previous step (its Adam update of the scene) and of the buffer zeroing above
         start = main.record_event() if overlap else None
         free = [start, start]
+        # On one rank the consistency term (it depends on the scene only) runs first, on the main
+        # stream, beside the first view's forward on the side stream; with N ranks it is added
+        # after the all-reduce (it is a once-per-step term of the replicated scene).
+        early_consistency = self.world == 1
+        if early_consistency:
+            self._consistency(want_grads, defer)
         recs = []
         loss_done = None  # the previous view's image loss (its scratch and the loss slots are shared)
         for v, (cam, tgt) in enumerate(zip(cams, targets)):
@@ -529,8 +535,13 @@ class Trainer:
             allreduce_step_buffers(self.gbuf, self.visible, self.losses[:3], self.dist)
             if not ctx._torch_stream:
                 torch.cuda.current_stream(ctx.device).synchronize()
-        if w.lambda_consistency != 0 and self.nbrs is not None and scene.n > 0:
-            consistency(ctx, scene, self.nbrs, w.lambda_consistency, self.grads if want_grads else None,
+        if not early_consistency:
+            self._consistency(want_grads, defer)
+
+    def _consistency(self, want_grads: bool, defer: bool):
+        w = self.cfg.loss
+        if w.lambda_consistency != 0 and self.nbrs is not None and self.scene.n > 0:
+            consistency(self.ctx, self.scene, self.nbrs, w.lambda_consistency, self.grads if want_grads else None,
                         self.losses[4:5], defer_checks=defer)
 
     def step(self, cams: Sequence[Camera], targets, read: bool = True) -> Optional[LossBreakdown]:
