@@ -308,6 +308,10 @@ __global__ void k_accumulate_stats(const TV* __restrict__ vnorm, const int32_t* 
 // K9: fused optimizer step, one thread per Gaussian (optim.cpp:110-166).
 __device__ __forceinline__ void adam_scalar(double& p, double& m, double& v, double g, double lr, double bc1,
                                             double bc2) {
+    // An all-zero (m, v, g) -- e.g. the SH coefficients above the active degree -- is a bitwise
+    // no-op of the update below (m and v stay +0, p - 0 = p); skipping it avoids three IEEE
+    // divisions and a square root of zero operands (their slow paths).
+    if (g == 0 && m == 0 && v == 0) return;
     // optim.cpp:19-23 (kAdamBeta1 = 0.9, kAdamBeta2 = 0.999, kAdamEps = 1e-15)
     m = 0.9 * m + (1 - 0.9) * g;
     v = 0.999 * v + (1 - 0.999) * g * g;
