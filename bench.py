@@ -507,13 +507,19 @@ def run_ours(args, rank, local_rank, world):
     def sweep():
         ctx.render_views(scene, cams, (0.0, 0.0, 0.0), out=images)
 
-    for _ in range(max(args.warmup, 1)):
-        sweep()
-    torch.cuda.synchronize(dev)
     if args.profile_only:
+        for _ in range(max(args.warmup, 1)):
+            sweep()
         sweep()
         torch.cuda.synchronize(dev)
         return
+    # K5 is timed live (CUDA events around each blend on its own stream) through warm-up and
+    # the timed region: the roofline's denominator is its duration inside the measured run
+    ctx.set_profiling(timing="live", count_evals=False)
+    for _ in range(max(args.warmup, args.steps, 1)):  # (also sizes the context's event pool)
+        sweep()
+    torch.cuda.synchronize(dev)
+    ctx.profile_reset()
 
     # ---- timed region: K sweeps, L2 flushed between sweeps.  Views are pipelined over
     # three streams inside each sweep; the CUDA events are on the torch current stream,
@@ -539,6 +545,9 @@ def run_ours(args, rank, local_rank, world):
     if dist:
         dist.barrier()
     clocks = sampler.stop()
+    live, _ = ctx.profile_read()
+    ctx.set_profiling(timing=False, count_evals=False)
+    k5_live_ms, k5_live_n = live.get("blend_fp32_k5", (0.0, 0))
     launches = ctx.kernel_launches - launches0
     step_ms = [a.elapsed_time(b) for a, b in evs]
     total_ms = sum(step_ms)
@@ -600,7 +609,18 @@ def run_ours(args, rank, local_rank, world):
     for name, (bound, work, unit, peak) in kernels.items():
         if name in per_stage and per_stage[name]["ms_per_frame"] > 0:
             ach = work / (per_stage[name]["ms_per_frame"] / 1e3)
-            roof_all[name] = {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak}
+            roof_all[name] = {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
+                              "timing": "serialised profiling sweep"}
+    if k5_live_n and "blend_fp32_k5" in roof_all:
+        # the headline roofline: K5's average duration measured live over the timed region
+        r = roof_all["blend_fp32_k5"]
+        work = kernels["blend_fp32_k5"][1]
+        live_ms = k5_live_ms / k5_live_n
+        r.update({"achieved_serialised": r["achieved"], "frac_serialised": r["frac"],
+                  "achieved": work / (live_ms / 1e3), "frac": work / (live_ms / 1e3) / r["peak"],
+                  "ms_per_launch": live_ms, "ms_per_launch_serialised": per_stage["blend_fp32_k5"]["ms_per_frame"],
+                  "timing": f"CUDA events around each of the {k5_live_n} K5 launches of the timed region, on "
+                            "its own stream (views pipelined over 3 streams, so it shares the GPU)"})
     dominant = max(per_stage, key=lambda k: per_stage[k]["share"]) if per_stage else None
     traffic = None
     try:

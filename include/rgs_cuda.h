@@ -115,9 +115,11 @@ int rgs_ctx_synchronize(rgs_ctx* ctx);
 long long rgs_ctx_kernel_launches(const rgs_ctx* ctx);
 
 /* ---------------------------------------------------------------- profiling */
-/* Per-stage CUDA-event timing on the launching stream (timing != 0) and
- * counting of evaluated / blended (pixel, splat) pairs in the FP32 blend
- * (count_evals != 0; the E and B of the blend roofline). */
+/* Per-stage CUDA-event timing on the launching stream and counting of evaluated / blended
+ * (pixel, splat) pairs in the FP32 blend (count_evals != 0; the E and B of the blend roofline).
+ * timing == 1: every stage, views serialised (each stage's own duration);
+ * timing == 2: live -- only the FP32 blend (K5), on its stream, views still pipelined (its
+ * duration inside a normal run, sharing the GPU). */
 int rgs_profile_num_stages(void);
 const char* rgs_profile_stage_name(int stage);
 int rgs_ctx_set_profiling(rgs_ctx* ctx, int timing, int count_evals);

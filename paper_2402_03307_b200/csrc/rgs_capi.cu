@@ -200,7 +200,7 @@ struct rgs_ctx {
     DevBuf tmp_splats, tmp_scan, tmp_ids;
     BinState* host_stats = nullptr;  // pinned
     // profiling: CUDA events around every stage, on the launching stream
-    bool timing = false;
+    int timing = 0;  // 1: all stages, serialised views; 2: live K5 timing (see rgs_ctx_set_profiling)
     bool count_evals = false;
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
@@ -259,13 +259,13 @@ struct StageTimer {
     cudaStream_t s;
     cudaEvent_t a = nullptr;
     StageTimer(rgs_ctx* ctx, int st, cudaStream_t stream) : c(ctx), stage(st), s(stream) {
-        if (c->timing) {
+        if (c->timing == 1 || (c->timing == 2 && stage == kStBlend)) {
             a = c->next_event();
             CK(cudaEventRecord(a, s));
         }
     }
     ~StageTimer() {
-        if (c->timing && a) {
+        if (a) {
             cudaEvent_t b = c->next_event();
             cudaEventRecord(b, s);
             c->pending.push_back({stage, a, b});
@@ -681,7 +681,7 @@ const char* rgs_profile_stage_name(int k) { return (k >= 0 && k < kNumStages) ? 
 int rgs_ctx_set_profiling(rgs_ctx* c, int timing, int count_evals) {
     return guarded(c, [&] {
         c->collect();
-        c->timing = timing != 0;
+        c->timing = timing < 0 ? 0 : (timing > 2 ? 1 : timing);
         c->count_evals = count_evals != 0;
         if (c->count_evals) {
             c->counters.ensure(64, c->stream);
@@ -1059,7 +1059,7 @@ int render_batch(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* cams, int
     for (int k = 0; k < rgs_ctx::kSlots; ++k) CK(cudaStreamWaitEvent(c->slot_stream[k], c->join_ev, 0));
     // Profiling mode serialises the views (one slot) so per-stage event times are the
     // kernels' own durations rather than shares of concurrently running views.
-    const int slots = c->timing ? 1 : rgs_ctx::kSlots;
+    const int slots = c->timing == 1 ? 1 : rgs_ctx::kSlots;
     for (int v = 0; v < n_views; ++v) {
         const int k = v % slots;
         cudaStream_t s = c->slot_stream[k];

@@ -504,8 +504,11 @@ class Context:
         self.check(self.L.rgs_ctx_synchronize(self.h))
 
     # --- profiling (CUDA events per pipeline stage, on the launching stream)
-    def set_profiling(self, timing: bool = True, count_evals: bool = False):
-        self.check(self.L.rgs_ctx_set_profiling(self.h, int(timing), int(count_evals)))
+    def set_profiling(self, timing=True, count_evals: bool = False):
+        """timing: True / 1 = every stage, views serialised; "live" / 2 = only the FP32 blend,
+        timed on its own stream inside a normal (pipelined) run."""
+        t = 2 if timing == "live" else int(timing)
+        self.check(self.L.rgs_ctx_set_profiling(self.h, t, int(count_evals)))
 
     def slow_reasons(self):
         """{reason: count} of the FP32 blend's slow-pixel decisions (count_evals profiling)."""
