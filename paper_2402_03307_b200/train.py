@@ -415,8 +415,9 @@ class Trainer:
         self.overlap = True  # forward of view v+1 alongside the backward of view v
         # Deferred checks: the step's forwards and consistency term do not synchronise; their
         # rotor / degenerate-time errors and pair-buffer overflows surface at the step's loss
-        # read (read_losses / pop_losses / last_losses).  The first step and the step after a
-        # densification run checked (they size the pair buffers).
+        # read (read_losses / pop_losses / last_losses).  The first step, the step after a
+        # densification and one step per KNN-rebuild interval run checked (they size the pair
+        # buffers).
         self.defer_checks = True
         self._checked_next = True
         self._alloc()
@@ -585,6 +586,9 @@ class Trainer:
         if mutated or step % cfg.knn_rebuild_interval == 0:
             self.nbrs = None
             self.rebuild_knn()
+            # a checked step now and then re-learns the pair counts the deferred forwards' 2x
+            # buffer headroom is based on (splats grow between densifications too)
+            self._checked_next = True
         return out
 
     def _queue_losses(self):
