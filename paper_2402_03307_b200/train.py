@@ -413,6 +413,7 @@ class Trainer:
         self._dl = None
         self._streams = None
         self.overlap = True  # forward of view v+1 alongside the backward of view v
+        self.n_slots = 3  # views whose forward / loss may be in flight at once (side streams)
         # Deferred checks: the step's forwards and consistency term do not synchronise; their
         # rotor / degenerate-time errors and pair-buffer overflows surface at the step's loss
         # read (read_losses / pop_losses / last_losses).  The first step, the step after a
@@ -462,8 +463,8 @@ class Trainer:
         shape = (cam.height, cam.width, 3)
         if self._img is None or tuple(self._img[0].shape) != shape:
             dev = f"cuda:{self.ctx.device}"
-            self._img = [torch.empty(shape, dtype=torch.float32, device=dev) for _ in range(2)]
-            self._dl = [torch.empty(shape, dtype=torch.float32, device=dev) for _ in range(2)]
+            self._img = [torch.empty(shape, dtype=torch.float32, device=dev) for _ in range(self.n_slots)]
+            self._dl = [torch.empty(shape, dtype=torch.float32, device=dev) for _ in range(self.n_slots)]
         return self._img[slot], self._dl[slot]
 
     def evaluate_loss(self, cams: Sequence[Camera], targets, want_grads: bool = True, defer: bool = False):
@@ -487,11 +488,11 @@ class Trainer:
         overlap = self.overlap and ctx._torch_stream and len(cams) > 1
         main = torch.cuda.current_stream(ctx.device)
         if overlap and self._streams is None:
-            self._streams = [torch.cuda.Stream(ctx.device), torch.cuda.Stream(ctx.device)]
+            self._streams = [torch.cuda.Stream(ctx.device) for _ in range(self.n_slots)]
         # per buffer slot: event after its last use on the main stream; initially the end of the
         # previous step (its Adam update of the scene) and of the buffer zeroing above
         start = main.record_event() if overlap else None
-        free = [start, start]
+        free = [start] * self.n_slots
         # On one rank the consistency term (it depends on the scene only) runs first, on the main
         # stream, beside the first view's forward on the side stream; with N ranks it is added
         # after the all-reduce (it is a once-per-step term of the replicated scene).
@@ -501,7 +502,7 @@ class Trainer:
         recs = []
         loss_done = None  # the previous view's image loss (its scratch and the loss slots are shared)
         for v, (cam, tgt) in enumerate(zip(cams, targets)):
-            slot = v % 2 if overlap else 0
+            slot = v % self.n_slots if overlap else 0
             img, dl = self._buffers(cam, slot)
             if overlap:
                 # side stream: forward of view v, then its image loss (FP64, SSIM) -- so the loss
