@@ -598,7 +598,7 @@ __device__ __forceinline__ void sh_rows(const ParamView& P, int i, int K, const 
 // is recomputed bit-identically either way).  Split from K7b so neither kernel carries the
 // SH basis gradients and the slice state at once (K7 was 255 registers with spills).
 template <bool F64>
-__global__ void __launch_bounds__(128) k_color_backward(ParamView P, int sh_degree, const uint8_t* __restrict__ valid,
+__global__ void __launch_bounds__(128, 6) k_color_backward(ParamView P, int sh_degree, const uint8_t* __restrict__ valid,
                                                         const double4* __restrict__ dir_dist,
                                                         const double* __restrict__ sgrad, int accumulate,
                                                         float* grads, double* cdm3) {
