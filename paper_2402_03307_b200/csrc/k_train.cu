@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(128) k_adam_plain(void* params, void* mom1, vo
 }
 
 template <bool F64>
-__global__ void __launch_bounds__(128) k_adam_step(void* params, void* mom1, void* mom2, const float* __restrict__ grads,
+__global__ void __launch_bounds__(128, 6) k_adam_step(void* params, void* mom1, void* mom2, const float* __restrict__ grads,
                                                    const float* __restrict__ vnorm, const int32_t* __restrict__ visible,
                                                    double* __restrict__ accum, int32_t* __restrict__ count, int n,
                                                    AdamArgs a, unsigned long long* err, double* part_entropy) {
