@@ -68,7 +68,7 @@ constexpr size_t k8a_smem_bytes() {
 }
 
 template <typename TI>
-__global__ void __launch_bounds__(kSsimAThreads) k_ssim_fields(const TI* __restrict__ img, const TI* __restrict__ tgt,
+__global__ void __launch_bounds__(kSsimAThreads, 3) k_ssim_fields(const TI* __restrict__ img, const TI* __restrict__ tgt,
                                                      int W, int H, int want_grad, double* __restrict__ dfield,
                                                      double* __restrict__ part_ssim) {
     constexpr int TX = kSsimTX, TY = kSsimATY, IX = TX + kSsimWin - 1, IY = TY + kSsimWin - 1;
