@@ -41,6 +41,10 @@ L2_FLUSH_BYTES = 256 << 20
 # Training leg (config C3, reported under "train"): D-NeRF-shaped 800x800, 200K Gaussians,
 # TrainConfig's default batch of 3 camera x timestamp views per step and rank.
 TRAIN_N, TRAIN_W, TRAIN_H, TRAIN_BATCH, TRAIN_SEED, TRAIN_VIEWS = 200_000, 800, 800, 3, 3, 24
+# Training legs resume a run at step 3000 of 6000, i.e. after the last SH unlock
+# (active degree min(3, (step - 1) // sh_unlock_interval) = 3, trainer.cpp:135): every
+# warm-up and timed step computes and updates all 48 SH coefficients.
+TRAIN_START_STEP, TRAIN_TOTAL_STEPS = 3000, 6000
 TRAIN_WORKLOAD = ("C3: 200K 4D rotor Gaussians, SH deg 3, 800x800, batch of 3 camera x timestamp views per rank "
                   "and step: render fwd + L1/SSIM image gradient + render bwd + batch all-reduce + entropy + "
                   "consistency (exact 4D KNN, k=8) + accumulate_stats + Adam")
@@ -284,13 +288,14 @@ def run_c5_leg(args, ctx, dev, dist, rank, world, flush):
     tsc.close()
     del truth
     scene = rgs.DeviceScene.from_store(ctx, store)
-    tr = train.Trainer(ctx, scene, train.TrainConfig(batch=C5_VIEWS, total_steps=2000, max_gaussians=2_000_000),
-                       dist)
+    tr = train.Trainer(ctx, scene, train.TrainConfig(batch=C5_VIEWS, total_steps=TRAIN_TOTAL_STEPS,
+                                                     max_gaussians=2_000_000), dist, start_step=TRAIN_START_STEP)
     tlist = [targets[v] for v in range(C5_VIEWS)]
     for _ in range(2):
         tr.step(cams, tlist)
     stream = torch.cuda.current_stream(dev)
     steps = 5
+    first_timed = tr.step_count + 1
     if dist:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -303,6 +308,7 @@ def run_c5_leg(args, ctx, dev, dist, rank, world, flush):
     b.record(stream)
     torch.cuda.synchronize(dev)
     last = tr.last_losses()
+    sh_timed = tr.scene.sh_degree
     ms = max_over_ranks(a.elapsed_time(b), dist, dev)
     its = steps / (ms / 1e3)
     out = {"metric": "train it/s (C5)", "value": its, "unit": "it/s", "n_gpus": world, "steps": steps,
@@ -312,7 +318,8 @@ def run_c5_leg(args, ctx, dev, dist, rank, world, flush):
            "loss_last": last.total,
            "config": {"workload": "C5: 1M 4D rotor Gaussians, SH deg 3, 1352x1014, 8 camera x timestamp views per rank "
                                   "and step, full training step, batch reduced by NCCL all-reduce",
-                      "n_gaussians": C5_N, "width": C5_W, "height": C5_H, "views_per_rank": C5_VIEWS}}
+                      "n_gaussians": C5_N, "width": C5_W, "height": C5_H, "views_per_rank": C5_VIEWS,
+                      "active_sh_degree": sh_timed, "first_timed_step": first_timed}}
     tr = None
     scene.close()
     del targets, tlist
@@ -346,6 +353,88 @@ def train_case():
     return truth, store
 
 
+def measured_peaks(ctx):
+    """Roofline denominators: HBM from MEASURED_PEAKS.json (driver-measured copy bandwidth),
+    FP32 / FP64 FMA from the bench's own probes (MEASURED_PEAKS.json has neither)."""
+    if not hasattr(measured_peaks, "cache"):
+        peaks = {}
+        try:
+            peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        except Exception:
+            pass
+        hbm = float(peaks.get("hbm_gbs", 6650.0))
+        src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "B200_PROFILING.md fallback 6.65 TB/s"
+        measured_peaks.cache = {"hbm_gbs": hbm, "hbm_source": src, "fp32_tflops": ctx.measure_fp32_tflops(),
+                                "fp64_tflops": ctx.measure_fp64_tflops()}
+    return measured_peaks.cache
+
+
+# FP64 FLOPs per valid SSIM position of the image-loss pair K8a + K8b, counted from
+# csrc/k_train.cu (FMA = 2; reference summation order, so no fused forms): K8a's two separable
+# 11-tap passes over the five moment fields of 3 channels (2 x 11 x 2 x 5 x 3 = 660) plus the
+# SSIM map and its three adjoint seeds (~40 x 3); K8b's three adjoint convolutions gathered over
+# the 11 x 11 window as two separable passes (2 x 11 x 2 x 3 x 3 = 396) plus the gradient
+# assembly (~15 x 3).
+K8_FLOP_PER_POS = 660 + 120 + 396 + 45
+
+
+def train_rooflines(ctx, tr, cams, stage_ms):
+    """Roofline of every training kernel over one C3 step (SURVEY.md §8(d) work counts).
+
+    Stage times: `stage_ms` (serialised step, CUDA events per stage).  Workload counts (E, B,
+    E_b, visible splats, pairs): the step's views re-rendered with the eval counters on (the
+    scene after that step -- one Adam update later)."""
+    peaks = measured_peaks(ctx)
+    ctx.set_profiling(timing=False, count_evals=True)
+    ctx.profile_reset()
+    e_b = n_vis = n_pairs = 0
+    for cam in cams:
+        _, rec = ctx.render_forward_device(tr.scene, cam, (0.0, 0.0, 0.0), retain=True)
+        e_b += int(rec.n_contrib.astype(np.int64).sum())  # E_b: evaluations in [0, contrib)
+        n_vis += rec._n_splats
+        n_pairs += rec.n_pairs
+        rec.close()
+    _, (E, B, E_k) = ctx.profile_read()
+    ctx.set_profiling(False, False)
+    n = tr.scene.n
+    px = sum(c.width * c.height for c in cams)
+    pos = sum(max(c.width - 10, 0) * max(c.height - 10, 0) for c in cams)
+    k = tr.cfg.loss.k_neighbors
+    fp32, fp64, hbm = peaks["fp32_tflops"], peaks["fp64_tflops"], peaks["hbm_gbs"]
+    # stage: (bound, algorithmic work of the step in GB or TFLOP, peak, definition)
+    spec = {
+        "backward_tiles_k6": ("fp32", (16 * e_b + 60 * B) / 1e12, fp32, "16 E_b + 60 B FLOP (E_b = sum of n_contrib)"),
+        "blend_fp32_k5": ("fp32", (16 * E + 10 * B) / 1e12, fp32, "16 E + 10 B FLOP"),
+        "preprocess_k1": ("hbm", (260 * n * len(cams) + 48 * n_vis) / 1e9, hbm, "260 N + 48 N_vis B per view"),
+        "backward_color_k7a": ("hbm", (248 + 216) * n_vis / 1e9, hbm,
+                               "SH 192 + view dir 32 + colour grads 24 B read, SH grads 192 + d mean3 24 B written "
+                               "per visible splat"),
+        "backward_gauss_k7b": ("hbm", (260 * n_vis + 268 * n_vis - (248 + 216) * n_vis) / 1e9, hbm,
+                               "the rest of SURVEY's 260 + 268 B per visible splat"),
+        "image_loss_k8": ("fp64", K8_FLOP_PER_POS * pos / 1e12, fp64,
+                          f"{K8_FLOP_PER_POS} FP64 FLOP per valid SSIM position (counted from k_train.cu)"),
+        "adam_k9": ("hbm", 1828 * n / 1e9, hbm, "1828 B per Gaussian (65 x (4 grad + 24 param/m/v) + 8)"),
+        "consistency_k10": ("hbm", (260 * n + 24 * n * (k + 2)) / 1e9, hbm, "260 N + 24 N (k + 2) B"),
+        "tile_radix_sort_k4": ("hbm", 2 * 20 * n_pairs / 1e9, hbm, "2 passes x 20 B per pair"),
+    }
+    kernels = {}
+    for name, (bound, work, peak, what) in spec.items():
+        ms = stage_ms.get(name)
+        if not ms:
+            continue
+        ach = work / (ms / 1e3)
+        kernels[name] = {"bound": "fp64" if bound == "fp64" else bound, "achieved": ach, "peak": peak,
+                         "unit": "GB/s" if bound == "hbm" else "TFLOP/s", "frac": ach / peak, "ms_per_step": ms,
+                         "work": what}
+    dominant = max(kernels, key=lambda k: kernels[k]["ms_per_step"]) if kernels else None
+    roof = dict(kernels.get(dominant, {}), kernel=dominant, traffic=None,
+                timing="serialised step (one stage at a time), CUDA events on the launching stream",
+                peak_source={"hbm": peaks["hbm_source"], "fp32": "bench FFMA probe", "fp64": "bench DFMA probe"})
+    counts = {"E": E, "B": B, "E_kernel": E_k, "E_b": e_b, "visible_splats": n_vis, "pairs": n_pairs,
+              "views": len(cams), "fp32_peak_tflops": fp32, "fp64_peak_tflops": fp64}
+    return {"roofline": roof, "kernels": kernels, "counts": counts}
+
+
 def run_train_leg(args, ctx, dev, dist, rank, world, flush):
     import torch
 
@@ -358,8 +447,9 @@ def run_train_leg(args, ctx, dev, dist, rank, world, flush):
     ctx.render_views(tsc, cams, (0.0, 0.0, 0.0), out=targets)
     tsc.close()
     scene = rgs.DeviceScene.from_store(ctx, store)
-    cfg = train.TrainConfig(batch=TRAIN_BATCH, total_steps=2000)
-    tr = train.Trainer(ctx, scene, cfg, dist)
+    cfg = train.TrainConfig(batch=TRAIN_BATCH, total_steps=TRAIN_TOTAL_STEPS)
+    # The timed steps are past the last SH unlock (trainer.cpp:135): active SH degree 3.
+    tr = train.Trainer(ctx, scene, cfg, dist, start_step=TRAIN_START_STEP)
     stream = torch.cuda.current_stream(dev)
     B = TRAIN_BATCH
 
@@ -377,6 +467,7 @@ def run_train_leg(args, ctx, dev, dist, rank, world, flush):
     torch.cuda.synchronize(dev)
     knn_ms = 1e3 * (time.perf_counter() - knn0)
     launches0 = ctx.kernel_launches
+    first_timed = tr.step_count + 1
     if dist:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -404,6 +495,7 @@ def run_train_leg(args, ctx, dev, dist, rank, world, flush):
     stages, _ = ctx.profile_read()
     ctx.set_profiling(False, False)
     stage_ms = {k: v[0] for k, v in stages.items() if v[1]}
+    train_roof = train_rooflines(ctx, tr, c, stage_ms)
 
     # e2e: the same steps through the public API with each step's target images copied
     # H2D from pinned host memory and the loss scalars read back (Trainer.step's D2H).
@@ -445,25 +537,34 @@ def run_train_leg(args, ctx, dev, dist, rank, world, flush):
         c, t = batch(0)
         tg = [x.cpu().numpy().astype(np.float64) for x in t]
         w = oracle.loss_weights()
+        # the same neighbour lists the GPU step uses (the KNN is rebuilt every 100 steps on both
+        # sides, so it is outside the per-step cost), the same SH degree (3)
+        nbrs = tr.nbrs.cpu().numpy() if tr.nbrs is not None else None
+        assert store.active_sh_degree == tr.scene.sh_degree == 3
         t0 = time.perf_counter()
-        L, g, vn, vis = ops.evaluate_loss(store, c, tg, w, (0.0, 0.0, 0.0), None, threads=threads)
+        L, g, vn, vis = ops.evaluate_loss(store, c, tg, w, (0.0, 0.0, 0.0), nbrs, threads=threads)
         n = store.size()
-        ops.adam_step(store, np.zeros((n, 65)), np.zeros((n, 65)), g, oracle.adam_config(), 1)
+        ops.adam_step(store, np.zeros((n, 65)), np.zeros((n, 65)), g,
+                      oracle.adam_config(total_steps=TRAIN_TOTAL_STEPS), TRAIN_START_STEP + 1)
         cpu_s = time.perf_counter() - t0
         cpu = {"value": 1.0 / cpu_s, "unit": "it/s", "cores": threads,
                "kind": "reference" if ops.ref else "port",
-               "sample": f"1 training step (evaluate_loss over {B} views without the consistency KNN + adam_step), "
-                         f"{threads} threads, {cpu_model()}"}
+               "sample": f"1 training step at active SH degree 3: the reference's evaluate_loss over {B} views "
+                         f"(render fwd, L1 + SSIM, render bwd, entropy, consistency with k={w.k_neighbors} "
+                         f"neighbours) + adam_step, {threads} threads, {cpu_model()}; omits accumulate_stats "
+                         f"(O(N) adds)"}
     return {
         "metric": "train it/s", "value": its, "unit": "it/s", "ms_per_step": ms / args.train_steps,
         "steps": args.train_steps, "warmup": max(args.warmup, 1), "n_gpus": world,
         "views_per_step": B * world,
         "config": {"workload": TRAIN_WORKLOAD, "n_gaussians": TRAIN_N, "width": TRAIN_W, "height": TRAIN_H,
-                   "batch_per_rank": B, "parallelism": f"dp{world}: replicated scene, NCCL all-reduce of "
+                   "batch_per_rank": B, "active_sh_degree": tr.scene.sh_degree, "first_timed_step": first_timed,
+                   "parallelism": f"dp{world}: replicated scene, NCCL all-reduce of "
                                                          "[65 grads | viewspace norm | visible | image losses]",
                    "l2": "256 MiB flush before the timed steps; per-step working set > L2"},
         "loss_first": first.total, "loss_last": last.total, "psnr_last": train.psnr_from_mse(last.mse),
         "knn_rebuild_ms": knn_ms, "stage_ms_one_step": stage_ms, "gpu_launches": launches,
+        "roofline": train_roof["roofline"], "kernels": train_roof["kernels"], "workload_counts": train_roof["counts"],
         "e2e": e2e, "cpu_baseline": cpu,
     }
 

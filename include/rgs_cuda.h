@@ -9,8 +9,9 @@
  *   GaussianStore      gaussian.hpp:79-103    -> rgs_scene   (device-resident FP32 SoA)
  *   StoreGrads         gaussian.hpp:106-119   -> grads / viewspace_norm / visible buffers
  *   Camera             camera.hpp:11-27       -> rgs_camera
- * The C++ drop-in (paper_2402_03307_b200/host/rgs_b200.hpp) and the Python
- * mirror (paper_2402_03307_b200/rgs.py) sit on top of exactly these symbols.
+ * The C++ drop-ins (paper_2402_03307_b200/host/rgs_adapter.cpp for rasterizer.hpp,
+ * host/rgs_train_adapter.cpp for image / ssim / loss / knn / optim) and the Python
+ * mirror (paper_2402_03307_b200/rgs.py, train.py) sit on top of exactly these symbols.
  *
  * Plain C: pointers and sizes only, no CUDA or torch types in signatures (streams
  * are passed as void*).  Every entry point returns an rgs_status; on failure
@@ -135,6 +136,9 @@ int rgs_ctx_profile_read(rgs_ctx* ctx, double* stage_ms, long long* stage_launch
 int rgs_ctx_profile_slow_reasons(rgs_ctx* ctx, unsigned long long* out4);
 /* FP32 FMA-pipe throughput of this device (FFMA probe, best of 5), TFLOP/s with FMA = 2. */
 int rgs_measure_fp32_tflops(rgs_ctx* ctx, double* tflops);
+/* FP64 FMA-pipe throughput of this device (DFMA probe, best of 5), TFLOP/s with FMA = 2: the
+ * denominator of the FP64-bound kernels' roofline (K1 / K7b / K8). */
+int rgs_measure_fp64_tflops(rgs_ctx* ctx, double* tflops);
 
 /* ---------------------------------------------------------------- scene */
 /* Device scene (GaussianStore replacement).  Host layout of the upload arrays
@@ -287,7 +291,10 @@ void rgs_optimizer_destroy(rgs_optimizer* opt);
  * re-normalised, static-mode masks (optim.cpp:110-157).  grads: 65*N floats (rgs_scene_params
  * layout, e.g. rgs_render_backward with RGS_FLAG_ACCUMULATE over the batch); vnorm / visible as
  * rgs_render_backward (needed with accumulate_stats).  losses (may be NULL): [0] = entropy_loss.
- * Rotor errors are reported by rgs_optimizer_status (no host sync here). */
+ * Rotor errors are reported by rgs_optimizer_status (no host sync here).  While the context's
+ * deferred status word holds an error (a RGS_FLAG_DEFER_CHECKS forward or consistency term of
+ * this step failed, or outgrew its pair buffers) the step is skipped on the device: scene and
+ * moments stay as they were, as when the reference throws before adam_step. */
 int rgs_adam_step(rgs_ctx* ctx, rgs_scene* scene, rgs_optimizer* opt, const float* grads, const float* vnorm,
                   const int32_t* visible, const rgs_adam_config* cfg, int step, double* losses);
 /* The context's deferred status word (RGS_FLAG_DEFER_CHECKS calls): rgs_ctx_status synchronises

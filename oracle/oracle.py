@@ -261,6 +261,15 @@ def reference_build() -> OracleLib:
     return _cache["ref"]
 
 
+def sum_order_variant(order: int) -> OracleLib:
+    """The restatement built with ORC_SUM_ORDER=order (Eigen 3.4's reduction orders; see
+    rgs_oracle.c): the summation-order sensitivity study only."""
+    key = f"sum{order}"
+    if key not in _cache:
+        _cache[key] = OracleLib(os.path.join(HERE, "_ref", f"liboracle_sum{order}.so"), "orc")
+    return _cache[key]
+
+
 def reference_available() -> bool:
     return os.path.exists(REF_SO)
 

@@ -94,6 +94,49 @@ typedef struct {
     int a, b;
     double c;
 } qterm;
+/* ------------------------------------------------------------------ fixed-size sums
+ * Reduction order of the fixed-size dot products / norms / small matrix products on the
+ * forward path (the sensitivity study of tests/test_eigen_order.py builds this file three
+ * ways):
+ *   ORC_SUM_ORDER 0: sequential, left to right -- the Eigen subset the reference is built
+ *                    against here (include/eigen_subset), and the default;
+ *   ORC_SUM_ORDER 1: Eigen 3.4's completely unrolled scalar redux (redux_novec_unroller):
+ *                    recursive halving, a0 + (a1 + a2), (a0 + a1) + (a2 + a3), ...;
+ *   ORC_SUM_ORDER 2: Eigen 3.4's SSE2 packet redux for doubles (packets of 2): the packets
+ *                    summed by halving, then the two lanes; an odd tail added last. */
+#ifndef ORC_SUM_ORDER
+#define ORC_SUM_ORDER 0
+#endif
+static double sum_halving(const double* t, int n) {
+    if (n == 1) return t[0];
+    const int h = n / 2;
+    return sum_halving(t, h) + sum_halving(t + h, n - h);
+}
+static double sum_packets(const double* t, int npk, int lane) { /* lane `lane` of packets [0, npk) */
+    if (npk == 1) return t[lane];
+    const int h = npk / 2;
+    return sum_packets(t, h, lane) + sum_packets(t + 2 * h, npk - h, lane);
+}
+static double sumn(const double* t, int n) {
+#if ORC_SUM_ORDER == 0
+    double s = t[0];
+    for (int i = 1; i < n; ++i) s += t[i];
+    return s;
+#elif ORC_SUM_ORDER == 1
+    return sum_halving(t, n);
+#else
+    if (n < 2) return t[0];
+    const int npk = n / 2;
+    double s = sum_packets(t, npk, 0) + sum_packets(t, npk, 1);
+    if (n & 1) s = s + t[n - 1];
+    return s;
+#endif
+}
+static inline double dot3(double a0, double b0, double a1, double b1, double a2, double b2) {
+    const double t[3] = {a0 * b0, a1 * b1, a2 * b2};
+    return sumn(t, 3);
+}
+
 static const qterm kMapTerms[16][8] = {
     {{0, 0, 1}, {1, 1, -1}, {2, 2, -1}, {3, 3, -1}, {4, 4, 1}, {5, 5, 1}, {6, 6, 1}, {7, 7, -1}},
     {{1, 0, 2}, {2, 4, -2}, {3, 5, -2}, {6, 7, 2}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}},
@@ -129,9 +172,9 @@ static void epsilon_gradient(const double* v, double* g) {
     g[7] = v[0];
 }
 static double sqnorm8(const double* v) {
-    double s = v[0] * v[0];
-    for (int i = 1; i < 8; ++i) s += v[i] * v[i];
-    return s;
+    double t[8];
+    for (int i = 0; i < 8; ++i) t[i] = v[i] * v[i];
+    return sumn(t, 8);
 }
 
 /* rotor.cpp:117-136.  Returns ORC_OK or an error code. */
@@ -260,9 +303,9 @@ static int assemble_cache(const double* ls, const double* rot, slice_cache* c) {
         for (int j = 0; j < 4; ++j) m1[i * 4 + j] = c->R[i * 4 + j] * c->q[j];
     for (int i = 0; i < 4; ++i)
         for (int j = 0; j < 4; ++j) {
-            double s = m1[i * 4 + 0] * c->R[j * 4 + 0];
-            for (int k = 1; k < 4; ++k) s += m1[i * 4 + k] * c->R[j * 4 + k];
-            sig[i * 4 + j] = s;
+            double t[4];
+            for (int k = 0; k < 4; ++k) t[k] = m1[i * 4 + k] * c->R[j * 4 + k];
+            sig[i * 4 + j] = sumn(t, 4);
         }
     for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j) c->U[i * 3 + j] = sig[i * 4 + j];
@@ -405,12 +448,7 @@ static void cam_center(const orc_camera* cam, double* c) {
     double r[9], t[3];
     cam_rotation(cam, r);
     cam_translation(cam, t);
-    for (int i = 0; i < 3; ++i) {
-        double s = (-r[0 * 3 + i]) * t[0];
-        s += (-r[1 * 3 + i]) * t[1];
-        s += (-r[2 * 3 + i]) * t[2];
-        c[i] = s;
-    }
+    for (int i = 0; i < 3; ++i) c[i] = dot3(-r[0 * 3 + i], t[0], -r[1 * 3 + i], t[1], -r[2 * 3 + i], t[2]);
 }
 /* camera.hpp:19-24 */
 static int cam_validate(const orc_camera* cam) {
@@ -453,12 +491,8 @@ static int project(const sliced3* s, const orc_camera* cam, const double* sh48, 
     cam_rotation(cam, R);
     cam_translation(cam, t);
     double p[3];
-    for (int i = 0; i < 3; ++i) {
-        double a = R[i * 3 + 0] * s->mean[0];
-        a += R[i * 3 + 1] * s->mean[1];
-        a += R[i * 3 + 2] * s->mean[2];
-        p[i] = a + t[i];
-    }
+    for (int i = 0; i < 3; ++i)
+        p[i] = dot3(R[i * 3 + 0], s->mean[0], R[i * 3 + 1], s->mean[1], R[i * 3 + 2], s->mean[2]) + t[i];
     if (p[2] <= kNearPlane) return 0;
 
     memset(out, 0, sizeof *out);
@@ -469,27 +503,17 @@ static int project(const sliced3* s, const orc_camera* cam, const double* sh48, 
     double J[6], T[6];
     projection_jacobian(cam, p, J);
     for (int i = 0; i < 2; ++i)
-        for (int j = 0; j < 3; ++j) {
-            double a = J[i * 3 + 0] * R[0 * 3 + j];
-            a += J[i * 3 + 1] * R[1 * 3 + j];
-            a += J[i * 3 + 2] * R[2 * 3 + j];
-            T[i * 3 + j] = a;
-        }
+        for (int j = 0; j < 3; ++j)
+            T[i * 3 + j] = dot3(J[i * 3 + 0], R[0 * 3 + j], J[i * 3 + 1], R[1 * 3 + j], J[i * 3 + 2], R[2 * 3 + j]);
     double A[6], cov2[4];
     for (int i = 0; i < 2; ++i)
-        for (int j = 0; j < 3; ++j) {
-            double a = T[i * 3 + 0] * s->cov[0 * 3 + j];
-            a += T[i * 3 + 1] * s->cov[1 * 3 + j];
-            a += T[i * 3 + 2] * s->cov[2 * 3 + j];
-            A[i * 3 + j] = a;
-        }
+        for (int j = 0; j < 3; ++j)
+            A[i * 3 + j] = dot3(T[i * 3 + 0], s->cov[0 * 3 + j], T[i * 3 + 1], s->cov[1 * 3 + j], T[i * 3 + 2],
+                                s->cov[2 * 3 + j]);
     for (int i = 0; i < 2; ++i)
-        for (int j = 0; j < 2; ++j) {
-            double a = A[i * 3 + 0] * T[j * 3 + 0];
-            a += A[i * 3 + 1] * T[j * 3 + 1];
-            a += A[i * 3 + 2] * T[j * 3 + 2];
-            cov2[i * 2 + j] = a + kCovDilation * (i == j ? 1.0 : 0.0);
-        }
+        for (int j = 0; j < 2; ++j)
+            cov2[i * 2 + j] = dot3(A[i * 3 + 0], T[j * 3 + 0], A[i * 3 + 1], T[j * 3 + 1], A[i * 3 + 2], T[j * 3 + 2]) +
+                              kCovDilation * (i == j ? 1.0 : 0.0);
     double det = cov2[0] * cov2[3] - cov2[2] * cov2[1];
     if (det <= 0) return 0;
     double invdet = 1.0 / (cov2[0] * cov2[3] - cov2[2] * cov2[1]);
@@ -511,7 +535,7 @@ static int project(const sliced3* s, const orc_camera* cam, const double* sh48, 
     double ctr[3], v[3];
     cam_center(cam, ctr);
     for (int i = 0; i < 3; ++i) v[i] = s->mean[i] - ctr[i];
-    double dist = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+    double dist = sqrt(dot3(v[0], v[0], v[1], v[1], v[2], v[2]));
     double dir[3];
     if (dist > 0) {
         for (int i = 0; i < 3; ++i) dir[i] = v[i] / dist;
@@ -525,19 +549,15 @@ static int project(const sliced3* s, const orc_camera* cam, const double* sh48, 
     int clamped[3];
     for (int ch = 0; ch < 3; ++ch) {
         const double* row = sh48 + ch * 16;
-        double a = row[0] * basis[0];
-        for (int k = 1; k < 16; ++k) a += row[k] * basis[k];
-        double col = a + 0.5;
+        double tt[16];
+        for (int k = 0; k < 16; ++k) tt[k] = row[k] * basis[k];
+        double col = sumn(tt, 16) + 0.5;
         clamped[ch] = col < 0;
         if (clamped[ch]) col = 0;
         out->color[ch] = col;
     }
-    for (int i = 0; i < 2; ++i) {
-        double a = T[i * 3 + 0] * s->speed[0];
-        a += T[i * 3 + 1] * s->speed[1];
-        a += T[i * 3 + 2] * s->speed[2];
-        out->flow2[i] = a;
-    }
+    for (int i = 0; i < 2; ++i)
+        out->flow2[i] = dot3(T[i * 3 + 0], s->speed[0], T[i * 3 + 1], s->speed[1], T[i * 3 + 2], s->speed[2]);
     if (cache) {
         memcpy(cache->cov3, s->cov, sizeof cache->cov3);
         memcpy(cache->mean3, s->mean, sizeof cache->mean3);

@@ -932,21 +932,26 @@ void backward_fp64_pixels(const SplatArrays& sp, const uint32_t* pair_vals, cons
                                                                   dL_dimage, slow_list, slow_count, screen_grads);
 }
 
+// K7a (part & 1): the colour / SH path; K7b (part & 2): the geometry chain (reads K7a's d mean3).
 void gaussian_backward(const float* params, const double* params64, int n, int sh_degree, const DevCamera& cam,
                        const double4* dir_dist, double* color_dmean3, const uint8_t* valid, const double* screen_grads,
-                       int accumulate, float* grads, float* vnorm, int32_t* visible, cudaStream_t s) {
+                       int accumulate, float* grads, float* vnorm, int32_t* visible, cudaStream_t s, int part) {
     if (n <= 0) return;
     ParamView P{params, n, params64};
     if (params64) {
-        k_color_backward<true><<<blocks(n, 128), 128, 0, s>>>(P, sh_degree, valid, dir_dist, screen_grads, accumulate,
-                                                               grads, color_dmean3);
-        k_gaussian_backward<true><<<blocks(n, 128), 128, 0, s>>>(P, sh_degree, cam, valid, screen_grads, color_dmean3,
-                                                                 accumulate, grads, vnorm, visible);
+        if (part & 1)
+            k_color_backward<true><<<blocks(n, 128), 128, 0, s>>>(P, sh_degree, valid, dir_dist, screen_grads,
+                                                                   accumulate, grads, color_dmean3);
+        if (part & 2)
+            k_gaussian_backward<true><<<blocks(n, 128), 128, 0, s>>>(P, sh_degree, cam, valid, screen_grads,
+                                                                     color_dmean3, accumulate, grads, vnorm, visible);
     } else {
-        k_color_backward<false><<<blocks(n, 128), 128, 0, s>>>(P, sh_degree, valid, dir_dist, screen_grads,
-                                                                accumulate, grads, color_dmean3);
-        k_gaussian_backward<false><<<blocks(n, 128), 128, 0, s>>>(P, sh_degree, cam, valid, screen_grads,
-                                                                  color_dmean3, accumulate, grads, vnorm, visible);
+        if (part & 1)
+            k_color_backward<false><<<blocks(n, 128), 128, 0, s>>>(P, sh_degree, valid, dir_dist, screen_grads,
+                                                                    accumulate, grads, color_dmean3);
+        if (part & 2)
+            k_gaussian_backward<false><<<blocks(n, 128), 128, 0, s>>>(P, sh_degree, cam, valid, screen_grads,
+                                                                      color_dmean3, accumulate, grads, vnorm, visible);
     }
 }
 

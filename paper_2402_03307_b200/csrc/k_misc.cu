@@ -246,8 +246,25 @@ __global__ void __launch_bounds__(256) k_ffma_peak(float* out, int iters, float 
     const float s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
     if (s == 1234.5f) out[0] = s;  // keep the chains live
 }
+__global__ void __launch_bounds__(256) k_dfma_peak(double* out, int iters, double a, double b) {
+    double x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6,
+           x7 = x0 + 7;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+            x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+        }
+    }
+    const double s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+    if (s == 1234.5) out[0] = s;
+}
 }  // namespace rgs_dev
 namespace rgs_launch {
+double dfma_peak(double* out, int blocks, int iters, cudaStream_t s) {
+    rgs_dev::k_dfma_peak<<<blocks, 256, 0, s>>>(out, iters, 0.999999, 1e-6);
+    return (double)blocks * 256.0 * iters * 16.0 * 8.0;
+}
 // Returns the FMA count of the launch.
 double ffma_peak(float* out, int blocks, int iters, cudaStream_t s) {
     rgs_dev::k_ffma_peak<<<blocks, 256, 0, s>>>(out, iters, 0.999999f, 1e-6f);

@@ -365,9 +365,10 @@ __device__ __forceinline__ void st1(void* base, size_t idx, double v) {
 // the FP64 divide / sqrt latency is hidden by occupancy.  Same arithmetic as k_adam_step.
 template <bool F64>
 __global__ void __launch_bounds__(128) k_adam_plain(void* params, void* mom1, void* mom2,
-                                                    const float* __restrict__ grads, int n, AdamArgs a) {
+                                                    const float* __restrict__ grads, int n, AdamArgs a,
+                                                    const unsigned long long* __restrict__ skip) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    if (i >= n || (skip && *skip != ~0ull)) return;
     const int grp = blockIdx.y < 2 ? blockIdx.y : blockIdx.y + 2;
     double p[4], m[4], v[4], g[4];
     ld4<F64>(params, n, grp, i, p);
@@ -398,8 +399,13 @@ template <bool F64>
 __global__ void __launch_bounds__(128, 6) k_adam_step(void* params, void* mom1, void* mom2, const float* __restrict__ grads,
                                                    const float* __restrict__ vnorm, const int32_t* __restrict__ visible,
                                                    double* __restrict__ accum, int32_t* __restrict__ count, int n,
-                                                   AdamArgs a, unsigned long long* err, double* part_entropy) {
+                                                   AdamArgs a, unsigned long long* err, double* part_entropy,
+                                                   const unsigned long long* __restrict__ skip) {
     __shared__ double red[256];
+    // A deferred forward of this step failed (rotor error, or a pair-buffer overflow that left
+    // its gradients incomplete): the reference would have thrown before adam_step, so the
+    // scene and moments are left untouched (block-uniform exit, before the barriers below).
+    if (skip && *skip != ~0ull) return;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int grp = 2 + blockIdx.y;  // groups 2 (rotor) and 3 (opacity / stats); k_adam_plain does the rest
     double ent = 0;
@@ -1010,16 +1016,17 @@ void image_loss_f64(const double* img, const double* tgt, int W, int H, const Im
 
 void adam_step(bool f64, void* params, void* m1, void* m2, const float* grads, const float* vnorm,
                const int32_t* visible, double* accum, int32_t* count, int n, const AdamArgs& a,
-               unsigned long long* err, double* part_entropy, double* losses_entropy, int accumulate, cudaStream_t s) {
+               unsigned long long* err, double* part_entropy, double* losses_entropy, int accumulate,
+               const unsigned long long* skip, cudaStream_t s) {
     const int nb = nblk(n, 128);
     if (f64) {
-        k_adam_plain<true><<<dim3(nb, 14), 128, 0, s>>>(params, m1, m2, grads, n, a);
+        k_adam_plain<true><<<dim3(nb, 14), 128, 0, s>>>(params, m1, m2, grads, n, a, skip);
         k_adam_step<true><<<dim3(nb, 2), 128, 0, s>>>(params, m1, m2, grads, vnorm, visible, accum, count, n, a, err,
-                                                      part_entropy);
+                                                      part_entropy, skip);
     } else {
-        k_adam_plain<false><<<dim3(nb, 14), 128, 0, s>>>(params, m1, m2, grads, n, a);
+        k_adam_plain<false><<<dim3(nb, 14), 128, 0, s>>>(params, m1, m2, grads, n, a, skip);
         k_adam_step<false><<<dim3(nb, 2), 128, 0, s>>>(params, m1, m2, grads, vnorm, visible, accum, count, n, a,
-                                                       err, part_entropy);
+                                                       err, part_entropy, skip);
     }
     if (part_entropy && losses_entropy)
         k_finalize<<<1, 256, 0, s>>>(part_entropy, nb, (double)n, 1.0, 0, accumulate, losses_entropy);

@@ -174,11 +174,12 @@ struct Frame {
 // Pipeline stages timed by the profiling mode (rgs_ctx_set_profiling).
 enum Stage {
     kStPreprocess = 0, kStDepthRank, kStHist, kStTileFill, kStTileSort, kStBlend, kStFixup, kStBwdTiles,
-    kStBwdFixup, kStBwdGauss, kNumStages
+    kStBwdFixup, kStBwdGauss, kStBwdColor, kStImageLoss, kStAdam, kStConsistency, kNumStages
 };
 static const char* kStageNames[kNumStages] = {
     "preprocess_k1", "depth_rank", "pair_offsets_scan", "duplicate_k3", "tile_radix_sort_k4", "blend_fp32_k5",
-    "blend_fp64_fixup", "backward_tiles_k6", "backward_fp64_fixup", "backward_gauss_k7"};
+    "blend_fp64_fixup", "backward_tiles_k6", "backward_fp64_fixup", "backward_gauss_k7b", "backward_color_k7a",
+    "image_loss_k8", "adam_k9", "consistency_k10"};
 
 struct rgs_records;
 struct rgs_ctx {
@@ -720,6 +721,35 @@ int rgs_measure_fp32_tflops(rgs_ctx* c, double* tflops) {
     });
 }
 
+int rgs_measure_fp64_tflops(rgs_ctx* c, double* tflops) {
+    if (!tflops) return RGS_E_INVALID;
+    return guarded(c, [&] {
+        DevBuf out;
+        out.ensure(64, c->stream);
+        cudaEvent_t a, b;
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b));
+        const int blocks = 148 * 8;
+        rgs_launch::dfma_peak(out.as<double>(), blocks, 16, c->stream);  // warm-up
+        double best = 0;
+        for (int rep = 0; rep < 5; ++rep) {
+            CK(cudaEventRecord(a, c->stream));
+            const double fmas = rgs_launch::dfma_peak(out.as<double>(), blocks, 256, c->stream);
+            CK(cudaEventRecord(b, c->stream));
+            CK(cudaEventSynchronize(b));
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, a, b));
+            best = std::max(best, 2.0 * fmas / (ms * 1e-3) / 1e12);
+        }
+        c->launches += 6;
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        out.release(c->stream);
+        *tflops = best;
+        return RGS_OK;
+    });
+}
+
 int rgs_ctx_profile_reset(rgs_ctx* c) {
     return guarded(c, [&] {
         c->collect();
@@ -993,20 +1023,32 @@ static int forward_common(rgs_ctx* c, Source src, const rgs_scene* scene, const 
             // pair count (an overflow is still reported, as RGS_E_OVERFLOW, never silent)
             f->pair_cap = std::max<long long>(f->pair_cap, 2 * f->n_pairs + 1024);
         }
-        rc = run_forward(c, *f, c->stream, src, scene, dsp, n_splats, monotone, cam, bg, flags, dimg, flow, !defer,
-                         nullptr);
-        if (defer && !rc) {
-            rgs_launch::fold_status(f->dstats(), c->deferred.as<unsigned long long>(), kOverflowWord, c->stream);
-            c->launches += 1;
-            if (!rec->ready) CK(cudaEventCreateWithFlags(&rec->ready, cudaEventDisableTiming));
-            CK(cudaEventRecord(rec->ready, c->stream));
-            rec->pending = true;
+        // A record whose forward fails (status code or CUDA error) is unregistered and its
+        // frame returned to the pool before the error propagates.
+        auto drop_rec = [&] {
+            if (!rec) return;
+            c->live_records.erase(rec);
+            frame_put(c, rec->pf);
+            if (rec->ready) cudaEventDestroy(rec->ready);
+            delete rec;
+            rec = nullptr;
+        };
+        try {
+            rc = run_forward(c, *f, c->stream, src, scene, dsp, n_splats, monotone, cam, bg, flags, dimg, flow,
+                             !defer, nullptr);
+            if (defer && !rc) {
+                rgs_launch::fold_status(f->dstats(), c->deferred.as<unsigned long long>(), kOverflowWord, c->stream);
+                c->launches += 1;
+                if (!rec->ready) CK(cudaEventCreateWithFlags(&rec->ready, cudaEventDisableTiming));
+                CK(cudaEventRecord(rec->ready, c->stream));
+                rec->pending = true;
+            }
+        } catch (...) {
+            drop_rec();
+            throw;
         }
         if (rc) {
-            if (rec) {
-                frame_put(c, rec->pf);
-                delete rec;
-            }
+            drop_rec();
             return rc;
         }
         if (host_io && image) {
@@ -1345,13 +1387,13 @@ int rgs_render_backward(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* ca
                                              &f.dstats()->slow_count, (int)((size_t)f.width * f.height),
                                              c->sgrad.as<double>(), s);
         }
-        {
-            StageTimer t(c, kStBwdGauss, s);
-            c->cgrad.ensure(sizeof(double) * 3 * (size_t)std::max(n, 1), s);
+        c->cgrad.ensure(sizeof(double) * 3 * (size_t)std::max(n, 1), s);
+        for (int part = 1; part <= 2; ++part) {
+            StageTimer t(c, part == 1 ? kStBwdColor : kStBwdGauss, s);
             rgs_launch::gaussian_backward(scene->params, scene->params64, n, scene->sh_degree, dc,
                                           f.dir_dist.as<double4>(), c->cgrad.as<double>(), f.valid.as<uint8_t>(),
                                           c->sgrad.as<double>(), (flags & RGS_FLAG_ACCUMULATE) ? 1 : 0, grads,
-                                          vnorm, visible, s);
+                                          vnorm, visible, s, part);
         }
         c->launches += 4;
         CK(cudaGetLastError());
@@ -1477,12 +1519,14 @@ void ensure_ssim_window(rgs_ctx* c) {
     done_device = c->device;
 }
 
+// `parts` holds the image-loss block partials, `cparts` the consistency term's: a training step
+// runs the consistency term on its main stream beside the image losses of its side streams.
 struct TrainScratch {
-    DevBuf dfield, parts, speeds, dspeed, pts, lo, hi, knn;
+    DevBuf dfield, parts, cparts, speeds, dspeed, pts, lo, hi, knn;
 };
 void train_scratch_free(void* p, cudaStream_t s) {
     TrainScratch* ts = static_cast<TrainScratch*>(p);
-    for (DevBuf* b : {&ts->dfield, &ts->parts, &ts->speeds, &ts->dspeed, &ts->pts, &ts->lo, &ts->hi, &ts->knn})
+    for (DevBuf* b : {&ts->dfield, &ts->parts, &ts->cparts, &ts->speeds, &ts->dspeed, &ts->pts, &ts->lo, &ts->hi, &ts->knn})
         b->release(s);
     delete ts;
 }
@@ -1519,6 +1563,7 @@ int rgs_image_loss(rgs_ctx* c, const float* rendered, const float* target, int w
         a.inv_n = 1 / (3.0 * (double)width * (double)height);
         a.ssim_scale = nv ? -1 / (3.0 * (double)nv) : 0.0;
         a.accumulate = (flags & RGS_FLAG_ACCUMULATE_GRAD) ? 1 : 0;
+        StageTimer t(c, kStImageLoss, s);
         rgs_launch::image_loss(rendered, target, width, height, a, dL_dimage, ts.dfield.as<double>(),
                                ts.parts.as<double>(), losses, loss_scale, (flags & RGS_FLAG_ACCUMULATE) ? 1 : 0, s);
         c->launches += losses ? 3 : 2;
@@ -1639,9 +1684,11 @@ int rgs_adam_step(rgs_ctx* c, rgs_scene* scene, rgs_optimizer* o, const float* g
         a.stats = cfg->accumulate_stats ? 1 : 0;
         void* params = scene->params64 ? (void*)scene->params64 : (void*)scene->params;
         const bool ent = losses && cfg->lambda_entropy != 0;
+        StageTimer t(c, kStAdam, c->stream);
         rgs_launch::adam_step(o->f64, params, o->m1, o->m2, grads, vnorm, visible, o->accum, o->count, scene->n, a,
                               o->err, ent ? o->part.as<double>() : nullptr, ent ? losses : nullptr,
-                              (cfg->flags & RGS_FLAG_ACCUMULATE) ? 1 : 0, c->stream);
+                              (cfg->flags & RGS_FLAG_ACCUMULATE) ? 1 : 0, c->deferred.as<unsigned long long>(),
+                              c->stream);
         c->launches += ent ? 3 : 2;
         CK(cudaGetLastError());
         return RGS_OK;
@@ -1870,7 +1917,7 @@ int rgs_consistency(rgs_ctx* c, const rgs_scene* scene, const int32_t* neighbors
         cudaStream_t s = c->stream;
         TrainScratch& ts = train_scratch(c);
         ts.speeds.ensure(sizeof(double) * 3 * (size_t)n, s);
-        ts.parts.ensure(sizeof(double) * (rgs_launch::consistency_blocks(n) + 16), s);
+        ts.cparts.ensure(sizeof(double) * (rgs_launch::consistency_blocks(n) + 16), s);
         const bool defer = (flags & RGS_FLAG_DEFER_CHECKS) != 0;
         DevBuf err;
         if (!defer) {
@@ -1878,6 +1925,7 @@ int rgs_consistency(rgs_ctx* c, const rgs_scene* scene, const int32_t* neighbors
             CK(cudaMemsetAsync(err.p, 0xff, sizeof(unsigned long long), s));
         }
         unsigned long long* errp = defer ? c->deferred.as<unsigned long long>() : err.as<unsigned long long>();
+        StageTimer t(c, kStConsistency, s);
         rgs_launch::speeds(scene->params, scene->params64, n, ts.speeds.as<double>(), errp, s);
         double* dspeed = nullptr;
         if (grads) {
@@ -1885,7 +1933,7 @@ int rgs_consistency(rgs_ctx* c, const rgs_scene* scene, const int32_t* neighbors
             CK(cudaMemsetAsync(ts.dspeed.p, 0, sizeof(double) * 3 * (size_t)n, s));
             dspeed = ts.dspeed.as<double>();
         }
-        rgs_launch::consistency(ts.speeds.as<double>(), neighbors, n, k, dspeed, ts.parts.as<double>(), losses,
+        rgs_launch::consistency(ts.speeds.as<double>(), neighbors, n, k, dspeed, ts.cparts.as<double>(), losses,
                                 (flags & RGS_FLAG_ACCUMULATE) ? 1 : 0, s);
         if (grads) rgs_launch::speed_backward(scene->params, scene->params64, n, dspeed, lambda, grads, s);
         c->launches += 2 + (losses ? 1 : 0) + (grads ? 1 : 0);
@@ -1939,6 +1987,13 @@ int rgs_scene_load_checkpoint(rgs_ctx* c, const char* path, unsigned scene_flags
     if (got < 3 || hdr[2] > 3) return ckpt_err(c, "malformed header: " + p);
     const size_t n = hdr[1];
     if (n > (size_t)0x7fffffff) return ckpt_err(c, "malformed header: " + p);
+    {  // the payload must be there before anything is allocated for it (checkpoint.cpp:71-73)
+        const long here = std::ftell(f);
+        if (here < 0 || std::fseek(f, 0, SEEK_END) != 0) return ckpt_err(c, "truncated: " + p);
+        const long end = std::ftell(f);
+        if (end < here || (size_t)(end - here) < 65 * sizeof(float) * n || std::fseek(f, here, SEEK_SET) != 0)
+            return ckpt_err(c, "truncated: " + p);
+    }
     return guarded(c, [&]() -> int {
         cudaStream_t s = c->stream;
         float* pinned = nullptr;

@@ -178,7 +178,7 @@ void backward_fp64_pixels(const SplatArrays& sp, const uint32_t* pair_vals, cons
 void gaussian_backward(const float* params, const double* params64, int n, int sh_degree, const DevCamera& cam,
                        const double4* dir_dist, double* color_dmean3, const uint8_t* valid,
                        const double* screen_grads, int accumulate, float* grads, float* vnorm,
-                       int32_t* visible, cudaStream_t s);
+                       int32_t* visible, cudaStream_t s, int part = 3);
 void export_splats(const SplatArrays& sp, const uint32_t* compact_ids, int n_valid, void* out,
                    cudaStream_t s);
 void compact_index(const uint8_t* valid, const uint32_t* scan, int n, uint32_t* compact_ids, cudaStream_t s);
@@ -193,4 +193,5 @@ void records_to_soa(const float* rec, int n, float* params, double* params64, cu
 void soa_to_records(const float* params, const double* params64, int n, float* rec, cudaStream_t s);
 void valid_to_u32(const uint8_t* valid, int n, uint32_t* out, cudaStream_t s);
 double ffma_peak(float* out, int blocks, int iters, cudaStream_t s);
+double dfma_peak(double* out, int blocks, int iters, cudaStream_t s);
 }  // namespace rgs_launch

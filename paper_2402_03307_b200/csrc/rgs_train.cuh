@@ -47,7 +47,8 @@ void image_loss(const float* img, const float* tgt, int W, int H, const ImageGra
                 double* dfield, double* parts, double* losses, double loss_scale, int accumulate, cudaStream_t s);
 void adam_step(bool f64, void* params, void* m1, void* m2, const float* grads, const float* vnorm,
                const int32_t* visible, double* accum, int32_t* count, int n, const AdamArgs& a,
-               unsigned long long* err, double* part_entropy, double* losses_entropy, int accumulate, cudaStream_t s);
+               unsigned long long* err, double* part_entropy, double* losses_entropy, int accumulate,
+               const unsigned long long* skip, cudaStream_t s);
 int adam_blocks(int n);
 void image_loss_f64(const double* img, const double* tgt, int W, int H, const ImageGradArgs& a, double* dl,
                     double* dfield, double* parts, double* losses, double loss_scale, int accumulate, cudaStream_t s);

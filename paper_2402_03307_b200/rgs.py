@@ -167,7 +167,7 @@ EXPORTS = [
     "rgs_rng_create", "rgs_rng_destroy", "rgs_rng_uniform_int", "rgs_densify_and_prune",
     "rgs_knn_query", "rgs_consistency_loss", "rgs_image_loss_f64", "rgs_entropy_loss", "rgs_accumulate_stats",
     "rgs_rng_get_state", "rgs_rng_set_state", "rgs_malloc", "rgs_free", "rgs_memcpy",
-    "rgs_accumulate_stats_f64", "rgs_ctx_profile_slow_reasons",
+    "rgs_accumulate_stats_f64", "rgs_ctx_profile_slow_reasons", "rgs_measure_fp64_tflops",
 ]
 
 
@@ -219,6 +219,7 @@ def load_library(path: str = LIB_PATH):
         "rgs_ctx_profile_reset": (i, [p]),
         "rgs_ctx_profile_read": (i, [p, p, p, p]),
         "rgs_measure_fp32_tflops": (i, [p, p]),
+        "rgs_measure_fp64_tflops": (i, [p, p]),
         "rgs_project_sliced": (i, [p, p, p, p, i, d, p, p]),
         "rgs_image_loss": (i, [p, p, p, i, i, d, d, d, ctypes.c_uint, p, p]),
         "rgs_optimizer_create": (i, [p, p, p]),
@@ -521,6 +522,11 @@ class Context:
         self.check(self.L.rgs_measure_fp32_tflops(self.h, ctypes.byref(v)))
         return v.value
 
+    def measure_fp64_tflops(self) -> float:
+        v = ctypes.c_double(0)
+        self.check(self.L.rgs_measure_fp64_tflops(self.h, ctypes.byref(v)))
+        return v.value
+
     def profile_reset(self):
         self.check(self.L.rgs_ctx_profile_reset(self.h))
 
@@ -583,7 +589,8 @@ class Context:
         return image, RenderRecords(self, h, cam, background, retain)
 
     def render_backward_device(self, scene: "DeviceScene", cam: Camera, records: "RenderRecords", dL_dimage,
-                               grads=None, vnorm=None, visible=None, accumulate=False):
+                               grads=None, vnorm=None, visible=None, accumulate=False, deterministic=False):
+        """``deterministic``: RGS_FLAG_DETERMINISTIC (fixed-order FP64 replay, bitwise repeatable)."""
         import torch
 
         self.sync_stream()
@@ -594,7 +601,7 @@ class Context:
             vnorm = torch.zeros(n, dtype=torch.float32, device=dev)
             visible = torch.zeros(n, dtype=torch.int32, device=dev)
         c = cam.to_c()
-        flags = FLAG_ACCUMULATE if accumulate else 0
+        flags = (FLAG_ACCUMULATE if accumulate else 0) | (FLAG_DETERMINISTIC if deterministic else 0)
         self.check(self.L.rgs_render_backward(self.h, scene.h, ctypes.byref(c), records.h,
                                               _vp(_ptr(dL_dimage.contiguous())), flags, _vp(_ptr(grads)),
                                               _vp(_ptr(vnorm)), _vp(_ptr(visible))))

@@ -401,13 +401,18 @@ class Trainer:
     batch (each rank passes its own views; the batch size is views_per_rank * world)."""
 
     def __init__(self, ctx: Context, scene: DeviceScene, config: TrainConfig, dist=None,
-                 scene_extent: Optional[float] = None, seed: int = 0):
+                 scene_extent: Optional[float] = None, seed: int = 0, start_step: int = 0):
+        """``start_step``: the number of steps already taken (resuming a run): the next step is
+        start_step + 1, with its SH degree, learning-rate schedule and intervals (trainer.cpp:115-150)."""
         config.validate()
+        if start_step < 0:
+            raise ValueError("Trainer: start_step must be >= 0")
         self.ctx, self.scene, self.cfg, self.dist = ctx, scene, config, dist
         self.scene_extent = scene_extent  # camera_extent(dataset) (trainer.cpp:88-99); None: no densification
         self.rng = Rng(ctx, seed)
         self.opt = DeviceOptimizer(ctx, scene)
-        self.step_count = 0
+        self.step_count = int(start_step)
+        self._knn_built = False
         self.nbrs = None
         self._img = None
         self._dl = None
@@ -451,6 +456,7 @@ class Trainer:
 
     # trainer.cpp:107-113
     def rebuild_knn(self):
+        self._knn_built = True
         w = self.cfg.loss
         if w.lambda_consistency != 0 and self.scene.n > w.k_neighbors:
             self.nbrs = build_knn4d(self.ctx, self.scene, w.k_neighbors, out=self.nbrs)
@@ -561,7 +567,7 @@ class Trainer:
         if sh != self.scene.sh_degree:
             self.ctx.L.rgs_scene_set_sh_degree(self.scene.h, sh)
             self.scene.sh_degree = sh
-        if self.nbrs is None and step == 1:
+        if self.nbrs is None and not self._knn_built:  # trainer.cpp:107-113 (first step of the run)
             self.rebuild_knn()
         defer = self.defer_checks and not self._checked_next
         self._checked_next = False
