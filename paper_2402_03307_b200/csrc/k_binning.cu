@@ -563,7 +563,7 @@ __global__ void k_frame_init(BinState* st, uint32_t pair_cap, uint32_t* bucket_c
         z.pair_cap = pair_cap;
         z.n_pairs_eff = 0;
         z.overflow = 0;
-        z.pad2 = 0;
+        z.pad2 = z.pad3 = 0;
         *st = z;
     }
     if (i < nb) {

@@ -13,6 +13,8 @@
 // the staged splats against its sub-tile with the bounding box of the alpha >= 1/255
 // ellipse (a ballot per 32 splats) and then walks only the surviving ones, in depth
 // order.  The exponent is kept in log2 units so alpha costs one MUFU.EX2.
+#include <cstdlib>
+
 #include "rgs_internal.cuh"
 
 namespace rgs_dev {
@@ -25,9 +27,11 @@ struct StagedSplat {
     float4 d;  // (ex, ey, pc2, R)     culling extents, clamp-gate power, R >= 1 / (1 - alpha_max)
 };
 
+// Staged values of one splat, relative to the tile origin (px0, py0); `lmax`: the radial cull's
+// eigenvalue bound.  Shared by K5 (structure-of-arrays staging) and K6 (StagedSplat).
 template <bool FLOW>
-__device__ __forceinline__ void stage(const SplatArrays& sp, uint32_t id, double px0, double py0, StagedSplat* dst,
-                                      float* lmax = nullptr) {
+__device__ __forceinline__ void stage_values(const SplatArrays& sp, uint32_t id, double px0, double py0, float4& A,
+                                             float4& Bv, float4& C, float4& Dv, float& lmax) {
     const double2 m = sp.mean2[id];
     const float mx = (float)(m.x - px0), my = (float)(m.y - py0);
     const float4 cf = sp.conic_f[id];
@@ -35,45 +39,57 @@ __device__ __forceinline__ void stage(const SplatArrays& sp, uint32_t id, double
     const float2 g = sp.guard_f[id];
     const float4 e = sp.ext_f[id];
     const float D = 1.5e-6f + 1.2e-7f * (fabsf(mx) * e.z + fabsf(my) * e.w);
-    dst->a = make_float4(mx, my, cf.x, cf.y);
-    dst->b = make_float4(cf.z, D, col.w, g.x);
+    A = make_float4(mx, my, cf.x, cf.y);
+    Bv = make_float4(cf.z, D, col.w, g.x);
     if (FLOW) {
         const double4 f = sp.flow_radius[id];
-        dst->c = make_float4((float)f.x, (float)f.y, 0.f, cf.w);
+        C = make_float4((float)f.x, (float)f.y, 0.f, cf.w);
     } else {
-        dst->c = make_float4(col.x, col.y, col.z, cf.w);
+        C = make_float4(col.x, col.y, col.z, cf.w);
     }
     // 1 / (1 - alpha) <= 1 / (1 - min(0.99, ab)): the T-gate error bound without a reciprocal
     const float am = fminf(0.99f, cf.w);
-    dst->d = make_float4(e.x, e.y, g.y, __fdiv_ru(1.f, __fsub_rd(1.f, am)) * 1.000001f);
-    if (lmax) {
-        // Largest eigenvalue of the (negative definite) log2-power form [[ca2, cb2/2], [cb2/2, cc2]]
-        // plus a slack far above its FP32 rounding: p2 <= lmax d^2 at Euclidean distance d from
-        // the mean.  Near-degenerate conics get lmax >= 0 (no culling from it).
-        const float h = 0.5f * (cf.x + cf.z), dd = 0.5f * (cf.x - cf.z), o = 0.5f * cf.y;
-        const float lm = h + sqrtf(fmaf(dd, dd, o * o));
-        *lmax = lm + 1e-5f * (fabsf(cf.x) + fabsf(cf.z) + fabsf(cf.y));
-    }
+    Dv = make_float4(e.x, e.y, g.y, __fdiv_ru(1.f, __fsub_rd(1.f, am)) * 1.000001f);
+    // Largest eigenvalue of the (negative definite) log2-power form [[ca2, cb2/2], [cb2/2, cc2]]
+    // plus a slack far above its FP32 rounding: p2 <= lmax d^2 at Euclidean distance d from
+    // the mean.  Near-degenerate conics get lmax >= 0 (no culling from it).
+    const float h = 0.5f * (cf.x + cf.z), dd = 0.5f * (cf.x - cf.z), o = 0.5f * cf.y;
+    const float lm = h + sqrtf(fmaf(dd, dd, o * o));
+    lmax = lm + 1e-5f * (fabsf(cf.x) + fabsf(cf.z) + fabsf(cf.y));
 }
 
-// Per-warp culling of a staged splat against the warp's 8x4 sub-tile with the bounding box
-// of its alpha >= 1/255 ellipse.  (An exact ellipse-rectangle test removed 19% of the
-// evaluations but cost more in the ballot phase than it saved: measured, round 1.)
-template <int H = 3>
-__device__ __forceinline__ bool overlaps(const StagedSplat& s, float sx0, float sy0) {
-    return (s.a.x + s.d.x >= sx0) && (s.a.x - s.d.x <= sx0 + 7.f) && (s.a.y + s.d.y >= sy0) &&
-           (s.a.y - s.d.y <= sy0 + (float)H);
+template <bool FLOW>
+__device__ __forceinline__ void stage(const SplatArrays& sp, uint32_t id, double px0, double py0, StagedSplat* dst,
+                                      float* lmax) {
+    float4 A, Bv, C, Dv;
+    float l;
+    stage_values<FLOW>(sp, id, px0, py0, A, Bv, C, Dv, l);
+    dst->a = A;
+    dst->b = Bv;
+    dst->c = C;
+    dst->d = Dv;
+    *lmax = l;
 }
-// ... and a radial bound: p2 <= lmax d^2 with d the distance from the mean to the sub-tile's
-// pixel rectangle (shrunk by 1e-3 px).  With the error floor D and a 1e-3 margin below the
-// alpha threshold, every pixel of the sub-tile certainly skips the splat in FP64, so K5 and K6
-// (which cull identically) drop it without changing any gate decision.
+
+// Per-warp culling of a staged splat against the warp's 8 x (H+1) sub-tile with the bounding box
+// of its alpha >= 1/255 ellipse (an exact ellipse-rectangle test removed 19% of the evaluations
+// but cost more in the ballot phase than it saved: measured, round 1), and a radial bound:
+// p2 <= lmax d^2 with d the distance from the mean to the sub-tile's pixel rectangle (shrunk by
+// 1e-3 px).  With the error floor D and a 1e-3 margin below the alpha threshold, every pixel of
+// the sub-tile certainly skips the splat in FP64, so K5 and K6 (which cull identically) drop it
+// without changing any gate decision.
+template <int H = 3>
+__device__ __forceinline__ bool overlaps_v(const float4& a, const float4& b, const float4& d, float lmax, float sx0,
+                                           float sy0) {
+    if (!((a.x + d.x >= sx0) && (a.x - d.x <= sx0 + 7.f) && (a.y + d.y >= sy0) && (a.y - d.y <= sy0 + (float)H)))
+        return false;
+    const float ddx = fmaxf(fmaxf(sx0 - a.x, a.x - (sx0 + 7.f)) - 1e-3f, 0.f);
+    const float ddy = fmaxf(fmaxf(sy0 - a.y, a.y - (sy0 + (float)H)) - 1e-3f, 0.f);
+    return lmax * fmaf(ddx, ddx, ddy * ddy) >= b.z - b.y - 1e-3f;
+}
 template <int H = 3>
 __device__ __forceinline__ bool overlaps_radial(const StagedSplat& s, float lmax, float sx0, float sy0) {
-    if (!overlaps<H>(s, sx0, sy0)) return false;
-    const float ddx = fmaxf(fmaxf(sx0 - s.a.x, s.a.x - (sx0 + 7.f)) - 1e-3f, 0.f);
-    const float ddy = fmaxf(fmaxf(sy0 - s.a.y, s.a.y - (sy0 + (float)H)) - 1e-3f, 0.f);
-    return lmax * fmaf(ddx, ddx, ddy * ddy) >= s.b.z - s.b.y - 1e-3f;
+    return overlaps_v<H>(s.a, s.b, s.d, lmax, sx0, sy0);
 }
 
 enum { kSkip = 0, kAccept = 1, kAmbiguous = 2 };
@@ -94,6 +110,17 @@ __device__ __forceinline__ bool gate_skip(float p, float M, float pa2) { return 
 // (not skipped and) power > 0 or alpha < 1/255 within the bound
 __device__ __forceinline__ bool gate_ambiguous(float p, float M, float pa2) {
     return (p > -M) | (__fsub_rn(p, M) <= pa2);
+}
+
+// gate_values with paired FP32 instructions (FADD2 / FMUL2, sm_100): the same IEEE operations
+// on the same operands, so p2 and M are bit-identical to gate_values (K6 replays K5's decisions).
+__device__ __forceinline__ void gate_values_x2(const float4& a, const float4& b, float2 fp, float& p, float& M) {
+    const float2 dxy = __fadd2_rn(fp, make_float2(-a.x, -a.y));           // (dx, dy)
+    const float2 tv = __fmul2_rn(make_float2(a.z, a.w), make_float2(dxy.x, dxy.x));  // (ca2 dx, cb2 dx)
+    const float u = __fmul_rn(b.x, dxy.y);
+    const float q = __fmaf_rn(tv.x, dxy.x, __fmul_rn(u, dxy.y));
+    p = __fmaf_rn(tv.y, dxy.y, q);
+    M = __fmaf_rn(b.w, q, b.y);
 }
 
 __device__ __forceinline__ int classify(const float4& a, const float4& b, float fpx, float fpy, float& p, float& M,
@@ -119,9 +146,9 @@ __device__ __forceinline__ float blend_alpha(float ab, float p) { return fminf(0
 
 constexpr unsigned kFull = 0xffffffffu;
 
-// K5: forward blend.
+// K5 (round-1 form, kept for A/B runs with RGS_K5=1): forward blend.
 template <bool FLOW, bool COUNT>
-__global__ void __launch_bounds__(256, 5) k_blend_fp32(SplatArrays sp, const uint32_t* __restrict__ vals,
+__global__ void __launch_bounds__(256, 5) k_blend_fp32_v1(SplatArrays sp, const uint32_t* __restrict__ vals,
                                                     const uint2* __restrict__ ranges, DevCamera cam, float3 bg,
                                                     float* __restrict__ image, double* __restrict__ final_T,
                                                     uint32_t* __restrict__ n_contrib, uint32_t* slow_list,
@@ -240,6 +267,176 @@ __global__ void __launch_bounds__(256, 5) k_blend_fp32(SplatArrays sp, const uin
     } else {
         image[(size_t)pix * 3 + 0] = fmaf(T, bg.x, acc0);
         image[(size_t)pix * 3 + 1] = fmaf(T, bg.y, acc1);
+        image[(size_t)pix * 3 + 2] = fmaf(T, bg.z, acc2);
+        final_T[pix] = (double)T;
+        n_contrib[pix] = (uint32_t)contrib;
+    }
+}
+
+// Transmittance-gate thresholds of K5's common-case test (rasterizer.cpp:111): with a relative
+// error bound errN on the FP32 test_T, test_T (1 - errN) > kStopHi certainly continues and
+// test_T (1 + errN) < kStopLo certainly stops; the 2e-7 margins cover the rounding of the
+// fused products and of the float constant 1e-4f against the double 1e-4.
+constexpr float kStopHi = 1.0000002e-4f, kStopLo = 0.9999998e-4f;
+
+// K5: forward blend.  CTA per 16x16 tile, warp per 8x4 sub-tile, one pixel per lane.
+// Per batch of 256 splats the CTA stages the blend records in shared memory as structure of
+// arrays; per window of 32 staged splats each warp culls them against its sub-tile (a ballot)
+// and copies the survivors, in order, into its own compacted list; then every lane walks that
+// list with a plain induction pointer.  The gate decisions are the shared gate_values /
+// gate_skip / gate_ambiguous of K6; the transmittance gate is one fused test in the common
+// case (certainly continue), with stop / ambiguity resolved on the rare path.  A lane that
+// stops or turns slow leaves the walk (no per-visit done test).
+template <bool FLOW, bool COUNT>
+__global__ void __launch_bounds__(256, 5) k_blend_fp32(SplatArrays sp, const uint32_t* __restrict__ vals,
+                                                    const uint2* __restrict__ ranges, DevCamera cam, float3 bg,
+                                                    float* __restrict__ image, double* __restrict__ final_T,
+                                                    uint32_t* __restrict__ n_contrib, uint32_t* slow_list,
+                                                    int* slow_count, unsigned long long* counters) {
+    constexpr int kWarps = kTilePixels / 32;
+    __shared__ float4 s_a[kTilePixels], s_b[kTilePixels], s_c[kTilePixels], s_d[kTilePixels];
+    __shared__ float s_l[kTilePixels];
+    __shared__ StagedSplat w_list[kWarps][32];  // (a, b, c, (pc2, R, -, -)) of the window's survivors
+    __shared__ uint8_t w_k[kWarps][32];
+    const int tile = blockIdx.x;
+    const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sx0 = (warp & 1) * 8, sy0 = (warp >> 1) * 4;
+    const int lx = sx0 + (lane & 7), ly = sy0 + (lane >> 3);
+    const int px = tx * kTile + lx, py = ty * kTile + ly;
+    const bool inside = px < cam.width && py < cam.height;
+    const uint2 rg = ranges[tile];
+    const double px0 = tx * kTile, py0 = ty * kTile;
+    const float fpx = (float)lx, fpy = (float)ly, fsx0 = (float)sx0, fsy0 = (float)sy0;
+    const unsigned lt_mask = (1u << lane) - 1u;
+
+    const float2 fp2 = make_float2(fpx, fpy);
+    float T = 1.f, errT3 = 3e-7f, acc2 = 0.f;  // errT3 = errT + 3e-7
+    float2 acc01 = make_float2(0.f, 0.f);
+    int contrib = 0;
+    bool done = !inside, slow = false, stopped = false;
+    uint32_t n_eval = 0, n_blend = 0, n_ref = 0;  // COUNT only
+    bool warp_done = __all_sync(kFull, done);
+
+    for (uint32_t start = rg.x; start < rg.y; start += kTilePixels) {
+        if (__syncthreads_count(done) == kTilePixels) break;
+        const uint32_t j = start + threadIdx.x;
+        if (j < rg.y) {
+            float4 A, Bv, C, Dv;
+            float l;
+            stage_values<FLOW>(sp, vals[j], px0, py0, A, Bv, C, Dv, l);
+            s_a[threadIdx.x] = A;
+            s_b[threadIdx.x] = Bv;
+            s_c[threadIdx.x] = C;
+            s_d[threadIdx.x] = Dv;
+            s_l[threadIdx.x] = l;
+        }
+        __syncthreads();
+        const int n = (int)min((uint32_t)kTilePixels, rg.y - start);
+        if (warp_done) continue;
+        for (int c = 0; c < n; c += 32) {
+            const int k0 = c + lane;
+            bool surv = false;
+            float4 a, b, d;
+            if (k0 < n) {
+                a = s_a[k0];
+                b = s_b[k0];
+                d = s_d[k0];
+                surv = overlaps_v(a, b, d, s_l[k0], fsx0, fsy0);
+            }
+            const unsigned m = __ballot_sync(kFull, surv);
+            if (surv) {
+                const int q = __popc(m & lt_mask);
+                StagedSplat* e = &w_list[warp][q];
+                e->a = a;
+                e->b = b;
+                e->c = s_c[k0];
+                e->d = d;
+                w_k[warp][q] = (uint8_t)lane;
+            }
+            __syncwarp();
+            if (!done) {
+                const StagedSplat* const first = w_list[warp];
+                const StagedSplat* const end = first + __popc(m);
+                int lastq = -1, q = 0;
+                for (const StagedSplat* e = first; e != end; ++e, ++q) {
+                    const float4 a2 = e->a, b2 = e->b;
+                    float p, M;
+                    gate_values_x2(a2, b2, fp2, p, M);
+                    if (COUNT) ++n_eval;
+                    if (gate_skip(p, M, b2.z)) continue;
+                    const float4 cc = e->c;
+                    const float2 pr = make_float2(e->d.z, e->d.w);  // (pc2, R)
+                    const float al = blend_alpha(cc.w, p);
+                    const float test_T = __fmul_rn(T, __fsub_rn(1.f, al));
+                    const float errN = fmaf(al * M, pr.y, errT3);
+                    // ambiguous alpha / power gate, or the backward's clamp gate (unclamped
+                    // alpha <= 0.99, rasterizer.cpp:356), within their error bounds
+                    const bool amb_gc = gate_ambiguous(p, M, b2.z) |
+                                        ((__fadd_rn(p, M) >= pr.x) & (__fsub_rn(p, M) <= pr.x));
+                    if (!amb_gc && fmaf(-test_T, errN, test_T) > kStopHi) {
+                        const float w = al * T;
+                        acc01 = __ffma2_rn(make_float2(cc.x, cc.y), make_float2(w, w), acc01);
+                        acc2 = fmaf(cc.z, w, acc2);
+                        T = test_T;
+                        errT3 = errN + 3e-7f;
+                        lastq = q;
+                        if (COUNT) ++n_blend;
+                        continue;
+                    }
+                    // rare: certainly stop (rasterizer.cpp:111, the splat is not blended), or a
+                    // decision inside its error bound -> the pixel goes to the FP64 fix-up
+                    if (!amb_gc && fmaf(test_T, errN, test_T) < kStopLo) {
+                        done = stopped = true;
+                        if (COUNT) n_ref = start - rg.x + c + w_k[warp][q] + 1;
+                        break;
+                    }
+                    if (COUNT) {
+                        // slow-pixel reasons: power > 0 / alpha gate, clamp gate, transmittance gate
+                        const bool amb_g = gate_ambiguous(p, M, b2.z);
+                        const int r = amb_g ? ((p > -M) ? 3 : 4) : (amb_gc ? 5 : 6);
+                        atomicAdd(counters + r, 1ull);
+                    }
+                    slow = done = true;
+                    break;
+                }
+                if (lastq >= 0) contrib = (int)(start - rg.x) + c + w_k[warp][lastq] + 1;
+            }
+            __syncwarp();  // the list is rewritten by the next window
+            if (__all_sync(kFull, done)) {
+                warp_done = true;
+                break;
+            }
+        }
+    }
+    if (COUNT) {
+        // E of the roofline = evaluations of the reference algorithm (every list entry up
+        // to the termination point); n_eval = the ones this kernel actually evaluated.
+        unsigned long long e = inside ? (stopped ? n_ref : rg.y - rg.x) : 0, b = n_blend, ke = n_eval;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            e += __shfl_xor_sync(kFull, e, o);
+            b += __shfl_xor_sync(kFull, b, o);
+            ke += __shfl_xor_sync(kFull, ke, o);
+        }
+        if (lane == 0) {
+            atomicAdd(counters + 0, e);
+            atomicAdd(counters + 1, b);
+            atomicAdd(counters + 2, ke);
+        }
+    }
+    if (!inside) return;
+    const uint32_t pix = (uint32_t)py * cam.width + px;
+    if (slow) {
+        slow_list[atomicAdd(slow_count, 1)] = pix;
+        return;
+    }
+    if (FLOW) {
+        image[(size_t)pix * 2 + 0] = acc01.x;
+        image[(size_t)pix * 2 + 1] = acc01.y;
+    } else {
+        image[(size_t)pix * 3 + 0] = fmaf(T, bg.x, acc01.x);
+        image[(size_t)pix * 3 + 1] = fmaf(T, bg.y, acc01.y);
         image[(size_t)pix * 3 + 2] = fmaf(T, bg.z, acc2);
         final_T[pix] = (double)T;
         n_contrib[pix] = (uint32_t)contrib;
@@ -417,23 +614,36 @@ __global__ void __launch_bounds__(kBwdThreads) k_backward_fp32(SplatArrays sp, c
 namespace rgs_launch {
 using namespace rgs_dev;
 
+static int g_k5_variant = 2;  // RGS_K5=1 selects the round-1 kernel (A/B measurements)
+
 void blend_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges, const DevCamera& cam,
                 float3 bg, int flow_mode, float* image, double* final_T, uint32_t* n_contrib, uint32_t* slow_list,
                 int* slow_count, unsigned long long* counters, cudaStream_t s) {
     const int tiles = cam.tiles_x * cam.tiles_y;
-    if (flow_mode)
-        k_blend_fp32<true, false><<<tiles, kTilePixels, 0, s>>>(sp, pair_vals, ranges, cam, bg, image, final_T,
-                                                                 n_contrib, slow_list, slow_count, counters);
-    else if (counters)
-        k_blend_fp32<false, true><<<tiles, kTilePixels, 0, s>>>(sp, pair_vals, ranges, cam, bg, image, final_T,
-                                                                 n_contrib, slow_list, slow_count, counters);
-    else
-        k_blend_fp32<false, false><<<tiles, kTilePixels, 0, s>>>(sp, pair_vals, ranges, cam, bg, image, final_T,
-                                                                  n_contrib, slow_list, slow_count, counters);
+#define RGS_K5_LAUNCH(K)                                                                                           \
+    if (flow_mode)                                                                                                 \
+        K<true, false><<<tiles, kTilePixels, 0, s>>>(sp, pair_vals, ranges, cam, bg, image, final_T, n_contrib,    \
+                                                     slow_list, slow_count, counters);                            \
+    else if (counters)                                                                                             \
+        K<false, true><<<tiles, kTilePixels, 0, s>>>(sp, pair_vals, ranges, cam, bg, image, final_T, n_contrib,    \
+                                                     slow_list, slow_count, counters);                            \
+    else                                                                                                           \
+        K<false, false><<<tiles, kTilePixels, 0, s>>>(sp, pair_vals, ranges, cam, bg, image, final_T, n_contrib,   \
+                                                      slow_list, slow_count, counters);
+    if (g_k5_variant == 1) {
+        RGS_K5_LAUNCH(k_blend_fp32_v1)
+    } else {
+        RGS_K5_LAUNCH(k_blend_fp32)
+    }
+#undef RGS_K5_LAUNCH
 }
 
 // Per-device kernel attributes (called from rgs_ctx_create on the context's device).
-bool raster_init() { return true; }
+bool raster_init() {
+    const char* v = std::getenv("RGS_K5");
+    g_k5_variant = (v && v[0] == '1') ? 1 : 2;
+    return true;
+}
 
 void backward_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges, const DevCamera& cam,
                    float3 bg, const double* final_T, const uint32_t* n_contrib, const float* dL_dimage,

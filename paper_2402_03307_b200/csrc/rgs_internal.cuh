@@ -107,8 +107,9 @@ struct BinState {
     uint32_t pair_cap;           // capacity of the pair buffers (set by the host)
     uint32_t n_pairs_eff;        // n_pairs, or 0 when it exceeds pair_cap (overflow)
     uint32_t overflow;           // 1: the view must be re-rendered with larger buffers
-    uint32_t pad2;
+    uint32_t pad2, pad3;         // (explicit: the whole 64 B are written, so copies read no padding)
 };
+static_assert(sizeof(BinState) == 64, "BinState is copied as 64 initialised bytes");
 
 // Guard-band constants for the FP32 blend (DESIGN.md §"FP32 blend with FP64 re-decision").
 constexpr float kGuardFloor = 1e-6f;

@@ -26,8 +26,6 @@ def test_compute_sanitizer(tool):
     cmd = [_sanitizer(), "--tool", tool, "--error-exitcode", "3", "--target-processes", "all"]
     if tool == "memcheck":
         cmd += ["--leak-check", "no"]
-    if tool == "initcheck":
-        cmd += ["--track-unused-memory", "no"]
     cmd += [sys.executable, os.path.join(ROOT, "tools", "sanitize_case.py")]
     env = dict(os.environ, PYTORCH_NO_CUDA_MEMORY_CACHING="1")
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=1500, env=env, cwd=ROOT)
