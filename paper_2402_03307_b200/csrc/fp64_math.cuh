@@ -158,10 +158,11 @@ struct SliceState {
     double lambda;
 };
 
-// gaussian.cpp:9-17 + 32-47.  Returns 0 (ok), an error code, or -1 for
-// DegenerateTimeError (caught by build_splats -> Gaussian skipped).
-__device__ __forceinline__ int d_slice(const double* mean4, const double* ls, const double* rot, double t,
-                                       SliceState& s) {
+// gaussian.cpp:9-17 + 32-40, the part of slice_at that does not depend on t: normalize,
+// to_matrix, Sigma4 = R diag(q) R^T, the DegenerateTime check, lambda, speed and the Schur
+// complement cov3.  Returns 0 (ok), an error code, or -1 for DegenerateTimeError (caught by
+// build_splats -> Gaussian skipped).
+__device__ __forceinline__ int d_slice_static(const double* ls, const double* rot, SliceState& s) {
     int rc = d_normalize(rot, s.nrm);
     if (rc) return rc;
     d_to_matrix(s.nrm, s.R);
@@ -186,7 +187,6 @@ __device__ __forceinline__ int d_slice(const double* mean4, const double* ls, co
             else s.W = a;
         }
     if (s.W < kTemporalFloor) return -1;
-    s.dt = t - mean4[3];
     s.lambda = 1 / s.W;
 #pragma unroll
     for (int i = 0; i < 3; ++i) s.speed[i] = s.V[i] / s.W;
@@ -198,9 +198,23 @@ __device__ __forceinline__ int d_slice(const double* mean4, const double* ls, co
             double d = kCov3Eps * (i == j ? 1.0 : 0.0);
             s.cov[i * 3 + j] = (s.U[i * 3 + j] - b) + d;
         }
+    return 0;
+}
+
+// gaussian.cpp:41-44, the t-dependent rest: dt, the conditional mean and the temporal decay.
+__device__ __forceinline__ void d_slice_time(const double* mean4, double t, SliceState& s) {
+    s.dt = t - mean4[3];
 #pragma unroll
     for (int i = 0; i < 3; ++i) s.mean[i] = mean4[i] + s.dt * s.speed[i];
     s.decay = rgs_exp::glibc_exp(-0.5 * s.lambda * s.dt * s.dt);
+}
+
+// gaussian.cpp:9-17 + 32-47 (the same operations in the same order as the two halves above).
+__device__ __forceinline__ int d_slice(const double* mean4, const double* ls, const double* rot, double t,
+                                       SliceState& s) {
+    const int rc = d_slice_static(ls, rot, s);
+    if (rc) return rc;
+    d_slice_time(mean4, t, s);
     return 0;
 }
 
@@ -383,8 +397,12 @@ struct ProjState {
 
 // rasterizer.cpp:215-243 geometric part (everything but SH colour / flow).
 // Returns true when the splat survives the culls.
-__device__ __forceinline__ bool d_project_geom(const SliceState& s, const DevCamera& cam, double opacity_logit,
+// `opacity_in`: the opacity logit, or (PRE_OPACITY) the opacity sigmoid(logit) already evaluated
+// with the same expression (the per-scene slice cache of a batch).
+template <bool PRE_OPACITY = false>
+__device__ __forceinline__ bool d_project_geom(const SliceState& s, const DevCamera& cam, double opacity_in,
                                                ProjState& o) {
+    const double opacity_logit = opacity_in;
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
         double a = cam.R[i * 3 + 0] * s.mean[0];
@@ -444,7 +462,7 @@ __device__ __forceinline__ bool d_project_geom(const SliceState& s, const DevCam
     if (o.mean2[0] + o.radius < 0 || o.mean2[0] - o.radius > cam.width - 1 || o.mean2[1] + o.radius < 0 ||
         o.mean2[1] - o.radius > cam.height - 1)
         return false;
-    o.opacity = 1 / (1 + rgs_exp::glibc_exp(-opacity_logit));
+    o.opacity = PRE_OPACITY ? opacity_in : 1 / (1 + rgs_exp::glibc_exp(-opacity_logit));
     o.alpha_base = o.opacity * s.decay;
     if (o.alpha_base < kMinAlpha) return false;
     double v[3];

@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(512) k_bucket_sort_big(const uint32_t* __restr
 // --------------------------------------------------------------------------- duplicate
 // Pair emission of one warp (32 consecutive ranks) for k_duplicate.
 __device__ __forceinline__ void emit_pairs(uint32_t id, uint32_t cnt, uint32_t off, ushort4 q, int lane,
-                                                uint32_t* keys, uint32_t* vals) {
+                                                uint32_t* keys, uint32_t* vals, int ty_shift) {
     // inclusive prefix of counts within the warp
     uint32_t incl = cnt;
 #pragma unroll
@@ -354,7 +354,7 @@ __device__ __forceinline__ void emit_pairs(uint32_t id, uint32_t cnt, uint32_t o
         if (k < total) {
             const int m = (int)(k - (o_incl - o_cnt));
             const int dy = m / o_w, dx = m - dy * o_w;
-            keys[base + k] = ((uint32_t)(o_y0 + dy) << 8) | (uint32_t)(o_x0 + dx);  // packed (ty, tx)
+            keys[base + k] = ((uint32_t)(o_y0 + dy) << ty_shift) | (uint32_t)(o_x0 + dx);  // packed (ty, tx)
             vals[base + k] = o_id;
         }
     }
@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(256) k_duplicate(const uint32_t* __restrict__ 
                                                    const uint32_t* __restrict__ pair_off,
                                                    const uint32_t* __restrict__ sorted_tiles,
                                                    const ushort4* __restrict__ rect, const BinState* __restrict__ st,
-                                                   int tiles_x, uint32_t* keys, uint32_t* vals, int* hist_diff) {
+                                                   int ty_shift, uint32_t* keys, uint32_t* vals, int* hist_diff) {
     __shared__ int sdx[257], sdy[257];
     for (int e = threadIdx.x; e < 257; e += blockDim.x) sdx[e] = sdy[e] = 0;
     __syncthreads();
@@ -385,14 +385,16 @@ __global__ void __launch_bounds__(256) k_duplicate(const uint32_t* __restrict__ 
         off = pair_off[r];
         if (cnt) {
             q = rect[id];
-            const int h = q.w - q.z + 1, wd = q.y - q.x + 1;
-            atomicAdd(&sdx[q.x], h);
-            atomicAdd(&sdx[q.y + 1], -h);
-            atomicAdd(&sdy[q.z], wd);
-            atomicAdd(&sdy[q.w + 1], -wd);
+            if (ty_shift == 8) {  // byte digits tx / ty: histograms per rectangle
+                const int h = q.w - q.z + 1, wd = q.y - q.x + 1;
+                atomicAdd(&sdx[q.x], h);
+                atomicAdd(&sdx[q.y + 1], -h);
+                atomicAdd(&sdy[q.z], wd);
+                atomicAdd(&sdy[q.w + 1], -wd);
+            }
         }
     }
-    if (warp_live) emit_pairs(id, cnt, off, q, lane, keys, vals);
+    if (warp_live) emit_pairs(id, cnt, off, q, lane, keys, vals, ty_shift);
     __syncthreads();
     for (int e = threadIdx.x; e < 257; e += blockDim.x) {
         if (sdx[e]) atomicAdd(&hist_diff[e], sdx[e]);
@@ -414,6 +416,7 @@ constexpr int kRadixWarps = kRadixThreads / 32;
 constexpr int kRadixRounds = 16;
 constexpr int kBlockTile = kRadixThreads * kRadixRounds;  // 4096
 constexpr int kRadixDigits = 256;
+constexpr int kAuxInts = 784;  // digit histograms + tickets (tile_radix_sort)
 
 // One-sweep digit pass: the global digit
 // starts come from the histograms k_duplicate built, and each block's offset inside a digit
@@ -425,7 +428,7 @@ constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kCountMask = (1u <<
 __global__ void __launch_bounds__(kRadixThreads) k_radix_onesweep(const uint32_t* __restrict__ keys_in,
                                                                   const uint32_t* __restrict__ vals_in,
                                                                   const BinState* __restrict__ st, int shift,
-                                                                  const int* __restrict__ hist_diff,
+                                                                  const int* __restrict__ hist_diff, int hist_plain,
                                                                   uint32_t* status, uint32_t* ticket,
                                                                   uint32_t* keys_out, uint32_t* vals_out) {
     __shared__ uint32_t wcnt[kRadixWarps][kRadixDigits];
@@ -508,7 +511,7 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_onesweep(const uint32_t
     // global digit start: exclusive prefix over digits of the histogram (difference array)
     {
         uint32_t t2;
-        const uint32_t h = (uint32_t)block_inclusive_diff(hist_diff[dd]);
+        const uint32_t h = hist_plain ? (uint32_t)hist_diff[dd] : (uint32_t)block_inclusive_diff(hist_diff[dd]);
         const uint32_t ex = block_exclusive_scan(h, &t2);
         gbase[dd] = ex + dstart[dd];
     }
@@ -537,6 +540,26 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_onesweep(const uint32_t
         keys_out[g] = k;
         vals_out[g] = sval[i];
     }
+}
+
+// Wide tile keys (images beyond 256 tiles per axis: key = ty << 12 | tx, three byte passes):
+// the byte-digit histograms of all three passes in one read of the keys (block histograms in
+// shared memory, then global atomics).
+__global__ void __launch_bounds__(256) k_digit_hist3(const uint32_t* __restrict__ keys, const BinState* __restrict__ st,
+                                                     int* hist) {
+    __shared__ int h[3][kRadixDigits];
+    for (int e = threadIdx.x; e < 3 * kRadixDigits; e += blockDim.x) (&h[0][0])[e] = 0;
+    __syncthreads();
+    const uint32_t n = st->n_pairs_eff;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t k = keys[i];
+        atomicAdd(&h[0][k & 0xffu], 1);
+        atomicAdd(&h[1][(k >> 8) & 0xffu], 1);
+        atomicAdd(&h[2][(k >> 16) & 0xffu], 1);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < 3 * kRadixDigits; e += blockDim.x)
+        if ((&h[0][0])[e]) atomicAdd(&hist[e], (&h[0][0])[e]);
 }
 
 // RGS_FLAG_DEFER_CHECKS: the view's rotor error / pair-buffer overflow into the context's
@@ -582,9 +605,10 @@ __global__ void k_check_capacity(BinState* st) {
 // Per-tile [start, end) from the sorted keys: grid-stride, four keys per thread (one 16-byte
 // load) compared with their neighbours; sized by the device-side pair count.
 __global__ void __launch_bounds__(256) k_tile_ranges(const uint32_t* __restrict__ keys, const BinState* __restrict__ st,
-                                                     int tiles_x, uint2* ranges) {
+                                                     int tiles_x, int ty_shift, uint2* ranges) {
     const uint32_t n = st->n_pairs_eff;
-    constexpr uint32_t kNone = 0xffffffffu;  // never a tile key (ty, tx < 2^8)
+    constexpr uint32_t kNone = 0xffffffffu;  // never a tile key (ty, tx < 2^12)
+    const uint32_t tx_mask = (1u << ty_shift) - 1u;
     for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; 4 * q < n; q += gridDim.x * blockDim.x) {
         const uint32_t i0 = 4 * q;
         uint32_t k[6];
@@ -603,7 +627,7 @@ __global__ void __launch_bounds__(256) k_tile_ranges(const uint32_t* __restrict_
 #pragma unroll
         for (int j = 1; j <= 4; ++j) {
             if (k[j] == kNone) break;
-            const uint32_t t = (k[j] >> 8) * (uint32_t)tiles_x + (k[j] & 0xffu);
+            const uint32_t t = (k[j] >> ty_shift) * (uint32_t)tiles_x + (k[j] & tx_mask);
             const uint32_t i = i0 + j - 1;
             if (k[j - 1] != k[j]) ranges[t].x = i;
             if (k[j + 1] != k[j]) ranges[t].y = i + 1;
@@ -660,34 +684,58 @@ void depth_ranks(const uint8_t* valid, const unsigned long long* key, const uint
                                                                    reinterpret_cast<SortRec*>(big_scratch));
 }
 
+// Tile key layout: ty << 8 | tx (two byte passes) up to 256 x 256 tiles, else ty << 12 | tx
+// (three byte passes, up to 4096 x 4096 tiles).
+int tile_key_shift(int tiles_x, int tiles_y) { return (tiles_x <= 256 && tiles_y <= 256) ? 8 : 12; }
+
 void duplicate(const uint32_t* sorted_ids, const uint32_t* pair_off, const uint32_t* sorted_tiles,
-               const ushort4* rect, const BinState* st, int n, int tiles_x, uint32_t* keys, uint32_t* vals,
-               int* aux, cudaStream_t s) {
-    cudaMemsetAsync(aux, 0, sizeof(int) * 528, s);
+               const ushort4* rect, const BinState* st, int n, int tiles_x, int tiles_y, uint32_t* keys,
+               uint32_t* vals, int* aux, cudaStream_t s) {
+    cudaMemsetAsync(aux, 0, sizeof(int) * kAuxInts, s);
     if (n > 0)
-        k_duplicate<<<blocks(n, 256), 256, 0, s>>>(sorted_ids, pair_off, sorted_tiles, rect, st, tiles_x, keys,
-                                                    vals, aux);
+        k_duplicate<<<blocks(n, 256), 256, 0, s>>>(sorted_ids, pair_off, sorted_tiles, rect, st,
+                                                    tile_key_shift(tiles_x, tiles_y), keys, vals, aux);
 }
 
 int radix_blocks(long long n_pairs) { return std::max(blocks(n_pairs, kBlockTile), 1); }
 size_t radix_count_entries(long long n_pairs) { return (size_t)kRadixDigits * radix_blocks(n_pairs); }
 
-// Two stable byte passes (tx, then ty); the sorted pairs end back in (keys_a, vals_a).
-// aux: [0, 514) the digit-histogram difference arrays k_duplicate filled, [520, 522) tickets;
-// status_a / status_b: radix_count_entries() u32 each (decoupled look-back state).
-void tile_radix_sort(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32_t* vals_b, const BinState* st,
-                     long long n_pairs, int tiles_x, int n_tiles, uint32_t* status_a, uint32_t* status_b,
-                     int* aux, uint2* ranges, cudaStream_t s) {
+// Two stable byte passes (tx, then ty) on ty << 8 | tx; the sorted pairs end back in (keys_a,
+// vals_a).  Wide keys (ty << 12 | tx): three byte passes, ending in (keys_b, vals_b) -- returned.
+// aux: [0, 514) the digit-histogram difference arrays k_duplicate filled (wide keys: [0, 768) the
+// plain histograms of k_digit_hist3), [780, 783) tickets; status_a / status_b:
+// radix_count_entries() u32 each (decoupled look-back state).
+int tile_radix_sort(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32_t* vals_b, const BinState* st,
+                    long long n_pairs, int tiles_x, int tiles_y, uint32_t* status_a, uint32_t* status_b, int* aux,
+                    uint2* ranges, cudaStream_t s) {
     const int nb = radix_blocks(n_pairs);
     const size_t entries = (size_t)kRadixDigits * nb;
+    const int n_tiles = tiles_x * tiles_y;
+    const int shift = tile_key_shift(tiles_x, tiles_y);
+    uint32_t* tickets = reinterpret_cast<uint32_t*>(aux + 780);
+    int out = 0;
     cudaMemsetAsync(status_a, 0, 4 * entries, s);
     cudaMemsetAsync(status_b, 0, 4 * entries, s);
-    uint32_t* tickets = reinterpret_cast<uint32_t*>(aux + 520);
-    k_radix_onesweep<<<nb, kRadixThreads, 0, s>>>(keys_a, vals_a, st, 0, aux, status_a, tickets, keys_b, vals_b);
-    k_radix_onesweep<<<nb, kRadixThreads, 0, s>>>(keys_b, vals_b, st, 8, aux + 257, status_b, tickets + 1, keys_a,
-                                                   vals_a);
+    if (shift == 8) {
+        k_radix_onesweep<<<nb, kRadixThreads, 0, s>>>(keys_a, vals_a, st, 0, aux, 0, status_a, tickets, keys_b,
+                                                       vals_b);
+        k_radix_onesweep<<<nb, kRadixThreads, 0, s>>>(keys_b, vals_b, st, 8, aux + 257, 0, status_b, tickets + 1,
+                                                       keys_a, vals_a);
+    } else {
+        k_digit_hist3<<<148 * 2, 256, 0, s>>>(keys_a, st, aux);
+        k_radix_onesweep<<<nb, kRadixThreads, 0, s>>>(keys_a, vals_a, st, 0, aux, 1, status_a, tickets, keys_b,
+                                                       vals_b);
+        k_radix_onesweep<<<nb, kRadixThreads, 0, s>>>(keys_b, vals_b, st, 8, aux + 256, 1, status_b, tickets + 1,
+                                                       keys_a, vals_a);
+        cudaMemsetAsync(status_a, 0, 4 * entries, s);
+        k_radix_onesweep<<<nb, kRadixThreads, 0, s>>>(keys_a, vals_a, st, 16, aux + 512, 1, status_a, tickets + 2,
+                                                       keys_b, vals_b);
+        out = 1;
+    }
     cudaMemsetAsync(ranges, 0, sizeof(uint2) * (size_t)n_tiles, s);
-    k_tile_ranges<<<std::max(std::min(blocks(n_pairs, 4 * 256), 148 * 8), 1), 256, 0, s>>>(keys_a, st, tiles_x, ranges);
+    k_tile_ranges<<<std::max(std::min(blocks(n_pairs, 4 * 256), 148 * 8), 1), 256, 0, s>>>(
+        out ? keys_b : keys_a, st, tiles_x, shift, ranges);
+    return out;
 }
 
 void check_capacity(BinState* st, cudaStream_t s) { k_check_capacity<<<1, 1, 0, s>>>(st); }

@@ -6,6 +6,7 @@
 // (see fp64_math.cuh), which is what makes tile rectangles, depths and culls
 // bit-identical to the CPU oracle.
 #include "fp64_math.cuh"
+#include <algorithm>
 #include <type_traits>
 
 #include "rgs_internal.cuh"
@@ -77,7 +78,7 @@ __device__ __forceinline__ void store_splat(const SplatArrays& out, int i, doubl
     out.mean2[i] = make_double2(mx, my);
     out.conic_ab[i] = make_double4(ca, cb, cc, ab);
     out.color_depth[i] = make_double4(r, g, b, depth);
-    out.flow_radius[i] = make_double4(fx, fy, radius, 0.0);
+    if (out.flow_radius) out.flow_radius[i] = make_double4(fx, fy, radius, 0.0);  // NULL: render-only batch
     ushort4 rect;
     *ntiles = d_tile_rect(mx, my, radius, tiles_x, tiles_y, &rect);
     out.rect[i] = rect;
@@ -102,54 +103,108 @@ __device__ __forceinline__ void count_valid(bool ok, unsigned long long key, Bin
     }
 }
 
+// Slice cache of a view batch: per Gaussian, the t-independent part of slice_at
+// (d_slice_static: normalize, to_matrix, Sigma4, lambda, speed, cov3) and sigmoid(opacity), so
+// the K1 of every view of a timestamp sweep only does the t-dependent rest.  The cached values
+// are the outputs of the same FP64 operations, so every splat record stays bit-identical.
+// SoA of double2 blocks: (cov00, cov01) (cov02, cov10) (cov11, cov12) (cov20, cov21)
+// (cov22, lambda) (speed0, speed1) (speed2, opacity); status: 0 ok, -1 degenerate time (the
+// Gaussian is skipped), > 0 rotor error code.
+constexpr int kSliceCacheBlocks = 7;
+
+template <bool F64>
+__global__ void __launch_bounds__(128) k_slice_cache(ParamView P, SliceCacheView C) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.n) return;
+    double ls[4], rot[8];
+    ld_block<F64>(P, 1, i, ls);
+    ld_block<F64>(P, 2, i, rot);
+    ld_block<F64>(P, 3, i, rot + 4);
+    SliceState s;
+    const int rc = d_slice_static(ls, rot, s);
+    C.status[i] = (int8_t)rc;
+    if (rc != 0) return;
+    const double op = 1 / (1 + rgs_exp::glibc_exp(-ld_opacity<F64>(P, i)));
+    const size_t n = (size_t)P.n;
+    C.blk[0 * n + i] = make_double2(s.cov[0], s.cov[1]);
+    C.blk[1 * n + i] = make_double2(s.cov[2], s.cov[3]);
+    C.blk[2 * n + i] = make_double2(s.cov[4], s.cov[5]);
+    C.blk[3 * n + i] = make_double2(s.cov[6], s.cov[7]);
+    C.blk[4 * n + i] = make_double2(s.cov[8], s.lambda);
+    C.blk[5 * n + i] = make_double2(s.speed[0], s.speed[1]);
+    C.blk[6 * n + i] = make_double2(s.speed[2], op);
+}
+
 // K1: slice + visibility gate + project + SH colour, one thread per Gaussian
 // (rasterizer.cpp:189-204, gaussian.cpp:32-47, rasterizer.cpp:215-276, sh.cpp:16-97).
-template <bool F64>
+// CACHED: the t-independent half of the slice and the opacity come from the batch's slice cache.
+template <bool F64, bool CACHED>
 __global__ void __launch_bounds__(128) k_preprocess(ParamView P, int sh_degree, DevCamera cam, SplatArrays out,
-                                                    BinState* st) {
+                                                    BinState* st, SliceCacheView C) {
     using ShT = typename std::conditional<F64, double, float>::type;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     bool ok = false;
     uint32_t ntiles = 0;
     unsigned long long key = ~0ull;
     if (i < P.n) {
-        double mean4[4], ls[4], rot[8];
+        double mean4[4];
         ld_block<F64>(P, 0, i, mean4);
-        ld_block<F64>(P, 1, i, ls);
-        ld_block<F64>(P, 2, i, rot);
-        ld_block<F64>(P, 3, i, rot + 4);
-        const double op = ld_opacity<F64>(P, i);
         SliceState s;
-        const int rc = d_slice(mean4, ls, rot, cam.time, s);
+        int rc;
+        double op;
+        if (CACHED) {
+            rc = C.status[i];
+            if (rc == 0) {
+                const size_t n = (size_t)P.n;
+                double2 v;
+                v = C.blk[0 * n + i]; s.cov[0] = v.x; s.cov[1] = v.y;
+                v = C.blk[1 * n + i]; s.cov[2] = v.x; s.cov[3] = v.y;
+                v = C.blk[2 * n + i]; s.cov[4] = v.x; s.cov[5] = v.y;
+                v = C.blk[3 * n + i]; s.cov[6] = v.x; s.cov[7] = v.y;
+                v = C.blk[4 * n + i]; s.cov[8] = v.x; s.lambda = v.y;
+                v = C.blk[5 * n + i]; s.speed[0] = v.x; s.speed[1] = v.y;
+                v = C.blk[6 * n + i]; s.speed[2] = v.x; op = v.y;
+                d_slice_time(mean4, cam.time, s);
+            }
+        } else {
+            double ls[4], rot[8];
+            ld_block<F64>(P, 1, i, ls);
+            ld_block<F64>(P, 2, i, rot);
+            ld_block<F64>(P, 3, i, rot + 4);
+            op = ld_opacity<F64>(P, i);
+            rc = d_slice(mean4, ls, rot, cam.time, s);
+        }
         if (rc > 0) {
             atomicMin(&st->err, ((unsigned long long)i << 8) | (unsigned long long)rc);
         } else if (rc == 0) {
             const double dt = cam.time - mean4[3];
             ProjState o;
-            if (!(s.lambda * dt * dt > kVisibility) && d_project_geom(s, cam, op, o)) {
+            if (!(s.lambda * dt * dt > kVisibility) && d_project_geom<CACHED>(s, cam, op, o)) {
                 ok = true;
                 double basis[16];
                 d_sh_basis(o.dir, sh_degree, basis);
                 const int deg = sh_degree < 0 ? 0 : (sh_degree > 3 ? 3 : sh_degree);
                 const int K = (deg + 1) * (deg + 1);
                 const int nblk = (3 * K + 3) / 4;
-                ShT shv[48];
+                // colour = sh . basis + 0.5 per channel (rasterizer.cpp:245-257): the SH blocks are
+                // streamed (coefficient j = 3k + ch), each channel still summed in increasing k
+                double col[3];
 #pragma unroll
                 for (int b = 0; b < 12; ++b) {
                     if (b < nblk) {
-                        ld_block<F64>(P, 4 + b, i, shv + 4 * b);
-                    } else {
-                        shv[4 * b + 0] = shv[4 * b + 1] = shv[4 * b + 2] = shv[4 * b + 3] = 0;
+                        ShT v[4];
+                        ld_block<F64>(P, 4 + b, i, v);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int j = 4 * b + e, k = j / 3, ch = j % 3;
+                            if (k == 0) col[ch] = (double)v[e] * basis[0];
+                            else if (k < K) col[ch] += (double)v[e] * basis[k];
+                        }
                     }
                 }
-                double col[3];
 #pragma unroll
                 for (int ch = 0; ch < 3; ++ch) {
-                    double a = (double)shv[ch] * basis[0];
-#pragma unroll
-                    for (int k = 1; k < 16; ++k)
-                        if (k < K) a += (double)shv[k * 3 + ch] * basis[k];
-                    double c = a + 0.5;
+                    const double c = col[ch] + 0.5;
                     col[ch] = c < 0 ? 0.0 : c;
                 }
                 double flow[2];
@@ -869,13 +924,28 @@ using namespace rgs_dev;
 static inline int blocks(long long n, int t) { return (int)((n + t - 1) / t); }
 
 void preprocess(const float* params, const double* params64, int n, int sh_degree, const DevCamera& cam,
-                const SplatArrays& out, BinState* st, cudaStream_t s) {
+                const SplatArrays& out, BinState* st, cudaStream_t s, const SliceCacheView* cache) {
     if (n <= 0) return;
     ParamView P{params, n, params64};
-    if (params64)
-        k_preprocess<true><<<blocks(n, 128), 128, 0, s>>>(P, sh_degree, cam, out, st);
-    else
-        k_preprocess<false><<<blocks(n, 128), 128, 0, s>>>(P, sh_degree, cam, out, st);
+    const SliceCacheView C = cache ? *cache : SliceCacheView{nullptr, nullptr};
+    if (params64) {
+        if (cache) k_preprocess<true, true><<<blocks(n, 128), 128, 0, s>>>(P, sh_degree, cam, out, st, C);
+        else k_preprocess<true, false><<<blocks(n, 128), 128, 0, s>>>(P, sh_degree, cam, out, st, C);
+    } else {
+        if (cache) k_preprocess<false, true><<<blocks(n, 128), 128, 0, s>>>(P, sh_degree, cam, out, st, C);
+        else k_preprocess<false, false><<<blocks(n, 128), 128, 0, s>>>(P, sh_degree, cam, out, st, C);
+    }
+}
+
+size_t slice_cache_bytes(int n) { return (size_t)std::max(n, 1) * (kSliceCacheBlocks * sizeof(double2) + 1) + 64; }
+
+void slice_cache(const float* params, const double* params64, int n, void* buf, SliceCacheView* view, cudaStream_t s) {
+    view->blk = static_cast<double2*>(buf);
+    view->status = reinterpret_cast<int8_t*>(view->blk + kSliceCacheBlocks * (size_t)std::max(n, 1));
+    if (n <= 0) return;
+    ParamView P{params, n, params64};
+    if (params64) k_slice_cache<true><<<blocks(n, 128), 128, 0, s>>>(P, *view);
+    else k_slice_cache<false><<<blocks(n, 128), 128, 0, s>>>(P, *view);
 }
 
 void splats_from_host(const void* splats, int n, const DevCamera& cam, const SplatArrays& out, BinState* st,

@@ -199,6 +199,7 @@ struct rgs_ctx {
     DevBuf tile_grads;  // P x 9 doubles (deterministic backward: per (tile, position))
     DevBuf tmp_img;   // host-buffer staging
     DevBuf tmp_splats, tmp_scan, tmp_ids;
+    DevBuf slice_cache;  // t-independent slice of the scene of the current view batch (render_batch)
     BinState* host_stats = nullptr;  // pinned
     // profiling: CUDA events around every stage, on the launching stream
     int timing = 0;  // 1: all stages, serialised views; 2: live K5 timing (see rgs_ctx_set_profiling)
@@ -413,13 +414,15 @@ namespace {
 // resolved before returning (errors reported, overflow re-rendered).
 int run_forward(rgs_ctx* ctx, Frame& f, cudaStream_t s, Source src, const rgs_scene* scene, const void* dev_splats,
                 int n_splats, bool splats_monotone, const rgs_camera* cam, const double bg[3], unsigned flags,
-                float* image, bool flow_mode, bool sync, BinState* host_stats) {
+                float* image, bool flow_mode, bool sync, BinState* host_stats,
+                const SliceCacheView* slice_cache = nullptr, bool render_only = false) {
     const DevCamera dc = make_dev_camera(cam);
     const int n = src == kFromScene ? scene->n : n_splats;
     const size_t npix = (size_t)cam->width * cam->height;
     const int ntiles = dc.tiles_x * dc.tiles_y;
-    if (dc.tiles_x > 256 || dc.tiles_y > 256)
-        return set_err(ctx, RGS_E_INVALID, "image too large: at most 4096x4096 pixels (256x256 tiles)");
+    // tile keys hold ty and tx in 12 bits each (rgs_launch::tile_key_shift); pixel indices are 32-bit
+    if (dc.tiles_x > 4096 || dc.tiles_y > 4096 || npix >= ((size_t)1 << 31))
+        return set_err(ctx, RGS_E_INVALID, "image too large: at most 65536 x 65536 tiles' worth, < 2^31 pixels");
     f.n = n;
     f.width = cam->width;
     f.height = cam->height;
@@ -435,13 +438,19 @@ int run_forward(rgs_ctx* ctx, Frame& f, cudaStream_t s, Source src, const rgs_sc
                            f.bucket_count.as<uint32_t>(), f.bucket_cur.as<uint32_t>(), s);
     ctx->launches += 1;
     SplatArrays sa = f.arrays();
+    if (render_only && !flow_mode) {
+        // no records are kept: the flow / radius records (export, flow renders) and the view
+        // directions (backward) are not written
+        sa.flow_radius = nullptr;
+        sa.dir_dist = nullptr;
+    }
     BinState* st_dev = f.dstats();
 
     // K1: slice + project + SH (or host splats), depth keys, key range.
     {
         StageTimer t(ctx, kStPreprocess, s);
         if (src == kFromScene)
-            rgs_launch::preprocess(scene->params, scene->params64, n, scene->sh_degree, dc, sa, st_dev, s);
+            rgs_launch::preprocess(scene->params, scene->params64, n, scene->sh_degree, dc, sa, st_dev, s, slice_cache);
         else
             rgs_launch::splats_from_host(dev_splats, n, dc, sa, st_dev, s);
         ctx->launches += 1;
@@ -486,17 +495,21 @@ int run_forward(rgs_ctx* ctx, Frame& f, cudaStream_t s, Source src, const rgs_sc
         StageTimer t(ctx, kStTileFill, s);
         // scan_tmp is free again after the pair-offset scan: it holds the digit histograms
         rgs_launch::duplicate(f.sorted_ids.as<uint32_t>(), f.pair_off.as<uint32_t>(), f.sorted_tiles.as<uint32_t>(),
-                              sa.rect, st_dev, n, dc.tiles_x, f.keys_a.as<uint32_t>(), f.pair_vals_buf.as<uint32_t>(),
-                              f.scan_tmp.as<int>(), s);
+                              sa.rect, st_dev, n, dc.tiles_x, dc.tiles_y, f.keys_a.as<uint32_t>(),
+                              f.pair_vals_buf.as<uint32_t>(), f.scan_tmp.as<int>(), s);
         ctx->launches += 1;
     }
     {
         StageTimer t(ctx, kStTileSort, s);
-        rgs_launch::tile_radix_sort(f.keys_a.as<uint32_t>(), f.pair_vals_buf.as<uint32_t>(), f.keys_b.as<uint32_t>(),
-                                    f.vals_b.as<uint32_t>(), st_dev, f.pair_cap, dc.tiles_x, ntiles,
-                                    f.radix_counts.as<uint32_t>(), f.radix_offsets.as<uint32_t>(),
-                                    f.scan_tmp.as<int>(), f.ranges.as<uint2>(), s);
-        ctx->launches += 3;
+        const int in_b = rgs_launch::tile_radix_sort(
+            f.keys_a.as<uint32_t>(), f.pair_vals_buf.as<uint32_t>(), f.keys_b.as<uint32_t>(), f.vals_b.as<uint32_t>(),
+            st_dev, f.pair_cap, dc.tiles_x, dc.tiles_y, f.radix_counts.as<uint32_t>(), f.radix_offsets.as<uint32_t>(),
+            f.scan_tmp.as<int>(), f.ranges.as<uint2>(), s);
+        ctx->launches += in_b ? 5 : 3;
+        if (in_b) {  // three passes: the sorted pairs are in the B buffers (roles swapped for this frame)
+            std::swap(f.keys_a, f.keys_b);
+            std::swap(f.pair_vals_buf, f.vals_b);
+        }
     }
 
     // Blend.
@@ -543,7 +556,7 @@ int run_forward(rgs_ctx* ctx, Frame& f, cudaStream_t s, Source src, const rgs_sc
     if (st.overflow) {
         f.pair_cap = (long long)st.n_pairs * 5 / 4 + 1024;
         return run_forward(ctx, f, s, src, scene, dev_splats, n_splats, splats_monotone, cam, bg, flags, image,
-                           flow_mode, true, host_stats);
+                           flow_mode, true, host_stats, slice_cache, render_only);
     }
     f.n_valid = st.n_valid;
     f.n_pairs = st.n_pairs;
@@ -640,6 +653,7 @@ void rgs_ctx_destroy(rgs_ctx* c) {
     c->tmp_splats.release(c->stream);
     c->tmp_scan.release(c->stream);
     c->tmp_ids.release(c->stream);
+    c->slice_cache.release(c->stream);
     for (void* v : c->frame_pool) {
         PooledFrame* pf = static_cast<PooledFrame*>(v);
         pf->f.release(c->stream);
@@ -1097,6 +1111,17 @@ int render_batch(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* cams, int
     }
     c->err_index = -1;
     c->ensure_view_stats(n_views);
+    // A batch of several views of one scene shares the t-independent half of the slice (and the
+    // opacity sigmoid): computed once here, before the slot streams join.
+    SliceCacheView cache_view{nullptr, nullptr};
+    const SliceCacheView* cache = nullptr;
+    if (n_views >= 2 && scene->n > 0) {
+        c->slice_cache.ensure(rgs_launch::slice_cache_bytes(scene->n), c->stream);
+        StageTimer t(c, kStPreprocess, c->stream);
+        rgs_launch::slice_cache(scene->params, scene->params64, scene->n, c->slice_cache.p, &cache_view, c->stream);
+        c->launches += 1;
+        cache = &cache_view;
+    }
     CK(cudaEventRecord(c->join_ev, c->stream));
     for (int k = 0; k < rgs_ctx::kSlots; ++k) CK(cudaStreamWaitEvent(c->slot_stream[k], c->join_ev, 0));
     // Profiling mode serialises the views (one slot) so per-stage event times are the
@@ -1110,7 +1135,7 @@ int render_batch(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* cams, int
         cudaStream_t s = c->slot_stream[k];
         const int rc = run_forward(c, c->slot_frame[k], s, kFromScene, scene, nullptr, 0, true, &cams[v], bg,
                                    flags & ~RGS_FLAG_HOST_BUFFERS, image_for(user, v, s), false, false,
-                                   &c->view_stats[v]);
+                                   &c->view_stats[v], cache, true);
         if (rc) return rc;
         copy_out(v, k, s);
     }
@@ -1133,7 +1158,7 @@ int render_batch(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* cams, int
         f.pair_cap = std::max<long long>(f.pair_cap, (long long)c->view_stats[v].n_pairs * 5 / 4 + 1024);
         const int rc = run_forward(c, f, c->stream, kFromScene, scene, nullptr, 0, true, &cams[v], bg,
                                    flags & ~RGS_FLAG_HOST_BUFFERS, image_for(user, v, c->stream), false, true,
-                                   nullptr);
+                                   nullptr, cache, true);
         if (rc) return rc;
         copy_out(v, 0, c->stream);
         CK(cudaStreamSynchronize(c->stream));

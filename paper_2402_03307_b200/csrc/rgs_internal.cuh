@@ -90,6 +90,12 @@ struct SplatArrays {
     double4* dir_dist;              // (view direction, distance) of valid splats (scene renders)
 };
 
+// Slice cache of a view batch (k_fp64.cu k_slice_cache): 7 double2 blocks of N + N status bytes.
+struct SliceCacheView {
+    double2* blk;
+    int8_t* status;
+};
+
 // Error word: (index << 8) | code, minimum wins (lowest failing index).
 constexpr unsigned long long kNoError = ~0ull;
 
@@ -125,7 +131,9 @@ namespace rgs_launch {
 using namespace rgs_dev;
 
 void preprocess(const float* params, const double* params64, int n, int sh_degree, const DevCamera& cam, const SplatArrays& out,
-                BinState* st, cudaStream_t s);
+                BinState* st, cudaStream_t s, const SliceCacheView* cache = nullptr);
+size_t slice_cache_bytes(int n);
+void slice_cache(const float* params, const double* params64, int n, void* buf, SliceCacheView* view, cudaStream_t s);
 void splats_from_host(const void* splats, int n, const DevCamera& cam, const SplatArrays& out, BinState* st,
                       cudaStream_t s);
 // k_binning.cu
@@ -144,17 +152,19 @@ void depth_ranks(const uint8_t* valid, const unsigned long long* key, const uint
                  const int32_t* src, BinState* st, const uint32_t* bucket_count, const uint32_t* bucket_off,
                  uint32_t* bucket_cur, unsigned long long* ent_key, uint32_t* ent_id, uint32_t* sorted_ids,
                  uint32_t* sorted_tiles, uint32_t* big_list, void* big_scratch, cudaStream_t s);
+int tile_key_shift(int tiles_x, int tiles_y);
 void duplicate(const uint32_t* sorted_ids, const uint32_t* pair_off, const uint32_t* sorted_tiles,
-               const ushort4* rect, const BinState* st, int n, int tiles_x, uint32_t* keys, uint32_t* vals,
-               int* aux, cudaStream_t s);
+               const ushort4* rect, const BinState* st, int n, int tiles_x, int tiles_y, uint32_t* keys,
+               uint32_t* vals, int* aux, cudaStream_t s);
 void check_capacity(BinState* st, cudaStream_t s);
 void fold_status(const BinState* st, unsigned long long* word, unsigned long long overflow_word, cudaStream_t s);
 void frame_init(BinState* st, uint32_t pair_cap, uint32_t* bucket_count, uint32_t* bucket_cur, cudaStream_t s);
 int radix_blocks(long long n_pairs);
 size_t radix_count_entries(long long n_pairs);
-void tile_radix_sort(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32_t* vals_b, const BinState* st,
-                     long long n_pairs, int tiles_x, int n_tiles, uint32_t* status_a, uint32_t* status_b,
-                     int* aux, uint2* ranges, cudaStream_t s);
+// Returns 1 when the sorted pairs end in (keys_b, vals_b) (three passes), 0 for (keys_a, vals_a).
+int tile_radix_sort(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32_t* vals_b, const BinState* st,
+                    long long n_pairs, int tiles_x, int tiles_y, uint32_t* status_a, uint32_t* status_b, int* aux,
+                    uint2* ranges, cudaStream_t s);
 void blend_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges, const DevCamera& cam,
                 float3 bg, int flow_mode, float* image, double* final_T, uint32_t* n_contrib,
                 uint32_t* slow_list, int* slow_count, unsigned long long* counters, cudaStream_t s);

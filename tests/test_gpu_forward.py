@@ -134,13 +134,37 @@ def test_equal_depth_ties(ctx, orc, n):
 
 
 def test_max_image_4096(ctx, orc):
-    """The largest supported image (4096 x 4096 = 256 x 256 tiles, the two byte passes' range)
-    on a sparse scene: records, tile lists and image against the oracle."""
+    """The largest image of the two-byte-pass tile keys (4096 x 4096 = 256 x 256 tiles) on a
+    sparse scene: records, tile lists and image against the oracle."""
     store = scenes.synthetic_scene(4000, 4096, 4096, seed=12)
     cam = scenes.bench_camera(4096, 4096, 0.4, scenes.yaw_pose(3.0, (0.02, 0.0, 0.05)))
     err, ncd, rec, ref, out = _compare_forward(ctx, orc, store, cam, threads=16)
     assert rec.tiles_x == 256 and rec.tiles_y == 256
     assert err <= 1e-4 and ncd == 0
+
+
+@pytest.mark.parametrize("shape", [(7680, 4320), (4112, 200)])
+def test_wide_tile_keys_8k(ctx, orc, shape):
+    """Beyond 256 tiles per axis the tile keys widen to ty << 12 | tx and the tile sort takes
+    three byte passes (rasterizer.cpp:26-28 has no size limit): an 8K frame (480 x 270 tiles)
+    and a 257-tile-wide strip -- splat records, tile lists, n_contrib and the image against the
+    oracle, plus the backward on the 8K frame."""
+    w, h = shape
+    store = scenes.synthetic_scene(300_000 if w == 7680 else 20_000, w, h, seed=13)
+    cam = scenes.bench_camera(w, h, 0.45, scenes.yaw_pose(3.0, (0.02, 0.0, 0.05)))
+    err, ncd, rec, ref, out = _compare_forward(ctx, orc, store, cam, threads=32)
+    assert rec.tiles_x == (w + 15) // 16 and rec.tiles_x > 256
+    assert err <= 1e-4 and ncd == 0
+    print(f"{w}x{h}: {len(ref.splats)} splats, {len(ref.tile_ids)} pairs bit-exact, max image err {err:.2e}")
+    if w == 7680:
+        from parity import floored_rel_err
+
+        dl = np.random.default_rng(8).uniform(-1, 1, (h, w, 3))
+        g = rgs.render_backward(store, cam, out.records, dl, ctx=ctx)
+        gr, vn, vis = orc.render_backward(store, cam, ref, dl, threads=32)
+        assert np.array_equal(g.visible.astype(bool), vis.astype(bool))
+        e = floored_rel_err(g.as_matrix(), gr)
+        assert float((e <= 1e-3).mean()) >= 0.9999, e.max()
 
 
 def test_scene_params_tensor_view(ctx):

@@ -58,6 +58,16 @@ def main():
                 print(f"   worst: gaussian {i} param {c}: got {gg[i, c]:.6e} ref {gr[i, c]:.6e} colmax {col:.3e}")
                 print(f"   |dl| mean {np.abs(dln).mean():.3e} max {np.abs(dln).max():.3e}; slow px {rec.n_slow_pixels}")
         rec.close()
+        # the reference-KAT precision mode: FP64 forward blend (exact final_T) + FP64 replay
+        img64, rec64 = ctx.render_forward_device(sc, cam, retain=True, blend_fp64=True)
+        g, _, _ = ctx.render_backward_device(sc, cam, rec64, dl, deterministic=True)
+        torch.cuda.synchronize()
+        mean, ls, rot, op, sh = rgs.grads_from_soa(g.cpu().numpy(), n)
+        gg = np.concatenate([mean, ls, rot, op[:, None], sh.reshape(n, 48)], axis=1)
+        err = floored_rel_err(gg, gr)
+        print(f"view {v} FP64 forward + FP64 replay: {int((err > 1e-3).sum())} of {err.size} above 1e-3, "
+              f"max {err.max():.3e}", flush=True)
+        rec64.close()
 
 
 if __name__ == "__main__":
