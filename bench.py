@@ -275,10 +275,7 @@ def run_c5_leg(args, ctx, dev, dist, rank, world, flush):
     from paper_2402_03307_b200 import rgs, scenes, train
 
     truth = scenes.synthetic_scene(C5_N, C5_W, C5_H, seed=C5_SEED)
-    store = truth.copy()
-    r = np.random.default_rng(C5_SEED)
-    store.mean[:, :3] += r.normal(0, 0.01, (C5_N, 3)).astype(np.float32)
-    store.sh[:, :, 0] += r.normal(0, 0.1, (C5_N, 3)).astype(np.float32)
+    store = scenes.perturbed(truth, C5_SEED)
     cams = [scenes.bench_camera(C5_W, C5_H, (v + 0.5) / C5_VIEWS,
                                 scenes.yaw_pose(-4.0 + 8.0 * v / (C5_VIEWS - 1) + 0.7 * rank, (0.02, 0.0, 0.03)))
             for v in range(C5_VIEWS)]
@@ -288,8 +285,10 @@ def run_c5_leg(args, ctx, dev, dist, rank, world, flush):
     tsc.close()
     del truth
     scene = rgs.DeviceScene.from_store(ctx, store)
+    comm = native_comm(ctx, dist, world)
     tr = train.Trainer(ctx, scene, train.TrainConfig(batch=C5_VIEWS, total_steps=TRAIN_TOTAL_STEPS,
-                                                     max_gaussians=2_000_000), dist, start_step=TRAIN_START_STEP)
+                                                     max_gaussians=2_000_000), dist, start_step=TRAIN_START_STEP,
+                       comm=comm)
     tlist = [targets[v] for v in range(C5_VIEWS)]
     for _ in range(2):
         tr.step(cams, tlist)
@@ -319,7 +318,8 @@ def run_c5_leg(args, ctx, dev, dist, rank, world, flush):
            "config": {"workload": "C5: 1M 4D rotor Gaussians, SH deg 3, 1352x1014, 8 camera x timestamp views per rank "
                                   "and step, full training step, batch reduced by NCCL all-reduce",
                       "n_gaussians": C5_N, "width": C5_W, "height": C5_H, "views_per_rank": C5_VIEWS,
-                      "active_sh_degree": sh_timed, "first_timed_step": first_timed}}
+                      "active_sh_degree": sh_timed, "first_timed_step": first_timed,
+                      "allreduce": allreduce_kind(world)}}
     tr = None
     scene.close()
     del targets, tlist
@@ -345,12 +345,26 @@ def train_case():
     from paper_2402_03307_b200 import scenes
 
     truth = scenes.synthetic_scene(TRAIN_N, TRAIN_W, TRAIN_H, seed=TRAIN_SEED)
-    store = truth.copy()
-    r = np.random.default_rng(TRAIN_SEED)
-    store.mean[:, :3] += r.normal(0, 0.01, (TRAIN_N, 3)).astype(np.float32)
-    store.sh[:, :, 0] += r.normal(0, 0.1, (TRAIN_N, 3)).astype(np.float32)
-    store.opacity_logit += r.normal(0, 0.2, TRAIN_N).astype(np.float32)
+    store = scenes.perturbed(truth, TRAIN_SEED, opacity_sigma=0.2)
     return truth, store
+
+
+def native_comm(ctx, dist, world):
+    """RGS_NATIVE_ALLREDUCE=1 (N > 1): the batch all-reduce through the C ABI's fused NCCL group
+    (rgs_allreduce_grads) instead of three torch.distributed collectives."""
+    from paper_2402_03307_b200 import train
+
+    if dist is None or world < 2 or os.environ.get("RGS_NATIVE_ALLREDUCE") != "1":
+        return None
+    return train.NcclComm(ctx, dist)
+
+
+def allreduce_kind(world):
+    if world < 2:
+        return "none (one rank)"
+    if os.environ.get("RGS_NATIVE_ALLREDUCE") == "1":
+        return "rgs_allreduce_grads: one NCCL group (grads|vnorm, visible, image losses) on the context stream"
+    return "torch.distributed NCCL all-reduce x3 (grads|vnorm, visible, image losses)"
 
 
 def measured_peaks(ctx):
@@ -449,7 +463,8 @@ def run_train_leg(args, ctx, dev, dist, rank, world, flush):
     scene = rgs.DeviceScene.from_store(ctx, store)
     cfg = train.TrainConfig(batch=TRAIN_BATCH, total_steps=TRAIN_TOTAL_STEPS)
     # The timed steps are past the last SH unlock (trainer.cpp:135): active SH degree 3.
-    tr = train.Trainer(ctx, scene, cfg, dist, start_step=TRAIN_START_STEP)
+    comm = native_comm(ctx, dist, world)
+    tr = train.Trainer(ctx, scene, cfg, dist, start_step=TRAIN_START_STEP, comm=comm)
     stream = torch.cuda.current_stream(dev)
     B = TRAIN_BATCH
 
@@ -559,6 +574,7 @@ def run_train_leg(args, ctx, dev, dist, rank, world, flush):
         "views_per_step": B * world,
         "config": {"workload": TRAIN_WORKLOAD, "n_gaussians": TRAIN_N, "width": TRAIN_W, "height": TRAIN_H,
                    "batch_per_rank": B, "active_sh_degree": tr.scene.sh_degree, "first_timed_step": first_timed,
+                   "allreduce": allreduce_kind(world),
                    "parallelism": f"dp{world}: replicated scene, NCCL all-reduce of "
                                                          "[65 grads | viewspace norm | visible | image losses]",
                    "l2": "256 MiB flush before the timed steps; per-step working set > L2"},

@@ -261,6 +261,13 @@ int rgs_camera_validate(rgs_ctx* ctx, const rgs_camera* cam);
 int rgs_image_loss(rgs_ctx* ctx, const float* rendered, const float* target, int width, int height,
                    double w_l1, double w_ssim, double loss_scale, unsigned flags, float* dL_dimage,
                    double* losses);
+/* rgs_image_loss with the retained records of the forward that rendered `rendered` (NULL: as
+ * rgs_image_loss): the L1 gradient's sign (image.cpp:32-33, on the reference's double image) is
+ * re-decided in FP64 wherever the FP32 image is within 1e-5 of the target in some channel --
+ * those pixels are recomputed from the records by the FP64 blend. */
+int rgs_image_loss_ex(rgs_ctx* ctx, const rgs_records* records, const float* rendered, const float* target,
+                      int width, int height, double w_l1, double w_ssim, double loss_scale, unsigned flags,
+                      float* dL_dimage, double* losses);
 
 /* As rgs_image_loss on float64 images (the reference's Image type) with a float64 dL_dimage: the
  * gradient is bit-identical to the reference's l1_loss_backward / ssim_loss_with_grad mix. */
@@ -297,6 +304,24 @@ void rgs_optimizer_destroy(rgs_optimizer* opt);
  * moments stay as they were, as when the reference throws before adam_step. */
 int rgs_adam_step(rgs_ctx* ctx, rgs_scene* scene, rgs_optimizer* opt, const float* grads, const float* vnorm,
                   const int32_t* visible, const rgs_adam_config* cfg, int step, double* losses);
+/* ---------------------------------------------------------------- multi-GPU
+ * The batch reduction of evaluate_loss (trainer.cpp:33-53: grads and viewspace norms summed,
+ * visible OR-ed, gaussian.cpp:199-209) across the ranks of a replicated-scene training job, over
+ * NCCL.  NCCL is resolved at run time (the process's libnccl, else libnccl.so.2): no link
+ * dependency; rgs_nccl_available() says whether it was found.  A communicator is an ncclComm_t
+ * passed as void* -- made by the caller's own NCCL, or by rgs_nccl_comm_create from a 128-byte
+ * ncclUniqueId that rank 0 made with rgs_nccl_unique_id and shared out of band. */
+int rgs_nccl_available(void);
+int rgs_nccl_unique_id(unsigned char* id128);
+int rgs_nccl_comm_create(rgs_ctx* ctx, int nranks, int rank, const unsigned char* id128, void** comm);
+void rgs_nccl_comm_destroy(void* comm);
+/* One NCCL group (a single fused launch) on the context's stream: all-reduce(sum) in place of
+ * grads_vnorm (n_floats floats: the [65 N grads | N viewspace norms] block of the accumulated
+ * backward), visible (n_visible int32 counts: > 0 is the reference's OR) and losses (n_losses
+ * doubles: the image-loss sums).  Any pointer may be NULL when its count is 0. */
+int rgs_allreduce_grads(rgs_ctx* ctx, void* nccl_comm, float* grads_vnorm, size_t n_floats, int32_t* visible,
+                        size_t n_visible, double* losses, int n_losses);
+
 /* The context's deferred status word (RGS_FLAG_DEFER_CHECKS calls): rgs_ctx_status synchronises
  * and returns (then clears) the first error, with its index in rgs_ctx_error_index;
  * rgs_ctx_status_async queues a copy of the raw word ((index << 8) | code, ~0 when clean; an

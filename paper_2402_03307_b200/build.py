@@ -37,6 +37,7 @@ SOURCES = [
     ("k_misc.cu", []),
     ("k_train.cu", ["-fmad=false"]),
     ("rgs_capi.cu", []),
+    ("rgs_nccl.cu", []),
 ]
 
 
@@ -70,7 +71,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
             if verbose:
                 sys.stderr.write(r.stderr)
     if force or _stale(LIB, objs):
-        _run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart"])
+        _run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart", "-ldl"])
     return LIB
 
 

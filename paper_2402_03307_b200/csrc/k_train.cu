@@ -222,7 +222,11 @@ __global__ void __launch_bounds__(kSsimAThreads) k_image_grad(const TI* __restri
                 g_ssim = g[0] + 2 * xv * g[1] + yv * g[2];  // ssim.cpp:124-125
                 g_ssim *= a.ssim_scale;                     // -1 / count (ssim.cpp:131-134)
             }
-            const double g_l1 = d > 0 ? a.inv_n : (d < 0 ? -a.inv_n : 0);  // image.cpp:33
+            double g_l1 = d > 0 ? a.inv_n : (d < 0 ? -a.inv_n : 0);  // image.cpp:33
+            if (a.l1_sign) {  // a near-tie pixel: the sign of the FP64 rendered value
+                const int o = a.l1_sign[p];
+                if (o) g_l1 = (double)(o - 2) * a.inv_n;
+            }
             const double v = a.w_l1 * g_l1 + a.w_ssim * g_ssim;            // trainer.cpp:47-49
             dl[p] = a.accumulate ? (TO)((double)dl[p] + v) : (TO)v;
         }
@@ -1033,6 +1037,45 @@ void adam_step(bool f64, void* params, void* m1, void* m2, const float* grads, c
 }
 
 int adam_blocks(int n) { return nblk(n, 128); }
+
+}  // namespace rgs_launch
+namespace rgs_dev {
+__global__ void k_l1_ties(const float* __restrict__ img, const float* __restrict__ tgt, int npix, float eps,
+                          uint32_t* list, int* count) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= npix) return;
+    bool tie = false;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) tie |= fabsf(img[3 * (size_t)i + ch] - tgt[3 * (size_t)i + ch]) <= eps;
+    if (tie) list[atomicAdd(count, 1)] = (uint32_t)i;
+}
+__global__ void k_l1_sign_set(const uint32_t* __restrict__ list, const int* __restrict__ count,
+                              const double* __restrict__ img64, const float* __restrict__ tgt, int8_t* sign) {
+    const int n = *count;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 3 * n; e += gridDim.x * blockDim.x) {
+        const size_t p = 3 * (size_t)list[e / 3] + e % 3;
+        const double d = img64[p] - (double)tgt[p];  // image.cpp:32 on the reference's double image
+        sign[p] = (int8_t)(d > 0 ? 3 : (d < 0 ? 1 : 2));
+    }
+}
+__global__ void k_l1_sign_clear(const uint32_t* __restrict__ list, const int* __restrict__ count, int8_t* sign) {
+    const int n = *count;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 3 * n; e += gridDim.x * blockDim.x)
+        sign[3 * (size_t)list[e / 3] + e % 3] = 0;
+}
+}  // namespace rgs_dev
+namespace rgs_launch {
+void l1_ties(const float* img, const float* tgt, int npix, float eps, uint32_t* list, int* count, cudaStream_t s) {
+    if (npix > 0) k_l1_ties<<<nblk(npix, 256), 256, 0, s>>>(img, tgt, npix, eps, list, count);
+}
+void l1_sign_set(const uint32_t* list, const int* count, int max_items, const double* img64, const float* tgt,
+                 int8_t* sign, cudaStream_t s) {
+    k_l1_sign_set<<<std::max(1, std::min(nblk(3 * max_items, 256), 148 * 4)), 256, 0, s>>>(list, count, img64, tgt,
+                                                                                         sign);
+}
+void l1_sign_clear(const uint32_t* list, const int* count, int max_items, int8_t* sign, cudaStream_t s) {
+    k_l1_sign_clear<<<std::max(1, std::min(nblk(3 * max_items, 256), 148 * 4)), 256, 0, s>>>(list, count, sign);
+}
 
 void entropy(const double* op, int n, double* grad, double* parts, double* loss, cudaStream_t s) {
     const int nb = nblk(n, 256);

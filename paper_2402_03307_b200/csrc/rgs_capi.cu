@@ -1548,10 +1548,12 @@ void ensure_ssim_window(rgs_ctx* c) {
 // runs the consistency term on its main stream beside the image losses of its side streams.
 struct TrainScratch {
     DevBuf dfield, parts, cparts, speeds, dspeed, pts, lo, hi, knn;
+    DevBuf tie_list, tie_count, tie_img64, l1_sign;  // rgs_image_loss_ex (l1_sign kept all-zero between calls)
 };
 void train_scratch_free(void* p, cudaStream_t s) {
     TrainScratch* ts = static_cast<TrainScratch*>(p);
-    for (DevBuf* b : {&ts->dfield, &ts->parts, &ts->cparts, &ts->speeds, &ts->dspeed, &ts->pts, &ts->lo, &ts->hi, &ts->knn})
+    for (DevBuf* b : {&ts->dfield, &ts->parts, &ts->cparts, &ts->speeds, &ts->dspeed, &ts->pts, &ts->lo, &ts->hi, &ts->knn,
+                      &ts->tie_list, &ts->tie_count, &ts->tie_img64, &ts->l1_sign})
         b->release(s);
     delete ts;
 }
@@ -1571,7 +1573,16 @@ extern "C" {
 
 int rgs_image_loss(rgs_ctx* c, const float* rendered, const float* target, int width, int height, double w_l1,
                    double w_ssim, double loss_scale, unsigned flags, float* dL_dimage, double* losses) {
+    return rgs_image_loss_ex(c, nullptr, rendered, target, width, height, w_l1, w_ssim, loss_scale, flags, dL_dimage,
+                             losses);
+}
+
+int rgs_image_loss_ex(rgs_ctx* c, const rgs_records* rec, const float* rendered, const float* target, int width,
+                      int height, double w_l1, double w_ssim, double loss_scale, unsigned flags, float* dL_dimage,
+                      double* losses) {
     if (!rendered || !target || width <= 0 || height <= 0) return RGS_E_INVALID;
+    if (rec && (rec->ctx != c || !rec->retained || rec->fb->width != width || rec->fb->height != height))
+        return set_err(c, RGS_E_INVALID, "image_loss: records do not belong to this image");
     if ((width < kSsimWin || height < kSsimWin) && w_ssim != 0)
         return set_err(c, RGS_E_INVALID, "ssim: image smaller than the 11x11 window");
     return guarded(c, [&]() -> int {
@@ -1589,9 +1600,47 @@ int rgs_image_loss(rgs_ctx* c, const float* rendered, const float* target, int w
         a.ssim_scale = nv ? -1 / (3.0 * (double)nv) : 0.0;
         a.accumulate = (flags & RGS_FLAG_ACCUMULATE_GRAD) ? 1 : 0;
         StageTimer t(c, kStImageLoss, s);
+        // L1 near ties (image.cpp:32-33 on the reference's double image): pixels whose FP32 value
+        // is within kL1Tie of the target in some channel are recomputed in FP64 from the view's
+        // records and their L1 sign taken from that value.  kL1Tie is 10x the largest FP32 image
+        // error measured at C1 / C2 / C4 (1.03e-6; the north-star bound is 1e-4).
+        constexpr float kL1Tie = 1e-5f;
+        const size_t npix = (size_t)width * height;
+        const bool ties = rec && dL_dimage && w_l1 != 0;
+        if (ties) {
+            const Frame& f = *rec->fb;
+            ts.tie_list.ensure(4 * npix, s);
+            ts.tie_count.ensure(16, s);
+            ts.tie_img64.ensure(sizeof(double) * 3 * npix, s);
+            if (ts.l1_sign.bytes < 3 * npix) {
+                ts.l1_sign.ensure(3 * npix, s);
+                CK(cudaMemsetAsync(ts.l1_sign.p, 0, ts.l1_sign.bytes, s));
+            }
+            CK(cudaMemsetAsync(ts.tie_count.p, 0, sizeof(int), s));
+            rgs_launch::l1_ties(rendered, target, (int)npix, kL1Tie, ts.tie_list.as<uint32_t>(), ts.tie_count.as<int>(),
+                                s);
+            DevCamera dc{};
+            dc.width = f.width;
+            dc.height = f.height;
+            dc.tiles_x = f.tiles_x;
+            dc.tiles_y = f.tiles_y;
+            rgs_launch::blend_fp64_pixels(f.arrays(), f.pair_vals(), f.ranges.as<uint2>(), dc,
+                                          make_double3(f.bg[0], f.bg[1], f.bg[2]), 0, nullptr,
+                                          ts.tie_img64.as<double>(), nullptr, nullptr, ts.tie_list.as<uint32_t>(),
+                                          ts.tie_count.as<int>(), (int)npix, s);
+            rgs_launch::l1_sign_set(ts.tie_list.as<uint32_t>(), ts.tie_count.as<int>(), (int)npix,
+                                    ts.tie_img64.as<double>(), target, ts.l1_sign.as<int8_t>(), s);
+            a.l1_sign = ts.l1_sign.as<int8_t>();
+            c->launches += 3;
+        }
         rgs_launch::image_loss(rendered, target, width, height, a, dL_dimage, ts.dfield.as<double>(),
                                ts.parts.as<double>(), losses, loss_scale, (flags & RGS_FLAG_ACCUMULATE) ? 1 : 0, s);
         c->launches += losses ? 3 : 2;
+        if (ties) {
+            rgs_launch::l1_sign_clear(ts.tie_list.as<uint32_t>(), ts.tie_count.as<int>(), (int)npix,
+                                      ts.l1_sign.as<int8_t>(), s);
+            c->launches += 1;
+        }
         CK(cudaGetLastError());
         return RGS_OK;
     });
@@ -2300,3 +2349,8 @@ int rgs_densify_and_prune(rgs_ctx* c, rgs_scene* scene, rgs_optimizer* o, const 
 }
 
 }  // extern "C"
+
+// For the other host translation units of the library (rgs_nccl.cu).
+namespace rgs_host {
+int set_ctx_error(rgs_ctx* c, int code, const char* msg) { return set_err(c, code, msg ? msg : ""); }
+}  // namespace rgs_host

@@ -21,6 +21,9 @@ struct ImageGradArgs {
     double inv_n;       // 1 / (3 W H)               (image.cpp:31)
     double ssim_scale;  // -1 / (3 (W-10) (H-10))    (ssim.cpp:131-134)
     int accumulate;     // dL/dimage += instead of =
+    // L1 signs decided in FP64 (rgs_image_loss_ex): per pixel and channel 0 = none, else
+    // sign(rendered64 - target) + 2; NULL: every sign from the FP32 image
+    const int8_t* l1_sign = nullptr;
 };
 
 struct ImageLossGrid {
@@ -50,6 +53,12 @@ void adam_step(bool f64, void* params, void* m1, void* m2, const float* grads, c
                unsigned long long* err, double* part_entropy, double* losses_entropy, int accumulate,
                const unsigned long long* skip, cudaStream_t s);
 int adam_blocks(int n);
+// L1 near-tie re-decision (rgs_image_loss_ex): pixels with |rendered - target| <= eps in some
+// channel -> list; after their FP64 recompute (blend_fp64_pixels into img64), the FP64 signs.
+void l1_ties(const float* img, const float* tgt, int npix, float eps, uint32_t* list, int* count, cudaStream_t s);
+void l1_sign_set(const uint32_t* list, const int* count, int max_items, const double* img64, const float* tgt,
+                 int8_t* sign, cudaStream_t s);
+void l1_sign_clear(const uint32_t* list, const int* count, int max_items, int8_t* sign, cudaStream_t s);
 void image_loss_f64(const double* img, const double* tgt, int W, int H, const ImageGradArgs& a, double* dl,
                     double* dfield, double* parts, double* losses, double loss_scale, int accumulate, cudaStream_t s);
 void entropy(const double* op, int n, double* grad, double* parts, double* loss, cudaStream_t s);

@@ -9,8 +9,13 @@
 //   render_backward    rasterizer.hpp:93-95   -> rgs_render_backward
 //   render_flow        rasterizer.hpp:99      -> rgs_render_flow
 // Behaviour differences: `threads` is ignored; ProjectCache / RenderRecords::caches are
-// not filled (the device backward recomputes what it needs; render_backward re-renders
-// the view from the store to rebuild its device records); rotor errors always throw.
+// not filled (the device backward recomputes what it needs); rotor errors always throw.
+// Device-side caching: the device copy of a store is kept and reused while
+// the store's contents (a 64-bit hash of every parameter array), size and SH degree are
+// unchanged, and the device records of the last render_forward stay alive so that the
+// render_backward of the same view (evaluate_loss, trainer.cpp:35-52) uses them instead of
+// re-rendering; a backward whose records were not the last forward's (or whose pixel records
+// were changed) re-renders the view from the store, as before.
 // Environment: RGS_DEVICE selects the CUDA device (default 0).  RGS_KAT_MODE=1 selects the
 // reference-KAT precision mode: FP64 blending with double images, and the deterministic
 // FP64 backward (reference summation order, bitwise reproducible).
@@ -59,6 +64,7 @@ void check(int rc) {
 
 rgs_camera to_c(const Camera& cam) {
     rgs_camera c;
+    std::memset(&c, 0, sizeof c);  // (compared bytewise by the records reuse)
     c.width = cam.width;
     c.height = cam.height;
     c.fx = cam.fx;
@@ -100,32 +106,116 @@ rgs_splat to_c(const Splat2D& s) {
     return o;
 }
 
-// GaussianStore (gaussian.hpp:79-103) -> a device scene.
-struct DeviceScene {
-    rgs_scene* s = nullptr;
-    explicit DeviceScene(const GaussianStore& store) {
-        const int n = store.size();
-        // FP64 storage: the store's double values reach the kernels unrounded.
-        check(rgs_scene_create_ex(context(), n, store.active_sh_degree, RGS_SCENE_F64, &s));
-        std::vector<double> mean(4 * (size_t)n), ls(4 * (size_t)n), rot(8 * (size_t)n), op(n), sh(48 * (size_t)n);
-        for (int i = 0; i < n; ++i) {
-            for (int a = 0; a < 4; ++a) mean[4 * i + a] = store.mean[i][a];
-            for (int a = 0; a < 4; ++a) ls[4 * i + a] = store.log_scales[i][a];
-            const Vec8 c = store.rotor[i].coeffs();
-            for (int a = 0; a < 8; ++a) rot[8 * i + a] = c[a];
-            op[i] = store.opacity_logit[i];
-            for (int ch = 0; ch < 3; ++ch)
-                for (int k = 0; k < 16; ++k) sh[48 * i + ch * 16 + k] = store.sh[i](ch, k);
+// 64-bit content hash (multiply-rotate over 8-byte words, four independent lanes).
+uint64_t hash_words(const void* p, size_t bytes, uint64_t h) {
+    const unsigned char* b = static_cast<const unsigned char*>(p);
+    const size_t nw = bytes / 8;
+    uint64_t l[4] = {h ^ 0x9e3779b97f4a7c15ull, h + 0xc2b2ae3d27d4eb4full, h * 31 + 1, ~h};
+    size_t i = 0;
+    for (; i + 4 <= nw; i += 4) {
+        for (int k = 0; k < 4; ++k) {
+            uint64_t w;
+            std::memcpy(&w, b + 8 * (i + k), 8);
+            l[k] = (l[k] ^ w) * 0x100000001b3ull;
+            l[k] = (l[k] << 29) | (l[k] >> 35);
         }
-        check(rgs_scene_upload_f64(context(), s, mean.data(), ls.data(), rot.data(), op.data(), sh.data(), nullptr));
     }
-    ~DeviceScene() { rgs_scene_destroy(s); }
+    for (; i < nw; ++i) {
+        uint64_t w;
+        std::memcpy(&w, b + 8 * i, 8);
+        l[0] = ((l[0] ^ w) * 0x100000001b3ull);
+        l[0] = (l[0] << 29) | (l[0] >> 35);
+    }
+    for (size_t j = 8 * nw; j < bytes; ++j) l[1] = (l[1] ^ b[j]) * 0x100000001b3ull;
+    return (l[0] * 3 + l[1]) * 0x9e3779b97f4a7c15ull ^ (l[2] * 5 + l[3]);
+}
+
+template <typename V>
+uint64_t hash_vec(const V& v, uint64_t h) {
+    return hash_words(v.data(), v.size() * sizeof(typename V::value_type), h);
+}
+
+// The parameters a render reads (gaussian.hpp:79-85), hashed per array.
+uint64_t store_hash(const GaussianStore& st) {
+    uint64_t h = 0x5bd1e995u ^ (uint64_t)st.size() ^ ((uint64_t)st.active_sh_degree << 40);
+    h = hash_vec(st.mean, h);
+    h = hash_vec(st.log_scales, h);
+    h = hash_vec(st.rotor, h);
+    h = hash_vec(st.opacity_logit, h);
+    h = hash_vec(st.sh, h);
+    return h;
+}
+
+// GaussianStore (gaussian.hpp:79-103) -> the cached device scene (FP64 storage: the store's
+// double values reach the kernels unrounded).  Re-uploaded only when the contents change.
+struct SceneCache {
+    rgs_scene* s = nullptr;
+    int n = -1, sh = -1;
+    uint64_t hash = 0;
+    long long uploads = 0, hits = 0;
 };
+SceneCache& scene_cache() {
+    static SceneCache c;
+    return c;
+}
+
+rgs_scene* device_scene(const GaussianStore& store, uint64_t* key = nullptr) {
+    SceneCache& c = scene_cache();
+    const int n = store.size();
+    const uint64_t h = store_hash(store);
+    if (key) *key = h;
+    if (c.s && c.n == n && c.sh == store.active_sh_degree && c.hash == h) {
+        ++c.hits;
+        return c.s;
+    }
+    if (c.s && c.n != n) {
+        rgs_scene_destroy(c.s);
+        c.s = nullptr;
+    }
+    if (!c.s) check(rgs_scene_create_ex(context(), n, store.active_sh_degree, RGS_SCENE_F64, &c.s));
+    rgs_scene_set_sh_degree(c.s, store.active_sh_degree);
+    std::vector<double> mean(4 * (size_t)n), ls(4 * (size_t)n), rot(8 * (size_t)n), op(n), sh(48 * (size_t)n);
+    for (int i = 0; i < n; ++i) {
+        for (int a = 0; a < 4; ++a) mean[4 * i + a] = store.mean[i][a];
+        for (int a = 0; a < 4; ++a) ls[4 * i + a] = store.log_scales[i][a];
+        const Vec8 cf = store.rotor[i].coeffs();
+        for (int a = 0; a < 8; ++a) rot[8 * i + a] = cf[a];
+        op[i] = store.opacity_logit[i];
+        for (int ch = 0; ch < 3; ++ch)
+            for (int k = 0; k < 16; ++k) sh[48 * i + ch * 16 + k] = store.sh[i](ch, k);
+    }
+    c.n = -1;  // invalid until the upload succeeded
+    check(rgs_scene_upload_f64(context(), c.s, mean.data(), ls.data(), rot.data(), op.data(), sh.data(), nullptr));
+    c.n = n;
+    c.sh = store.active_sh_degree;
+    c.hash = h;
+    ++c.uploads;
+    return c.s;
+}
 
 struct RecordsHandle {
     rgs_records* r = nullptr;
     ~RecordsHandle() { rgs_records_destroy(r); }
 };
+
+// The device records of the last render_forward, for its render_backward.
+struct LastForward {
+    rgs_records* r = nullptr;
+    uint64_t scene_key = 0, nc_hash = 0;
+    rgs_camera cam{};
+    double bg[3] = {0, 0, 0};
+    const int* nc_data = nullptr;
+    size_t nc_size = 0;
+    long long reused = 0;
+    void reset(rgs_records* nr) {
+        if (r) rgs_records_destroy(r);
+        r = nr;
+    }
+};
+LastForward& last_forward() {
+    static LastForward lf;
+    return lf;
+}
 
 unsigned image_flags() { return RGS_FLAG_HOST_BUFFERS | (kat_mode() ? RGS_FLAG_IMAGE_F64 : 0u); }
 
@@ -201,36 +291,61 @@ void rasterize_forward(const std::vector<Splat2D>& splats, const Camera& cam, co
 
 RenderOutput render_forward(const GaussianStore& store, const Camera& cam, const RenderOptions& opts) {
     cam.validate();
-    DeviceScene scene(store);
+    uint64_t key = 0;
+    rgs_scene* scene = device_scene(store, &key);
     const rgs_camera c = to_c(cam);
     const double bg[3] = {opts.background[0], opts.background[1], opts.background[2]};
     RenderOutput out;
     RecordsHandle h;
     render_image(&out.image, cam.width, cam.height, 3, [&](float* img) {
-        check(rgs_render_forward(context(), scene.s, &c, bg, image_flags() | RGS_FLAG_RETAIN_RECORDS, img, &h.r));
+        check(rgs_render_forward(context(), scene, &c, bg, image_flags() | RGS_FLAG_RETAIN_RECORDS, img, &h.r));
     });
     export_records(h, &out.records, opts.background);
     out.records.retained = opts.retain_records;
+    if (opts.retain_records) {  // kept for the render_backward of this view
+        LastForward& lf = last_forward();
+        lf.reset(h.r);
+        h.r = nullptr;
+        lf.scene_key = key;
+        lf.cam = c;
+        for (int k = 0; k < 3; ++k) lf.bg[k] = bg[k];
+        lf.nc_data = out.records.n_contrib.data();
+        lf.nc_size = out.records.n_contrib.size();
+        lf.nc_hash = hash_vec(out.records.n_contrib, 7);
+    }
     return out;
 }
 
 StoreGrads render_backward(const GaussianStore& store, const Camera& cam, const RenderRecords& rec,
                            const Image& dL_dimage, int /*threads*/) {
     if (!rec.retained) throw MissingRecordsError();
-    DeviceScene scene(store);
+    uint64_t key = 0;
+    rgs_scene* scene = device_scene(store, &key);
     const rgs_camera c = to_c(cam);
     const double bg[3] = {rec.background[0], rec.background[1], rec.background[2]};
-    // Rebuild the device records of this view (deterministic: same decisions as `rec`).
+    // The device records of this view: the last forward's when `rec` came from it (same store
+    // contents, camera, background, and the very pixel records it returned), else rebuilt by
+    // re-rendering (deterministic: the same decisions as `rec`).
     RecordsHandle h;
-    std::vector<double> img64((size_t)cam.width * cam.height * 3);
-    check(rgs_render_forward(context(), scene.s, &c, bg, image_flags() | RGS_FLAG_RETAIN_RECORDS,
-                             reinterpret_cast<float*>(img64.data()), &h.r));
+    rgs_records* dev_rec = nullptr;
+    LastForward& lf = last_forward();
+    if (lf.r && lf.scene_key == key && std::memcmp(&lf.cam, &c, sizeof c) == 0 && lf.bg[0] == bg[0] &&
+        lf.bg[1] == bg[1] && lf.bg[2] == bg[2] && lf.nc_data == rec.n_contrib.data() &&
+        lf.nc_size == rec.n_contrib.size() && lf.nc_hash == hash_vec(rec.n_contrib, 7)) {
+        dev_rec = lf.r;
+        ++lf.reused;
+    } else {
+        std::vector<double> img64((size_t)cam.width * cam.height * 3);
+        check(rgs_render_forward(context(), scene, &c, bg, image_flags() | RGS_FLAG_RETAIN_RECORDS,
+                                 reinterpret_cast<float*>(img64.data()), &h.r));
+        dev_rec = h.r;
+    }
     const int n = store.size();
     std::vector<float> dl(dL_dimage.data.begin(), dL_dimage.data.end());
     std::vector<float> g(65 * (size_t)std::max(n, 1)), vn(std::max(n, 1));
     std::vector<int32_t> vis(std::max(n, 1));
     const unsigned flags = RGS_FLAG_HOST_BUFFERS | (kat_mode() ? RGS_FLAG_DETERMINISTIC : 0u);
-    check(rgs_render_backward(context(), scene.s, &c, h.r, dl.data(), flags, g.data(), vn.data(), vis.data()));
+    check(rgs_render_backward(context(), scene, &c, dev_rec, dl.data(), flags, g.data(), vn.data(), vis.data()));
     // device SoA (rgs_scene_params layout) -> per-Gaussian gradients
     StoreGrads out;
     out.resize(n);
@@ -253,13 +368,21 @@ StoreGrads render_backward(const GaussianStore& store, const Camera& cam, const 
 
 Image render_flow(const GaussianStore& store, const Camera& cam, int /*threads*/) {
     cam.validate();
-    DeviceScene scene(store);
+    rgs_scene* scene = device_scene(store);
     const rgs_camera c = to_c(cam);
     Image flow;
     render_image(&flow, cam.width, cam.height, 2, [&](float* img) {
-        check(rgs_render_flow(context(), scene.s, &c, image_flags() | (kat_mode() ? RGS_FLAG_BLEND_FP64 : 0u), img));
+        check(rgs_render_flow(context(), scene, &c, image_flags() | (kat_mode() ? RGS_FLAG_BLEND_FP64 : 0u), img));
     });
     return flow;
 }
 
 }  // namespace rgs
+
+// Adapter statistics (tests / bench of the drop-in path): device-scene uploads, cache hits and
+// backward passes that reused the forward's device records.
+extern "C" void rgs_adapter_stats(long long* uploads, long long* hits, long long* records_reused) {
+    if (uploads) *uploads = rgs::scene_cache().uploads;
+    if (hits) *hits = rgs::scene_cache().hits;
+    if (records_reused) *records_reused = rgs::last_forward().reused;
+}

@@ -168,6 +168,9 @@ EXPORTS = [
     "rgs_knn_query", "rgs_consistency_loss", "rgs_image_loss_f64", "rgs_entropy_loss", "rgs_accumulate_stats",
     "rgs_rng_get_state", "rgs_rng_set_state", "rgs_malloc", "rgs_free", "rgs_memcpy",
     "rgs_accumulate_stats_f64", "rgs_ctx_profile_slow_reasons", "rgs_measure_fp64_tflops",
+    # multi-GPU (train.NcclComm)
+    "rgs_nccl_available", "rgs_nccl_unique_id", "rgs_nccl_comm_create", "rgs_nccl_comm_destroy",
+    "rgs_allreduce_grads", "rgs_image_loss_ex",
 ]
 
 
@@ -220,8 +223,14 @@ def load_library(path: str = LIB_PATH):
         "rgs_ctx_profile_read": (i, [p, p, p, p]),
         "rgs_measure_fp32_tflops": (i, [p, p]),
         "rgs_measure_fp64_tflops": (i, [p, p]),
+        "rgs_nccl_available": (i, []),
+        "rgs_nccl_unique_id": (i, [p]),
+        "rgs_nccl_comm_create": (i, [p, i, i, p, p]),
+        "rgs_nccl_comm_destroy": (None, [p]),
+        "rgs_allreduce_grads": (i, [p, p, p, ctypes.c_size_t, p, ctypes.c_size_t, p, i]),
         "rgs_project_sliced": (i, [p, p, p, p, i, d, p, p]),
         "rgs_image_loss": (i, [p, p, p, i, i, d, d, d, ctypes.c_uint, p, p]),
+        "rgs_image_loss_ex": (i, [p, p, p, p, i, i, d, d, d, ctypes.c_uint, p, p]),
         "rgs_optimizer_create": (i, [p, p, p]),
         "rgs_optimizer_destroy": (None, [p]),
         "rgs_adam_step": (i, [p, p, p, p, p, p, p, i, p]),

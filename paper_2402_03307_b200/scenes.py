@@ -205,6 +205,23 @@ def random_scene(n: int, sh_degree: int = 1, seed: int = 0, f32: bool = True) ->
 
 
 # ----------------------------------------------------------------------------- cameras
+def perturbed(store: GaussianStore, seed: int, mean_sigma: float = 0.01, sh_dc_sigma: float = 0.1,
+              opacity_sigma: float = 0.0) -> GaussianStore:
+    """A training start from a ground-truth scene: Gaussian noise on the spatial means, the SH DC
+    coefficients and (optionally) the opacity logits, every parameter rounded to float32 (so the
+    FP32 device scene and the double host store the CPU reference reads hold the same values)."""
+    out = store.copy()
+    r = np.random.default_rng(seed)
+    n = out.size()
+    out.mean[:, :3] += r.normal(0, mean_sigma, (n, 3))
+    out.sh[:, :, 0] += r.normal(0, sh_dc_sigma, (n, 3))
+    if opacity_sigma:
+        out.opacity_logit += r.normal(0, opacity_sigma, n)
+    for a in (out.mean, out.log_scales, out.rotor, out.opacity_logit, out.sh):
+        a[...] = a.astype(np.float32)
+    return out
+
+
 def yaw_pose(yaw_deg: float = 0.0, t=(0.0, 0.0, 0.0)) -> np.ndarray:
     a = np.deg2rad(yaw_deg)
     w = np.eye(4)

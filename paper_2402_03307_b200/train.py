@@ -268,16 +268,19 @@ def densify_and_prune(ctx: Context, scene: DeviceScene, opt: "DeviceOptimizer", 
 
 
 def image_loss(ctx: Context, rendered, target, w_l1: float = 1.0, w_ssim: float = 0.0, dL_dimage=None,
-               losses=None, loss_scale: float = 1.0, accumulate: bool = False, accumulate_grad: bool = False):
+               losses=None, loss_scale: float = 1.0, accumulate: bool = False, accumulate_grad: bool = False,
+               records=None):
     """L1 + SSIM losses and dL/dimage on device tensors (rgs_image_loss).  ``accumulate``: losses
-    +=; ``accumulate_grad``: dL_dimage +=."""
+    +=; ``accumulate_grad``: dL_dimage +=.  ``records``: the retained RenderRecords of the forward
+    that rendered ``rendered`` -- L1 signs at near ties are then decided on the FP64 pixel value
+    (rgs_image_loss_ex), as the reference's double image decides them."""
     h, w = int(rendered.shape[0]), int(rendered.shape[1])
     ctx.sync_stream()
     flags = (rgs.FLAG_ACCUMULATE if accumulate else 0) | (rgs.FLAG_ACCUMULATE_GRAD if accumulate_grad else 0)
-    ctx.check(ctx.L.rgs_image_loss(ctx.h, _vp(_ptr(rendered)), _vp(_ptr(target)), w, h, float(w_l1), float(w_ssim),
-                                   float(loss_scale), flags,
-                                   _vp(_ptr(dL_dimage)) if dL_dimage is not None else None,
-                                   _vp(_ptr(losses)) if losses is not None else None))
+    ctx.check(ctx.L.rgs_image_loss_ex(ctx.h, records.h if records is not None else None, _vp(_ptr(rendered)),
+                                      _vp(_ptr(target)), w, h, float(w_l1), float(w_ssim), float(loss_scale), flags,
+                                      _vp(_ptr(dL_dimage)) if dL_dimage is not None else None,
+                                      _vp(_ptr(losses)) if losses is not None else None))
     ctx.fence()
 
 
@@ -314,10 +317,63 @@ def consistency(ctx: Context, scene: DeviceScene, nbrs, lam: float, grads=None, 
 
 
 # ----------------------------------------------------------------------------- multi-GPU plumbing
-def allreduce_step_buffers(gbuf, visible, losses_img, dist=None):
-    """The batch reduction across ranks: sum of [65 grads | viewspace_norm] (one NCCL call),
-    of the visible counts and of the three image-loss slots.  A no-op on one process.
-    Works on any backend (gloo on CPU in the tests, NCCL over NVLink on the GPUs)."""
+class NcclComm:
+    """A native NCCL communicator of the C ABI (rgs_nccl_comm_create) for the fused gradient
+    all-reduce (rgs_allreduce_grads: one NCCL group, a single launch, on the context's stream).
+    Rank 0 makes the ncclUniqueId; it reaches the other ranks through ``dist`` (any backend)."""
+
+    def __init__(self, ctx: Context, dist):
+        L = ctx.L
+        if not L.rgs_nccl_available():
+            raise rgs.RgsUnavailableError("NCCL not found (rgs_nccl_available() == 0)")
+        world, rank = dist.get_world_size(), dist.get_rank()
+        uid = (ctypes.c_ubyte * 128)()
+        if rank == 0:
+            ctx.check(L.rgs_nccl_unique_id(uid))
+        box = [bytes(uid)]
+        dist.broadcast_object_list(box, src=0)
+        uid = (ctypes.c_ubyte * 128).from_buffer_copy(box[0])
+        h = _vp()
+        ctx.check(L.rgs_nccl_comm_create(ctx.h, world, rank, uid, ctypes.byref(h)))
+        self.ctx, self.h, self.world, self.rank = ctx, h, world, rank
+
+    @staticmethod
+    def single(ctx: Context) -> "NcclComm":
+        """A one-rank communicator (the all-reduce is the identity): tests of the native path."""
+        self = NcclComm.__new__(NcclComm)
+        uid = (ctypes.c_ubyte * 128)()
+        ctx.check(ctx.L.rgs_nccl_unique_id(uid))
+        h = _vp()
+        ctx.check(ctx.L.rgs_nccl_comm_create(ctx.h, 1, 0, uid, ctypes.byref(h)))
+        self.ctx, self.h, self.world, self.rank = ctx, h, 1, 0
+        return self
+
+    def allreduce_step(self, gbuf, visible, losses_img) -> None:
+        ctx = self.ctx
+        ctx.sync_stream()
+        ctx.check(ctx.L.rgs_allreduce_grads(ctx.h, self.h, _vp(_ptr(gbuf)), gbuf.numel(), _vp(_ptr(visible)),
+                                            visible.numel(), _vp(_ptr(losses_img)), losses_img.numel()))
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.L.rgs_nccl_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def allreduce_step_buffers(gbuf, visible, losses_img, dist=None, comm: Optional[NcclComm] = None):
+    """The batch reduction across ranks: sum of the [65 grads | viewspace_norm] block, of the
+    visible counts and of the three image-loss slots.  A no-op on one process.  With ``comm``
+    (NcclComm): one fused NCCL group through the C ABI; otherwise three torch.distributed
+    collectives on any backend (gloo on CPU in the tests, NCCL over NVLink on the GPUs)."""
+    if comm is not None:
+        comm.allreduce_step(gbuf, visible, losses_img)
+        return
     if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
         return
     dist.all_reduce(gbuf)
@@ -401,9 +457,12 @@ class Trainer:
     batch (each rank passes its own views; the batch size is views_per_rank * world)."""
 
     def __init__(self, ctx: Context, scene: DeviceScene, config: TrainConfig, dist=None,
-                 scene_extent: Optional[float] = None, seed: int = 0, start_step: int = 0):
+                 scene_extent: Optional[float] = None, seed: int = 0, start_step: int = 0,
+                 comm: Optional[NcclComm] = None):
         """``start_step``: the number of steps already taken (resuming a run): the next step is
-        start_step + 1, with its SH degree, learning-rate schedule and intervals (trainer.cpp:115-150)."""
+        start_step + 1, with its SH degree, learning-rate schedule and intervals (trainer.cpp:115-150).
+        ``comm``: a native NcclComm for the batch all-reduce (else torch.distributed's)."""
+        self.comm = comm
         config.validate()
         if start_step < 0:
             raise ValueError("Trainer: start_step must be >= 0")
@@ -522,7 +581,7 @@ class Trainer:
                     if loss_done is not None:
                         side.wait_event(loss_done)
                     image_loss(ctx, img, tgt, wl1, wss, dl if want_grads else None, self.losses, loss_scale=inv_b,
-                               accumulate=True)
+                               accumulate=True, records=rec if want_grads else None)
                     loss_done = side.record_event()
                 main.wait_stream(side)
                 ctx.sync_stream()
@@ -530,7 +589,7 @@ class Trainer:
                 img, rec = ctx.render_forward_device(scene, cam, self.cfg.background, retain=want_grads, image=img,
                                                      defer_checks=defer)
                 image_loss(ctx, img, tgt, wl1, wss, dl if want_grads else None, self.losses, loss_scale=inv_b,
-                           accumulate=True)
+                           accumulate=True, records=rec if want_grads else None)
             if want_grads:
                 ctx.render_backward_device(scene, cam, rec, dl, self.grads, self.vnorm, self.visible, accumulate=True)
             if overlap:
@@ -538,9 +597,9 @@ class Trainer:
             recs.append(rec)
         for rec in recs:  # returned to the context's frame pool (stream-ordered, no host sync)
             rec.close()
-        if self.world > 1:
+        if self.world > 1 or self.comm is not None:
             ctx.fence()
-            allreduce_step_buffers(self.gbuf, self.visible, self.losses[:3], self.dist)
+            allreduce_step_buffers(self.gbuf, self.visible, self.losses[:3], self.dist, self.comm)
             if not ctx._torch_stream:
                 torch.cuda.current_stream(ctx.device).synchronize()
         if not early_consistency:

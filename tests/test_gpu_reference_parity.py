@@ -112,10 +112,7 @@ def test_c5_evaluate_loss_vs_reference_build(ctx, ref):
     T = O.train_ops("ref")
     n, w, h, views = 1_000_000, 1352, 1014, 8
     truth = scenes.synthetic_scene(n, w, h, seed=5)
-    store = truth.copy()
-    r = np.random.default_rng(5)
-    store.mean[:, :3] += r.normal(0, 0.01, (n, 3)).astype(np.float32)
-    store.sh[:, :, 0] += r.normal(0, 0.1, (n, 3)).astype(np.float32)
+    store = scenes.perturbed(truth, 5)
     cams = [scenes.bench_camera(w, h, (v + 0.5) / views,
                                 scenes.yaw_pose(-4.0 + 8.0 * v / (views - 1), (0.02, 0.0, 0.03)))
             for v in range(views)]
@@ -145,9 +142,10 @@ def test_c5_evaluate_loss_vs_reference_build(ctx, ref):
     assert np.array_equal(tr.visible.cpu().numpy() > 0, vis.astype(bool))
     assert np.allclose(tr.vnorm.cpu().numpy(), vn, rtol=1e-3, atol=1e-3 * vn.max())
 
-    # Where does the rest come from?  (i) L1's sign(rendered - target) flips where the float
-    # image and the reference's double image straddle the target; (ii) the backward itself,
-    # isolated by feeding the device's own dL/dimage to the reference's render_backward.
+    # The two sources of difference, isolated: (i) L1's sign(rendered - target) where the float
+    # image and the reference's double image straddle the target (counted; the device decides
+    # those pixels on their FP64 value, rgs_image_loss_ex); (ii) the render backward alone, fed
+    # the device's own dL/dimage on both sides.
     flips = 0
     gsum = np.zeros_like(gref)
     tr0 = train.Trainer(ctx, sc, train.TrainConfig(batch=views))
@@ -155,9 +153,9 @@ def test_c5_evaluate_loss_vs_reference_build(ctx, ref):
     torch.cuda.synchronize()
     inv_b = 1.0 / views
     for cam, tgt in zip(cams, targets):
-        img, rec = ctx.render_forward_device(sc, cam, retain=False)
+        img, rec = ctx.render_forward_device(sc, cam, retain=True)
         dl = torch.zeros_like(img)
-        train.image_loss(ctx, img, tgt, 0.8 * inv_b, 0.2 * inv_b, dl)
+        train.image_loss(ctx, img, tgt, 0.8 * inv_b, 0.2 * inv_b, dl, records=rec)  # as evaluate_loss does
         torch.cuda.synchronize()
         rec.close()
         ref_img, rr = ref.render_forward(store, cam, (0.0, 0.0, 0.0), threads=THREADS, retain=True)

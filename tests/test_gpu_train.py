@@ -61,6 +61,32 @@ def test_image_loss_bit_exact(ctx, T, shape):
     assert abs(losses.cpu().numpy()[0] - 1.5 * l1) <= 1e-12 * l1
 
 
+def test_l1_ties_decided_in_fp64(ctx, orc, T):
+    """rgs_image_loss_ex: with the target equal to the FP32 render every pixel is a tie for the
+    FP32 image (sign 0), while the reference's double image decides sign(img64 - target)
+    (image.cpp:32-33).  With the records the device takes those signs from its FP64 recompute:
+    dL/dimage equals float(l1_loss_backward(reference double image, target)) bit for bit."""
+    import torch
+
+    store = scenes.synthetic_scene(3000, 96, 72, seed=17)
+    cam = scenes.bench_camera(96, 72, 0.4, scenes.yaw_pose(3.0, (0.02, 0.0, 0.04)))
+    sc = DeviceScene.from_store(ctx, store)
+    img, rec = ctx.render_forward_device(sc, cam, retain=True)
+    tgt = img.clone()
+    dl = torch.zeros_like(img)
+    train.image_loss(ctx, img, tgt, 1.0, 0.0, dl, records=rec)
+    dl_plain = torch.zeros_like(img)
+    train.image_loss(ctx, img, tgt, 1.0, 0.0, dl_plain)
+    torch.cuda.synchronize()
+    ref_img, _ = orc.render_forward(store, cam, (0.0, 0.0, 0.0), threads=8)
+    _, g1 = T.l1_loss(ref_img, tgt.cpu().numpy().astype(np.float64))
+    got = dl.cpu().numpy()
+    assert np.count_nonzero(dl_plain.cpu().numpy()) == 0  # every FP32 difference is exactly 0
+    assert np.count_nonzero(g1) > 0.5 * g1.size  # ... the double image's mostly are not
+    assert np.array_equal(got, g1.astype(np.float32)), f"{np.count_nonzero(got != g1.astype(np.float32))} differ"
+    rec.close()
+
+
 def test_image_loss_small_images(ctx, T):
     """Below the 11x11 window: SSIM is rejected (ssim.cpp:81-82), the L1 part still works."""
     import torch
@@ -243,10 +269,8 @@ def _training_case(n=2500, views=3, w=96, h=72, seed=5):
     store = scenes.synthetic_scene(n, w, h, seed=seed)
     cams = [scenes.bench_camera(w, h, 0.2 + 0.3 * k, scenes.yaw_pose(4.0 * k, (0.03, -0.01, 0.05)))
             for k in range(views)]
-    truth = store.copy()
-    r = np.random.default_rng(seed)
-    store.mean[:, :3] += r.normal(0, 0.01, (n, 3)).astype(np.float32)
-    store.sh[:, :, 0] += r.normal(0, 0.1, (n, 3)).astype(np.float32)
+    truth = store
+    store = scenes.perturbed(truth, seed)
     return store, truth, cams
 
 

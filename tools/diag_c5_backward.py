@@ -25,10 +25,7 @@ def main():
     ref = O.reference_build()
     n, w, h = 1_000_000, 1352, 1014
     truth = scenes.synthetic_scene(n, w, h, seed=5)
-    store = truth.copy()
-    r = np.random.default_rng(5)
-    store.mean[:, :3] += r.normal(0, 0.01, (n, 3)).astype(np.float32)
-    store.sh[:, :, 0] += r.normal(0, 0.1, (n, 3)).astype(np.float32)
+    store = scenes.perturbed(truth, 5)
     views = int(os.environ.get("VIEWS", "2"))
     cams = [scenes.bench_camera(w, h, (v + 0.5) / 8, scenes.yaw_pose(-4.0 + 8.0 * v / 7, (0.02, 0.0, 0.03)))
             for v in range(views)]
