@@ -64,6 +64,7 @@ def parse():
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 1M-Gaussian training leg")
     ap.add_argument("--train-only", action="store_true", help="only the C3 training leg (profiling)")
     ap.add_argument("--train-steps", type=int, default=10)
+    ap.add_argument("--no-dropin", action="store_true", help="skip the drop-in (reference trainer.cpp) leg")
     return ap.parse_args()
 
 
@@ -449,6 +450,63 @@ def train_rooflines(ctx, tr, cams, stage_ms):
     return {"roofline": roof, "kernels": kernels, "counts": counts}
 
 
+DROPIN_SO = os.path.join(ROOT, "tests", "cpp", "_build", "librgs_ref_dropin.so")
+
+
+def dropin_leg(store, cams, targets64, nbrs, k, steps=4):
+    """The reference's own training step (trainer.cpp evaluate_loss + accumulate_stats +
+    adam_step, unmodified) compiled against the C++ drop-ins (tests/cpp/Makefile): host
+    GaussianStore in, every render / image loss / optimizer call on the device through the C ABI
+    -- what a maintainer of the reference gets by swapping the sources.  The
+    first step is a warm-up (context, first scene upload)."""
+    import ctypes
+
+    if not os.path.exists(DROPIN_SO):
+        return {"unavailable": "tests/cpp/_build/librgs_ref_dropin.so not built (needs /root/reference at build time)"}
+    L = ctypes.CDLL(DROPIN_SO)
+
+    class Cam(ctypes.Structure):
+        _fields_ = [("width", ctypes.c_int), ("height", ctypes.c_int), ("fx", ctypes.c_double),
+                    ("fy", ctypes.c_double), ("cx", ctypes.c_double), ("cy", ctypes.c_double),
+                    ("world_to_camera", ctypes.c_double * 16), ("time", ctypes.c_double)]
+
+    arr = [np.ascontiguousarray(a, dtype=np.float64) for a in store.arrays_f64()]
+    cs = (Cam * len(cams))(*[Cam(c.width, c.height, c.fx, c.fy, c.cx, c.cy,
+                                 (ctypes.c_double * 16)(*np.asarray(c.world_to_camera, np.float64).reshape(-1)),
+                                 c.time) for c in cams])
+    tg = np.ascontiguousarray(np.concatenate([t.reshape(-1) for t in targets64]))
+    nb = np.ascontiguousarray(nbrs, dtype=np.int32) if nbrs is not None else None
+    losses = np.zeros(5)
+    secs = np.zeros(steps)
+    p = lambda a: a.ctypes.data_as(ctypes.c_void_p) if a is not None else None  # noqa: E731
+    rc = L.dropin_train_steps(ctypes.c_int(store.size()), *[p(a) for a in arr], ctypes.c_int(store.active_sh_degree),
+                              ctypes.c_int(len(cams)), cs, p(tg), p(nb), ctypes.c_int(k),
+                              ctypes.c_int(TRAIN_START_STEP + 1), ctypes.c_int(TRAIN_TOTAL_STEPS), ctypes.c_int(steps),
+                              p(losses), p(secs))
+    if rc != 0:
+        return {"unavailable": "dropin_train_steps failed"}
+    prof = np.zeros(10)
+    L.dropin_profile_step(ctypes.c_int(store.size()), *[p(a) for a in arr], ctypes.c_int(store.active_sh_degree),
+                          ctypes.c_int(len(cams)), cs, p(tg), p(nb), ctypes.c_int(k),
+                          ctypes.c_int(TRAIN_START_STEP + 1), p(prof))
+    parts = ["render_forward", "l1_loss(+backward)", "ssim_loss_with_grad", "dL/dimage assembly", "render_backward",
+             "StoreGrads::add", "entropy", "consistency (host slice loops + consistency_loss)", "accumulate_stats",
+             "adam_step"]
+    stats = (ctypes.c_longlong * 5)()
+    L.rgs_adapter_stats(ctypes.byref(stats, 0), ctypes.byref(stats, 8), ctypes.byref(stats, 16))
+    L.rgs_train_adapter_stats(ctypes.byref(stats, 24), ctypes.byref(stats, 32))
+    timed = secs[1:]
+    return {"value": 1.0 / float(np.median(timed)), "unit": "it/s", "step_ms": [1e3 * x for x in secs],
+            "statistic": f"median of {len(timed)} steps after one warm-up", "loss_last": float(losses[4]),
+            "scene_uploads": int(stats[0]), "scene_cache_hits": int(stats[1]), "backward_records_reused": int(stats[2]),
+            "optimizer_store_uploads": int(stats[3]), "optimizer_store_reuses": int(stats[4]),
+            "step_breakdown_ms": {k: 1e3 * float(v) for k, v in zip(parts, prof)},
+            "note": "the reference's evaluate_loss + accumulate_stats + adam_step (trainer.cpp:134-150) on its host "
+                    "GaussianStore, compiled against host/rgs_adapter.cpp + host/rgs_train_adapter.cpp: renders, "
+                    "image losses and Adam on the device; the store crosses PCIe where the reference API hands it "
+                    "over (adam_step each step; renders reuse the cached device scene until it changes)"}
+
+
 def run_train_leg(args, ctx, dev, dist, rank, world, flush):
     import torch
 
@@ -568,6 +626,11 @@ def run_train_leg(args, ctx, dev, dist, rank, world, flush):
                          f"(render fwd, L1 + SSIM, render bwd, entropy, consistency with k={w.k_neighbors} "
                          f"neighbours) + adam_step, {threads} threads, {cpu_model()}; omits accumulate_stats "
                          f"(O(N) adds)"}
+    dropin = None
+    if rank == 0 and world == 1 and not args.no_dropin:
+        c, t = batch(0)
+        dropin = dropin_leg(store, c, [x.cpu().numpy().astype(np.float64) for x in t],
+                            tr.nbrs.cpu().numpy() if tr.nbrs is not None else None, tr.cfg.loss.k_neighbors)
     return {
         "metric": "train it/s", "value": its, "unit": "it/s", "ms_per_step": ms / args.train_steps,
         "steps": args.train_steps, "warmup": max(args.warmup, 1), "n_gpus": world,
@@ -581,7 +644,7 @@ def run_train_leg(args, ctx, dev, dist, rank, world, flush):
         "loss_first": first.total, "loss_last": last.total, "psnr_last": train.psnr_from_mse(last.mse),
         "knn_rebuild_ms": knn_ms, "stage_ms_one_step": stage_ms, "gpu_launches": launches,
         "roofline": train_roof["roofline"], "kernels": train_roof["kernels"], "workload_counts": train_roof["counts"],
-        "e2e": e2e, "cpu_baseline": cpu,
+        "e2e": e2e, "cpu_baseline": cpu, "dropin": dropin,
     }
 
 

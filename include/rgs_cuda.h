@@ -64,6 +64,10 @@ typedef enum {
                                        rotor / degenerate-time errors and pair-buffer overflow are
                                        folded into the context's deferred status word
                                        (rgs_ctx_status / rgs_ctx_status_async) */
+#define RGS_FLAG_REPRODUCIBLE 256u  /* backward (production FP32 path): the screen-space gradients are
+                                       summed in order-independent 2 x 64-bit fixed point instead of
+                                       FP64 atomics -- bitwise identical results run to run (the
+                                       reference's thread invariance, rasterizer.cpp:372-384) */
 
 typedef struct rgs_ctx rgs_ctx;
 typedef struct rgs_scene rgs_scene;

@@ -20,6 +20,7 @@
 // Stable passes over pairs emitted in rank order leave every tile's list in
 // (depth, index) order: the reference's std::sort order bit for bit.
 #include <algorithm>
+#include <cstdlib>
 
 #include "rgs_internal.cuh"
 
@@ -413,8 +414,10 @@ __global__ void __launch_bounds__(256) k_duplicate(const uint32_t* __restrict__ 
 // round, lane) order = element order.
 constexpr int kRadixThreads = 256;
 constexpr int kRadixWarps = kRadixThreads / 32;
-constexpr int kRadixRounds = 16;
+constexpr int kRadixRounds = 16;  // the largest tile (allocation); RGS_RADIX=8 selects 2048-item tiles
 constexpr int kBlockTile = kRadixThreads * kRadixRounds;  // 4096
+constexpr int kMinBlockTile = kRadixThreads * 8;
+static int g_radix_rounds = 16;
 constexpr int kRadixDigits = 256;
 constexpr int kAuxInts = 784;  // digit histograms + tickets (tile_radix_sort)
 
@@ -425,7 +428,8 @@ constexpr int kAuxInts = 784;  // digit histograms + tickets (tile_radix_sort)
 // aggregate before looking back itself): the spin-wait always terminates.
 constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kCountMask = (1u << 30) - 1u;
 
-__global__ void __launch_bounds__(kRadixThreads) k_radix_onesweep(const uint32_t* __restrict__ keys_in,
+template <int ROUNDS, int MINB>
+__global__ void __launch_bounds__(kRadixThreads, MINB) k_radix_onesweep(const uint32_t* __restrict__ keys_in,
                                                                   const uint32_t* __restrict__ vals_in,
                                                                   const BinState* __restrict__ st, int shift,
                                                                   const int* __restrict__ hist_diff, int hist_plain,
@@ -434,27 +438,27 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_onesweep(const uint32_t
     __shared__ uint32_t wcnt[kRadixWarps][kRadixDigits];
     __shared__ uint32_t dstart[kRadixDigits];
     __shared__ uint32_t gbase[kRadixDigits];
-    __shared__ uint32_t skey[kBlockTile], sval[kBlockTile];
+    __shared__ uint32_t skey[(kRadixThreads * ROUNDS)], sval[(kRadixThreads * ROUNDS)];
     __shared__ uint32_t s_bid;
     if (threadIdx.x == 0) s_bid = atomicAdd(ticket, 1u);
     __syncthreads();
     const uint32_t bid = s_bid;
     const uint32_t n = st->n_pairs_eff;
-    if (bid * (uint32_t)kBlockTile >= n) return;  // past the end (all later tickets too)
+    if (bid * (uint32_t)(kRadixThreads * ROUNDS) >= n) return;  // past the end (all later tickets too)
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
     for (int k = 0; k < kRadixWarps; ++k) wcnt[k][threadIdx.x] = 0;
-    const uint32_t base = bid * kBlockTile + w * (kBlockTile / kRadixWarps);
-    uint32_t key[kRadixRounds], val[kRadixRounds], rk[kRadixRounds];
+    const uint32_t base = bid * (kRadixThreads * ROUNDS) + w * ((kRadixThreads * ROUNDS) / kRadixWarps);
+    uint32_t key[ROUNDS], val[ROUNDS], rk[ROUNDS];
 #pragma unroll
-    for (int j = 0; j < kRadixRounds; ++j) {
+    for (int j = 0; j < ROUNDS; ++j) {
         const uint32_t e = base + j * 32 + lane;
         key[j] = e < n ? keys_in[e] : 0xffffffffu;
         val[j] = e < n ? vals_in[e] : 0u;
     }
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < kRadixRounds; ++j) {
+    for (int j = 0; j < ROUNDS; ++j) {
         const uint32_t d = key[j] != 0xffffffffu ? (key[j] >> shift) & 0xffu : 0xffffffffu;
         const unsigned peers = __match_any_sync(0xffffffffu, d);
         const uint32_t below = __popc(peers & ((1u << lane) - 1u));
@@ -524,7 +528,7 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_onesweep(const uint32_t
     }
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < kRadixRounds; ++j) {
+    for (int j = 0; j < ROUNDS; ++j) {
         if (key[j] == 0xffffffffu) continue;
         const uint32_t d = (key[j] >> shift) & 0xffu;
         const uint32_t p = dstart[d] + wcnt[w][d] + rk[j];
@@ -532,7 +536,7 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_onesweep(const uint32_t
         sval[p] = val[j];
     }
     __syncthreads();
-    const uint32_t valid_in_tile = min((uint32_t)kBlockTile, n - bid * (uint32_t)kBlockTile);
+    const uint32_t valid_in_tile = min((uint32_t)(kRadixThreads * ROUNDS), n - bid * (uint32_t)(kRadixThreads * ROUNDS));
     for (uint32_t i = threadIdx.x; i < valid_in_tile; i += kRadixThreads) {
         const uint32_t k = skey[i];
         const uint32_t d = (k >> shift) & 0xffu;
@@ -697,7 +701,15 @@ void duplicate(const uint32_t* sorted_ids, const uint32_t* pair_off, const uint3
                                                     tile_key_shift(tiles_x, tiles_y), keys, vals, aux);
 }
 
-int radix_blocks(long long n_pairs) { return std::max(blocks(n_pairs, kBlockTile), 1); }
+int radix_blocks(long long n_pairs) { return std::max(blocks(n_pairs, kMinBlockTile), 1); }
+static int radix_grid(long long n_pairs) {
+    return std::max(blocks(n_pairs, kRadixThreads * g_radix_rounds), 1);
+}
+template <typename... A>
+static void radix_pass(int nb, cudaStream_t s, A... a) {
+    if (g_radix_rounds == 8) k_radix_onesweep<8, 4><<<nb, kRadixThreads, 0, s>>>(a...);
+    else k_radix_onesweep<16, 2><<<nb, kRadixThreads, 0, s>>>(a...);
+}
 size_t radix_count_entries(long long n_pairs) { return (size_t)kRadixDigits * radix_blocks(n_pairs); }
 
 // Two stable byte passes (tx, then ty) on ty << 8 | tx; the sorted pairs end back in (keys_a,
@@ -708,7 +720,7 @@ size_t radix_count_entries(long long n_pairs) { return (size_t)kRadixDigits * ra
 int tile_radix_sort(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32_t* vals_b, const BinState* st,
                     long long n_pairs, int tiles_x, int tiles_y, uint32_t* status_a, uint32_t* status_b, int* aux,
                     uint2* ranges, cudaStream_t s) {
-    const int nb = radix_blocks(n_pairs);
+    const int nb = radix_grid(n_pairs);
     const size_t entries = (size_t)kRadixDigits * nb;
     const int n_tiles = tiles_x * tiles_y;
     const int shift = tile_key_shift(tiles_x, tiles_y);
@@ -717,18 +729,18 @@ int tile_radix_sort(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32
     cudaMemsetAsync(status_a, 0, 4 * entries, s);
     cudaMemsetAsync(status_b, 0, 4 * entries, s);
     if (shift == 8) {
-        k_radix_onesweep<<<nb, kRadixThreads, 0, s>>>(keys_a, vals_a, st, 0, aux, 0, status_a, tickets, keys_b,
+        radix_pass(nb, s, keys_a, vals_a, st, 0, aux, 0, status_a, tickets, keys_b,
                                                        vals_b);
-        k_radix_onesweep<<<nb, kRadixThreads, 0, s>>>(keys_b, vals_b, st, 8, aux + 257, 0, status_b, tickets + 1,
+        radix_pass(nb, s, keys_b, vals_b, st, 8, aux + 257, 0, status_b, tickets + 1,
                                                        keys_a, vals_a);
     } else {
         k_digit_hist3<<<148 * 2, 256, 0, s>>>(keys_a, st, aux);
-        k_radix_onesweep<<<nb, kRadixThreads, 0, s>>>(keys_a, vals_a, st, 0, aux, 1, status_a, tickets, keys_b,
+        radix_pass(nb, s, keys_a, vals_a, st, 0, aux, 1, status_a, tickets, keys_b,
                                                        vals_b);
-        k_radix_onesweep<<<nb, kRadixThreads, 0, s>>>(keys_b, vals_b, st, 8, aux + 256, 1, status_b, tickets + 1,
+        radix_pass(nb, s, keys_b, vals_b, st, 8, aux + 256, 1, status_b, tickets + 1,
                                                        keys_a, vals_a);
         cudaMemsetAsync(status_a, 0, 4 * entries, s);
-        k_radix_onesweep<<<nb, kRadixThreads, 0, s>>>(keys_a, vals_a, st, 16, aux + 512, 1, status_a, tickets + 2,
+        radix_pass(nb, s, keys_a, vals_a, st, 16, aux + 512, 1, status_a, tickets + 2,
                                                        keys_b, vals_b);
         out = 1;
     }
@@ -749,6 +761,8 @@ void frame_init(BinState* st, uint32_t pair_cap, uint32_t* bucket_count, uint32_
 }
 
 bool binning_init() {
+    const char* v = std::getenv("RGS_RADIX");
+    g_radix_rounds = (v && v[0] == '8') ? 8 : 16;
     return cudaFuncSetAttribute(k_bucket_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kBigSmem * (int)sizeof(SortRec)) == cudaSuccess;
 }

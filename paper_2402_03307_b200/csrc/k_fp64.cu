@@ -524,7 +524,7 @@ __global__ void __launch_bounds__(256) k_backward_fp64(SplatArrays sp, const uin
                                                        double3 bg, const double* __restrict__ final_T,
                                                        const uint32_t* __restrict__ n_contrib,
                                                        const float* __restrict__ dL, const uint32_t* list,
-                                                       const int* count, double* sg) {
+                                                       const int* count, double* sg, unsigned long long* sgx) {
     const int lane = threadIdx.x & 31;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
     const int total = *count;
@@ -598,9 +598,14 @@ __global__ void __launch_bounds__(256) k_backward_fp64(SplatArrays sp, const uin
                 const double T_before = my_Tb;
                 const double wgt = a * T_before;
                 double* o = sg + (size_t)id * 9;
-                atomicAdd(o + 0, wgt * g0);
-                atomicAdd(o + 1, wgt * g1);
-                atomicAdd(o + 2, wgt * g2);
+                unsigned long long* ox = sgx ? sgx + (size_t)id * 18 : nullptr;
+                auto add = [&](int q, double val) {
+                    if (ox) fixed_add(ox + 2 * q, val);
+                    else atomicAdd(o + q, val);
+                };
+                add(0, wgt * g0);
+                add(1, wgt * g1);
+                add(2, wgt * g2);
                 const double v0 = c0 * T_before - my_s0 / (1 - a);
                 const double v1 = c1 * T_before - my_s1 / (1 - a);
                 const double v2 = c2 * T_before - my_s2 / (1 - a);
@@ -608,13 +613,13 @@ __global__ void __launch_bounds__(256) k_backward_fp64(SplatArrays sp, const uin
                 dL_da += g1 * v1;
                 dL_da += g2 * v2;
                 if (raw <= kAlphaClamp) {
-                    atomicAdd(o + 8, dL_da * (a / cab.w));
+                    add(8, dL_da * (a / cab.w));
                     const double dpow = dL_da * a;
-                    atomicAdd(o + 3, dpow * (-0.5 * dx * dx));
-                    atomicAdd(o + 4, dpow * (-dx * dy));
-                    atomicAdd(o + 5, dpow * (-0.5 * dy * dy));
-                    atomicAdd(o + 6, dpow * (cab.x * dx + cab.y * dy));
-                    atomicAdd(o + 7, dpow * (cab.y * dx + cab.z * dy));
+                    add(3, dpow * (-0.5 * dx * dx));
+                    add(4, dpow * (-dx * dy));
+                    add(5, dpow * (-0.5 * dy * dy));
+                    add(6, dpow * (cab.x * dx + cab.y * dy));
+                    add(7, dpow * (cab.y * dx + cab.z * dy));
                 }
             }
         }
@@ -996,10 +1001,24 @@ int project_one(const double* sliced16_dev, const DevCamera& cam, const double* 
 void backward_fp64_pixels(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges,
                           const DevCamera& cam, double3 bg, const double* final_T, const uint32_t* n_contrib,
                           const float* dL_dimage, const uint32_t* slow_list, const int* slow_count, int max_pixels,
-                          double* screen_grads, cudaStream_t s) {
+                          double* screen_grads, cudaStream_t s, unsigned long long* screen_grads_fixed) {
     if (max_pixels <= 0) return;
     k_backward_fp64<<<persistent_blocks(max_pixels), 256, 0, s>>>(sp, pair_vals, ranges, cam, bg, final_T, n_contrib,
-                                                                  dL_dimage, slow_list, slow_count, screen_grads);
+                                                                  dL_dimage, slow_list, slow_count, screen_grads,
+                                                                  screen_grads_fixed);
+}
+
+}  // namespace rgs_launch
+namespace rgs_dev {
+__global__ void k_fixed_to_double(const unsigned long long* __restrict__ fixed, size_t n, double* __restrict__ out) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        out[i] = fixed_value(fixed + 2 * i);
+}
+}  // namespace rgs_dev
+namespace rgs_launch {
+void fixed_to_double(const unsigned long long* fixed, size_t n_values, double* out, cudaStream_t s) {
+    if (n_values == 0) return;
+    k_fixed_to_double<<<(int)std::min<size_t>((n_values + 255) / 256, 148 * 8), 256, 0, s>>>(fixed, n_values, out);
 }
 
 // K7a (part & 1): the colour / SH path; K7b (part & 2): the geometry chain (reads K7a's d mean3).

@@ -498,7 +498,8 @@ __global__ void __launch_bounds__(kBwdThreads) k_backward_fp32(SplatArrays sp, c
                                                                 const uint2* __restrict__ ranges, DevCamera cam,
                                                                 float3 bg, const double* __restrict__ final_T,
                                                                 const uint32_t* __restrict__ n_contrib,
-                                                                const float* __restrict__ dL, double* sg) {
+                                                                const float* __restrict__ dL, double* sg,
+                                                                unsigned long long* sgx) {
     __shared__ StagedSplat smw[kBwdWarps][32];
     __shared__ float slmw[kBwdWarps][32];
     const int tile = blockIdx.x;
@@ -592,18 +593,25 @@ __global__ void __launch_bounds__(kBwdThreads) k_backward_fp32(SplatArrays sp, c
             }
             const unsigned am = __ballot_sync(kFull, act);
             if (am == 0) continue;
-            double* o = sg + (size_t)__shfl_sync(kFull, myid, k) * 9;
+            const size_t sid = (size_t)__shfl_sync(kFull, myid, k);
+            double* o = sg + sid * 9;
             if (__popc(am) == 1) {
                 if (act) {
 #pragma unroll
                     for (int q = 0; q < 9; ++q)
-                        if (v[q] != 0.f) atomicAdd(o + q, (double)v[q]);
+                        if (v[q] != 0.f) {
+                            if (sgx) fixed_add(sgx + 18 * sid + 2 * q, (double)v[q]);
+                            else atomicAdd(o + q, (double)v[q]);
+                        }
                 }
             } else {
                 int idx;
                 bool ok;
                 const float r = reduce_scatter9(v, lane, idx, ok);
-                if (ok && !(lane & 1) && r != 0.f) atomicAdd(o + idx, (double)r);
+                if (ok && !(lane & 1) && r != 0.f) {
+                    if (sgx) fixed_add(sgx + 18 * sid + 2 * idx, (double)r);
+                    else atomicAdd(o + idx, (double)r);
+                }
             }
         }
     }
@@ -647,10 +655,10 @@ bool raster_init() {
 
 void backward_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges, const DevCamera& cam,
                    float3 bg, const double* final_T, const uint32_t* n_contrib, const float* dL_dimage,
-                   double* screen_grads, cudaStream_t s) {
+                   double* screen_grads, cudaStream_t s, unsigned long long* screen_grads_fixed) {
     const int tiles = cam.tiles_x * cam.tiles_y;
     k_backward_fp32<<<tiles, kBwdThreads, 0, s>>>(sp, pair_vals, ranges, cam, bg, final_T, n_contrib, dL_dimage,
-                                                  screen_grads);
+                                                  screen_grads, screen_grads_fixed);
 }
 
 }  // namespace rgs_launch

@@ -523,11 +523,15 @@ __global__ void __launch_bounds__(128) k_speeds(ParamView P, double* __restrict_
     for (int a = 0; a < 3; ++a) speeds[3 * (size_t)i + a] = s.V[a] / s.W;
 }
 
-// loss.cpp:33-58: loss partials and dL/dspeed (own term written, neighbour terms
-// scattered with FP64 atomics).
+// loss.cpp:33-58: loss partials and dL/dspeed.  Every term of dL/dspeed is +-inv_n (own) or
+// -+inv_n inv_k (neighbour), so the gradient is accumulated exactly as an integer count of
+// inv_n inv_k units (own sign x k, minus each neighbour's sign; integer atomics: the result is
+// independent of their order) and scaled once where it is read (k_speed_backward /
+// k_count_to_speed): bitwise reproducible, and no further from the exact sum than the
+// reference's sequential FP64 accumulation.
 __global__ void __launch_bounds__(256) k_consistency(const double* __restrict__ speeds,
                                                      const int32_t* __restrict__ nbrs, int n, int k,
-                                                     double* __restrict__ dspeed, double* part) {
+                                                     int* __restrict__ dcount, double* part) {
     __shared__ double red[256];
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     double tot = 0;
@@ -550,14 +554,15 @@ __global__ void __launch_bounds__(256) k_consistency(const double* __restrict__ 
         s += fabs(diff[1]);
         s += fabs(diff[2]);
         tot = s;
-        if (dspeed) {
+        if (dcount) {
 #pragma unroll
-            for (int a = 0; a < 3; ++a) atomicAdd(&dspeed[3 * (size_t)i + a], inv_n * sgn[a]);
+            for (int a = 0; a < 3; ++a)
+                if (sgn[a] != 0) atomicAdd(&dcount[3 * (size_t)i + a], k * (int)sgn[a]);
             for (int j = 0; j < k; ++j) {
                 const int q = nbrs[(size_t)k * i + j];
 #pragma unroll
                 for (int a = 0; a < 3; ++a)
-                    if (sgn[a] != 0) atomicAdd(&dspeed[3 * (size_t)q + a], -(inv_n * inv_k * sgn[a]));
+                    if (sgn[a] != 0) atomicAdd(&dcount[3 * (size_t)q + a], -(int)sgn[a]);
             }
         }
     }
@@ -568,13 +573,13 @@ __global__ void __launch_bounds__(256) k_consistency(const double* __restrict__ 
 // slice_backward with only dL/dspeed (trainer.cpp:72-76): the speed gradient enters
 // G4 through V and W; added into the FP32 gradient block (log scales, rotor).
 template <bool F64>
-__global__ void __launch_bounds__(128) k_speed_backward(ParamView P, const double* __restrict__ dspeed,
+__global__ void __launch_bounds__(128) k_speed_backward(ParamView P, const int* __restrict__ dcount, double unit,
                                                         double lambda, float* grads) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= P.n) return;
     double ds[3];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) ds[a] = lambda * dspeed[3 * (size_t)i + a];
+    for (int a = 0; a < 3; ++a) ds[a] = lambda * (unit * (double)dcount[3 * (size_t)i + a]);
     if (ds[0] == 0 && ds[1] == 0 && ds[2] == 0) return;
     double mean4[4], ls[4], rot[8];
     ld_block<F64>(P, 0, i, mean4);
@@ -1108,22 +1113,39 @@ void speeds(const float* params, const double* params64, int n, double* out, uns
         k_speeds<false><<<nblk(n, 128), 128, 0, s>>>(P, out, err);
 }
 
-void consistency(const double* speeds, const int32_t* nbrs, int n, int k, double* dspeed, double* parts,
+void consistency(const double* speeds, const int32_t* nbrs, int n, int k, int* dcount, double* parts,
                  double* losses_slot, int accumulate, cudaStream_t s) {
     const int nb = nblk(n, 256);
-    k_consistency<<<nb, 256, 0, s>>>(speeds, nbrs, n, k, dspeed, parts);
+    k_consistency<<<nb, 256, 0, s>>>(speeds, nbrs, n, k, dcount, parts);
     if (losses_slot) k_finalize<<<1, 256, 0, s>>>(parts, nb, (double)n, 1.0, 0, accumulate, losses_slot);
+}
+
+}  // namespace rgs_launch
+namespace rgs_dev {
+__global__ void k_count_to_speed(const int* __restrict__ dcount, size_t m, double unit, double* __restrict__ dspeed) {
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < m; e += (size_t)gridDim.x * blockDim.x)
+        dspeed[e] = unit * (double)dcount[e];
+}
+}  // namespace rgs_dev
+namespace rgs_launch {
+double consistency_unit(int n, int k) { return (n > 0 && k > 0) ? (1 / (double)n) * (1 / (double)k) : 0.0; }
+
+void count_to_speed(const int* dcount, int n, int k, double* dspeed, cudaStream_t s) {
+    const size_t m = 3 * (size_t)n;
+    if (m) k_count_to_speed<<<std::max(1, std::min(nblk((long long)m, 256), 148 * 8)), 256, 0, s>>>(
+        dcount, m, consistency_unit(n, k), dspeed);
 }
 
 int consistency_blocks(int n) { return nblk(n, 256); }
 
-void speed_backward(const float* params, const double* params64, int n, const double* dspeed, double lambda,
+void speed_backward(const float* params, const double* params64, int n, int k, const int* dcount, double lambda,
                     float* grads, cudaStream_t s) {
     ParamView P{params, n, params64};
+    const double unit = consistency_unit(n, k);
     if (params64)
-        k_speed_backward<true><<<nblk(n, 128), 128, 0, s>>>(P, dspeed, lambda, grads);
+        k_speed_backward<true><<<nblk(n, 128), 128, 0, s>>>(P, dcount, unit, lambda, grads);
     else
-        k_speed_backward<false><<<nblk(n, 128), 128, 0, s>>>(P, dspeed, lambda, grads);
+        k_speed_backward<false><<<nblk(n, 128), 128, 0, s>>>(P, dcount, unit, lambda, grads);
 }
 
 void knn_points(const float* params, const double* params64, int n, const double* scales, double* pts4,

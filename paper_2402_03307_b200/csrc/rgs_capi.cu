@@ -195,6 +195,7 @@ struct rgs_ctx {
     DevBuf deferred;  // u64 deferred status word (RGS_FLAG_DEFER_CHECKS), ~0 when clean
     unsigned long long* host_word = nullptr;  // pinned
     DevBuf sgrad;     // N x 9 doubles (screen-space gradients)
+    DevBuf sgrad_fixed;  // N x 9 x 2 u64 (RGS_FLAG_REPRODUCIBLE fixed-point counters)
     DevBuf cgrad;     // N x 3 doubles (the colour path's d mean3, K7a -> K7b)
     DevBuf tile_grads;  // P x 9 doubles (deterministic backward: per (tile, position))
     DevBuf tmp_img;   // host-buffer staging
@@ -648,6 +649,7 @@ void rgs_ctx_destroy(rgs_ctx* c) {
     c->scratch.release(c->stream);
     c->deferred.release(c->stream);
     c->sgrad.release(c->stream);
+    c->sgrad_fixed.release(c->stream);
     c->cgrad.release(c->stream);
     c->tmp_img.release(c->stream);
     c->tmp_splats.release(c->stream);
@@ -1400,17 +1402,31 @@ int rgs_render_backward(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* ca
                                                &f.dstats()->n_valid, n, f.ent_id.as<uint32_t>(),
                                                c->tile_grads.as<double>(), c->sgrad.as<double>(), s);
         } else {
-            StageTimer t(c, kStBwdTiles, s);
-            rgs_launch::backward_fp32(sa, f.pair_vals(), f.ranges.as<uint2>(), dc, bgf, f.final_T.as<double>(),
-                                      f.n_contrib.as<uint32_t>(), dL_dimage, c->sgrad.as<double>(), s);
-        }
-        if (!(flags & RGS_FLAG_DETERMINISTIC)) {
-            StageTimer t(c, kStBwdFixup, s);
-            rgs_launch::backward_fp64_pixels(sa, f.pair_vals(), f.ranges.as<uint2>(), dc,
-                                             make_double3(f.bg[0], f.bg[1], f.bg[2]), f.final_T.as<double>(),
-                                             f.n_contrib.as<uint32_t>(), dL_dimage, f.slow_list.as<uint32_t>(),
-                                             &f.dstats()->slow_count, (int)((size_t)f.width * f.height),
-                                             c->sgrad.as<double>(), s);
+            // RGS_FLAG_REPRODUCIBLE: the same kernels, accumulating in order-independent fixed point
+            unsigned long long* fx = nullptr;
+            if (flags & RGS_FLAG_REPRODUCIBLE) {
+                const size_t bytes = sizeof(unsigned long long) * 18 * (size_t)std::max(n, 1);
+                c->sgrad_fixed.ensure(bytes, s);
+                CK(cudaMemsetAsync(c->sgrad_fixed.p, 0, bytes, s));
+                fx = c->sgrad_fixed.as<unsigned long long>();
+            }
+            {
+                StageTimer t(c, kStBwdTiles, s);
+                rgs_launch::backward_fp32(sa, f.pair_vals(), f.ranges.as<uint2>(), dc, bgf, f.final_T.as<double>(),
+                                          f.n_contrib.as<uint32_t>(), dL_dimage, c->sgrad.as<double>(), s, fx);
+            }
+            {
+                StageTimer t(c, kStBwdFixup, s);
+                rgs_launch::backward_fp64_pixels(sa, f.pair_vals(), f.ranges.as<uint2>(), dc,
+                                                 make_double3(f.bg[0], f.bg[1], f.bg[2]), f.final_T.as<double>(),
+                                                 f.n_contrib.as<uint32_t>(), dL_dimage, f.slow_list.as<uint32_t>(),
+                                                 &f.dstats()->slow_count, (int)((size_t)f.width * f.height),
+                                                 c->sgrad.as<double>(), s, fx);
+                if (fx) {
+                    rgs_launch::fixed_to_double(fx, 9 * (size_t)n, c->sgrad.as<double>(), s);
+                    c->launches += 1;
+                }
+            }
         }
         c->cgrad.ensure(sizeof(double) * 3 * (size_t)std::max(n, 1), s);
         for (int part = 1; part <= 2; ++part) {
@@ -1547,12 +1563,12 @@ void ensure_ssim_window(rgs_ctx* c) {
 // `parts` holds the image-loss block partials, `cparts` the consistency term's: a training step
 // runs the consistency term on its main stream beside the image losses of its side streams.
 struct TrainScratch {
-    DevBuf dfield, parts, cparts, speeds, dspeed, pts, lo, hi, knn;
+    DevBuf dfield, parts, cparts, speeds, dcount, pts, lo, hi, knn;
     DevBuf tie_list, tie_count, tie_img64, l1_sign;  // rgs_image_loss_ex (l1_sign kept all-zero between calls)
 };
 void train_scratch_free(void* p, cudaStream_t s) {
     TrainScratch* ts = static_cast<TrainScratch*>(p);
-    for (DevBuf* b : {&ts->dfield, &ts->parts, &ts->cparts, &ts->speeds, &ts->dspeed, &ts->pts, &ts->lo, &ts->hi, &ts->knn,
+    for (DevBuf* b : {&ts->dfield, &ts->parts, &ts->cparts, &ts->speeds, &ts->dcount, &ts->pts, &ts->lo, &ts->hi, &ts->knn,
                       &ts->tie_list, &ts->tie_count, &ts->tie_img64, &ts->l1_sign})
         b->release(s);
     delete ts;
@@ -1974,9 +1990,15 @@ int rgs_consistency_loss(rgs_ctx* c, const double* speeds, int n, const int32_t*
         if (n == 0) return RGS_OK;
         TrainScratch& ts = train_scratch(c);
         ts.parts.ensure(sizeof(double) * (rgs_launch::consistency_blocks(n) + 16), c->stream);
-        if (dspeed) CK(cudaMemsetAsync(dspeed, 0, sizeof(double) * 3 * (size_t)n, c->stream));
-        rgs_launch::consistency(speeds, neighbors, n, k, dspeed, ts.parts.as<double>(), losses, 0, c->stream);
-        c->launches += losses ? 2 : 1;
+        int* cnt = nullptr;
+        if (dspeed) {
+            ts.dcount.ensure(sizeof(int) * 3 * (size_t)n, c->stream);
+            CK(cudaMemsetAsync(ts.dcount.p, 0, sizeof(int) * 3 * (size_t)n, c->stream));
+            cnt = ts.dcount.as<int>();
+        }
+        rgs_launch::consistency(speeds, neighbors, n, k, cnt, ts.parts.as<double>(), losses, 0, c->stream);
+        if (dspeed) rgs_launch::count_to_speed(cnt, n, k, dspeed, c->stream);
+        c->launches += (losses ? 2 : 1) + (dspeed ? 1 : 0);
         CK(cudaGetLastError());
         return RGS_OK;
     });
@@ -2001,15 +2023,15 @@ int rgs_consistency(rgs_ctx* c, const rgs_scene* scene, const int32_t* neighbors
         unsigned long long* errp = defer ? c->deferred.as<unsigned long long>() : err.as<unsigned long long>();
         StageTimer t(c, kStConsistency, s);
         rgs_launch::speeds(scene->params, scene->params64, n, ts.speeds.as<double>(), errp, s);
-        double* dspeed = nullptr;
+        int* dcount = nullptr;
         if (grads) {
-            ts.dspeed.ensure(sizeof(double) * 3 * (size_t)n, s);
-            CK(cudaMemsetAsync(ts.dspeed.p, 0, sizeof(double) * 3 * (size_t)n, s));
-            dspeed = ts.dspeed.as<double>();
+            ts.dcount.ensure(sizeof(int) * 3 * (size_t)n, s);
+            CK(cudaMemsetAsync(ts.dcount.p, 0, sizeof(int) * 3 * (size_t)n, s));
+            dcount = ts.dcount.as<int>();
         }
-        rgs_launch::consistency(ts.speeds.as<double>(), neighbors, n, k, dspeed, ts.cparts.as<double>(), losses,
+        rgs_launch::consistency(ts.speeds.as<double>(), neighbors, n, k, dcount, ts.cparts.as<double>(), losses,
                                 (flags & RGS_FLAG_ACCUMULATE) ? 1 : 0, s);
-        if (grads) rgs_launch::speed_backward(scene->params, scene->params64, n, dspeed, lambda, grads, s);
+        if (grads) rgs_launch::speed_backward(scene->params, scene->params64, n, k, dcount, lambda, grads, s);
         c->launches += 2 + (losses ? 1 : 0) + (grads ? 1 : 0);
         if (defer) return RGS_OK;  // the speeds' error is in the deferred status word
         unsigned long long e = 0;

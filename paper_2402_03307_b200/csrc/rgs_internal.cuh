@@ -123,6 +123,21 @@ constexpr float kGuardFloor = 1e-6f;
 // Packed per-pixel state written by the forward: bit 31 = slow (FP64) pixel.
 constexpr uint32_t kSlowBit = 0x80000000u;
 
+// Reproducible accumulation of the screen-space gradients (RGS_FLAG_REPRODUCIBLE): each double
+// contribution v is added to a pair of 64-bit integer counters as fixed point -- v 2^20 =
+// hi + f (hi = floor, f in [0, 1)), hi into the first (two's complement), f 2^40 (truncated) into
+// the second.  Integer addition is associative, so the sums are bitwise independent of the
+// order the atomics land in: |sum| < 2^43, resolution 2^-60, up to 2^23 contributions per value.
+__device__ __forceinline__ void fixed_add(unsigned long long* hl, double v) {
+    const double s = v * 1048576.0;  // 2^20
+    const double h = floor(s);
+    atomicAdd(hl, (unsigned long long)(long long)h);
+    atomicAdd(hl + 1, (unsigned long long)((s - h) * 1099511627776.0));  // 2^40
+}
+__device__ __forceinline__ double fixed_value(const unsigned long long* hl) {
+    return ((double)(long long)hl[0] + (double)hl[1] * 9.094947017729282e-13) * 9.5367431640625e-07;  // 2^-40, 2^-20
+}
+
 }  // namespace rgs_dev
 
 // ---------------------------------------------------------------------------
@@ -179,13 +194,18 @@ void backward_deterministic(const SplatArrays& sp, const uint32_t* pair_vals, co
                             uint32_t* rank, double* tile_grads, double* screen_grads, cudaStream_t s);
 int project_one(const double* sliced16_dev, const DevCamera& cam, const double* sh48_dev, int sh_degree,
                 double opacity_logit, void* out_dev, int* survived_dev, cudaStream_t s);
+// screen_grads_fixed (NULL: FP64 atomics into screen_grads): RGS_FLAG_REPRODUCIBLE's fixed-point
+// counters (18 u64 per splat, fixed_add), turned into screen_grads by fixed_to_double.
 void backward_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges,
                    const DevCamera& cam, float3 bg, const double* final_T, const uint32_t* n_contrib,
-                   const float* dL_dimage, double* screen_grads, cudaStream_t s);
+                   const float* dL_dimage, double* screen_grads, cudaStream_t s,
+                   unsigned long long* screen_grads_fixed = nullptr);
 void backward_fp64_pixels(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges,
                           const DevCamera& cam, double3 bg, const double* final_T, const uint32_t* n_contrib,
                           const float* dL_dimage, const uint32_t* slow_list, const int* slow_count,
-                          int max_pixels, double* screen_grads, cudaStream_t s);
+                          int max_pixels, double* screen_grads, cudaStream_t s,
+                          unsigned long long* screen_grads_fixed = nullptr);
+void fixed_to_double(const unsigned long long* fixed, size_t n_values, double* out, cudaStream_t s);
 void gaussian_backward(const float* params, const double* params64, int n, int sh_degree, const DevCamera& cam,
                        const double4* dir_dist, double* color_dmean3, const uint8_t* valid,
                        const double* screen_grads, int accumulate, float* grads, float* vnorm,

@@ -69,10 +69,14 @@ void accumulate_stats_f64(const double* vnorm, const int32_t* visible, int n, do
 void reset_opacity(bool f64, void* params, void* m1, void* m2, int n, double value, cudaStream_t s);
 void speeds(const float* params, const double* params64, int n, double* out, unsigned long long* err,
             cudaStream_t s);
-void consistency(const double* speeds, const int32_t* nbrs, int n, int k, double* dspeed, double* parts,
+// dL/dspeed as integer counts of consistency_unit(n, k) = inv_n inv_k (3 int per Gaussian, zeroed by
+// the caller); count_to_speed turns them into doubles.
+void consistency(const double* speeds, const int32_t* nbrs, int n, int k, int* dcount, double* parts,
                  double* losses_slot, int accumulate, cudaStream_t s);
+double consistency_unit(int n, int k);
+void count_to_speed(const int* dcount, int n, int k, double* dspeed, cudaStream_t s);
 int consistency_blocks(int n);
-void speed_backward(const float* params, const double* params64, int n, const double* dspeed, double lambda,
+void speed_backward(const float* params, const double* params64, int n, int k, const int* dcount, double lambda,
                     float* grads, cudaStream_t s);
 void knn_points(const float* params, const double* params64, int n, const double* scales, double* pts4,
                 cudaStream_t s);

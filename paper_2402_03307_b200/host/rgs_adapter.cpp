@@ -26,21 +26,12 @@
 
 #include "rgs/rasterizer.hpp"
 #include "rgs_cuda.h"
+#include "rgs_dropin_common.hpp"
 
 namespace rgs {
 namespace {
 
-rgs_ctx* context() {
-    static rgs_ctx* c = [] {
-        rgs_ctx* h = nullptr;
-        const char* dev = std::getenv("RGS_DEVICE");
-        const int rc = rgs_ctx_create(dev ? std::atoi(dev) : 0, &h);
-        if (rc != RGS_OK)
-            throw std::runtime_error("rgs_b200: no CUDA device (the B200 render path has no CPU fallback)");
-        return h;
-    }();
-    return c;
-}
+rgs_ctx* context() { return dropin::context(); }
 
 bool kat_mode() {
     const char* v = std::getenv("RGS_KAT_MODE");
@@ -106,45 +97,7 @@ rgs_splat to_c(const Splat2D& s) {
     return o;
 }
 
-// 64-bit content hash (multiply-rotate over 8-byte words, four independent lanes).
-uint64_t hash_words(const void* p, size_t bytes, uint64_t h) {
-    const unsigned char* b = static_cast<const unsigned char*>(p);
-    const size_t nw = bytes / 8;
-    uint64_t l[4] = {h ^ 0x9e3779b97f4a7c15ull, h + 0xc2b2ae3d27d4eb4full, h * 31 + 1, ~h};
-    size_t i = 0;
-    for (; i + 4 <= nw; i += 4) {
-        for (int k = 0; k < 4; ++k) {
-            uint64_t w;
-            std::memcpy(&w, b + 8 * (i + k), 8);
-            l[k] = (l[k] ^ w) * 0x100000001b3ull;
-            l[k] = (l[k] << 29) | (l[k] >> 35);
-        }
-    }
-    for (; i < nw; ++i) {
-        uint64_t w;
-        std::memcpy(&w, b + 8 * i, 8);
-        l[0] = ((l[0] ^ w) * 0x100000001b3ull);
-        l[0] = (l[0] << 29) | (l[0] >> 35);
-    }
-    for (size_t j = 8 * nw; j < bytes; ++j) l[1] = (l[1] ^ b[j]) * 0x100000001b3ull;
-    return (l[0] * 3 + l[1]) * 0x9e3779b97f4a7c15ull ^ (l[2] * 5 + l[3]);
-}
-
-template <typename V>
-uint64_t hash_vec(const V& v, uint64_t h) {
-    return hash_words(v.data(), v.size() * sizeof(typename V::value_type), h);
-}
-
-// The parameters a render reads (gaussian.hpp:79-85), hashed per array.
-uint64_t store_hash(const GaussianStore& st) {
-    uint64_t h = 0x5bd1e995u ^ (uint64_t)st.size() ^ ((uint64_t)st.active_sh_degree << 40);
-    h = hash_vec(st.mean, h);
-    h = hash_vec(st.log_scales, h);
-    h = hash_vec(st.rotor, h);
-    h = hash_vec(st.opacity_logit, h);
-    h = hash_vec(st.sh, h);
-    return h;
-}
+using dropin::hash_vec;
 
 // GaussianStore (gaussian.hpp:79-103) -> the cached device scene (FP64 storage: the store's
 // double values reach the kernels unrounded).  Re-uploaded only when the contents change.
@@ -152,7 +105,7 @@ struct SceneCache {
     rgs_scene* s = nullptr;
     int n = -1, sh = -1;
     uint64_t hash = 0;
-    long long uploads = 0, hits = 0;
+    long long uploads = 0, hits = 0, d2d = 0;
 };
 SceneCache& scene_cache() {
     static SceneCache c;
@@ -162,7 +115,7 @@ SceneCache& scene_cache() {
 rgs_scene* device_scene(const GaussianStore& store, uint64_t* key = nullptr) {
     SceneCache& c = scene_cache();
     const int n = store.size();
-    const uint64_t h = store_hash(store);
+    const uint64_t h = dropin::params_hash(store);
     if (key) *key = h;
     if (c.s && c.n == n && c.sh == store.active_sh_degree && c.hash == h) {
         ++c.hits;
@@ -174,6 +127,16 @@ rgs_scene* device_scene(const GaussianStore& store, uint64_t* key = nullptr) {
     }
     if (!c.s) check(rgs_scene_create_ex(context(), n, store.active_sh_degree, RGS_SCENE_F64, &c.s));
     rgs_scene_set_sh_degree(c.s, store.active_sh_degree);
+    // the training side just wrote exactly these parameters on the device: copy them over
+    if (const double* src = dropin::published_params(h, n, store.active_sh_degree)) {
+        c.n = -1;
+        if (n) check(rgs_memcpy(context(), rgs_scene_params_f64(c.s), src, sizeof(double) * 65 * (size_t)n));
+        c.n = n;
+        c.sh = store.active_sh_degree;
+        c.hash = h;
+        ++c.d2d;
+        return c.s;
+    }
     std::vector<double> mean(4 * (size_t)n), ls(4 * (size_t)n), rot(8 * (size_t)n), op(n), sh(48 * (size_t)n);
     for (int i = 0; i < n; ++i) {
         for (int a = 0; a < 4; ++a) mean[4 * i + a] = store.mean[i][a];
@@ -344,7 +307,9 @@ StoreGrads render_backward(const GaussianStore& store, const Camera& cam, const 
     std::vector<float> dl(dL_dimage.data.begin(), dL_dimage.data.end());
     std::vector<float> g(65 * (size_t)std::max(n, 1)), vn(std::max(n, 1));
     std::vector<int32_t> vis(std::max(n, 1));
-    const unsigned flags = RGS_FLAG_HOST_BUFFERS | (kat_mode() ? RGS_FLAG_DETERMINISTIC : 0u);
+    // thread-count invariant like the reference's fixed-order reduction (rasterizer.cpp:372-384):
+    // the FP64 replay in KAT mode, the fixed-point accumulation otherwise
+    const unsigned flags = RGS_FLAG_HOST_BUFFERS | (kat_mode() ? RGS_FLAG_DETERMINISTIC : RGS_FLAG_REPRODUCIBLE);
     check(rgs_render_backward(context(), scene, &c, dev_rec, dl.data(), flags, g.data(), vn.data(), vis.data()));
     // device SoA (rgs_scene_params layout) -> per-Gaussian gradients
     StoreGrads out;

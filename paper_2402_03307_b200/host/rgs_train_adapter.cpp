@@ -35,20 +35,12 @@
 #include "rgs/sh.hpp"
 #include "rgs/ssim.hpp"
 #include "rgs_cuda.h"
+#include "rgs_dropin_common.hpp"
 
 namespace rgs {
 namespace {
 
-rgs_ctx* tctx() {
-    static rgs_ctx* c = [] {
-        rgs_ctx* h = nullptr;
-        const char* dev = std::getenv("RGS_DEVICE");
-        if (rgs_ctx_create(dev ? std::atoi(dev) : 0, &h) != RGS_OK)
-            throw std::runtime_error("rgs_b200: no CUDA device (the B200 path has no CPU fallback)");
-        return h;
-    }();
-    return c;
-}
+rgs_ctx* tctx() { return dropin::context(); }
 
 [[noreturn]] void raise(int rc) {
     const std::string msg = rgs_ctx_last_error(tctx());
@@ -63,14 +55,11 @@ void check(int rc) {
     if (rc != RGS_OK) raise(rc);
 }
 
-// Owning device buffer.
+// Device buffer borrowed from the drop-ins' pool for the duration of a call.
 struct Dev {
     void* p = nullptr;
-    explicit Dev(size_t bytes) {
-        p = rgs_malloc(tctx(), bytes);
-        if (!p) raise(RGS_E_CUDA);
-    }
-    ~Dev() { rgs_free(tctx(), p); }
+    explicit Dev(size_t bytes) { p = dropin::pool_get(bytes); }
+    ~Dev() { dropin::pool_put(p); }
     Dev(const Dev&) = delete;
     Dev& operator=(const Dev&) = delete;
     template <typename T>
@@ -116,6 +105,21 @@ struct DeviceStore {
         if (scene) rgs_scene_destroy(scene);
     }
 };
+
+// The device copy of the last store an optimizer entry point (adam_step, accumulate_stats,
+// reset_opacity) worked on: parameters, moments and statistics, with the hashes of the host
+// store it was last synchronised with.  While the host store still hashes to them (train_from
+// changes it only through these entry points) the next call skips the upload.
+struct Mirror {
+    DeviceStore d;
+    int n = -1;
+    uint64_t hp = 0, hm = 0, hs = 0;
+    long long uploads = 0, reuses = 0;
+};
+Mirror& mirror() {
+    static Mirror m;
+    return m;
+}
 
 void rows65(const GaussianStore& s, bool moments_v, std::vector<double>& out) {
     const size_t n = (size_t)s.size();
@@ -198,6 +202,109 @@ void download(const DeviceStore& d, GaussianStore& s) {
         o.grad_count[i] = cnt[i];
     }
     s = std::move(o);
+}
+
+// Parameters / moments of the device store into the host store, in place (sizes equal).
+void download_params(const DeviceStore& d, GaussianStore& s) {
+    const size_t n = (size_t)s.size();
+    std::vector<double> mean(4 * n), ls(4 * n), rot(8 * n), op(n), sh(48 * n);
+    check(rgs_scene_download_f64(tctx(), d.scene, mean.data(), ls.data(), rot.data(), op.data(), sh.data()));
+    for (size_t i = 0; i < n; ++i) {
+        for (int a = 0; a < 4; ++a) s.mean[i][a] = mean[4 * i + a], s.log_scales[i][a] = ls[4 * i + a];
+        Vec8 c;
+        for (int a = 0; a < 8; ++a) c[a] = rot[8 * i + a];
+        s.rotor[i] = Rotor4::from_coeffs(c);
+        s.opacity_logit[i] = op[i];
+        for (int ch = 0; ch < 3; ++ch)
+            for (int k = 0; k < 16; ++k) s.sh[i](ch, k) = sh[48 * i + ch * 16 + k];
+    }
+}
+
+void download_moments(const DeviceStore& d, GaussianStore& s) {
+    const size_t n = (size_t)s.size();
+    std::vector<double> m(65 * n), v(65 * n);
+    check(rgs_optimizer_download(tctx(), d.opt, m.data(), v.data(), nullptr, nullptr));
+    for (size_t i = 0; i < n; ++i) {
+        const double* mr = m.data() + 65 * i;
+        const double* vr = v.data() + 65 * i;
+        for (int a = 0; a < 4; ++a) {
+            s.m_mean[i][a] = mr[a], s.v_mean[i][a] = vr[a];
+            s.m_ls[i][a] = mr[4 + a], s.v_ls[i][a] = vr[4 + a];
+        }
+        for (int a = 0; a < 8; ++a) s.m_rot[i][a] = mr[8 + a], s.v_rot[i][a] = vr[8 + a];
+        s.m_op[i] = mr[16];
+        s.v_op[i] = vr[16];
+        for (int ch = 0; ch < 3; ++ch)
+            for (int k = 0; k < 16; ++k) {
+                s.m_sh[i](ch, k) = mr[17 + ch * 16 + k];
+                s.v_sh[i](ch, k) = vr[17 + ch * 16 + k];
+            }
+    }
+}
+
+// The mirror brought in line with the host store: only the parts whose hash changed are
+// uploaded (nothing, when the store is the one the last call wrote back).
+DeviceStore& synced(const GaussianStore& s) {
+    Mirror& m = mirror();
+    const int n = s.size();
+    const uint64_t hp = dropin::params_hash(s), hm = dropin::moments_hash(s), hs = dropin::stats_hash(s);
+    const bool fresh = !m.d.scene || m.n != n;
+    if (fresh) {
+        m.d.~DeviceStore();
+        new (&m.d) DeviceStore();
+        m.n = -1;
+        check(rgs_scene_create_ex(tctx(), n, s.active_sh_degree, RGS_SCENE_F64, &m.d.scene));
+        check(rgs_optimizer_create(tctx(), m.d.scene, &m.d.opt));
+    }
+    rgs_scene_set_sh_degree(m.d.scene, s.active_sh_degree);
+    if (!fresh && m.hp == hp && m.hm == hm && m.hs == hs) {
+        ++m.reuses;
+        return m.d;
+    }
+    m.n = -1;  // invalid until every part is up
+    if (fresh || m.hp != hp) {
+        std::vector<double> mean(4 * (size_t)n), ls(4 * (size_t)n), rot(8 * (size_t)n), op((size_t)n),
+            sh(48 * (size_t)n);
+        for (int i = 0; i < n; ++i) {
+            for (int a = 0; a < 4; ++a) mean[4 * i + a] = s.mean[i][a], ls[4 * i + a] = s.log_scales[i][a];
+            const Vec8 c = s.rotor[i].coeffs();
+            for (int a = 0; a < 8; ++a) rot[8 * i + a] = c[a];
+            op[i] = s.opacity_logit[i];
+            for (int ch = 0; ch < 3; ++ch)
+                for (int k = 0; k < 16; ++k) sh[48 * (size_t)i + ch * 16 + k] = s.sh[i](ch, k);
+        }
+        if (n) check(rgs_scene_upload_f64(tctx(), m.d.scene, mean.data(), ls.data(), rot.data(), op.data(), sh.data(),
+                                          nullptr));
+    }
+    if (n && (fresh || m.hm != hm)) {
+        std::vector<double> mo, vo;
+        rows65(s, false, mo);
+        rows65(s, true, vo);
+        check(rgs_optimizer_upload(tctx(), m.d.opt, mo.data(), vo.data(), nullptr, nullptr));
+    }
+    if (n && (fresh || m.hs != hs)) {
+        std::vector<int32_t> cnt((size_t)n);
+        for (int i = 0; i < n; ++i) cnt[i] = s.grad_count[i];
+        check(rgs_optimizer_upload(tctx(), m.d.opt, nullptr, nullptr, s.grad_accum.data(), cnt.data()));
+    }
+    m.n = n;
+    m.hp = hp;
+    m.hm = hm;
+    m.hs = hs;
+    ++m.uploads;
+    return m.d;
+}
+
+// After a device update of the mirror written back into `s`: the new hashes, and the new
+// parameters published for the render drop-in (a device-to-device copy instead of an upload).
+void written_back(const GaussianStore& s, bool params, bool moments, bool stats) {
+    Mirror& m = mirror();
+    if (params) {
+        m.hp = dropin::params_hash(s);
+        dropin::publish_params(m.hp, s.size(), s.active_sh_degree, rgs_scene_params_f64(m.d.scene));
+    }
+    if (moments) m.hm = dropin::moments_hash(s);
+    if (stats) m.hs = dropin::stats_hash(s);
 }
 
 // Device KNN of `queries` among `points` (exclude[q] skipped), k <= 16.
@@ -419,8 +526,7 @@ void adam_step(GaussianStore& store, const StoreGrads& grads, const TrainConfig&
     if (grads.size() != store.size()) throw ShapeMismatchGradError();
     const int n = store.size();
     if (n == 0) return;
-    DeviceStore d;
-    upload(store, d, true);
+    DeviceStore& d = synced(store);
     // gradients in the rgs_scene_params SoA layout (float32, the device gradient format)
     std::vector<float> g(65 * (size_t)n);
     for (int i = 0; i < n; ++i) {
@@ -454,22 +560,26 @@ void adam_step(GaussianStore& store, const StoreGrads& grads, const TrainConfig&
     c.flags = 0;
     check(rgs_adam_step(tctx(), d.scene, d.opt, dg.as<float>(), nullptr, nullptr, &c, step, nullptr));
     check(rgs_optimizer_status(tctx(), d.opt));
-    download(d, store);
+    download_params(d, store);
+    download_moments(d, store);
+    written_back(store, true, true, false);
 }
 
 void accumulate_stats(GaussianStore& store, const StoreGrads& view_grads) {
     if (view_grads.size() != store.size()) throw ShapeMismatchGradError();
     const int n = store.size();
     if (n == 0) return;
-    DeviceStore d;
-    upload(store, d, true);
+    DeviceStore& d = synced(store);
     std::vector<int32_t> vis(n);
     for (int i = 0; i < n; ++i) vis[i] = view_grads.visible[i];
     Dev dvn(8 * (size_t)n), dvis(4 * (size_t)n);
     dvn.put(view_grads.viewspace_norm.data(), 8 * (size_t)n);
     dvis.put(vis.data(), 4 * (size_t)n);
     check(rgs_accumulate_stats_f64(tctx(), d.opt, dvn.as<double>(), dvis.as<int32_t>()));
-    download(d, store);
+    std::vector<int32_t> cnt((size_t)n);
+    check(rgs_optimizer_download(tctx(), d.opt, nullptr, nullptr, store.grad_accum.data(), cnt.data()));
+    for (int i = 0; i < n; ++i) store.grad_count[i] = cnt[i];
+    written_back(store, false, false, true);
 }
 
 DensifyReport densify_and_prune(GaussianStore& store, const TrainConfig& config, Scalar scene_extent,
@@ -501,6 +611,7 @@ DensifyReport densify_and_prune(GaussianStore& store, const TrainConfig& config,
     std::istringstream is(st);
     is >> rng;
     download(d, store);
+    mirror().n = -1;  // the store was resized: the mirror no longer matches it
     DensifyReport out;
     out.cloned = rep.cloned;
     out.split = rep.split;
@@ -510,10 +621,17 @@ DensifyReport densify_and_prune(GaussianStore& store, const TrainConfig& config,
 
 void reset_opacity(GaussianStore& store, Scalar value) {
     if (store.size() == 0) return;
-    DeviceStore d;
-    upload(store, d, true);
+    DeviceStore& d = synced(store);
     check(rgs_reset_opacity(tctx(), d.scene, d.opt, value));
-    download(d, store);
+    download_params(d, store);
+    download_moments(d, store);
+    written_back(store, true, true, false);
 }
 
 }  // namespace rgs
+
+// Drop-in statistics (bench / tests): optimizer-store uploads and reuses of the device mirror.
+extern "C" void rgs_train_adapter_stats(long long* uploads, long long* reuses) {
+    if (uploads) *uploads = rgs::mirror().uploads;
+    if (reuses) *reuses = rgs::mirror().reuses;
+}

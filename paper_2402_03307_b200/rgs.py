@@ -49,6 +49,7 @@ FLAG_IMAGE_F64 = 16
 FLAG_DETERMINISTIC = 32
 FLAG_ACCUMULATE_GRAD = 64
 FLAG_DEFER_CHECKS = 128
+FLAG_REPRODUCIBLE = 256
 
 _CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy
 SCENE_F64 = 1  # rgs_scene_create_ex storage flag
@@ -426,8 +427,17 @@ class Context:
         self.sync_stream()
 
     def sync_stream(self):
-        """Order our kernels on torch's current stream (when torch is in use)."""
+        """Order our next kernels after torch's work: on torch's current stream (the default),
+        or -- a context on its own stream -- after torch's current stream has drained (its
+        allocations / fills / copies of the tensors handed to us)."""
         if not self._torch_stream:
+            try:
+                import torch
+
+                if torch.cuda.is_available() and torch.cuda.is_initialized():
+                    torch.cuda.current_stream(self.device).synchronize()
+            except ImportError:
+                pass
             return
         try:
             import torch
@@ -595,11 +605,15 @@ class Context:
         h = _vp()
         self.check(self.L.rgs_render_forward(self.h, scene.h, ctypes.byref(c), bg, flags, _vp(_ptr(image)),
                                              ctypes.byref(h)))
+        self.fence()
         return image, RenderRecords(self, h, cam, background, retain)
 
     def render_backward_device(self, scene: "DeviceScene", cam: Camera, records: "RenderRecords", dL_dimage,
-                               grads=None, vnorm=None, visible=None, accumulate=False, deterministic=False):
-        """``deterministic``: RGS_FLAG_DETERMINISTIC (fixed-order FP64 replay, bitwise repeatable)."""
+                               grads=None, vnorm=None, visible=None, accumulate=False, deterministic=False,
+                               reproducible=False):
+        """``deterministic``: RGS_FLAG_DETERMINISTIC (the reference-order FP64 replay, bitwise
+        repeatable); ``reproducible``: RGS_FLAG_REPRODUCIBLE (the production path with
+        order-independent fixed-point accumulation, bitwise repeatable)."""
         import torch
 
         self.sync_stream()
@@ -610,10 +624,13 @@ class Context:
             vnorm = torch.zeros(n, dtype=torch.float32, device=dev)
             visible = torch.zeros(n, dtype=torch.int32, device=dev)
         c = cam.to_c()
-        flags = (FLAG_ACCUMULATE if accumulate else 0) | (FLAG_DETERMINISTIC if deterministic else 0)
-        self.check(self.L.rgs_render_backward(self.h, scene.h, ctypes.byref(c), records.h,
-                                              _vp(_ptr(dL_dimage.contiguous())), flags, _vp(_ptr(grads)),
-                                              _vp(_ptr(vnorm)), _vp(_ptr(visible))))
+        flags = (FLAG_ACCUMULATE if accumulate else 0) | (FLAG_DETERMINISTIC if deterministic else 0) | \
+            (FLAG_REPRODUCIBLE if reproducible else 0)
+        dl = dL_dimage.contiguous()
+        self.sync_stream()  # (after the gradient buffers' allocation / fill on torch's stream)
+        self.check(self.L.rgs_render_backward(self.h, scene.h, ctypes.byref(c), records.h, _vp(_ptr(dl)), flags,
+                                              _vp(_ptr(grads)), _vp(_ptr(vnorm)), _vp(_ptr(visible))))
+        self.fence()
         return grads, vnorm, visible
 
 

@@ -154,6 +154,7 @@ class DeviceOptimizer:
                                                 _vp(_ptr(visible)) if visible is not None else None,
                                                 ctypes.byref(cfg), int(step),
                                                 _vp(_ptr(losses)) if losses is not None else None))
+        self.ctx.fence()
 
     def status(self):
         """Raises the rotor error of the steps since the last call (synchronises)."""
@@ -477,6 +478,8 @@ class Trainer:
         self._dl = None
         self._streams = None
         self.overlap = True  # forward of view v+1 alongside the backward of view v
+        # RGS_FLAG_REPRODUCIBLE backward: bitwise identical steps run to run (fixed-point sums)
+        self.reproducible = False
         self.n_slots = 3  # views whose forward / loss may be in flight at once (side streams)
         # Deferred checks: the step's forwards and consistency term do not synchronise; their
         # rotor / degenerate-time errors and pair-buffer overflows surface at the step's loss
@@ -591,7 +594,8 @@ class Trainer:
                 image_loss(ctx, img, tgt, wl1, wss, dl if want_grads else None, self.losses, loss_scale=inv_b,
                            accumulate=True, records=rec if want_grads else None)
             if want_grads:
-                ctx.render_backward_device(scene, cam, rec, dl, self.grads, self.vnorm, self.visible, accumulate=True)
+                ctx.render_backward_device(scene, cam, rec, dl, self.grads, self.vnorm, self.visible, accumulate=True,
+                                           reproducible=self.reproducible)
             if overlap:
                 free[slot] = main.record_event()
             recs.append(rec)

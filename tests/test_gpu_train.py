@@ -87,6 +87,62 @@ def test_l1_ties_decided_in_fp64(ctx, orc, T):
     rec.close()
 
 
+@pytest.mark.parametrize("steps", [3])
+def test_reproducible_training_steps(ctx, steps):
+    """Trainer.reproducible (RGS_FLAG_REPRODUCIBLE backward: fixed-point screen-gradient sums;
+    integer-count consistency gradient): two runs of the same steps from the same start give
+    bitwise identical scenes and losses; the result stays within the atomic path's tolerance."""
+    import torch
+
+    store, truth, cams = _training_case(n=6000, views=3, w=160, h=120)
+    tsc = DeviceScene.from_store(ctx, truth)
+    targets = [ctx.render_forward_device(tsc, c, retain=False)[0].clone() for c in cams]
+    runs = []
+    for reproducible in (True, True, False):
+        sc = DeviceScene.from_store(ctx, store)
+        tr = train.Trainer(ctx, sc, train.TrainConfig(), start_step=3000)
+        tr.reproducible = reproducible
+        losses = [tr.step(cams, targets).total for _ in range(steps)]
+        torch.cuda.synchronize()
+        runs.append((sc.download(), losses))
+    (s1, l1), (s2, l2), (s3, l3) = runs
+    assert l1 == l2
+    for a, b in zip(s1, s2):
+        assert np.array_equal(a, b)
+    for a, b in zip(s1, s3):
+        assert np.allclose(a, b, rtol=1e-4, atol=1e-6)
+
+
+def test_reproducible_backward_matches_atomic(ctx, orc):
+    """RGS_FLAG_REPRODUCIBLE against the oracle: the same floored 1e-3 bar as the atomic path,
+    and repeat calls bitwise identical."""
+    import torch
+
+    store = scenes.synthetic_scene(20000, 320, 240, seed=6)
+    cam = scenes.bench_camera(320, 240, 0.5, scenes.yaw_pose(5.0, (0.02, 0.0, 0.04)))
+    sc = DeviceScene.from_store(ctx, store)
+    _, rec = ctx.render_forward_device(sc, cam, retain=True)
+    dl = torch.from_numpy(np.random.default_rng(2).uniform(-1, 1, (240, 320, 3)).astype(np.float32)).cuda()
+    a = ctx.render_backward_device(sc, cam, rec, dl, reproducible=True)[0].cpu().numpy()
+    b = ctx.render_backward_device(sc, cam, rec, dl, reproducible=True)[0].cpu().numpy()
+    c = ctx.render_backward_device(sc, cam, rec, dl)[0].cpu().numpy()
+    assert np.array_equal(a, b)
+    _, rr = orc.render_forward(store, cam, retain=True)
+    gr, _, _ = orc.render_backward(store, cam, rr, dl.cpu().numpy().astype(np.float64))
+    n = store.size()
+
+    def err(x):
+        mean, ls, rot, op, sh = rgs.grads_from_soa(x, n)
+        return floored_rel_err(np.concatenate([mean, ls, rot, op[:, None], sh.reshape(n, 48)], axis=1), gr)
+
+    e_rep, e_atomic = err(a), err(c)
+    print(f"reproducible: max {e_rep.max():.3e} above 1e-3 {(e_rep > 1e-3).sum()}; "
+          f"atomic: max {e_atomic.max():.3e} above 1e-3 {(e_atomic > 1e-3).sum()}")
+    assert (e_rep > 1e-3).sum() <= (e_atomic > 1e-3).sum()
+    assert float((e_rep <= 1e-3).mean()) >= 0.9999
+    rec.close()
+
+
 def test_image_loss_small_images(ctx, T):
     """Below the 11x11 window: SSIM is rejected (ssim.cpp:81-82), the L1 part still works."""
     import torch
