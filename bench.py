@@ -450,6 +450,36 @@ def train_rooflines(ctx, tr, cams, stage_ms):
     return {"roofline": roof, "kernels": kernels, "counts": counts}
 
 
+def backward_mode_times(ctx, tr, cams, targets, reps=5):
+    """One C3 view's render backward (K6 + FP64 fix-up + K7) in the three accumulation modes, CUDA
+    events on the launching stream: FP64 atomics (production), RGS_FLAG_REPRODUCIBLE, and
+    RGS_FLAG_DETERMINISTIC (the reference-order FP64 replay, per tile and per splat)."""
+    import torch
+
+    from paper_2402_03307_b200 import train
+
+    cam, tgt = cams[0], targets[0]
+    img, rec = ctx.render_forward_device(tr.scene, cam, retain=True)
+    dl = torch.zeros_like(img)
+    train.image_loss(ctx, img, tgt, 0.8 / 3, 0.2 / 3, dl, records=rec)
+    stream = torch.cuda.current_stream()
+    out = {}
+    for name, kw in (("atomic", {}), ("reproducible", {"reproducible": True}),
+                     ("deterministic_fp64", {"deterministic": True})):
+        ctx.render_backward_device(tr.scene, cam, rec, dl, **kw)  # warm
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            ctx.render_backward_device(tr.scene, cam, rec, dl, **kw)
+        b.record(stream)
+        torch.cuda.synchronize()
+        out[name] = a.elapsed_time(b) / reps
+    rec.close()
+    return out
+
+
 DROPIN_SO = os.path.join(ROOT, "tests", "cpp", "_build", "librgs_ref_dropin.so")
 
 
@@ -558,6 +588,22 @@ def run_train_leg(args, ctx, dev, dist, rank, world, flush):
     launches = ctx.kernel_launches - launches0
     its = args.train_steps / (ms / 1e3)
 
+    # the same steps with the bitwise-reproducible backward (RGS_FLAG_REPRODUCIBLE)
+    tr.reproducible = True
+    tr.step(*batch(0))
+    torch.cuda.synchronize(dev)
+    a2 = torch.cuda.Event(enable_timing=True)
+    b2 = torch.cuda.Event(enable_timing=True)
+    a2.record(stream)
+    for k in range(args.train_steps):
+        tr.step(*batch(args.warmup + k), read=False)
+    b2.record(stream)
+    torch.cuda.synchronize(dev)
+    tr.last_losses()
+    tr.reproducible = False
+    repro_its = args.train_steps / (max_over_ranks(a2.elapsed_time(b2), dist, dev) / 1e3)
+    backward_modes = backward_mode_times(ctx, tr, *batch(0))
+
     # per-stage breakdown of one step (serialised CUDA events on the launching stream)
     ctx.set_profiling(timing=True, count_evals=False)
     ctx.profile_reset()
@@ -644,6 +690,11 @@ def run_train_leg(args, ctx, dev, dist, rank, world, flush):
         "loss_first": first.total, "loss_last": last.total, "psnr_last": train.psnr_from_mse(last.mse),
         "knn_rebuild_ms": knn_ms, "stage_ms_one_step": stage_ms, "gpu_launches": launches,
         "roofline": train_roof["roofline"], "kernels": train_roof["kernels"], "workload_counts": train_roof["counts"],
+        "reproducible": {"value": repro_its, "unit": "it/s", "steps": args.train_steps,
+                         "note": "Trainer.reproducible: RGS_FLAG_REPRODUCIBLE backward (order-independent fixed-point "
+                                 "screen-gradient sums) + integer-count consistency gradient: bitwise identical "
+                                 "steps run to run"},
+        "backward_modes_ms_one_view": backward_modes,
         "e2e": e2e, "cpu_baseline": cpu, "dropin": dropin,
     }
 

@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(128) k_slice_cache(ParamView P, SliceCacheView
 // (rasterizer.cpp:189-204, gaussian.cpp:32-47, rasterizer.cpp:215-276, sh.cpp:16-97).
 // CACHED: the t-independent half of the slice and the opacity come from the batch's slice cache.
 template <bool F64, bool CACHED>
-__global__ void __launch_bounds__(128) k_preprocess(ParamView P, int sh_degree, DevCamera cam, SplatArrays out,
+__global__ void __launch_bounds__(128, CACHED ? 8 : 1) k_preprocess(ParamView P, int sh_degree, DevCamera cam, SplatArrays out,
                                                     BinState* st, SliceCacheView C) {
     using ShT = typename std::conditional<F64, double, float>::type;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;

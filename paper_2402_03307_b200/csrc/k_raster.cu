@@ -358,8 +358,9 @@ __global__ void __launch_bounds__(256, 5) k_blend_fp32(SplatArrays sp, const uin
             if (!done) {
                 const StagedSplat* const first = w_list[warp];
                 const StagedSplat* const end = first + __popc(m);
-                int lastq = -1, q = 0;
-                for (const StagedSplat* e = first; e != end; ++e, ++q) {
+                // the last blended entry, as a 32-bit shared-memory address (0: none in this window)
+                uint32_t last = 0;
+                for (const StagedSplat* e = first; e != end; ++e) {
                     const float4 a2 = e->a, b2 = e->b;
                     float p, M;
                     gate_values_x2(a2, b2, fp2, p, M);
@@ -380,7 +381,7 @@ __global__ void __launch_bounds__(256, 5) k_blend_fp32(SplatArrays sp, const uin
                         acc2 = fmaf(cc.z, w, acc2);
                         T = test_T;
                         errT3 = errN + 3e-7f;
-                        lastq = q;
+                        last = (uint32_t)__cvta_generic_to_shared(e);
                         if (COUNT) ++n_blend;
                         continue;
                     }
@@ -388,7 +389,7 @@ __global__ void __launch_bounds__(256, 5) k_blend_fp32(SplatArrays sp, const uin
                     // decision inside its error bound -> the pixel goes to the FP64 fix-up
                     if (!amb_gc && fmaf(test_T, errN, test_T) < kStopLo) {
                         done = stopped = true;
-                        if (COUNT) n_ref = start - rg.x + c + w_k[warp][q] + 1;
+                        if (COUNT) n_ref = start - rg.x + c + w_k[warp][e - first] + 1;
                         break;
                     }
                     if (COUNT) {
@@ -400,7 +401,10 @@ __global__ void __launch_bounds__(256, 5) k_blend_fp32(SplatArrays sp, const uin
                     slow = done = true;
                     break;
                 }
-                if (lastq >= 0) contrib = (int)(start - rg.x) + c + w_k[warp][lastq] + 1;
+                if (last) {
+                    const int lastq = (int)((last - (uint32_t)__cvta_generic_to_shared(first)) / sizeof(StagedSplat));
+                    contrib = (int)(start - rg.x) + c + w_k[warp][lastq] + 1;
+                }
             }
             __syncwarp();  // the list is rewritten by the next window
             if (__all_sync(kFull, done)) {
