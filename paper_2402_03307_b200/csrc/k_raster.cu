@@ -498,6 +498,7 @@ constexpr int kBwdPx = 2;  // pixels per lane, rows y + 4 i
 constexpr int kBwdThreads = kTilePixels / kBwdPx;
 constexpr int kBwdWarps = kBwdThreads / 32;
 
+template <bool FIXED>
 __global__ void __launch_bounds__(kBwdThreads) k_backward_fp32(SplatArrays sp, const uint32_t* __restrict__ vals,
                                                                 const uint2* __restrict__ ranges, DevCamera cam,
                                                                 float3 bg, const double* __restrict__ final_T,
@@ -604,7 +605,7 @@ __global__ void __launch_bounds__(kBwdThreads) k_backward_fp32(SplatArrays sp, c
 #pragma unroll
                     for (int q = 0; q < 9; ++q)
                         if (v[q] != 0.f) {
-                            if (sgx) fixed_add(sgx + 18 * sid + 2 * q, (double)v[q]);
+                            if (FIXED) fixed_add(sgx + 18 * sid + 2 * q, (double)v[q]);
                             else atomicAdd(o + q, (double)v[q]);
                         }
                 }
@@ -613,7 +614,7 @@ __global__ void __launch_bounds__(kBwdThreads) k_backward_fp32(SplatArrays sp, c
                 bool ok;
                 const float r = reduce_scatter9(v, lane, idx, ok);
                 if (ok && !(lane & 1) && r != 0.f) {
-                    if (sgx) fixed_add(sgx + 18 * sid + 2 * idx, (double)r);
+                    if (FIXED) fixed_add(sgx + 18 * sid + 2 * idx, (double)r);
                     else atomicAdd(o + idx, (double)r);
                 }
             }
@@ -661,8 +662,12 @@ void backward_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2
                    float3 bg, const double* final_T, const uint32_t* n_contrib, const float* dL_dimage,
                    double* screen_grads, cudaStream_t s, unsigned long long* screen_grads_fixed) {
     const int tiles = cam.tiles_x * cam.tiles_y;
-    k_backward_fp32<<<tiles, kBwdThreads, 0, s>>>(sp, pair_vals, ranges, cam, bg, final_T, n_contrib, dL_dimage,
-                                                  screen_grads, screen_grads_fixed);
+    if (screen_grads_fixed)
+        k_backward_fp32<true><<<tiles, kBwdThreads, 0, s>>>(sp, pair_vals, ranges, cam, bg, final_T, n_contrib,
+                                                            dL_dimage, screen_grads, screen_grads_fixed);
+    else
+        k_backward_fp32<false><<<tiles, kBwdThreads, 0, s>>>(sp, pair_vals, ranges, cam, bg, final_T, n_contrib,
+                                                             dL_dimage, screen_grads, nullptr);
 }
 
 }  // namespace rgs_launch
