@@ -447,6 +447,219 @@ __global__ void __launch_bounds__(256, 5) k_blend_fp32(SplatArrays sp, const uin
     }
 }
 
+// K5 (two pixels per lane): CTA of 128 threads per 16x16 tile, warp per 8x8 sub-tile, lane
+// pixels (x, y) and (x, y + 4) -- the sub-tiles and pixel pairs of K6, whose 8x8 cull is then
+// exactly this kernel's.  The two pixels share dx and every per-splat operand, so their gate
+// values are one set of paired FP32 instructions (bit-identical to gate_values); the accept path
+// runs for both whenever either accepts, and predicated selects keep a pixel that skipped,
+// finished or went slow unchanged.  Decisions per (pixel, splat) are those of k_blend_fp32.
+constexpr int kX2Threads = 128;
+constexpr int kX2Warps = kX2Threads / 32;
+constexpr int kX2Stage = 256;  // staged splats per batch (two per thread)
+
+template <bool FLOW, bool COUNT>
+__global__ void __launch_bounds__(kX2Threads, 8) k_blend_fp32_x2(SplatArrays sp, const uint32_t* __restrict__ vals,
+                                                              const uint2* __restrict__ ranges, DevCamera cam,
+                                                              float3 bg, float* __restrict__ image,
+                                                              double* __restrict__ final_T,
+                                                              uint32_t* __restrict__ n_contrib, uint32_t* slow_list,
+                                                              int* slow_count, unsigned long long* counters) {
+    __shared__ float4 s_a[kX2Stage], s_b[kX2Stage], s_c[kX2Stage], s_d[kX2Stage];
+    __shared__ float s_l[kX2Stage];
+    __shared__ StagedSplat w_list[kX2Warps][32];
+    __shared__ uint8_t w_k[kX2Warps][32];
+    const int tile = blockIdx.x;
+    const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sx0 = (warp & 1) * 8, sy0 = (warp >> 1) * 8;
+    const int lx = sx0 + (lane & 7), ly = sy0 + (lane >> 3);
+    const int px = tx * kTile + lx, py0 = ty * kTile + ly, py1 = py0 + 4;
+    const bool in0 = px < cam.width && py0 < cam.height, in1 = px < cam.width && py1 < cam.height;
+    const uint2 rg = ranges[tile];
+    const double px0 = tx * kTile, py0t = ty * kTile;
+    const float fpx = (float)lx, fsx0 = (float)sx0, fsy0 = (float)sy0;
+    const float2 fpy = make_float2((float)ly, (float)(ly + 4));
+    const unsigned lt_mask = (1u << lane) - 1u;
+
+    float2 T = make_float2(1.f, 1.f), errT3 = make_float2(3e-7f, 3e-7f);
+    float2 acc0 = make_float2(0.f, 0.f), acc1 = acc0, acc2 = acc0;  // channel c of pixels (0, 1)
+    int contrib0 = 0, contrib1 = 0;
+    bool done0 = !in0, done1 = !in1, slow0 = false, slow1 = false, stopped0 = false, stopped1 = false;
+    uint32_t n_eval = 0, n_blend = 0, n_ref0 = 0, n_ref1 = 0;  // COUNT only
+    bool warp_done = __all_sync(kFull, done0 && done1);
+
+    for (uint32_t start = rg.x; start < rg.y; start += kX2Stage) {
+        if (__syncthreads_count(done0 && done1) == kX2Threads) break;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int t = threadIdx.x + h * kX2Threads;
+            const uint32_t j = start + t;
+            if (j < rg.y) {
+                float4 A, Bv, C, Dv;
+                float l;
+                stage_values<FLOW>(sp, vals[j], px0, py0t, A, Bv, C, Dv, l);
+                s_a[t] = A;
+                s_b[t] = Bv;
+                s_c[t] = C;
+                s_d[t] = Dv;
+                s_l[t] = l;
+            }
+        }
+        __syncthreads();
+        const int n = (int)min((uint32_t)kX2Stage, rg.y - start);
+        if (warp_done) continue;
+        for (int c = 0; c < n; c += 32) {
+            const int k0 = c + lane;
+            bool surv = false;
+            float4 a, b, d;
+            if (k0 < n) {
+                a = s_a[k0];
+                b = s_b[k0];
+                d = s_d[k0];
+                surv = overlaps_v<7>(a, b, d, s_l[k0], fsx0, fsy0);
+            }
+            const unsigned m = __ballot_sync(kFull, surv);
+            if (surv) {
+                const int q = __popc(m & lt_mask);
+                StagedSplat* e = &w_list[warp][q];
+                e->a = a;
+                e->b = b;
+                e->c = s_c[k0];
+                e->d = d;
+                w_k[warp][q] = (uint8_t)lane;
+            }
+            __syncwarp();
+            if (!(done0 && done1)) {
+                const StagedSplat* const first = w_list[warp];
+                const StagedSplat* const end = first + __popc(m);
+                int last0 = -1, last1 = -1;
+                int q = 0;
+                for (const StagedSplat* e = first; e != end; ++e, ++q) {
+                    const float4 a2 = e->a, b2 = e->b;
+                    // gate_values for both pixels (shared dx, paired dy)
+                    const float dx = __fsub_rn(fpx, a2.x);
+                    const float2 dy = __fadd2_rn(fpy, make_float2(-a2.y, -a2.y));
+                    const float2 tv = __fmul2_rn(make_float2(a2.z, a2.w), make_float2(dx, dx));
+                    const float2 u = __fmul2_rn(make_float2(b2.x, b2.x), dy);
+                    const float2 q2 = __ffma2_rn(make_float2(tv.x, tv.x), make_float2(dx, dx), __fmul2_rn(u, dy));
+                    const float2 p = __ffma2_rn(make_float2(tv.y, tv.y), dy, q2);
+                    const float2 M = __ffma2_rn(make_float2(b2.w, b2.w), q2, make_float2(b2.y, b2.y));
+                    if (COUNT) n_eval += (done0 ? 0u : 1u) + (done1 ? 0u : 1u);
+                    const bool act0 = !done0 && !gate_skip(p.x, M.x, b2.z);
+                    const bool act1 = !done1 && !gate_skip(p.y, M.y, b2.z);
+                    if (!(act0 | act1)) continue;
+                    const float4 cc = e->c;
+                    const float2 pr = make_float2(e->d.z, e->d.w);  // (pc2, R)
+                    const float2 ex = make_float2(ex2_approx(p.x), ex2_approx(p.y));
+                    const float2 abx = __fmul2_rn(make_float2(cc.w, cc.w), ex);
+                    const float2 al = make_float2(fminf(0.99f, abx.x), fminf(0.99f, abx.y));
+                    const float2 test_T = __fmul2_rn(T, __fadd2_rn(make_float2(1.f, 1.f), make_float2(-al.x, -al.y)));
+                    const float2 errN = __ffma2_rn(__fmul2_rn(al, M), make_float2(pr.y, pr.y), errT3);
+                    const float2 lo = __ffma2_rn(make_float2(-test_T.x, -test_T.y), errN, test_T);
+                    const float2 pM = __fadd2_rn(p, M), pm = __fadd2_rn(p, make_float2(-M.x, -M.y));
+                    const bool amb0 = gate_ambiguous(p.x, M.x, b2.z) | ((pM.x >= pr.x) & (pm.x <= pr.x));
+                    const bool amb1 = gate_ambiguous(p.y, M.y, b2.z) | ((pM.y >= pr.x) & (pm.y <= pr.x));
+                    const bool bl0 = act0 & !amb0 & (lo.x > kStopHi);
+                    const bool bl1 = act1 & !amb1 & (lo.y > kStopHi);
+                    const float2 w = __fmul2_rn(al, T);
+                    const float2 wm = make_float2(bl0 ? w.x : 0.f, bl1 ? w.y : 0.f);
+                    acc0 = __ffma2_rn(make_float2(cc.x, cc.x), wm, acc0);
+                    acc1 = __ffma2_rn(make_float2(cc.y, cc.y), wm, acc1);
+                    acc2 = __ffma2_rn(make_float2(cc.z, cc.z), wm, acc2);
+                    const float2 eT3 = __fadd2_rn(errN, make_float2(3e-7f, 3e-7f));
+                    if (bl0) {
+                        T.x = test_T.x;
+                        errT3.x = eT3.x;
+                        last0 = q;
+                    }
+                    if (bl1) {
+                        T.y = test_T.y;
+                        errT3.y = eT3.y;
+                        last1 = q;
+                    }
+                    if (COUNT) n_blend += (bl0 ? 1u : 0u) + (bl1 ? 1u : 0u);
+                    if ((act0 & !bl0) | (act1 & !bl1)) {
+                        // rare: certainly stop (rasterizer.cpp:111, the splat is not blended), or
+                        // a decision inside its error bound -> the pixel goes to the FP64 fix-up
+                        const float2 hi = __ffma2_rn(test_T, errN, test_T);
+                        if (act0 & !bl0) {
+                            if (!amb0 && hi.x < kStopLo) {
+                                stopped0 = true;
+                                if (COUNT) n_ref0 = start - rg.x + c + w_k[warp][q] + 1;
+                            } else {
+                                slow0 = true;
+                                if (COUNT) {
+                                    const bool g = gate_ambiguous(p.x, M.x, b2.z);
+                                    atomicAdd(counters + (g ? ((p.x > -M.x) ? 3 : 4) : (amb0 ? 5 : 6)), 1ull);
+                                }
+                            }
+                            done0 = true;
+                        }
+                        if (act1 & !bl1) {
+                            if (!amb1 && hi.y < kStopLo) {
+                                stopped1 = true;
+                                if (COUNT) n_ref1 = start - rg.x + c + w_k[warp][q] + 1;
+                            } else {
+                                slow1 = true;
+                                if (COUNT) {
+                                    const bool g = gate_ambiguous(p.y, M.y, b2.z);
+                                    atomicAdd(counters + (g ? ((p.y > -M.y) ? 3 : 4) : (amb1 ? 5 : 6)), 1ull);
+                                }
+                            }
+                            done1 = true;
+                        }
+                        if (done0 && done1) break;
+                    }
+                }
+                if (last0 >= 0) contrib0 = (int)(start - rg.x) + c + w_k[warp][last0] + 1;
+                if (last1 >= 0) contrib1 = (int)(start - rg.x) + c + w_k[warp][last1] + 1;
+            }
+            __syncwarp();  // the list is rewritten by the next window
+            if (__all_sync(kFull, done0 && done1)) {
+                warp_done = true;
+                break;
+            }
+        }
+    }
+    if (COUNT) {
+        unsigned long long e = (in0 ? (stopped0 ? n_ref0 : rg.y - rg.x) : 0) +
+                               (in1 ? (stopped1 ? n_ref1 : rg.y - rg.x) : 0),
+                           b = n_blend, ke = n_eval;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            e += __shfl_xor_sync(kFull, e, o);
+            b += __shfl_xor_sync(kFull, b, o);
+            ke += __shfl_xor_sync(kFull, ke, o);
+        }
+        if (lane == 0) {
+            atomicAdd(counters + 0, e);
+            atomicAdd(counters + 1, b);
+            atomicAdd(counters + 2, ke);
+        }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        if (!(h ? in1 : in0)) continue;
+        const uint32_t pix = (uint32_t)(h ? py1 : py0) * cam.width + px;
+        if (h ? slow1 : slow0) {
+            slow_list[atomicAdd(slow_count, 1)] = pix;
+            continue;
+        }
+        const float Th = h ? T.y : T.x;
+        const float r = h ? acc0.y : acc0.x, g = h ? acc1.y : acc1.x, bb = h ? acc2.y : acc2.x;
+        if (FLOW) {
+            image[(size_t)pix * 2 + 0] = r;
+            image[(size_t)pix * 2 + 1] = g;
+        } else {
+            image[(size_t)pix * 3 + 0] = fmaf(Th, bg.x, r);
+            image[(size_t)pix * 3 + 1] = fmaf(Th, bg.y, g);
+            image[(size_t)pix * 3 + 2] = fmaf(Th, bg.z, bb);
+            final_T[pix] = (double)Th;
+            n_contrib[pix] = (uint32_t)(h ? contrib1 : contrib0);
+        }
+    }
+}
+
 // Reduce-scatter of 9 per-lane partials across the warp (butterfly, 12 shuffles instead of
 // 9 x 5): at each level the lanes split their remaining slots in two halves, keep one half
 // and receive the partner's contribution to it.  Afterwards lane pairs (l, l^1) hold the
@@ -645,6 +858,17 @@ void blend_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* r
                                                       slow_list, slow_count, counters);
     if (g_k5_variant == 1) {
         RGS_K5_LAUNCH(k_blend_fp32_v1)
+    } else if (g_k5_variant == 3) {
+        if (flow_mode)
+            k_blend_fp32_x2<true, false><<<tiles, kX2Threads, 0, s>>>(sp, pair_vals, ranges, cam, bg, image, final_T,
+                                                                      n_contrib, slow_list, slow_count, counters);
+        else if (counters)
+            k_blend_fp32_x2<false, true><<<tiles, kX2Threads, 0, s>>>(sp, pair_vals, ranges, cam, bg, image, final_T,
+                                                                      n_contrib, slow_list, slow_count, counters);
+        else
+            k_blend_fp32_x2<false, false><<<tiles, kX2Threads, 0, s>>>(sp, pair_vals, ranges, cam, bg, image,
+                                                                       final_T, n_contrib, slow_list, slow_count,
+                                                                       counters);
     } else {
         RGS_K5_LAUNCH(k_blend_fp32)
     }
@@ -654,7 +878,7 @@ void blend_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* r
 // Per-device kernel attributes (called from rgs_ctx_create on the context's device).
 bool raster_init() {
     const char* v = std::getenv("RGS_K5");
-    g_k5_variant = (v && v[0] == '1') ? 1 : 2;
+    g_k5_variant = (v && (v[0] == '1' || v[0] == '3')) ? v[0] - '0' : 2;
     return true;
 }
 
