@@ -450,6 +450,33 @@ def train_rooflines(ctx, tr, cams, stage_ms):
     return {"roofline": roof, "kernels": kernels, "counts": counts}
 
 
+def f64_scene_its(ctx, store, cfg, batch, args, dist, dev, steps=5):
+    """Training it/s of the C3 step on an FP64 device scene (the store's doubles and FP64 Adam
+    moments, as the reference keeps them)."""
+    import torch
+
+    from paper_2402_03307_b200 import rgs, train
+
+    sc = rgs.DeviceScene.from_store(ctx, store, f64=True)
+    tr = train.Trainer(ctx, sc, cfg, dist, start_step=TRAIN_START_STEP)
+    for k in range(2):
+        tr.step(*batch(k))
+    stream = torch.cuda.current_stream(dev)
+    torch.cuda.synchronize(dev)
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for k in range(steps):
+        tr.step(*batch(2 + k), read=False)
+    b.record(stream)
+    torch.cuda.synchronize(dev)
+    tr.last_losses()
+    its = steps / (max_over_ranks(a.elapsed_time(b), dist, dev) / 1e3)
+    tr = None
+    sc.close()
+    return its
+
+
 def backward_mode_times(ctx, tr, cams, targets, reps=5):
     """One C3 view's render backward (K6 + FP64 fix-up + K7) in the three accumulation modes, CUDA
     events on the launching stream: FP64 atomics (production), RGS_FLAG_REPRODUCIBLE, and
@@ -603,6 +630,7 @@ def run_train_leg(args, ctx, dev, dist, rank, world, flush):
     tr.reproducible = False
     repro_its = args.train_steps / (max_over_ranks(a2.elapsed_time(b2), dist, dev) / 1e3)
     backward_modes = backward_mode_times(ctx, tr, *batch(0))
+    f64_its = f64_scene_its(ctx, store, cfg, batch, args, dist, dev)
 
     # per-stage breakdown of one step (serialised CUDA events on the launching stream)
     ctx.set_profiling(timing=True, count_evals=False)
@@ -695,6 +723,9 @@ def run_train_leg(args, ctx, dev, dist, rank, world, flush):
                                  "screen-gradient sums) + integer-count consistency gradient: bitwise identical "
                                  "steps run to run"},
         "backward_modes_ms_one_view": backward_modes,
+        "f64_scene": {"value": f64_its, "unit": "it/s",
+                      "note": "the same step on an FP64 device scene (RGS_SCENE_F64: the reference's doubles "
+                              "unrounded; parameters and Adam moments in FP64)"},
         "e2e": e2e, "cpu_baseline": cpu, "dropin": dropin,
     }
 
