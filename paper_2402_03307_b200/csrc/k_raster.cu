@@ -47,9 +47,11 @@ __device__ __forceinline__ void stage_values(const SplatArrays& sp, uint32_t id,
     } else {
         C = make_float4(col.x, col.y, col.z, cf.w);
     }
-    // 1 / (1 - alpha) <= 1 / (1 - min(0.99, ab)): the T-gate error bound without a reciprocal
+    // The T-gate's per-blend error growth alpha ln2 M / (1 - alpha) (M bounds the error of the
+    // log2 power, so ln2 M bounds the relative error of alpha), with 1 / (1 - alpha) <=
+    // 1 / (1 - min(0.99, ab)): R = ln2 / (1 - min(0.99, ab)), rounded up; no reciprocal per pixel.
     const float am = fminf(0.99f, cf.w);
-    Dv = make_float4(e.x, e.y, g.y, __fdiv_ru(1.f, __fsub_rd(1.f, am)) * 1.000001f);
+    Dv = make_float4(e.x, e.y, g.y, __fdiv_ru(1.f, __fsub_rd(1.f, am)) * (0.6931472f * 1.000001f));
     // Largest eigenvalue of the (negative definite) log2-power form [[ca2, cb2/2], [cb2/2, cc2]]
     // plus a slack far above its FP32 rounding: p2 <= lmax d^2 at Euclidean distance d from
     // the mean.  Near-degenerate conics get lmax >= 0 (no culling from it).
