@@ -365,7 +365,9 @@ def allreduce_kind(world):
         return "none (one rank)"
     if os.environ.get("RGS_NATIVE_ALLREDUCE") == "1":
         return "rgs_allreduce_grads: one NCCL group (grads|vnorm, visible, image losses) on the context stream"
-    return "torch.distributed NCCL all-reduce x3 (grads|vnorm, visible, image losses)"
+    import torch.distributed as dist
+
+    return f"torch.distributed {dist.get_backend()} all-reduce x3 (grads|vnorm, visible, image losses)"
 
 
 def measured_peaks(ctx):
