@@ -1046,9 +1046,12 @@ int adam_blocks(int n) { return nblk(n, 128); }
 }  // namespace rgs_launch
 namespace rgs_dev {
 __global__ void k_l1_ties(const float* __restrict__ img, const float* __restrict__ tgt, int npix, float eps,
-                          uint32_t* list, int* count) {
+                          const uint32_t* __restrict__ n_contrib, uint32_t* list, int* count) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= npix) return;
+    // a pixel no splat reached is the background in both precisions (n_contrib = 0, not slow;
+    // n_contrib is NULL when the background is not float32-exact): nothing to re-decide
+    if (n_contrib && n_contrib[i] == 0u) return;
     bool tie = false;
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) tie |= fabsf(img[3 * (size_t)i + ch] - tgt[3 * (size_t)i + ch]) <= eps;
@@ -1070,8 +1073,9 @@ __global__ void k_l1_sign_clear(const uint32_t* __restrict__ list, const int* __
 }
 }  // namespace rgs_dev
 namespace rgs_launch {
-void l1_ties(const float* img, const float* tgt, int npix, float eps, uint32_t* list, int* count, cudaStream_t s) {
-    if (npix > 0) k_l1_ties<<<nblk(npix, 256), 256, 0, s>>>(img, tgt, npix, eps, list, count);
+void l1_ties(const float* img, const float* tgt, int npix, float eps, const uint32_t* n_contrib, uint32_t* list,
+             int* count, cudaStream_t s) {
+    if (npix > 0) k_l1_ties<<<nblk(npix, 256), 256, 0, s>>>(img, tgt, npix, eps, n_contrib, list, count);
 }
 void l1_sign_set(const uint32_t* list, const int* count, int max_items, const double* img64, const float* tgt,
                  int8_t* sign, cudaStream_t s) {

@@ -1633,8 +1633,10 @@ int rgs_image_loss_ex(rgs_ctx* c, const rgs_records* rec, const float* rendered,
                 CK(cudaMemsetAsync(ts.l1_sign.p, 0, ts.l1_sign.bytes, s));
             }
             CK(cudaMemsetAsync(ts.tie_count.p, 0, sizeof(int), s));
-            rgs_launch::l1_ties(rendered, target, (int)npix, kL1Tie, ts.tie_list.as<uint32_t>(), ts.tie_count.as<int>(),
-                                s);
+            const bool bg_exact = (double)(float)f.bg[0] == f.bg[0] && (double)(float)f.bg[1] == f.bg[1] &&
+                                  (double)(float)f.bg[2] == f.bg[2];
+            rgs_launch::l1_ties(rendered, target, (int)npix, kL1Tie, bg_exact ? f.n_contrib.as<uint32_t>() : nullptr,
+                                ts.tie_list.as<uint32_t>(), ts.tie_count.as<int>(), s);
             DevCamera dc{};
             dc.width = f.width;
             dc.height = f.height;

@@ -55,7 +55,8 @@ void adam_step(bool f64, void* params, void* m1, void* m2, const float* grads, c
 int adam_blocks(int n);
 // L1 near-tie re-decision (rgs_image_loss_ex): pixels with |rendered - target| <= eps in some
 // channel -> list; after their FP64 recompute (blend_fp64_pixels into img64), the FP64 signs.
-void l1_ties(const float* img, const float* tgt, int npix, float eps, uint32_t* list, int* count, cudaStream_t s);
+void l1_ties(const float* img, const float* tgt, int npix, float eps, const uint32_t* n_contrib, uint32_t* list,
+             int* count, cudaStream_t s);
 void l1_sign_set(const uint32_t* list, const int* count, int max_items, const double* img64, const float* tgt,
                  int8_t* sign, cudaStream_t s);
 void l1_sign_clear(const uint32_t* list, const int* count, int max_items, int8_t* sign, cudaStream_t s);
