@@ -734,13 +734,13 @@ __global__ void __launch_bounds__(kBwdThreads) k_backward_fp32(SplatArrays sp, c
     StagedSplat* sm = smw[warp];
     float* slm = slmw[warp];
 
+    static_assert(kBwdPx == 2, "the replay pairs the lane's two pixels");
     int contrib[kBwdPx];
-    float fpy[kBwdPx], T_run[kBwdPx], g0[kBwdPx], g1[kBwdPx], g2[kBwdPx], S[kBwdPx];
+    float T_run[kBwdPx], g0[kBwdPx], g1[kBwdPx], g2[kBwdPx], S[kBwdPx];
     int cmax = 0;
 #pragma unroll
     for (int h = 0; h < kBwdPx; ++h) {
         const int px = tx * kTile + lx, py = ty * kTile + ly + 4 * h;
-        fpy[h] = (float)(ly + 4 * h);
         contrib[h] = 0;
         T_run[h] = 1.f;
         g0[h] = g1[h] = g2[h] = S[h] = 0.f;
@@ -759,6 +759,9 @@ __global__ void __launch_bounds__(kBwdThreads) k_backward_fp32(SplatArrays sp, c
         }
         cmax = max(cmax, contrib[h]);
     }
+    const float2 fpy2 = make_float2((float)ly, (float)(ly + 4));
+    float2 T_run2 = make_float2(T_run[0], T_run[1]), S2 = make_float2(S[0], S[1]);
+    const float2 g0_2 = make_float2(g0[0], g0[1]), g1_2 = make_float2(g1[0], g1[1]), g2_2 = make_float2(g2[0], g2[1]);
     const int wmax = __reduce_max_sync(kFull, cmax);
 
     for (int end = wmax; end > 0; end -= 32) {
@@ -775,41 +778,66 @@ __global__ void __launch_bounds__(kBwdThreads) k_backward_fp32(SplatArrays sp, c
         while (mask) {
             const int k = 31 - __clz(mask);
             mask &= ~(1u << k);
-            float v[9];
-#pragma unroll
-            for (int q = 0; q < 9; ++q) v[q] = 0.f;
-            bool act = false;
+            // The lane's two pixels (rows y and y + 4) share dx and every per-splat operand: their
+            // gate values and replay arithmetic are paired FP32 instructions (FADD2 / FMUL2 /
+            // FFMA2); gate_values' operations, so K5's decisions are replayed exactly.  A pixel that
+            // does not accept this splat contributes zero through masked weights.
             const float4 a = sm[k].a, b = sm[k].b;
-#pragma unroll
-            for (int h = 0; h < kBwdPx; ++h) {
-                if (beg + k >= contrib[h]) continue;
-                float p, M, dx, dy;
-                if (classify(a, b, fpx, fpy[h], p, M, dx, dy) != kAccept) continue;
+            const float dx = __fsub_rn(fpx, a.x);
+            const float2 dy = __fadd2_rn(fpy2, make_float2(-a.y, -a.y));
+            const float2 tv = __fmul2_rn(make_float2(a.z, a.w), make_float2(dx, dx));
+            const float2 u = __fmul2_rn(make_float2(b.x, b.x), dy);
+            const float2 q2 = __ffma2_rn(make_float2(tv.x, tv.x), make_float2(dx, dx), __fmul2_rn(u, dy));
+            const float2 p = __ffma2_rn(make_float2(tv.y, tv.y), dy, q2);
+            const float2 M = __ffma2_rn(make_float2(b.w, b.w), q2, make_float2(b.y, b.y));
+            // classify(...) == kAccept: neither a certain skip nor ambiguous
+            const bool acc0 = beg + k < contrib[0] && !gate_skip(p.x, M.x, b.z) && !gate_ambiguous(p.x, M.x, b.z);
+            const bool acc1 = beg + k < contrib[1] && !gate_skip(p.y, M.y, b.z) && !gate_ambiguous(p.y, M.y, b.z);
+            const bool act = acc0 | acc1;
+            float v[9];
+            if (act) {
                 const float4 cc = sm[k].c;
-                const float e = ex2_approx(p);
-                const float al = fminf(0.99f, __fmul_rn(cc.w, e));
-                const float om = 1.f - al;
-                const float inv_om = rcp_approx(om);
-                const float T_before = T_run[h] * inv_om;
-                const float w = al * T_before;
-                v[0] = fmaf(w, g0[h], v[0]);
-                v[1] = fmaf(w, g1[h], v[1]);
-                v[2] = fmaf(w, g2[h], v[2]);
-                const float G = fmaf(g0[h], cc.x, fmaf(g1[h], cc.y, g2[h] * cc.z));
-                const float dL_da = fmaf(T_before, G, -S[h] * inv_om);
-                if (p <= sm[k].d.z) {  // unclamped alpha <= 0.99: al = ab * e
-                    const float A = -2.f * kLn2 * a.z, B = -kLn2 * a.w, C = -2.f * kLn2 * b.x;
-                    v[8] = fmaf(dL_da, e, v[8]);
-                    const float dp = dL_da * al;
-                    v[3] = fmaf(dp, -0.5f * dx * dx, v[3]);
-                    v[4] = fmaf(dp, -dx * dy, v[4]);
-                    v[5] = fmaf(dp, -0.5f * dy * dy, v[5]);
-                    v[6] = fmaf(dp, fmaf(A, dx, B * dy), v[6]);
-                    v[7] = fmaf(dp, fmaf(B, dx, C * dy), v[7]);
-                }
-                S[h] = fmaf(w, G, S[h]);
-                T_run[h] = T_before;
-                act = true;
+                const float2 e = make_float2(ex2_approx(p.x), ex2_approx(p.y));
+                const float2 abx = __fmul2_rn(make_float2(cc.w, cc.w), e);
+                const float2 al = make_float2(fminf(0.99f, abx.x), fminf(0.99f, abx.y));
+                const float2 om = __fadd2_rn(make_float2(1.f, 1.f), make_float2(-al.x, -al.y));
+                const float2 inv_om = make_float2(rcp_approx(om.x), rcp_approx(om.y));
+                const float2 Tb = __fmul2_rn(T_run2, inv_om);
+                const float2 w = __fmul2_rn(al, Tb);
+                const float2 wm = make_float2(acc0 ? w.x : 0.f, acc1 ? w.y : 0.f);
+                const float2 V0 = __fmul2_rn(wm, g0_2), V1 = __fmul2_rn(wm, g1_2), V2 = __fmul2_rn(wm, g2_2);
+                const float2 G = __ffma2_rn(g0_2, make_float2(cc.x, cc.x),
+                                            __ffma2_rn(g1_2, make_float2(cc.y, cc.y),
+                                                       __fmul2_rn(g2_2, make_float2(cc.z, cc.z))));
+                const float2 dL_da = __ffma2_rn(Tb, G, __fmul2_rn(make_float2(-S2.x, -S2.y), inv_om));
+                // unclamped alpha <= 0.99 (al = ab * e): the conic / mean / alpha_base terms
+                const float pc2 = sm[k].d.z;
+                const float2 dam = make_float2(acc0 && p.x <= pc2 ? dL_da.x : 0.f, acc1 && p.y <= pc2 ? dL_da.y : 0.f);
+                const float A = -2.f * kLn2 * a.z, B = -kLn2 * a.w, C = -2.f * kLn2 * b.x;
+                const float2 dp = __fmul2_rn(dam, al);
+                const float2 V8 = __fmul2_rn(dam, e);
+                const float2 V3 = __fmul2_rn(dp, make_float2(-0.5f * dx * dx, -0.5f * dx * dx));
+                const float2 V4 = __fmul2_rn(dp, __fmul2_rn(make_float2(-dx, -dx), dy));
+                const float2 V5 = __fmul2_rn(dp, __fmul2_rn(__fmul2_rn(make_float2(-0.5f, -0.5f), dy), dy));
+                const float2 V6 = __fmul2_rn(dp, __ffma2_rn(make_float2(A, A), make_float2(dx, dx),
+                                                             __fmul2_rn(make_float2(B, B), dy)));
+                const float2 V7 = __fmul2_rn(dp, __ffma2_rn(make_float2(B, B), make_float2(dx, dx),
+                                                             __fmul2_rn(make_float2(C, C), dy)));
+                v[0] = V0.x + V0.y;
+                v[1] = V1.x + V1.y;
+                v[2] = V2.x + V2.y;
+                v[3] = V3.x + V3.y;
+                v[4] = V4.x + V4.y;
+                v[5] = V5.x + V5.y;
+                v[6] = V6.x + V6.y;
+                v[7] = V7.x + V7.y;
+                v[8] = V8.x + V8.y;
+                S2 = __ffma2_rn(wm, G, S2);
+                if (acc0) T_run2.x = Tb.x;
+                if (acc1) T_run2.y = Tb.y;
+            } else {
+#pragma unroll
+                for (int q = 0; q < 9; ++q) v[q] = 0.f;
             }
             const unsigned am = __ballot_sync(kFull, act);
             if (am == 0) continue;
