@@ -147,6 +147,19 @@ __global__ void __launch_bounds__(128, CACHED ? 8 : 1) k_preprocess(ParamView P,
     uint32_t ntiles = 0;
     unsigned long long key = ~0ull;
     if (i < P.n) {
+        if (CACHED) {
+            // The SH blocks are read only after the projection (by the splats that survive it):
+            // start them towards L1 now, so their latency overlaps the FP64 chain.
+            const int deg = sh_degree < 0 ? 0 : (sh_degree > 3 ? 3 : sh_degree);
+            const int nblk = (3 * (deg + 1) * (deg + 1) + 3) / 4;
+#pragma unroll
+            for (int b = 0; b < 12; ++b) {
+                if (b >= nblk) break;
+                const void* a = F64 ? (const void*)(P.base64 + 4 * ((size_t)(4 + b) * P.n + i))
+                                    : (const void*)(P.base + 4 * ((size_t)(4 + b) * P.n + i));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
+            }
+        }
         double mean4[4];
         ld_block<F64>(P, 0, i, mean4);
         SliceState s;
