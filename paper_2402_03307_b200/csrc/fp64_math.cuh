@@ -258,6 +258,50 @@ __device__ __forceinline__ void d_sh_basis(const double* dir, int degree, double
     }
 }
 
+// Basis entry k of d_sh_basis (the same expression; k a compile-time constant in unrolled loops,
+// so a caller can compute each entry where it is used instead of keeping all 16 live).
+template <int K>
+__device__ __forceinline__ double d_sh_basis_k(double x, double y, double z, double xx, double yy, double zz) {
+    if constexpr (K == 0) return kC0;
+    else if constexpr (K == 1) return -kC1 * y;
+    else if constexpr (K == 2) return kC1 * z;
+    else if constexpr (K == 3) return -kC1 * x;
+    else if constexpr (K == 4) return kC2_0 * x * y;
+    else if constexpr (K == 5) return kC2_1 * y * z;
+    else if constexpr (K == 6) return kC2_2 * (2 * zz - xx - yy);
+    else if constexpr (K == 7) return kC2_3 * x * z;
+    else if constexpr (K == 8) return kC2_4 * (xx - yy);
+    else if constexpr (K == 9) return kC3_0 * y * (3 * xx - yy);
+    else if constexpr (K == 10) return kC3_1 * x * y * z;
+    else if constexpr (K == 11) return kC3_2 * y * (4 * zz - xx - yy);
+    else if constexpr (K == 12) return kC3_3 * z * (2 * zz - 3 * xx - 3 * yy);
+    else if constexpr (K == 13) return kC3_4 * x * (4 * zz - xx - yy);
+    else if constexpr (K == 14) return kC3_5 * z * (xx - yy);
+    else return kC3_6 * x * (xx - 3 * yy);
+}
+
+__device__ __forceinline__ double d_sh_basis_at(int k, double x, double y, double z, double xx, double yy,
+                                                double zz) {
+    switch (k) {
+        case 0: return d_sh_basis_k<0>(x, y, z, xx, yy, zz);
+        case 1: return d_sh_basis_k<1>(x, y, z, xx, yy, zz);
+        case 2: return d_sh_basis_k<2>(x, y, z, xx, yy, zz);
+        case 3: return d_sh_basis_k<3>(x, y, z, xx, yy, zz);
+        case 4: return d_sh_basis_k<4>(x, y, z, xx, yy, zz);
+        case 5: return d_sh_basis_k<5>(x, y, z, xx, yy, zz);
+        case 6: return d_sh_basis_k<6>(x, y, z, xx, yy, zz);
+        case 7: return d_sh_basis_k<7>(x, y, z, xx, yy, zz);
+        case 8: return d_sh_basis_k<8>(x, y, z, xx, yy, zz);
+        case 9: return d_sh_basis_k<9>(x, y, z, xx, yy, zz);
+        case 10: return d_sh_basis_k<10>(x, y, z, xx, yy, zz);
+        case 11: return d_sh_basis_k<11>(x, y, z, xx, yy, zz);
+        case 12: return d_sh_basis_k<12>(x, y, z, xx, yy, zz);
+        case 13: return d_sh_basis_k<13>(x, y, z, xx, yy, zz);
+        case 14: return d_sh_basis_k<14>(x, y, z, xx, yy, zz);
+        default: return d_sh_basis_k<15>(x, y, z, xx, yy, zz);
+    }
+}
+
 // sh.cpp:40-83 (direction gradient, 16x3 row-major; entries beyond degree zero).
 __device__ __forceinline__ void d_sh_basis_grad(const double* dir, int degree, double* g) {
     const double x = dir[0], y = dir[1], z = dir[2];

@@ -194,13 +194,14 @@ __global__ void __launch_bounds__(128, CACHED ? 8 : 1) k_preprocess(ParamView P,
             ProjState o;
             if (!(s.lambda * dt * dt > kVisibility) && d_project_geom<CACHED>(s, cam, op, o)) {
                 ok = true;
-                double basis[16];
-                d_sh_basis(o.dir, sh_degree, basis);
                 const int deg = sh_degree < 0 ? 0 : (sh_degree > 3 ? 3 : sh_degree);
                 const int K = (deg + 1) * (deg + 1);
                 const int nblk = (3 * K + 3) / 4;
                 // colour = sh . basis + 0.5 per channel (rasterizer.cpp:245-257): the SH blocks are
-                // streamed (coefficient j = 3k + ch), each channel still summed in increasing k
+                // streamed (coefficient j = 3k + ch), each channel still summed in increasing k, and
+                // each basis entry (sh.cpp:16-85's expression) computed where it is used
+                const double x = o.dir[0], y = o.dir[1], z = o.dir[2];
+                const double xx = x * x, yy = y * y, zz = z * z;
                 double col[3];
 #pragma unroll
                 for (int b = 0; b < 12; ++b) {
@@ -210,8 +211,8 @@ __global__ void __launch_bounds__(128, CACHED ? 8 : 1) k_preprocess(ParamView P,
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
                             const int j = 4 * b + e, k = j / 3, ch = j % 3;
-                            if (k == 0) col[ch] = (double)v[e] * basis[0];
-                            else if (k < K) col[ch] += (double)v[e] * basis[k];
+                            if (k == 0) col[ch] = (double)v[e] * kC0;
+                            else if (k < K) col[ch] += (double)v[e] * d_sh_basis_at(k, x, y, z, xx, yy, zz);
                         }
                     }
                 }
