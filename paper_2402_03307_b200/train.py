@@ -548,8 +548,12 @@ class Trainer:
         w = self.cfg.loss
         ctx, scene = self.ctx, self.scene
         ctx.fence()
-        self.gbuf.zero_()
-        self.visible.zero_()
+        # The first view's backward writes every Gaussian's gradients, norm and visible count
+        # (accumulate=False), so the gradient buffers are only zeroed when no backward runs.
+        first_writes = want_grads and len(cams) > 0
+        if not first_writes:
+            self.gbuf.zero_()
+            self.visible.zero_()
         self.losses.zero_()
         inv_b = 1.0 / (len(cams) * self.world) if cams else 0.0
         wl1, wss = (1 - w.lambda_ssim) * inv_b, w.lambda_ssim * inv_b
@@ -561,11 +565,12 @@ class Trainer:
         # previous step (its Adam update of the scene) and of the buffer zeroing above
         start = main.record_event() if overlap else None
         free = [start] * self.n_slots
-        # On one rank the consistency term (it depends on the scene only) runs first, on the main
-        # stream, beside the first view's forward on the side stream; with N ranks it is added
-        # after the all-reduce (it is a once-per-step term of the replicated scene).
+        # On one rank the consistency term (it depends on the scene only) runs on the main stream
+        # right after the first view's backward (which initialises the gradients), beside the
+        # next view's forward on the side stream; with N ranks it is added after the all-reduce
+        # (it is a once-per-step term of the replicated scene).
         early_consistency = self.world == 1
-        if early_consistency:
+        if early_consistency and not first_writes:
             self._consistency(want_grads, defer)
         recs = []
         loss_done = None  # the previous view's image loss (its scratch and the loss slots are shared)
@@ -594,8 +599,10 @@ class Trainer:
                 image_loss(ctx, img, tgt, wl1, wss, dl if want_grads else None, self.losses, loss_scale=inv_b,
                            accumulate=True, records=rec if want_grads else None)
             if want_grads:
-                ctx.render_backward_device(scene, cam, rec, dl, self.grads, self.vnorm, self.visible, accumulate=True,
+                ctx.render_backward_device(scene, cam, rec, dl, self.grads, self.vnorm, self.visible, accumulate=v > 0,
                                            reproducible=self.reproducible)
+                if v == 0 and early_consistency:
+                    self._consistency(want_grads, defer)
             if overlap:
                 free[slot] = main.record_event()
             recs.append(rec)
