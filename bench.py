@@ -433,6 +433,8 @@ def train_rooflines(ctx, tr, cams, stage_ms):
         "adam_k9": ("hbm", 1828 * n / 1e9, hbm, "1828 B per Gaussian (65 x (4 grad + 24 param/m/v) + 8)"),
         "consistency_k10": ("hbm", (260 * n + 24 * n * (k + 2)) / 1e9, hbm, "260 N + 24 N (k + 2) B"),
         "tile_radix_sort_k4": ("hbm", 2 * 20 * n_pairs / 1e9, hbm, "2 passes x 20 B per pair"),
+        "tile_scatter_k4": ("hbm", (4 * n_pairs + 16 * n_vis) / 1e9, hbm,
+                            "16 B per visible splat read, 4 B per pair written"),
     }
     kernels = {}
     for name, (bound, work, peak, what) in spec.items():
@@ -832,6 +834,30 @@ def run_ours(args, rank, local_rank, world):
     stages, _ = ctx.profile_read()
     ctx.set_profiling(timing=False, count_evals=False)
 
+    # ---- the other binning (DESIGN.md §3 "Binning"): the batch uses the radix passes; the
+    # tile-major scatter (the single-view default) measured on the same sweep -- serialised
+    # stage times and one live sweep
+    ctx.set_binning("scatter")
+    ctx.set_profiling(timing=True, count_evals=False)
+    ctx.profile_reset()
+    torch.cuda.synchronize(dev)
+    flush.zero_()
+    sweep()
+    torch.cuda.synchronize(dev)
+    stages_sc, _ = ctx.profile_read()
+    ctx.set_profiling(timing=False, count_evals=False)
+    sc_ms = []
+    for _ in range(2):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        sweep()
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        sc_ms.append(a.elapsed_time(b))
+    ctx.set_binning("auto")
+
     # ---- workload counters (untimed extra sweep): E, B, splats, pairs
     ctx.set_profiling(timing=False, count_evals=True)
     ctx.profile_reset()
@@ -888,6 +914,26 @@ def run_ours(args, rank, local_rank, world):
                   "ms_per_launch": live_ms, "ms_per_launch_serialised": per_stage["blend_fp32_k5"]["ms_per_frame"],
                   "timing": f"CUDA events around each of the {k5_live_n} K5 launches of the timed region, on "
                             "its own stream (views pipelined over 8 streams, so it shares the GPU)"})
+    # binning, both ways (per frame, serialised; depth ranks included)
+    def _bin(st, names):
+        return {k: st[k][0] / n_frames_rank for k in names if k in st and st[k][1]}
+
+    b_radix = _bin(stages, ("depth_rank", "pair_offsets_scan", "duplicate_k3", "tile_radix_sort_k4"))
+    b_scat = _bin(stages_sc, ("depth_rank", "tile_counts", "tile_scatter_k4"))
+    sc_fps = N_TIMES / (min(sc_ms) / 1e3)
+    t_scat = b_scat.get("tile_scatter_k4", 0.0)
+    binning = {
+        "batch_uses": "radix (RGS_BINNING_AUTO)",
+        "radix": {"stages_ms_per_frame": b_radix, "total_ms_per_frame": sum(b_radix.values()), "fps_live": fps},
+        "scatter": {"stages_ms_per_frame": b_scat, "total_ms_per_frame": sum(b_scat.values()),
+                    "fps_live": sc_fps,
+                    # algorithmic bytes of the scatter kernel: rect + id + tile count per visible
+                    # splat read, one 4-byte splat id per pair written
+                    "tile_scatter_k4_hbm_frac": ((4 * n_pairs + 16 * n_vis) / (t_scat / 1e3)) / 1e9 / hbm_peak
+                    if t_scat else None},
+        "note": "same per-tile lists; the scatter has the shorter serialised path (single views: training, "
+                "drop-in), the radix passes overlap the blends of the other views in flight better (batch)",
+    }
     dominant = max(per_stage, key=lambda k: per_stage[k]["share"]) if per_stage else None
     traffic = None
     try:
@@ -972,7 +1018,7 @@ def run_ours(args, rank, local_rank, world):
                        "kernel_evals_per_frame": E_kernel / N_TIMES,
                        "slow_pixel_reasons_per_sweep": slow_reasons},
             "ms_per_frame": total_ms / (N_TIMES * args.steps), "wall_s": t_wall,
-            "target_fps": 600, "roofline": roofline, "kernels": roof_all, "stages": per_stage,
+            "target_fps": 600, "roofline": roofline, "kernels": roof_all, "stages": per_stage, "binning": binning,
             "stages_note": "per-stage CUDA events from a serialised profiling sweep after the timed region "
                            "(the timed sweeps pipeline 8 views over 8 streams, so stages overlap there)",
             "fp32_peak_tflops": fp32_peak, "clocks": clocks, "gpu_launches": launches,

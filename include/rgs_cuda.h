@@ -119,6 +119,21 @@ int rgs_ctx_synchronize(rgs_ctx* ctx);
 /* Count of kernels this context launched since creation (bench evidence). */
 long long rgs_ctx_kernel_launches(const rgs_ctx* ctx);
 
+/* ---------------------------------------------------------------- binning */
+/* How a view's (tile, splat) pairs are put into per-tile (depth, index) order -- the result is
+ * identical (bin_and_sort, rasterizer.cpp:57-74), the cost profile differs:
+ *   RGS_BINNING_RADIX:   pairs emitted in depth-rank order, then stable LSD byte passes by tile;
+ *   RGS_BINNING_SCATTER: per-chunk tile counts, then every pair written at its final position
+ *                        (images up to 256 x 256 and 8192 tiles; larger ones use the radix passes);
+ *   RGS_BINNING_AUTO:    the scatter for single views (shorter critical path: training, drop-in),
+ *                        the radix passes for the views of rgs_render_views / rgs_render_batch
+ *                        (several views in flight: they overlap the other views' blends better).
+ * The default comes from the environment variable RGS_BINNING=auto|radix|scatter (auto if unset). */
+#define RGS_BINNING_AUTO 0
+#define RGS_BINNING_RADIX 1
+#define RGS_BINNING_SCATTER 2
+int rgs_ctx_set_binning(rgs_ctx* ctx, int mode);
+
 /* ---------------------------------------------------------------- profiling */
 /* Per-stage CUDA-event timing on the launching stream and counting of evaluated / blended
  * (pixel, splat) pairs in the FP32 blend (count_evals != 0; the E and B of the blend roofline).

@@ -7,7 +7,9 @@
 //      top bits of key - min_key, 2^18 buckets); every bucket is then sorted by the
 //      exact (64-bit depth key, source index) -- insertion sort per bucket, shared-memory
 //      bitonic for rare large buckets.  sorted_ids[r] = splat of rank r.
-//   2. Duplicate-with-key in rank order: an exclusive scan of tiles-touched over the
+//   2. Up to 256 x 256 (and 8192) tiles: the tile-major scatter below writes every pair at its
+//      final place directly.  Larger images take steps 2' and 3:
+//   2'. Duplicate-with-key in rank order: an exclusive scan of tiles-touched over the
 //      ranks gives each splat its pair offset; warps emit the (tile, splat) pairs of 32
 //      consecutive ranks cooperatively (coalesced stores).
 //   3. LSD radix sort of the pairs on the packed key (ty << 8 | tx), as two stable 8-bit
@@ -566,6 +568,339 @@ __global__ void __launch_bounds__(256) k_digit_hist3(const uint32_t* __restrict_
         if ((&h[0][0])[e]) atomicAdd(&hist[e], (&h[0][0])[e]);
 }
 
+// --------------------------------------------------------------------------- tile-major scatter
+// For images up to 256 x 256 tiles and kScatterMaxTiles tiles the pairs are not materialised and
+// sorted at all: every (tile, splat) pair is written straight to its final position
+//
+//     pos(r, t) = start(t) + #{ r' < r : rect(r') contains t }
+//
+// (r = depth rank), which is exactly the reference's per-tile (depth, index) order.  The count is
+// split three ways:
+//   A  k_chunk_tile_counts -- per chunk of 32 * rounds consecutive ranks, the pair count of every
+//      tile (row difference arrays in shared memory, a warp scan per tile row);
+//   B  k_tile_offsets      -- per tile, the exclusive prefix of those counts over the chunks plus
+//      the tile's start (an exclusive scan of the tile totals: decoupled look-back over groups of
+//      32 tiles), in place; the tile ranges and the pair count;
+//   C  k_tile_scatter      -- per chunk, rounds of 32 ranks: lane masks per tile column and tile row
+//      (which of the round's 32 rectangles cover it; prefix-OR of begin / end marks), so a pair's
+//      offset inside the round is popc(col_mask & row_mask & lanes below); a per-tile running
+//      position in shared memory carries the rounds.  Tile row ty belongs to warp ty % 4 of the
+//      block, so the running positions need no atomics and no cross-warp ordering.
+// Traffic: rect + id + count per visible splat, 4 B per pair written, and the chunk x tile count
+// matrix (written by A, read and rewritten by B, read by C) -- against 2 x 16 B per pair for the
+// two radix passes plus 8 B per pair of K3.
+constexpr int kScatWarps = 4;
+constexpr int kScatThreads = 32 * kScatWarps;
+constexpr int kScatterMaxTiles = 8192;
+constexpr int kOffThreads = 512;  // k_tile_offsets: 16 warps share the chunks of 32 tiles
+constexpr uint32_t kRunMask = (1u << 26) - 1u;  // k_tile_scatter: positions < 2^26, 6-bit round stamp
+static int g_scatter_rounds = 16;
+// 0: the scatter for single views, the radix passes for multi-view batches;
+// 1: radix passes only; 2: the scatter wherever it applies (RGS_BINNING=auto|radix|scatter)
+static int g_binning_mode = 0;
+
+__global__ void __launch_bounds__(256) k_chunk_tile_counts(const uint32_t* __restrict__ sorted_ids,
+                                                           const uint32_t* __restrict__ sorted_tiles,
+                                                           const ushort4* __restrict__ rect,
+                                                           const BinState* __restrict__ st, int chunk, int tiles_x,
+                                                           int tiles_y, uint32_t* counts) {
+    extern __shared__ int s_diff[];  // tiles_y rows of tiles_x + 1
+    const int W = tiles_x + 1;
+    const int nv = st->n_valid;
+    const int r0 = blockIdx.x * chunk;
+    if (r0 >= nv) return;
+    for (int e = threadIdx.x; e < tiles_y * W; e += blockDim.x) s_diff[e] = 0;
+    __syncthreads();
+    const int r1 = min(r0 + chunk, nv);
+    for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+        if (!sorted_tiles[r]) continue;
+        const ushort4 q = rect[sorted_ids[r]];
+        for (int y = q.z; y <= q.w; ++y) {
+            atomicAdd(&s_diff[y * W + q.x], 1);
+            atomicAdd(&s_diff[y * W + q.y + 1], -1);
+        }
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    uint32_t* out = counts + (size_t)blockIdx.x * tiles_x * tiles_y;
+    for (int y = threadIdx.x >> 5; y < tiles_y; y += nw) {
+        int carry = 0;
+        for (int x0 = 0; x0 < tiles_x; x0 += 32) {
+            const int x = x0 + lane;
+            int v = x < tiles_x ? s_diff[y * W + x] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u = __shfl_up_sync(kFullMask, v, o);
+                if (lane >= o) v += u;
+            }
+            v += carry;
+            if (x < tiles_x) out[y * tiles_x + x] = (uint32_t)v;
+            carry = __shfl_sync(kFullMask, v, 31);
+        }
+    }
+}
+
+// B: per tile, the exclusive prefix of its counts over the chunks (in place) and its total; a
+// block takes 32 tiles (lanes) and its 16 warps split the chunks into segments.  The last block to
+// finish (the completion counter BinState::tile_blocks_done, reset by frame_init) turns the totals into the
+// tile starts (exclusive scan, in place), the tile ranges and the pair count.
+__global__ void __launch_bounds__(kOffThreads) k_tile_offsets(uint32_t* counts, BinState* st, int chunk, int n_tiles,
+                                                              uint32_t* totals_starts, uint2* ranges) {
+    constexpr int kW = kOffThreads / 32;
+    __shared__ uint32_t seg[kW][32];
+    __shared__ bool s_last;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int t = blockIdx.x * 32 + lane;
+    const int nch = (st->n_valid + chunk - 1) / chunk;
+    const int per = (nch + kW - 1) / kW;
+    const int c0 = min(w * per, nch), c1 = min(c0 + per, nch);
+    uint32_t s = 0;
+    if (t < n_tiles) {
+#pragma unroll 8
+        for (int c = c0; c < c1; ++c) s += counts[(size_t)c * n_tiles + t];
+    }
+    seg[w][lane] = s;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t tot = 0;
+#pragma unroll
+        for (int k = 0; k < kW; ++k) {
+            const uint32_t v = seg[k][lane];
+            seg[k][lane] = tot;
+            tot += v;
+        }
+        if (t < n_tiles) totals_starts[t] = tot;
+    }
+    __syncthreads();
+    if (t < n_tiles) {
+        uint32_t run = seg[w][lane];
+#pragma unroll 8
+        for (int c = c0; c < c1; ++c) {
+            const size_t e = (size_t)c * n_tiles + t;
+            const uint32_t v = counts[e];
+            counts[e] = run;
+            run += v;
+        }
+    }
+    // last block: tile starts
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(&st->tile_blocks_done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    constexpr int kItems = kScatterMaxTiles / kOffThreads;
+    volatile const uint32_t* tv = totals_starts;
+    uint32_t v[kItems];
+    uint32_t sum = 0;
+    const int base = threadIdx.x * kItems;
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+        v[k] = base + k < n_tiles ? tv[base + k] : 0u;
+        sum += v[k];
+    }
+    uint32_t total;
+    uint32_t run = block_exclusive_scan(sum, &total);
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+        if (base + k < n_tiles) {
+            totals_starts[base + k] = run;
+            ranges[base + k] = make_uint2(run, run + v[k]);
+        }
+        run += v[k];
+    }
+    if (threadIdx.x == 0) st->n_pairs = total;
+}
+
+// Lane masks of one round: col[x] = lanes whose rectangle spans column x, row[y] likewise.  Begin
+// marks go into col / row directly, end marks (x1 + 1) into the warp's scratch, then an inclusive
+// prefix-OR of both along the axis: covered = begun & ~ended.
+__device__ __forceinline__ void scatter_axis_masks(uint32_t* m, uint32_t* f, int n, int lo, int hi, bool valid,
+                                                   int lane) {
+    for (int e = lane; e <= n; e += 32) {
+        if (e < n) m[e] = 0;
+        f[e] = 0;
+    }
+    __syncwarp();
+    if (valid) {
+        atomicOr(&m[lo], 1u << lane);
+        atomicOr(&f[hi + 1], 1u << lane);
+    }
+    __syncwarp();
+    uint32_t cb = 0, cf = 0;
+    for (int x0 = 0; x0 < n; x0 += 32) {
+        const int x = x0 + lane;
+        uint32_t b = x < n ? m[x] : 0u, e = x < n ? f[x] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t ub = __shfl_up_sync(kFullMask, b, o), ue = __shfl_up_sync(kFullMask, e, o);
+            if (lane >= o) {
+                b |= ub;
+                e |= ue;
+            }
+        }
+        b |= cb;
+        e |= cf;
+        if (x < n) m[x] = b & ~e;
+        cb = __shfl_sync(kFullMask, b, 31);
+        cf = __shfl_sync(kFullMask, e, 31);
+    }
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(kScatThreads) k_tile_scatter(const uint32_t* __restrict__ sorted_ids,
+                                                               const uint32_t* __restrict__ sorted_tiles,
+                                                               const ushort4* __restrict__ rect,
+                                                               BinState* st, int rounds,
+                                                               int tiles_x, int tiles_y,
+                                                               const uint32_t* __restrict__ base,
+                                                               const uint32_t* __restrict__ starts, uint2* ranges,
+                                                               uint32_t* vals) {
+    extern __shared__ uint32_t s_scat[];
+    const int n_tiles = tiles_x * tiles_y;
+    const int chunk = 32 * rounds;
+    uint32_t* run = s_scat;                                     // n_tiles running positions
+    uint32_t* s_id = run + ((n_tiles + 1) & ~1);               // chunk splat ids
+    ushort4* s_rect = reinterpret_cast<ushort4*>(s_id + chunk);  // chunk rectangles (x1 < x0: none)
+    uint32_t* s_col = reinterpret_cast<uint32_t*>(s_rect + chunk);  // kScatWarps slots x 256
+    uint32_t* s_row = s_col + kScatWarps * 256;                     // kScatWarps slots x 256
+    uint32_t* s_end = s_row + kScatWarps * 256;                     // per warp 2 x 257 end marks
+    if (st->overflow || st->n_pairs > kRunMask) {
+        // the view is re-rendered (beyond 2^26 pairs: by the radix passes): no tile ranges into
+        // the unwritten pairs
+        if (blockIdx.x == 0 && threadIdx.x == 0) st->overflow = 1;
+        for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n_tiles; e += gridDim.x * blockDim.x)
+            ranges[e] = make_uint2(0, 0);
+        return;
+    }
+    const int nv = st->n_valid;
+    const int r0 = blockIdx.x * chunk;
+    if (r0 >= nv) return;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    // running positions: tile start + the chunk's prefix; stamp 63 (no round yet)
+    const uint32_t* b = base + (size_t)blockIdx.x * n_tiles;
+    if ((n_tiles & 3) == 0) {
+        const uint4* b4 = reinterpret_cast<const uint4*>(b);
+        const uint4* s4 = reinterpret_cast<const uint4*>(starts);
+        uint4* r4 = reinterpret_cast<uint4*>(run);
+        for (int e = threadIdx.x; e < (n_tiles >> 2); e += kScatThreads) {
+            const uint4 x = b4[e], y = s4[e];
+            r4[e] = make_uint4((63u << 26) | (x.x + y.x), (63u << 26) | (x.y + y.y), (63u << 26) | (x.z + y.z),
+                               (63u << 26) | (x.w + y.w));
+        }
+    } else {
+        for (int e = threadIdx.x; e < n_tiles; e += kScatThreads) run[e] = (63u << 26) | (b[e] + starts[e]);
+    }
+    const int n_here = min(chunk, nv - r0);
+    const int nr = (n_here + 31) >> 5;
+    for (int i = threadIdx.x; i < nr * 32; i += kScatThreads) {
+        const int r = r0 + i;
+        ushort4 q = make_ushort4(1, 0, 0, 0);
+        uint32_t id = 0;
+        if (i < n_here && sorted_tiles[r]) {
+            id = sorted_ids[r];
+            q = rect[id];
+        }
+        s_id[i] = id;
+        s_rect[i] = q;
+    }
+    __syncthreads();
+    uint32_t* endx = s_end + w * 514;
+    uint32_t* endy = endx + 257;
+    for (int g = 0; g < nr; g += kScatWarps) {
+        // warp w builds the masks of round g + w into slot w
+        if (g + w < nr) {
+            const ushort4 q = s_rect[(g + w) * 32 + lane];
+            const bool valid = q.x <= q.y;
+            scatter_axis_masks(s_col + w * 256, endx, tiles_x, q.x, q.y, valid, lane);
+            scatter_axis_masks(s_row + w * 256, endy, tiles_y, q.z, q.w, valid, lane);
+        }
+        __syncthreads();
+        const int kr = min(kScatWarps, nr - g);
+        for (int k = 0; k < kr; ++k) {
+            const int i = (g + k) * 32 + lane;
+            const ushort4 q = s_rect[i];
+            const bool valid = q.x <= q.y;
+            // rows of this warp's band inside the rectangle: y = first, first + 4, ... <= y1
+            const int first = q.z + ((w - q.z) & (kScatWarps - 1));
+            const int nb = valid && first <= q.w ? ((q.w - first) >> 2) + 1 : 0;
+            const int wd = q.y - q.x + 1;
+            const uint32_t cnt = nb ? (uint32_t)(wd * nb) : 0u;
+            uint32_t incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t u = __shfl_up_sync(kFullMask, incl, o);
+                if (lane >= o) incl += u;
+            }
+            const uint32_t total = __shfl_sync(kFullMask, incl, 31);
+            const uint32_t excl = incl - cnt;
+            if (total == 0) continue;
+            const uint32_t nonempty = __ballot_sync(kFullMask, cnt != 0);  // rectangles with band rows
+            const uint32_t* cm = s_col + k * 256;
+            const uint32_t* rm = s_row + k * 256;
+            const int ri = g + k;  // round index inside the chunk: the running positions' stamp
+            // Lane L takes the contiguous pairs [L per, (L + 1) per) of the round and walks them:
+            // one owner search and one division per lane, then column / band-row / owner steps.
+            const uint32_t per = (total + 31) >> 5;
+            uint32_t kk = lane * per;
+            int o = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const uint32_t v = __shfl_sync(kFullMask, incl, o + step - 1);
+                if (v <= kk) o += step;
+            }
+            const uint32_t o_excl = __shfl_sync(kFullMask, excl, o & 31);
+            int tx = 0, ty = 0, x0 = 0, x1 = -1, y1 = -1;
+            uint32_t id = 0;
+            if (kk < total) {
+                const ushort4 oq = s_rect[(g + k) * 32 + o];
+                const int ofirst = oq.z + ((w - oq.z) & (kScatWarps - 1));
+                const int owd = oq.y - oq.x + 1;
+                const int m = (int)(kk - o_excl);
+                // m / owd: m < 2^14, owd <= 256 -- (m + 0.5) / owd is >= 0.5 / owd from an integer
+                const int dy = (int)__fdividef((float)m + 0.5f, (float)owd);
+                x0 = oq.x;
+                x1 = oq.y;
+                y1 = oq.w;
+                tx = x0 + (m - dy * owd);
+                ty = ofirst + kScatWarps * dy;
+                id = s_id[(g + k) * 32 + o];
+            }
+            for (uint32_t j = 0; j < per; ++j, ++kk) {
+                if (kk >= total) break;
+                const int t = ty * tiles_x + tx;
+                const uint32_t mask = cm[tx] & rm[ty];
+                const uint32_t c = __popc(mask);
+                // run[t] = stamp << 26 | position; stamped with this round, it already includes
+                // the round's pairs of tile t (its last rectangle has been processed)
+                const uint32_t v = run[t];
+                const uint32_t p0 = (v & kRunMask) - ((int)(v >> 26) == ri ? c : 0u);
+                vals[p0 + __popc(mask & ((1u << o) - 1u))] = id;
+                if (!(mask & ~((2u << o) - 1u))) run[t] = ((uint32_t)ri << 26) | (p0 + c);
+                // next pair: next column, next band row, next rectangle with rows in the band
+                if (++tx > x1) {
+                    tx = x0;
+                    ty += kScatWarps;
+                    if (ty > y1) {
+                        const uint32_t later = nonempty & ~((2u << o) - 1u);
+                        if (later) {
+                            o = __ffs(later) - 1;
+                            const ushort4 oq = s_rect[(g + k) * 32 + o];
+                            x0 = tx = oq.x;
+                            x1 = oq.y;
+                            ty = oq.z + ((w - oq.z) & (kScatWarps - 1));
+                            y1 = oq.w;
+                            id = s_id[(g + k) * 32 + o];
+                        }
+                    }
+                }
+            }
+            __syncwarp();  // the round's running positions, before the next round reads them
+        }
+        __syncthreads();
+    }
+}
+
 // RGS_FLAG_DEFER_CHECKS: the view's rotor error / pair-buffer overflow into the context's
 // deferred status word (min wins: the lowest failing index, as the synchronous check).
 __global__ void k_fold_status(const BinState* st, unsigned long long* word, unsigned long long overflow_word) {
@@ -590,7 +925,7 @@ __global__ void k_frame_init(BinState* st, uint32_t pair_cap, uint32_t* bucket_c
         z.pair_cap = pair_cap;
         z.n_pairs_eff = 0;
         z.overflow = 0;
-        z.pad2 = z.pad3 = 0;
+        z.tile_blocks_done = z.pad3 = 0;
         *st = z;
     }
     if (i < nb) {
@@ -760,11 +1095,52 @@ void frame_init(BinState* st, uint32_t pair_cap, uint32_t* bucket_count, uint32_
     k_frame_init<<<blocks(kNumBuckets, 256), 256, 0, s>>>(st, pair_cap, bucket_count, bucket_cur, kNumBuckets);
 }
 
+// ---- tile-major scatter (k_chunk_tile_counts, k_tile_offsets, k_tile_scatter)
+static int scatter_chunk() { return 32 * g_scatter_rounds; }
+static size_t scatter_smem(int n_tiles) {
+    const int chunk = scatter_chunk();
+    return 4 * ((size_t)((n_tiles + 1) & ~1) + chunk + 2 * (size_t)chunk + 2 * kScatWarps * 256 + kScatWarps * 514);
+}
+size_t tile_count_words(int n, int n_tiles) {
+    return (size_t)blocks(std::max(n, 1), scatter_chunk()) * (size_t)std::max(n_tiles, 1);
+}
+int default_binning_mode() { return g_binning_mode; }
+bool tile_scatter_usable(int tiles_x, int tiles_y, int n, long long pair_cap, bool batch, int mode) {
+    if (mode == 1 || (batch && mode == 0)) return false;
+    return pair_cap <= (long long)kRunMask && tiles_x <= 256 && tiles_y <= 256 && tiles_x * tiles_y <= kScatterMaxTiles &&
+           tile_count_words(n, tiles_x * tiles_y) <= ((size_t)1 << 26);
+}
+
+void tile_counts(const uint32_t* sorted_ids, const uint32_t* sorted_tiles, const ushort4* rect, BinState* st, int n,
+                 int tiles_x, int tiles_y, uint32_t* counts, uint32_t* starts, uint2* ranges, cudaStream_t s) {
+    const int chunk = scatter_chunk();
+    const int n_tiles = tiles_x * tiles_y;
+    k_chunk_tile_counts<<<blocks(std::max(n, 1), chunk), 256, 4 * (size_t)tiles_y * (tiles_x + 1), s>>>(
+        sorted_ids, sorted_tiles, rect, st, chunk, tiles_x, tiles_y, counts);
+    k_tile_offsets<<<blocks(n_tiles, 32), kOffThreads, 0, s>>>(counts, st, chunk, n_tiles, starts, ranges);
+}
+
+void tile_scatter(const uint32_t* sorted_ids, const uint32_t* sorted_tiles, const ushort4* rect, BinState* st,
+                  int n, int tiles_x, int tiles_y, const uint32_t* counts, const uint32_t* starts, uint2* ranges,
+                  uint32_t* vals, cudaStream_t s) {
+    k_tile_scatter<<<blocks(std::max(n, 1), scatter_chunk()), kScatThreads, scatter_smem(tiles_x * tiles_y), s>>>(
+        sorted_ids, sorted_tiles, rect, st, g_scatter_rounds, tiles_x, tiles_y, counts, starts, ranges, vals);
+}
+
 bool binning_init() {
     const char* v = std::getenv("RGS_RADIX");
     g_radix_rounds = (v && v[0] == '8') ? 8 : 16;
+    const char* b = std::getenv("RGS_BINNING");
+    g_binning_mode = !b ? 0 : (b[0] == 'r' ? 1 : (b[0] == 's' ? 2 : 0));
+    const char* r = std::getenv("RGS_SCATTER_ROUNDS");
+    if (r) {
+        const int k = std::atoi(r);
+        if (k == 8 || k == 16 || k == 32) g_scatter_rounds = k;
+    }
     return cudaFuncSetAttribute(k_bucket_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                kBigSmem * (int)sizeof(SortRec)) == cudaSuccess;
+                                kBigSmem * (int)sizeof(SortRec)) == cudaSuccess &&
+           cudaFuncSetAttribute(k_tile_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)scatter_smem(kScatterMaxTiles)) == cudaSuccess;
 }
 
 }  // namespace rgs_launch

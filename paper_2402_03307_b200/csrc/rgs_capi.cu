@@ -3,11 +3,12 @@
 //
 // Forward pipeline per view (render_forward, rasterizer.cpp:308-318):
 //   K1 preprocess (FP64)  -> per-Gaussian splat records, tile rects, depth keys
-//   depth sort            -> splat order by (depth, index)       [stable radix sort]
-//   counts + scan         -> pair offsets in depth order
-//   duplicate-with-key    -> (tile, splat) pairs in depth order
-//   stable sort by tile   -> per-tile lists in (depth, index) order == bin_and_sort
-//   tile ranges           -> [begin, end) per tile
+//   depth ranks           -> splat order by (depth, index)
+//   tile-major scatter    -> per-chunk tile counts, tile ranges [begin, end), then every
+//                            (tile, splat) pair written at its place in the per-tile
+//                            (depth, index) order == bin_and_sort
+//   (images beyond 256 x 256 / 8192 tiles: pair offsets, duplicate-with-key, stable LSD
+//    radix passes by tile, tile ranges)
 //   K5 FP32 blend         -> image, final_T, n_contrib, slow-pixel list
 //   FP64 fix-up           -> slow pixels recomputed exactly
 #include <cuda_runtime.h>
@@ -71,6 +72,7 @@ struct Frame {
     DevBuf bucket_count, bucket_off, bucket_cur, big_list, big_scratch;
     // tiles / pairs / pixels: pairs ping-pong between (keys_a, pair_vals_buf) and (keys_b, vals_b)
     DevBuf ranges, keys_a, pair_vals_buf, keys_b, vals_b, radix_counts, radix_offsets;
+    DevBuf tile_counts;  // tile-major scatter: chunk x tile pair counts, then absolute positions
     DevBuf final_T, n_contrib, slow_list;
     DevBuf stats;  // BinState
     DevBuf scan_tmp;
@@ -103,6 +105,10 @@ struct Frame {
         return a;
     }
     const uint32_t* pair_vals() const { return pair_vals_buf.as<uint32_t>(); }
+    // tile-major scatter: the tile starts follow the chunk x tile matrix (16-byte aligned)
+    uint32_t* tile_starts(int ntiles, int n) const {
+        return tile_counts.as<uint32_t>() + ((rgs_launch::tile_count_words(n, ntiles) + 3) & ~size_t(3));
+    }
     BinState* dstats() const { return stats.as<BinState>(); }
 
     void ensure_gaussians(int cap, cudaStream_t s) {
@@ -142,10 +148,11 @@ struct Frame {
         const size_t nt = (size_t)std::max(ntiles, 1) + 1;
         ranges.ensure(8 * nt, s);
     }
-    void ensure_pairs(long long p, cudaStream_t s) {
+    void ensure_pairs(long long p, bool radix, cudaStream_t s) {
         size_t p1 = (size_t)std::max<long long>(p, 1);
-        keys_a.ensure(4 * p1, s);
         pair_vals_buf.ensure(4 * p1, s);
+        if (!radix) return;  // the tile-major scatter writes the sorted splat ids only
+        keys_a.ensure(4 * p1, s);
         keys_b.ensure(4 * p1, s);
         vals_b.ensure(4 * p1, s);
         const size_t e = rgs_launch::radix_count_entries(p);
@@ -157,7 +164,8 @@ struct Frame {
         DevBuf* all[] = {&valid, &tiles, &mean2, &conic_ab, &color_depth, &flow_radius, &rect, &conic_f,
                          &color_f, &guard_f, &ext_f, &src, &key, &dir_dist, &ent_key, &ent_id, &sorted_ids, &sorted_tiles,
                          &pair_off, &bucket_count, &bucket_off, &bucket_cur, &big_list, &big_scratch, &ranges,
-                         &keys_a, &pair_vals_buf, &keys_b, &vals_b, &radix_counts, &radix_offsets, &final_T,
+                         &keys_a, &pair_vals_buf, &keys_b, &vals_b, &radix_counts, &radix_offsets, &tile_counts,
+                         &final_T,
                          &n_contrib, &slow_list, &stats, &scan_tmp, &tmp_img};
         for (DevBuf* b : all) b->release(s);
         if (host_stats) {
@@ -174,12 +182,13 @@ struct Frame {
 // Pipeline stages timed by the profiling mode (rgs_ctx_set_profiling).
 enum Stage {
     kStPreprocess = 0, kStDepthRank, kStHist, kStTileFill, kStTileSort, kStBlend, kStFixup, kStBwdTiles,
-    kStBwdFixup, kStBwdGauss, kStBwdColor, kStImageLoss, kStAdam, kStConsistency, kNumStages
+    kStBwdFixup, kStBwdGauss, kStBwdColor, kStImageLoss, kStAdam, kStConsistency, kStTileCounts, kStTileScatter,
+    kNumStages
 };
 static const char* kStageNames[kNumStages] = {
     "preprocess_k1", "depth_rank", "pair_offsets_scan", "duplicate_k3", "tile_radix_sort_k4", "blend_fp32_k5",
     "blend_fp64_fixup", "backward_tiles_k6", "backward_fp64_fixup", "backward_gauss_k7b", "backward_color_k7a",
-    "image_loss_k8", "adam_k9", "consistency_k10"};
+    "image_loss_k8", "adam_k9", "consistency_k10", "tile_counts", "tile_scatter_k4"};
 
 struct rgs_records;
 struct rgs_ctx {
@@ -204,6 +213,7 @@ struct rgs_ctx {
     BinState* host_stats = nullptr;  // pinned
     // profiling: CUDA events around every stage, on the launching stream
     int timing = 0;  // 1: all stages, serialised views; 2: live K5 timing (see rgs_ctx_set_profiling)
+    int binning_mode = 0;  // RGS_BINNING_* (rgs_ctx_set_binning)
     bool count_evals = false;
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
@@ -416,7 +426,7 @@ namespace {
 int run_forward(rgs_ctx* ctx, Frame& f, cudaStream_t s, Source src, const rgs_scene* scene, const void* dev_splats,
                 int n_splats, bool splats_monotone, const rgs_camera* cam, const double bg[3], unsigned flags,
                 float* image, bool flow_mode, bool sync, BinState* host_stats,
-                const SliceCacheView* slice_cache = nullptr, bool render_only = false) {
+                const SliceCacheView* slice_cache = nullptr, bool render_only = false, bool batch = false) {
     const DevCamera dc = make_dev_camera(cam);
     const int n = src == kFromScene ? scene->n : n_splats;
     const size_t npix = (size_t)cam->width * cam->height;
@@ -435,6 +445,11 @@ int run_forward(rgs_ctx* ctx, Frame& f, cudaStream_t s, Source src, const rgs_sc
     f.have_src = src == kFromSplats;  // frames are recycled between scene and splat renders
     if (f.have_src) f.src.ensure(4 * (size_t)std::max(n, 1), s);
     const int nb = rgs_launch::num_depth_buckets();
+    // Binning: the tile-major scatter (up to 256 x 256 and 8192 tiles) for single views -- the
+    // shorter critical path; K3 + the radix passes for the views of a batch, which overlap the
+    // blends of the other views in flight better ("Binning").
+    const bool scatter =
+        rgs_launch::tile_scatter_usable(dc.tiles_x, dc.tiles_y, n, f.pair_cap, batch, ctx->binning_mode);
     rgs_launch::frame_init(f.dstats(), (uint32_t)std::min<long long>(f.pair_cap, 0xffffffffll),
                            f.bucket_count.as<uint32_t>(), f.bucket_cur.as<uint32_t>(), s);
     ctx->launches += 1;
@@ -471,8 +486,16 @@ int run_forward(rgs_ctx* ctx, Frame& f, cudaStream_t s, Source src, const rgs_sc
                                 f.big_list.as<uint32_t>(), f.big_scratch.p, s);
         ctx->launches += 6;
     }
-    // Pair offsets in rank order (exclusive scan of tiles-touched; total = pair count).
-    {
+    if (scatter) {
+        // Per-chunk tile counts -> absolute positions, tile ranges and the pair count.
+        StageTimer t(ctx, kStTileCounts, s);
+        f.tile_counts.ensure(4 * (rgs_launch::tile_count_words(n, ntiles) + ntiles + 4), s);
+        rgs_launch::tile_counts(f.sorted_ids.as<uint32_t>(), f.sorted_tiles.as<uint32_t>(), sa.rect, st_dev, n,
+                                dc.tiles_x, dc.tiles_y, f.tile_counts.as<uint32_t>(), f.tile_starts(ntiles, n),
+                                f.ranges.as<uint2>(), s);
+        ctx->launches += 3;
+    } else {
+        // Pair offsets in rank order (exclusive scan of tiles-touched; total = pair count).
         StageTimer t(ctx, kStHist, s);
         rgs_launch::exclusive_scan_1p(f.sorted_tiles.as<uint32_t>(), n, f.pair_off.as<uint32_t>(), scan_tmp + 4096,
                                    &st_dev->n_pairs, s, &st_dev->n_valid);
@@ -487,20 +510,26 @@ int run_forward(rgs_ctx* ctx, Frame& f, cudaStream_t s, Source src, const rgs_sc
         CK(cudaMemcpyAsync(&st_dev->pair_cap, &cap, sizeof cap, cudaMemcpyHostToDevice, s));
         CK(cudaStreamSynchronize(s));
     }
-    f.ensure_pairs(f.pair_cap, s);
+    f.ensure_pairs(f.pair_cap, !scatter, s);
     rgs_launch::check_capacity(st_dev, s);
     ctx->launches += 1;
 
-    // Duplicate-with-key in rank order, then the two stable tile-digit passes.
-    {
-        StageTimer t(ctx, kStTileFill, s);
-        // scan_tmp is free again after the pair-offset scan: it holds the digit histograms
-        rgs_launch::duplicate(f.sorted_ids.as<uint32_t>(), f.pair_off.as<uint32_t>(), f.sorted_tiles.as<uint32_t>(),
-                              sa.rect, st_dev, n, dc.tiles_x, dc.tiles_y, f.keys_a.as<uint32_t>(),
-                              f.pair_vals_buf.as<uint32_t>(), f.scan_tmp.as<int>(), s);
+    if (scatter) {
+        StageTimer t(ctx, kStTileScatter, s);
+        rgs_launch::tile_scatter(f.sorted_ids.as<uint32_t>(), f.sorted_tiles.as<uint32_t>(), sa.rect, st_dev, n,
+                                 dc.tiles_x, dc.tiles_y, f.tile_counts.as<uint32_t>(), f.tile_starts(ntiles, n),
+                                 f.ranges.as<uint2>(), f.pair_vals_buf.as<uint32_t>(), s);
         ctx->launches += 1;
-    }
-    {
+    } else {
+        // Duplicate-with-key in rank order, then the two stable tile-digit passes.
+        {
+            StageTimer t(ctx, kStTileFill, s);
+            // scan_tmp is free again after the pair-offset scan: it holds the digit histograms
+            rgs_launch::duplicate(f.sorted_ids.as<uint32_t>(), f.pair_off.as<uint32_t>(),
+                                  f.sorted_tiles.as<uint32_t>(), sa.rect, st_dev, n, dc.tiles_x, dc.tiles_y,
+                                  f.keys_a.as<uint32_t>(), f.pair_vals_buf.as<uint32_t>(), f.scan_tmp.as<int>(), s);
+            ctx->launches += 1;
+        }
         StageTimer t(ctx, kStTileSort, s);
         const int in_b = rgs_launch::tile_radix_sort(
             f.keys_a.as<uint32_t>(), f.pair_vals_buf.as<uint32_t>(), f.keys_b.as<uint32_t>(), f.vals_b.as<uint32_t>(),
@@ -535,6 +564,7 @@ int run_forward(rgs_ctx* ctx, Frame& f, cudaStream_t s, Source src, const rgs_sc
                                make_float3((float)f.bg[0], (float)f.bg[1], (float)f.bg[2]), flow_mode ? 1 : 0,
                                image32, fT, nc, f.slow_list.as<uint32_t>(), slow_count, counters, s);
         ctx->launches += 1;
+
     }
     {
         StageTimer t(ctx, kStFixup, s);
@@ -557,7 +587,7 @@ int run_forward(rgs_ctx* ctx, Frame& f, cudaStream_t s, Source src, const rgs_sc
     if (st.overflow) {
         f.pair_cap = (long long)st.n_pairs * 5 / 4 + 1024;
         return run_forward(ctx, f, s, src, scene, dev_splats, n_splats, splats_monotone, cam, bg, flags, image,
-                           flow_mode, true, host_stats, slice_cache, render_only);
+                           flow_mode, true, host_stats, slice_cache, render_only, batch);
     }
     f.n_valid = st.n_valid;
     f.n_pairs = st.n_pairs;
@@ -612,6 +642,7 @@ int rgs_ctx_create(int device, rgs_ctx** out) {
         }
         CK(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
         if (!rgs_launch::binning_init()) throw CudaError{cudaErrorInvalidValue, "binning_init"};
+        c->binning_mode = rgs_launch::default_binning_mode();
         if (!rgs_launch::raster_init()) throw CudaError{cudaErrorInvalidValue, "raster_init"};
         if (!rgs_launch::train_init()) throw CudaError{cudaErrorInvalidValue, "train_init"};
         // Keep freed blocks in the pool: frames re-grow without hitting the driver.
@@ -694,6 +725,13 @@ long long rgs_ctx_kernel_launches(const rgs_ctx* c) { return c ? c->launches : 0
 
 int rgs_profile_num_stages(void) { return kNumStages; }
 const char* rgs_profile_stage_name(int k) { return (k >= 0 && k < kNumStages) ? kStageNames[k] : ""; }
+
+int rgs_ctx_set_binning(rgs_ctx* c, int mode) {
+    if (!c) return RGS_E_INVALID;
+    if (mode < RGS_BINNING_AUTO || mode > RGS_BINNING_SCATTER) return set_err(c, RGS_E_INVALID, "unknown binning mode");
+    c->binning_mode = mode;
+    return RGS_OK;
+}
 
 int rgs_ctx_set_profiling(rgs_ctx* c, int timing, int count_evals) {
     return guarded(c, [&] {
@@ -1137,7 +1175,7 @@ int render_batch(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* cams, int
         cudaStream_t s = c->slot_stream[k];
         const int rc = run_forward(c, c->slot_frame[k], s, kFromScene, scene, nullptr, 0, true, &cams[v], bg,
                                    flags & ~RGS_FLAG_HOST_BUFFERS, image_for(user, v, s), false, false,
-                                   &c->view_stats[v], cache, true);
+                                   &c->view_stats[v], cache, true, true);
         if (rc) return rc;
         copy_out(v, k, s);
     }

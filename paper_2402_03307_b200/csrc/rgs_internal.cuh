@@ -113,7 +113,8 @@ struct BinState {
     uint32_t pair_cap;           // capacity of the pair buffers (set by the host)
     uint32_t n_pairs_eff;        // n_pairs, or 0 when it exceeds pair_cap (overflow)
     uint32_t overflow;           // 1: the view must be re-rendered with larger buffers
-    uint32_t pad2, pad3;         // (explicit: the whole 64 B are written, so copies read no padding)
+    uint32_t tile_blocks_done;   // tile-major scatter: completion counter of k_tile_offsets
+    uint32_t pad3;               // (explicit: the whole 64 B are written, so copies read no padding)
 };
 static_assert(sizeof(BinState) == 64, "BinState is copied as 64 initialised bytes");
 
@@ -174,6 +175,20 @@ void duplicate(const uint32_t* sorted_ids, const uint32_t* pair_off, const uint3
 void check_capacity(BinState* st, cudaStream_t s);
 void fold_status(const BinState* st, unsigned long long* word, unsigned long long overflow_word, cudaStream_t s);
 void frame_init(BinState* st, uint32_t pair_cap, uint32_t* bucket_count, uint32_t* bucket_cur, cudaStream_t s);
+// Tile-major scatter (images up to 256 x 256 tiles and 8192 tiles; k_binning.cu): per-chunk tile
+// counts -> per-chunk prefixes, tile starts, tile ranges and the pair count (into `st`), then the
+// pairs' splat ids straight to their sorted positions.
+// mode: RGS_BINNING_AUTO (the scatter for single views, the radix passes for the views of a
+// batch), RGS_BINNING_RADIX, RGS_BINNING_SCATTER (where it applies); the process default comes
+// from the environment variable RGS_BINNING=auto|radix|scatter.
+int default_binning_mode();
+bool tile_scatter_usable(int tiles_x, int tiles_y, int n, long long pair_cap, bool batch, int mode);
+size_t tile_count_words(int n, int n_tiles);
+void tile_counts(const uint32_t* sorted_ids, const uint32_t* sorted_tiles, const ushort4* rect, BinState* st, int n,
+                 int tiles_x, int tiles_y, uint32_t* counts, uint32_t* starts, uint2* ranges, cudaStream_t s);
+void tile_scatter(const uint32_t* sorted_ids, const uint32_t* sorted_tiles, const ushort4* rect, BinState* st,
+                  int n, int tiles_x, int tiles_y, const uint32_t* counts, const uint32_t* starts, uint2* ranges,
+                  uint32_t* vals, cudaStream_t s);
 int radix_blocks(long long n_pairs);
 size_t radix_count_entries(long long n_pairs);
 // Returns 1 when the sorted pairs end in (keys_b, vals_b) (three passes), 0 for (keys_a, vals_a).

@@ -51,6 +51,10 @@ FLAG_ACCUMULATE_GRAD = 64
 FLAG_DEFER_CHECKS = 128
 FLAG_REPRODUCIBLE = 256
 
+BINNING_AUTO = 0
+BINNING_RADIX = 1
+BINNING_SCATTER = 2
+
 _CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy
 SCENE_F64 = 1  # rgs_scene_create_ex storage flag
 
@@ -171,7 +175,7 @@ EXPORTS = [
     "rgs_accumulate_stats_f64", "rgs_ctx_profile_slow_reasons", "rgs_measure_fp64_tflops",
     # multi-GPU (train.NcclComm)
     "rgs_nccl_available", "rgs_nccl_unique_id", "rgs_nccl_comm_create", "rgs_nccl_comm_destroy",
-    "rgs_allreduce_grads", "rgs_image_loss_ex",
+    "rgs_allreduce_grads", "rgs_image_loss_ex", "rgs_ctx_set_binning",
 ]
 
 
@@ -220,6 +224,7 @@ def load_library(path: str = LIB_PATH):
         "rgs_profile_num_stages": (i, []),
         "rgs_profile_stage_name": (ctypes.c_char_p, [i]),
         "rgs_ctx_set_profiling": (i, [p, i, i]),
+        "rgs_ctx_set_binning": (i, [p, i]),
         "rgs_ctx_profile_reset": (i, [p]),
         "rgs_ctx_profile_read": (i, [p, p, p, p]),
         "rgs_measure_fp32_tflops": (i, [p, p]),
@@ -522,6 +527,13 @@ class Context:
 
     def synchronize(self):
         self.check(self.L.rgs_ctx_synchronize(self.h))
+
+    def set_binning(self, mode):
+        """Binning of the (tile, splat) pairs (same result, different cost profile): "auto" (the
+        tile-major scatter for single views, the radix passes for multi-view batches), "radix",
+        "scatter" -- or BINNING_AUTO / BINNING_RADIX / BINNING_SCATTER."""
+        m = {"auto": BINNING_AUTO, "radix": BINNING_RADIX, "scatter": BINNING_SCATTER}.get(mode, mode)
+        self.check(self.L.rgs_ctx_set_binning(self.h, int(m)))
 
     # --- profiling (CUDA events per pipeline stage, on the launching stream)
     def set_profiling(self, timing=True, count_evals: bool = False):

@@ -167,6 +167,27 @@ def test_wide_tile_keys_8k(ctx, orc, shape):
         assert float((e <= 1e-3).mean()) >= 0.9999, e.max()
 
 
+@pytest.mark.parametrize("shape", [(320, 240), (2048, 1024), (4096, 512)])
+def test_binning_modes_identical(orc, shape):
+    """The tile-major scatter and the radix passes produce the same per-tile lists: a small
+    frame, the scatter's largest tile count (128 x 64 = 8192 tiles) and its widest rows (256 x 32
+    tiles); the scatter's lists also against the oracle."""
+    w, h = shape
+    store = scenes.synthetic_scene(40_000, w, h, seed=21)
+    cam = scenes.bench_camera(w, h, 0.35, scenes.yaw_pose(5.0, (0.03, -0.01, 0.08)))
+    out = {}
+    for mode in ("scatter", "radix"):
+        c = rgs.Context(0, use_torch_stream=False)
+        c.set_binning(mode)
+        r = rgs.render_forward(store, cam, rgs.RenderOptions(retain_records=True), ctx=c)
+        out[mode] = (r.image, r.records.tile_offsets, r.records.tile_ids, r.records.n_contrib)
+    for a, b in zip(out["scatter"], out["radix"]):
+        assert np.array_equal(a, b)
+    ref_img, ref = orc.render_forward(store, cam, (0.0, 0.0, 0.0), threads=16, retain=True)
+    assert np.array_equal(out["scatter"][2], ref.tile_ids)
+    print(f"{w}x{h}: {len(ref.tile_ids)} pairs, scatter == radix == oracle")
+
+
 def test_scene_params_tensor_view(ctx):
     """DeviceScene.params_tensor is a live view of the device SoA: writing through it (as an
     NCCL broadcast into a replica does) changes what the renderer sees."""
