@@ -114,18 +114,18 @@ __global__ void k_scene_unpack(const T* __restrict__ P, int n, double* mean, dou
 // R4GS v1 records (checkpoint.cpp:36-47: 65 float32 per Gaussian -- mean4, log_scales4,
 // rotor8, opacity_logit, sh48 channel-major) <-> the scene SoA.  Records are staged in
 // shared memory so both sides of the transpose are coalesced.
-template <typename T>
-__global__ void __launch_bounds__(128) k_records_to_soa(const float* __restrict__ rec, int n, T* P) {
-    __shared__ float st[128 * 65];
-    const int i0 = blockIdx.x * 128, cnt = min(128, n - i0);
-    for (int e = threadIdx.x; e < cnt * 65; e += 128) st[e] = rec[65 * (size_t)i0 + e];
+template <typename R, typename T, int B>
+__global__ void __launch_bounds__(B) k_records_to_soa(const R* __restrict__ rec, int n, T* P) {
+    __shared__ R st[B * 65];
+    const int i0 = blockIdx.x * B, cnt = min(B, n - i0);
+    for (int e = threadIdx.x; e < cnt * 65; e += B) st[e] = rec[65 * (size_t)i0 + e];
     __syncthreads();
     const int li = threadIdx.x, i = i0 + li;
     if (li >= cnt) return;
-    const float* r = st + 65 * li;
-    auto put = [&](int blk, float a, float b, float c, float d) {
+    const R* r = st + 65 * li;
+    auto put = [&](int blk, R a, R b, R c, R d) {
         T* q = P + 4 * (size_t)blk * n + 4 * (size_t)i;
-        q[0] = a; q[1] = b; q[2] = c; q[3] = d;
+        q[0] = (T)a; q[1] = (T)b; q[2] = (T)c; q[3] = (T)d;
     };
     put(0, r[0], r[1], r[2], r[3]);
     put(1, r[4], r[5], r[6], r[7]);
@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(128) k_records_to_soa(const float* __restrict_
     put(3, r[12], r[13], r[14], r[15]);
 #pragma unroll
     for (int b = 0; b < 12; ++b) {
-        float v[4];
+        R v[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             const int j = 4 * b + e, k = j / 3, ch = j % 3;  // j = k*3 + ch
@@ -141,31 +141,31 @@ __global__ void __launch_bounds__(128) k_records_to_soa(const float* __restrict_
         }
         put(4 + b, v[0], v[1], v[2], v[3]);
     }
-    P[64 * (size_t)n + i] = r[16];
+    P[64 * (size_t)n + i] = (T)r[16];
 }
 
-template <typename T>
-__global__ void __launch_bounds__(128) k_soa_to_records(const T* __restrict__ P, int n, float* rec) {
-    __shared__ float st[128 * 65];
-    const int i0 = blockIdx.x * 128, cnt = min(128, n - i0);
+template <typename T, typename R, int B>
+__global__ void __launch_bounds__(B) k_soa_to_records(const T* __restrict__ P, int n, R* rec) {
+    __shared__ R st[B * 65];
+    const int i0 = blockIdx.x * B, cnt = min(B, n - i0);
     const int li = threadIdx.x, i = i0 + li;
     if (li < cnt) {
-        float* r = st + 65 * li;
-        auto get = [&](int blk, int c) -> float { return (float)P[4 * (size_t)blk * n + 4 * (size_t)i + c]; };
+        R* r = st + 65 * li;
+        auto get = [&](int blk, int c) -> R { return (R)P[4 * (size_t)blk * n + 4 * (size_t)i + c]; };
         for (int c = 0; c < 4; ++c) {
             r[c] = get(0, c);
             r[4 + c] = get(1, c);
             r[8 + c] = get(2, c);
             r[12 + c] = get(3, c);
         }
-        r[16] = (float)P[64 * (size_t)n + i];
+        r[16] = (R)P[64 * (size_t)n + i];
         for (int j = 0; j < 48; ++j) {
             const int k = j / 3, ch = j % 3;
             r[17 + ch * 16 + k] = get(4 + j / 4, j % 4);
         }
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < cnt * 65; e += 128) rec[65 * (size_t)i0 + e] = st[e];
+    for (int e = threadIdx.x; e < cnt * 65; e += B) rec[65 * (size_t)i0 + e] = st[e];
 }
 
 }  // namespace rgs_dev
@@ -178,17 +178,33 @@ static inline int blocks(long long n, int t) { return (int)((n + t - 1) / t); }
 void records_to_soa(const float* rec, int n, float* params, double* params64, cudaStream_t s) {
     if (n <= 0) return;
     if (params64)
-        k_records_to_soa<double><<<blocks(n, 128), 128, 0, s>>>(rec, n, params64);
+        k_records_to_soa<float, double, 128><<<blocks(n, 128), 128, 0, s>>>(rec, n, params64);
     else
-        k_records_to_soa<float><<<blocks(n, 128), 128, 0, s>>>(rec, n, params);
+        k_records_to_soa<float, float, 128><<<blocks(n, 128), 128, 0, s>>>(rec, n, params);
 }
 
 void soa_to_records(const float* params, const double* params64, int n, float* rec, cudaStream_t s) {
     if (n <= 0) return;
     if (params64)
-        k_soa_to_records<double><<<blocks(n, 128), 128, 0, s>>>(params64, n, rec);
+        k_soa_to_records<double, float, 128><<<blocks(n, 128), 128, 0, s>>>(params64, n, rec);
     else
-        k_soa_to_records<float><<<blocks(n, 128), 128, 0, s>>>(params, n, rec);
+        k_soa_to_records<float, float, 128><<<blocks(n, 128), 128, 0, s>>>(params, n, rec);
+}
+
+void rows_to_soa(const double* rows, int n, float* params, double* params64, cudaStream_t s) {
+    if (n <= 0) return;
+    if (params64)
+        k_records_to_soa<double, double, 64><<<blocks(n, 64), 64, 0, s>>>(rows, n, params64);
+    else
+        k_records_to_soa<double, float, 64><<<blocks(n, 64), 64, 0, s>>>(rows, n, params);
+}
+
+void soa_to_rows(const float* params, const double* params64, int n, double* rows, cudaStream_t s) {
+    if (n <= 0) return;
+    if (params64)
+        k_soa_to_records<double, double, 64><<<blocks(n, 64), 64, 0, s>>>(params64, n, rows);
+    else
+        k_soa_to_records<float, double, 64><<<blocks(n, 64), 64, 0, s>>>(params, n, rows);
 }
 
 void compact_index(const uint8_t* valid, const uint32_t* scan, int n, uint32_t* compact_ids, cudaStream_t s) {

@@ -1523,46 +1523,14 @@ struct rgs_optimizer {
 namespace {
 
 // Host (N, 65) rows in the reference order -> the five upload arrays (and back).
-void split65(const double* r, size_t n, std::vector<double>& d) {
-    d.assign(65 * n, 0.0);
-    for (size_t i = 0; i < n; ++i) {
-        const double* s = r + 65 * i;
-        for (int a = 0; a < 4; ++a) d[4 * i + a] = s[a];
-        for (int a = 0; a < 4; ++a) d[4 * n + 4 * i + a] = s[4 + a];
-        for (int a = 0; a < 8; ++a) d[8 * n + 8 * i + a] = s[8 + a];
-        d[16 * n + i] = s[16];
-        for (int a = 0; a < 48; ++a) d[17 * n + 48 * i + a] = s[17 + a];
-    }
-}
-void join65(const std::vector<double>& d, size_t n, double* r) {
-    for (size_t i = 0; i < n; ++i) {
-        double* s = r + 65 * i;
-        for (int a = 0; a < 4; ++a) s[a] = d[4 * i + a];
-        for (int a = 0; a < 4; ++a) s[4 + a] = d[4 * n + 4 * i + a];
-        for (int a = 0; a < 8; ++a) s[8 + a] = d[8 * n + 8 * i + a];
-        s[16] = d[16 * n + i];
-        for (int a = 0; a < 48; ++a) s[17 + a] = d[17 * n + 48 * i + a];
-    }
-}
-
-// SoA device block (float or double) <-> host (N, 65) rows.
+// SoA device block (float or double) <-> host (N, 65) rows: one copy of the rows, the transpose
+// on the device.
 void soa_upload(rgs_ctx* c, size_t n, bool f64, const double* rows, void* dst) {
-    std::vector<double> d;
-    split65(rows, n, d);
     DevBuf tmp;
     cudaStream_t s = c->stream;
-    if (f64) {
-        tmp.ensure(sizeof(double) * 65 * n, s);
-        double* t = tmp.as<double>();
-        CK(cudaMemcpyAsync(t, d.data(), sizeof(double) * 65 * n, cudaMemcpyHostToDevice, s));
-        rgs_launch::scene_pack64(t, t + 4 * n, t + 8 * n, t + 16 * n, t + 17 * n, (int)n, (double*)dst, s);
-    } else {
-        std::vector<float> f(d.begin(), d.end());
-        tmp.ensure(sizeof(float) * 65 * n, s);
-        float* t = tmp.as<float>();
-        CK(cudaMemcpyAsync(t, f.data(), sizeof(float) * 65 * n, cudaMemcpyHostToDevice, s));
-        rgs_launch::scene_pack(t, t + 4 * n, t + 8 * n, t + 16 * n, t + 17 * n, (int)n, (float*)dst, s);
-    }
+    tmp.ensure(sizeof(double) * 65 * n, s);
+    CK(cudaMemcpyAsync(tmp.p, rows, sizeof(double) * 65 * n, cudaMemcpyHostToDevice, s));
+    rgs_launch::rows_to_soa(tmp.as<double>(), (int)n, f64 ? nullptr : (float*)dst, f64 ? (double*)dst : nullptr, s);
     c->launches += 1;
     CK(cudaStreamSynchronize(s));
     tmp.release(s);
@@ -1571,15 +1539,12 @@ void soa_download(rgs_ctx* c, size_t n, bool f64, const void* src, double* rows)
     DevBuf tmp;
     cudaStream_t s = c->stream;
     tmp.ensure(sizeof(double) * 65 * n, s);
-    double* t = tmp.as<double>();
-    rgs_launch::scene_unpack(f64 ? nullptr : (const float*)src, f64 ? (const double*)src : nullptr, (int)n, t,
-                             t + 4 * n, t + 8 * n, t + 16 * n, t + 17 * n, s);
+    rgs_launch::soa_to_rows(f64 ? nullptr : (const float*)src, f64 ? (const double*)src : nullptr, (int)n,
+                            tmp.as<double>(), s);
     c->launches += 1;
-    std::vector<double> d(65 * n);
-    CK(cudaMemcpyAsync(d.data(), t, sizeof(double) * 65 * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(rows, tmp.p, sizeof(double) * 65 * n, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     tmp.release(s);
-    join65(d, n, rows);
 }
 
 // ssim.cpp:15-31 on the host (glibc exp), uploaded once per context.

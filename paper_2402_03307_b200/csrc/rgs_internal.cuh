@@ -237,6 +237,9 @@ void scene_unpack(const float* params, const double* params64, int n, double* me
                   double* op, double* sh, cudaStream_t s);
 void records_to_soa(const float* rec, int n, float* params, double* params64, cudaStream_t s);
 void soa_to_records(const float* params, const double* params64, int n, float* rec, cudaStream_t s);
+// (n, 65) double rows (mean4, log_scales4, rotor8, opacity_logit, sh48 channel-major) <-> the SoA
+void rows_to_soa(const double* rows, int n, float* params, double* params64, cudaStream_t s);
+void soa_to_rows(const float* params, const double* params64, int n, double* rows, cudaStream_t s);
 void valid_to_u32(const uint8_t* valid, int n, uint32_t* out, cudaStream_t s);
 double ffma_peak(float* out, int blocks, int iters, cudaStream_t s);
 double dfma_peak(double* out, int blocks, int iters, cudaStream_t s);

@@ -137,18 +137,24 @@ rgs_scene* device_scene(const GaussianStore& store, uint64_t* key = nullptr) {
         ++c.d2d;
         return c.s;
     }
-    std::vector<double> mean(4 * (size_t)n), ls(4 * (size_t)n), rot(8 * (size_t)n), op(n), sh(48 * (size_t)n);
-    for (int i = 0; i < n; ++i) {
-        for (int a = 0; a < 4; ++a) mean[4 * i + a] = store.mean[i][a];
-        for (int a = 0; a < 4; ++a) ls[4 * i + a] = store.log_scales[i][a];
-        const Vec8 cf = store.rotor[i].coeffs();
-        for (int a = 0; a < 8; ++a) rot[8 * i + a] = cf[a];
-        op[i] = store.opacity_logit[i];
-        for (int ch = 0; ch < 3; ++ch)
-            for (int k = 0; k < 16; ++k) sh[48 * i + ch * 16 + k] = store.sh[i](ch, k);
-    }
+    double* mean = dropin::scratch<double>(0, 4 * (size_t)n).data();
+    double* ls = dropin::scratch<double>(1, 4 * (size_t)n).data();
+    double* rot = dropin::scratch<double>(2, 8 * (size_t)n).data();
+    double* op = dropin::scratch<double>(3, (size_t)n).data();
+    double* sh = dropin::scratch<double>(4, 48 * (size_t)n).data();
+    dropin::parallel_for((size_t)n, [&](size_t i0, size_t i1) {
+        for (size_t i = i0; i < i1; ++i) {
+            for (int a = 0; a < 4; ++a) mean[4 * i + a] = store.mean[i][a];
+            for (int a = 0; a < 4; ++a) ls[4 * i + a] = store.log_scales[i][a];
+            const Vec8 cf = store.rotor[i].coeffs();
+            for (int a = 0; a < 8; ++a) rot[8 * i + a] = cf[a];
+            op[i] = store.opacity_logit[i];
+            for (int ch = 0; ch < 3; ++ch)
+                for (int k = 0; k < 16; ++k) sh[48 * i + ch * 16 + k] = store.sh[i](ch, k);
+        }
+    });
     c.n = -1;  // invalid until the upload succeeded
-    check(rgs_scene_upload_f64(context(), c.s, mean.data(), ls.data(), rot.data(), op.data(), sh.data(), nullptr));
+    check(rgs_scene_upload_f64(context(), c.s, mean, ls, rot, op, sh, nullptr));
     c.n = n;
     c.sh = store.active_sh_degree;
     c.hash = h;
@@ -189,27 +195,34 @@ void render_image(Image* image, int w, int h, int channels, Fn&& fn) {
     if (kat_mode()) {
         fn(reinterpret_cast<float*>(image->data.data()));
     } else {
-        std::vector<float> tmp((size_t)w * h * channels);
-        fn(tmp.data());
-        for (size_t i = 0; i < tmp.size(); ++i) image->data[i] = tmp[i];
+        const size_t cnt = (size_t)w * h * channels;
+        float* tmp = dropin::scratch<float>(3, cnt).data();
+        fn(tmp);
+        dropin::parallel_for(cnt, [&](size_t i0, size_t i1) {
+            for (size_t i = i0; i < i1; ++i) image->data[i] = tmp[i];
+        });
     }
 }
 
 void export_records(const RecordsHandle& h, RenderRecords* rec, const Vec3& background) {
     rgs_records_info info;
     check(rgs_records_info_get(h.r, &info));
-    std::vector<rgs_splat> sp(info.n_splats);
+    const size_t ns = (size_t)info.n_splats, npix = (size_t)info.width * info.height;
+    const rgs_splat* sp = dropin::scratch<rgs_splat>(0, ns).data();
     const int nt = info.tiles_x * info.tiles_y;
-    std::vector<long long> off(nt + 1);
-    std::vector<int32_t> ids(std::max<long long>(info.n_pairs, 1));
-    rec->final_T.assign((size_t)info.width * info.height, 1);
-    std::vector<int32_t> nc((size_t)info.width * info.height);
-    check(rgs_records_export(context(), h.r, sp.data(), off.data(), ids.data(), rec->final_T.data(), nc.data()));
-    rec->splats.resize(sp.size());
-    for (size_t i = 0; i < sp.size(); ++i) rec->splats[i] = from_c(sp[i]);
-    rec->tile_splats.assign(nt, {});
-    for (int t = 0; t < nt; ++t) rec->tile_splats[t].assign(ids.begin() + off[t], ids.begin() + off[t + 1]);
-    rec->n_contrib.assign(nc.begin(), nc.end());
+    const long long* off = dropin::scratch<long long>(0, (size_t)nt + 1).data();
+    const int32_t* ids = dropin::scratch<int32_t>(2, (size_t)std::max<long long>(info.n_pairs, 1)).data();
+    const int32_t* nc = dropin::scratch<int32_t>(1, npix).data();
+    rec->final_T.resize(npix);
+    check(rgs_records_export(context(), h.r, const_cast<rgs_splat*>(sp), const_cast<long long*>(off),
+                             const_cast<int32_t*>(ids), rec->final_T.data(), const_cast<int32_t*>(nc)));
+    rec->splats.resize(ns);
+    dropin::parallel_for(ns, [&](size_t i0, size_t i1) {
+        for (size_t i = i0; i < i1; ++i) rec->splats[i] = from_c(sp[i]);
+    });
+    rec->tile_splats.resize(nt);
+    for (int t = 0; t < nt; ++t) rec->tile_splats[t].assign(ids + off[t], ids + off[t + 1]);
+    rec->n_contrib.assign(nc, nc + npix);
     rec->tiles_x = info.tiles_x;
     rec->tiles_y = info.tiles_y;
     rec->background = background;
@@ -304,30 +317,38 @@ StoreGrads render_backward(const GaussianStore& store, const Camera& cam, const 
         dev_rec = h.r;
     }
     const int n = store.size();
-    std::vector<float> dl(dL_dimage.data.begin(), dL_dimage.data.end());
-    std::vector<float> g(65 * (size_t)std::max(n, 1)), vn(std::max(n, 1));
-    std::vector<int32_t> vis(std::max(n, 1));
+    const size_t ndl = dL_dimage.data.size(), n1 = (size_t)std::max(n, 1);
+    float* dl = dropin::scratch<float>(2, ndl).data();
+    dropin::parallel_for(ndl, [&](size_t i0, size_t i1) {
+        for (size_t i = i0; i < i1; ++i) dl[i] = (float)dL_dimage.data[i];
+    });
+    const float* g = dropin::scratch<float>(0, 65 * n1).data();
+    const float* vn = dropin::scratch<float>(1, n1).data();
+    const int32_t* vis = dropin::scratch<int32_t>(0, n1).data();
     // thread-count invariant like the reference's fixed-order reduction (rasterizer.cpp:372-384):
     // the FP64 replay in KAT mode, the fixed-point accumulation otherwise
     const unsigned flags = RGS_FLAG_HOST_BUFFERS | (kat_mode() ? RGS_FLAG_DETERMINISTIC : RGS_FLAG_REPRODUCIBLE);
-    check(rgs_render_backward(context(), scene, &c, dev_rec, dl.data(), flags, g.data(), vn.data(), vis.data()));
+    check(rgs_render_backward(context(), scene, &c, dev_rec, dl, flags, const_cast<float*>(g), const_cast<float*>(vn),
+                              const_cast<int32_t*>(vis)));
     // device SoA (rgs_scene_params layout) -> per-Gaussian gradients
     StoreGrads out;
     out.resize(n);
     const size_t N = (size_t)n;
-    for (int i = 0; i < n; ++i) {
-        GaussianParamGrad& p = out.g[i];
-        for (int a = 0; a < 4; ++a) p.d_mean[a] = g[4 * i + a];
-        for (int a = 0; a < 4; ++a) p.d_log_scales[a] = g[4 * N + 4 * i + a];
-        Vec8 r;
-        for (int a = 0; a < 4; ++a) r[a] = g[8 * N + 4 * i + a];
-        for (int a = 0; a < 4; ++a) r[4 + a] = g[12 * N + 4 * i + a];
-        p.d_rotor = r;
-        p.d_opacity_logit = g[64 * N + i];
-        for (int j = 0; j < 48; ++j) p.d_sh(j % 3, j / 3) = g[(16 + 4 * (size_t)(j / 4)) * N + 4 * i + (j % 4)];
-        out.viewspace_norm[i] = vn[i];
-        out.visible[i] = vis[i] > 0 ? 1 : 0;
-    }
+    dropin::parallel_for(N, [&](size_t i0, size_t i1) {
+        for (size_t i = i0; i < i1; ++i) {
+            GaussianParamGrad& p = out.g[i];
+            for (int a = 0; a < 4; ++a) p.d_mean[a] = g[4 * i + a];
+            for (int a = 0; a < 4; ++a) p.d_log_scales[a] = g[4 * N + 4 * i + a];
+            Vec8 r;
+            for (int a = 0; a < 4; ++a) r[a] = g[8 * N + 4 * i + a];
+            for (int a = 0; a < 4; ++a) r[4 + a] = g[12 * N + 4 * i + a];
+            p.d_rotor = r;
+            p.d_opacity_logit = g[64 * N + i];
+            for (int j = 0; j < 48; ++j) p.d_sh(j % 3, j / 3) = g[(16 + 4 * (size_t)(j / 4)) * N + 4 * i + (j % 4)];
+            out.viewspace_norm[i] = vn[i];
+            out.visible[i] = vis[i] > 0 ? 1 : 0;
+        }
+    });
     return out;
 }
 

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <malloc.h>
 #include <mutex>
 #include <stdexcept>
 #include <thread>
@@ -14,6 +15,14 @@ namespace dropin {
 
 rgs_ctx* context() {
     static rgs_ctx* c = [] {
+        // The reference API hands ~100 MB per-Gaussian structs (StoreGrads, RenderRecords) across
+        // every call; above glibc's mmap threshold each one is a fresh mmap whose pages fault and
+        // zero on first touch.  Serve them from the heap instead, so freed blocks are reused
+        // (RGS_DROPIN_NO_MALLOPT=1 leaves the process's malloc settings alone).
+        if (!std::getenv("RGS_DROPIN_NO_MALLOPT")) {
+            mallopt(M_MMAP_THRESHOLD, 1 << 30);
+            mallopt(M_TRIM_THRESHOLD, 1 << 30);
+        }
         rgs_ctx* h = nullptr;
         const char* dev = std::getenv("RGS_DEVICE");
         if (rgs_ctx_create(dev ? std::atoi(dev) : 0, &h) != RGS_OK)

@@ -4,8 +4,11 @@
 // copies it device to device instead of uploading the host store again).
 #pragma once
 
+#include <algorithm>
 #include <cstddef>
 #include <cstdint>
+#include <thread>
+#include <vector>
 
 #include "rgs/gaussian.hpp"
 #include "rgs_cuda.h"
@@ -22,6 +25,40 @@ uint64_t hash_bytes(const void* p, size_t bytes, uint64_t seed);
 template <typename V>
 uint64_t hash_vec(const V& v, uint64_t seed) {
     return hash_bytes(v.data(), v.size() * sizeof(typename V::value_type), seed);
+}
+
+// f(begin, end) over [0, n) split into contiguous ranges on up to hardware_concurrency threads
+// (the host-side layout conversions between the reference's per-Gaussian structs and the
+// device SoA; every index is written by exactly one range, so the result is thread-count free).
+template <typename F>
+void parallel_for(size_t n, F&& f) {
+    const size_t kMinPerThread = 4096;
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const size_t nt = std::min<size_t>({(size_t)hw, (n + kMinPerThread - 1) / kMinPerThread, 32});
+    if (nt <= 1) {
+        f(size_t(0), n);
+        return;
+    }
+    std::vector<std::thread> pool;
+    pool.reserve(nt - 1);
+    const size_t per = (n + nt - 1) / nt;
+    for (size_t t = 1; t < nt; ++t) {
+        const size_t b = t * per, e = std::min(n, b + per);
+        if (b < e) pool.emplace_back([&f, b, e] { f(b, e); });
+    }
+    f(size_t(0), std::min(n, per));
+    for (auto& th : pool) th.join();
+}
+
+// Grow-only host scratch vectors, reused across calls (per element type and slot): their pages
+// stay mapped, so the 50-100 MB layout conversions of a large store pay no page faults or zero
+// fills per call.  Returns a vector of at least n elements (contents unspecified).
+template <typename T>
+std::vector<T>& scratch(int slot, size_t n) {
+    static thread_local std::vector<T> bufs[8];
+    std::vector<T>& v = bufs[slot];
+    if (v.size() < n) v.resize(n);
+    return v;
 }
 
 // The parameters a render reads (gaussian.hpp:79-85) and the SH degree.

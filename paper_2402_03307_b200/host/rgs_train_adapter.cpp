@@ -123,19 +123,21 @@ Mirror& mirror() {
 
 void rows65(const GaussianStore& s, bool moments_v, std::vector<double>& out) {
     const size_t n = (size_t)s.size();
-    out.assign(65 * n, 0.0);
-    for (size_t i = 0; i < n; ++i) {
-        double* r = out.data() + 65 * i;
-        const Vec4& mm = moments_v ? s.v_mean[i] : s.m_mean[i];
-        const Vec4& ml = moments_v ? s.v_ls[i] : s.m_ls[i];
-        const Vec8& mr = moments_v ? s.v_rot[i] : s.m_rot[i];
-        const ShCoeffs& msh = moments_v ? s.v_sh[i] : s.m_sh[i];
-        for (int a = 0; a < 4; ++a) r[a] = mm[a], r[4 + a] = ml[a];
-        for (int a = 0; a < 8; ++a) r[8 + a] = mr[a];
-        r[16] = moments_v ? s.v_op[i] : s.m_op[i];
-        for (int ch = 0; ch < 3; ++ch)
-            for (int k = 0; k < 16; ++k) r[17 + ch * 16 + k] = msh(ch, k);
-    }
+    out.resize(65 * n);
+    dropin::parallel_for(n, [&](size_t i0, size_t i1) {
+        for (size_t i = i0; i < i1; ++i) {
+            double* r = out.data() + 65 * i;
+            const Vec4& mm = moments_v ? s.v_mean[i] : s.m_mean[i];
+            const Vec4& ml = moments_v ? s.v_ls[i] : s.m_ls[i];
+            const Vec8& mr = moments_v ? s.v_rot[i] : s.m_rot[i];
+            const ShCoeffs& msh = moments_v ? s.v_sh[i] : s.m_sh[i];
+            for (int a = 0; a < 4; ++a) r[a] = mm[a], r[4 + a] = ml[a];
+            for (int a = 0; a < 8; ++a) r[8 + a] = mr[a];
+            r[16] = moments_v ? s.v_op[i] : s.m_op[i];
+            for (int ch = 0; ch < 3; ++ch)
+                for (int k = 0; k < 16; ++k) r[17 + ch * 16 + k] = msh(ch, k);
+        }
+    });
 }
 
 void upload(const GaussianStore& s, DeviceStore& d, bool with_optimizer) {
@@ -207,39 +209,48 @@ void download(const DeviceStore& d, GaussianStore& s) {
 // Parameters / moments of the device store into the host store, in place (sizes equal).
 void download_params(const DeviceStore& d, GaussianStore& s) {
     const size_t n = (size_t)s.size();
-    std::vector<double> mean(4 * n), ls(4 * n), rot(8 * n), op(n), sh(48 * n);
-    check(rgs_scene_download_f64(tctx(), d.scene, mean.data(), ls.data(), rot.data(), op.data(), sh.data()));
-    for (size_t i = 0; i < n; ++i) {
-        for (int a = 0; a < 4; ++a) s.mean[i][a] = mean[4 * i + a], s.log_scales[i][a] = ls[4 * i + a];
-        Vec8 c;
-        for (int a = 0; a < 8; ++a) c[a] = rot[8 * i + a];
-        s.rotor[i] = Rotor4::from_coeffs(c);
-        s.opacity_logit[i] = op[i];
-        for (int ch = 0; ch < 3; ++ch)
-            for (int k = 0; k < 16; ++k) s.sh[i](ch, k) = sh[48 * i + ch * 16 + k];
-    }
+    double* mean = dropin::scratch<double>(0, 4 * n).data();
+    double* ls = dropin::scratch<double>(1, 4 * n).data();
+    double* rot = dropin::scratch<double>(2, 8 * n).data();
+    double* op = dropin::scratch<double>(3, n).data();
+    double* sh = dropin::scratch<double>(4, 48 * n).data();
+    check(rgs_scene_download_f64(tctx(), d.scene, mean, ls, rot, op, sh));
+    dropin::parallel_for(n, [&](size_t i0, size_t i1) {
+        for (size_t i = i0; i < i1; ++i) {
+            for (int a = 0; a < 4; ++a) s.mean[i][a] = mean[4 * i + a], s.log_scales[i][a] = ls[4 * i + a];
+            Vec8 c;
+            for (int a = 0; a < 8; ++a) c[a] = rot[8 * i + a];
+            s.rotor[i] = Rotor4::from_coeffs(c);
+            s.opacity_logit[i] = op[i];
+            for (int ch = 0; ch < 3; ++ch)
+                for (int k = 0; k < 16; ++k) s.sh[i](ch, k) = sh[48 * i + ch * 16 + k];
+        }
+    });
 }
 
 void download_moments(const DeviceStore& d, GaussianStore& s) {
     const size_t n = (size_t)s.size();
-    std::vector<double> m(65 * n), v(65 * n);
-    check(rgs_optimizer_download(tctx(), d.opt, m.data(), v.data(), nullptr, nullptr));
-    for (size_t i = 0; i < n; ++i) {
-        const double* mr = m.data() + 65 * i;
-        const double* vr = v.data() + 65 * i;
-        for (int a = 0; a < 4; ++a) {
-            s.m_mean[i][a] = mr[a], s.v_mean[i][a] = vr[a];
-            s.m_ls[i][a] = mr[4 + a], s.v_ls[i][a] = vr[4 + a];
-        }
-        for (int a = 0; a < 8; ++a) s.m_rot[i][a] = mr[8 + a], s.v_rot[i][a] = vr[8 + a];
-        s.m_op[i] = mr[16];
-        s.v_op[i] = vr[16];
-        for (int ch = 0; ch < 3; ++ch)
-            for (int k = 0; k < 16; ++k) {
-                s.m_sh[i](ch, k) = mr[17 + ch * 16 + k];
-                s.v_sh[i](ch, k) = vr[17 + ch * 16 + k];
+    double* m = dropin::scratch<double>(5, 65 * n).data();
+    double* v = dropin::scratch<double>(6, 65 * n).data();
+    check(rgs_optimizer_download(tctx(), d.opt, m, v, nullptr, nullptr));
+    dropin::parallel_for(n, [&](size_t i0, size_t i1) {
+        for (size_t i = i0; i < i1; ++i) {
+            const double* mr = m + 65 * i;
+            const double* vr = v + 65 * i;
+            for (int a = 0; a < 4; ++a) {
+                s.m_mean[i][a] = mr[a], s.v_mean[i][a] = vr[a];
+                s.m_ls[i][a] = mr[4 + a], s.v_ls[i][a] = vr[4 + a];
             }
-    }
+            for (int a = 0; a < 8; ++a) s.m_rot[i][a] = mr[8 + a], s.v_rot[i][a] = vr[8 + a];
+            s.m_op[i] = mr[16];
+            s.v_op[i] = vr[16];
+            for (int ch = 0; ch < 3; ++ch)
+                for (int k = 0; k < 16; ++k) {
+                    s.m_sh[i](ch, k) = mr[17 + ch * 16 + k];
+                    s.v_sh[i](ch, k) = vr[17 + ch * 16 + k];
+                }
+        }
+    });
 }
 
 // The mirror brought in line with the host store: only the parts whose hash changed are
@@ -263,18 +274,22 @@ DeviceStore& synced(const GaussianStore& s) {
     }
     m.n = -1;  // invalid until every part is up
     if (fresh || m.hp != hp) {
-        std::vector<double> mean(4 * (size_t)n), ls(4 * (size_t)n), rot(8 * (size_t)n), op((size_t)n),
-            sh(48 * (size_t)n);
-        for (int i = 0; i < n; ++i) {
-            for (int a = 0; a < 4; ++a) mean[4 * i + a] = s.mean[i][a], ls[4 * i + a] = s.log_scales[i][a];
-            const Vec8 c = s.rotor[i].coeffs();
-            for (int a = 0; a < 8; ++a) rot[8 * i + a] = c[a];
-            op[i] = s.opacity_logit[i];
-            for (int ch = 0; ch < 3; ++ch)
-                for (int k = 0; k < 16; ++k) sh[48 * (size_t)i + ch * 16 + k] = s.sh[i](ch, k);
-        }
-        if (n) check(rgs_scene_upload_f64(tctx(), m.d.scene, mean.data(), ls.data(), rot.data(), op.data(), sh.data(),
-                                          nullptr));
+        double* mean = dropin::scratch<double>(0, 4 * (size_t)n).data();
+        double* ls = dropin::scratch<double>(1, 4 * (size_t)n).data();
+        double* rot = dropin::scratch<double>(2, 8 * (size_t)n).data();
+        double* op = dropin::scratch<double>(3, (size_t)n).data();
+        double* sh = dropin::scratch<double>(4, 48 * (size_t)n).data();
+        dropin::parallel_for((size_t)n, [&](size_t i0, size_t i1) {
+            for (size_t i = i0; i < i1; ++i) {
+                for (int a = 0; a < 4; ++a) mean[4 * i + a] = s.mean[i][a], ls[4 * i + a] = s.log_scales[i][a];
+                const Vec8 c = s.rotor[i].coeffs();
+                for (int a = 0; a < 8; ++a) rot[8 * i + a] = c[a];
+                op[i] = s.opacity_logit[i];
+                for (int ch = 0; ch < 3; ++ch)
+                    for (int k = 0; k < 16; ++k) sh[48 * i + ch * 16 + k] = s.sh[i](ch, k);
+            }
+        });
+        if (n) check(rgs_scene_upload_f64(tctx(), m.d.scene, mean, ls, rot, op, sh, nullptr));
     }
     if (n && (fresh || m.hm != hm)) {
         std::vector<double> mo, vo;
@@ -528,23 +543,26 @@ void adam_step(GaussianStore& store, const StoreGrads& grads, const TrainConfig&
     if (n == 0) return;
     DeviceStore& d = synced(store);
     // gradients in the rgs_scene_params SoA layout (float32, the device gradient format)
-    std::vector<float> g(65 * (size_t)n);
-    for (int i = 0; i < n; ++i) {
-        const GaussianParamGrad& gi = grads.g[i];
-        for (int a = 0; a < 4; ++a) {
-            g[4 * (size_t)i + a] = (float)gi.d_mean[a];
-            g[4 * (size_t)n + 4 * (size_t)i + a] = (float)gi.d_log_scales[a];
-            g[8 * (size_t)n + 4 * (size_t)i + a] = (float)gi.d_rotor[a];
-            g[12 * (size_t)n + 4 * (size_t)i + a] = (float)gi.d_rotor[4 + a];
+    const size_t N = (size_t)n;
+    float* g = dropin::scratch<float>(0, 65 * N).data();
+    dropin::parallel_for(N, [&](size_t i0, size_t i1) {
+        for (size_t i = i0; i < i1; ++i) {
+            const GaussianParamGrad& gi = grads.g[i];
+            for (int a = 0; a < 4; ++a) {
+                g[4 * i + a] = (float)gi.d_mean[a];
+                g[4 * N + 4 * i + a] = (float)gi.d_log_scales[a];
+                g[8 * N + 4 * i + a] = (float)gi.d_rotor[a];
+                g[12 * N + 4 * i + a] = (float)gi.d_rotor[4 + a];
+            }
+            for (int j = 0; j < 48; ++j) {
+                const int k = j / 3, ch = j % 3;
+                g[(16 + 4 * (size_t)(j / 4)) * N + 4 * i + j % 4] = (float)gi.d_sh(ch, k);
+            }
+            g[64 * N + i] = (float)gi.d_opacity_logit;
         }
-        for (int j = 0; j < 48; ++j) {
-            const int k = j / 3, ch = j % 3;
-            g[(16 + 4 * (size_t)(j / 4)) * n + 4 * (size_t)i + j % 4] = (float)gi.d_sh(ch, k);
-        }
-        g[64 * (size_t)n + i] = (float)gi.d_opacity_logit;
-    }
-    Dev dg(4 * g.size());
-    dg.put(g.data(), 4 * g.size());
+    });
+    Dev dg(4 * 65 * N);
+    dg.put(g, 4 * 65 * N);
     rgs_adam_config c;
     c.lr_position = config.lr_position;
     c.lr_position_final = config.lr_position_final;

@@ -157,70 +157,74 @@ extern "C" int dropin_profile_step(int n, const double* mean, const double* ls, 
             off += cnt;
             imgs.push_back(std::move(im));
         }
-        for (int q = 0; q < 10; ++q) seconds[q] = 0;
         TrainConfig cfg;
-        const LossWeights& w = cfg.loss;
-        RenderOptions opts;
-        opts.retain_records = true;
-        StoreGrads grads;
-        grads.resize(n);
-        const double inv_b = 1.0 / n_frames;
-        for (int f = 0; f < n_frames; ++f) {
+        // two steps on the same store: the timings are the second's (device mirrors warm, as in
+        // the timed steps of dropin_train_steps)
+        for (int rep = 0; rep < 2; ++rep) {
+            for (int q = 0; q < 10; ++q) seconds[q] = 0;
+            const LossWeights& w = cfg.loss;
+            RenderOptions opts;
+            opts.retain_records = true;
+            StoreGrads grads;
+            grads.resize(n);
+            const double inv_b = 1.0 / n_frames;
+            for (int f = 0; f < n_frames; ++f) {
+                auto t = clk::now();
+                RenderOutput ro = render_forward(store, cm[f], opts);
+                seconds[0] += sec(t);
+                t = clk::now();
+                Image g_l1 = l1_loss_backward(ro.image, imgs[f]);
+                volatile double l1 = l1_loss(ro.image, imgs[f]) * inv_b;
+                (void)l1;
+                seconds[1] += sec(t);
+                t = clk::now();
+                Image g_ssim;
+                volatile double ss = ssim_loss_with_grad(ro.image, imgs[f], &g_ssim);
+                (void)ss;
+                seconds[2] += sec(t);
+                t = clk::now();
+                Image dl(ro.image.width, ro.image.height, 3);
+                for (size_t i = 0; i < dl.data.size(); ++i)
+                    dl.data[i] = (1 - w.lambda_ssim) * inv_b * g_l1.data[i] + w.lambda_ssim * inv_b * g_ssim.data[i];
+                seconds[3] += sec(t);
+                t = clk::now();
+                StoreGrads fg = render_backward(store, cm[f], ro.records, dl, 1);
+                seconds[4] += sec(t);
+                t = clk::now();
+                grads.add(fg);
+                seconds[5] += sec(t);
+            }
             auto t = clk::now();
-            RenderOutput ro = render_forward(store, cm[f], opts);
-            seconds[0] += sec(t);
+            std::vector<Scalar> ops(n), g_op;
+            for (int i = 0; i < n; ++i) ops[i] = store.opacity(i);
+            entropy_loss_with_grad(ops, &g_op);
+            for (int i = 0; i < n; ++i) grads.g[i].d_opacity_logit += w.lambda_entropy * g_op[i] * ops[i] * (1 - ops[i]);
+            seconds[6] = sec(t);
+            if (nbrs) {
+                t = clk::now();
+                Knn4DIndex knn;
+                knn.k = k;
+                knn.store_size = n;
+                knn.neighbors.assign(n, std::vector<int>(k));
+                for (int i = 0; i < n; ++i)
+                    for (int j = 0; j < k; ++j) knn.neighbors[i][j] = nbrs[(size_t)k * i + j];
+                std::vector<Vec3> speeds(n);
+                std::vector<SliceCache> caches(n);
+                for (int i = 0; i < n; ++i) speeds[i] = gaussian_speed(store.get(i), &caches[i]);
+                std::vector<Vec3> g_speed;
+                consistency_loss(speeds, knn, &g_speed);
+                for (int i = 0; i < n; ++i)
+                    slice_backward(store.get(i), caches[i], Mat3::Zero(), Vec3::Zero(), 0,
+                                   w.lambda_consistency * g_speed[i], &grads.g[i]);
+                seconds[7] = sec(t);
+            }
             t = clk::now();
-            Image g_l1 = l1_loss_backward(ro.image, imgs[f]);
-            volatile double l1 = l1_loss(ro.image, imgs[f]) * inv_b;
-            (void)l1;
-            seconds[1] += sec(t);
+            accumulate_stats(store, grads);
+            seconds[8] = sec(t);
             t = clk::now();
-            Image g_ssim;
-            volatile double ss = ssim_loss_with_grad(ro.image, imgs[f], &g_ssim);
-            (void)ss;
-            seconds[2] += sec(t);
-            t = clk::now();
-            Image dl(ro.image.width, ro.image.height, 3);
-            for (size_t i = 0; i < dl.data.size(); ++i)
-                dl.data[i] = (1 - w.lambda_ssim) * inv_b * g_l1.data[i] + w.lambda_ssim * inv_b * g_ssim.data[i];
-            seconds[3] += sec(t);
-            t = clk::now();
-            StoreGrads fg = render_backward(store, cm[f], ro.records, dl, 1);
-            seconds[4] += sec(t);
-            t = clk::now();
-            grads.add(fg);
-            seconds[5] += sec(t);
+            adam_step(store, grads, cfg, step + rep);
+            seconds[9] = sec(t);
         }
-        auto t = clk::now();
-        std::vector<Scalar> ops(n), g_op;
-        for (int i = 0; i < n; ++i) ops[i] = store.opacity(i);
-        entropy_loss_with_grad(ops, &g_op);
-        for (int i = 0; i < n; ++i) grads.g[i].d_opacity_logit += w.lambda_entropy * g_op[i] * ops[i] * (1 - ops[i]);
-        seconds[6] = sec(t);
-        if (nbrs) {
-            t = clk::now();
-            Knn4DIndex knn;
-            knn.k = k;
-            knn.store_size = n;
-            knn.neighbors.assign(n, std::vector<int>(k));
-            for (int i = 0; i < n; ++i)
-                for (int j = 0; j < k; ++j) knn.neighbors[i][j] = nbrs[(size_t)k * i + j];
-            std::vector<Vec3> speeds(n);
-            std::vector<SliceCache> caches(n);
-            for (int i = 0; i < n; ++i) speeds[i] = gaussian_speed(store.get(i), &caches[i]);
-            std::vector<Vec3> g_speed;
-            consistency_loss(speeds, knn, &g_speed);
-            for (int i = 0; i < n; ++i)
-                slice_backward(store.get(i), caches[i], Mat3::Zero(), Vec3::Zero(), 0,
-                               w.lambda_consistency * g_speed[i], &grads.g[i]);
-            seconds[7] = sec(t);
-        }
-        t = clk::now();
-        accumulate_stats(store, grads);
-        seconds[8] = sec(t);
-        t = clk::now();
-        adam_step(store, grads, cfg, step);
-        seconds[9] = sec(t);
         return 0;
     } catch (const std::exception&) {
         return 1;
