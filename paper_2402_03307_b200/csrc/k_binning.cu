@@ -872,11 +872,13 @@ __global__ void __launch_bounds__(kScatThreads) k_tile_scatter(const uint32_t* _
                 const uint32_t mask = cm[tx] & rm[ty];
                 const uint32_t c = __popc(mask);
                 // run[t] = stamp << 26 | position; stamped with this round, it already includes
-                // the round's pairs of tile t (its last rectangle has been processed)
-                const uint32_t v = run[t];
+                // the round's pairs of tile t (its last rectangle has been processed).  Lanes of
+                // the warp read it while the round's last rectangle over t may be updating it:
+                // both sides are shared-memory atomics (a read-only atomicOr, an atomicExch).
+                const uint32_t v = atomicOr(&run[t], 0u);
                 const uint32_t p0 = (v & kRunMask) - ((int)(v >> 26) == ri ? c : 0u);
                 vals[p0 + __popc(mask & ((1u << o) - 1u))] = id;
-                if (!(mask & ~((2u << o) - 1u))) run[t] = ((uint32_t)ri << 26) | (p0 + c);
+                if (!(mask & ~((2u << o) - 1u))) atomicExch(&run[t], ((uint32_t)ri << 26) | (p0 + c));
                 // next pair: next column, next band row, next rectangle with rows in the band
                 if (++tx > x1) {
                     tx = x0;

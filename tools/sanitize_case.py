@@ -1,7 +1,7 @@
 """A small end-to-end case for compute-sanitizer (tests/test_gpu_sanitizer.py): the forward
-(K1, depth ranks, scan, duplicate, radix passes, ranges, K5, FP64 fix-up), a forced-FP64
+(K1, depth ranks, the tile-major scatter binning, K5, FP64 fix-up), a forced-FP64
 forward, the backward (K6, FP64 fix-up, K7a/K7b), the deterministic backward, a batched
-render sweep over the 8 view slots, and one training step (K8, K9, K10, K11)."""
+render sweep over the 8 view slots (depth ranks, scan, duplicate, radix passes, ranges), and one training step (K8, K9, K10, K11)."""
 import os
 import sys
 
