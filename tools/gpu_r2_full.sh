@@ -12,7 +12,7 @@ timeout 900 ncu --set full --clock-control none --import-source on \
     -k regex:'k_blend_fp32|k_preprocess|k_radix_onesweep|k_duplicate|k_slice_cache' -s 40 -c 6 \
     -o gpurun_out/r2/prof_render python bench.py --profile-only --warmup 1 > gpurun_out/r2/ncu_render.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on \
-    -k regex:'k_backward_fp32|k_gaussian_backward|k_color_backward|k_adam|k_ssim_fields|k_image_grad' -s 8 -c 8 \
+    -k regex:'k_backward_fp32|k_gaussian_backward|k_color_backward|k_adam|k_ssim_fields|k_image_grad|k_tile_scatter|k_chunk_tile_counts|k_tile_offsets' -s 8 -c 11 \
     -o gpurun_out/r2/prof_train python bench.py --train-only --train-steps 1 --warmup 1 --no-cpu-baseline --no-dropin > gpurun_out/r2/ncu_train.log 2>&1
 tail -2 gpurun_out/r2/ncu_render.log gpurun_out/r2/ncu_train.log
 ls -la gpurun_out/r2 | tail -12

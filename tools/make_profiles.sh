@@ -13,6 +13,6 @@ cp $G/launches_train.csv $P/ncu_launches_train_$R.csv
 python tools/ncu_summary.py $G/prof_render.ncu-rep > $P/ncu_full_render_$R.md
 python tools/ncu_summary.py $G/prof_train.ncu-rep > $P/ncu_full_train_$R.md
 python tools/ncu_stalls.py $G/prof_render.ncu-rep 'k_blend_fp32|k_preprocess|k_radix|k_duplicate|k_slice_cache' > $P/ncu_stalls_render_$R.md
-python tools/ncu_stalls.py $G/prof_train.ncu-rep 'k_backward_fp32|k_gaussian_backward|k_color_backward|k_ssim|k_image_grad|k_adam' > $P/ncu_stalls_train_$R.md
+python tools/ncu_stalls.py $G/prof_train.ncu-rep 'k_backward_fp32|k_gaussian_backward|k_color_backward|k_ssim|k_image_grad|k_adam|k_tile_scatter|k_chunk_tile_counts|k_tile_offsets' > $P/ncu_stalls_train_$R.md
 cp $G/bench_full.json $P/bench_${R}_full.json
 ls -la $P | grep $R
