@@ -297,14 +297,34 @@ __global__ void __launch_bounds__(256) k_blend_fp64(SplatArrays sp, const uint32
         double T = 1, acc0 = 0, acc1 = 0, acc2 = 0;
         int contrib = 0;
         bool done = false;
+        // Software pipeline over the 32-entry batches: the splat ids run two batches ahead and
+        // the records one batch ahead, so their dependent L2 round trips overlap the current
+        // batch's exp and transmittance walk instead of starting it.
+        const double4* __restrict__ colrec = flow_mode ? sp.flow_radius : sp.color_depth;
+        uint32_t id1 = 0, id2 = 0;  // ids of the next batch and the one after
+        if (rg.x + lane < rg.y) id1 = vals[rg.x + lane];
+        if (rg.x + 32 + lane < rg.y) id2 = vals[rg.x + 32 + lane];
+        double2 mN = make_double2(0, 0);
+        double4 cabN = make_double4(0, 0, 0, 0), colN = make_double4(0, 0, 0, 0);
+        if (rg.x + lane < rg.y) {
+            mN = sp.mean2[id1];
+            cabN = sp.conic_ab[id1];
+            colN = colrec[id1];
+        }
         for (uint32_t base = rg.x; base < rg.y && !done; base += 32) {
             const uint32_t j = base + lane;
+            const double2 m = mN;
+            const double4 cab = cabN, col = colN;
+            // prefetch: records of batch base + 32 (ids already here), ids of batch base + 64
+            if (j + 32 < rg.y) {
+                mN = sp.mean2[id2];
+                cabN = sp.conic_ab[id2];
+                colN = colrec[id2];
+            }
+            if (j + 64 < rg.y) id2 = vals[j + 64];
             bool accept = false;
             double a = 0, c0 = 0, c1 = 0, c2 = 0;
             if (j < rg.y) {
-                const uint32_t id = vals[j];
-                const double2 m = sp.mean2[id];
-                const double4 cab = sp.conic_ab[id];
                 const double dx = x - m.x, dy = y - m.y;
                 const double power = -0.5 * (cab.x * dx * dx + cab.z * dy * dy) - cab.y * dx * dy;
                 if (!(power > 0)) {
@@ -312,17 +332,9 @@ __global__ void __launch_bounds__(256) k_blend_fp64(SplatArrays sp, const uint32
                     accept = !(a < kMinAlpha);
                 }
                 if (accept) {
-                    if (flow_mode) {
-                        const double4 f = sp.flow_radius[id];
-                        c0 = f.x;
-                        c1 = f.y;
-                        c2 = 0;
-                    } else {
-                        const double4 c = sp.color_depth[id];
-                        c0 = c.x;
-                        c1 = c.y;
-                        c2 = c.z;
-                    }
+                    c0 = col.x;
+                    c1 = col.y;
+                    c2 = flow_mode ? 0.0 : col.z;
                 }
             }
             // The transmittance walk (the only sequential part) is replayed by every lane with
@@ -553,16 +565,33 @@ __global__ void __launch_bounds__(256) k_backward_fp64(SplatArrays sp, const uin
         const double fT = final_T[pix];
         double T_run = fT;
         double s0 = bg.x * fT, s1 = bg.y * fT, s2 = bg.z * fT;
+        // Software pipeline over the 32-entry batches (as k_blend_fp64): ids two batches ahead,
+        // records one batch ahead.
+        uint32_t idN = 0, id2 = 0;
+        if (contrib - 1 - lane >= 0) idN = vals[rg.x + contrib - 1 - lane];
+        if (contrib - 33 - lane >= 0) id2 = vals[rg.x + contrib - 33 - lane];
+        double2 mN = make_double2(0, 0);
+        double4 cabN = make_double4(0, 0, 0, 0), colN = make_double4(0, 0, 0, 0);
+        if (contrib - 1 - lane >= 0) {
+            mN = sp.mean2[idN];
+            cabN = sp.conic_ab[idN];
+            colN = sp.color_depth[idN];
+        }
         for (int hi = contrib; hi > 0; hi -= 32) {
             const int pos = hi - 1 - lane;
+            const uint32_t id = idN;
+            const double2 m = mN;
+            const double4 cab = cabN, col = colN;
+            if (pos - 32 >= 0) {
+                idN = id2;
+                mN = sp.mean2[id2];
+                cabN = sp.conic_ab[id2];
+                colN = sp.color_depth[id2];
+            }
+            if (pos - 64 >= 0) id2 = vals[rg.x + pos - 64];
             bool pass = false;
             double a = 0, raw = 0, dx = 0, dy = 0, c0 = 0, c1 = 0, c2 = 0;
-            double4 cab = make_double4(0, 0, 0, 0);
-            uint32_t id = 0;
             if (pos >= 0) {
-                id = vals[rg.x + pos];
-                const double2 m = sp.mean2[id];
-                cab = sp.conic_ab[id];
                 dx = (double)x - m.x;
                 dy = (double)y - m.y;
                 const double power = -0.5 * (cab.x * dx * dx + cab.z * dy * dy) - cab.y * dx * dy;
@@ -572,10 +601,9 @@ __global__ void __launch_bounds__(256) k_backward_fp64(SplatArrays sp, const uin
                     pass = !(a < kMinAlpha);
                 }
                 if (pass) {
-                    const double4 c = sp.color_depth[id];
-                    c0 = c.x;
-                    c1 = c.y;
-                    c2 = c.z;
+                    c0 = col.x;
+                    c1 = col.y;
+                    c2 = col.z;
                 }
             }
             // The back-to-front recursion T_before = T_run / (1 - a), suffix += c a T_before over
