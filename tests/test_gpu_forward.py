@@ -188,6 +188,30 @@ def test_binning_modes_identical(orc, shape):
     print(f"{w}x{h}: {len(ref.tile_ids)} pairs, scatter == radix == oracle")
 
 
+def test_binning_large_splats(orc):
+    """Rectangles from one tile to most of the frame in the same rounds of 32 ranks (the scatter's
+    per-lane walks across owners, band rows and empty rectangles): both binnings against the
+    oracle's tile lists."""
+    store = scenes.synthetic_scene(20_000, 640, 480, seed=23)
+    big = np.random.default_rng(5).choice(store.size(), 60, replace=False)
+    store.log_scales[big, :3] += np.float32(2.5)
+    store.log_scales[big, :3] = store.log_scales[big, :3].astype(np.float32)
+    cam = scenes.bench_camera(640, 480, 0.5, scenes.yaw_pose(4.0, (0.02, 0.0, 0.05)))
+    ref_img, ref = orc.render_forward(store, cam, (0.0, 0.0, 0.0), threads=16, retain=True)
+    radius = np.asarray(ref.splats["radius"])
+    assert radius.max() > 10 * np.median(radius) and radius.max() > 80  # rectangles of 100+ tiles
+    for mode in ("scatter", "radix"):
+        c = rgs.Context(0, use_torch_stream=False)
+        c.set_binning(mode)
+        r = rgs.render_forward(store, cam, rgs.RenderOptions(retain_records=True), ctx=c)
+        assert np.array_equal(r.records.tile_offsets, ref.tile_offsets), mode
+        assert np.array_equal(r.records.tile_ids, ref.tile_ids), mode
+        assert np.array_equal(r.records.n_contrib, ref.n_contrib), mode
+        assert np.abs(r.image.astype(np.float64) - ref_img).max() <= 1e-4, mode
+    with pytest.raises(rgs.RgsCudaError, match="binning"):
+        rgs.Context(0, use_torch_stream=False).set_binning(7)
+
+
 def test_scene_params_tensor_view(ctx):
     """DeviceScene.params_tensor is a live view of the device SoA: writing through it (as an
     NCCL broadcast into a replica does) changes what the renderer sees."""
