@@ -578,14 +578,15 @@ __global__ void __launch_bounds__(256) k_digit_hist3(const uint32_t* __restrict_
 // split three ways:
 //   A  k_chunk_tile_counts -- per chunk of 32 * rounds consecutive ranks, the pair count of every
 //      tile (row difference arrays in shared memory, a warp scan per tile row);
-//   B  k_tile_offsets      -- per tile, the exclusive prefix of those counts over the chunks plus
-//      the tile's start (an exclusive scan of the tile totals: decoupled look-back over groups of
-//      32 tiles), in place; the tile ranges and the pair count;
+//   B  k_tile_offsets      -- per tile, the exclusive prefix of those counts over the chunks (in
+//      place) and the tile's total; the last block to finish scans the totals into the tile
+//      starts, the tile ranges and the pair count;
 //   C  k_tile_scatter      -- per chunk, rounds of 32 ranks: lane masks per tile column and tile row
 //      (which of the round's 32 rectangles cover it; prefix-OR of begin / end marks), so a pair's
 //      offset inside the round is popc(col_mask & row_mask & lanes below); a per-tile running
-//      position in shared memory carries the rounds.  Tile row ty belongs to warp ty % 4 of the
-//      block, so the running positions need no atomics and no cross-warp ordering.
+//      position in shared memory (tile start + chunk prefix, stamped with the round that last
+//      advanced it) carries the rounds.  Tile row ty belongs to warp ty % 4 of the block, so no
+//      two warps touch a running position; inside a warp each lane walks its own run of pairs.
 // Traffic: rect + id + count per visible splat, 4 B per pair written, and the chunk x tile count
 // matrix (written by A, read and rewritten by B, read by C) -- against 2 x 16 B per pair for the
 // two radix passes plus 8 B per pair of K3.
