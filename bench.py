@@ -864,6 +864,7 @@ def run_ours(args, rank, local_rank, world):
     sweep()
     _, (E, B, E_kernel) = ctx.profile_read()
     slow_reasons = ctx.slow_reasons()
+    visits, visits_blend = ctx.blend_visits()
     ctx.set_profiling(False, False)
     img0, rec0 = ctx.render_forward_device(scene, cams[N_TIMES // 2], retain=False)
     n_vis, n_pairs, n_slow = rec0._n_splats, rec0.n_pairs, rec0.n_slow_pixels
@@ -1016,7 +1017,9 @@ def run_ours(args, rank, local_rank, world):
                        "n_visible_mid": n_vis, "n_pairs_mid": n_pairs, "slow_pixels_mid": n_slow,
                        "evals_per_frame": e_frame, "blends_per_frame": b_frame,
                        "kernel_evals_per_frame": E_kernel / N_TIMES,
-                       "slow_pixel_reasons_per_sweep": slow_reasons},
+                       "slow_pixel_reasons_per_sweep": slow_reasons,
+                       "k5_warp_visits_per_frame": visits / N_TIMES,
+                       "k5_warp_visits_blending_per_frame": visits_blend / N_TIMES},
             "ms_per_frame": total_ms / (N_TIMES * args.steps), "wall_s": t_wall,
             "target_fps": 600, "roofline": roofline, "kernels": roof_all, "stages": per_stage, "binning": binning,
             "stages_note": "per-stage CUDA events from a serialised profiling sweep after the timed region "

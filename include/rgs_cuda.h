@@ -153,6 +153,9 @@ int rgs_ctx_profile_read(rgs_ctx* ctx, double* stage_ms, long long* stage_launch
 /* With count_evals: the FP32 blend's slow-pixel decisions by reason since the last reset --
  * out4 = {power > 0 gate, alpha >= 1/255 gate, backward clamp gate, T(1 - alpha) < 1e-4 gate}. */
 int rgs_ctx_profile_slow_reasons(rgs_ctx* ctx, unsigned long long* out4);
+/* With count_evals: the FP32 blend's warp visits since the last reset -- out2 = {survivor
+ * entries walked by a warp, of those the ones where at least one lane blended}. */
+int rgs_ctx_profile_blend_visits(rgs_ctx* ctx, unsigned long long* out2);
 /* FP32 FMA-pipe throughput of this device (FFMA probe, best of 5), TFLOP/s with FMA = 2. */
 int rgs_measure_fp32_tflops(rgs_ctx* ctx, double* tflops);
 /* FP64 FMA-pipe throughput of this device (DFMA probe, best of 5), TFLOP/s with FMA = 2: the

@@ -148,6 +148,18 @@ __device__ __forceinline__ float blend_alpha(float ab, float p) { return fminf(0
 
 constexpr unsigned kFull = 0xffffffffu;
 
+// Shared-memory loads from a 32-bit shared-window address.
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+    float4 v;
+    asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float2 lds_f2(uint32_t a) {
+    float2 v;
+    asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+    return v;
+}
+
 // K5 (round-1 form, kept for A/B runs with RGS_K5=1): forward blend.
 template <bool FLOW, bool COUNT>
 __global__ void __launch_bounds__(256, 5) k_blend_fp32_v1(SplatArrays sp, const uint32_t* __restrict__ vals,
@@ -327,6 +339,9 @@ __global__ void __launch_bounds__(256, 5) k_blend_fp32(SplatArrays sp, const uin
             float4 A, Bv, C, Dv;
             float l;
             stage_values<FLOW>(sp, vals[j], px0, py0, A, Bv, C, Dv, l);
+            // K5's merged ambiguity test (below) takes the clamp gate as p + M >= pcq with
+            // pcq = pc2 for pc2 <= 0 and the smallest positive float otherwise
+            Dv.z = Dv.z > 0.f ? __int_as_float(1) : Dv.z;
             s_a[threadIdx.x] = A;
             s_b[threadIdx.x] = Bv;
             s_c[threadIdx.x] = C;
@@ -357,41 +372,53 @@ __global__ void __launch_bounds__(256, 5) k_blend_fp32(SplatArrays sp, const uin
                 w_k[warp][q] = (uint8_t)lane;
             }
             __syncwarp();
+            unsigned bmask = 0;  // COUNT only: the window entries this lane blended
             if (!done) {
-                const StagedSplat* const first = w_list[warp];
-                const StagedSplat* const end = first + __popc(m);
-                // the last blended entry, as a 32-bit shared-memory address (0: none in this window)
+                // the survivor list walked on one 32-bit shared-memory address (a single
+                // induction variable: it is also the `last` record)
+                const uint32_t first = (uint32_t)__cvta_generic_to_shared(w_list[warp]);
+                const uint32_t end = first + (uint32_t)__popc(m) * (uint32_t)sizeof(StagedSplat);
+                // the last blended entry's address (0: none in this window)
                 uint32_t last = 0;
-                for (const StagedSplat* e = first; e != end; ++e) {
-                    const float4 a2 = e->a, b2 = e->b;
+                for (uint32_t e = first; e != end; e += (uint32_t)sizeof(StagedSplat)) {
+                    // (loading the colour / guard entries before the skip branch as well, with
+                    // volatile loads so ptxas keeps them there, measured 0.353 vs 0.328 ms)
+                    const float4 a2 = lds_f4(e), b2 = lds_f4(e + 16);
                     float p, M;
                     gate_values_x2(a2, b2, fp2, p, M);
                     if (COUNT) ++n_eval;
                     if (gate_skip(p, M, b2.z)) continue;
-                    const float4 cc = e->c;
-                    const float2 pr = make_float2(e->d.z, e->d.w);  // (pc2, R)
+                    const float4 cc = lds_f4(e + 32);
+                    const float2 pr = lds_f2(e + 56);  // (pcq, R)
                     const float al = blend_alpha(cc.w, p);
                     const float test_T = __fmul_rn(T, __fsub_rn(1.f, al));
                     const float errN = fmaf(al * M, pr.y, errT3);
                     // ambiguous alpha / power gate, or the backward's clamp gate (unclamped
-                    // alpha <= 0.99, rasterizer.cpp:356), within their error bounds
-                    const bool amb_gc = gate_ambiguous(p, M, b2.z) |
-                                        ((__fadd_rn(p, M) >= pr.x) & (__fsub_rn(p, M) <= pr.x));
-                    if (!amb_gc && fmaf(-test_T, errN, test_T) > kStopHi) {
+                    // alpha <= 0.99, rasterizer.cpp:356), within their error bounds, as one
+                    // superset test: p > -M (exactly: RN(p + M) > 0, i.e. >= the smallest
+                    // positive float) or RN(p - M) <= pa2 or [RN(p + M) >= pc2 and
+                    // RN(p - M) <= pc2] all imply RN(p + M) >= pcq or RN(p - M) <= pa2 (pcq:
+                    // staging).  The extra pixels it sends to the FP64 fix-up are those within
+                    // |p| < 0.0145 of the centre of a splat with alpha_base > 0.99.
+                    const bool amb_gc = (__fadd_rn(p, M) >= pr.x) | (__fsub_rn(p, M) <= b2.z);
+                    if (!amb_gc & (fmaf(-test_T, errN, test_T) > kStopHi)) {  // one branch: both tests evaluated
                         const float w = al * T;
                         acc01 = __ffma2_rn(make_float2(cc.x, cc.y), make_float2(w, w), acc01);
                         acc2 = fmaf(cc.z, w, acc2);
                         T = test_T;
                         errT3 = errN + 3e-7f;
-                        last = (uint32_t)__cvta_generic_to_shared(e);
-                        if (COUNT) ++n_blend;
+                        last = e;
+                        if (COUNT) {
+                            ++n_blend;
+                            bmask |= 1u << (int)((e - first) / sizeof(StagedSplat));
+                        }
                         continue;
                     }
                     // rare: certainly stop (rasterizer.cpp:111, the splat is not blended), or a
                     // decision inside its error bound -> the pixel goes to the FP64 fix-up
                     if (!amb_gc && fmaf(test_T, errN, test_T) < kStopLo) {
                         done = stopped = true;
-                        if (COUNT) n_ref = start - rg.x + c + w_k[warp][e - first] + 1;
+                        if (COUNT) n_ref = start - rg.x + c + w_k[warp][(e - first) / sizeof(StagedSplat)] + 1;
                         break;
                     }
                     if (COUNT) {
@@ -404,11 +431,19 @@ __global__ void __launch_bounds__(256, 5) k_blend_fp32(SplatArrays sp, const uin
                     break;
                 }
                 if (last) {
-                    const int lastq = (int)((last - (uint32_t)__cvta_generic_to_shared(first)) / sizeof(StagedSplat));
+                    const int lastq = (int)((last - first) / sizeof(StagedSplat));
                     contrib = (int)(start - rg.x) + c + w_k[warp][lastq] + 1;
                 }
             }
             __syncwarp();  // the list is rewritten by the next window
+            if (COUNT) {
+                // warp visits of the window (entries walked) and those where some lane blended
+                const unsigned anyb = __reduce_or_sync(kFull, bmask);
+                if (lane == 0 && __popc(m)) {
+                    atomicAdd(counters + 7, (unsigned long long)__popc(m));
+                    atomicAdd(counters + 8, (unsigned long long)__popc(anyb));
+                }
+            }
             if (__all_sync(kFull, done)) {
                 warp_done = true;
                 break;
@@ -870,7 +905,7 @@ __global__ void __launch_bounds__(kBwdThreads) k_backward_fp32(SplatArrays sp, c
 namespace rgs_launch {
 using namespace rgs_dev;
 
-static int g_k5_variant = 2;  // RGS_K5=1 selects the round-1 kernel (A/B measurements)
+static int g_k5_variant = 2;  // RGS_K5=1: round-1 kernel, 3: two pixels per lane (A/B)
 
 void blend_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges, const DevCamera& cam,
                 float3 bg, int flow_mode, float* image, double* final_T, uint32_t* n_contrib, uint32_t* slow_list,

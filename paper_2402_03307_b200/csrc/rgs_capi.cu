@@ -224,7 +224,7 @@ struct rgs_ctx {
     std::vector<Pending> pending;
     double stage_ms[kNumStages] = {0};
     long long stage_n[kNumStages] = {0};
-    DevBuf counters;  // 3 x u64: E, B, E_kernel of the FP32 blend
+    DevBuf counters;  // 16 x u64: E, B, E_kernel of the FP32 blend, slow reasons (3-6), warp visits (7, 8)
     // multi-view batches (render_batch)
     static constexpr int kSlots = 8;
     Frame slot_frame[kSlots];
@@ -739,8 +739,8 @@ int rgs_ctx_set_profiling(rgs_ctx* c, int timing, int count_evals) {
         c->timing = timing < 0 ? 0 : (timing > 2 ? 1 : timing);
         c->count_evals = count_evals != 0;
         if (c->count_evals) {
-            c->counters.ensure(64, c->stream);
-            CK(cudaMemsetAsync(c->counters.p, 0, 64, c->stream));
+            c->counters.ensure(128, c->stream);
+            CK(cudaMemsetAsync(c->counters.p, 0, 128, c->stream));
         }
         return RGS_OK;
     });
@@ -811,7 +811,7 @@ int rgs_ctx_profile_reset(rgs_ctx* c) {
             c->stage_ms[k] = 0;
             c->stage_n[k] = 0;
         }
-        if (c->counters.p) CK(cudaMemsetAsync(c->counters.p, 0, 64, c->stream));
+        if (c->counters.p) CK(cudaMemsetAsync(c->counters.p, 0, 128, c->stream));
         return RGS_OK;
     });
 }
@@ -839,6 +839,17 @@ int rgs_ctx_profile_slow_reasons(rgs_ctx* c, unsigned long long* out4) {
         for (int k = 0; k < 4; ++k) out4[k] = 0;
         if (!c->counters.p) return RGS_OK;
         CK(cudaMemcpyAsync(out4, c->counters.as<unsigned long long>() + 3, 32, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        return RGS_OK;
+    });
+}
+
+int rgs_ctx_profile_blend_visits(rgs_ctx* c, unsigned long long* out2) {
+    if (!out2) return RGS_E_INVALID;
+    return guarded(c, [&]() -> int {
+        out2[0] = out2[1] = 0;
+        if (!c->counters.p) return RGS_OK;
+        CK(cudaMemcpyAsync(out2, c->counters.as<unsigned long long>() + 7, 16, cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
         return RGS_OK;
     });

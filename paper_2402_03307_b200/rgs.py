@@ -172,7 +172,7 @@ EXPORTS = [
     "rgs_rng_create", "rgs_rng_destroy", "rgs_rng_uniform_int", "rgs_densify_and_prune",
     "rgs_knn_query", "rgs_consistency_loss", "rgs_image_loss_f64", "rgs_entropy_loss", "rgs_accumulate_stats",
     "rgs_rng_get_state", "rgs_rng_set_state", "rgs_malloc", "rgs_free", "rgs_memcpy",
-    "rgs_accumulate_stats_f64", "rgs_ctx_profile_slow_reasons", "rgs_measure_fp64_tflops",
+    "rgs_accumulate_stats_f64", "rgs_ctx_profile_slow_reasons", "rgs_ctx_profile_blend_visits", "rgs_measure_fp64_tflops",
     # multi-GPU (train.NcclComm)
     "rgs_nccl_available", "rgs_nccl_unique_id", "rgs_nccl_comm_create", "rgs_nccl_comm_destroy",
     "rgs_allreduce_grads", "rgs_image_loss_ex", "rgs_ctx_set_binning",
@@ -262,6 +262,7 @@ def load_library(path: str = LIB_PATH):
         "rgs_accumulate_stats": (i, [p, p, p, p]),
         "rgs_accumulate_stats_f64": (i, [p, p, p, p]),
         "rgs_ctx_profile_slow_reasons": (i, [p, p]),
+        "rgs_ctx_profile_blend_visits": (i, [p, p]),
         "rgs_rng_get_state": (i, [p, p, ctypes.c_size_t, p]),
         "rgs_rng_set_state": (i, [p, ctypes.c_char_p]),
         "rgs_malloc": (p, [p, ctypes.c_size_t]),
@@ -547,6 +548,12 @@ class Context:
         out = (ctypes.c_ulonglong * 4)()
         self.check(self.L.rgs_ctx_profile_slow_reasons(self.h, out))
         return dict(zip(("power_gate", "alpha_gate", "clamp_gate", "T_gate"), [int(x) for x in out]))
+
+    def blend_visits(self):
+        """(warp visits, visits where some lane blended) of the FP32 blend (count_evals profiling)."""
+        out = (ctypes.c_ulonglong * 2)()
+        self.check(self.L.rgs_ctx_profile_blend_visits(self.h, out))
+        return int(out[0]), int(out[1])
 
     def measure_fp32_tflops(self) -> float:
         v = ctypes.c_double(0)
