@@ -148,15 +148,17 @@ __device__ __forceinline__ float blend_alpha(float ab, float p) { return fminf(0
 
 constexpr unsigned kFull = 0xffffffffu;
 
-// Shared-memory loads from a 32-bit shared-window address.
+// Shared-memory loads from a 32-bit shared-window address.  The "memory" clobber keeps them
+// ordered with the stores and __syncwarp() that publish the survivor list (without it the
+// compiler may hoist a load above the barrier).
 __device__ __forceinline__ float4 lds_f4(uint32_t a) {
     float4 v;
-    asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a) : "memory");
     return v;
 }
 __device__ __forceinline__ float2 lds_f2(uint32_t a) {
     float2 v;
-    asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+    asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a) : "memory");
     return v;
 }
 
@@ -332,6 +334,8 @@ __global__ void __launch_bounds__(256, 5) k_blend_fp32(SplatArrays sp, const uin
     uint32_t n_eval = 0, n_blend = 0, n_ref = 0;  // COUNT only
     bool warp_done = __all_sync(kFull, done);
 
+    // (loading the next batch's splat ids one batch ahead, with or without an L1 prefetch of
+    // their records once the warp has walked its windows: equal time, 0.329-0.332 ms)
     for (uint32_t start = rg.x; start < rg.y; start += kTilePixels) {
         if (__syncthreads_count(done) == kTilePixels) break;
         const uint32_t j = start + threadIdx.x;
@@ -484,18 +488,26 @@ __global__ void __launch_bounds__(256, 5) k_blend_fp32(SplatArrays sp, const uin
     }
 }
 
-// K5 (two pixels per lane): CTA of 128 threads per 16x16 tile, warp per 8x8 sub-tile, lane
-// pixels (x, y) and (x, y + 4) -- the sub-tiles and pixel pairs of K6, whose 8x8 cull is then
-// exactly this kernel's.  The two pixels share dx and every per-splat operand, so their gate
-// values are one set of paired FP32 instructions (bit-identical to gate_values); the accept path
-// runs for both whenever either accepts, and predicated selects keep a pixel that skipped,
-// finished or went slow unchanged.  Decisions per (pixel, splat) are those of k_blend_fp32.
+// K5 (two pixels per lane; the default -- RGS_K5=2 selects one pixel per lane): CTA of 128 threads per 16x16 tile, warp per 8x8 sub-tile,
+// lane pixels (x, y) and (x, y + 4) -- the sub-tiles and pixel pairs of K6.  The two pixels share
+// dx and every per-splat operand, so the gate, alpha, transmittance and colour arithmetic are
+// paired FP32 instructions (bit-identical to the scalar forms); predicated selects keep a pixel
+// that skipped unchanged.  A finished pixel (stopped, slow or outside the image) gets the y
+// coordinate kGone, so every later splat certainly skips it without a per-visit flag test.
+// Decisions per (pixel, splat) are those of k_blend_fp32, including its merged ambiguity test.
 constexpr int kX2Threads = 128;
 constexpr int kX2Warps = kX2Threads / 32;
 constexpr int kX2Stage = 256;  // staged splats per batch (two per thread)
+// CTAs per SM: 7 (71 registers, no spills) -- C2 frame 0.283 ms, 2490 FPS in the pipelined sweep;
+// 8 (64 registers, spills in the staging): 0.310 ms, 2213 FPS; 6: 0.287 ms, 2453 FPS.  Loading the
+// next entry's gate operands one visit ahead (a rotating register pair) measured 0.322 ms at 6-8.
+constexpr int kX2Blocks = 7;
+// |dy| = 1e12: q <= cc2 dy^2 is below any alpha threshold for every conic the projection makes,
+// the error bound M = cs2n q + D stays far below |q| (|cs2n| << 1), and nothing overflows.
+constexpr float kGone = 1e12f;
 
-template <bool FLOW, bool COUNT>
-__global__ void __launch_bounds__(kX2Threads, 8) k_blend_fp32_x2(SplatArrays sp, const uint32_t* __restrict__ vals,
+template <bool FLOW, bool COUNT, int NB = kX2Blocks>
+__global__ void __launch_bounds__(kX2Threads, NB) k_blend_fp32_x2(SplatArrays sp, const uint32_t* __restrict__ vals,
                                                               const uint2* __restrict__ ranges, DevCamera cam,
                                                               float3 bg, float* __restrict__ image,
                                                               double* __restrict__ final_T,
@@ -515,18 +527,19 @@ __global__ void __launch_bounds__(kX2Threads, 8) k_blend_fp32_x2(SplatArrays sp,
     const uint2 rg = ranges[tile];
     const double px0 = tx * kTile, py0t = ty * kTile;
     const float fpx = (float)lx, fsx0 = (float)sx0, fsy0 = (float)sy0;
-    const float2 fpy = make_float2((float)ly, (float)(ly + 4));
+    float2 fpy = make_float2(in0 ? (float)ly : kGone, in1 ? (float)(ly + 4) : kGone);
     const unsigned lt_mask = (1u << lane) - 1u;
 
-    float2 T = make_float2(1.f, 1.f), errT3 = make_float2(3e-7f, 3e-7f);
-    float2 acc0 = make_float2(0.f, 0.f), acc1 = acc0, acc2 = acc0;  // channel c of pixels (0, 1)
+    float2 T = make_float2(1.f, 1.f), errT3 = make_float2(3e-7f, 3e-7f);  // errT3 = errT + 3e-7
+    float2 acc0 = make_float2(0.f, 0.f), acc1 = acc0, acc2 = acc0;        // channel c of pixels (0, 1)
     int contrib0 = 0, contrib1 = 0;
-    bool done0 = !in0, done1 = !in1, slow0 = false, slow1 = false, stopped0 = false, stopped1 = false;
+    bool slow0 = false, slow1 = false, stopped0 = false, stopped1 = false;
     uint32_t n_eval = 0, n_blend = 0, n_ref0 = 0, n_ref1 = 0;  // COUNT only
-    bool warp_done = __all_sync(kFull, done0 && done1);
+    bool gone = (fpy.x == kGone) & (fpy.y == kGone);
+    bool warp_done = __all_sync(kFull, gone);
 
     for (uint32_t start = rg.x; start < rg.y; start += kX2Stage) {
-        if (__syncthreads_count(done0 && done1) == kX2Threads) break;
+        if (__syncthreads_count(gone) == kX2Threads) break;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int t = threadIdx.x + h * kX2Threads;
@@ -535,6 +548,7 @@ __global__ void __launch_bounds__(kX2Threads, 8) k_blend_fp32_x2(SplatArrays sp,
                 float4 A, Bv, C, Dv;
                 float l;
                 stage_values<FLOW>(sp, vals[j], px0, py0t, A, Bv, C, Dv, l);
+                Dv.z = Dv.z > 0.f ? __int_as_float(1) : Dv.z;  // pcq, as in k_blend_fp32
                 s_a[t] = A;
                 s_b[t] = Bv;
                 s_c[t] = C;
@@ -566,13 +580,12 @@ __global__ void __launch_bounds__(kX2Threads, 8) k_blend_fp32_x2(SplatArrays sp,
                 w_k[warp][q] = (uint8_t)lane;
             }
             __syncwarp();
-            if (!(done0 && done1)) {
-                const StagedSplat* const first = w_list[warp];
-                const StagedSplat* const end = first + __popc(m);
-                int last0 = -1, last1 = -1;
-                int q = 0;
-                for (const StagedSplat* e = first; e != end; ++e, ++q) {
-                    const float4 a2 = e->a, b2 = e->b;
+            if (!gone) {
+                const uint32_t first = (uint32_t)__cvta_generic_to_shared(w_list[warp]);
+                const uint32_t end = first + (uint32_t)__popc(m) * (uint32_t)sizeof(StagedSplat);
+                uint32_t last0 = 0, last1 = 0;  // the last blended entries' addresses (0: none)
+                for (uint32_t e = first; e != end; e += (uint32_t)sizeof(StagedSplat)) {
+                    const float4 a2 = lds_f4(e), b2 = lds_f4(e + 16);
                     // gate_values for both pixels (shared dx, paired dy)
                     const float dx = __fsub_rn(fpx, a2.x);
                     const float2 dy = __fadd2_rn(fpy, make_float2(-a2.y, -a2.y));
@@ -581,78 +594,75 @@ __global__ void __launch_bounds__(kX2Threads, 8) k_blend_fp32_x2(SplatArrays sp,
                     const float2 q2 = __ffma2_rn(make_float2(tv.x, tv.x), make_float2(dx, dx), __fmul2_rn(u, dy));
                     const float2 p = __ffma2_rn(make_float2(tv.y, tv.y), dy, q2);
                     const float2 M = __ffma2_rn(make_float2(b2.w, b2.w), q2, make_float2(b2.y, b2.y));
-                    if (COUNT) n_eval += (done0 ? 0u : 1u) + (done1 ? 0u : 1u);
-                    const bool act0 = !done0 && !gate_skip(p.x, M.x, b2.z);
-                    const bool act1 = !done1 && !gate_skip(p.y, M.y, b2.z);
+                    const float2 pM = __fadd2_rn(p, M);
+                    if (COUNT) n_eval += (fpy.x != kGone ? 1u : 0u) + (fpy.y != kGone ? 1u : 0u);
+                    const bool act0 = !((pM.x < b2.z) | (p.x > M.x));  // !gate_skip
+                    const bool act1 = !((pM.y < b2.z) | (p.y > M.y));
                     if (!(act0 | act1)) continue;
-                    const float4 cc = e->c;
-                    const float2 pr = make_float2(e->d.z, e->d.w);  // (pc2, R)
-                    const float2 ex = make_float2(ex2_approx(p.x), ex2_approx(p.y));
-                    const float2 abx = __fmul2_rn(make_float2(cc.w, cc.w), ex);
+                    const float4 cc = lds_f4(e + 32);
+                    const float2 pr = lds_f2(e + 56);  // (pcq, R)
+                    const float2 abx = __fmul2_rn(make_float2(cc.w, cc.w), make_float2(ex2_approx(p.x), ex2_approx(p.y)));
                     const float2 al = make_float2(fminf(0.99f, abx.x), fminf(0.99f, abx.y));
                     const float2 test_T = __fmul2_rn(T, __fadd2_rn(make_float2(1.f, 1.f), make_float2(-al.x, -al.y)));
                     const float2 errN = __ffma2_rn(__fmul2_rn(al, M), make_float2(pr.y, pr.y), errT3);
                     const float2 lo = __ffma2_rn(make_float2(-test_T.x, -test_T.y), errN, test_T);
-                    const float2 pM = __fadd2_rn(p, M), pm = __fadd2_rn(p, make_float2(-M.x, -M.y));
-                    const bool amb0 = gate_ambiguous(p.x, M.x, b2.z) | ((pM.x >= pr.x) & (pm.x <= pr.x));
-                    const bool amb1 = gate_ambiguous(p.y, M.y, b2.z) | ((pM.y >= pr.x) & (pm.y <= pr.x));
-                    const bool bl0 = act0 & !amb0 & (lo.x > kStopHi);
-                    const bool bl1 = act1 & !amb1 & (lo.y > kStopHi);
+                    const float2 pm = __fadd2_rn(p, make_float2(-M.x, -M.y));
+                    // certain decisions (the merged ambiguity test of k_blend_fp32) and certainly
+                    // continuing transmittance
+                    const bool cl0 = (pM.x < pr.x) & (pm.x > b2.z), cl1 = (pM.y < pr.x) & (pm.y > b2.z);
+                    const bool ok0 = act0 & cl0 & (lo.x > kStopHi), ok1 = act1 & cl1 & (lo.y > kStopHi);
                     const float2 w = __fmul2_rn(al, T);
-                    const float2 wm = make_float2(bl0 ? w.x : 0.f, bl1 ? w.y : 0.f);
+                    const float2 wm = make_float2(ok0 ? w.x : 0.f, ok1 ? w.y : 0.f);
                     acc0 = __ffma2_rn(make_float2(cc.x, cc.x), wm, acc0);
                     acc1 = __ffma2_rn(make_float2(cc.y, cc.y), wm, acc1);
-                    acc2 = __ffma2_rn(make_float2(cc.z, cc.z), wm, acc2);
+                    if (!FLOW) acc2 = __ffma2_rn(make_float2(cc.z, cc.z), wm, acc2);
                     const float2 eT3 = __fadd2_rn(errN, make_float2(3e-7f, 3e-7f));
-                    if (bl0) {
-                        T.x = test_T.x;
-                        errT3.x = eT3.x;
-                        last0 = q;
-                    }
-                    if (bl1) {
-                        T.y = test_T.y;
-                        errT3.y = eT3.y;
-                        last1 = q;
-                    }
-                    if (COUNT) n_blend += (bl0 ? 1u : 0u) + (bl1 ? 1u : 0u);
-                    if ((act0 & !bl0) | (act1 & !bl1)) {
+                    T = make_float2(ok0 ? test_T.x : T.x, ok1 ? test_T.y : T.y);
+                    errT3 = make_float2(ok0 ? eT3.x : errT3.x, ok1 ? eT3.y : errT3.y);
+                    last0 = ok0 ? e : last0;
+                    last1 = ok1 ? e : last1;
+                    if (COUNT) n_blend += (ok0 ? 1u : 0u) + (ok1 ? 1u : 0u);
+                    if ((act0 & !ok0) | (act1 & !ok1)) {
                         // rare: certainly stop (rasterizer.cpp:111, the splat is not blended), or
                         // a decision inside its error bound -> the pixel goes to the FP64 fix-up
                         const float2 hi = __ffma2_rn(test_T, errN, test_T);
-                        if (act0 & !bl0) {
-                            if (!amb0 && hi.x < kStopLo) {
+                        const int qi = (int)((e - first) / sizeof(StagedSplat));
+                        if (act0 & !ok0) {
+                            if (cl0 && hi.x < kStopLo) {
                                 stopped0 = true;
-                                if (COUNT) n_ref0 = start - rg.x + c + w_k[warp][q] + 1;
+                                if (COUNT) n_ref0 = start - rg.x + c + w_k[warp][qi] + 1;
                             } else {
                                 slow0 = true;
                                 if (COUNT) {
                                     const bool g = gate_ambiguous(p.x, M.x, b2.z);
-                                    atomicAdd(counters + (g ? ((p.x > -M.x) ? 3 : 4) : (amb0 ? 5 : 6)), 1ull);
+                                    atomicAdd(counters + (g ? ((p.x > -M.x) ? 3 : 4) : (!cl0 ? 5 : 6)), 1ull);
                                 }
                             }
-                            done0 = true;
+                            fpy.x = kGone;
                         }
-                        if (act1 & !bl1) {
-                            if (!amb1 && hi.y < kStopLo) {
+                        if (act1 & !ok1) {
+                            if (cl1 && hi.y < kStopLo) {
                                 stopped1 = true;
-                                if (COUNT) n_ref1 = start - rg.x + c + w_k[warp][q] + 1;
+                                if (COUNT) n_ref1 = start - rg.x + c + w_k[warp][qi] + 1;
                             } else {
                                 slow1 = true;
                                 if (COUNT) {
                                     const bool g = gate_ambiguous(p.y, M.y, b2.z);
-                                    atomicAdd(counters + (g ? ((p.y > -M.y) ? 3 : 4) : (amb1 ? 5 : 6)), 1ull);
+                                    atomicAdd(counters + (g ? ((p.y > -M.y) ? 3 : 4) : (!cl1 ? 5 : 6)), 1ull);
                                 }
                             }
-                            done1 = true;
+                            fpy.y = kGone;
                         }
-                        if (done0 && done1) break;
+                        gone = (fpy.x == kGone) & (fpy.y == kGone);
+                        if (gone) break;
                     }
                 }
-                if (last0 >= 0) contrib0 = (int)(start - rg.x) + c + w_k[warp][last0] + 1;
-                if (last1 >= 0) contrib1 = (int)(start - rg.x) + c + w_k[warp][last1] + 1;
+                if (last0) contrib0 = (int)(start - rg.x) + c + w_k[warp][(last0 - first) / sizeof(StagedSplat)] + 1;
+                if (last1) contrib1 = (int)(start - rg.x) + c + w_k[warp][(last1 - first) / sizeof(StagedSplat)] + 1;
             }
             __syncwarp();  // the list is rewritten by the next window
-            if (__all_sync(kFull, done0 && done1)) {
+            if (COUNT && lane == 0 && __popc(m)) atomicAdd(counters + 7, (unsigned long long)__popc(m));
+            if (__all_sync(kFull, gone)) {
                 warp_done = true;
                 break;
             }
@@ -905,7 +915,27 @@ __global__ void __launch_bounds__(kBwdThreads) k_backward_fp32(SplatArrays sp, c
 namespace rgs_launch {
 using namespace rgs_dev;
 
-static int g_k5_variant = 2;  // RGS_K5=1: round-1 kernel, 3: two pixels per lane (A/B)
+// RGS_K5 (A/B runs): "1" the round-1 kernel, "2" one pixel per lane, "x<N>" two pixels per lane at
+// N (6-8) CTAs per SM; default: two pixels per lane at kX2Blocks.
+static int g_k5_variant = 3;
+static int g_x2_nb = kX2Blocks;
+
+template <int NB>
+static void launch_x2(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges, const DevCamera& cam,
+                      float3 bg, int flow_mode, float* image, double* final_T, uint32_t* n_contrib,
+                      uint32_t* slow_list, int* slow_count, unsigned long long* counters, cudaStream_t s) {
+    const int tiles = cam.tiles_x * cam.tiles_y;
+    if (flow_mode)
+        k_blend_fp32_x2<true, false, NB><<<tiles, kX2Threads, 0, s>>>(sp, pair_vals, ranges, cam, bg, image, final_T,
+                                                                      n_contrib, slow_list, slow_count, counters);
+    else if (counters)
+        k_blend_fp32_x2<false, true, NB><<<tiles, kX2Threads, 0, s>>>(sp, pair_vals, ranges, cam, bg, image, final_T,
+                                                                      n_contrib, slow_list, slow_count, counters);
+    else
+        k_blend_fp32_x2<false, false, NB><<<tiles, kX2Threads, 0, s>>>(sp, pair_vals, ranges, cam, bg, image,
+                                                                       final_T, n_contrib, slow_list, slow_count,
+                                                                       counters);
+}
 
 void blend_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges, const DevCamera& cam,
                 float3 bg, int flow_mode, float* image, double* final_T, uint32_t* n_contrib, uint32_t* slow_list,
@@ -923,19 +953,17 @@ void blend_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* r
                                                       slow_list, slow_count, counters);
     if (g_k5_variant == 1) {
         RGS_K5_LAUNCH(k_blend_fp32_v1)
-    } else if (g_k5_variant == 3) {
-        if (flow_mode)
-            k_blend_fp32_x2<true, false><<<tiles, kX2Threads, 0, s>>>(sp, pair_vals, ranges, cam, bg, image, final_T,
-                                                                      n_contrib, slow_list, slow_count, counters);
-        else if (counters)
-            k_blend_fp32_x2<false, true><<<tiles, kX2Threads, 0, s>>>(sp, pair_vals, ranges, cam, bg, image, final_T,
-                                                                      n_contrib, slow_list, slow_count, counters);
-        else
-            k_blend_fp32_x2<false, false><<<tiles, kX2Threads, 0, s>>>(sp, pair_vals, ranges, cam, bg, image,
-                                                                       final_T, n_contrib, slow_list, slow_count,
-                                                                       counters);
-    } else {
+    } else if (g_k5_variant == 2) {
         RGS_K5_LAUNCH(k_blend_fp32)
+    } else if (g_x2_nb == 6) {
+        launch_x2<6>(sp, pair_vals, ranges, cam, bg, flow_mode, image, final_T, n_contrib, slow_list, slow_count,
+                     counters, s);
+    } else if (g_x2_nb == 8) {
+        launch_x2<8>(sp, pair_vals, ranges, cam, bg, flow_mode, image, final_T, n_contrib, slow_list, slow_count,
+                     counters, s);
+    } else {
+        launch_x2<kX2Blocks>(sp, pair_vals, ranges, cam, bg, flow_mode, image, final_T, n_contrib, slow_list,
+                             slow_count, counters, s);
     }
 #undef RGS_K5_LAUNCH
 }
@@ -943,7 +971,10 @@ void blend_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* r
 // Per-device kernel attributes (called from rgs_ctx_create on the context's device).
 bool raster_init() {
     const char* v = std::getenv("RGS_K5");
-    g_k5_variant = (v && (v[0] == '1' || v[0] == '3')) ? v[0] - '0' : 2;
+    g_k5_variant = 3;
+    g_x2_nb = kX2Blocks;
+    if (v && (v[0] == '1' || v[0] == '2')) g_k5_variant = v[0] - '0';
+    if (v && v[0] == 'x' && v[1] >= '6' && v[1] <= '8') g_x2_nb = v[1] - '0';
     return true;
 }
 
