@@ -596,8 +596,11 @@ __global__ void __launch_bounds__(kX2Threads, NB) k_blend_fp32_x2(SplatArrays sp
                     const float2 M = __ffma2_rn(make_float2(b2.w, b2.w), q2, make_float2(b2.y, b2.y));
                     const float2 pM = __fadd2_rn(p, M);
                     if (COUNT) n_eval += (fpy.x != kGone ? 1u : 0u) + (fpy.y != kGone ? 1u : 0u);
-                    const bool act0 = !((pM.x < b2.z) | (p.x > M.x));  // !gate_skip
-                    const bool act1 = !((pM.y < b2.z) | (p.y > M.y));
+                    // act: not certainly below the alpha threshold.  gate_skip's other half, power
+                    // > 0 for certain (p > M), is left to the rare path below: such a pixel fails
+                    // the merged test (p + M < pcq <= the smallest positive float), so it never
+                    // blends, and the rare path skips it without a state change.
+                    const bool act0 = !(pM.x < b2.z), act1 = !(pM.y < b2.z);
                     if (!(act0 | act1)) continue;
                     const float4 cc = lds_f4(e + 32);
                     const float2 pr = lds_f2(e + 56);  // (pcq, R)
@@ -609,8 +612,9 @@ __global__ void __launch_bounds__(kX2Threads, NB) k_blend_fp32_x2(SplatArrays sp
                     const float2 pm = __fadd2_rn(p, make_float2(-M.x, -M.y));
                     // certain decisions (the merged ambiguity test of k_blend_fp32) and certainly
                     // continuing transmittance
+                    // (cl implies act: p - M > pa2 gives p + M > pa2)
                     const bool cl0 = (pM.x < pr.x) & (pm.x > b2.z), cl1 = (pM.y < pr.x) & (pm.y > b2.z);
-                    const bool ok0 = act0 & cl0 & (lo.x > kStopHi), ok1 = act1 & cl1 & (lo.y > kStopHi);
+                    const bool ok0 = cl0 & (lo.x > kStopHi), ok1 = cl1 & (lo.y > kStopHi);
                     const float2 w = __fmul2_rn(al, T);
                     const float2 wm = make_float2(ok0 ? w.x : 0.f, ok1 ? w.y : 0.f);
                     acc0 = __ffma2_rn(make_float2(cc.x, cc.x), wm, acc0);
@@ -627,7 +631,7 @@ __global__ void __launch_bounds__(kX2Threads, NB) k_blend_fp32_x2(SplatArrays sp
                         // a decision inside its error bound -> the pixel goes to the FP64 fix-up
                         const float2 hi = __ffma2_rn(test_T, errN, test_T);
                         const int qi = (int)((e - first) / sizeof(StagedSplat));
-                        if (act0 & !ok0) {
+                        if (act0 & !ok0 & !(p.x > M.x)) {
                             if (cl0 && hi.x < kStopLo) {
                                 stopped0 = true;
                                 if (COUNT) n_ref0 = start - rg.x + c + w_k[warp][qi] + 1;
@@ -640,7 +644,7 @@ __global__ void __launch_bounds__(kX2Threads, NB) k_blend_fp32_x2(SplatArrays sp
                             }
                             fpy.x = kGone;
                         }
-                        if (act1 & !ok1) {
+                        if (act1 & !ok1 & !(p.y > M.y)) {
                             if (cl1 && hi.y < kStopLo) {
                                 stopped1 = true;
                                 if (COUNT) n_ref1 = start - rg.x + c + w_k[warp][qi] + 1;

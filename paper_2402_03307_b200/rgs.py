@@ -26,7 +26,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librgs_cuda.so")
+LIB_PATH = os.environ.get("RGS_LIB") or os.path.join(_HERE, "librgs_cuda.so")  # RGS_LIB: A/B runs of another build
 
 # ----------------------------------------------------------------------------- errors
 RGS_OK = 0
