@@ -43,7 +43,7 @@ __device__ __forceinline__ uint32_t d_tile_rect(double mx, double my, double r, 
 // alpha = alpha_base * 2^p2 with one MUFU.EX2:
 //   conic_f = (ca2, cb2, cc2, ab),  p2 = ca2 dx^2 + cc2 dy^2 + cb2 dx dy
 //   color_f = (r, g, b, pa2),        pa2 = log2(1/(255 ab))   alpha gate: p2 < pa2
-//   guard_f = (cs2n, pc2),           pc2 = log2(0.99 / ab)    clamp gate: p2 <= pc2
+//   guard_f = (cs2n, pc2, R, lmax),  pc2 = log2(0.99 / ab)    clamp gate: p2 <= pc2
 //   ext_f   = (ex, ey, gx2, gy2)     bbox half-extents of the alpha ellipse (per-warp
 //                                    culling) and max |dp2/dx|, |dp2/dy| inside it.
 // cs2n * q (q = ca2 dx^2 + cc2 dy^2 <= 0) bounds the FP32 rounding error of p2.
@@ -63,10 +63,20 @@ __device__ __forceinline__ void d_blend_record(const SplatArrays& out, int i, do
     const double ey = sqrt(L * fmax(s11, 0.0)) * (1 + 1e-3) + 1e-2;
     const double gx = kLog2e * sqrt(L * fmax(ca, 0.0));
     const double gy = kLog2e * sqrt(L * fmax(cc, 0.0));
-    out.conic_f[i] = make_float4((float)(-0.5 * kLog2e * ca), (float)(-kLog2e * cb), (float)(-0.5 * kLog2e * cc),
-                                 (float)ab);
+    const float4 cf = make_float4((float)(-0.5 * kLog2e * ca), (float)(-kLog2e * cb), (float)(-0.5 * kLog2e * cc),
+                                  (float)ab);
+    out.conic_f[i] = cf;
     out.color_f[i] = make_float4((float)r, (float)g, (float)b, (float)(kLog2e * pa));
-    out.guard_f[i] = make_float2((float)(-2.0 * cs), (float)log2(kAlphaClamp / ab));
+    // The blend kernels' per-splat constants, once per splat here instead of once per (tile, splat)
+    // staging: R >= ln2 / (1 - min(0.99, ab)) (the T-gate's error growth per blend, rounded up) and
+    // lmax >= the largest eigenvalue of the log2-power form (the radial cull), both from the FP32
+    // conic K5 / K6 evaluate.
+    const float am = fminf(0.99f, cf.w);
+    const float R = __fmul_ru(__fdiv_ru(1.f, __fsub_rd(1.f, am)), 0.6931472f * 1.000001f);
+    const float h = 0.5f * (cf.x + cf.z), dd = 0.5f * (cf.x - cf.z), o = 0.5f * cf.y;
+    const float lm = h + sqrtf(fmaf(dd, dd, o * o));
+    const float lmax = lm + 1e-5f * (fabsf(cf.x) + fabsf(cf.z) + fabsf(cf.y));
+    out.guard_f[i] = make_float4((float)(-2.0 * cs), (float)log2(kAlphaClamp / ab), R, lmax);
     out.ext_f[i] = make_float4(isfinite(ex) ? (float)ex : 3e38f, isfinite(ey) ? (float)ey : 3e38f, (float)gx,
                                (float)gy);
 }

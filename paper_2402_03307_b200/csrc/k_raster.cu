@@ -36,7 +36,7 @@ __device__ __forceinline__ void stage_values(const SplatArrays& sp, uint32_t id,
     const float mx = (float)(m.x - px0), my = (float)(m.y - py0);
     const float4 cf = sp.conic_f[id];
     const float4 col = sp.color_f[id];
-    const float2 g = sp.guard_f[id];
+    const float4 g = sp.guard_f[id];
     const float4 e = sp.ext_f[id];
     const float D = 1.5e-6f + 1.2e-7f * (fabsf(mx) * e.z + fabsf(my) * e.w);
     A = make_float4(mx, my, cf.x, cf.y);
@@ -49,15 +49,13 @@ __device__ __forceinline__ void stage_values(const SplatArrays& sp, uint32_t id,
     }
     // The T-gate's per-blend error growth alpha ln2 M / (1 - alpha) (M bounds the error of the
     // log2 power, so ln2 M bounds the relative error of alpha), with 1 / (1 - alpha) <=
-    // 1 / (1 - min(0.99, ab)): R = ln2 / (1 - min(0.99, ab)), rounded up; no reciprocal per pixel.
-    const float am = fminf(0.99f, cf.w);
-    Dv = make_float4(e.x, e.y, g.y, __fdiv_ru(1.f, __fsub_rd(1.f, am)) * (0.6931472f * 1.000001f));
-    // Largest eigenvalue of the (negative definite) log2-power form [[ca2, cb2/2], [cb2/2, cc2]]
-    // plus a slack far above its FP32 rounding: p2 <= lmax d^2 at Euclidean distance d from
-    // the mean.  Near-degenerate conics get lmax >= 0 (no culling from it).
-    const float h = 0.5f * (cf.x + cf.z), dd = 0.5f * (cf.x - cf.z), o = 0.5f * cf.y;
-    const float lm = h + sqrtf(fmaf(dd, dd, o * o));
-    lmax = lm + 1e-5f * (fabsf(cf.x) + fabsf(cf.z) + fabsf(cf.y));
+    // 1 / (1 - min(0.99, ab)): R = ln2 / (1 - min(0.99, ab)), rounded up -- and the largest
+    // eigenvalue of the (negative definite) log2-power form [[ca2, cb2/2], [cb2/2, cc2]] plus a
+    // slack far above its FP32 rounding: p2 <= lmax d^2 at Euclidean distance d from the mean
+    // (near-degenerate conics get lmax >= 0: no culling from it).  Both precomputed per splat by K1
+    // (d_blend_record, k_fp64.cu).
+    Dv = make_float4(e.x, e.y, g.y, g.z);
+    lmax = g.w;
 }
 
 template <bool FLOW>
@@ -604,8 +602,12 @@ __global__ void __launch_bounds__(kX2Threads, NB) k_blend_fp32_x2(SplatArrays sp
                     if (!(act0 | act1)) continue;
                     const float4 cc = lds_f4(e + 32);
                     const float2 pr = lds_f2(e + 56);  // (pcq, R)
-                    const float2 abx = __fmul2_rn(make_float2(cc.w, cc.w), make_float2(ex2_approx(p.x), ex2_approx(p.y)));
-                    const float2 al = make_float2(fminf(0.99f, abx.x), fminf(0.99f, abx.y));
+                    // alpha without blend_alpha's clamp at 0.99: wherever it is used -- a pixel that
+                    // blends, or stops, passed the merged test p + M < pcq -- it is already below
+                    // 0.99: for ab < 0.99, p < 0 gives ab 2^p < ab; for ab >= 0.99, p < pc2 - M with
+                    // M >= 1.5e-6 keeps ab 2^p below 0.99 (1 - 1e-6), far outside the EX2 / rounding
+                    // error.  So it equals K6's clamped alpha for every pixel K6 replays.
+                    const float2 al = __fmul2_rn(make_float2(cc.w, cc.w), make_float2(ex2_approx(p.x), ex2_approx(p.y)));
                     const float2 test_T = __fmul2_rn(T, __fadd2_rn(make_float2(1.f, 1.f), make_float2(-al.x, -al.y)));
                     const float2 errN = __ffma2_rn(__fmul2_rn(al, M), make_float2(pr.y, pr.y), errT3);
                     const float2 lo = __ffma2_rn(make_float2(-test_T.x, -test_T.y), errN, test_T);

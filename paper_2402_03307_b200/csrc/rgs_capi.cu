@@ -97,7 +97,7 @@ struct Frame {
         a.rect = rect.as<ushort4>();
         a.conic_f = conic_f.as<float4>();
         a.color_f = color_f.as<float4>();
-        a.guard_f = guard_f.as<float2>();
+        a.guard_f = guard_f.as<float4>();
         a.ext_f = ext_f.as<float4>();
         a.source_index = have_src ? src.as<int32_t>() : nullptr;
         a.depth_key = key.as<unsigned long long>();
@@ -122,7 +122,7 @@ struct Frame {
         rect.ensure(8 * n1, s);
         conic_f.ensure(16 * n1, s);
         color_f.ensure(16 * n1, s);
-        guard_f.ensure(8 * n1, s);
+        guard_f.ensure(16 * n1, s);
         ext_f.ensure(16 * n1, s);
         dir_dist.ensure(32 * n1, s);
         key.ensure(8 * n1, s);

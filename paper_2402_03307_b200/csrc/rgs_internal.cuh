@@ -83,7 +83,8 @@ struct SplatArrays {
     ushort4* rect;           // tile rectangle (x0, x1, y0, y1), inclusive
     float4* conic_f;         // (ca2, cb2, cc2, alpha_base): -log2(e) * (A/2, B, C/2)
     float4* color_f;         // (r, g, b, pa2): pa2 = log2(1/(255 ab))
-    float2* guard_f;         // (cs2n, pc2): error-bound slope, clamp-gate power log2(0.99/ab)
+    float4* guard_f;         // (cs2n, pc2, R, lmax): error-bound slope, clamp-gate power log2(0.99/ab),
+                             // T-gate error growth bound, radial-cull eigenvalue bound
     float4* ext_f;           // (ex, ey, gx2, gy2): alpha-ellipse bbox, max |grad p2| inside it
     int32_t* source_index;   // only for rasterize_forward (else NULL -> index)
     unsigned long long* depth_key;  // order-preserving bits of the FP64 depth (valid splats)
