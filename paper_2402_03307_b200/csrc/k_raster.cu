@@ -495,7 +495,9 @@ __global__ void __launch_bounds__(256, 5) k_blend_fp32(SplatArrays sp, const uin
 // Decisions per (pixel, splat) are those of k_blend_fp32, including its merged ambiguity test.
 constexpr int kX2Threads = 128;
 constexpr int kX2Warps = kX2Threads / 32;
-constexpr int kX2Stage = 256;  // staged splats per batch (two per thread)
+// staged splats per batch, one per thread: 0.261 ms per C2 frame vs 0.265 at 256 (two per thread;
+// the warps of a block wait less for each other at the batch barrier) and 0.320 at 512 (5 CTAs/SM)
+constexpr int kX2Stage = 128;
 // CTAs per SM: 7 (71 registers, no spills) -- C2 frame 0.283 ms, 2490 FPS in the pipelined sweep;
 // 8 (64 registers, spills in the staging): 0.310 ms, 2213 FPS; 6: 0.287 ms, 2453 FPS.  Loading the
 // next entry's gate operands one visit ahead (a rotating register pair) measured 0.322 ms at 6-8.
@@ -504,15 +506,15 @@ constexpr int kX2Blocks = 7;
 // the error bound M = cs2n q + D stays far below |q| (|cs2n| << 1), and nothing overflows.
 constexpr float kGone = 1e12f;
 
-template <bool FLOW, bool COUNT, int NB = kX2Blocks>
+template <bool FLOW, bool COUNT, int NB = kX2Blocks, int STAGE = kX2Stage>
 __global__ void __launch_bounds__(kX2Threads, NB) k_blend_fp32_x2(SplatArrays sp, const uint32_t* __restrict__ vals,
                                                               const uint2* __restrict__ ranges, DevCamera cam,
                                                               float3 bg, float* __restrict__ image,
                                                               double* __restrict__ final_T,
                                                               uint32_t* __restrict__ n_contrib, uint32_t* slow_list,
                                                               int* slow_count, unsigned long long* counters) {
-    __shared__ float4 s_a[kX2Stage], s_b[kX2Stage], s_c[kX2Stage], s_d[kX2Stage];
-    __shared__ float s_l[kX2Stage];
+    __shared__ float4 s_a[STAGE], s_b[STAGE], s_c[STAGE], s_d[STAGE];
+    __shared__ float s_l[STAGE];
     __shared__ StagedSplat w_list[kX2Warps][32];
     __shared__ uint8_t w_k[kX2Warps][32];
     const int tile = blockIdx.x;
@@ -536,10 +538,10 @@ __global__ void __launch_bounds__(kX2Threads, NB) k_blend_fp32_x2(SplatArrays sp
     bool gone = (fpy.x == kGone) & (fpy.y == kGone);
     bool warp_done = __all_sync(kFull, gone);
 
-    for (uint32_t start = rg.x; start < rg.y; start += kX2Stage) {
+    for (uint32_t start = rg.x; start < rg.y; start += STAGE) {
         if (__syncthreads_count(gone) == kX2Threads) break;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < STAGE / kX2Threads; ++h) {
             const int t = threadIdx.x + h * kX2Threads;
             const uint32_t j = start + t;
             if (j < rg.y) {
@@ -555,7 +557,7 @@ __global__ void __launch_bounds__(kX2Threads, NB) k_blend_fp32_x2(SplatArrays sp
             }
         }
         __syncthreads();
-        const int n = (int)min((uint32_t)kX2Stage, rg.y - start);
+        const int n = (int)min((uint32_t)STAGE, rg.y - start);
         if (warp_done) continue;
         for (int c = 0; c < n; c += 32) {
             const int k0 = c + lane;
@@ -926,7 +928,7 @@ using namespace rgs_dev;
 static int g_k5_variant = 3;
 static int g_x2_nb = kX2Blocks;
 
-template <int NB>
+template <int NB, int STAGE = kX2Stage>
 static void launch_x2(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges, const DevCamera& cam,
                       float3 bg, int flow_mode, float* image, double* final_T, uint32_t* n_contrib,
                       uint32_t* slow_list, int* slow_count, unsigned long long* counters, cudaStream_t s) {
@@ -938,7 +940,7 @@ static void launch_x2(const SplatArrays& sp, const uint32_t* pair_vals, const ui
         k_blend_fp32_x2<false, true, NB><<<tiles, kX2Threads, 0, s>>>(sp, pair_vals, ranges, cam, bg, image, final_T,
                                                                       n_contrib, slow_list, slow_count, counters);
     else
-        k_blend_fp32_x2<false, false, NB><<<tiles, kX2Threads, 0, s>>>(sp, pair_vals, ranges, cam, bg, image,
+        k_blend_fp32_x2<false, false, NB, STAGE><<<tiles, kX2Threads, 0, s>>>(sp, pair_vals, ranges, cam, bg, image,
                                                                        final_T, n_contrib, slow_list, slow_count,
                                                                        counters);
 }
