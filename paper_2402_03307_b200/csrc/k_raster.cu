@@ -160,133 +160,6 @@ __device__ __forceinline__ float2 lds_f2(uint32_t a) {
     return v;
 }
 
-// K5 (round-1 form, kept for A/B runs with RGS_K5=1): forward blend.
-template <bool FLOW, bool COUNT>
-__global__ void __launch_bounds__(256, 5) k_blend_fp32_v1(SplatArrays sp, const uint32_t* __restrict__ vals,
-                                                    const uint2* __restrict__ ranges, DevCamera cam, float3 bg,
-                                                    float* __restrict__ image, double* __restrict__ final_T,
-                                                    uint32_t* __restrict__ n_contrib, uint32_t* slow_list,
-                                                    int* slow_count, unsigned long long* counters) {
-    __shared__ StagedSplat sm[kTilePixels];
-    __shared__ float slm[kTilePixels];
-    __shared__ uint8_t wlist[kTilePixels / 32][32];
-    const int tile = blockIdx.x;
-    const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int sx0 = (warp & 1) * 8, sy0 = (warp >> 1) * 4;
-    const int lx = sx0 + (lane & 7), ly = sy0 + (lane >> 3);
-    const int px = tx * kTile + lx, py = ty * kTile + ly;
-    const bool inside = px < cam.width && py < cam.height;
-    const uint2 rg = ranges[tile];
-    const double px0 = tx * kTile, py0 = ty * kTile;
-    const float fpx = (float)lx, fpy = (float)ly, fsx0 = (float)sx0, fsy0 = (float)sy0;
-
-    float T = 1.f, errT = 0.f, acc0 = 0.f, acc1 = 0.f, acc2 = 0.f;
-    int contrib = 0;
-    bool done = !inside, slow = false, stopped = false;
-    uint32_t n_eval = 0, n_blend = 0, n_ref = 0;  // COUNT only
-    bool warp_done = __all_sync(kFull, done);
-
-    for (uint32_t start = rg.x; start < rg.y; start += kTilePixels) {
-        if (__syncthreads_count(done) == kTilePixels) break;
-        const uint32_t j = start + threadIdx.x;
-        if (j < rg.y) stage<FLOW>(sp, vals[j], px0, py0, &sm[threadIdx.x], &slm[threadIdx.x]);
-        __syncthreads();
-        const int n = (int)min((uint32_t)kTilePixels, rg.y - start);
-        if (warp_done) continue;
-        for (int c = 0; c < n; c += 32) {
-            const int k0 = c + lane;
-            // the window's survivors, compacted in order into the warp's list and walked by a
-            // counted loop (double-buffered staging with one barrier per batch measured +1.4%)
-            const bool surv = k0 < n && overlaps_radial(sm[k0], slm[k0], fsx0, fsy0);
-            const unsigned m = __ballot_sync(kFull, surv);
-            if (surv) wlist[warp][__popc(m & ((1u << lane) - 1u))] = (uint8_t)lane;
-            __syncwarp();
-            const int ns = __popc(m);
-            for (int q = 0; q < ns; ++q) {
-                const int k = c + wlist[warp][q];
-                if (done) continue;
-                const float4 a = sm[k].a, b = sm[k].b;
-                float p, M, dx, dy;
-                gate_values(a, b, fpx, fpy, p, M, dx, dy);
-                if (COUNT) ++n_eval;
-                if (gate_skip(p, M, b.z)) continue;
-                const float4 cc = sm[k].c;
-                const float2 pr = make_float2(sm[k].d.z, sm[k].d.w);
-                const float al = blend_alpha(cc.w, p);
-                const float om = __fsub_rn(1.f, al);
-                const float test_T = __fmul_rn(T, om);
-                const float errN = fmaf(al * M, pr.y, errT + 3e-7f);
-                // ambiguous: a classify gate, the backward's clamp gate (unclamped alpha <= 0.99,
-                // rasterizer.cpp:356) or T(1 - alpha) < 1e-4 within their error bounds
-                const bool amb_g = gate_ambiguous(p, M, b.z);
-                const bool amb_c = (__fadd_rn(p, M) >= pr.x) & (__fsub_rn(p, M) <= pr.x);
-                const bool amb_t = fabsf(test_T - 1e-4f) <= test_T * errN;
-                const bool amb = amb_g | amb_c | amb_t;
-                if (COUNT && amb) {
-                    // slow-pixel reasons: power > 0 / alpha gate, clamp gate, transmittance gate
-                    const int r = amb_g ? ((p > -M) ? 3 : 4) : (amb_c ? 5 : 6);
-                    atomicAdd(counters + r, 1ull);
-                }
-                if (amb) {
-                    slow = done = true;
-                    continue;
-                }
-                if (test_T < 1e-4f) {  // rasterizer.cpp:111: the splat is not blended
-                    done = stopped = true;
-                    if (COUNT) n_ref = start - rg.x + k + 1;
-                    continue;
-                }
-                const float w = al * T;
-                acc0 = fmaf(cc.x, w, acc0);
-                acc1 = fmaf(cc.y, w, acc1);
-                acc2 = fmaf(cc.z, w, acc2);
-                T = test_T;
-                errT = errN;
-                contrib = (int)(start - rg.x) + k + 1;
-                if (COUNT) ++n_blend;
-            }
-            __syncwarp();  // the list is rewritten by the next window
-            if (__all_sync(kFull, done)) {
-                warp_done = true;
-                break;
-            }
-        }
-    }
-    if (COUNT) {
-        // E of the roofline = evaluations of the reference algorithm (every list entry up
-        // to the termination point); n_eval = the ones this kernel actually evaluated.
-        unsigned long long e = inside ? (stopped ? n_ref : rg.y - rg.x) : 0, b = n_blend, ke = n_eval;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            e += __shfl_xor_sync(kFull, e, o);
-            b += __shfl_xor_sync(kFull, b, o);
-            ke += __shfl_xor_sync(kFull, ke, o);
-        }
-        if (lane == 0) {
-            atomicAdd(counters + 0, e);
-            atomicAdd(counters + 1, b);
-            atomicAdd(counters + 2, ke);
-        }
-    }
-    if (!inside) return;
-    const uint32_t pix = (uint32_t)py * cam.width + px;
-    if (slow) {
-        slow_list[atomicAdd(slow_count, 1)] = pix;
-        return;
-    }
-    if (FLOW) {
-        image[(size_t)pix * 2 + 0] = acc0;
-        image[(size_t)pix * 2 + 1] = acc1;
-    } else {
-        image[(size_t)pix * 3 + 0] = fmaf(T, bg.x, acc0);
-        image[(size_t)pix * 3 + 1] = fmaf(T, bg.y, acc1);
-        image[(size_t)pix * 3 + 2] = fmaf(T, bg.z, acc2);
-        final_T[pix] = (double)T;
-        n_contrib[pix] = (uint32_t)contrib;
-    }
-}
-
 // Transmittance-gate thresholds of K5's common-case test (rasterizer.cpp:111): with a relative
 // error bound errN on the FP32 test_T, test_T (1 - errN) > kStopHi certainly continues and
 // test_T (1 + errN) < kStopLo certainly stops; the 2e-7 margins cover the rounding of the
@@ -825,6 +698,8 @@ __global__ void __launch_bounds__(kBwdThreads) k_backward_fp32(SplatArrays sp, c
         if (lane < cnt) {
             myid = vals[rg.x + beg + lane];
             stage<false>(sp, myid, px0, py0, &sm[lane], &slm[lane]);
+            const float pc2 = sm[lane].d.z;
+            sm[lane].d.z = pc2 > 0.f ? __int_as_float(1) : pc2;  // pcq, as K5
         }
         __syncwarp();
         unsigned mask = __ballot_sync(kFull, lane < cnt && overlaps_radial<4 * kBwdPx - 1>(sm[lane], slm[lane], fsx0, fsy0));
@@ -843,16 +718,22 @@ __global__ void __launch_bounds__(kBwdThreads) k_backward_fp32(SplatArrays sp, c
             const float2 q2 = __ffma2_rn(make_float2(tv.x, tv.x), make_float2(dx, dx), __fmul2_rn(u, dy));
             const float2 p = __ffma2_rn(make_float2(tv.y, tv.y), dy, q2);
             const float2 M = __ffma2_rn(make_float2(b.w, b.w), q2, make_float2(b.y, b.y));
-            // classify(...) == kAccept: neither a certain skip nor ambiguous
-            const bool acc0 = beg + k < contrib[0] && !gate_skip(p.x, M.x, b.z) && !gate_ambiguous(p.x, M.x, b.z);
-            const bool acc1 = beg + k < contrib[1] && !gate_skip(p.y, M.y, b.z) && !gate_ambiguous(p.y, M.y, b.z);
+            // K5's blend decision.  A pixel K6 replays is not slow, so every splat before its
+            // n_contrib was either blended -- K5's merged test held: p - M > pa2 and p + M < pcq --
+            // or certainly skipped (p + M < pa2, or p > M): the merged test alone tells them apart.
+            // It also puts every blended splat certainly below the clamp (p < pc2), so the unclamped
+            // alpha is the clamped one and the clamp gate's gradient mask is all ones
+            // (rasterizer.cpp:356).
+            const float2 pM = __fadd2_rn(p, M), pm = __fadd2_rn(p, make_float2(-M.x, -M.y));
+            const float pcq = sm[k].d.z;
+            const bool acc0 = (beg + k < contrib[0]) & (pm.x > b.z) & (pM.x < pcq);
+            const bool acc1 = (beg + k < contrib[1]) & (pm.y > b.z) & (pM.y < pcq);
             const bool act = acc0 | acc1;
             float v[9];
             if (act) {
                 const float4 cc = sm[k].c;
                 const float2 e = make_float2(ex2_approx(p.x), ex2_approx(p.y));
-                const float2 abx = __fmul2_rn(make_float2(cc.w, cc.w), e);
-                const float2 al = make_float2(fminf(0.99f, abx.x), fminf(0.99f, abx.y));
+                const float2 al = __fmul2_rn(make_float2(cc.w, cc.w), e);  // below 0.99 (above)
                 const float2 om = __fadd2_rn(make_float2(1.f, 1.f), make_float2(-al.x, -al.y));
                 const float2 inv_om = make_float2(rcp_approx(om.x), rcp_approx(om.y));
                 const float2 Tb = __fmul2_rn(T_run2, inv_om);
@@ -863,9 +744,8 @@ __global__ void __launch_bounds__(kBwdThreads) k_backward_fp32(SplatArrays sp, c
                                             __ffma2_rn(g1_2, make_float2(cc.y, cc.y),
                                                        __fmul2_rn(g2_2, make_float2(cc.z, cc.z))));
                 const float2 dL_da = __ffma2_rn(Tb, G, __fmul2_rn(make_float2(-S2.x, -S2.y), inv_om));
-                // unclamped alpha <= 0.99 (al = ab * e): the conic / mean / alpha_base terms
-                const float pc2 = sm[k].d.z;
-                const float2 dam = make_float2(acc0 && p.x <= pc2 ? dL_da.x : 0.f, acc1 && p.y <= pc2 ? dL_da.y : 0.f);
+                // the conic / mean / alpha_base terms (unclamped alpha, al = ab * e)
+                const float2 dam = make_float2(acc0 ? dL_da.x : 0.f, acc1 ? dL_da.y : 0.f);
                 const float A = -2.f * kLn2 * a.z, B = -kLn2 * a.w, C = -2.f * kLn2 * b.x;
                 const float2 dp = __fmul2_rn(dam, al);
                 const float2 V8 = __fmul2_rn(dam, e);
@@ -923,8 +803,9 @@ __global__ void __launch_bounds__(kBwdThreads) k_backward_fp32(SplatArrays sp, c
 namespace rgs_launch {
 using namespace rgs_dev;
 
-// RGS_K5 (A/B runs): "1" the round-1 kernel, "2" one pixel per lane, "x<N>" two pixels per lane at
-// N (6-8) CTAs per SM; default: two pixels per lane at kX2Blocks.
+// RGS_K5 (A/B runs): "2" one pixel per lane, "x<N>" two pixels per lane at N (6-8) CTAs per SM;
+// default: two pixels per lane at kX2Blocks.  (The round-1 kernel, with separate ambiguity tests,
+// is gone: K6 replays the merged test's decisions.)
 static int g_k5_variant = 3;
 static int g_x2_nb = kX2Blocks;
 
@@ -959,9 +840,7 @@ void blend_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* r
     else                                                                                                           \
         K<false, false><<<tiles, kTilePixels, 0, s>>>(sp, pair_vals, ranges, cam, bg, image, final_T, n_contrib,   \
                                                       slow_list, slow_count, counters);
-    if (g_k5_variant == 1) {
-        RGS_K5_LAUNCH(k_blend_fp32_v1)
-    } else if (g_k5_variant == 2) {
+    if (g_k5_variant == 2) {
         RGS_K5_LAUNCH(k_blend_fp32)
     } else if (g_x2_nb == 6) {
         launch_x2<6>(sp, pair_vals, ranges, cam, bg, flow_mode, image, final_T, n_contrib, slow_list, slow_count,
@@ -981,7 +860,7 @@ bool raster_init() {
     const char* v = std::getenv("RGS_K5");
     g_k5_variant = 3;
     g_x2_nb = kX2Blocks;
-    if (v && (v[0] == '1' || v[0] == '2')) g_k5_variant = v[0] - '0';
+    if (v && v[0] == '2') g_k5_variant = 2;
     if (v && v[0] == 'x' && v[1] >= '6' && v[1] <= '8') g_x2_nb = v[1] - '0';
     return true;
 }
