@@ -33,3 +33,14 @@ t = time.perf_counter()
 host.copy_(dev_imgs, non_blocking=True)
 torch.cuda.synchronize()
 print("one bulk D2H of 4.9 GB: %.1f ms" % (1e3 * (time.perf_counter() - t)))
+# copy-only bounds: the e2e ring's 300 per-view copies, on one stream and alternating over two
+per = dev_imgs[0].numel()
+for nstreams in (1, 2, 4):
+    streams = [torch.cuda.Stream() for _ in range(nstreams)]
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    for v in range(300):
+        with torch.cuda.stream(streams[v % nstreams]):
+            host[v].copy_(dev_imgs[v], non_blocking=True)
+    torch.cuda.synchronize()
+    print(f"300 per-view D2H copies on {nstreams} stream(s): %.1f ms" % (1e3 * (time.perf_counter() - t)))
