@@ -379,18 +379,57 @@ constexpr int kX2Blocks = 7;
 // the error bound M = cs2n q + D stays far below |q| (|cs2n| << 1), and nothing overflows.
 constexpr float kGone = 1e12f;
 
+// Tile order for K5: longest list first (a counting sort on 255 - min(255, length / 4)), so the
+// blocks of the last wave are short ones.  One block.
+__global__ void __launch_bounds__(1024) k_tile_order(const uint2* __restrict__ ranges, int nt, uint32_t* order) {
+    __shared__ uint32_t cnt[256];
+    if (threadIdx.x < 256) cnt[threadIdx.x] = 0;
+    __syncthreads();
+    for (int t = threadIdx.x; t < nt; t += blockDim.x) {
+        const uint2 r = ranges[t];
+        atomicAdd(&cnt[255 - min(255u, (r.y - r.x) >> 2)], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // exclusive scan of the 256 counts by one warp, 8 per lane
+        uint32_t v[8], s = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            v[j] = cnt[threadIdx.x * 8 + j];
+            s += v[j];
+        }
+        uint32_t incl = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, incl, o);
+            if ((int)threadIdx.x >= o) incl += y;
+        }
+        uint32_t run = incl - s;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            cnt[threadIdx.x * 8 + j] = run;
+            run += v[j];
+        }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < nt; t += blockDim.x) {
+        const uint2 r = ranges[t];
+        order[atomicAdd(&cnt[255 - min(255u, (r.y - r.x) >> 2)], 1u)] = (uint32_t)t;
+    }
+}
+
 template <bool FLOW, bool COUNT, int NB = kX2Blocks, int STAGE = kX2Stage>
 __global__ void __launch_bounds__(kX2Threads, NB) k_blend_fp32_x2(SplatArrays sp, const uint32_t* __restrict__ vals,
                                                               const uint2* __restrict__ ranges, DevCamera cam,
                                                               float3 bg, float* __restrict__ image,
                                                               double* __restrict__ final_T,
                                                               uint32_t* __restrict__ n_contrib, uint32_t* slow_list,
-                                                              int* slow_count, unsigned long long* counters) {
+                                                              int* slow_count, unsigned long long* counters,
+                                                              const uint32_t* __restrict__ tile_order) {
     __shared__ float4 s_a[STAGE], s_b[STAGE], s_c[STAGE], s_d[STAGE];
     __shared__ float s_l[STAGE];
     __shared__ StagedSplat w_list[kX2Warps][32];
     __shared__ uint8_t w_k[kX2Warps][32];
-    const int tile = blockIdx.x;
+    const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
     const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int sx0 = (warp & 1) * 8, sy0 = (warp >> 1) * 8;
@@ -645,10 +684,11 @@ __global__ void __launch_bounds__(kBwdThreads) k_backward_fp32(SplatArrays sp, c
                                                                 float3 bg, const double* __restrict__ final_T,
                                                                 const uint32_t* __restrict__ n_contrib,
                                                                 const float* __restrict__ dL, double* sg,
-                                                                unsigned long long* sgx) {
+                                                                unsigned long long* sgx,
+                                                                const uint32_t* __restrict__ tile_order) {
     __shared__ StagedSplat smw[kBwdWarps][32];
     __shared__ float slmw[kBwdWarps][32];
-    const int tile = blockIdx.x;
+    const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
     const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int sx0 = (warp & 1) * 8, sy0 = (warp >> 1) * 4 * kBwdPx;
@@ -809,26 +849,33 @@ using namespace rgs_dev;
 static int g_k5_variant = 3;
 static int g_x2_nb = kX2Blocks;
 
+static bool g_tile_order = true;
+
 template <int NB, int STAGE = kX2Stage>
 static void launch_x2(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges, const DevCamera& cam,
                       float3 bg, int flow_mode, float* image, double* final_T, uint32_t* n_contrib,
-                      uint32_t* slow_list, int* slow_count, unsigned long long* counters, cudaStream_t s) {
+                      uint32_t* slow_list, int* slow_count, unsigned long long* counters, cudaStream_t s,
+                      uint32_t* order) {
     const int tiles = cam.tiles_x * cam.tiles_y;
+    if (!g_tile_order) order = nullptr;
+    if (order) k_tile_order<<<1, 1024, 0, s>>>(ranges, tiles, order);
     if (flow_mode)
         k_blend_fp32_x2<true, false, NB><<<tiles, kX2Threads, 0, s>>>(sp, pair_vals, ranges, cam, bg, image, final_T,
-                                                                      n_contrib, slow_list, slow_count, counters);
+                                                                      n_contrib, slow_list, slow_count, counters,
+                                                                      order);
     else if (counters)
         k_blend_fp32_x2<false, true, NB><<<tiles, kX2Threads, 0, s>>>(sp, pair_vals, ranges, cam, bg, image, final_T,
-                                                                      n_contrib, slow_list, slow_count, counters);
+                                                                      n_contrib, slow_list, slow_count, counters,
+                                                                      order);
     else
         k_blend_fp32_x2<false, false, NB, STAGE><<<tiles, kX2Threads, 0, s>>>(sp, pair_vals, ranges, cam, bg, image,
                                                                        final_T, n_contrib, slow_list, slow_count,
-                                                                       counters);
+                                                                       counters, order);
 }
 
 void blend_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges, const DevCamera& cam,
                 float3 bg, int flow_mode, float* image, double* final_T, uint32_t* n_contrib, uint32_t* slow_list,
-                int* slow_count, unsigned long long* counters, cudaStream_t s) {
+                int* slow_count, unsigned long long* counters, cudaStream_t s, uint32_t* tile_order) {
     const int tiles = cam.tiles_x * cam.tiles_y;
 #define RGS_K5_LAUNCH(K)                                                                                           \
     if (flow_mode)                                                                                                 \
@@ -844,13 +891,13 @@ void blend_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* r
         RGS_K5_LAUNCH(k_blend_fp32)
     } else if (g_x2_nb == 6) {
         launch_x2<6>(sp, pair_vals, ranges, cam, bg, flow_mode, image, final_T, n_contrib, slow_list, slow_count,
-                     counters, s);
+                     counters, s, tile_order);
     } else if (g_x2_nb == 8) {
         launch_x2<8>(sp, pair_vals, ranges, cam, bg, flow_mode, image, final_T, n_contrib, slow_list, slow_count,
-                     counters, s);
+                     counters, s, tile_order);
     } else {
         launch_x2<kX2Blocks>(sp, pair_vals, ranges, cam, bg, flow_mode, image, final_T, n_contrib, slow_list,
-                             slow_count, counters, s);
+                             slow_count, counters, s, tile_order);
     }
 #undef RGS_K5_LAUNCH
 }
@@ -861,20 +908,25 @@ bool raster_init() {
     g_k5_variant = 3;
     g_x2_nb = kX2Blocks;
     if (v && v[0] == '2') g_k5_variant = 2;
+    const char* o = std::getenv("RGS_K5_ORDER");
+    g_tile_order = !(o && o[0] == '0');
     if (v && v[0] == 'x' && v[1] >= '6' && v[1] <= '8') g_x2_nb = v[1] - '0';
     return true;
 }
 
 void backward_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges, const DevCamera& cam,
                    float3 bg, const double* final_T, const uint32_t* n_contrib, const float* dL_dimage,
-                   double* screen_grads, cudaStream_t s, unsigned long long* screen_grads_fixed) {
+                   double* screen_grads, cudaStream_t s, unsigned long long* screen_grads_fixed,
+                   uint32_t* tile_order) {
     const int tiles = cam.tiles_x * cam.tiles_y;
+    if (!g_tile_order) tile_order = nullptr;
+    if (tile_order) k_tile_order<<<1, 1024, 0, s>>>(ranges, tiles, tile_order);
     if (screen_grads_fixed)
         k_backward_fp32<true><<<tiles, kBwdThreads, 0, s>>>(sp, pair_vals, ranges, cam, bg, final_T, n_contrib,
-                                                            dL_dimage, screen_grads, screen_grads_fixed);
+                                                            dL_dimage, screen_grads, screen_grads_fixed, tile_order);
     else
         k_backward_fp32<false><<<tiles, kBwdThreads, 0, s>>>(sp, pair_vals, ranges, cam, bg, final_T, n_contrib,
-                                                             dL_dimage, screen_grads, nullptr);
+                                                             dL_dimage, screen_grads, nullptr, tile_order);
 }
 
 }  // namespace rgs_launch

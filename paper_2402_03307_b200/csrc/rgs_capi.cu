@@ -73,6 +73,7 @@ struct Frame {
     // tiles / pairs / pixels: pairs ping-pong between (keys_a, pair_vals_buf) and (keys_b, vals_b)
     DevBuf ranges, keys_a, pair_vals_buf, keys_b, vals_b, radix_counts, radix_offsets;
     DevBuf tile_counts;  // tile-major scatter: chunk x tile pair counts, then absolute positions
+    DevBuf tile_order;   // K5's tile order (longest list first)
     DevBuf final_T, n_contrib, slow_list;
     DevBuf stats;  // BinState
     DevBuf scan_tmp;
@@ -147,6 +148,7 @@ struct Frame {
         slow_list.ensure(4 * std::max<size_t>(npix, 1), s);
         const size_t nt = (size_t)std::max(ntiles, 1) + 1;
         ranges.ensure(8 * nt, s);
+        tile_order.ensure(4 * nt, s);
     }
     void ensure_pairs(long long p, bool radix, cudaStream_t s) {
         size_t p1 = (size_t)std::max<long long>(p, 1);
@@ -165,7 +167,7 @@ struct Frame {
                          &color_f, &guard_f, &ext_f, &src, &key, &dir_dist, &ent_key, &ent_id, &sorted_ids, &sorted_tiles,
                          &pair_off, &bucket_count, &bucket_off, &bucket_cur, &big_list, &big_scratch, &ranges,
                          &keys_a, &pair_vals_buf, &keys_b, &vals_b, &radix_counts, &radix_offsets, &tile_counts,
-                         &final_T,
+                         &tile_order, &final_T,
                          &n_contrib, &slow_list, &stats, &scan_tmp, &tmp_img};
         for (DevBuf* b : all) b->release(s);
         if (host_stats) {
@@ -562,8 +564,12 @@ int run_forward(rgs_ctx* ctx, Frame& f, cudaStream_t s, Source src, const rgs_sc
         StageTimer t(ctx, kStBlend, s);
         rgs_launch::blend_fp32(sa, f.pair_vals(), f.ranges.as<uint2>(), dc,
                                make_float3((float)f.bg[0], (float)f.bg[1], (float)f.bg[2]), flow_mode ? 1 : 0,
-                               image32, fT, nc, f.slow_list.as<uint32_t>(), slow_count, counters, s);
-        ctx->launches += 1;
+                               image32, fT, nc, f.slow_list.as<uint32_t>(), slow_count, counters, s,
+                               // longest tiles first when the view has the GPU to itself (single
+                               // views, the serialised profiling mode); in a pipelined batch the
+                               // other views fill the tail and the order kernel only adds latency
+                               (!batch || ctx->timing == 1) ? f.tile_order.as<uint32_t>() : nullptr);
+        ctx->launches += (!batch || ctx->timing == 1) ? 2 : 1;
 
     }
     {
@@ -1462,7 +1468,8 @@ int rgs_render_backward(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* ca
             {
                 StageTimer t(c, kStBwdTiles, s);
                 rgs_launch::backward_fp32(sa, f.pair_vals(), f.ranges.as<uint2>(), dc, bgf, f.final_T.as<double>(),
-                                          f.n_contrib.as<uint32_t>(), dL_dimage, c->sgrad.as<double>(), s, fx);
+                                          f.n_contrib.as<uint32_t>(), dL_dimage, c->sgrad.as<double>(), s, fx,
+                                          f.tile_order.as<uint32_t>());
             }
             {
                 StageTimer t(c, kStBwdFixup, s);

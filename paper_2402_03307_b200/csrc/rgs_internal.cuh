@@ -196,9 +196,12 @@ size_t radix_count_entries(long long n_pairs);
 int tile_radix_sort(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32_t* vals_b, const BinState* st,
                     long long n_pairs, int tiles_x, int tiles_y, uint32_t* status_a, uint32_t* status_b, int* aux,
                     uint2* ranges, cudaStream_t s);
+// tile_order (optional, n_tiles u32): K5's blocks take the tiles longest list first (one
+// counting-sort kernel before it), so the last wave is made of short tiles.
 void blend_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges, const DevCamera& cam,
                 float3 bg, int flow_mode, float* image, double* final_T, uint32_t* n_contrib,
-                uint32_t* slow_list, int* slow_count, unsigned long long* counters, cudaStream_t s);
+                uint32_t* slow_list, int* slow_count, unsigned long long* counters, cudaStream_t s,
+                uint32_t* tile_order = nullptr);
 void mark_all_slow(int n_pixels, uint32_t* slow_list, int* slow_count, cudaStream_t s);
 void blend_fp64_pixels(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges,
                        const DevCamera& cam, double3 bg, int flow_mode, float* image, double* image64,
@@ -215,7 +218,8 @@ int project_one(const double* sliced16_dev, const DevCamera& cam, const double* 
 void backward_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges,
                    const DevCamera& cam, float3 bg, const double* final_T, const uint32_t* n_contrib,
                    const float* dL_dimage, double* screen_grads, cudaStream_t s,
-                   unsigned long long* screen_grads_fixed = nullptr);
+                   unsigned long long* screen_grads_fixed = nullptr,
+                   uint32_t* tile_order = nullptr);
 void backward_fp64_pixels(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges,
                           const DevCamera& cam, double3 bg, const double* final_T, const uint32_t* n_contrib,
                           const float* dL_dimage, const uint32_t* slow_list, const int* slow_count,
