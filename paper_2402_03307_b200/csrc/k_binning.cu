@@ -28,7 +28,10 @@
 
 namespace rgs_dev {
 
-constexpr int kBucketBits = 18;
+// Depth buckets: 2^bits with bits = ceil(log2 n) - 3 in [12, 18] (about 8 splats per bucket at
+// most): C2 (300K) 16 bits -- 0.046 -> 0.042 ms for the depth ranks against 18 bits (a quarter of
+// the bucket scan and the per-view bucket reset); C4 (2M) keeps 18.
+constexpr int kBucketBits = 18;  // the largest (allocation)
 constexpr int kNumBuckets = 1 << kBucketBits;
 constexpr int kSmallBucket = 32;
 constexpr unsigned kFullMask = 0xffffffffu;
@@ -201,13 +204,13 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_apply(const uint32_t* __r
 }
 
 // --------------------------------------------------------------------------- depth ranks
-__global__ void k_bucket_setup(BinState* st) {
+__global__ void k_bucket_setup(BinState* st, int bucket_bits) {
     const unsigned long long lo = st->key_min, hi = st->key_max;
     int shift = 0;
     if (hi > lo) {
         const unsigned long long range = hi - lo;
         const int bits = 64 - __clzll(range);
-        shift = bits > kBucketBits ? bits - kBucketBits : 0;
+        shift = bits > bucket_bits ? bits - bucket_bits : 0;
     }
     st->shift = shift;
 }
@@ -990,6 +993,11 @@ using namespace rgs_dev;
 static inline int blocks(long long n, int t) { return (int)((n + t - 1) / t); }
 
 int num_depth_buckets() { return kNumBuckets; }
+int depth_bucket_bits(int n) {
+    int b = 0;
+    while (b < 31 && (1ll << b) < (long long)std::max(n, 1)) ++b;
+    return std::min(kBucketBits, std::max(12, b - 3));
+}
 
 // Single-pass variant; scratch: scan1_scratch_words(n) u32 (status words + ticket).
 size_t scan1_scratch_words(int n) { return 2 * (size_t)(blocks(std::max(n, 1), kScan1Tile) + 1) + 4; }
@@ -1013,7 +1021,7 @@ void exclusive_scan(const uint32_t* in, int n, uint32_t* out, uint32_t* scratch,
 
 void bucket_hist(const uint8_t* valid, const unsigned long long* key, int n, BinState* st, uint32_t* bucket_count,
                  cudaStream_t s) {
-    k_bucket_setup<<<1, 1, 0, s>>>(st);
+    k_bucket_setup<<<1, 1, 0, s>>>(st, depth_bucket_bits(n));
     if (n > 0) k_bucket_hist<<<blocks(n, 256), 256, 0, s>>>(valid, key, n, st, bucket_count);
 }
 
@@ -1098,8 +1106,10 @@ void fold_status(const BinState* st, unsigned long long* word, unsigned long lon
     k_fold_status<<<1, 1, 0, s>>>(st, word, overflow_word);
 }
 
-void frame_init(BinState* st, uint32_t pair_cap, uint32_t* bucket_count, uint32_t* bucket_cur, cudaStream_t s) {
-    k_frame_init<<<blocks(kNumBuckets, 256), 256, 0, s>>>(st, pair_cap, bucket_count, bucket_cur, kNumBuckets);
+void frame_init(BinState* st, uint32_t pair_cap, uint32_t* bucket_count, uint32_t* bucket_cur, int n,
+                cudaStream_t s) {
+    const int nb = 1 << depth_bucket_bits(n);
+    k_frame_init<<<blocks(nb, 256), 256, 0, s>>>(st, pair_cap, bucket_count, bucket_cur, nb);
 }
 
 // ---- tile-major scatter (k_chunk_tile_counts, k_tile_offsets, k_tile_scatter)

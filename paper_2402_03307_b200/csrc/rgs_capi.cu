@@ -447,14 +447,14 @@ int run_forward(rgs_ctx* ctx, Frame& f, cudaStream_t s, Source src, const rgs_sc
     f.ensure_pixels(npix, ntiles, s);
     f.have_src = src == kFromSplats;  // frames are recycled between scene and splat renders
     if (f.have_src) f.src.ensure(4 * (size_t)std::max(n, 1), s);
-    const int nb = rgs_launch::num_depth_buckets();
+    const int nb = 1 << rgs_launch::depth_bucket_bits(n);
     // Binning: the tile-major scatter (up to 256 x 256 and 8192 tiles) for single views -- the
     // shorter critical path; K3 + the radix passes for the views of a batch, which overlap the
     // blends of the other views in flight better ("Binning").
     const bool scatter =
         rgs_launch::tile_scatter_usable(dc.tiles_x, dc.tiles_y, n, f.pair_cap, batch, ctx->binning_mode);
     rgs_launch::frame_init(f.dstats(), (uint32_t)std::min<long long>(f.pair_cap, 0xffffffffll),
-                           f.bucket_count.as<uint32_t>(), f.bucket_cur.as<uint32_t>(), s);
+                           f.bucket_count.as<uint32_t>(), f.bucket_cur.as<uint32_t>(), n, s);
     ctx->launches += 1;
     SplatArrays sa = f.arrays();
     if (render_only && !flow_mode) {

@@ -154,7 +154,8 @@ void slice_cache(const float* params, const double* params64, int n, void* buf, 
 void splats_from_host(const void* splats, int n, const DevCamera& cam, const SplatArrays& out, BinState* st,
                       cudaStream_t s);
 // k_binning.cu
-int num_depth_buckets();
+int num_depth_buckets();     // allocation (the largest bucket count)
+int depth_bucket_bits(int n);  // the bucket count used for n splats: 1 << depth_bucket_bits(n)
 bool binning_init();
 bool raster_init();  // k_raster.cu
 bool train_init();   // k_train.cu
@@ -175,7 +176,8 @@ void duplicate(const uint32_t* sorted_ids, const uint32_t* pair_off, const uint3
                uint32_t* vals, int* aux, cudaStream_t s);
 void check_capacity(BinState* st, cudaStream_t s);
 void fold_status(const BinState* st, unsigned long long* word, unsigned long long overflow_word, cudaStream_t s);
-void frame_init(BinState* st, uint32_t pair_cap, uint32_t* bucket_count, uint32_t* bucket_cur, cudaStream_t s);
+void frame_init(BinState* st, uint32_t pair_cap, uint32_t* bucket_count, uint32_t* bucket_cur, int n,
+                cudaStream_t s);
 // Tile-major scatter (images up to 256 x 256 tiles and 8192 tiles; k_binning.cu): per-chunk tile
 // counts -> per-chunk prefixes, tile starts, tile ranges and the pair count (into `st`), then the
 // pairs' splat ids straight to their sorted positions.

@@ -44,3 +44,22 @@ for nstreams in (1, 2, 4):
             host[v].copy_(dev_imgs[v], non_blocking=True)
     torch.cuda.synchronize()
     print(f"300 per-view D2H copies on {nstreams} stream(s): %.1f ms" % (1e3 * (time.perf_counter() - t)))
+# fixed vs per-view cost of the host path: t(n) for n = 8, 60, 150, 300 views (best of 3)
+for n in (8, 60, 150, 300):
+    best = 1e9
+    for _ in range(3):
+        t = time.perf_counter()
+        ctx.render_views_host([p.numpy() for p in pinned], 3, cams[:n], (0, 0, 0), host[:n].numpy())
+        best = min(best, time.perf_counter() - t)
+    bd = 1e9
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        ctx.render_views(scene, cams[:n], out=dev_imgs[:n])
+        torch.cuda.synchronize()
+        bd = min(bd, time.perf_counter() - t)
+    print(f"n={n}: host path {1e3 * best:.1f} ms, device path {1e3 * bd:.1f} ms")
+t = time.perf_counter()
+sc2 = rgs.DeviceScene.from_store(ctx, store)
+torch.cuda.synchronize()
+print("scene upload (from_store): %.1f ms" % (1e3 * (time.perf_counter() - t)))
