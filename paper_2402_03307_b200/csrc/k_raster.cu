@@ -547,7 +547,9 @@ __global__ void __launch_bounds__(kX2Threads, NB) k_blend_fp32_x2(SplatArrays sp
                         // a decision inside its error bound -> the pixel goes to the FP64 fix-up
                         const float2 hi = __ffma2_rn(test_T, errN, test_T);
                         const int qi = (int)((e - first) / sizeof(StagedSplat));
-                        if (act0 & !ok0 & !(p.x > M.x)) {
+                        // (a finished pixel only gets here through an overflowing bound -- a
+                        // degenerate conic's M at y = kGone -- and stays as it is)
+                        if (act0 & !ok0 & !(p.x > M.x) & (fpy.x != kGone)) {
                             if (cl0 && hi.x < kStopLo) {
                                 stopped0 = true;
                                 if (COUNT) n_ref0 = start - rg.x + c + w_k[warp][qi] + 1;
@@ -560,7 +562,7 @@ __global__ void __launch_bounds__(kX2Threads, NB) k_blend_fp32_x2(SplatArrays sp
                             }
                             fpy.x = kGone;
                         }
-                        if (act1 & !ok1 & !(p.y > M.y)) {
+                        if (act1 & !ok1 & !(p.y > M.y) & (fpy.y != kGone)) {
                             if (cl1 && hi.y < kStopLo) {
                                 stopped1 = true;
                                 if (COUNT) n_ref1 = start - rg.x + c + w_k[warp][qi] + 1;

@@ -375,3 +375,37 @@ def test_unrounded_store_fp64_scene(ctx, orc, seed):
     back = scene.download()
     for a, b in zip(back, store.arrays_f64()):
         assert np.array_equal(np.asarray(a).reshape(-1), np.asarray(b).reshape(-1))
+
+
+_K5_VARIANT_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r}); sys.path.insert(0, {root!r} + '/oracle'); sys.path.insert(0, {root!r} + '/tests')
+from paper_2402_03307_b200 import rgs, scenes
+import oracle
+store = scenes.synthetic_scene(20_000, 333, 250, seed=31)
+cam = scenes.bench_camera(333, 250, 0.4, scenes.yaw_pose(4.0, (0.02, 0.01, 0.05)))
+ctx = rgs.Context(0, use_torch_stream=False)
+out = rgs.render_forward(store, cam, rgs.RenderOptions(background=(0.2, 0.1, 0.3), retain_records=True), ctx=ctx)
+img, ref = oracle.restatement().render_forward(store, cam, (0.2, 0.1, 0.3), threads=8, retain=True)
+assert np.array_equal(out.records.tile_ids, ref.tile_ids)
+assert np.array_equal(out.records.n_contrib, ref.n_contrib), "n_contrib differs"
+err = float(np.abs(out.image.astype(np.float64) - img).max())
+assert err <= 1e-4, err
+print("variant ok", err)
+"""
+
+
+@pytest.mark.parametrize("env", [{"RGS_K5": "2"}, {"RGS_K5": "x6"}, {"RGS_K5": "x8"}, {"RGS_K5_ORDER": "0"}])
+def test_k5_variants_match_oracle(env):
+    """The A/B variants of K5 selected by environment (read once per process, so each runs in a
+    subprocess): one pixel per lane, the two-pixel kernel at 6 / 8 CTAs per SM, launch-order tiles
+    -- the same n_contrib as the oracle and the image within 1e-4."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _K5_VARIANT_SCRIPT.format(root=root)], env={**os.environ, **env},
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "variant ok" in r.stdout
