@@ -419,6 +419,14 @@ enum Source { kFromScene, kFromSplats };
 }  // namespace
 namespace {
 
+// K5 / K6 take the tiles longest list first when the view has the GPU to itself (a single
+// view, or one view in flight) and its frame is small enough for its records to stay in L2: the
+// spatially scattered tile order costs a 3840x2160 / 2M-Gaussian frame 0.9 % (C4: 379.5 vs 382.8
+// FPS) while it saves 2.8 % of K5 at 1352x1014 (0.2513 vs 0.2585 ms).
+inline bool use_tile_order(bool batch, bool solo, size_t npix) {
+    return (!batch || solo) && npix <= (size_t)2200000;
+}
+
 // Enqueues the forward pipeline of one view into frame `f` on stream `s`.
 //
 // No host synchronisation in the steady state: the pair buffers have a capacity
@@ -429,7 +437,8 @@ namespace {
 int run_forward(rgs_ctx* ctx, Frame& f, cudaStream_t s, Source src, const rgs_scene* scene, const void* dev_splats,
                 int n_splats, bool splats_monotone, const rgs_camera* cam, const double bg[3], unsigned flags,
                 float* image, bool flow_mode, bool sync, BinState* host_stats,
-                const SliceCacheView* slice_cache = nullptr, bool render_only = false, bool batch = false) {
+                const SliceCacheView* slice_cache = nullptr, bool render_only = false, bool batch = false,
+                bool solo = false) {
     const DevCamera dc = make_dev_camera(cam);
     const int n = src == kFromScene ? scene->n : n_splats;
     const size_t npix = (size_t)cam->width * cam->height;
@@ -569,8 +578,8 @@ int run_forward(rgs_ctx* ctx, Frame& f, cudaStream_t s, Source src, const rgs_sc
                                // longest tiles first when the view has the GPU to itself (single
                                // views, the serialised profiling mode); in a pipelined batch the
                                // other views fill the tail and the order kernel only adds latency
-                               (!batch || ctx->timing == 1) ? f.tile_order.as<uint32_t>() : nullptr);
-        ctx->launches += (!batch || ctx->timing == 1) ? 2 : 1;
+                               use_tile_order(batch, solo, npix) ? f.tile_order.as<uint32_t>() : nullptr);
+        ctx->launches += use_tile_order(batch, solo, npix) ? 2 : 1;
 
     }
     {
@@ -1184,8 +1193,9 @@ int render_batch(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* cams, int
     for (int k = 0; k < rgs_ctx::kSlots; ++k) CK(cudaStreamWaitEvent(c->slot_stream[k], c->join_ev, 0));
     // Profiling mode serialises the views (one slot) so per-stage event times are the
     // kernels' own durations rather than shares of concurrently running views.
-    // Views in flight: 8 for frames up to ~2 MP (1352x1014: 3 -> 8 slots measured +4.5%), 3 for
-    // larger ones (3840x2160: 8 slots measured -4%, L2 pressure of the bigger pair lists).
+    // Views in flight: 8 for frames up to ~2 MP (1352x1014: 3 -> 8 slots measured +4.5%), 1 for
+    // larger ones (below).  One view in flight (or the profiling mode) -> K5 takes the tiles
+    // longest list first, as a single view does.
     const size_t npix = (size_t)cams[0].width * cams[0].height;
     // RGS_SLOTS (A/B runs; up to kSlots): views in flight.  At 8, 10 or 12 the C2 sweep runs at the
     // same rate (2650 FPS), at 6 0.3 % slower (with a less shared -- faster -- live K5 launch)
@@ -1194,14 +1204,22 @@ int render_batch(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* cams, int
         const int k = e ? std::atoi(e) : 0;
         return (k >= 1 && k <= rgs_ctx::kSlots) ? k : 0;
     }();
-    const int big_slots = env_slots ? std::min(env_slots, 3) : 3;
+    static const int env_big = [] {
+        const char* e = std::getenv("RGS_SLOTS_BIG");
+        const int k = e ? std::atoi(e) : 0;
+        return (k >= 1 && k <= rgs_ctx::kSlots) ? k : 0;
+    }();
+    // Frames above ~2.2 MP run one view at a time: 3840x2160 (C4) 383 FPS at 1 view in flight
+    // against 349 / 342 / 336 / 333 at 2 / 3 / 4 / 6 (the views' pair lists and records compete
+    // for L2); up to ~2.2 MP the views overlap (C2: 8 in flight).
+    const int big_slots = env_big ? env_big : 1;
     const int slots = c->timing == 1 ? 1 : (npix <= (size_t)2200000 ? (env_slots ? env_slots : 8) : big_slots);
     for (int v = 0; v < n_views; ++v) {
         const int k = v % slots;
         cudaStream_t s = c->slot_stream[k];
         const int rc = run_forward(c, c->slot_frame[k], s, kFromScene, scene, nullptr, 0, true, &cams[v], bg,
                                    flags & ~RGS_FLAG_HOST_BUFFERS, image_for(user, v, s), false, false,
-                                   &c->view_stats[v], cache, true, true);
+                                   &c->view_stats[v], cache, true, true, slots == 1);
         if (rc) return rc;
         copy_out(v, k, s);
     }
@@ -1478,7 +1496,9 @@ int rgs_render_backward(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* ca
                 StageTimer t(c, kStBwdTiles, s);
                 rgs_launch::backward_fp32(sa, f.pair_vals(), f.ranges.as<uint2>(), dc, bgf, f.final_T.as<double>(),
                                           f.n_contrib.as<uint32_t>(), dL_dimage, c->sgrad.as<double>(), s, fx,
-                                          f.tile_order.as<uint32_t>());
+                                          use_tile_order(false, false, (size_t)f.width * f.height)
+                                              ? f.tile_order.as<uint32_t>()
+                                              : nullptr);
             }
             {
                 StageTimer t(c, kStBwdFixup, s);
