@@ -24,6 +24,8 @@ scene = rgs.DeviceScene.from_store(ctx, store)
 tr = train.Trainer(ctx, scene, train.TrainConfig(batch=bench.C5_VIEWS, total_steps=bench.TRAIN_TOTAL_STEPS,
                                                  max_gaussians=2_000_000), None, start_step=bench.TRAIN_START_STEP)
 tl = [targets[v] for v in range(bench.C5_VIEWS)]
+if os.environ.get("C5_NO_OVERLAP") == "1":
+    tr.overlap = False
 for _ in range(3):
     tr.step(cams, tl)
 torch.cuda.synchronize()
