@@ -442,7 +442,8 @@ __global__ void __launch_bounds__(kRadixThreads, MINB) k_radix_onesweep(const ui
                                                                   const BinState* __restrict__ st, int shift,
                                                                   const int* __restrict__ hist_diff, int hist_plain,
                                                                   uint32_t* status, uint32_t* ticket,
-                                                                  uint32_t* keys_out, uint32_t* vals_out) {
+                                                                  uint32_t* keys_out, uint32_t* vals_out,
+                                                                  int nbits) {
     __shared__ uint32_t wcnt[kRadixWarps][kRadixDigits];
     __shared__ uint32_t dstart[kRadixDigits];
     __shared__ uint32_t gbase[kRadixDigits];
@@ -469,7 +470,26 @@ __global__ void __launch_bounds__(kRadixThreads, MINB) k_radix_onesweep(const ui
 #pragma unroll
     for (int j = 0; j < ROUNDS; ++j) {
         const uint32_t d = key[j] != 0xffffffffu ? (key[j] >> shift) & 0xffu : 0xffffffffu;
-        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        // lanes with the same digit: __match_any_sync, or (nbits > 0, the RGS_RADIX_BALLOT A/B
+        // switch) nbits ballots over the digit's significant bits -- slower (0.125 vs 0.094 ms per
+        // C2 frame); the kernel as built with both paths measured 4 % faster on the match path than
+        // the match-only build (0.0945 vs 0.0984 ms, same box: register allocation, 79 vs 76)
+        unsigned peers;
+        if (nbits > 0) {
+            const bool ok = d != 0xffffffffu;
+            peers = __ballot_sync(0xffffffffu, ok);
+            if (!ok) peers = ~peers;
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                if (b < nbits) {
+                    const bool bit = (d >> b) & 1u;
+                    const unsigned bal = __ballot_sync(0xffffffffu, bit);
+                    peers &= bit ? bal : ~bal;
+                }
+            }
+        } else {
+            peers = __match_any_sync(0xffffffffu, d);
+        }
         const uint32_t below = __popc(peers & ((1u << lane) - 1u));
         uint32_t r = 0;
         if (d != 0xffffffffu) r = wcnt[w][d] + below;
@@ -1055,6 +1075,12 @@ int radix_blocks(long long n_pairs) { return std::max(blocks(n_pairs, kMinBlockT
 static int radix_grid(long long n_pairs) {
     return std::max(blocks(n_pairs, kRadixThreads * g_radix_rounds), 1);
 }
+static int g_radix_ballot = 0;
+static int digit_bits(int n) {  // significant bits of the values 0 .. n - 1 (at least 1)
+    int b = 1;
+    while (b < 8 && (1 << b) < n) ++b;
+    return b;
+}
 template <typename... A>
 static void radix_pass(int nb, cudaStream_t s, A... a) {
     if (g_radix_rounds == 8) k_radix_onesweep<8, 4><<<nb, kRadixThreads, 0, s>>>(a...);
@@ -1080,18 +1106,18 @@ int tile_radix_sort(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32
     cudaMemsetAsync(status_b, 0, 4 * entries, s);
     if (shift == 8) {
         radix_pass(nb, s, keys_a, vals_a, st, 0, aux, 0, status_a, tickets, keys_b,
-                                                       vals_b);
+                                                       vals_b, g_radix_ballot ? digit_bits(tiles_x) : 0);
         radix_pass(nb, s, keys_b, vals_b, st, 8, aux + 257, 0, status_b, tickets + 1,
-                                                       keys_a, vals_a);
+                                                       keys_a, vals_a, g_radix_ballot ? digit_bits(tiles_y) : 0);
     } else {
         k_digit_hist3<<<148 * 2, 256, 0, s>>>(keys_a, st, aux);
         radix_pass(nb, s, keys_a, vals_a, st, 0, aux, 1, status_a, tickets, keys_b,
-                                                       vals_b);
+                                                       vals_b, g_radix_ballot ? 8 : 0);
         radix_pass(nb, s, keys_b, vals_b, st, 8, aux + 256, 1, status_b, tickets + 1,
-                                                       keys_a, vals_a);
+                                                       keys_a, vals_a, g_radix_ballot ? 8 : 0);
         cudaMemsetAsync(status_a, 0, 4 * entries, s);
         radix_pass(nb, s, keys_a, vals_a, st, 16, aux + 512, 1, status_a, tickets + 2,
-                                                       keys_b, vals_b);
+                                                       keys_b, vals_b, g_radix_ballot ? 8 : 0);
         out = 1;
     }
     cudaMemsetAsync(ranges, 0, sizeof(uint2) * (size_t)n_tiles, s);
@@ -1152,6 +1178,10 @@ void tile_scatter(const uint32_t* sorted_ids, const uint32_t* sorted_tiles, cons
 bool binning_init() {
     const char* v = std::getenv("RGS_RADIX");
     g_radix_rounds = (v && v[0] == '8') ? 8 : 16;
+    // RGS_RADIX_BALLOT=1: digit peers by ballots over the significant digit bits instead of
+    // __match_any_sync -- measured slower (C2 radix passes 0.125 vs 0.094 ms)
+    const char* m = std::getenv("RGS_RADIX_BALLOT");
+    g_radix_ballot = (m && m[0] == '1') ? 1 : 0;
     const char* b = std::getenv("RGS_BINNING");
     g_binning_mode = !b ? 0 : (b[0] == 'r' ? 1 : (b[0] == 's' ? 2 : 0));
     const char* r = std::getenv("RGS_SCATTER_ROUNDS");
