@@ -325,6 +325,23 @@ def test_render_views_batch_matches_single_views(ctx):
     assert torch.all(batch[0] == torch.tensor([0.1, 0.2, 0.3], device=batch.device))
 
 
+def test_render_views_large_frames_one_at_a_time(ctx):
+    """Frames above ~2.2 MP render one view at a time with the longest-first tile order (the
+    solo path): bitwise the per-view renders, incl. a view that sees nothing first."""
+    import torch
+
+    w, h = 2000, 1200
+    store = scenes.synthetic_scene(60_000, w, h, seed=12)
+    scene = rgs.DeviceScene.from_store(ctx, store)
+    cams = [scenes.bench_camera(w, h, 0.5, scenes.yaw_pose(180.0))] + scenes.sweep_cameras(w, h, 3)
+    batch = ctx.render_views(scene, cams, (0.05, 0.1, 0.2))
+    torch.cuda.synchronize()
+    for v, cam in enumerate(cams):
+        img, rec = ctx.render_forward_device(scene, cam, (0.05, 0.1, 0.2), retain=False)
+        torch.cuda.synchronize()
+        assert torch.equal(batch[v], img), v
+
+
 def test_missing_records(ctx):
     st = scenes.random_scene(3, seed=2)
     cam = scenes.bench_camera(32, 32, 0.3)
