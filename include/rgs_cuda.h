@@ -253,6 +253,15 @@ int rgs_render_backward(rgs_ctx* ctx, const rgs_scene* scene, const rgs_camera* 
  * *out filled (source_index = -1) when the splat passes the culls, 0 when culled. */
 int rgs_project_sliced(rgs_ctx* ctx, const double* sliced16, const rgs_camera* cam, const double* sh48,
                        int sh_degree, double opacity_logit, rgs_splat* out, int* survived);
+/* The same, also returning project()'s ProjectCache (rasterizer.hpp:33-48, filled as
+ * rasterizer.cpp:261-275 does) when the splat survives: cache = RGS_PROJECT_CACHE_DOUBLES doubles,
+ *   [0, 3) p_cam, [3, 9) T = J R_wc (2 x 3 row-major), [9, 13) cov2 (dilated, 2 x 2 row-major),
+ *   [13, 16) dir, [16] view_dist, [17, 33) SH basis, [33, 81) basis gradient (16 x 3 row-major,
+ *   d basis_k / d dir_j), [81, 84) clamped (1 / 0 per channel), [84] opacity (sigmoid).
+ * cov3, mean3, speed and decay are the sliced input.  cache may be NULL. */
+#define RGS_PROJECT_CACHE_DOUBLES 85
+int rgs_project_sliced_cache(rgs_ctx* ctx, const double* sliced16, const rgs_camera* cam, const double* sh48,
+                             int sh_degree, double opacity_logit, rgs_splat* out, int* survived, double* cache);
 
 /* ---------------------------------------------------------------- utilities */
 /* Device memory for FFI callers without the CUDA runtime (the C++ drop-ins use these):

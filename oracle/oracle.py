@@ -218,6 +218,18 @@ class OracleLib:
         self._check(self._f("to_matrix")(_p(np.ascontiguousarray(rot, np.float64)), _p(out)))
         return out.reshape(4, 4)
 
+    def project_cache(self, sliced16, cam, sh48, sh_degree, opacity_logit):
+        """project() with its ProjectCache, flattened as rgs_project_sliced_cache (reference build)."""
+        c = make_ccamera(cam)
+        out = np.zeros(1, dtype=SPLAT_DTYPE)
+        pc = np.zeros(85, dtype=np.float64)
+        r = self._f("project_cache")(_p(np.ascontiguousarray(sliced16, np.float64)), ctypes.byref(c),
+                                     _p(np.ascontiguousarray(sh48, np.float64)), ctypes.c_int(sh_degree),
+                                     ctypes.c_double(opacity_logit), _p(out), _p(pc))
+        if r < 0:
+            self._check(-r)
+        return (out[0], pc) if r == 1 else (None, None)
+
     def project(self, sliced16, cam, sh48, sh_degree, opacity_logit):
         c = make_ccamera(cam)
         out = np.zeros(1, dtype=SPLAT_DTYPE)

@@ -364,6 +364,42 @@ int ref_to_matrix(const double* rot, double* out16) {
 // Single projection of an already-sliced Gaussian (rasterizer.cpp:215-276).
 // sliced: mean3, cov9 row-major, decay, speed3 (16 doubles).  Returns 1 and fills
 // *out when the splat survives, 0 when culled, <0 on error.
+// The same with project()'s ProjectCache flattened as rgs_project_sliced_cache's layout
+// (include/rgs_cuda.h): p_cam, T, cov2, dir, view_dist, basis, basis_grad, clamped, opacity.
+int ref_project_cache(const double* sliced, const ref_camera* c, const double* sh48, int sh_degree,
+                      double opacity_logit, ref_splat* out, double* pc) {
+    try {
+        SlicedGaussian3D s;
+        s.mean = Vec3(sliced[0], sliced[1], sliced[2]);
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) s.cov(i, j) = sliced[3 + 3 * i + j];
+        s.decay = sliced[12];
+        s.speed = Vec3(sliced[13], sliced[14], sliced[15]);
+        ShCoeffs sh;
+        for (int ch = 0; ch < 3; ++ch)
+            for (int k = 0; k < 16; ++k) sh(ch, k) = sh48[ch * 16 + k];
+        ProjectCache cache;
+        auto sp = project(s, to_cam(c), sh, sh_degree, opacity_logit, &cache);
+        if (!sp) return 0;
+        from_splat(*sp, out);
+        for (int k = 0; k < 3; ++k) pc[k] = cache.p_cam[k];
+        for (int r = 0; r < 2; ++r)
+            for (int k = 0; k < 3; ++k) pc[3 + 3 * r + k] = cache.T(r, k);
+        for (int r = 0; r < 2; ++r)
+            for (int k = 0; k < 2; ++k) pc[9 + 2 * r + k] = cache.cov2(r, k);
+        for (int k = 0; k < 3; ++k) pc[13 + k] = cache.dir[k];
+        pc[16] = cache.view_dist;
+        for (int k = 0; k < 16; ++k) pc[17 + k] = cache.basis[k];
+        for (int k = 0; k < 16; ++k)
+            for (int j = 0; j < 3; ++j) pc[33 + 3 * k + j] = cache.basis_grad(k, j);
+        for (int ch = 0; ch < 3; ++ch) pc[81 + ch] = cache.clamped[ch] ? 1.0 : 0.0;
+        pc[84] = cache.opacity;
+        return 1;
+    } catch (...) {
+        return -map_exception();
+    }
+}
+
 int ref_project(const double* sliced, const ref_camera* c, const double* sh48, int sh_degree,
                 double opacity_logit, ref_splat* out) {
     try {

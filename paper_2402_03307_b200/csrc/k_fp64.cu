@@ -501,7 +501,7 @@ __global__ void k_backward_det_reduce(SplatArrays sp, const uint32_t* __restrict
 // project() of one already-sliced Gaussian (rasterizer.cpp:215-276) for the C++
 // drop-in's single-Gaussian entry point; SH exactly as the reference (all 16 terms).
 __global__ void k_project_one(const double* __restrict__ sl, DevCamera cam, const double* __restrict__ sh,
-                              int sh_degree, double opacity_logit, HostSplat* out, int* survived) {
+                              int sh_degree, double opacity_logit, HostSplat* out, int* survived, double* cache) {
     SliceState s;
 #pragma unroll
     for (int k = 0; k < 3; ++k) s.mean[k] = sl[k];
@@ -518,11 +518,24 @@ __global__ void k_project_one(const double* __restrict__ sl, DevCamera cam, cons
     double basis[16];
     d_sh_basis(o.dir, sh_degree, basis);
     HostSplat h;
+    bool clamped[3];
     for (int ch = 0; ch < 3; ++ch) {
         double a = sh[ch * 16] * basis[0];
         for (int k = 1; k < 16; ++k) a += sh[ch * 16 + k] * basis[k];
         const double c = a + 0.5;
+        clamped[ch] = c < 0;
         h.color[ch] = c < 0 ? 0.0 : c;
+    }
+    if (cache) {  // ProjectCache (rasterizer.cpp:261-275), layout of rgs_project_sliced_cache
+        for (int k = 0; k < 3; ++k) cache[k] = o.p[k];
+        for (int k = 0; k < 6; ++k) cache[3 + k] = o.T[k];
+        for (int k = 0; k < 4; ++k) cache[9 + k] = o.cov2[k];
+        for (int k = 0; k < 3; ++k) cache[13 + k] = o.dir[k];
+        cache[16] = o.dist;
+        for (int k = 0; k < 16; ++k) cache[17 + k] = basis[k];
+        d_sh_basis_grad(o.dir, sh_degree, cache + 33);
+        for (int ch = 0; ch < 3; ++ch) cache[81 + ch] = clamped[ch] ? 1.0 : 0.0;
+        cache[84] = o.opacity;
     }
     for (int r = 0; r < 2; ++r) {
         double a = o.T[r * 3 + 0] * s.speed[0];
@@ -1044,9 +1057,9 @@ void backward_deterministic(const SplatArrays& sp, const uint32_t* pair_vals, co
 }
 
 int project_one(const double* sliced16_dev, const DevCamera& cam, const double* sh48_dev, int sh_degree,
-                double opacity_logit, void* out_dev, int* survived_dev, cudaStream_t s) {
+                double opacity_logit, void* out_dev, int* survived_dev, cudaStream_t s, double* cache_dev) {
     k_project_one<<<1, 1, 0, s>>>(sliced16_dev, cam, sh48_dev, sh_degree, opacity_logit,
-                                  reinterpret_cast<HostSplat*>(out_dev), survived_dev);
+                                  reinterpret_cast<HostSplat*>(out_dev), survived_dev, cache_dev);
     return 0;
 }
 

@@ -1527,26 +1527,35 @@ int rgs_render_backward(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* ca
     });
 }
 
-int rgs_project_sliced(rgs_ctx* c, const double* sliced16, const rgs_camera* cam, const double* sh48, int sh_degree,
-                       double opacity_logit, rgs_splat* out, int* survived) {
+int rgs_project_sliced_cache(rgs_ctx* c, const double* sliced16, const rgs_camera* cam, const double* sh48,
+                             int sh_degree, double opacity_logit, rgs_splat* out, int* survived, double* cache) {
     if (!sliced16 || !cam || !sh48 || !out || !survived) return RGS_E_INVALID;
     return guarded(c, [&]() -> int {
         cudaStream_t s = c->stream;
         DevBuf buf;
-        buf.ensure(sizeof(double) * 64 + sizeof(rgs_splat) + 16, s);
+        buf.ensure(sizeof(double) * (64 + RGS_PROJECT_CACHE_DOUBLES) + sizeof(rgs_splat) + 16, s);
         double* d = buf.as<double>();
-        rgs_splat* o = reinterpret_cast<rgs_splat*>(d + 64);
+        double* dc = d + 64;
+        rgs_splat* o = reinterpret_cast<rgs_splat*>(dc + RGS_PROJECT_CACHE_DOUBLES);
         int* surv = reinterpret_cast<int*>(o + 1);
         CK(cudaMemcpyAsync(d, sliced16, sizeof(double) * 16, cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(d + 16, sh48, sizeof(double) * 48, cudaMemcpyHostToDevice, s));
-        rgs_launch::project_one(d, make_dev_camera(cam), d + 16, sh_degree, opacity_logit, o, surv, s);
+        rgs_launch::project_one(d, make_dev_camera(cam), d + 16, sh_degree, opacity_logit, o, surv, s,
+                                cache ? dc : nullptr);
         c->launches += 1;
         CK(cudaMemcpyAsync(out, o, sizeof(rgs_splat), cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(survived, surv, sizeof(int), cudaMemcpyDeviceToHost, s));
+        if (cache)
+            CK(cudaMemcpyAsync(cache, dc, sizeof(double) * RGS_PROJECT_CACHE_DOUBLES, cudaMemcpyDeviceToHost, s));
         buf.release(s);
         CK(cudaStreamSynchronize(s));
         return RGS_OK;
     });
+}
+
+int rgs_project_sliced(rgs_ctx* c, const double* sliced16, const rgs_camera* cam, const double* sh48, int sh_degree,
+                       double opacity_logit, rgs_splat* out, int* survived) {
+    return rgs_project_sliced_cache(c, sliced16, cam, sh48, sh_degree, opacity_logit, out, survived, nullptr);
 }
 
 }  // extern "C"

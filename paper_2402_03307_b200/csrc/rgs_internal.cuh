@@ -214,7 +214,7 @@ void backward_deterministic(const SplatArrays& sp, const uint32_t* pair_vals, co
                             const float* dL_dimage, const uint32_t* sorted_ids, const int* n_valid_dev, int n,
                             uint32_t* rank, double* tile_grads, double* screen_grads, cudaStream_t s);
 int project_one(const double* sliced16_dev, const DevCamera& cam, const double* sh48_dev, int sh_degree,
-                double opacity_logit, void* out_dev, int* survived_dev, cudaStream_t s);
+                double opacity_logit, void* out_dev, int* survived_dev, cudaStream_t s, double* cache_dev = nullptr);
 // screen_grads_fixed (NULL: FP64 atomics into screen_grads): RGS_FLAG_REPRODUCIBLE's fixed-point
 // counters (18 u64 per splat, fixed_add), turned into screen_grads by fixed_to_double.
 void backward_fp32(const SplatArrays& sp, const uint32_t* pair_vals, const uint2* ranges,

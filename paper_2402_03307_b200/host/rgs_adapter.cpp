@@ -3,13 +3,14 @@
 // A maintainer of /root/reference/proj compiles this file INSTEAD OF src/rasterizer.cpp
 // and links librgs_cuda.so: every declaration of include/rgs/rasterizer.hpp keeps its
 // signature, argument meaning and exceptions:
-//   project            rasterizer.hpp:52-54   -> rgs_project_sliced (device, FP64)
+//   project            rasterizer.hpp:52-54   -> rgs_project_sliced_cache (device, FP64)
 //   render_forward     rasterizer.hpp:82-83   -> rgs_render_forward + rgs_records_export
 //   rasterize_forward  rasterizer.hpp:87-89   -> rgs_rasterize_forward
 //   render_backward    rasterizer.hpp:93-95   -> rgs_render_backward
 //   render_flow        rasterizer.hpp:99      -> rgs_render_flow
-// Behaviour differences: `threads` is ignored; ProjectCache / RenderRecords::caches are
-// not filled (the device backward recomputes what it needs); rotor errors always throw.
+// Behaviour differences: `threads` is ignored; project() fills ProjectCache (computed on the
+// device) but RenderRecords::caches are not filled (the device backward recomputes what it
+// needs); rotor errors always throw.
 // Device-side caching: the device copy of a store is kept and reused while
 // the store's contents (a 64-bit hash of every parameter array), size and SH degree are
 // unchanged, and the device records of the last render_forward stay alive so that the
@@ -231,7 +232,7 @@ void export_records(const RecordsHandle& h, RenderRecords* rec, const Vec3& back
 }  // namespace
 
 std::optional<Splat2D> project(const SlicedGaussian3D& s, const Camera& cam, const ShCoeffs& sh, int sh_degree,
-                               Scalar opacity_logit, ProjectCache* /*cache: not filled, see header comment*/) {
+                               Scalar opacity_logit, ProjectCache* cache) {
     double sliced[16];
     for (int a = 0; a < 3; ++a) sliced[a] = s.mean[a];
     for (int i = 0; i < 3; ++i)
@@ -244,8 +245,28 @@ std::optional<Splat2D> project(const SlicedGaussian3D& s, const Camera& cam, con
     const rgs_camera c = to_c(cam);
     rgs_splat out;
     int survived = 0;
-    check(rgs_project_sliced(context(), sliced, &c, sh48, sh_degree, opacity_logit, &out, &survived));
+    double pc[RGS_PROJECT_CACHE_DOUBLES];
+    check(rgs_project_sliced_cache(context(), sliced, &c, sh48, sh_degree, opacity_logit, &out, &survived,
+                                   cache ? pc : nullptr));
     if (!survived) return std::nullopt;
+    if (cache) {  // rasterizer.cpp:261-275
+        cache->cov3 = s.cov;
+        cache->mean3 = s.mean;
+        cache->speed = s.speed;
+        cache->decay = s.decay;
+        cache->p_cam = Vec3(pc[0], pc[1], pc[2]);
+        for (int r = 0; r < 2; ++r)
+            for (int k = 0; k < 3; ++k) cache->T(r, k) = pc[3 + 3 * r + k];
+        for (int r = 0; r < 2; ++r)
+            for (int k = 0; k < 2; ++k) cache->cov2(r, k) = pc[9 + 2 * r + k];
+        cache->dir = Vec3(pc[13], pc[14], pc[15]);
+        cache->view_dist = pc[16];
+        for (int k = 0; k < 16; ++k) cache->basis[k] = pc[17 + k];
+        for (int k = 0; k < 16; ++k)
+            for (int j = 0; j < 3; ++j) cache->basis_grad(k, j) = pc[33 + 3 * k + j];
+        for (int ch = 0; ch < 3; ++ch) cache->clamped[ch] = pc[81 + ch] != 0.0;
+        cache->opacity = pc[84];
+    }
     return from_c(out);
 }
 

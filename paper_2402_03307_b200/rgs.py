@@ -163,7 +163,7 @@ EXPORTS = [
     "rgs_rasterize_forward", "rgs_render_flow", "rgs_records_destroy", "rgs_records_info_get",
     "rgs_records_export", "rgs_render_backward", "rgs_camera_validate", "rgs_profile_num_stages",
     "rgs_profile_stage_name", "rgs_ctx_set_profiling", "rgs_ctx_profile_reset", "rgs_ctx_profile_read",
-    "rgs_measure_fp32_tflops", "rgs_project_sliced", "rgs_scene_create_ex", "rgs_scene_params_f64",
+    "rgs_measure_fp32_tflops", "rgs_project_sliced", "rgs_project_sliced_cache", "rgs_scene_create_ex", "rgs_scene_params_f64",
     # training side (train.py)
     "rgs_image_loss", "rgs_optimizer_create", "rgs_optimizer_destroy", "rgs_adam_step", "rgs_optimizer_status",
     "rgs_optimizer_status_async", "rgs_optimizer_download", "rgs_optimizer_upload", "rgs_optimizer_reset_stats", "rgs_reset_opacity",
@@ -235,6 +235,7 @@ def load_library(path: str = LIB_PATH):
         "rgs_nccl_comm_destroy": (None, [p]),
         "rgs_allreduce_grads": (i, [p, p, p, ctypes.c_size_t, p, ctypes.c_size_t, p, i]),
         "rgs_project_sliced": (i, [p, p, p, p, i, d, p, p]),
+        "rgs_project_sliced_cache": (i, [p, p, p, p, i, d, p, p, p]),
         "rgs_image_loss": (i, [p, p, p, i, i, d, d, d, ctypes.c_uint, p, p]),
         "rgs_image_loss_ex": (i, [p, p, p, p, i, i, d, d, d, ctypes.c_uint, p, p]),
         "rgs_optimizer_create": (i, [p, p, p]),
@@ -844,6 +845,30 @@ def render_forward(store: GaussianStore, cam: Camera, opts: RenderOptions = Rend
     rec = RenderRecords(ctx, h, cam, opts.background, opts.retain_records)
     rec._scene = scene  # keep alive (backward re-reads the parameters)
     return RenderOutput(img, rec)
+
+
+PROJECT_CACHE_DOUBLES = 85  # RGS_PROJECT_CACHE_DOUBLES (include/rgs_cuda.h)
+
+
+def project(sliced16, cam: Camera, sh48, sh_degree: int, opacity_logit: float, ctx: Optional[Context] = None,
+            want_cache: bool = False):
+    """project() of one already-sliced Gaussian (rasterizer.hpp:52-54): sliced16 = mean[3],
+    cov[9] row-major, decay, speed[3]; sh48 channel-major.  Returns the SPLAT_DTYPE record (None
+    when culled) and, with want_cache, ProjectCache's fields as rgs_project_sliced_cache's flat
+    layout (p_cam, T, cov2, dir, view_dist, basis, basis_grad, clamped, opacity)."""
+    ctx = ctx or default_context()
+    sl = np.ascontiguousarray(sliced16, dtype=np.float64)
+    sh = np.ascontiguousarray(sh48, dtype=np.float64)
+    out = np.zeros(1, dtype=SPLAT_DTYPE)
+    cache = np.zeros(PROJECT_CACHE_DOUBLES, dtype=np.float64) if want_cache else None
+    surv = ctypes.c_int(0)
+    c = cam.to_c()
+    ctx.check(ctx.L.rgs_project_sliced_cache(ctx.h, _vp(sl.ctypes.data), ctypes.byref(c), _vp(sh.ctypes.data),
+                                             int(sh_degree), float(opacity_logit), _vp(out.ctypes.data),
+                                             ctypes.byref(surv), _vp(cache.ctypes.data) if want_cache else None))
+    if not surv.value:
+        return (None, None) if want_cache else None
+    return (out[0], cache) if want_cache else out[0]
 
 
 def rasterize_forward(splats: np.ndarray, cam: Camera, background=(0.0, 0.0, 0.0), threads: int = 1,
