@@ -981,7 +981,8 @@ def run_ours(args, rank, local_rank, world):
                "rep_ms": [1e3 * x for x in rep_s], "statistic": "median of the per-sweep times",
                "best_sweep_value": N_TIMES * world / min(rep_s),
                "note": "rgs_render_views_host: pinned host scene -> HBM, 300 renders, 300 images -> pinned host; "
-                       "bound by the D2H of 4.9 GB of float32 images per sweep"}
+                       "the D2H of 4.9 GB of float32 images per sweep overlaps the renders (copy-only "
+                       "4.9 GB / pcie_d2h_gbs_measured; on links below ~45 GB/s it bounds the sweep)"}
 
     # ---- CPU baseline (rank 0, N=1 only, bounded sample)
     cpu = None

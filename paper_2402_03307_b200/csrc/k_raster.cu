@@ -492,6 +492,7 @@ __global__ void __launch_bounds__(kX2Threads, NB) k_blend_fp32_x2(SplatArrays sp
                 w_k[warp][q] = (uint8_t)lane;
             }
             __syncwarp();
+            unsigned bmask = 0;  // COUNT only: the window entries this lane blended
             if (!gone) {
                 const uint32_t first = (uint32_t)__cvta_generic_to_shared(w_list[warp]);
                 const uint32_t end = first + (uint32_t)__popc(m) * (uint32_t)sizeof(StagedSplat);
@@ -541,7 +542,10 @@ __global__ void __launch_bounds__(kX2Threads, NB) k_blend_fp32_x2(SplatArrays sp
                     errT3 = make_float2(ok0 ? eT3.x : errT3.x, ok1 ? eT3.y : errT3.y);
                     last0 = ok0 ? e : last0;
                     last1 = ok1 ? e : last1;
-                    if (COUNT) n_blend += (ok0 ? 1u : 0u) + (ok1 ? 1u : 0u);
+                    if (COUNT) {
+                        n_blend += (ok0 ? 1u : 0u) + (ok1 ? 1u : 0u);
+                        if (ok0 | ok1) bmask |= 1u << (int)((e - first) / sizeof(StagedSplat));
+                    }
                     if ((act0 & !ok0) | (act1 & !ok1)) {
                         // rare: certainly stop (rasterizer.cpp:111, the splat is not blended), or
                         // a decision inside its error bound -> the pixel goes to the FP64 fix-up
@@ -583,7 +587,14 @@ __global__ void __launch_bounds__(kX2Threads, NB) k_blend_fp32_x2(SplatArrays sp
                 if (last1) contrib1 = (int)(start - rg.x) + c + w_k[warp][(last1 - first) / sizeof(StagedSplat)] + 1;
             }
             __syncwarp();  // the list is rewritten by the next window
-            if (COUNT && lane == 0 && __popc(m)) atomicAdd(counters + 7, (unsigned long long)__popc(m));
+            if (COUNT) {
+                // warp visits of the window and those where some lane blended
+                const unsigned anyb = __reduce_or_sync(kFull, bmask);
+                if (lane == 0 && __popc(m)) {
+                    atomicAdd(counters + 7, (unsigned long long)__popc(m));
+                    atomicAdd(counters + 8, (unsigned long long)__popc(anyb));
+                }
+            }
             if (__all_sync(kFull, gone)) {
                 warp_done = true;
                 break;
