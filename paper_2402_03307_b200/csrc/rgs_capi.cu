@@ -1193,9 +1193,9 @@ int render_batch(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* cams, int
     for (int k = 0; k < rgs_ctx::kSlots; ++k) CK(cudaStreamWaitEvent(c->slot_stream[k], c->join_ev, 0));
     // Profiling mode serialises the views (one slot) so per-stage event times are the
     // kernels' own durations rather than shares of concurrently running views.
-    // Views in flight: 8 for frames up to ~2 MP (1352x1014: 3 -> 8 slots measured +4.5%), 1 for
-    // larger ones (below).  One view in flight (or the profiling mode) -> K5 takes the tiles
-    // longest list first, as a single view does.
+    // Views in flight: 8 for frames up to ~2 MP (1352x1014: 3 -> 8 slots measured +4.5%), 3 for
+    // larger ones (below).  One view in flight (the profiling mode, or RGS_SLOTS=1) -> K5 takes the
+    // tiles longest list first, as a single view does.
     const size_t npix = (size_t)cams[0].width * cams[0].height;
     // RGS_SLOTS (A/B runs; up to kSlots): views in flight.  At 8, 10 or 12 the C2 sweep runs at the
     // same rate (2650 FPS), at 6 0.3 % slower (with a less shared -- faster -- live K5 launch)
@@ -1209,10 +1209,9 @@ int render_batch(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* cams, int
         const int k = e ? std::atoi(e) : 0;
         return (k >= 1 && k <= rgs_ctx::kSlots) ? k : 0;
     }();
-    // Frames above ~2.2 MP run one view at a time: 3840x2160 (C4) 383 FPS at 1 view in flight
-    // against 349 / 342 / 336 / 333 at 2 / 3 / 4 / 6 (the views' pair lists and records compete
-    // for L2); up to ~2.2 MP the views overlap (C2: 8 in flight).
-    const int big_slots = env_big ? env_big : 1;
+    // Frames above ~2.2 MP: 3 views in flight (3840x2160, 2M Gaussians, orbit cameras: 407 FPS
+    // at 3, 403 at 8, 390 at 1 -- tools/probe_slots.py); up to ~2.2 MP 8 (C2).
+    const int big_slots = env_big ? env_big : 3;
     const int slots = c->timing == 1 ? 1 : (npix <= (size_t)2200000 ? (env_slots ? env_slots : 8) : big_slots);
     for (int v = 0; v < n_views; ++v) {
         const int k = v % slots;
@@ -1238,8 +1237,19 @@ int render_batch(rgs_ctx* c, const rgs_scene* scene, const rgs_camera* cams, int
     }
     for (int v = 0; v < n_views; ++v) {
         if (!c->view_stats[v].overflow) continue;
+        // every slot learns the larger capacity (it grows its pair buffers on its next view): a
+        // slot that kept the capacity of an earlier, smaller workload would overflow -- and be
+        // re-rendered serially here -- on every later batch (C4 after C2 in one context: 342
+        // FPS at 3 views in flight before this, the overflowing views rendered twice)
+        const long long need = (long long)c->view_stats[v].n_pairs * 5 / 4 + 1024;
+        for (int k = 0; k < rgs_ctx::kSlots; ++k) {
+            Frame& fk = c->slot_frame[k];
+            if (fk.pair_cap <= 0 || fk.pair_cap >= need) continue;
+            fk.pair_cap = need;
+            fk.ensure_pairs(need, true, c->slot_stream[k]);  // grown now, not inside the next batch
+        }
         Frame& f = c->slot_frame[0];
-        f.pair_cap = std::max<long long>(f.pair_cap, (long long)c->view_stats[v].n_pairs * 5 / 4 + 1024);
+        f.pair_cap = std::max<long long>(f.pair_cap, need);
         const int rc = run_forward(c, f, c->stream, kFromScene, scene, nullptr, 0, true, &cams[v], bg,
                                    flags & ~RGS_FLAG_HOST_BUFFERS, image_for(user, v, c->stream), false, true,
                                    nullptr, cache, true);
